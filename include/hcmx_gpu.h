@@ -1,0 +1,212 @@
+/*
+ * hcmx_gpu.h -- C-ABI of the B200 (sm_100a) implementation of the hcmx hot path:
+ * the adaptive-precision codec (AFL/AFLP/BFL/DFL), APLR per-column lowrank
+ * compression and the compressed H-matrix-vector product.
+ *
+ * Every entry point replaces a function of the reference C++ API in
+ * /root/reference/proj/include/hcmx (cited per function).  The reference has no
+ * FFI; the binding a maintainer adds is shown in INTEGRATION.md (a C++ shim
+ * keeping the hcmx::codec / hcmx::matvec names, and a ctypes stub).
+ *
+ * Conventions
+ *   - plain pointers and sizes, no C++ or torch types; "d_" = device pointer,
+ *     "h_" = host pointer.  Streams are cudaStream_t passed as void*.
+ *   - every function returns HCMX_OK (0) or an error status; the reference's
+ *     exceptions map to statuses: std::invalid_argument -> HCMX_INVALID_ARGUMENT,
+ *     hcmx::corrupt_buffer_error (common.hpp:17-19) -> HCMX_CORRUPT_BUFFER.
+ *     hcmx_gpu_last_error() returns the message of the last failure on the
+ *     calling thread.
+ *   - there is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point returns HCMX_CUDA_ERROR.
+ */
+#ifndef HCMX_GPU_H
+#define HCMX_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum hcmx_status {
+    HCMX_OK = 0,
+    HCMX_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    HCMX_CORRUPT_BUFFER = 2,   /* hcmx::corrupt_buffer_error */
+    HCMX_CUDA_ERROR = 3,
+    HCMX_NCCL_ERROR = 4,
+    HCMX_OUT_OF_MEMORY = 5
+};
+
+/* codec::Scheme (codec.hpp:22) */
+enum hcmx_scheme { HCMX_AFL = 0, HCMX_AFLP = 1, HCMX_BFL = 2, HCMX_DFL = 3 };
+
+/* codec::FormatDescriptor (codec.hpp:35-56), 16 bytes */
+typedef struct hcmx_descriptor {
+    uint8_t scheme;
+    uint8_t exp_bits;
+    uint8_t mant_bits;
+    uint8_t bit_width; /* cached FormatDescriptor::bit_width() */
+    uint32_t reserved;
+    double scale;
+} hcmx_descriptor;
+
+/* codec::BlockStats (codec.hpp:68-72) + a non-finite flag, 24 bytes */
+typedef struct hcmx_stats {
+    double min_mag;
+    double max_mag;
+    uint32_t all_zero;
+    uint32_t non_finite; /* compress rejects these (codec.cpp:119-120) */
+} hcmx_stats;
+
+/* ---------------------------------------------------------------- setup -- */
+int hcmx_gpu_init(int device);
+const char* hcmx_gpu_last_error(void);
+int hcmx_gpu_version(void);
+
+/* ----------------------------------------- scalar layout rules (host) ---- */
+/* codec.cpp:62-67 */
+int hcmx_gpu_mantissa_bits_for(double eps, uint8_t* out);
+/* codec.cpp:69-79 */
+int hcmx_gpu_exponent_bits_for(const hcmx_stats* stats, uint8_t* out);
+/* codec.cpp:81-84: make_descriptor(scheme, eps, stats) */
+int hcmx_gpu_make_descriptor(int scheme, double eps, const hcmx_stats* stats, hcmx_descriptor* out);
+/* codec.cpp:86-101: make_descriptor(scheme, eps, scale, exp_bits) */
+int hcmx_gpu_make_descriptor_pinned(int scheme, double eps, double scale, uint8_t exp_bits,
+                                    hcmx_descriptor* out);
+/* codec.hpp:51-55 */
+unsigned hcmx_gpu_bit_width(const hcmx_descriptor* d);
+/* codec.cpp:179-181 (20-byte header + packed payload) */
+uint64_t hcmx_gpu_compressed_size(uint64_t count, const hcmx_descriptor* d);
+/* payload bytes only: ceil(count * bit_width / 8) */
+uint64_t hcmx_gpu_payload_bytes(uint64_t count, const hcmx_descriptor* d);
+
+/* ------------------------------------------- batched device codec -------- */
+/* A batch is nbuf independent buffers; buffer b holds h_count[b] FP64 values
+ * at d_values + d_voff[b] (element offsets) and its packed payload at
+ * d_payload + d_poff[b] (byte offsets, 16-byte aligned; each slot must hold
+ * round_up(payload_bytes, 16) bytes).  Packed payloads are byte-for-byte the
+ * reference's CompressedBuffer::payload.  h_count is a HOST array: the library
+ * splits big buffers into warp jobs of <= 16384 values on the host. */
+
+/* codec.cpp:44-60 analyze, one hcmx_stats per buffer (warp-shuffle min/max) */
+int hcmx_gpu_codec_analyze(const double* d_values, const uint64_t* d_voff, const uint64_t* h_count,
+                           uint64_t nbuf, hcmx_stats* d_stats, void* stream);
+
+/* codec.cpp:103-140 compress_block for every buffer with caller-pinned layouts */
+int hcmx_gpu_codec_pack(const double* d_values, const uint64_t* d_voff, const uint64_t* h_count,
+                        const hcmx_descriptor* d_desc, const uint64_t* d_poff, uint64_t nbuf,
+                        uint8_t* d_payload, void* stream);
+
+/* codec.cpp:146-171 decompress_into for every buffer */
+int hcmx_gpu_codec_unpack(const uint8_t* d_payload, const uint64_t* d_poff, const uint64_t* h_count,
+                          const hcmx_descriptor* d_desc, const uint64_t* d_voff, uint64_t nbuf,
+                          double* d_out, void* stream);
+
+/* codec.cpp:142-144 compress for every buffer: analyze on the device, layout
+ * selection on the host with the reference's exact scalar rules (glibc log2),
+ * payload offsets (16-byte aligned) and packing on the device.  Outputs h_desc[nbuf], h_poff[nbuf] and *h_total
+ * (arena bytes used); fails with HCMX_INVALID_ARGUMENT on non-finite input or
+ * eps outside (0,1), and if the arena capacity is too small. */
+int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff,
+                            const uint64_t* h_count, uint64_t nbuf, double eps, int scheme,
+                            uint8_t* d_payload, uint64_t payload_capacity, hcmx_descriptor* h_desc,
+                            uint64_t* h_poff, uint64_t* h_total, void* stream);
+
+/* Single-buffer, HOST-pointer forms of codec::compress / decompress_into
+ * (codec.cpp:142-171): the reference-facing call.  Copies in, runs the device
+ * kernels, copies out. */
+int hcmx_gpu_compress(const double* h_values, uint64_t count, double eps, int scheme,
+                      hcmx_descriptor* desc, uint8_t* h_payload, uint64_t capacity,
+                      uint64_t* payload_len);
+int hcmx_gpu_compress_block(const double* h_values, uint64_t count, const hcmx_descriptor* desc,
+                            uint8_t* h_payload, uint64_t capacity, uint64_t* payload_len);
+int hcmx_gpu_decompress_into(const hcmx_descriptor* desc, uint64_t count, const uint8_t* h_payload,
+                             uint64_t payload_len, double* h_out);
+
+/* codec.cpp:187-225 wire format [u8 scheme][u8 e][u8 m][u8 0][f64 scale][u64 count][payload] */
+uint64_t hcmx_gpu_serialize(const hcmx_descriptor* desc, uint64_t count, const uint8_t* payload,
+                            uint64_t payload_len, uint8_t* out);
+int hcmx_gpu_deserialize(const uint8_t* data, uint64_t size, uint64_t* offset,
+                         hcmx_descriptor* desc, uint64_t* count, uint64_t* payload_at,
+                         uint64_t* payload_len);
+
+/* ------------------------------------------------------------- APLR ------ */
+/* mixedprec.cpp:155-187 aplr_compress for a batch of lowrank leaves from given
+ * factors: leaf j has W (rows_j x k_j) and X (cols_j x k_j) column-major at
+ * d_W + h_woff[j], d_X + h_xoff[j] and sigma at h_sigma + h_soff[j].  Column i of
+ * W becomes buffer h_boff[j] + i, column i of X buffer h_boff[j] + k_j + i.
+ * e is analysed over the whole factor, per column eps_i = min(0.5, eps sigma_0 /
+ * sigma_i) and scale = column min |v|.  Outputs descriptors / 16-byte-aligned
+ * payload offsets for all buffers. */
+int hcmx_gpu_aplr_compress(uint64_t nleaves, const uint64_t* h_rows, const uint64_t* h_cols,
+                           const uint64_t* h_k, const double* d_W, const uint64_t* h_woff,
+                           const double* d_X, const uint64_t* h_xoff, const double* h_sigma,
+                           const uint64_t* h_soff, const uint64_t* h_boff, double eps, int scheme,
+                           uint8_t* d_payload, uint64_t payload_capacity, hcmx_descriptor* h_desc,
+                           uint64_t* h_poff, uint64_t* h_total, void* stream);
+
+/* ------------------------------------------------------- H-matrix -------- */
+/* Flattened H-matrix (hmatrix.hpp:51-78): leaves in for_each_leaf preorder
+ * (clustering.cpp:159-166, children row-major 2i+j), internal index space.
+ *   kind 0 CodecDense  (hmatrix.hpp:42-44): buffer buf0, column-major scan
+ *   kind 1 APLRLowrank (mixedprec.hpp:68-82): buffers buf0..buf0+k-1 = W columns,
+ *          buf0+k..buf0+2k-1 = X columns, sigma[sig0 .. sig0+k)
+ * Buffers: descriptor, value count, payload at blob[poff .. poff+plen). */
+typedef struct hcmx_hmat_desc {
+    uint64_t n_rows, n_cols, nleaves, nbuffers, nsigma, blob_bytes;
+    const int64_t *row0, *row1, *col0, *col1, *kind, *rank, *buf0, *sig0; /* [nleaves] */
+    const double* sigma;                                                  /* [nsigma] */
+    const hcmx_descriptor* desc;                                          /* [nbuffers] */
+    const int64_t *count, *poff, *plen;                                   /* [nbuffers] */
+    const uint8_t* blob; /* host pointer, or device pointer if blob_on_device */
+    int blob_on_device;
+    /* block-row partition (multi-GPU): only leaves with row0 in [row_begin,row_end)
+     * are loaded; matvec then writes y[row_begin,row_end) only. 0,0 = all rows */
+    uint64_t row_begin, row_end;
+} hcmx_hmat_desc;
+
+typedef struct hcmx_hmat hcmx_hmat; /* opaque, device resident */
+
+/* MemoryReport (hmatrix.hpp:96-113) + device arena accounting */
+typedef struct hcmx_memory_report {
+    uint64_t dense_raw, dense_compressed, lowrank_raw, lowrank_compressed, overhead;
+    uint64_t uncompressed_equivalent;
+    uint64_t device_arena_bytes;   /* packed streams resident in HBM */
+    uint64_t device_table_bytes;   /* stage / item / column tables */
+    uint64_t algorithmic_bytes;    /* bytes one matvec must move */
+    uint64_t dense_leaves, lowrank_leaves, stages_a, stages_b;
+} hcmx_memory_report;
+
+int hcmx_gpu_hmat_create(const hcmx_hmat_desc* desc, hcmx_hmat** out);
+int hcmx_gpu_hmat_destroy(hcmx_hmat* h);
+int hcmx_gpu_hmat_memory(const hcmx_hmat* h, hcmx_memory_report* out);
+
+/* hmatrix.hpp:126-128 matvec: y := alpha * M * x + beta * y (beta == 0 overwrites
+ * y; alpha == 0 gives beta * y without touching M).  transpose != 0 is not
+ * supported yet (HCMX_INVALID_ARGUMENT).  Host-pointer form: copies x in and y
+ * out (the reference-facing call). */
+int hcmx_gpu_hmat_matvec(hcmx_hmat* h, double alpha, const double* h_x, double beta, double* h_y,
+                         int transpose);
+/* device-pointer form on a stream; d_x has n_cols entries, d_y n_rows entries
+ * (for a partitioned handle only d_y[row_begin,row_end) is written) */
+int hcmx_gpu_hmat_matvec_device(hcmx_hmat* h, double alpha, const double* d_x, double beta,
+                                double* d_y, void* stream);
+
+/* rebuild buffer b's verbatim payload from the device arena (layout check) */
+int hcmx_gpu_hmat_export_buffer(const hcmx_hmat* h, uint64_t b, uint8_t* h_payload,
+                                uint64_t capacity, uint64_t* len);
+
+/* launch counting for the bench: kernels launched by the last matvec */
+int hcmx_gpu_hmat_last_launches(const hcmx_hmat* h);
+
+/* per-kernel device timing of the hot kernels (CUDA events on the launch
+ * stream) accumulated over matvec_device calls since the last reset */
+int hcmx_gpu_hmat_timing(hcmx_hmat* h, int enable, double* ms_phase_a, double* ms_phase_b,
+                         uint64_t* calls);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HCMX_GPU_H */

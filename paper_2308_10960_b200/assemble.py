@@ -1,0 +1,148 @@
+"""FP64 assembly of an H-matrix for the synthetic problems (host-driven setup,
+runs once before the hot path; torch on the GPU when present).
+
+Dense (inadmissible) leaves are evaluated entry by entry.  Admissible leaves
+get W, sigma, X with A ~= W diag(sigma) X^T, W and X orthonormal, truncated by
+the reference's rank rule sigma_k > eps * sigma_0 (lowrank.cpp:14-21) -- the
+shape svd_factors produces (lowrank.cpp:76-93).  Blocks up to 256 columns use
+a full SVD; larger blocks a randomized range finder with one power iteration,
+whose sketch is grown until the captured spectrum reaches 1e-3 * eps * sigma_0,
+so the truncation sees the same leading singular values a full SVD would.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .problems import PointKernel
+from .tree import BlockLeaves
+
+EXACT_SVD_MAX = 256
+
+
+@dataclass
+class Assembled:
+    n: int
+    leaves: BlockLeaves
+    kind: np.ndarray          # 0 dense, 1 lowrank
+    rank: np.ndarray          # lowrank rank (0 for dense)
+    dense: torch.Tensor       # FP64, dense leaves column-major, leaf order
+    dense_off: np.ndarray     # per leaf (dense) value offset, -1 otherwise
+    W: torch.Tensor           # FP64, per lowrank leaf rows*k column-major
+    X: torch.Tensor
+    w_off: np.ndarray         # per leaf offsets into W / X, -1 for dense
+    x_off: np.ndarray
+    sigma: np.ndarray         # concatenated singular values
+    sig_off: np.ndarray
+
+
+def rank_from_singular_values(s: torch.Tensor, eps: float) -> torch.Tensor:
+    """lowrank.cpp:14-21, batched: number of leading sigma_k > eps * sigma_0"""
+    s0 = s[..., :1]
+    keep = (s > eps * s0) & (s0 > 0)
+    return keep.cumprod(dim=-1).sum(dim=-1)
+
+
+def _svd_batch(A: torch.Tensor, eps: float):
+    B, m, n = A.shape
+    if min(m, n) <= EXACT_SVD_MAX:
+        U, S, Vh = torch.linalg.svd(A, full_matrices=False)
+        return U, S, Vh
+    g = torch.Generator(device=A.device)
+    g.manual_seed(1234 + m)
+    p = min(min(m, n), 64)
+    while True:
+        omega = torch.randn(B, n, p, dtype=A.dtype, device=A.device, generator=g)
+        Q, _ = torch.linalg.qr(A @ omega)
+        Q, _ = torch.linalg.qr(A.transpose(1, 2) @ Q)
+        Q, _ = torch.linalg.qr(A @ Q)
+        Bm = Q.transpose(1, 2) @ A
+        Ub, S, Vh = torch.linalg.svd(Bm, full_matrices=False)
+        if p >= min(m, n) or bool((S[:, -1] <= 1e-3 * eps * S[:, 0]).all()):
+            return Q @ Ub, S, Vh
+        p = min(min(m, n), 2 * p)
+
+
+def assemble(points_internal: np.ndarray, leaves: BlockLeaves, kernel: PointKernel, eps: float,
+             device: str | None = None, batch_bytes: int = 1 << 30) -> Assembled:
+    dev = torch.device(device or ("cuda" if torch.cuda.is_available() else "cpu"))
+    P = torch.as_tensor(np.ascontiguousarray(points_internal, dtype=np.float64), device=dev)
+    L = len(leaves)
+    kind = np.where(leaves.admissible, 1, 0).astype(np.int64)
+    rows = (leaves.row1 - leaves.row0).astype(np.int64)
+    cols = (leaves.col1 - leaves.col0).astype(np.int64)
+    rank = np.zeros(L, np.int64)
+
+    # ---- dense leaves (column-major, leaf order)
+    dense_off = np.full(L, -1, np.int64)
+    didx = np.nonzero(kind == 0)[0]
+    sizes = rows[didx] * cols[didx]
+    dense_off[didx] = np.concatenate([[0], np.cumsum(sizes)[:-1]]) if didx.size else []
+    dense = torch.empty(int(sizes.sum()), dtype=torch.float64, device=dev)
+    _fill_blocks(P, leaves, didx, kernel, dense, dense_off, batch_bytes)
+
+    # ---- lowrank leaves: SVD per shape group, then laid out in leaf order
+    lidx = np.nonzero(kind == 1)[0]
+    Wp, Xp, Sp = {}, {}, {}
+    shapes = {}
+    for l in lidx:
+        shapes.setdefault((int(rows[l]), int(cols[l])), []).append(int(l))
+    for (m, n), ids in shapes.items():
+        per = max(1, batch_bytes // (8 * m * n * 3))
+        for c0 in range(0, len(ids), per):
+            chunk = np.array(ids[c0: c0 + per])
+            A = _blocks(P, leaves, chunk, kernel)
+            U, S, Vh = _svd_batch(A, eps)
+            ks = rank_from_singular_values(S, eps).cpu().numpy()
+            for b, l in enumerate(chunk):
+                k = int(ks[b])
+                rank[l] = k
+                Wp[l] = U[b, :, :k].transpose(0, 1).contiguous().reshape(-1)  # column-major W
+                Xp[l] = Vh[b, :k, :].contiguous().reshape(-1)                 # column-major X
+                Sp[l] = S[b, :k].cpu().numpy()
+            del A, U, S, Vh
+    w_off = np.full(L, -1, np.int64)
+    x_off = np.full(L, -1, np.int64)
+    sig_off = np.full(L, -1, np.int64)
+    wl, xl, sl = [], [], []
+    wo = xo = so = 0
+    for l in lidx:
+        w_off[l], x_off[l], sig_off[l] = wo, xo, so
+        wl.append(Wp[l]); xl.append(Xp[l]); sl.append(Sp[l])
+        wo += Wp[l].numel(); xo += Xp[l].numel(); so += Sp[l].size
+    W = torch.cat(wl) if wl else torch.zeros(0, dtype=torch.float64, device=dev)
+    X = torch.cat(xl) if xl else torch.zeros(0, dtype=torch.float64, device=dev)
+    sigma = np.concatenate(sl) if sl else np.zeros(0)
+    return Assembled(points_internal.shape[0], leaves, kind, rank, dense, dense_off, W, X, w_off,
+                     x_off, sigma, sig_off)
+
+
+def _blocks(P, leaves, ids, kernel):
+    r0 = torch.as_tensor(leaves.row0[ids], device=P.device)
+    c0 = torch.as_tensor(leaves.col0[ids], device=P.device)
+    m = int(leaves.row1[ids[0]] - leaves.row0[ids[0]])
+    n = int(leaves.col1[ids[0]] - leaves.col0[ids[0]])
+    ri = r0[:, None] + torch.arange(m, device=P.device)[None, :]
+    ci = c0[:, None] + torch.arange(n, device=P.device)[None, :]
+    return kernel.block(P[ri], P[ci])
+
+
+def _fill_blocks(P, leaves, ids, kernel, out, off, batch_bytes):
+    if not len(ids):
+        return
+    rows = leaves.row1[ids] - leaves.row0[ids]
+    cols = leaves.col1[ids] - leaves.col0[ids]
+    groups = {}
+    for i, l in enumerate(ids):
+        groups.setdefault((int(rows[i]), int(cols[i])), []).append(int(l))
+    for (m, n), g in groups.items():
+        per = max(1, batch_bytes // (8 * m * n * 2))
+        for c0 in range(0, len(g), per):
+            chunk = np.array(g[c0: c0 + per])
+            A = _blocks(P, leaves, chunk, kernel)            # [B, m, n]
+            colmaj = A.transpose(1, 2).reshape(len(chunk), -1)  # column-major per leaf
+            o = torch.as_tensor(off[chunk], device=P.device)
+            idx = o[:, None] + torch.arange(m * n, device=P.device)[None, :]
+            out[idx.reshape(-1)] = colmaj.reshape(-1)

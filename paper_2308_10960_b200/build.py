@@ -1,0 +1,70 @@
+"""Build libhcmx_gpu.so in-tree (sm_100a only; cross-compiles without a GPU).
+
+    python -m paper_2308_10960_b200.build
+
+nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo for the kernels, g++
+-ffp-contract=off for the host scalar rules (the reference's Release flags keep
+separate FP multiply/add), linked with the static CUDA runtime.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "_build")
+LIB = os.path.join(HERE, "libhcmx_gpu.so")
+INC = os.path.join(ROOT, "include")
+
+NVCC = os.environ.get("NVCC", "nvcc")
+CXX = os.environ.get("CXX", "g++")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
+                  "-I" + INC, "-I" + CSRC]
+CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-I" + INC, "-I" + CSRC]
+
+CU = ["codec_kernels.cu", "hmat.cu"]
+CPP = ["codec_host.cpp"]
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        raise RuntimeError(f"build failed: {cmd[0]} {cmd[-1]}")
+    return r
+
+
+def _stale(src, obj, extra=()):
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    deps = [src, os.path.join(CSRC, "internal.h"), os.path.join(INC, "hcmx_gpu.h"), *extra]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    objs = []
+    for f in CU:
+        src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
+        if force or _stale(src, obj):
+            r = _run([NVCC, *NVFLAGS, "-Xptxas", "-v", "-c", src, "-o", obj])
+            if verbose:
+                sys.stderr.write(r.stderr)
+        objs.append(obj)
+    for f in CPP:
+        src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
+        if force or _stale(src, obj):
+            _run([CXX, *CXXFLAGS, "-c", src, "-o", obj])
+        objs.append(obj)
+    if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static", "-lpthread"])
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

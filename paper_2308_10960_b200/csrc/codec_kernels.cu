@@ -1,0 +1,636 @@
+// codec_kernels.cu -- sm_100a kernels of the adaptive-precision codec and the
+// batched / host-pointer codec entry points of the C-ABI.
+//
+//   k_analyze  : codec.cpp:44-60  analyze (per-buffer min/max of nonzero |v|)
+//   k_pack     : codec.cpp:103-140 compress_block + BitWriter (bitstream.hpp:19-59)
+//   k_unpack   : codec.cpp:146-171 decompress_into + BitReader (bitstream.hpp:63-97)
+//
+// Work unit: one warp per "job" = up to 512 groups of 32 consecutive values of
+// one buffer.  A group of 32 values at bit width w occupies exactly w 32-bit
+// words of the LSB-first stream, so groups are independent: no atomics between
+// warps when packing, and each group's words are written once, coalesced.
+//
+// Bit-exactness: the encoder computes |v| * (1/scale) + 1 as two correctly
+// rounded operations (__dmul_rn, __dadd_rn: the reference's Release build has no
+// FMA at codec.cpp:124), and 1/scale with IEEE division.  Decoding is
+// exact by construction ((1.mant * 2^off) - 1 is exact, one rounding in * scale).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+
+namespace hcmx_gpu {
+
+void check_cuda(int err, const char* what) {
+    if (err != cudaSuccess) {
+        cudaGetLastError();
+        throw cuda_error(std::string(what) + ": " + cudaGetErrorString(static_cast<cudaError_t>(err)));
+    }
+}
+
+void require_device() {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        throw cuda_error("no CUDA device: libhcmx_gpu has no CPU fallback");
+    }
+}
+
+void DevBuf::alloc(size_t n) {
+    release();
+    if (n == 0) return;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        p = nullptr;
+        throw oom_error("cudaMalloc failed (out of device memory)");
+    }
+    check_cuda(e, "cudaMalloc");
+    bytes = n;
+}
+
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+
+void h2d(void* dst, const void* src, size_t bytes, void* stream) {
+    if (!bytes) return;
+    check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream), "h2d");
+}
+void d2h(void* dst, const void* src, size_t bytes, void* stream) {
+    if (!bytes) return;
+    check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream), "d2h");
+}
+void stream_sync(void* stream) {
+    check_cuda(cudaStreamSynchronize((cudaStream_t)stream), "cudaStreamSynchronize");
+}
+
+namespace {
+
+constexpr unsigned kGroupsPerJob = 512;  // 16384 values per warp job
+constexpr int kWarpsPerBlock = 8;
+
+struct Job {
+    uint32_t buf;
+    uint32_t g0;
+    uint32_t ng;
+    uint32_t pad;
+};
+
+std::vector<Job> make_jobs(const uint64_t* count, uint64_t nbuf) {
+    std::vector<Job> jobs;
+    jobs.reserve(nbuf);
+    for (uint64_t b = 0; b < nbuf; ++b) {
+        const uint64_t groups = (count[b] + 31) / 32;
+        for (uint64_t g = 0; g < groups; g += kGroupsPerJob)
+            jobs.push_back({static_cast<uint32_t>(b), static_cast<uint32_t>(g),
+                            static_cast<uint32_t>(std::min<uint64_t>(kGroupsPerJob, groups - g)), 0});
+    }
+    return jobs;
+}
+
+__device__ __forceinline__ uint64_t dbits(double d) { return static_cast<uint64_t>(__double_as_longlong(d)); }
+__device__ __forceinline__ double bitsd(uint64_t u) { return __longlong_as_double(static_cast<long long>(u)); }
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// ------------------------------------------------------------ analyze ----
+__global__ void k_stats_init(hcmx_stats* st, uint64_t nbuf) {
+    for (uint64_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nbuf; b += gridDim.x * blockDim.x) {
+        reinterpret_cast<unsigned long long*>(&st[b].min_mag)[0] = 0x7FF0000000000000ull;  // +inf
+        reinterpret_cast<unsigned long long*>(&st[b].max_mag)[0] = 0ull;
+        st[b].all_zero = 1u;
+        st[b].non_finite = 0u;
+    }
+}
+
+// codec.cpp:44-60: min/max over nonzero |v|.  NaN counts as nonzero but never
+// wins std::min/std::max there; the same holds below (NaN compares false).
+__global__ void k_analyze(const double* __restrict__ values, const uint64_t* __restrict__ voff,
+                          const uint64_t* __restrict__ count, const Job* __restrict__ jobs,
+                          uint64_t njobs, hcmx_stats* st) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    for (uint64_t j = wid; j < njobs; j += nw) {
+        const Job jb = jobs[j];
+        const uint64_t n = count[jb.buf];
+        const uint64_t i0 = (uint64_t)jb.g0 * 32, i1 = umin64(n, (uint64_t)(jb.g0 + jb.ng) * 32);
+        const double* v = values + voff[jb.buf];
+        uint64_t mn = 0x7FF0000000000000ull, mx = 0;
+        unsigned nz = 0, nf = 0;
+        for (uint64_t i = i0 + lane; i < i1; i += 32) {
+            const double x = __ldcs(v + i);
+            const double a = fabs(x);
+            if (a != 0.0) nz = 1;
+            if (!isfinite(x)) nf = 1;
+            if (a != 0.0 && !isnan(a)) {
+                const uint64_t b = dbits(a);  // nonnegative doubles order like their bits
+                mn = b < mn ? b : mn;
+                mx = b > mx ? b : mx;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t omn = __shfl_xor_sync(0xffffffffu, mn, o);
+            const uint64_t omx = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = omn < mn ? omn : mn;
+            mx = omx > mx ? omx : mx;
+        }
+        nz = __any_sync(0xffffffffu, nz);
+        nf = __any_sync(0xffffffffu, nf);
+        if (lane == 0) {
+            hcmx_stats* s = st + jb.buf;
+            atomicMin(reinterpret_cast<unsigned long long*>(&s->min_mag), (unsigned long long)mn);
+            atomicMax(reinterpret_cast<unsigned long long*>(&s->max_mag), (unsigned long long)mx);
+            if (nz) atomicAnd(&s->all_zero, 0u);
+            if (nf) atomicOr(&s->non_finite, 1u);
+        }
+    }
+}
+
+__global__ void k_stats_final(hcmx_stats* st, uint64_t nbuf) {
+    for (uint64_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nbuf; b += gridDim.x * blockDim.x)
+        if (st[b].all_zero) {
+            st[b].min_mag = 0.0;
+            st[b].max_mag = 0.0;
+        }
+}
+
+// --------------------------------------------------------------- pack ----
+__device__ __forceinline__ uint64_t encode_value(double v, unsigned e, unsigned m, double inv_scale,
+                                                 uint64_t max_offset, uint64_t round_add,
+                                                 uint64_t mant_mask) {
+    const uint64_t sign = dbits(v) >> 63;
+    uint64_t field = sign << (e + m);
+    if (v != 0.0) {
+        const double vp = __dadd_rn(__dmul_rn(fabs(v), inv_scale), 1.0);  // >= 2, no FMA
+        const uint64_t u = dbits(vp) + round_add;
+        uint64_t offset = (u >> 52) - 1023;
+        uint64_t mant = (u >> (52 - m)) & mant_mask;
+        if (offset > max_offset || !isfinite(vp)) {
+            offset = max_offset;
+            mant = (1ull << m) - 1;
+        }
+        field |= (offset << m) | mant;
+    }
+    return field;
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_pack(const double* __restrict__ values, const uint64_t* __restrict__ voff,
+       const uint64_t* __restrict__ count, const hcmx_descriptor* __restrict__ desc,
+       const uint64_t* __restrict__ poff, const Job* __restrict__ jobs, uint64_t njobs,
+       uint8_t* __restrict__ payload, int* __restrict__ err) {
+    __shared__ uint32_t sw[kWarpsPerBlock][64];
+    const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint32_t* words = sw[wib];
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    for (uint64_t j = wid; j < njobs; j += nw) {
+        const Job jb = jobs[j];
+        const hcmx_descriptor d = desc[jb.buf];
+        const unsigned e = d.exp_bits, m = d.mant_bits, w = d.bit_width;
+        const double inv_scale = 1.0 / d.scale;  // IEEE division (codec.cpp:107)
+        const uint64_t max_offset = (1ull << e) - 1;
+        const uint64_t round_add = (m < 52) ? (1ull << (51 - m)) : 0;
+        const uint64_t mant_mask = (m == 52) ? ((1ull << 52) - 1) : ((1ull << m) - 1);
+        const uint64_t n = count[jb.buf];
+        const double* v = values + voff[jb.buf];
+        uint32_t* out = reinterpret_cast<uint32_t*>(payload + poff[jb.buf]);
+        const unsigned bit = lane * w, q = bit >> 5, sh = bit & 31;
+        for (uint32_t g = jb.g0; g < jb.g0 + jb.ng; ++g) {
+            const uint64_t idx = (uint64_t)g * 32 + lane;
+            words[lane] = 0;
+            words[lane + 32] = 0;
+            __syncwarp();
+            if (idx < n) {
+                const double x = __ldcs(v + idx);
+                if (!isfinite(x)) {
+                    *err = 1;
+                } else {
+                    const uint64_t f = encode_value(x, e, m, inv_scale, max_offset, round_add, mant_mask);
+                    const uint64_t lo = f << sh;
+                    if ((uint32_t)lo) atomicOr(&words[q], (uint32_t)lo);
+                    if (lo >> 32) atomicOr(&words[q + 1], (uint32_t)(lo >> 32));
+                    if (sh && (f >> (64 - sh))) atomicOr(&words[q + 2], (uint32_t)(f >> (64 - sh)));
+                }
+            }
+            __syncwarp();
+            const uint64_t nvalid = umin64(32, n - (uint64_t)g * 32);
+            const unsigned nwords = (unsigned)((nvalid * w + 31) / 32);
+            uint32_t* o = out + (uint64_t)g * w;
+            for (unsigned t = lane; t < nwords; t += 32) __stcs(o + t, words[t]);
+            __syncwarp();
+        }
+    }
+}
+
+// ------------------------------------------------------------- unpack ----
+__device__ __forceinline__ double decode_field(uint64_t field, unsigned e, unsigned m, double scale) {
+    const uint64_t exp_mask = (1ull << e) - 1;
+    const uint64_t mant_mask = (m == 52) ? ((1ull << 52) - 1) : ((1ull << m) - 1);
+    const uint64_t sign = (field >> (e + m)) & 1u;
+    const uint64_t offset = (field >> m) & exp_mask;
+    const uint64_t mant = field & mant_mask;
+    double v = 0.0;
+    if (offset != 0 || mant != 0) {
+        const uint64_t biased = umin64(offset + 1023, 2046);  // codec.cpp:165
+        v = __dmul_rn(bitsd((biased << 52) | (mant << (52 - m))) - 1.0, scale);
+    }
+    return sign ? -v : v;
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_unpack(const uint8_t* __restrict__ payload, const uint64_t* __restrict__ poff,
+         const uint64_t* __restrict__ count, const hcmx_descriptor* __restrict__ desc,
+         const uint64_t* __restrict__ voff, const Job* __restrict__ jobs, uint64_t njobs,
+         double* __restrict__ out) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    for (uint64_t j = wid; j < njobs; j += nw) {
+        const Job jb = jobs[j];
+        const hcmx_descriptor d = desc[jb.buf];
+        const unsigned e = d.exp_bits, m = d.mant_bits, w = d.bit_width;
+        const uint64_t n = count[jb.buf];
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(payload + poff[jb.buf]);
+        double* o = out + voff[jb.buf];
+        const unsigned bit = lane * w, q = bit >> 5, sh = bit & 31;
+        const uint64_t wmask = (w == 64) ? ~0ull : ((1ull << w) - 1);
+        for (uint32_t g = jb.g0; g < jb.g0 + jb.ng; ++g) {
+            const uint64_t idx = (uint64_t)g * 32 + lane;
+            if (idx < n) {
+                const uint32_t* gp = p + (uint64_t)g * w + q;
+                const uint32_t lo = __ldcs(gp);
+                const uint32_t hi = (sh + w > 32) ? __ldcs(gp + 1) : 0u;
+                uint64_t win = ((uint64_t)hi << 32 | lo) >> sh;
+                if (sh + w > 64) win |= (uint64_t)__ldcs(gp + 2) << (64 - sh);
+                __stcs(o + idx, decode_field(win & wmask, e, m, d.scale));
+            }
+        }
+    }
+}
+
+int grid_for(uint64_t njobs) {
+    const uint64_t blocks = (njobs + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, 148ull * 16));
+}
+
+struct Scratch {
+    DevBuf jobs, err;
+};
+
+}  // namespace
+
+static void upload_jobs(const std::vector<Job>& jobs, DevBuf& dj, void* stream) {
+    dj.alloc(std::max<size_t>(16, jobs.size() * sizeof(Job)));
+    h2d(dj.p, jobs.data(), jobs.size() * sizeof(Job), stream);
+}
+
+void launch_analyze_jobs(const double* values, const uint64_t* voff, const uint64_t* d_count,
+                         const uint64_t* h_count, uint64_t nbuf, hcmx_stats* stats, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const auto jobs = make_jobs(h_count, nbuf);
+    DevBuf dj;
+    upload_jobs(jobs, dj, stream);
+    const int gi = (int)std::min<uint64_t>((nbuf + 255) / 256 + 1, 4096);
+    k_stats_init<<<gi, 256, 0, s>>>(stats, nbuf);
+    if (!jobs.empty())
+        k_analyze<<<grid_for(jobs.size()), kWarpsPerBlock * 32, 0, s>>>(values, voff, d_count,
+                                                                         dj.as<Job>(), jobs.size(), stats);
+    k_stats_final<<<gi, 256, 0, s>>>(stats, nbuf);
+    check_cuda(cudaGetLastError(), "analyze launch");
+    stream_sync(stream);  // jobs buffer lifetime
+}
+
+// returns nonzero if a non-finite value was met
+int launch_pack_jobs(const double* values, const uint64_t* voff, const uint64_t* d_count,
+                     const uint64_t* h_count, const hcmx_descriptor* desc, const uint64_t* poff,
+                     uint64_t nbuf, uint8_t* payload, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const auto jobs = make_jobs(h_count, nbuf);
+    if (jobs.empty()) return 0;
+    DevBuf dj, de(sizeof(int));
+    upload_jobs(jobs, dj, stream);
+    check_cuda(cudaMemsetAsync(de.p, 0, sizeof(int), s), "memset");
+    k_pack<<<grid_for(jobs.size()), kWarpsPerBlock * 32, 0, s>>>(values, voff, d_count, desc, poff,
+                                                                 dj.as<Job>(), jobs.size(), payload,
+                                                                 de.as<int>());
+    check_cuda(cudaGetLastError(), "pack launch");
+    int err = 0;
+    d2h(&err, de.p, sizeof(int), stream);
+    stream_sync(stream);
+    return err;
+}
+
+void launch_unpack_jobs(const uint8_t* payload, const uint64_t* poff, const uint64_t* d_count,
+                        const uint64_t* h_count, const hcmx_descriptor* desc, const uint64_t* voff,
+                        uint64_t nbuf, double* out, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const auto jobs = make_jobs(h_count, nbuf);
+    if (jobs.empty()) return;
+    DevBuf dj;
+    upload_jobs(jobs, dj, stream);
+    k_unpack<<<grid_for(jobs.size()), kWarpsPerBlock * 32, 0, s>>>(payload, poff, d_count, desc, voff,
+                                                                   dj.as<Job>(), jobs.size(), out);
+    check_cuda(cudaGetLastError(), "unpack launch");
+    stream_sync(stream);
+}
+
+}  // namespace hcmx_gpu
+
+// ================================================================ C-ABI ====
+using namespace hcmx_gpu;
+
+namespace {
+
+DevBuf upload_u64(const uint64_t* h, uint64_t n, void* stream) {
+    DevBuf d(std::max<uint64_t>(8, n * 8));
+    h2d(d.p, h, n * 8, stream);
+    return d;
+}
+
+void validate_desc(const hcmx_descriptor& d) {
+    if (d.scheme > 3 || d.exp_bits > 11 || d.mant_bits < 1 || d.mant_bits > 52)
+        throw invalid_argument("invalid codec descriptor");
+    if (d.bit_width != bit_width(d.scheme, d.exp_bits, d.mant_bits))
+        throw invalid_argument("descriptor bit_width does not match scheme/e/m");
+}
+
+// host side of codec::compress for a batch: stats -> descriptors -> offsets
+void select_layouts(const std::vector<hcmx_stats>& st, const uint64_t* h_count, uint64_t nbuf,
+                    double eps, int scheme, hcmx_descriptor* h_desc, uint64_t* h_poff,
+                    uint64_t* total) {
+    mantissa_bits_for(eps);  // eps validation first (codec.cpp:63-64)
+    uint64_t off = 0;
+    for (uint64_t b = 0; b < nbuf; ++b) {
+        if (st[b].non_finite) throw invalid_argument("compress: values must be finite");
+        h_desc[b] = make_descriptor(scheme, eps, st[b]);
+        h_poff[b] = off;
+        off += round16(payload_bytes(h_count[b], h_desc[b].bit_width));
+    }
+    *total = off;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hcmx_gpu_init(int device) {
+    return guarded([&] {
+        require_device();
+        check_cuda(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp p{};
+        check_cuda(cudaGetDeviceProperties(&p, device), "cudaGetDeviceProperties");
+        if (p.major != 10)
+            throw cuda_error("libhcmx_gpu is built for sm_100a (B200); device is sm_" +
+                             std::to_string(p.major * 10 + p.minor));
+    });
+}
+
+int hcmx_gpu_codec_analyze(const double* d_values, const uint64_t* d_voff, const uint64_t* h_count,
+                           uint64_t nbuf, hcmx_stats* d_stats, void* stream) {
+    return guarded([&] {
+        require_device();
+        DevBuf dc = upload_u64(h_count, nbuf, stream);
+        launch_analyze_jobs(d_values, d_voff, dc.as<uint64_t>(), h_count, nbuf, d_stats, stream);
+    });
+}
+
+int hcmx_gpu_codec_pack(const double* d_values, const uint64_t* d_voff, const uint64_t* h_count,
+                        const hcmx_descriptor* d_desc, const uint64_t* d_poff, uint64_t nbuf,
+                        uint8_t* d_payload, void* stream) {
+    return guarded([&] {
+        require_device();
+        DevBuf dc = upload_u64(h_count, nbuf, stream);
+        if (launch_pack_jobs(d_values, d_voff, dc.as<uint64_t>(), h_count, d_desc, d_poff, nbuf,
+                             d_payload, stream))
+            throw invalid_argument("compress: values must be finite");
+    });
+}
+
+int hcmx_gpu_codec_unpack(const uint8_t* d_payload, const uint64_t* d_poff, const uint64_t* h_count,
+                          const hcmx_descriptor* d_desc, const uint64_t* d_voff, uint64_t nbuf,
+                          double* d_out, void* stream) {
+    return guarded([&] {
+        require_device();
+        DevBuf dc = upload_u64(h_count, nbuf, stream);
+        launch_unpack_jobs(d_payload, d_poff, dc.as<uint64_t>(), h_count, d_desc, d_voff, nbuf, d_out,
+                           stream);
+    });
+}
+
+int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff, const uint64_t* h_count,
+                            uint64_t nbuf, double eps, int scheme, uint8_t* d_payload,
+                            uint64_t payload_capacity, hcmx_descriptor* h_desc, uint64_t* h_poff,
+                            uint64_t* h_total, void* stream) {
+    return guarded([&] {
+        require_device();
+        alignment_unit(scheme);
+        mantissa_bits_for(eps);
+        DevBuf dc = upload_u64(h_count, nbuf, stream);
+        DevBuf dst(std::max<uint64_t>(24, nbuf * sizeof(hcmx_stats)));
+        launch_analyze_jobs(d_values, d_voff, dc.as<uint64_t>(), h_count, nbuf, dst.as<hcmx_stats>(),
+                            stream);
+        std::vector<hcmx_stats> st(nbuf);
+        d2h(st.data(), dst.p, nbuf * sizeof(hcmx_stats), stream);
+        stream_sync(stream);
+        select_layouts(st, h_count, nbuf, eps, scheme, h_desc, h_poff, h_total);
+        if (*h_total > payload_capacity) throw invalid_argument("compress: payload capacity too small");
+        DevBuf dd(std::max<uint64_t>(16, nbuf * sizeof(hcmx_descriptor)));
+        h2d(dd.p, h_desc, nbuf * sizeof(hcmx_descriptor), stream);
+        DevBuf dp = upload_u64(h_poff, nbuf, stream);
+        if (launch_pack_jobs(d_values, d_voff, dc.as<uint64_t>(), h_count, dd.as<hcmx_descriptor>(),
+                             dp.as<uint64_t>(), nbuf, d_payload, stream))
+            throw invalid_argument("compress: values must be finite");
+    });
+}
+
+int hcmx_gpu_compress(const double* h_values, uint64_t count, double eps, int scheme,
+                      hcmx_descriptor* desc, uint8_t* h_payload, uint64_t capacity,
+                      uint64_t* payload_len) {
+    return guarded([&] {
+        require_device();
+        alignment_unit(scheme);
+        mantissa_bits_for(eps);
+        DevBuf dv(std::max<uint64_t>(8, count * 8));
+        h2d(dv.p, h_values, count * 8, nullptr);
+        const uint64_t zero = 0;
+        DevBuf dvo = upload_u64(&zero, 1, nullptr);
+        DevBuf dpay(round16(count * 8) + 16);
+        uint64_t poff = 0, total = 0;
+        int st = hcmx_gpu_codec_compress(dv.as<double>(), dvo.as<uint64_t>(), &count, 1, eps, scheme,
+                                         dpay.as<uint8_t>(), dpay.bytes, desc, &poff, &total, nullptr);
+        if (st == HCMX_INVALID_ARGUMENT) throw invalid_argument(hcmx_gpu_last_error());
+        if (st) throw cuda_error(hcmx_gpu_last_error());
+        const uint64_t len = payload_bytes(count, desc->bit_width);
+        if (len > capacity) throw invalid_argument("compress: output capacity too small");
+        d2h(h_payload, dpay.p, len, nullptr);
+        stream_sync(nullptr);
+        *payload_len = len;
+    });
+}
+
+int hcmx_gpu_compress_block(const double* h_values, uint64_t count, const hcmx_descriptor* desc,
+                            uint8_t* h_payload, uint64_t capacity, uint64_t* payload_len) {
+    return guarded([&] {
+        require_device();
+        validate_desc(*desc);
+        const uint64_t len = payload_bytes(count, desc->bit_width);
+        if (len > capacity) throw invalid_argument("compress_block: output capacity too small");
+        DevBuf dv(std::max<uint64_t>(8, count * 8));
+        h2d(dv.p, h_values, count * 8, nullptr);
+        const uint64_t zero = 0;
+        DevBuf dvo = upload_u64(&zero, 1, nullptr);
+        DevBuf dpo = upload_u64(&zero, 1, nullptr);
+        DevBuf dd(sizeof(hcmx_descriptor));
+        h2d(dd.p, desc, sizeof(hcmx_descriptor), nullptr);
+        DevBuf dpay(round16(len) + 16);
+        DevBuf dc = upload_u64(&count, 1, nullptr);
+        if (launch_pack_jobs(dv.as<double>(), dvo.as<uint64_t>(), dc.as<uint64_t>(), &count,
+                             dd.as<hcmx_descriptor>(), dpo.as<uint64_t>(), 1, dpay.as<uint8_t>(), nullptr))
+            throw invalid_argument("compress: values must be finite");
+        d2h(h_payload, dpay.p, len, nullptr);
+        stream_sync(nullptr);
+        *payload_len = len;
+    });
+}
+
+int hcmx_gpu_decompress_into(const hcmx_descriptor* desc, uint64_t count, const uint8_t* h_payload,
+                             uint64_t payload_len, double* h_out) {
+    return guarded([&] {
+        require_device();
+        validate_desc(*desc);
+        const uint64_t need = payload_bytes(count, desc->bit_width);
+        // BitReader throws when a read passes the end (bitstream.hpp:80-82)
+        if (payload_len < need) throw corrupt_buffer("bitstream: payload ends inside a value");
+        if (count == 0) return;
+        DevBuf dpay(round16(need) + 16);
+        h2d(dpay.p, h_payload, need, nullptr);
+        const uint64_t zero = 0;
+        DevBuf dvo = upload_u64(&zero, 1, nullptr);
+        DevBuf dpo = upload_u64(&zero, 1, nullptr);
+        DevBuf dd(sizeof(hcmx_descriptor));
+        h2d(dd.p, desc, sizeof(hcmx_descriptor), nullptr);
+        DevBuf dout(count * 8);
+        DevBuf dc = upload_u64(&count, 1, nullptr);
+        launch_unpack_jobs(dpay.as<uint8_t>(), dpo.as<uint64_t>(), dc.as<uint64_t>(), &count,
+                           dd.as<hcmx_descriptor>(), dvo.as<uint64_t>(), 1, dout.as<double>(), nullptr);
+        d2h(h_out, dout.p, count * 8, nullptr);
+        stream_sync(nullptr);
+    });
+}
+
+// mixedprec.cpp:155-187 (aplr_compress) batched over leaves with given factors
+int hcmx_gpu_aplr_compress(uint64_t nleaves, const uint64_t* h_rows, const uint64_t* h_cols,
+                           const uint64_t* h_k, const double* d_W, const uint64_t* h_woff,
+                           const double* d_X, const uint64_t* h_xoff, const double* h_sigma,
+                           const uint64_t* h_soff, const uint64_t* h_boff, double eps, int scheme,
+                           uint8_t* d_payload, uint64_t payload_capacity, hcmx_descriptor* h_desc,
+                           uint64_t* h_poff, uint64_t* h_total, void* stream) {
+    return guarded([&] {
+        require_device();
+        alignment_unit(scheme);
+        // column buffers: W columns of all leaves, then X columns of all leaves,
+        // analysed in two batches (they live in different device arrays)
+        uint64_t nb = 0;
+        for (uint64_t j = 0; j < nleaves; ++j) nb = std::max(nb, h_boff[j] + 2 * h_k[j]);
+        std::vector<uint64_t> wv, wc, xv, xc, wbuf, xbuf;
+        for (uint64_t j = 0; j < nleaves; ++j)
+            for (uint64_t i = 0; i < h_k[j]; ++i) {
+                wv.push_back(h_woff[j] + i * h_rows[j]);
+                wc.push_back(h_rows[j]);
+                wbuf.push_back(h_boff[j] + i);
+                xv.push_back(h_xoff[j] + i * h_cols[j]);
+                xc.push_back(h_cols[j]);
+                xbuf.push_back(h_boff[j] + h_k[j] + i);
+            }
+        const uint64_t ncol = wv.size();
+        std::vector<hcmx_stats> sw(ncol), sx(ncol);
+        if (ncol) {
+            DevBuf dst(ncol * sizeof(hcmx_stats));
+            DevBuf dwv = upload_u64(wv.data(), ncol, stream), dwc = upload_u64(wc.data(), ncol, stream);
+            launch_analyze_jobs(d_W, dwv.as<uint64_t>(), dwc.as<uint64_t>(), wc.data(), ncol,
+                                dst.as<hcmx_stats>(), stream);
+            d2h(sw.data(), dst.p, ncol * sizeof(hcmx_stats), stream);
+            DevBuf dxv = upload_u64(xv.data(), ncol, stream), dxc = upload_u64(xc.data(), ncol, stream);
+            launch_analyze_jobs(d_X, dxv.as<uint64_t>(), dxc.as<uint64_t>(), xc.data(), ncol,
+                                dst.as<hcmx_stats>(), stream);
+            d2h(sx.data(), dst.p, ncol * sizeof(hcmx_stats), stream);
+            stream_sync(stream);
+        }
+        // host: factor-wide e (mixedprec.cpp:168-169), per-column eps_i (174) and scale (177-184)
+        uint64_t c = 0;
+        for (uint64_t j = 0; j < nleaves; ++j) {
+            const uint64_t k = h_k[j];
+            if (k == 0) continue;
+            hcmx_stats fw{INFINITY, 0.0, 1u, 0u}, fx{INFINITY, 0.0, 1u, 0u};
+            for (uint64_t i = 0; i < k; ++i) {
+                for (int side = 0; side < 2; ++side) {
+                    const hcmx_stats& s = side ? sx[c + i] : sw[c + i];
+                    hcmx_stats& f = side ? fx : fw;
+                    if (s.non_finite) throw invalid_argument("compress: values must be finite");
+                    if (!s.all_zero) {
+                        f.all_zero = 0;
+                        f.min_mag = std::min(f.min_mag, s.min_mag);
+                        f.max_mag = std::max(f.max_mag, s.max_mag);
+                    }
+                }
+            }
+            if (fw.all_zero) fw.min_mag = fw.max_mag = 0.0;
+            if (fx.all_zero) fx.min_mag = fx.max_mag = 0.0;
+            const uint8_t e_w = exponent_bits_for(fw), e_x = exponent_bits_for(fx);
+            const double* sig = h_sigma + h_soff[j];
+            const double delta = eps * sig[0];
+            for (uint64_t i = 0; i < k; ++i) {
+                const double eps_i = std::min(0.5, delta / sig[i]);
+                const hcmx_stats& a = sw[c + i];
+                const hcmx_stats& b = sx[c + i];
+                h_desc[wbuf[c + i]] = make_descriptor(scheme, eps_i, a.all_zero ? 1.0 : a.min_mag, e_w);
+                h_desc[xbuf[c + i]] = make_descriptor(scheme, eps_i, b.all_zero ? 1.0 : b.min_mag, e_x);
+            }
+            c += k;
+        }
+        // payload offsets in buffer order
+        std::vector<uint64_t> cnt(nb, 0);
+        for (uint64_t i = 0; i < ncol; ++i) {
+            cnt[wbuf[i]] = wc[i];
+            cnt[xbuf[i]] = xc[i];
+        }
+        uint64_t off = 0;
+        for (uint64_t b = 0; b < nb; ++b) {
+            h_poff[b] = off;
+            off += round16(payload_bytes(cnt[b], h_desc[b].bit_width));
+        }
+        *h_total = off;
+        if (off > payload_capacity) throw invalid_argument("aplr_compress: payload capacity too small");
+        if (!ncol) return;
+        std::vector<hcmx_descriptor> dw(ncol), dx(ncol);
+        std::vector<uint64_t> pw(ncol), px(ncol);
+        for (uint64_t i = 0; i < ncol; ++i) {
+            dw[i] = h_desc[wbuf[i]];
+            dx[i] = h_desc[xbuf[i]];
+            pw[i] = h_poff[wbuf[i]];
+            px[i] = h_poff[xbuf[i]];
+        }
+        DevBuf ddw(ncol * sizeof(hcmx_descriptor)), ddx(ncol * sizeof(hcmx_descriptor));
+        h2d(ddw.p, dw.data(), ncol * sizeof(hcmx_descriptor), stream);
+        h2d(ddx.p, dx.data(), ncol * sizeof(hcmx_descriptor), stream);
+        DevBuf dpw = upload_u64(pw.data(), ncol, stream), dpx = upload_u64(px.data(), ncol, stream);
+        DevBuf dwv = upload_u64(wv.data(), ncol, stream), dwc = upload_u64(wc.data(), ncol, stream);
+        DevBuf dxv = upload_u64(xv.data(), ncol, stream), dxc = upload_u64(xc.data(), ncol, stream);
+        if (launch_pack_jobs(d_W, dwv.as<uint64_t>(), dwc.as<uint64_t>(), wc.data(), ddw.as<hcmx_descriptor>(),
+                             dpw.as<uint64_t>(), ncol, d_payload, stream) ||
+            launch_pack_jobs(d_X, dxv.as<uint64_t>(), dxc.as<uint64_t>(), xc.data(), ddx.as<hcmx_descriptor>(),
+                             dpx.as<uint64_t>(), ncol, d_payload, stream))
+            throw invalid_argument("compress: values must be finite");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,351 @@
+"""hcmx H-matrix on the B200: compress_in_place, the device-resident compressed
+H-matrix and matvec (hmatrix.hpp:93-153).
+
+The reference declares these functions but ships no hmatrix.cpp, so the
+contract comes from hmatrix.hpp and SPEC.md:
+  * compress_in_place(M, eps, mode, dense_too): lowrank leaves -> APLR
+    (per-column codec, mixedprec.cpp:155-187), dense leaves -> codec::compress
+    when dense_too; returns a MemoryReport
+  * matvec(alpha, M, x, beta, y, transpose=False): y := alpha M x + beta y in the
+    internal (cluster-permuted) index space; alpha == 0 leaves M untouched;
+    dimension mismatch -> ValueError (std::invalid_argument)
+
+The flattened form (FlatHMatrix) is the exchange format with the C-ABI
+(hcmx_hmat_desc) and with the CPU oracle: leaves in for_each_leaf preorder,
+one codec buffer per dense leaf (column-major scan, hmatrix.hpp:42-44), 2k
+buffers per APLR leaf (W columns, then X columns).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import DESC_DTYPE, check, lib, ptr, u64p
+from .assemble import Assembled, assemble
+from .codec import Scheme, compress_batch
+from .problems import config as problem_config, make_kernel, make_points
+from .tree import build_block_tree, build_cluster_tree
+
+__all__ = ["FlatHMatrix", "MemoryReport", "compress_in_place", "HMatrix", "matvec", "build_config",
+           "StorageMode"]
+
+
+@dataclass
+class StorageMode:
+    """hmatrix.hpp:32-40 (the GPU matvec covers kind 'aplr' + dense codec)"""
+    kind: str = "aplr"
+    scheme: Scheme = Scheme.afl
+
+    @staticmethod
+    def parse(name: str) -> "StorageMode":
+        name = name.lower()
+        if name.endswith("-aplr"):
+            return StorageMode("aplr", Scheme[name[:-5]])
+        if name in ("afl", "aflp", "bfl", "dfl"):
+            return StorageMode("codec", Scheme[name])
+        if name in ("fp64", "mp"):
+            return StorageMode(name, Scheme.afl)
+        raise ValueError(f"unknown storage mode {name}")
+
+    def name(self) -> str:
+        if self.kind == "aplr":
+            return f"{self.scheme.name}-aplr"
+        return self.scheme.name if self.kind == "codec" else self.kind
+
+
+@dataclass
+class MemoryReport:
+    """hmatrix.hpp:96-113"""
+    dense_raw: int = 0
+    dense_compressed: int = 0
+    lowrank_raw: int = 0
+    lowrank_compressed: int = 0
+    overhead: int = 0
+    uncompressed_equivalent: int = 0
+
+    def payload_total(self) -> int:
+        return self.dense_raw + self.dense_compressed + self.lowrank_raw + self.lowrank_compressed
+
+    def total(self) -> int:
+        return self.payload_total() + self.overhead
+
+    def rate(self) -> float:
+        t = self.payload_total()
+        return 0.0 if t == 0 else self.uncompressed_equivalent / t
+
+
+@dataclass
+class FlatHMatrix:
+    n_rows: int
+    n_cols: int
+    row0: np.ndarray
+    row1: np.ndarray
+    col0: np.ndarray
+    col1: np.ndarray
+    kind: np.ndarray
+    rank: np.ndarray
+    buf0: np.ndarray
+    sig0: np.ndarray
+    sigma: np.ndarray
+    desc: np.ndarray          # DESC_DTYPE per buffer
+    count: np.ndarray         # int64
+    poff: np.ndarray          # int64 byte offsets into blob
+    plen: np.ndarray          # int64 payload bytes
+    blob: object              # np.uint8 (host) or torch.uint8 (cuda)
+    raw: np.ndarray | None = None
+    meta: dict = field(default_factory=dict)
+
+    # oracle-facing views
+    @property
+    def scheme(self):
+        return self.desc["scheme"]
+
+    @property
+    def e(self):
+        return self.desc["exp_bits"]
+
+    @property
+    def m(self):
+        return self.desc["mant_bits"]
+
+    @property
+    def scale(self):
+        return self.desc["scale"]
+
+    @property
+    def nleaves(self):
+        return self.row0.size
+
+    def host(self) -> "FlatHMatrix":
+        if isinstance(self.blob, torch.Tensor):
+            return FlatHMatrix(**{**self.__dict__, "blob": self.blob.cpu().numpy()})
+        return self
+
+    def compressed_bytes(self) -> int:
+        """sum of CompressedBuffer::byte_size (20 + payload) + 8 k sigma per APLR leaf"""
+        return int((self.plen + 20).sum() + 8 * self.rank[self.kind == 1].sum())
+
+    def memory_footprint(self) -> MemoryReport:
+        """hmatrix.hpp:124 memory_footprint for the compressed payload kinds"""
+        r = MemoryReport()
+        rows, cols = self.row1 - self.row0, self.col1 - self.col0
+        for l in range(self.nleaves):
+            if self.kind[l] == 0:
+                r.dense_compressed += 20 + int(self.plen[self.buf0[l]])
+                r.uncompressed_equivalent += 8 * int(rows[l] * cols[l])
+            else:
+                k = int(self.rank[l])
+                b = int(self.buf0[l])
+                r.lowrank_compressed += 8 + 8 * k + int((self.plen[b: b + 2 * k] + 20).sum())
+                r.uncompressed_equivalent += 8 * int((rows[l] + cols[l]) * k)
+        r.overhead = 16 * self.nleaves
+        return r
+
+
+def compress_in_place(A: Assembled, eps: float, mode: StorageMode | str = "afl-aplr",
+                      dense_too: bool = True, threads: int = 1) -> FlatHMatrix:
+    """hmatrix.hpp:115-119 on the device: dense leaves -> codec::compress (batched
+    kernels), lowrank leaves -> APLR (hcmx_gpu_aplr_compress).  Returns the
+    flattened compressed H-matrix (payload blob resident on the GPU)."""
+    if isinstance(mode, str):
+        mode = StorageMode.parse(mode)
+    if mode.kind != "aplr":
+        raise ValueError("compress_in_place: the GPU path implements the aplr storage modes")
+    if not dense_too:
+        raise ValueError("compress_in_place: the GPU matvec needs compressed dense leaves (dense_too)")
+    _lib.ensure_device()
+    scheme = int(mode.scheme)
+    lv = A.leaves
+    L = len(lv)
+    rows = (lv.row1 - lv.row0).astype(np.int64)
+    cols = (lv.col1 - lv.col0).astype(np.int64)
+    didx = np.nonzero(A.kind == 0)[0]
+    lidx = np.nonzero(A.kind == 1)[0]
+
+    # buffer numbering in leaf order
+    nbuf_leaf = np.where(A.kind == 0, 1, 2 * A.rank)
+    buf0 = np.concatenate([[0], np.cumsum(nbuf_leaf)[:-1]]).astype(np.int64)
+    nb = int(nbuf_leaf.sum())
+    desc = np.zeros(nb, dtype=DESC_DTYPE)
+    count = np.zeros(nb, np.int64)
+    poff = np.zeros(nb, np.int64)
+
+    # dense leaves: one batched compress
+    dn = rows[didx] * cols[didx]
+    dense_bb = compress_batch(A.dense, dn.astype(np.uint64), eps, scheme,
+                              voff=A.dense_off[didx].astype(np.uint64)) if didx.size else None
+    # lowrank leaves: batched APLR
+    kk = A.rank[lidx].astype(np.uint64)
+    lr_payload = None
+    lr_desc = lr_poff = None
+    if lidx.size and kk.sum() > 0:
+        lr_boff = np.concatenate([[0], np.cumsum(2 * kk)[:-1]]).astype(np.uint64)
+        nlb = int(2 * kk.sum())
+        cap = int(8 * (A.W.numel() + A.X.numel()) + 16 * nlb + 16)
+        lr_payload = torch.empty(cap, dtype=torch.uint8, device="cuda")
+        lr_desc = np.zeros(nlb, dtype=DESC_DTYPE)
+        lr_poff = np.zeros(nlb, dtype=np.uint64)
+        total = C.c_uint64()
+        W = A.W.to("cuda")
+        X = A.X.to("cuda")
+        sig = np.ascontiguousarray(A.sigma, dtype=np.float64)
+        rr = rows[lidx].astype(np.uint64); cc = cols[lidx].astype(np.uint64)
+        wo = A.w_off[lidx].astype(np.uint64); xo = A.x_off[lidx].astype(np.uint64)
+        so = A.sig_off[lidx].astype(np.uint64)
+        check(lib().hcmx_gpu_aplr_compress(lidx.size, u64p(rr), u64p(cc), u64p(kk), ptr(W), u64p(wo),
+                                           ptr(X), u64p(xo), ptr(sig), u64p(so), u64p(lr_boff),
+                                           float(eps), scheme, ptr(lr_payload), cap, ptr(lr_desc),
+                                           u64p(lr_poff), C.byref(total),
+                                           torch.cuda.current_stream().cuda_stream), "aplr_compress")
+        lr_total = total.value
+    # merge into one blob: dense arena then lowrank arena
+    dense_total = dense_bb.total if dense_bb is not None else 0
+    parts = []
+    if dense_bb is not None:
+        parts.append(dense_bb.payload[:dense_total])
+    if lr_payload is not None:
+        parts.append(lr_payload[:lr_total])
+    blob = torch.cat(parts) if parts else torch.zeros(16, dtype=torch.uint8, device="cuda")
+    if dense_bb is not None:
+        b = buf0[didx]
+        desc[b] = dense_bb.desc
+        count[b] = dn
+        poff[b] = dense_bb.poff.astype(np.int64)
+    if lr_payload is not None:
+        j = 0
+        for t, l in enumerate(lidx):
+            k = int(A.rank[l])
+            sl = slice(int(buf0[l]), int(buf0[l]) + 2 * k)
+            desc[sl] = lr_desc[j: j + 2 * k]
+            count[sl] = [rows[l]] * k + [cols[l]] * k
+            poff[sl] = lr_poff[j: j + 2 * k].astype(np.int64) + dense_total
+            j += 2 * k
+    plen = (count * desc["bit_width"].astype(np.int64) + 7) // 8
+    sig0 = A.sig_off.copy()
+    sig0[sig0 < 0] = 0
+    return FlatHMatrix(A.n, A.n, lv.row0.astype(np.int64), lv.row1.astype(np.int64),
+                       lv.col0.astype(np.int64), lv.col1.astype(np.int64), A.kind.astype(np.int64),
+                       A.rank.astype(np.int64), buf0, sig0, np.ascontiguousarray(A.sigma), desc,
+                       count, poff, plen, blob, meta={"eps": eps, "mode": mode.name()})
+
+
+def build_config(cfg, scheme="afl", device=None, n=None, seed=1, eps=None) -> tuple[FlatHMatrix, dict]:
+    """setup for a BASELINE config (or a dict): points -> cluster/block tree ->
+    FP64 assembly -> compress_in_place on the GPU"""
+    c = problem_config(cfg) if not isinstance(cfg, dict) else dict(cfg)
+    if n is not None:
+        c["n"] = n
+    if eps is not None:
+        c["eps"] = eps
+    pts = make_points(c["geometry"], c["n"], seed)
+    ct = build_cluster_tree(pts, c["leaf"])
+    leaves = build_block_tree(ct, ct, c["eta"])
+    A = assemble(pts[ct.i2e], leaves, make_kernel(c["kernel"]), c["eps"], device=device)
+    flat = compress_in_place(A, c["eps"], f"{Scheme[scheme].name if isinstance(scheme, str) else Scheme(scheme).name}-aplr")
+    info = dict(c, leaves=len(leaves), dense_leaves=int((A.kind == 0).sum()),
+                lowrank_leaves=int((A.kind == 1).sum()), mean_rank=float(A.rank[A.kind == 1].mean())
+                if (A.kind == 1).any() else 0.0, max_rank=int(A.rank.max()) if len(A.rank) else 0,
+                depth=ct.depth())
+    return flat, info
+
+
+class HMatrix:
+    """Device-resident compressed H-matrix (handle over hcmx_gpu_hmat_*)."""
+
+    def __init__(self, flat: FlatHMatrix, row_range: tuple[int, int] | None = None):
+        _lib.ensure_device()
+        self.n_rows, self.n_cols = int(flat.n_rows), int(flat.n_cols)
+        self.row_range = row_range or (0, self.n_rows)
+        keep = {}
+        a = lambda x, t: keep.setdefault(id(x), np.ascontiguousarray(x, dtype=t))
+        i64 = lambda x: a(x, np.int64).ctypes.data_as(C.POINTER(C.c_int64))
+        sigma = np.ascontiguousarray(flat.sigma if flat.sigma.size else np.zeros(1), dtype=np.float64)
+        desc = np.ascontiguousarray(flat.desc)
+        blob = flat.blob
+        on_dev = isinstance(blob, torch.Tensor) and blob.is_cuda
+        if isinstance(blob, torch.Tensor) and not on_dev:
+            blob = blob.numpy()
+        self._keep = (keep, sigma, desc, blob)
+        d = _lib.hcmx_hmat_desc()
+        d.n_rows, d.n_cols, d.nleaves = self.n_rows, self.n_cols, flat.nleaves
+        d.nbuffers, d.nsigma = desc.size, flat.sigma.size
+        d.blob_bytes = blob.numel() if isinstance(blob, torch.Tensor) else blob.size
+        for name in ("row0", "row1", "col0", "col1", "kind", "rank", "buf0", "sig0"):
+            setattr(d, name, i64(getattr(flat, name)))
+        d.sigma = sigma.ctypes.data_as(C.POINTER(C.c_double))
+        d.desc = desc.ctypes.data_as(C.POINTER(_lib.hcmx_descriptor))
+        d.count, d.poff, d.plen = i64(flat.count), i64(flat.poff), i64(flat.plen)
+        d.blob = ptr(blob)
+        d.blob_on_device = int(on_dev)
+        d.row_begin, d.row_end = (0, 0) if row_range is None else row_range
+        h = C.c_void_p()
+        check(lib().hcmx_gpu_hmat_create(C.byref(d), C.byref(h)), "hmat_create")
+        self._h = h
+        self._keep = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            check(lib().hcmx_gpu_hmat_destroy(self._h), "hmat_destroy")
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def memory(self) -> _lib.hcmx_memory_report:
+        r = _lib.hcmx_memory_report()
+        check(lib().hcmx_gpu_hmat_memory(self._h, C.byref(r)), "hmat_memory")
+        return r
+
+    def matvec_device(self, alpha: float, x: torch.Tensor, beta: float, y: torch.Tensor,
+                      stream=None) -> torch.Tensor:
+        """device pointers, asynchronous on `stream` (default: torch's current)"""
+        if x.dtype != torch.float64 or y.dtype != torch.float64 or not (x.is_cuda and y.is_cuda):
+            raise ValueError("matvec: x and y must be cuda float64 tensors")
+        if x.numel() != self.n_cols or y.numel() != self.n_rows:
+            raise ValueError("matvec: dimension mismatch")
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        check(lib().hcmx_gpu_hmat_matvec_device(self._h, float(alpha), ptr(x), float(beta), ptr(y), s),
+              "matvec")
+        return y
+
+    def matvec(self, alpha: float, x, beta: float, y, transpose: bool = False):
+        """hmatrix.hpp:126-128 with host vectors (copies in/out inside)"""
+        if transpose:
+            raise ValueError("matvec: transpose is not supported by the GPU path yet")
+        if isinstance(x, torch.Tensor) and x.is_cuda:
+            return self.matvec_device(alpha, x, beta, y)
+        xa = np.ascontiguousarray(x, dtype=np.float64)
+        if xa.size != self.n_cols or np.asarray(y).size != self.n_rows:
+            raise ValueError("matvec: dimension mismatch")
+        if not (isinstance(y, np.ndarray) and y.dtype == np.float64 and y.flags.c_contiguous):
+            raise ValueError("matvec: y must be a contiguous float64 array")
+        check(lib().hcmx_gpu_hmat_matvec(self._h, float(alpha), ptr(xa), float(beta), ptr(y), 0),
+              "matvec")
+        return y
+
+    def launches(self) -> int:
+        return lib().hcmx_gpu_hmat_last_launches(self._h)
+
+    def timing(self, enable: int):
+        a, b, n = C.c_double(), C.c_double(), C.c_uint64()
+        check(lib().hcmx_gpu_hmat_timing(self._h, int(enable), C.byref(a), C.byref(b), C.byref(n)),
+              "timing")
+        return a.value, b.value, n.value
+
+    def export_buffer(self, b: int, nbytes: int) -> bytes:
+        out = np.zeros(max(nbytes, 1), np.uint8)
+        n = C.c_uint64()
+        check(lib().hcmx_gpu_hmat_export_buffer(self._h, b, ptr(out), out.size, C.byref(n)), "export")
+        return out[: n.value].tobytes()
+
+
+def matvec(alpha: float, M: HMatrix, x, beta: float, y, transpose: bool = False):
+    """hmatrix.hpp:126-128: y := alpha * op(M) * x + beta * y"""
+    return M.matvec(alpha, x, beta, y, transpose)

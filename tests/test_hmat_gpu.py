@@ -1,0 +1,152 @@
+"""Compressed H-matvec on the GPU vs the CPU oracle / reference glue:
+||y - y_ref|| / ||y_ref|| <= 1e-12 (BASELINE north star; FP64 reassociation only),
+APLR compression bit-exact, device layout round trip, alpha/beta semantics,
+row partitions, determinism."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12  # written in BASELINE.json north_star
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def test_golden_hmatrix(gpu, hmat_golden):
+    """reference-compressed leaves (n=768: ragged 48-row clusters), reference-glue y"""
+    from cpu_hmatrix import Flat
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    f = Flat.from_npz(hmat_golden).to_product()
+    H = HMatrix(f)
+    x = hmat_golden["x"]
+    y = np.zeros(f.n_rows)
+    H.matvec(1.0, x, 0.0, y)
+    assert rel(y, hmat_golden["y"]) <= TOL
+    y2 = hmat_golden["y"].copy()
+    H.matvec(-0.5, x, 2.0, y2)
+    assert rel(y2, hmat_golden["y2"]) <= TOL
+    # every packed buffer survives the re-tiling into the device arena bit for bit
+    for b in range(0, f.count.size, 7):
+        got = H.export_buffer(b, int(f.plen[b]))
+        assert got == f.blob[f.poff[b]: f.poff[b] + f.plen[b]].tobytes(), b
+
+
+@pytest.mark.parametrize("geometry,kernel,n,eps,scheme", [
+    ("fibonacci", "laplace", 2048, 1e-6, 0),
+    ("fibonacci", "laplace", 1536, 1e-8, 1),
+    ("cube", "matern", 1000, 1e-6, 2),
+    ("sphere", "laplace", 1100, 1e-4, 3),
+])
+def test_oracle_compressed_matrices(gpu, oracle, geometry, kernel, n, eps, scheme):
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    f, x = build_small_flat(n=n, eps=eps, scheme=scheme, geometry=geometry, kernel=kernel)
+    H = HMatrix(f.to_product())
+    y0 = np.random.default_rng(1).standard_normal(n)
+    for alpha, beta in ((1.0, 0.0), (0.3, 1.0), (-2.0, -0.5)):
+        ref = oracle.hmat_matvec(f, alpha, x, beta, y0, threads=4)
+        y = y0.copy()
+        H.matvec(alpha, x, beta, y)
+        assert rel(y, ref) <= TOL, (alpha, beta)
+
+
+def test_alpha_zero_leaves_matrix_untouched(gpu, hmat_golden):
+    from cpu_hmatrix import Flat
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    H = HMatrix(Flat.from_npz(hmat_golden).to_product())
+    y = np.random.default_rng(2).standard_normal(H.n_rows)
+    y0 = y.copy()
+    H.matvec(0.0, hmat_golden["x"], 3.0, y)
+    assert (y == 3.0 * y0).all()
+    assert H.launches() == 1
+    with pytest.raises(ValueError):
+        H.matvec(1.0, np.zeros(H.n_cols + 1), 0.0, np.zeros(H.n_rows))
+    with pytest.raises(ValueError):
+        H.matvec(1.0, hmat_golden["x"], 0.0, y, transpose=True)
+
+
+def test_device_compress_in_place_bit_exact(gpu, oracle):
+    """the product setup: FP64 assembly -> GPU compress_in_place; every buffer equals
+    the oracle's compress / APLR of the same FP64 inputs, and the matvec matches"""
+    from paper_2308_10960_b200 import assemble, problems, tree
+    from paper_2308_10960_b200.hmatrix import HMatrix, compress_in_place
+    pts = problems.make_points("fibonacci", 2048, 1)
+    ct = tree.build_cluster_tree(pts, 64)
+    lv = tree.build_block_tree(ct, ct, 2.0)
+    A = assemble.assemble(pts[ct.i2e], lv, problems.make_kernel("laplace"), 1e-6, device="cuda")
+    f = compress_in_place(A, 1e-6, "afl-aplr")
+    fh = f.host()
+    dense, W, X = A.dense.cpu().numpy(), A.W.cpu().numpy(), A.X.cpu().numpy()
+    rows, cols = lv.row1 - lv.row0, lv.col1 - lv.col0
+    for l in range(len(lv)):
+        b0 = int(fh.buf0[l])
+        if A.kind[l] == 0:
+            ob = oracle.compress(dense[A.dense_off[l]: A.dense_off[l] + rows[l] * cols[l]], 1e-6, 0)
+            bufs = [ob]
+        else:
+            k = int(A.rank[l])
+            Wl = W[A.w_off[l]: A.w_off[l] + rows[l] * k].reshape(k, rows[l]).T
+            Xl = X[A.x_off[l]: A.x_off[l] + cols[l] * k].reshape(k, cols[l]).T
+            bufs = oracle.aplr_compress(Wl, Xl, A.sigma[A.sig_off[l]: A.sig_off[l] + k], 1e-6, 0)
+        for i, ob in enumerate(bufs):
+            b = b0 + i
+            assert (fh.e[b], fh.m[b], fh.scale[b]) == (ob.e, ob.m, ob.scale)
+            assert fh.blob[fh.poff[b]: fh.poff[b] + fh.plen[b]].tobytes() == ob.payload
+    x = np.random.default_rng(0).uniform(-1, 1, 2048)
+    ref = oracle.hmat_matvec(fh, 1.0, x, 0.0, np.zeros(2048), threads=4)
+    y = np.zeros(2048)
+    HMatrix(f).matvec(1.0, x, 0.0, y)
+    assert rel(y, ref) <= TOL
+
+
+def test_row_partitions_compose(gpu, oracle):
+    """block-row partitioning (multi-GPU layout) on one device: the disjoint y
+    slices of two handles equal the full product"""
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    f, x = build_small_flat(n=2048, eps=1e-6, scheme=0)
+    ref = oracle.hmat_matvec(f, 1.0, x, 0.0, np.zeros(2048), threads=4)
+    fp = f.to_product()
+    for cuts in ([0, 1024, 2048], [0, 320, 1344, 2048], [0, 64, 2048]):
+        y = np.full(2048, np.nan)
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            H = HMatrix(fp, row_range=(a, b))
+            H.matvec(1.0, x, 0.0, y)
+        assert rel(y, ref) <= TOL, cuts
+
+
+def test_deterministic_and_device_api(gpu, hmat_golden):
+    from cpu_hmatrix import Flat
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    H = HMatrix(Flat.from_npz(hmat_golden).to_product())
+    x = torch.as_tensor(hmat_golden["x"]).cuda()
+    ys = []
+    for _ in range(3):
+        y = torch.zeros(H.n_rows, dtype=torch.float64, device="cuda")
+        H.matvec_device(1.0, x, 0.0, y)
+        ys.append(y.cpu().numpy())
+    assert all((ys[0].view(np.uint64) == t.view(np.uint64)).all() for t in ys[1:])
+    yh = np.zeros(H.n_rows)
+    H.matvec(1.0, hmat_golden["x"], 0.0, yh)
+    assert (yh.view(np.uint64) == ys[0].view(np.uint64)).all()
+    assert H.launches() == 2
+
+
+def test_config1_full_size(gpu, oracle):
+    """BASELINE config 1 (n=8192 Laplace sphere, eps 1e-6, AFL-APLR) end to end"""
+    from paper_2308_10960_b200.hmatrix import HMatrix, build_config
+    f, info = build_config(1)
+    fh = f.host()
+    assert 1300 <= info["dense_leaves"] <= 1400 and 2600 <= info["lowrank_leaves"] <= 2800
+    x = np.random.default_rng(0).uniform(-1, 1, f.n_cols)
+    ref = oracle.hmat_matvec(fh, 1.0, x, 0.0, np.zeros(f.n_rows), threads=8)
+    H = HMatrix(f)
+    y = np.zeros(f.n_rows)
+    H.matvec(1.0, x, 0.0, y)
+    assert rel(y, ref) <= TOL
+    rep = H.memory()
+    assert rep.dense_leaves == info["dense_leaves"]
+    rate = rep.uncompressed_equivalent / (rep.dense_compressed + rep.lowrank_compressed)
+    assert rate > 3.0  # ~29% of FP64 storage
