@@ -1,0 +1,485 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: compressed H-matrix-vector product on the B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 3] [--scheme afl]
+
+Workload (BASELINE.json metric "compressed H-matvec GB/s (compressed bytes)"):
+config 3 -- Laplace 1/(4 pi r) on n=131072 Fibonacci-sphere points, leaf 64,
+eta 2, SVD truncation 1e-8, AFL-APLR lowrank + AFL dense leaves; a step is one
+FP64 product y = A x over the whole matrix (100 repeated products with fixed x
+in the BASELINE).  Compressed streams (~1 GB) are far larger than L2, so no L2
+flush is needed between products.  Bytes per product follow SURVEY 8(d):
+sum(ceil(N w / 8) + 20) over codec buffers + 8 k per APLR leaf + 8 n (x) + 8 n (y).
+
+N > 1 (torchrun): block-row partition, x replicated, NCCL all-gather of the
+y slices after every product (strong scaling: the matrix is fixed).
+--impl reference: the reference codec (oracle/_ref, /root/reference
+codec.cpp) + the restated matvec glue on all host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region"""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(1)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0])); mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def partition_rows(flat, world):
+    """contiguous row ranges on row-block boundaries balanced by compressed bytes"""
+    n = flat.n_rows
+    if world == 1:
+        return [(0, n)]
+    rows = flat.row1 - flat.row0
+    # spread each leaf's bytes uniformly over its rows for the prefix
+    dens = np.zeros(n)
+    for l in range(flat.nleaves):
+        b0 = int(flat.buf0[l])
+        tot = float(flat.plen[b0]) if flat.kind[l] == 0 else float(flat.plen[b0: b0 + 2 * int(flat.rank[l])].sum())
+        dens[flat.row0[l]: flat.row1[l]] += tot / rows[l]
+    pref = np.concatenate([[0], np.cumsum(dens)])
+    cuts = [0]
+    for r in range(1, world):
+        target = pref[-1] * r / world
+        c = int(np.searchsorted(pref, target))
+        c = max(cuts[-1] + 64, (c + 32) // 64 * 64)
+        cuts.append(min(c, n))
+    cuts.append(n)
+    return list(zip(cuts[:-1], cuts[1:]))
+
+
+def step_bytes(flat, row_range=None):
+    """SURVEY 8(d) algorithmic bytes of one product (beta = 0)"""
+    a, b = row_range or (0, flat.n_rows)
+    sel = (flat.row0 >= a) & (flat.row1 <= b)  # the leaves restrict() keeps
+    tot = 0
+    for l in np.nonzero(sel)[0]:
+        b0 = int(flat.buf0[l])
+        if flat.kind[l] == 0:
+            tot += int(flat.plen[b0]) + 20
+        else:
+            k = int(flat.rank[l])
+            tot += int((flat.plen[b0: b0 + 2 * k] + 20).sum()) + 8 * k
+    return tot + 8 * flat.n_cols + 8 * (b - a)
+
+
+def kernel_bytes(flat):
+    """algorithmic bytes per launch of phase A (X streams, sigma, x) and phase B
+    (dense + W streams, y)"""
+    a = bb = 0
+    for l in range(flat.nleaves):
+        b0 = int(flat.buf0[l])
+        if flat.kind[l] == 0:
+            bb += int(flat.plen[b0]) + 20
+        else:
+            k = int(flat.rank[l])
+            a += int((flat.plen[b0 + k: b0 + 2 * k] + 20).sum()) + 8 * k
+            bb += int((flat.plen[b0: b0 + k] + 20).sum())
+    return a + 8 * flat.n_cols, bb + 8 * flat.n_rows
+
+
+def build_flat(cfg, scheme):
+    from paper_2308_10960_b200.hmatrix import build_config
+    t0 = time.time()
+    flat, info = build_config(cfg, scheme=scheme)
+    info["setup_s"] = round(time.time() - t0, 2)
+    return flat, info
+
+
+def cpu_reference_value(flat, threads, budget_s=15.0, max_reps=3):
+    """the reference codec (oracle/_ref) + restated matvec glue, timed on host
+    cores over a bounded sample (whole matrix, or a row slice if one product
+    would exceed the budget)"""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle, RefOracle
+    if RefOracle.available():
+        impl, kind = RefOracle(), "reference"
+    else:
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), os.path.join(ROOT, "oracle", "liboracle.so")],
+                       capture_output=True)
+        impl, kind = Oracle(), "port"
+    fh = flat.host()
+    x = np.random.default_rng(0).uniform(-1, 1, fh.n_cols)
+    # calibrate on a 1/16 row slice, then pick a sample that fits the budget
+    sub = restrict(fh, (0, max(64, fh.n_rows // 16 // 64 * 64)))
+    t = time.perf_counter()
+    impl.hmat_matvec(sub, 1.0, x, 0.0, np.zeros(fh.n_rows), threads=threads)
+    dt = time.perf_counter() - t
+    frac = min(1.0, (budget_s / max_reps) / max(dt * 16, 1e-9))
+    rows = max(64, int(fh.n_rows * frac) // 64 * 64)
+    sample = restrict(fh, (0, rows))
+    sb = step_bytes(fh, (0, rows))
+    times = []
+    for _ in range(max_reps):
+        t = time.perf_counter()
+        impl.hmat_matvec(sample, 1.0, x, 0.0, np.zeros(fh.n_rows), threads=threads)
+        times.append(time.perf_counter() - t)
+    best = min(times)
+    return {"value": sb / best / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": f"rows [0,{rows}) of {fh.n_rows} ({sb / 1e6:.1f} MB compressed), best of {max_reps}, "
+                      f"{threads} threads"}, sb, best
+
+
+def restrict(flat, rr):
+    """leaves of a row range (same buffers/blob; oracle ignores unlisted leaves)"""
+    from dataclasses import replace
+    a, b = rr
+    sel = (flat.row0 >= a) & (flat.row1 <= b)
+    return replace(flat, row0=flat.row0[sel], row1=flat.row1[sel], col0=flat.col0[sel],
+                   col1=flat.col1[sel], kind=flat.kind[sel], rank=flat.rank[sel],
+                   buf0=flat.buf0[sel], sig0=flat.sig0[sel])
+
+
+def codec_microbench(reps=5):
+    """BASELINE config 2: 4096 64x64 blocks, sign * 10^U[-6,0]; AFL at 1e-6"""
+    import torch
+    from paper_2308_10960_b200 import codec
+    nb, bs = 4096, 4096
+    rng = np.random.default_rng(2)
+    vals = np.sign(rng.standard_normal(nb * bs)) * 10 ** rng.uniform(-6, 0, nb * bs)
+    d = torch.as_tensor(vals).cuda()
+    counts = np.full(nb, bs, np.uint64)
+    out = {}
+    for eps in (1e-4, 1e-6, 1e-8):
+        bb = codec.compress_batch(d, counts, eps, codec.Scheme.afl)
+        dec = codec.decompress_batch(bb)
+        torch.cuda.synchronize()
+        pay = int(((counts * bb.desc["bit_width"].astype(np.uint64) + 7) // 8).sum()) + 20 * nb
+        algo = 8 * nb * bs + pay
+        tc, td = [], []
+        for _ in range(reps):
+            t = time.perf_counter()
+            bb = codec.compress_batch(d, counts, eps, codec.Scheme.afl, payload=bb.payload)
+            torch.cuda.synchronize()
+            tc.append(time.perf_counter() - t)
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record()
+            codec.decompress_batch(bb, out=dec)
+            t1.record()
+            torch.cuda.synchronize()
+            td.append(t0.elapsed_time(t1) / 1e3)
+        out[f"afl_{eps:g}"] = {"w_bits": int(bb.desc["bit_width"][0]),
+                               "compress_gbs": round(algo / min(tc) / 1e9, 1),
+                               "decompress_gbs": round(algo / min(td) / 1e9, 1)}
+    return out
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    flat, info = build_flat(args.config, args.scheme)
+    parts = partition_rows(flat, world)
+    rr = parts[rank]
+    H = HMatrix(flat, row_range=None if world == 1 else rr)
+    rep = H.memory()
+    n = flat.n_rows
+    x = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, n)).cuda()
+    y = torch.zeros(n, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    maxlen = max(b - a for a, b in parts)
+    slab = torch.zeros(maxlen, dtype=torch.float64, device="cuda")
+    gathered = torch.zeros(maxlen * world, dtype=torch.float64, device="cuda")
+
+    def step():
+        H.matvec_device(1.0, x, 0.0, y)
+        if world > 1:  # exchange step: every rank needs all of y for the next product
+            slab[: rr[1] - rr[0]].copy_(y[rr[0]: rr[1]])
+            dist.all_gather_into_tensor(gathered, slab)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    H.timing(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ms_a, ms_b, calls = H.timing(0)
+    clk = clocks.stop()
+    launches = H.launches() * args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    total_bytes = step_bytes(flat)  # whole matrix, once per product
+    value = total_bytes * args.steps / (ms / 1e3) / 1e9
+
+    # end to end through the reference-facing call: host x in, host y out
+    xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    xh.copy_(x.cpu())
+    yh = torch.zeros(n, dtype=torch.float64, pin_memory=True)
+    from paper_2308_10960_b200._lib import check, lib
+    if world == 1:
+        for _ in range(args.warmup):
+            check(lib().hcmx_gpu_hmat_matvec(H._h, 1.0, xh.data_ptr(), 0.0, yh.data_ptr(), 0))
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            check(lib().hcmx_gpu_hmat_matvec(H._h, 1.0, xh.data_ptr(), 0.0, yh.data_ptr(), 0))
+        e2e_s = time.perf_counter() - t
+    else:
+        e2e_s = None
+    line = None
+    if rank == 0:
+        peak, peak_src = _peaks()
+        ka, kb = kernel_bytes(flat)
+        per_a = ms_a / max(calls, 1)
+        per_b = ms_b / max(calls, 1)
+        dom = "phase_b" if per_b >= per_a else "phase_a"
+        dom_bytes, dom_ms = (kb, per_b) if dom == "phase_b" else (ka, per_a)
+        achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(dom)
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu, _, _ = cpu_reference_value(flat, os.cpu_count() or 1)
+        codec_res = codec_microbench() if (world == 1 and not args.no_codec) else None
+        line = {
+            "metric": "compressed H-matvec GB/s (compressed bytes)",
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Fibonacci sphere, Laplace kernel, BASELINE config 3)",
+            "config": {"workload": f"config{args.config}: Laplace sphere n={n}, leaf 64, eta 2, "
+                                   f"SVD 1e-8, {args.scheme.upper()}-APLR + {args.scheme.upper()} dense, y=Ax",
+                       "n": n, "leaves": info["leaves"], "dense_leaves": info["dense_leaves"],
+                       "lowrank_leaves": info["lowrank_leaves"], "mean_rank": round(info["mean_rank"], 2),
+                       "bytes_per_step": total_bytes,
+                       "fp64_bytes": int(rep.uncompressed_equivalent),
+                       "compression_rate": round(rep.uncompressed_equivalent / max(1, rep.dense_compressed + rep.lowrank_compressed), 3),
+                       "l2": "inputs larger than L2 (no flush)", "setup_s": info["setup_s"],
+                       "parallelism": f"block-row x{world}" if world > 1 else "single GPU",
+                       "matvec_frac_of_peak": round(value / world / peak, 4)},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic, "algorithmic_bytes_per_launch": dom_bytes,
+                         "ms_per_launch": round(dom_ms, 5),
+                         "phase_ms": {"phase_a": round(per_a, 5), "phase_b": round(per_b, 5)}},
+            "cpu_baseline": cpu,
+            "e2e": ({"value": round(total_bytes * args.steps / e2e_s / 1e9, 2), "unit": "GB/s",
+                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                     "api": "hcmx_gpu_hmat_matvec (host pointers, pinned)"} if e2e_s else None),
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if codec_res:
+            line["codec"] = codec_res
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    H.close()
+    return line
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    t0 = time.time()
+    flat, info = build_flat_cpu(args.config, args.scheme)
+    threads = os.cpu_count() or 1
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle, RefOracle
+    impl, kind = (RefOracle(), "reference") if RefOracle.available() else (Oracle(), "port")
+    n = flat.n_rows
+    x = np.random.default_rng(0).uniform(-1, 1, n)
+    # one step = the product over a row-slice sample sized to ~1 s
+    sub = restrict(flat, (0, max(64, n // 16 // 64 * 64)))
+    t = time.perf_counter()
+    impl.hmat_matvec(sub, 1.0, x, 0.0, np.zeros(n), threads=threads)
+    dt = max(time.perf_counter() - t, 1e-6) * 16
+    rows = min(n, max(64, int(n * min(1.0, 1.0 / dt)) // 64 * 64))
+    sample = restrict(flat, (0, rows))
+    sb = step_bytes(flat, (0, rows))
+    for _ in range(args.warmup):
+        impl.hmat_matvec(sample, 1.0, x, 0.0, np.zeros(n), threads=threads)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        impl.hmat_matvec(sample, 1.0, x, 0.0, np.zeros(n), threads=threads)
+    el = time.perf_counter() - t
+    v = sb * args.steps / el / 1e9
+    desc = f"rows [0,{rows}) of {n} ({sb / 1e6:.1f} MB compressed) per step, {threads} threads"
+    line = {"impl": "reference", "metric": "compressed H-matvec GB/s (compressed bytes)",
+            "value": round(v, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Fibonacci sphere, Laplace kernel, BASELINE config 3)",
+            "config": {"workload": f"config{args.config}: Laplace sphere n={n}, leaf 64, eta 2, SVD 1e-8, "
+                                   f"{args.scheme.upper()}-APLR + {args.scheme.upper()} dense, y=Ax",
+                       "n": n, "setup_s": round(time.time() - t0, 1)},
+            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+                             "sample": desc},
+            "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return line
+
+
+def build_flat_cpu(cfg, scheme):
+    """reference arm setup: FP64 assembly (torch), then the REFERENCE codec on the
+    host (compress for dense leaves, restated APLR glue for lowrank leaves)"""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle import Oracle, RefOracle
+    from paper_2308_10960_b200 import assemble, problems, tree
+    from cpu_hmatrix import Flat
+    o = RefOracle() if RefOracle.available() else Oracle()
+    s = {"afl": 0, "aflp": 1, "bfl": 2, "dfl": 3}[scheme]
+    c = problems.config(cfg)
+    pts = problems.make_points(c["geometry"], c["n"], 1)
+    ct = tree.build_cluster_tree(pts, c["leaf"])
+    lv = tree.build_block_tree(ct, ct, c["eta"])
+    A = assemble.assemble(pts[ct.i2e], lv, problems.make_kernel(c["kernel"]), c["eps"])
+    dense, W, X = A.dense.cpu().numpy(), A.W.cpu().numpy(), A.X.cpu().numpy()
+    rows = (lv.row1 - lv.row0).astype(np.int64)
+    cols = (lv.col1 - lv.col0).astype(np.int64)
+    didx = np.nonzero(A.kind == 0)[0]
+    dn = rows[didx] * cols[didx]
+    vals = np.concatenate([dense[A.dense_off[l]: A.dense_off[l] + rows[l] * cols[l]] for l in didx])
+    if isinstance(o, RefOracle):
+        de, dm, dsc, dpo, dblob, dpl = o.compress_batch(vals, dn, c["eps"], s, threads=os.cpu_count())
+    else:
+        de, dm, dsc, dpo, dblob = o.compress_batch(vals, dn, c["eps"], s, threads=os.cpu_count())
+    from oracle import Buf
+    bufs, buf0 = [], np.zeros(len(lv), np.int64)
+    di = {int(l): i for i, l in enumerate(didx)}
+    for l in range(len(lv)):
+        buf0[l] = len(bufs)
+        if A.kind[l] == 0:
+            i = di[l]
+            n = (int(dn[i]) * o.bit_width(s, int(de[i]), int(dm[i])) + 7) // 8
+            bufs.append(Buf(s, int(de[i]), int(dm[i]), float(dsc[i]), int(dn[i]),
+                            dblob[int(dpo[i]): int(dpo[i]) + n].tobytes()))
+        else:
+            k = int(A.rank[l])
+            if k:
+                Wl = W[A.w_off[l]: A.w_off[l] + rows[l] * k].reshape(k, rows[l]).T
+                Xl = X[A.x_off[l]: A.x_off[l] + cols[l] * k].reshape(k, cols[l]).T
+                bufs.extend(o.aplr_compress(Wl, Xl, A.sigma[A.sig_off[l]: A.sig_off[l] + k], c["eps"], s))
+    poff = np.zeros(len(bufs), np.int64)
+    parts, off = [], 0
+    for i, b in enumerate(bufs):
+        poff[i] = off
+        parts.append(np.frombuffer(b.payload, np.uint8))
+        off += len(b.payload)
+    sig0 = A.sig_off.copy()
+    sig0[sig0 < 0] = 0
+    flat = Flat(c["n"], c["n"], lv.row0.astype(np.int64), lv.row1.astype(np.int64),
+                lv.col0.astype(np.int64), lv.col1.astype(np.int64), A.kind.astype(np.int64),
+                A.rank.astype(np.int64), buf0, sig0, A.sigma, np.array([b.scheme for b in bufs], np.uint8),
+                np.array([b.e for b in bufs], np.uint8), np.array([b.m for b in bufs], np.uint8),
+                np.array([b.scale for b in bufs]), np.array([b.count for b in bufs], np.int64), poff,
+                np.array([len(b.payload) for b in bufs], np.int64), np.concatenate(parts))
+    flat.nleaves = len(lv)
+    return flat, {}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="3")
+    ap.add_argument("--scheme", default="afl", choices=["afl", "aflp", "bfl", "dfl"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-codec", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()
