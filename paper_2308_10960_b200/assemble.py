@@ -11,6 +11,9 @@ so the truncation sees the same leading singular values a full SVD would.
 """
 from __future__ import annotations
 
+import os
+import sys
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -19,7 +22,7 @@ import torch
 from .problems import PointKernel
 from .tree import BlockLeaves
 
-EXACT_SVD_MAX = 256
+EXACT_SVD_MAX = 64
 
 
 @dataclass
@@ -45,29 +48,54 @@ def rank_from_singular_values(s: torch.Tensor, eps: float) -> torch.Tensor:
     return keep.cumprod(dim=-1).sum(dim=-1)
 
 
+def _cpu_svd(M: torch.Tensor):
+    """batched SVD of small matrices on the host (LAPACK gesdd per matrix, threads
+    over the batch): cuSOLVER runs batched SVDs above 32x32 one matrix at a time"""
+    from concurrent.futures import ThreadPoolExecutor
+    a = M.detach().cpu().numpy()
+    B = a.shape[0]
+    U = np.empty(a.shape[:-1] + (min(a.shape[-2:]),))
+    S = np.empty((B, min(a.shape[-2:])))
+    Vh = np.empty((B, min(a.shape[-2:]), a.shape[-1]))
+    nt = min(32, os.cpu_count() or 1)
+    cuts = np.linspace(0, B, nt + 1).astype(int)
+
+    def work(i):
+        lo, hi = cuts[i], cuts[i + 1]
+        if hi > lo:
+            U[lo:hi], S[lo:hi], Vh[lo:hi] = np.linalg.svd(a[lo:hi], full_matrices=False)
+
+    with ThreadPoolExecutor(nt) as ex:
+        list(ex.map(work, range(nt)))
+    dev = M.device
+    return torch.from_numpy(U).to(dev), torch.from_numpy(S).to(dev), torch.from_numpy(Vh).to(dev)
+
+
 def _svd_batch(A: torch.Tensor, eps: float):
     B, m, n = A.shape
     if min(m, n) <= EXACT_SVD_MAX:
-        U, S, Vh = torch.linalg.svd(A, full_matrices=False)
-        return U, S, Vh
+        return _cpu_svd(A)
     g = torch.Generator(device=A.device)
     g.manual_seed(1234 + m)
     p = min(min(m, n), 64)
     while True:
         omega = torch.randn(B, n, p, dtype=A.dtype, device=A.device, generator=g)
         Q, _ = torch.linalg.qr(A @ omega)
-        Q, _ = torch.linalg.qr(A.transpose(1, 2) @ Q)
+        Q, _ = torch.linalg.qr(A.transpose(1, 2) @ Q)   # one power iteration
         Q, _ = torch.linalg.qr(A @ Q)
-        Bm = Q.transpose(1, 2) @ A
-        Ub, S, Vh = torch.linalg.svd(Bm, full_matrices=False)
+        Bt = A.transpose(1, 2) @ Q                        # (Q^T A)^T, n x p
+        Q2, R2 = torch.linalg.qr(Bt)                      # Q^T A = R2^T Q2^T
+        Ur, S, Vrh = _cpu_svd(R2.transpose(1, 2))         # p x p
         if p >= min(m, n) or bool((S[:, -1] <= 1e-3 * eps * S[:, 0]).all()):
-            return Q @ Ub, S, Vh
+            return Q @ Ur, S, (Q2 @ Vrh.transpose(1, 2)).transpose(1, 2)
         p = min(min(m, n), 2 * p)
 
 
 def assemble(points_internal: np.ndarray, leaves: BlockLeaves, kernel: PointKernel, eps: float,
-             device: str | None = None, batch_bytes: int = 1 << 30) -> Assembled:
+             device: str | None = None, batch_bytes: int | None = None) -> Assembled:
     dev = torch.device(device or ("cuda" if torch.cuda.is_available() else "cpu"))
+    if batch_bytes is None:
+        batch_bytes = (8 << 30) if dev.type == "cuda" else (1 << 30)
     P = torch.as_tensor(np.ascontiguousarray(points_internal, dtype=np.float64), device=dev)
     L = len(leaves)
     kind = np.where(leaves.admissible, 1, 0).astype(np.int64)
@@ -83,35 +111,43 @@ def assemble(points_internal: np.ndarray, leaves: BlockLeaves, kernel: PointKern
     dense = torch.empty(int(sizes.sum()), dtype=torch.float64, device=dev)
     _fill_blocks(P, leaves, didx, kernel, dense, dense_off, batch_bytes)
 
-    # ---- lowrank leaves: SVD per shape group, then laid out in leaf order
+    # ---- lowrank leaves: SVD per shape group; factors packed per chunk with
+    # one masked gather (column-major W and X, leaf by leaf within a chunk)
     lidx = np.nonzero(kind == 1)[0]
-    Wp, Xp, Sp = {}, {}, {}
-    shapes = {}
-    for l in lidx:
-        shapes.setdefault((int(rows[l]), int(cols[l])), []).append(int(l))
-    for (m, n), ids in shapes.items():
-        per = max(1, batch_bytes // (8 * m * n * 3))
-        for c0 in range(0, len(ids), per):
-            chunk = np.array(ids[c0: c0 + per])
-            A = _blocks(P, leaves, chunk, kernel)
-            U, S, Vh = _svd_batch(A, eps)
-            ks = rank_from_singular_values(S, eps).cpu().numpy()
-            for b, l in enumerate(chunk):
-                k = int(ks[b])
-                rank[l] = k
-                Wp[l] = U[b, :, :k].transpose(0, 1).contiguous().reshape(-1)  # column-major W
-                Xp[l] = Vh[b, :k, :].contiguous().reshape(-1)                 # column-major X
-                Sp[l] = S[b, :k].cpu().numpy()
-            del A, U, S, Vh
     w_off = np.full(L, -1, np.int64)
     x_off = np.full(L, -1, np.int64)
     sig_off = np.full(L, -1, np.int64)
     wl, xl, sl = [], [], []
     wo = xo = so = 0
+    shapes = {}
     for l in lidx:
-        w_off[l], x_off[l], sig_off[l] = wo, xo, so
-        wl.append(Wp[l]); xl.append(Xp[l]); sl.append(Sp[l])
-        wo += Wp[l].numel(); xo += Xp[l].numel(); so += Sp[l].size
+        shapes.setdefault((int(rows[l]), int(cols[l])), []).append(int(l))
+    verbose = os.environ.get("HCMX_VERBOSE")
+    for (m, n), ids in shapes.items():
+        t0 = time.time()
+        per = max(1, batch_bytes // (8 * m * n * 3))
+        for c0 in range(0, len(ids), per):
+            chunk = np.array(ids[c0: c0 + per])
+            A = _blocks(P, leaves, chunk, kernel)
+            U, S, Vh = _svd_batch(A, eps)
+            ks_t = rank_from_singular_values(S, eps)
+            keep = torch.arange(S.shape[1], device=S.device)[None, :] < ks_t[:, None]   # (B, p)
+            Wc = U.transpose(1, 2)[keep].reshape(-1)     # rows of U^T = columns of W
+            Xc = Vh[keep].reshape(-1)
+            Sc = S[keep].cpu().numpy()
+            ks = ks_t.cpu().numpy().astype(np.int64)
+            rank[chunk] = ks
+            cw = np.concatenate([[0], np.cumsum(ks * m)[:-1]])
+            cx = np.concatenate([[0], np.cumsum(ks * n)[:-1]])
+            cs = np.concatenate([[0], np.cumsum(ks)[:-1]])
+            w_off[chunk] = wo + cw
+            x_off[chunk] = xo + cx
+            sig_off[chunk] = so + cs
+            wl.append(Wc); xl.append(Xc); sl.append(Sc)
+            wo += Wc.numel(); xo += Xc.numel(); so += Sc.size
+            del A, U, S, Vh
+        if verbose:
+            sys.stderr.write(f"[assemble] {len(ids)} blocks {m}x{n}: {time.time() - t0:.2f}s\n")
     W = torch.cat(wl) if wl else torch.zeros(0, dtype=torch.float64, device=dev)
     X = torch.cat(xl) if xl else torch.zeros(0, dtype=torch.float64, device=dev)
     sigma = np.concatenate(sl) if sl else np.zeros(0)

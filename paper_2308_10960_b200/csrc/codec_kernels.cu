@@ -73,7 +73,7 @@ void stream_sync(void* stream) {
 
 namespace {
 
-constexpr unsigned kGroupsPerJob = 512;  // 16384 values per warp job
+constexpr unsigned kGroupsPerJob = 64;  // 2048 values per warp job
 constexpr int kWarpsPerBlock = 8;
 
 struct Job {
@@ -124,15 +124,21 @@ __global__ void k_analyze(const double* __restrict__ values, const uint64_t* __r
         const double* v = values + voff[jb.buf];
         uint64_t mn = 0x7FF0000000000000ull, mx = 0;
         unsigned nz = 0, nf = 0;
-        for (uint64_t i = i0 + lane; i < i1; i += 32) {
-            const double x = __ldcs(v + i);
-            const double a = fabs(x);
-            if (a != 0.0) nz = 1;
-            if (!isfinite(x)) nf = 1;
-            if (a != 0.0 && !isnan(a)) {
-                const uint64_t b = dbits(a);  // nonnegative doubles order like their bits
-                mn = b < mn ? b : mn;
-                mx = b > mx ? b : mx;
+        for (uint64_t i = i0 + lane; i < i1; i += 128) {
+            double xs[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) xs[u] = i + 32 * u < i1 ? __ldcs(v + i + 32 * u) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double x = xs[u];
+                const double a = fabs(x);
+                if (a != 0.0) nz = 1;
+                if (!isfinite(x)) nf = 1;
+                if (a != 0.0 && !isnan(a)) {
+                    const uint64_t b = dbits(a);  // nonnegative doubles order like their bits
+                    mn = b < mn ? b : mn;
+                    mx = b > mx ? b : mx;
+                }
             }
         }
 #pragma unroll
@@ -182,14 +188,16 @@ __device__ __forceinline__ uint64_t encode_value(double v, unsigned e, unsigned 
     return field;
 }
 
+// Packing without atomics: lane j encodes value 32g + j into a 64-bit field F_j;
+// lane K then assembles output word K of the group (bits [32K, 32K+32)) from
+// the <= ceil(32/w)+1 fields that overlap it, fetched with warp shuffles.  The
+// w words of a group are stored by w lanes at once (coalesced).
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_pack(const double* __restrict__ values, const uint64_t* __restrict__ voff,
        const uint64_t* __restrict__ count, const hcmx_descriptor* __restrict__ desc,
        const uint64_t* __restrict__ poff, const Job* __restrict__ jobs, uint64_t njobs,
        uint8_t* __restrict__ payload, int* __restrict__ err) {
-    __shared__ uint32_t sw[kWarpsPerBlock][64];
-    const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    uint32_t* words = sw[wib];
+    const unsigned lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
     for (uint64_t j = wid; j < njobs; j += nw) {
@@ -203,31 +211,40 @@ k_pack(const double* __restrict__ values, const uint64_t* __restrict__ voff,
         const uint64_t n = count[jb.buf];
         const double* v = values + voff[jb.buf];
         uint32_t* out = reinterpret_cast<uint32_t*>(payload + poff[jb.buf]);
-        const unsigned bit = lane * w, q = bit >> 5, sh = bit & 31;
+        const unsigned T = (32 + w - 1) / w + 1;  // fields overlapping one output word
+        // output words K = lane and K = lane + 32: first overlapping field and its bit shift
+        const unsigned i0a = (32 * lane) / w, i0b = (32 * (lane + 32)) / w;
+        int nf_bad = 0;
         for (uint32_t g = jb.g0; g < jb.g0 + jb.ng; ++g) {
             const uint64_t idx = (uint64_t)g * 32 + lane;
-            words[lane] = 0;
-            words[lane + 32] = 0;
-            __syncwarp();
+            uint64_t f = 0;
             if (idx < n) {
                 const double x = __ldcs(v + idx);
-                if (!isfinite(x)) {
-                    *err = 1;
-                } else {
-                    const uint64_t f = encode_value(x, e, m, inv_scale, max_offset, round_add, mant_mask);
-                    const uint64_t lo = f << sh;
-                    if ((uint32_t)lo) atomicOr(&words[q], (uint32_t)lo);
-                    if (lo >> 32) atomicOr(&words[q + 1], (uint32_t)(lo >> 32));
-                    if (sh && (f >> (64 - sh))) atomicOr(&words[q + 2], (uint32_t)(f >> (64 - sh)));
-                }
+                if (!isfinite(x)) nf_bad = 1;
+                else f = encode_value(x, e, m, inv_scale, max_offset, round_add, mant_mask);
             }
-            __syncwarp();
+            const uint32_t flo = static_cast<uint32_t>(f), fhi = static_cast<uint32_t>(f >> 32);
             const uint64_t nvalid = umin64(32, n - (uint64_t)g * 32);
             const unsigned nwords = (unsigned)((nvalid * w + 31) / 32);
             uint32_t* o = out + (uint64_t)g * w;
-            for (unsigned t = lane; t < nwords; t += 32) __stcs(o + t, words[t]);
-            __syncwarp();
+            for (unsigned half = 0; half < (w > 32 ? 2u : 1u); ++half) {
+                const unsigned K = lane + 32 * half;
+                const unsigned i0 = half ? i0b : i0a;
+                uint32_t word = 0;
+                for (unsigned t = 0; t < T; ++t) {
+                    const unsigned i = i0 + t;
+                    const uint32_t lo = __shfl_sync(0xffffffffu, flo, i & 31u);
+                    const uint32_t hi = __shfl_sync(0xffffffffu, fhi, i & 31u);
+                    const int sft = static_cast<int>(i * w) - static_cast<int>(32 * K);  // field bit 0 vs word bit 0
+                    if (i < 32 && sft < 32) {
+                        const uint64_t F = (static_cast<uint64_t>(hi) << 32) | lo;
+                        word |= sft >= 0 ? static_cast<uint32_t>(F << sft) : static_cast<uint32_t>(F >> (-sft));
+                    }
+                }
+                if (K < nwords) __stcs(o + K, word);
+            }
         }
+        if (__any_sync(0xffffffffu, nf_bad) && lane == 0) *err = 1;
     }
 }
 
@@ -246,6 +263,9 @@ __device__ __forceinline__ double decode_field(uint64_t field, unsigned e, unsig
     return sign ? -v : v;
 }
 
+// Unpacking: the w words of a group are loaded by w lanes (coalesced, four
+// groups in flight per warp); lane j pulls the 2-3 words holding field j with
+// shuffles and decodes it; the 32 doubles are stored coalesced.
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_unpack(const uint8_t* __restrict__ payload, const uint64_t* __restrict__ poff,
          const uint64_t* __restrict__ count, const hcmx_descriptor* __restrict__ desc,
@@ -263,15 +283,43 @@ k_unpack(const uint8_t* __restrict__ payload, const uint64_t* __restrict__ poff,
         double* o = out + voff[jb.buf];
         const unsigned bit = lane * w, q = bit >> 5, sh = bit & 31;
         const uint64_t wmask = (w == 64) ? ~0ull : ((1ull << w) - 1);
-        for (uint32_t g = jb.g0; g < jb.g0 + jb.ng; ++g) {
-            const uint64_t idx = (uint64_t)g * 32 + lane;
-            if (idx < n) {
-                const uint32_t* gp = p + (uint64_t)g * w + q;
-                const uint32_t lo = __ldcs(gp);
-                const uint32_t hi = (sh + w > 32) ? __ldcs(gp + 1) : 0u;
-                uint64_t win = ((uint64_t)hi << 32 | lo) >> sh;
-                if (sh + w > 64) win |= (uint64_t)__ldcs(gp + 2) << (64 - sh);
-                __stcs(o + idx, decode_field(win & wmask, e, m, d.scale));
+        const uint32_t gend = jb.g0 + jb.ng;
+        for (uint32_t g = jb.g0; g < gend; g += 4) {
+            uint32_t wa[4], wb[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t gi = g + i;
+                wa[i] = wb[i] = 0;
+                if (gi < gend) {
+                    const uint64_t nvalid = umin64(32, n - (uint64_t)gi * 32);
+                    const unsigned nwords = (unsigned)((nvalid * w + 31) / 32);
+                    if (lane < nwords) wa[i] = __ldcs(p + (uint64_t)gi * w + lane);
+                    if (lane + 32 < nwords) wb[i] = __ldcs(p + (uint64_t)gi * w + 32 + lane);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t gi = g + i;
+                if (gi >= gend) break;
+                uint32_t w0, w1, w2 = 0;
+                if (w <= 32) {
+                    w0 = __shfl_sync(0xffffffffu, wa[i], q);
+                    w1 = __shfl_sync(0xffffffffu, wa[i], (q + 1) & 31u);
+                } else {
+                    const uint32_t a0 = __shfl_sync(0xffffffffu, wa[i], q & 31u);
+                    const uint32_t b0 = __shfl_sync(0xffffffffu, wb[i], q & 31u);
+                    const uint32_t a1 = __shfl_sync(0xffffffffu, wa[i], (q + 1) & 31u);
+                    const uint32_t b1 = __shfl_sync(0xffffffffu, wb[i], (q + 1) & 31u);
+                    const uint32_t a2 = __shfl_sync(0xffffffffu, wa[i], (q + 2) & 31u);
+                    const uint32_t b2 = __shfl_sync(0xffffffffu, wb[i], (q + 2) & 31u);
+                    w0 = q < 32 ? a0 : b0;
+                    w1 = q + 1 < 32 ? a1 : b1;
+                    w2 = q + 2 < 32 ? a2 : b2;
+                }
+                uint64_t win = ((uint64_t)w1 << 32 | w0) >> sh;
+                if (sh + w > 64) win |= (uint64_t)w2 << (64 - sh);
+                const uint64_t idx = (uint64_t)gi * 32 + lane;
+                if (idx < n) __stcs(o + idx, decode_field(win & wmask, e, m, d.scale));
             }
         }
     }

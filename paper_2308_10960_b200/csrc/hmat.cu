@@ -3,29 +3,33 @@
 //
 // Layout (built once on the host by hcmx_gpu_hmat_create):
 //   The packed codec streams of every leaf are re-tiled, field-for-field and
-//   bit-identical, into one HBM arena of 16-byte aligned "stages" (<= 32 KB):
+//   bit-identical, into one HBM arena of 16-byte aligned "stages" (<= 24 KB).
 //
 //   phase A (lowrank X^T x): item = (APLR leaf, <= 256 consecutive columns of
 //     the block, <= 16 rank columns); its data is, for each rank column, the
 //     fields of that X column over the column chunk, word aligned.  One warp
-//     decodes an item with the 256 x values in registers (8 per lane), reduces
+//     decodes an item with the x values in registers (8 per lane), reduces
 //     per rank column with shuffles, and either writes t_i directly (one chunk)
 //     or a partial that the last-arriving warp sums in fixed chunk order.
-//   phase B (row-stationary): one CTA owns one row block (<= 64 rows, a row
-//     leaf cluster) and streams the "stripe" of everything that writes those
-//     rows: dense leaves (column groups of 16 columns, each column's |rows|
-//     fields) and the W slices of every APLR leaf covering the block.  Lane l
-//     owns rows l and l+32; y is written once per row, no atomics.
+//   phase B (row-stationary): one CTA owns one block of 128 rows and streams
+//     the "stripe" of everything that writes those rows: dense leaves (column
+//     groups of 16) and the W slices of every APLR leaf covering the block.
+//     Lane l owns rows 32 g + l (4 accumulators); y is written once per row.
 //
-//   Stages are moved HBM -> shared memory with cp.async.bulk (the TMA bulk
-//   engine) into a 3-deep ring guarded by mbarriers, so the SM only spends
-//   issue slots on the decode itself: two LDS + a funnel shift per field, a
-//   few integer ops to rebuild the FP64 pattern, one DADD and one DFMA.
+//   Each CTA = 16 consumer warps + 1 producer warp.  The producer moves stages
+//   HBM -> shared memory with cp.async.bulk (the TMA bulk engine, L2
+//   evict_first) into a 4-deep ring; full/empty mbarriers replace CTA-wide
+//   barriers.  Items of a stage are assigned to warps by LPT on their field
+//   counts.  Per item, one round of independent loads fetches the column
+//   widths and coefficients (x, or the phase-A results) -- nothing in the
+//   per-column loop waits on global memory.  A field costs two LDS, a funnel
+//   shift, ~4 integer ops to rebuild the FP64 pattern (32-bit fast paths for
+//   w <= 32), one DADD and one DFMA.
 //
 // Numerics: decoded values are bit-identical to codec::decompress_into; the
 // multiply by the buffer scale is folded into the coefficients (dense: alpha *
-// scale per item, lowrank: alpha * sigma_i * scale_X_i * scale_W_i), so the sum
-// differs from the oracle only by FP64 reassociation (||dy||/||y|| ~ 1e-15).
+// scale * x_j, lowrank: alpha * sigma_i * scale_X_i * scale_W_i * t_i), so the
+// sum differs from the oracle only by FP64 reassociation (||dy||/||y|| ~ 1e-15).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -38,47 +42,78 @@
 namespace hcmx_gpu {
 namespace {
 
-constexpr int kNW = 8;                // warps per CTA
-constexpr int kStageBytes = 32768;    // bytes per stage buffer
-constexpr int kNStage = 3;            // ring depth
-constexpr int kSlack = 16;            // decode reads up to 2 words past a segment
+constexpr int kNW = 16;                   // consumer warps per CTA
+constexpr int kThreads = (kNW + 1) * 32;  // + one producer warp (bulk copies)
+constexpr int kStageBytes = 24576;        // packed data per stage
+constexpr int kMaxItems = 32;             // items per stage (one per producer lane)
+constexpr int kItemBytes = 48;            // descriptor size (A and B)
+constexpr int kCoefBytes = 8192;          // staged coefficients + column params per stage
+constexpr int kNStage = 3;                // ring depth
+constexpr int kSlack = 16;                // decode reads up to 2 words past a segment
+constexpr int kOffDesc = kStageBytes + kSlack;
+constexpr int kOffWb = kOffDesc + kMaxItems * kItemBytes;
+constexpr int kOffCoef = kOffWb + 48;
+constexpr int kSlotBytes = kOffCoef + kCoefBytes;
+constexpr int kR = 128;               // rows per phase-B CTA
+constexpr int kG = kR / 32;           // row groups (accumulators) per lane
 constexpr int kAChunk = 256;          // X fields per A item (8 per lane)
 constexpr int kAGroup = 16;           // rank columns per A item
 constexpr int kBDenseGroup = 16;      // dense columns per B item
 constexpr int kBLRGroup = 32;         // rank columns per B item
-constexpr int kRowBlock = 64;         // rows per phase-B CTA (2 per lane)
 constexpr int kAStagesPerStripe = 8;  // phase-A stages per CTA
+constexpr size_t kRingBytes = static_cast<size_t>(kNStage) * kSlotBytes;
+constexpr size_t kSmemBytes = kRingBytes + 2 * kNStage * sizeof(uint64_t);
+static_assert(kOffDesc % 16 == 0 && kOffCoef % 16 == 0 && kSlotBytes % 16 == 0, "slot alignment");
+static_assert(kNW * kR * sizeof(double) <= kRingBytes, "reduction reuses the ring");
 
 struct Stage {
-    uint64_t byte_off;
+    uint64_t byte_off;   // packed data in the arena
     uint32_t bytes;
-    uint32_t item0;
+    uint32_t item0;      // first descriptor (A or B array); grouped by warp
     uint32_t nitems;
-    uint32_t pad;
+    uint32_t coef_bytes; // bytes of staged coefficients / params (exact sum of the copies)
+    uint64_t pad;
 };
-static_assert(sizeof(Stage) == 24, "Stage layout");
+static_assert(sizeof(Stage) == 32, "Stage layout");
+
+// Column layout parameters, precomputed on the host (16 bytes, one LDS.128)
+struct ColPar {
+    uint32_t mask_em;    // (1 << (e + m)) - 1, all ones for e + m >= 32
+    uint32_t mul_rsh;    // mode 0: 1 << (20 - m); mode 1: m - 20
+    uint32_t packed;     // w | m << 8 | e << 16 | mode << 24
+    uint32_t sgn_sh;     // 31 - e - m (mode 0/1)
+};
 
 struct BItem {
-    uint32_t word_off;  // from the stage start
-    uint16_t nseg;      // columns in this item
-    uint8_t kind;       // 0 dense, 1 lowrank
-    uint8_t e;          // exponent bits (lowrank: factor-wide)
-    uint32_t a;         // dense: x index of first column; lowrank: global W column id
-    uint32_t b;         // dense: dense-leaf id
+    uint32_t word_off;   // packed data, from the stage start
+    uint8_t nseg;        // columns in this item
+    uint8_t kind;        // 0 dense, 1 lowrank
+    uint8_t ra;          // first row of the item inside the row block
+    uint8_t nr;          // rows (fields per column segment)
+    uint32_t coef_off;   // staged coefficients in the slot's coef area (bytes)
+    uint32_t src;        // dense: x index of first column; lowrank: global W column id (even)
+    ColPar par;          // dense: the leaf's layout
+    uint32_t shift;      // dense: x slice starts at x[src & ~1], first value at + shift
+    uint32_t pad;
+    double scale;        // dense: buffer scale
 };
-static_assert(sizeof(BItem) == 16, "BItem layout");
+static_assert(sizeof(BItem) == kItemBytes, "BItem layout");
 
 struct AItem {
     uint32_t word_off;
-    uint16_t nseg;      // rank columns
-    uint16_t nf;        // fields per column (<= kAChunk)
-    uint32_t xcol;      // global X column id of the first rank column
-    uint32_t xidx;      // x index of field 0
-    uint32_t leaf;      // lowrank-leaf id
-    uint16_t chunk;     // column-chunk index within the leaf
-    uint16_t icol0;     // first rank column within the leaf
+    uint8_t nseg;        // rank columns
+    uint8_t pad0;
+    uint16_t nf;         // fields per column (<= kAChunk)
+    uint32_t coef_off;   // staged x slice then X column params
+    uint32_t xidx;       // x index of field 0
+    uint32_t xcol;       // global X column id of the first rank column
+    uint32_t leaf;       // lowrank-leaf id
+    uint16_t chunk;      // column-chunk index within the leaf
+    uint16_t icol0;      // first rank column within the leaf
+    uint32_t shift;      // x slice starts at x[xidx & ~1], first value at + shift
+    uint64_t pad1, pad2;
 };
-static_assert(sizeof(AItem) == 24, "AItem layout");
+static_assert(sizeof(AItem) == kItemBytes, "AItem layout");
 
 struct LeafA {
     uint32_t colbase;   // global column id of rank column 0
@@ -86,34 +121,27 @@ struct LeafA {
     uint32_t pbase;     // partials base (nchunks > 1)
     uint32_t nitems;    // A items of this leaf
     uint32_t nchunks;
-    uint32_t e;         // X exponent bits
+    uint32_t pad;
 };
-
-struct DenseInfo {
-    double scale;
-    uint8_t w, m, e, pad[5];
-};
-static_assert(sizeof(DenseInfo) == 16, "DenseInfo layout");
 
 struct Params {
     const uint8_t* arena;
     const Stage* stages;
+    const uint16_t* stage_wb;   // [nstages * 24] per-warp item ranges (kNW + 1 used)
     const BItem* bitems;
     const AItem* aitems;
     const uint32_t* stripe_a;   // [nstripe_a + 1] stage ranges
     const uint32_t* stripe_b;   // [nblocks + 1]
-    const uint32_t* row_first;  // [nblocks]
-    const uint32_t* row_count;
     const LeafA* leafa;
-    const DenseInfo* dense;
-    const uint16_t* colw_wm;    // (w | m << 8) per W column
-    const uint16_t* colx_wm;
+    const ColPar* colw_par;
+    const ColPar* colx_par;
     const double* coef;         // sigma_i * scale_X_i * scale_W_i
     double* c;                  // alpha * coef * (X^T x)_i, written by phase A
     double* partial;
     unsigned* counter;
-    const double* x;
+    const double* x;            // padded internal copy (16-byte aligned, readable + 16 B)
     double* y;
+    uint32_t row_begin, row_end;
     double alpha, beta;
 };
 
@@ -139,6 +167,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ uint64_t evict_first_policy() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -154,28 +188,53 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         : "memory");
 }
 
-// ------------------------------------------------------------- decode ----
-// Field at bit offset (q * 32 + sh) of the word stream wp, width w, layout
-// [mant m][offset e][sign] (codec.cpp:118-137).  Returns (1.mant * 2^offset) - 1
-// (exact: the codec's value divided by scale, codec.cpp:161-169) and the sign.
-__device__ __forceinline__ double decode_a(const uint32_t* wp, unsigned q, unsigned sh, unsigned w,
-                                           unsigned e, unsigned m, uint64_t& sgn) {
-    const uint32_t lo = wp[q], hi = wp[q + 1];
-    uint64_t win = ((static_cast<uint64_t>(hi) << 32) | lo) >> sh;
-    if (w > 32 && sh + w > 64) win |= static_cast<uint64_t>(wp[q + 2]) << (64 - sh);
-    const unsigned em = e + m;
-    sgn = (win >> em) & 1ull;
-    const uint64_t fem = win & ((1ull << em) - 1);
-    uint64_t bits = (fem << (52 - m)) + (1023ull << 52);
-    if (e == 11) {  // min(offset + 1023, 2046): only an 11-bit offset can exceed it
-        if ((fem >> m) >= 1024) bits = (2046ull << 52) | ((fem << (52 - m)) & ((1ull << 52) - 1));
-    }
-    return __longlong_as_double(static_cast<long long>(bits)) - 1.0;
+
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__device__ __forceinline__ double signed_coef(double c, uint64_t sgn) {
-    return __longlong_as_double(__double_as_longlong(c) ^ static_cast<long long>(sgn << 63));
+
+
+// ------------------------------------------------------------- decode ----
+// A field of width w sits at bit sh of the word pair sp[0..1] (sp[2] too when
+// w > 32).  Layout [mant m][offset e][sign] (codec.cpp:118-137).  Each mode
+// returns (1.mant * 2^offset) - 1 -- exactly the codec's value / scale
+// (codec.cpp:161-169) -- and xors the sign into the coefficient's high word.
+//   mode 0: w <= 32, m <= 20, e < 11   (the whole double lives in the high word)
+//   mode 1: w <= 32, m  > 20, e < 11
+//   mode 2: anything else (64-bit window, min(offset + 1023, 2046) clamp)
+template <int MODE>
+__device__ __forceinline__ double dec(const uint32_t* sp, const ColPar& c, unsigned sh, double coef, double& cs) {
+    if (MODE == 0) {
+        const uint32_t t = __funnelshift_r(sp[0], sp[1], sh);
+        const uint32_t sgn = (t << c.sgn_sh) & 0x80000000u;
+        const uint32_t hi = (t & c.mask_em) * c.mul_rsh + (1023u << 20);
+        cs = __hiloint2double(__double2hiint(coef) ^ sgn, __double2loint(coef));
+        return __hiloint2double(hi, 0) - 1.0;
+    } else if (MODE == 1) {
+        const uint32_t t = __funnelshift_r(sp[0], sp[1], sh);
+        const uint32_t sgn = (t << c.sgn_sh) & 0x80000000u;
+        const uint32_t hi = ((t & c.mask_em) >> c.mul_rsh) + (1023u << 20);
+        const uint32_t lo = t << (32u - c.mul_rsh);
+        cs = __hiloint2double(__double2hiint(coef) ^ sgn, __double2loint(coef));
+        return __hiloint2double(hi, lo) - 1.0;
+    } else {
+        const unsigned w = c.packed & 0xffu, m = (c.packed >> 8) & 0xffu, e = (c.packed >> 16) & 0xffu;
+        uint64_t win = ((static_cast<uint64_t>(sp[1]) << 32) | sp[0]) >> sh;
+        if (w > 32 && sh + w > 64) win |= static_cast<uint64_t>(sp[2]) << (64 - sh);
+        const unsigned em = e + m;
+        const uint64_t sgn = (win >> em) & 1ull;
+        const uint64_t fem = win & ((1ull << em) - 1);
+        uint64_t bits = (fem << (52 - m)) + (1023ull << 52);
+        if ((fem >> m) >= 1024) bits = (2046ull << 52) | ((fem << (52 - m)) & ((1ull << 52) - 1));
+        cs = __longlong_as_double(__double_as_longlong(coef) ^ static_cast<long long>(sgn << 63));
+        return __longlong_as_double(static_cast<long long>(bits)) - 1.0;
+    }
 }
+
+__device__ __forceinline__ unsigned par_w(const ColPar& c) { return c.packed & 0xffu; }
+__device__ __forceinline__ unsigned par_mode(const ColPar& c) { return c.packed >> 24; }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -183,172 +242,393 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// ring of kNStage stage buffers fed by cp.async.bulk
-struct Ring {
-    uint8_t* buf;
-    uint64_t* bars;
-    __device__ __forceinline__ uint32_t* stage_words(int slot) const {
-        return reinterpret_cast<uint32_t*>(buf + slot * (kStageBytes + kSlack));
-    }
+__device__ __forceinline__ unsigned round16u(unsigned x) { return (x + 15u) & ~15u; }
+
+// ---------------------------------------------------- producer warp ----
+// One warp fills the ring: the stage's packed data, its item descriptors and
+// per-warp ranges, and -- per item -- the coefficient slice (x or the phase-A
+// results) plus the column parameters, all as cp.async.bulk copies completing
+// on the slot's full barrier.  Consumers never wait on global memory.
+// staged copies of one item (sizes must match the host's coef_bytes):
+// copy 0 = coefficient slice (x, or the phase-A results C), copy 1 = column params
+struct ProdItem {
+    uint32_t coef_off;
+    uint32_t sizes;   // n0 | n1 << 16 (bytes)
+    uint32_t i0;      // element index of copy 0 in x (or C when lowrank)
+    uint32_t i1;      // column id of copy 1; bit 31 set: copy 0 reads C
 };
 
-__device__ __forceinline__ void issue_stage(const Params& p, const Ring& r, uint32_t s, int slot,
-                                            uint64_t policy) {
-    const Stage st = p.stages[s];
-    mbar_expect_tx(&r.bars[slot], st.bytes);
-    bulk_g2s(r.buf + slot * (kStageBytes + kSlack), p.arena + st.byte_off, st.bytes, &r.bars[slot], policy);
+template <bool PHASE_A>
+__device__ __forceinline__ ProdItem prod_item(const Params& p, uint32_t idx) {
+    ProdItem r{};
+    if (PHASE_A) {
+        const AItem a = p.aitems[idx];
+        r.coef_off = a.coef_off;
+        r.sizes = round16u((a.nf + a.shift) * 8u) | ((a.nseg * 16u) << 16);
+        r.i0 = a.xidx & ~1u;
+        r.i1 = a.xcol;
+    } else {
+        const BItem b = p.bitems[idx];
+        r.coef_off = b.coef_off;
+        if (b.kind == 0) {
+            r.sizes = round16u((b.nseg + b.shift) * 8u);
+            r.i0 = b.src & ~1u;
+        } else {
+            r.sizes = round16u(b.nseg * 8u) | ((b.nseg * 16u) << 16);
+            r.i0 = b.src;
+            r.i1 = b.src | 0x80000000u;
+        }
+    }
+    return r;
 }
 
-// ------------------------------------------------------------ phase A ----
-__device__ __forceinline__ void a_item(const Params& p, const AItem& it, const uint32_t* sw,
-                                       unsigned lane) {
-    const LeafA L = p.leafa[it.leaf];
-    const unsigned nf = it.nf;
-    double xv[kAChunk / 32];
-#pragma unroll
-    for (int u = 0; u < kAChunk / 32; ++u) {
-        const unsigned f = lane + 32u * u;
-        xv[u] = f < nf ? __ldg(p.x + it.xidx + f) : 0.0;
-    }
-    const uint32_t* wp = sw + it.word_off;
-    for (unsigned c = 0; c < it.nseg; ++c) {
-        const uint32_t j = it.xcol + c;
-        const uint16_t wm = __ldg(p.colx_wm + j);
-        const unsigned w = wm & 0xffu, m = wm >> 8;
-        const unsigned bit = lane * w, q = bit >> 5, sh = bit & 31u;
-        double acc = 0.0;
-#pragma unroll
-        for (int u = 0; u < kAChunk / 32; ++u) {
-            if (lane + 32u * u < nf) {
-                uint64_t sg;
-                const double a = decode_a(wp, q + u * w, sh, w, L.e, m, sg);
-                acc = fma(a, signed_coef(xv[u], sg), acc);
-            }
-        }
-        acc = warp_sum(acc);
-        if (lane == 0) {
-            if (L.nchunks == 1)
-                p.c[j] = p.alpha * __ldg(p.coef + j) * acc;
-            else
-                p.partial[L.pbase + static_cast<uint32_t>(it.chunk) * L.k + it.icol0 + c] = acc;
-        }
-        wp += (nf * w + 31) >> 5;
-    }
-    if (L.nchunks > 1) {
-        __threadfence();
-        __syncwarp();
-        unsigned last = 0;
-        if (lane == 0) last = atomicAdd(p.counter + it.leaf, 1u) == L.nitems - 1;
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {  // every chunk is in: sum in fixed chunk order (deterministic)
-            __threadfence();
-            for (unsigned i = lane; i < L.k; i += 32) {
-                double s = 0.0;
-                for (unsigned ch = 0; ch < L.nchunks; ++ch) s += __ldcg(p.partial + L.pbase + ch * L.k + i);
-                p.c[L.colbase + i] = p.alpha * __ldg(p.coef + L.colbase + i) * s;
-            }
-            if (lane == 0) p.counter[it.leaf] = 0u;  // re-armed for the next product
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kNW * 32) k_phase_a(Params p) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    Ring r{smem, reinterpret_cast<uint64_t*>(smem + kNStage * (kStageBytes + kSlack))};
-    const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint32_t s0 = p.stripe_a[blockIdx.x], s1 = p.stripe_a[blockIdx.x + 1];
-    uint64_t policy = 0;
-    if (tid == 0) {
-        policy = evict_first_policy();
-        for (int b = 0; b < kNStage; ++b) mbar_init(&r.bars[b], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-    if (tid == 0)
-        for (int b = 0; b < kNStage && s0 + b < s1; ++b) issue_stage(p, r, s0 + b, b, policy);
+// One warp fills the ring: the stage's packed data, its item descriptors and
+// per-warp ranges, and -- per item, one item per lane -- the coefficient slice
+// (x or the phase-A results) plus the column parameters, all as cp.async.bulk
+// copies completing on the slot's full barrier.  Consumers never wait on global
+// memory.  The metadata of stage s+1 is fetched while waiting for a free slot.
+template <bool PHASE_A>
+__device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_t* full, uint64_t* empty,
+                                         uint32_t s0, uint32_t s1, unsigned lane) {
+    if (s0 >= s1) return;
+    const uint64_t policy = evict_first_policy();
+    Stage st = p.stages[s0];
+    ProdItem pi{};
+    if (lane < st.nitems) pi = prod_item<PHASE_A>(p, st.item0 + lane);
     for (uint32_t s = s0; s < s1; ++s) {
         const uint32_t it = s - s0;
         const int slot = static_cast<int>(it % kNStage);
-        mbar_wait(&r.bars[slot], (it / kNStage) & 1u);
-        const Stage st = p.stages[s];
-        const uint32_t* sw = r.stage_words(slot);
-        for (uint32_t i = warp; i < st.nitems; i += kNW) a_item(p, p.aitems[st.item0 + i], sw, lane);
-        __syncthreads();
-        if (tid == 0 && s + kNStage < s1) issue_stage(p, r, s + kNStage, slot, policy);
+        Stage nst{};
+        ProdItem npi{};
+        if (s + 1 < s1) {
+            nst = p.stages[s + 1];
+            if (lane < nst.nitems) npi = prod_item<PHASE_A>(p, nst.item0 + lane);
+        }
+        if (it >= kNStage) mbar_wait(&empty[slot], ((it / kNStage) - 1) & 1u);
+        uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
+        if (lane == 0) {
+            mbar_expect_tx(&full[slot], st.bytes + st.nitems * kItemBytes + 48 + st.coef_bytes);
+            bulk_g2s(base, p.arena + st.byte_off, st.bytes, &full[slot], policy);
+            const void* d = PHASE_A ? static_cast<const void*>(p.aitems + st.item0)
+                                    : static_cast<const void*>(p.bitems + st.item0);
+            bulk_g2s_plain(base + kOffDesc, d, st.nitems * kItemBytes, &full[slot]);
+            bulk_g2s_plain(base + kOffWb, p.stage_wb + static_cast<size_t>(s) * 24, 48, &full[slot]);
+        }
+        __syncwarp();
+        if (lane < st.nitems) {
+            uint8_t* cdst = base + kOffCoef + pi.coef_off;
+            const unsigned n0 = pi.sizes & 0xffffu, n1 = pi.sizes >> 16;
+            const bool from_c = !PHASE_A && (pi.i1 & 0x80000000u);
+            bulk_g2s_plain(cdst, (from_c ? p.c : p.x) + pi.i0, n0, &full[slot]);
+            if (n1) {
+                const ColPar* par = PHASE_A ? p.colx_par : p.colw_par;
+                bulk_g2s_plain(cdst + n0, par + (pi.i1 & 0x7fffffffu), n1, &full[slot]);
+            }
+        }
+        st = nst;
+        pi = npi;
+    }
+}
+
+// ------------------------------------------------------------ phase A ----
+// U = fields per lane (nf = 32 U) known at compile time: no predication
+template <int MODE, int U>
+__device__ __forceinline__ double a_column_full(const uint32_t* seg, const ColPar& c, unsigned lane,
+                                                const double (&xv)[kAChunk / 32]) {
+    const unsigned w = par_w(c);
+    const unsigned bit = lane * w;
+    const uint32_t* sp = seg + (bit >> 5);
+    const unsigned sh = bit & 31u;
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        double cs;
+        const double d = dec<MODE>(sp + u * w, c, sh, xv[u], cs);
+        if (u & 1) acc1 = fma(d, cs, acc1);
+        else acc0 = fma(d, cs, acc0);
+    }
+    return acc0 + acc1;
+}
+
+template <int MODE>
+__device__ __forceinline__ double a_column(const uint32_t* seg, const ColPar& c, unsigned lane, unsigned nf,
+                                           const double (&xv)[kAChunk / 32]) {
+    const unsigned w = par_w(c);
+    const unsigned bit = lane * w;
+    const uint32_t* sp = seg + (bit >> 5);
+    const unsigned sh = bit & 31u;
+    double acc = 0.0;
+    const unsigned U = (nf + 31) >> 5;
+#pragma unroll
+    for (int u = 0; u < kAChunk / 32; ++u) {
+        if (static_cast<unsigned>(u) < U) {
+            if (lane + 32u * u < nf) {
+                double cs;
+                const double d = dec<MODE>(sp + u * w, c, sh, xv[u], cs);
+                acc = fma(d, cs, acc);
+            }
+        }
+    }
+    return acc;
+}
+
+template <int MODE>
+__device__ __forceinline__ double a_dispatch_u(const uint32_t* seg, const ColPar& c, unsigned lane, unsigned nf,
+                                               const double (&xv)[kAChunk / 32]) {
+    switch (nf) {
+        case 256: return a_column_full<MODE, 8>(seg, c, lane, xv);
+        case 128: return a_column_full<MODE, 4>(seg, c, lane, xv);
+        case 64: return a_column_full<MODE, 2>(seg, c, lane, xv);
+        default: return a_column<MODE>(seg, c, lane, nf, xv);
+    }
+}
+
+__device__ __forceinline__ void a_item(const Params& p, const AItem& it, const uint8_t* slot, unsigned lane) {
+    const unsigned nseg = it.nseg, nf = it.nf;
+    const double* xs = reinterpret_cast<const double*>(slot + kOffCoef + it.coef_off) + it.shift;
+    const ColPar* par = reinterpret_cast<const ColPar*>(slot + kOffCoef + it.coef_off + round16u((nf + it.shift) * 8u));
+    double xv[kAChunk / 32];
+    const unsigned U = (nf + 31) >> 5;
+#pragma unroll
+    for (int u = 0; u < kAChunk / 32; ++u) {
+        const unsigned f = lane + 32u * u;
+        xv[u] = (static_cast<unsigned>(u) < U && f < nf) ? xs[f] : 0.0;
+    }
+    const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
+    double res = 0.0;
+    for (unsigned c = 0; c < nseg; ++c) {
+        const ColPar col = par[c];
+        double acc;
+        switch (par_mode(col)) {
+            case 0: acc = a_dispatch_u<0>(seg, col, lane, nf, xv); break;
+            case 1: acc = a_dispatch_u<1>(seg, col, lane, nf, xv); break;
+            default: acc = a_dispatch_u<2>(seg, col, lane, nf, xv); break;
+        }
+        acc = warp_sum(acc);
+        if (lane == c) res = acc;
+        seg += (nf * par_w(col) + 31) >> 5;
+    }
+    const LeafA L = p.leafa[it.leaf];
+    if (L.nchunks == 1) {
+        if (lane < nseg) p.c[it.xcol + lane] = p.alpha * __ldg(p.coef + it.xcol + lane) * res;
+        return;
+    }
+    if (lane < nseg) p.partial[L.pbase + static_cast<uint32_t>(it.chunk) * L.k + it.icol0 + lane] = res;
+    __threadfence();
+    __syncwarp();
+    unsigned last = 0;
+    if (lane == 0) last = atomicAdd(p.counter + it.leaf, 1u) == L.nitems - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {  // every chunk is in: sum in fixed chunk order (deterministic)
+        __threadfence();
+        for (unsigned i = lane; i < L.k; i += 32) {
+            double s = 0.0;
+            for (unsigned ch = 0; ch < L.nchunks; ++ch) s += __ldcg(p.partial + L.pbase + ch * L.k + i);
+            p.c[L.colbase + i] = p.alpha * __ldg(p.coef + L.colbase + i) * s;
+        }
+        if (lane == 0) p.counter[it.leaf] = 0u;  // re-armed for the next product
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_phase_a(Params p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
+    uint64_t* empty = full + kNStage;
+    const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t s0 = p.stripe_a[blockIdx.x], s1 = p.stripe_a[blockIdx.x + 1];
+    if (tid == 0) {
+        for (int b = 0; b < kNStage; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&empty[b], kNW);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == kNW) {
+        producer<true>(p, smem, full, empty, s0, s1, lane);
+        return;
+    }
+    for (uint32_t s = s0; s < s1; ++s) {
+        const uint32_t it = s - s0;
+        const int slot = static_cast<int>(it % kNStage);
+        mbar_wait(&full[slot], (it / kNStage) & 1u);
+        const uint8_t* base = smem + static_cast<size_t>(slot) * kSlotBytes;
+        const uint16_t* wb = reinterpret_cast<const uint16_t*>(base + kOffWb);
+        const AItem* items = reinterpret_cast<const AItem*>(base + kOffDesc);
+        const unsigned b = wb[warp], e = wb[warp + 1];
+        for (unsigned i = b; i < e; ++i) a_item(p, items[i], base, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
     }
 }
 
 // ------------------------------------------------------------ phase B ----
-__global__ void __launch_bounds__(kNW * 32) k_phase_b(Params p) {
+// generic path: any row offset / count (lanes individually predicated)
+template <int MODE>
+__device__ __forceinline__ void b_column(const uint32_t* seg, const ColPar& c, int f0, unsigned vmask,
+                                         unsigned umask, double coef, double (&acc)[kG]) {
+    const unsigned w = par_w(c);
+    const int bit0 = f0 * static_cast<int>(w);
+    const uint32_t* sp = seg + (bit0 >> 5);
+    const unsigned sh = static_cast<unsigned>(bit0) & 31u;
+#pragma unroll
+    for (int g = 0; g < kG; ++g) {
+        if (umask & (1u << g)) {
+            if (vmask & (1u << g)) {
+                double cs;
+                const double d = dec<MODE>(sp + g * w, c, sh, coef, cs);
+                acc[g] = fma(d, cs, acc[g]);
+            }
+        }
+    }
+}
+
+// fast path: the item covers row groups [GLO, GHI) of the block completely, so
+// every lane decodes one field per group with no predication
+template <int MODE, int GLO, int GHI>
+__device__ __forceinline__ void b_column_full(const uint32_t* sp, const ColPar& c, unsigned sh, double coef,
+                                              double (&acc)[kG]) {
+    const unsigned w = par_w(c);
+#pragma unroll
+    for (int g = GLO; g < GHI; ++g) {
+        double cs;
+        const double d = dec<MODE>(sp + (g - GLO) * w, c, sh, coef, cs);
+        acc[g] = fma(d, cs, acc[g]);
+    }
+}
+
+template <int GLO, int GHI>
+__device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg, const uint8_t* cbase,
+                                            unsigned lane, double dmul, double (&acc)[kG]) {
+    const unsigned nseg = it.nseg;
+    constexpr unsigned nr = 32 * (GHI - GLO);
+    if (it.kind == 0) {  // dense: one layout for the whole item
+        const ColPar col = it.par;
+        const double* cf = reinterpret_cast<const double*>(cbase) + it.shift;
+        const double mul = dmul;
+        const unsigned w = par_w(col);
+        const unsigned bit = lane * w;
+        const uint32_t* sp = seg + (bit >> 5);
+        const unsigned sh = bit & 31u;
+        const unsigned segw = (nr * w + 31) >> 5;
+        const unsigned mode = par_mode(col);
+        for (unsigned c = 0; c < nseg; ++c) {
+            const double cc = mul * cf[c];
+            if (mode == 0) b_column_full<0, GLO, GHI>(sp, col, sh, cc, acc);
+            else if (mode == 1) b_column_full<1, GLO, GHI>(sp, col, sh, cc, acc);
+            else b_column_full<2, GLO, GHI>(sp, col, sh, cc, acc);
+            sp += segw;
+        }
+    } else {
+        const double* cf = reinterpret_cast<const double*>(cbase);
+        const ColPar* par = reinterpret_cast<const ColPar*>(cbase + round16u(nseg * 8u));
+        for (unsigned c = 0; c < nseg; ++c) {
+            const ColPar col = par[c];
+            const double cc = cf[c];
+            const unsigned w = par_w(col);
+            const unsigned bit = lane * w;
+            const uint32_t* sp = seg + (bit >> 5);
+            const unsigned sh = bit & 31u;
+            switch (par_mode(col)) {
+                case 0: b_column_full<0, GLO, GHI>(sp, col, sh, cc, acc); break;
+                case 1: b_column_full<1, GLO, GHI>(sp, col, sh, cc, acc); break;
+                default: b_column_full<2, GLO, GHI>(sp, col, sh, cc, acc); break;
+            }
+            seg += (nr * w + 31) >> 5;
+        }
+    }
+}
+
+__device__ __forceinline__ void b_item(const Params& p, const BItem& it, const uint8_t* slot, unsigned lane,
+                                       double (&acc)[kG]) {
+    const unsigned nseg = it.nseg, nr = it.nr;
+    const uint8_t* cbase = slot + kOffCoef + it.coef_off;
+    const double dmul = p.alpha * it.scale;  // dense: alpha * buffer scale folded into x
+    // lane owns rows 32 g + lane of the block; field index f0 + 32 g in each segment
+    const int f0 = static_cast<int>(lane) - static_cast<int>(it.ra);
+    unsigned vmask = 0;
+#pragma unroll
+    for (int g = 0; g < kG; ++g) {
+        const int f = f0 + 32 * g;
+        if (f >= 0 && f < static_cast<int>(nr)) vmask |= 1u << g;
+    }
+    const unsigned umask = __reduce_or_sync(0xffffffffu, vmask);
+    const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
+    if (__all_sync(0xffffffffu, vmask == umask)) {
+        static_assert(kG == 4, "fast-path table assumes 128-row blocks");
+        switch (umask) {
+            case 0x3: b_item_full<0, 2>(it, seg, cbase, lane, dmul, acc); return;
+            case 0xc: b_item_full<2, 4>(it, seg, cbase, lane, dmul, acc); return;
+            case 0xf: b_item_full<0, 4>(it, seg, cbase, lane, dmul, acc); return;
+            case 0x1: b_item_full<0, 1>(it, seg, cbase, lane, dmul, acc); return;
+            case 0x2: b_item_full<1, 2>(it, seg, cbase, lane, dmul, acc); return;
+            case 0x4: b_item_full<2, 3>(it, seg, cbase, lane, dmul, acc); return;
+            case 0x8: b_item_full<3, 4>(it, seg, cbase, lane, dmul, acc); return;
+            default: break;
+        }
+    }
+    const double* cf = reinterpret_cast<const double*>(cbase) + (it.kind == 0 ? it.shift : 0u);
+    const ColPar* par = reinterpret_cast<const ColPar*>(cbase + round16u(nseg * 8u));
+    for (unsigned c = 0; c < nseg; ++c) {
+        const ColPar col = it.kind == 0 ? it.par : par[c];
+        const double cc = it.kind == 0 ? dmul * cf[c] : cf[c];
+        switch (par_mode(col)) {
+            case 0: b_column<0>(seg, col, f0, vmask, umask, cc, acc); break;
+            case 1: b_column<1>(seg, col, f0, vmask, umask, cc, acc); break;
+            default: b_column<2>(seg, col, f0, vmask, umask, cc, acc); break;
+        }
+        seg += (nr * par_w(col) + 31) >> 5;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_phase_b(Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
-    Ring r{smem, reinterpret_cast<uint64_t*>(smem + kNStage * (kStageBytes + kSlack))};
-    double* red = reinterpret_cast<double*>(smem + kNStage * (kStageBytes + kSlack) + 64);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
+    uint64_t* empty = full + kNStage;
     const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t blk = blockIdx.x;
     const uint32_t s0 = p.stripe_b[blk], s1 = p.stripe_b[blk + 1];
-    const unsigned nrows = p.row_count[blk];
-    const bool v0 = lane < nrows, v1 = lane + 32 < nrows;
-    uint64_t policy = 0;
     if (tid == 0) {
-        policy = evict_first_policy();
-        for (int b = 0; b < kNStage; ++b) mbar_init(&r.bars[b], 1);
+        for (int b = 0; b < kNStage; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&empty[b], kNW);
+        }
         fence_barrier_init();
     }
     __syncthreads();
-    if (tid == 0)
-        for (int b = 0; b < kNStage && s0 + b < s1; ++b) issue_stage(p, r, s0 + b, b, policy);
-    double acc0 = 0.0, acc1 = 0.0;
-    for (uint32_t s = s0; s < s1; ++s) {
-        const uint32_t it = s - s0;
-        const int slot = static_cast<int>(it % kNStage);
-        mbar_wait(&r.bars[slot], (it / kNStage) & 1u);
-        const Stage st = p.stages[s];
-        const uint32_t* sw = r.stage_words(slot);
-        for (uint32_t i = warp; i < st.nitems; i += kNW) {
-            const BItem item = p.bitems[st.item0 + i];
-            const uint32_t* wp = sw + item.word_off;
-            const unsigned e = item.e;
-            if (item.kind == 0) {
-                const DenseInfo di = p.dense[item.b];
-                const unsigned w = di.w, m = di.m;
-                const unsigned bit = lane * w, q = bit >> 5, sh = bit & 31u;
-                const unsigned segw = (nrows * w + 31) >> 5;
-                double i0 = 0.0, i1 = 0.0;
-                for (unsigned c = 0; c < item.nseg; ++c) {
-                    const double xc = __ldg(p.x + item.a + c);
-                    uint64_t sg;
-                    if (v0) i0 = fma(decode_a(wp, q, sh, w, e, m, sg), signed_coef(xc, sg), i0);
-                    if (v1) i1 = fma(decode_a(wp, q + w, sh, w, e, m, sg), signed_coef(xc, sg), i1);
-                    wp += segw;
-                }
-                const double mul = p.alpha * di.scale;
-                acc0 = fma(mul, i0, acc0);
-                acc1 = fma(mul, i1, acc1);
-            } else {
-                for (unsigned c = 0; c < item.nseg; ++c) {
-                    const uint32_t j = item.a + c;
-                    const uint16_t wm = __ldg(p.colw_wm + j);
-                    const unsigned w = wm & 0xffu, m = wm >> 8;
-                    const double cj = p.c[j];
-                    const unsigned bit = lane * w, q = bit >> 5, sh = bit & 31u;
-                    uint64_t sg;
-                    if (v0) acc0 = fma(decode_a(wp, q, sh, w, e, m, sg), signed_coef(cj, sg), acc0);
-                    if (v1) acc1 = fma(decode_a(wp, q + w, sh, w, e, m, sg), signed_coef(cj, sg), acc1);
-                    wp += (nrows * w + 31) >> 5;
-                }
-            }
+    double acc[kG];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) acc[g] = 0.0;
+    if (warp == kNW) {
+        producer<false>(p, smem, full, empty, s0, s1, lane);
+    } else {
+        for (uint32_t s = s0; s < s1; ++s) {
+            const uint32_t it = s - s0;
+            const int slot = static_cast<int>(it % kNStage);
+            mbar_wait(&full[slot], (it / kNStage) & 1u);
+            const uint8_t* base = smem + static_cast<size_t>(slot) * kSlotBytes;
+            const uint16_t* wb = reinterpret_cast<const uint16_t*>(base + kOffWb);
+            const BItem* items = reinterpret_cast<const BItem*>(base + kOffDesc);
+            const unsigned b = wb[warp], e = wb[warp + 1];
+            for (unsigned i = b; i < e; ++i) b_item(p, items[i], base, lane, acc);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
         }
-        __syncthreads();
-        if (tid == 0 && s + kNStage < s1) issue_stage(p, r, s + kNStage, slot, policy);
     }
-    red[warp * 64 + lane] = acc0;
-    red[warp * 64 + lane + 32] = acc1;
+    __syncthreads();  // ring drained: reuse it for the cross-warp reduction
+    double* red = reinterpret_cast<double*>(smem);
+    if (warp < kNW) {
+#pragma unroll
+        for (int g = 0; g < kG; ++g) red[warp * kR + 32 * g + lane] = acc[g];
+    }
     __syncthreads();
-    if (tid < nrows) {
+    const uint32_t r0 = p.row_begin + blk * kR;
+    const uint32_t nrows = min(static_cast<uint32_t>(kR), p.row_end - r0);
+    for (uint32_t r = tid; r < nrows; r += kThreads) {
         double sum = 0.0;
 #pragma unroll
-        for (int wv = 0; wv < kNW; ++wv) sum += red[wv * 64 + tid];
-        double* yp = p.y + p.row_first[blk] + tid;
+        for (int wv = 0; wv < kNW; ++wv) sum += red[wv * kR + r];
+        double* yp = p.y + r0 + r;
         *yp = p.beta == 0.0 ? sum : fma(p.beta, *yp, sum);
     }
 }
@@ -357,8 +637,6 @@ __global__ void k_scale(double* y, uint64_t n, double beta) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (uint64_t)blockDim.x)
         y[i] = beta == 0.0 ? 0.0 : beta * y[i];
 }
-
-constexpr size_t kSmemBytes = kNStage * (kStageBytes + kSlack) + 64 + kNW * 64 * sizeof(double);
 
 // ------------------------------------------------------- host: layout ----
 // copy nbits starting at bit `bit` of the LSB-first stream src[0, len) into
@@ -381,6 +659,7 @@ void copy_bits(const uint8_t* src, uint64_t len, uint64_t bit, uint64_t nbits, u
     }
 }
 
+
 struct SegRef {  // where a run of a buffer's fields landed in the arena (export)
     uint64_t word;  // arena word index
     uint32_t f0, nf;
@@ -393,8 +672,8 @@ using namespace hcmx_gpu;
 
 struct hcmx_hmat {
     uint64_t n_rows = 0, n_cols = 0, rb = 0, re = 0;
-    DevBuf arena, stages, bitems, aitems, stripe_a, stripe_b, row_first, row_count, leafa, dense, colw, colx,
-        coef, c, partial, counter, xbuf, ybuf;
+    DevBuf arena, stages, stage_wb, bitems, aitems, stripe_a, stripe_b, leafa, colw, colx, coef, c, partial, xpad,
+        counter, xbuf, ybuf;
     uint32_t nstripe_a = 0, nblocks = 0, nlr = 0;
     hcmx_memory_report report{};
     std::vector<std::vector<SegRef>> segs;  // per buffer (export); empty if too big
@@ -440,14 +719,109 @@ void drain_timing(hcmx_hmat* h) {
     h->pending.clear();
 }
 
+
+
+// Stage packing: items are appended (data written to the arena as they come);
+// when a stage is full it is closed, its items are assigned to the kNW consumer
+// warps by LPT on their field counts, and the descriptors are emitted grouped
+// by warp (data stays where it is: word offsets are stage-relative).
+template <class Item>
+struct StagePacker {
+    std::vector<uint32_t>& arena;
+    std::vector<Stage>& stages;
+    std::vector<uint16_t>& wb;
+    std::vector<Item>& out;
+    std::vector<std::pair<Item, uint64_t>> pending;  // item, cost
+    uint64_t start = 0;
+    uint32_t coef = 0;  // staged coefficient bytes of the open stage
+    bool open = false;
+
+    StagePacker(std::vector<uint32_t>& a, std::vector<Stage>& s, std::vector<uint16_t>& w, std::vector<Item>& o)
+        : arena(a), stages(s), wb(w), out(o) {}
+
+    // reserve room for an item of `words` packed words and `cbytes` staged
+    // coefficient bytes; returns the stage-relative word offset of its data and
+    // sets *coef_off to its offset in the slot's coefficient area
+    uint32_t place(uint64_t words, uint32_t cbytes, uint32_t* coef_off) {
+        if (words * 4 > static_cast<uint64_t>(kStageBytes) || cbytes > static_cast<uint32_t>(kCoefBytes))
+            throw invalid_argument("hmat: item exceeds a stage");
+        if (open && ((arena.size() - start + words) * 4 > static_cast<uint64_t>(kStageBytes) ||
+                     coef + cbytes > static_cast<uint32_t>(kCoefBytes) || pending.size() >= kMaxItems))
+            close();
+        if (!open) {
+            while (arena.size() % 4) arena.push_back(0u);  // 16-byte aligned stages
+            start = arena.size();
+            coef = 0;
+            open = true;
+        }
+        *coef_off = coef;
+        coef += cbytes;
+        return static_cast<uint32_t>(arena.size() - start);
+    }
+    void add(const Item& it, uint64_t cost) { pending.emplace_back(it, cost); }
+    void close() {
+        if (!open) return;
+        open = false;
+        while (arena.size() % 4) arena.push_back(0u);
+        if (pending.empty()) return;
+        // LPT: biggest item first onto the least-loaded warp; keep arrival order per warp
+        std::vector<size_t> order(pending.size());
+        for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](size_t a, size_t b) { return pending[a].second > pending[b].second; });
+        std::vector<uint64_t> load(kNW, 0);
+        std::vector<int> owner(pending.size());
+        for (size_t i : order) {
+            const int wv = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+            owner[i] = wv;
+            load[wv] += pending[i].second + 64;
+        }
+        Stage s{};
+        s.byte_off = start * 4;
+        s.bytes = static_cast<uint32_t>((arena.size() - start) * 4);
+        s.item0 = static_cast<uint32_t>(out.size());
+        s.nitems = static_cast<uint32_t>(pending.size());
+        s.coef_bytes = coef;
+        stages.push_back(s);
+        uint16_t cnt = 0;
+        for (int wv = 0; wv < kNW; ++wv) {
+            wb.push_back(cnt);
+            for (size_t i = 0; i < pending.size(); ++i)
+                if (owner[i] == wv) {
+                    out.push_back(pending[i].first);
+                    ++cnt;
+                }
+        }
+        wb.push_back(cnt);
+        while (wb.size() % 24) wb.push_back(cnt);  // 48 bytes per stage (one bulk copy)
+        pending.clear();
+    }
+};
+
+// host-side column parameters for the decoder (see dec<MODE>)
+ColPar col_par(const hcmx_descriptor& x) {
+    ColPar c{};
+    const unsigned w = x.bit_width, m = x.mant_bits, e = x.exp_bits, em = e + m;
+    const unsigned mode = (w > 32 || e == 11) ? 2u : (m <= 20 ? 0u : 1u);
+    c.mask_em = em >= 32 ? 0xffffffffu : ((1u << em) - 1u);
+    c.mul_rsh = mode == 0 ? (1u << (20 - m)) : (mode == 1 ? m - 20 : 0u);
+    c.packed = w | (m << 8) | (e << 16) | (mode << 24);
+    c.sgn_sh = em <= 31 ? 31 - em : 0u;
+    return c;
+}
+
+inline uint32_t r16(uint64_t x) { return static_cast<uint32_t>((x + 15) & ~uint64_t(15)); }
+
 struct Builder {
     const hcmx_hmat_desc& d;
     hcmx_hmat* h;
     std::vector<uint8_t> blob_host;
     const uint8_t* blob = nullptr;
+    bool keep_map = false;
 
     std::vector<uint32_t> arena;  // words
     std::vector<Stage> stages;
+    std::vector<uint16_t> wb;
     std::vector<BItem> bitems;
     std::vector<AItem> aitems;
 
@@ -455,57 +829,15 @@ struct Builder {
 
     unsigned width(uint64_t b) const { return d.desc[b].bit_width; }
 
-    // append words of fields [f0, f0+nf) of buffer b; returns words appended
-    uint64_t put_fields(uint64_t b, uint64_t f0, uint64_t nf, bool keep_map) {
+    // append the words of fields [f0, f0+nf) of buffer b (word aligned)
+    void put_fields(uint64_t b, uint64_t f0, uint64_t nf) {
         const unsigned w = width(b);
         const uint64_t nw = (nf * w + 31) / 32;
         const uint64_t at = arena.size();
         arena.resize(at + nw);
         copy_bits(blob + d.poff[b], static_cast<uint64_t>(d.plen[b]), f0 * w, nf * w, arena.data() + at);
         if (keep_map) h->segs[b].push_back({at, static_cast<uint32_t>(f0), static_cast<uint32_t>(nf)});
-        return nw;
     }
-
-    // greedy stage packing over a list of items whose sizes are known; returns
-    // for each item its stage-relative word offset
-    struct Packer {
-        Builder& B;
-        uint64_t stage_start_word = 0;
-        uint32_t cur_items = 0, item0 = 0;
-        bool open = false;
-        explicit Packer(Builder& b) : B(b) {}
-        void begin(uint32_t first_item) {
-            // stages start 16-byte aligned
-            while (B.arena.size() % 4) B.arena.push_back(0u);
-            stage_start_word = B.arena.size();
-            item0 = first_item;
-            cur_items = 0;
-            open = true;
-        }
-        // called before writing an item of `words` words; may close/open a stage
-        uint32_t place(uint64_t words, uint32_t item_index) {
-            if (!open) begin(item_index);
-            const uint64_t used = B.arena.size() - stage_start_word;
-            if (cur_items > 0 && (used + words) * 4 > static_cast<uint64_t>(kStageBytes)) {
-                close();
-                begin(item_index);
-            }
-            if (words * 4 > static_cast<uint64_t>(kStageBytes)) throw invalid_argument("hmat: item exceeds a stage");
-            ++cur_items;
-            return static_cast<uint32_t>(B.arena.size() - stage_start_word);
-        }
-        void close() {
-            if (!open) return;
-            while (B.arena.size() % 4) B.arena.push_back(0u);
-            Stage s{};
-            s.byte_off = stage_start_word * 4;
-            s.bytes = static_cast<uint32_t>((B.arena.size() - stage_start_word) * 4);
-            s.item0 = item0;
-            s.nitems = cur_items;
-            if (s.nitems) B.stages.push_back(s);
-            open = false;
-        }
-    };
 };
 
 void validate(const hcmx_hmat_desc& d) {
@@ -544,6 +876,8 @@ void validate(const hcmx_hmat_desc& d) {
     }
 }
 
+
+
 void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     validate(d);
     Builder B(d, h);
@@ -568,38 +902,15 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     for (uint64_t l = 0; l < d.nleaves; ++l)
         if ((uint64_t)d.row0[l] < h->re && (uint64_t)d.row1[l] > h->rb) leaves.push_back(l);
 
-    // row blocks: every leaf boundary, then <= 64 rows each
-    std::vector<uint64_t> cuts = {h->rb, h->re};
-    for (uint64_t l : leaves) {
-        cuts.push_back(std::clamp<uint64_t>(d.row0[l], h->rb, h->re));
-        cuts.push_back(std::clamp<uint64_t>(d.row1[l], h->rb, h->re));
-    }
-    std::sort(cuts.begin(), cuts.end());
-    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
-    std::vector<uint32_t> rfirst, rcount;
-    for (size_t i = 0; i + 1 < cuts.size(); ++i)
-        for (uint64_t r = cuts[i]; r < cuts[i + 1]; r += kRowBlock) {
-            rfirst.push_back(static_cast<uint32_t>(r));
-            rcount.push_back(static_cast<uint32_t>(std::min<uint64_t>(kRowBlock, cuts[i + 1] - r)));
-        }
-    const uint32_t nblocks = static_cast<uint32_t>(rfirst.size());
-    std::vector<std::vector<uint32_t>> block_leaves(nblocks);
-    for (uint64_t l : leaves) {
-        const uint64_t a = std::max<uint64_t>(d.row0[l], h->rb), b = std::min<uint64_t>(d.row1[l], h->re);
-        auto it = std::lower_bound(rfirst.begin(), rfirst.end(), static_cast<uint32_t>(a));
-        for (; it != rfirst.end() && *it < b; ++it) block_leaves[it - rfirst.begin()].push_back(static_cast<uint32_t>(l));
-    }
-
-    // per-leaf tables
     uint64_t total_fields = 0;
     for (uint64_t b = 0; b < d.nbuffers; ++b) total_fields += d.count[b];
-    const bool keep_map = total_fields <= (1ull << 28);
-    if (keep_map) h->segs.assign(d.nbuffers, {});
+    B.keep_map = total_fields <= (1ull << 28);
+    if (B.keep_map) h->segs.assign(d.nbuffers, {});
 
-    std::vector<int64_t> lr_id(d.nleaves, -1), dense_id(d.nleaves, -1);
+    // per-leaf tables
+    std::vector<int64_t> lr_id(d.nleaves, -1);
     std::vector<LeafA> leafa;
-    std::vector<DenseInfo> dense;
-    std::vector<uint16_t> colw, colx;
+    std::vector<ColPar> colw, colx;
     std::vector<double> coef;
     uint64_t npartial = 0;
     hcmx_memory_report& rep = h->report;
@@ -608,13 +919,6 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         const int64_t rows = d.row1[l] - d.row0[l], cols = d.col1[l] - d.col0[l];
         if (d.kind[l] == 0) {
             const hcmx_descriptor& x = d.desc[d.buf0[l]];
-            dense_id[l] = static_cast<int64_t>(dense.size());
-            DenseInfo di{};
-            di.scale = x.scale;
-            di.w = x.bit_width;
-            di.m = x.mant_bits;
-            di.e = x.exp_bits;
-            dense.push_back(di);
             rep.dense_leaves++;
             rep.dense_compressed += 20 + d.plen[d.buf0[l]];
             rep.uncompressed_equivalent += 8ull * rows * cols;
@@ -622,21 +926,25 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         } else {
             const uint32_t k = static_cast<uint32_t>(d.rank[l]);
             lr_id[l] = static_cast<int64_t>(leafa.size());
+            if (colw.size() % 2) {  // even column bases: 16-byte aligned bulk copies of C
+                colw.push_back(ColPar{});
+                colx.push_back(ColPar{});
+                coef.push_back(0.0);
+            }
             LeafA L{};
             L.colbase = static_cast<uint32_t>(colw.size());
             L.k = k;
             L.nchunks = static_cast<uint32_t>((cols + kAChunk - 1) / kAChunk);
             L.nitems = L.nchunks * ((k + kAGroup - 1) / kAGroup);
             L.pbase = static_cast<uint32_t>(npartial);
-            L.e = k ? d.desc[d.buf0[l] + k].exp_bits : 2;
             if (L.nchunks > 1) npartial += static_cast<uint64_t>(L.nchunks) * k;
             leafa.push_back(L);
             uint64_t bytes = 8 + 8ull * k;  // APLRLowrank::byte_size (mixedprec.cpp:210-217)
             for (uint32_t i = 0; i < k; ++i) {
                 const hcmx_descriptor& xw = d.desc[d.buf0[l] + i];
                 const hcmx_descriptor& xx = d.desc[d.buf0[l] + k + i];
-                colw.push_back(static_cast<uint16_t>(xw.bit_width | (xw.mant_bits << 8)));
-                colx.push_back(static_cast<uint16_t>(xx.bit_width | (xx.mant_bits << 8)));
+                colw.push_back(col_par(xw));
+                colx.push_back(col_par(xx));
                 coef.push_back(d.sigma[d.sig0[l] + i] * xx.scale * xw.scale);
                 bytes += 40 + d.plen[d.buf0[l] + i] + d.plen[d.buf0[l] + k + i];
                 rep.algorithmic_bytes += 40 + payload_bytes(rows, xw.bit_width) + payload_bytes(cols, xx.bit_width);
@@ -649,12 +957,16 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     }
     rep.algorithmic_bytes += 8ull * d.n_cols + 8ull * (h->re - h->rb);
     h->nlr = static_cast<uint32_t>(leafa.size());
+    for (int pad = 0; pad < 4; ++pad) {  // bulk copies may round up past the last column
+        colw.push_back(ColPar{});
+        colx.push_back(ColPar{});
+        coef.push_back(0.0);
+    }
 
-    // ---- phase A items / stages / stripes
+    // ---- phase A: items (leaf, <= 256 columns of the block, <= 16 rank columns)
     std::vector<uint32_t> stripe_a = {0};
     {
-        Builder::Packer P(B);
-        uint32_t stages_in_stripe = 0;
+        StagePacker<AItem> P(B.arena, B.stages, B.wb, B.aitems);
         for (uint64_t l : leaves) {
             if (d.kind[l] != 1) continue;
             const LeafA& L = leafa[lr_id[l]];
@@ -666,22 +978,21 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                     const uint32_t ng = std::min<uint32_t>(kAGroup, L.k - g);
                     uint64_t words = 0;
                     for (uint32_t i = g; i < g + ng; ++i) words += (nf * B.width(d.buf0[l] + L.k + i) + 31) / 32;
-                    const size_t before = B.stages.size();
+                    const size_t nst = B.stages.size();
                     AItem it{};
-                    it.word_off = P.place(words, static_cast<uint32_t>(B.aitems.size()));
-                    if (B.stages.size() != before && ++stages_in_stripe >= kAStagesPerStripe) {
+                    it.xidx = static_cast<uint32_t>(d.col0[l] + f0);
+                    it.shift = it.xidx & 1u;
+                    it.word_off = P.place(words, r16((nf + it.shift) * 8) + ng * 16, &it.coef_off);
+                    if (B.stages.size() != nst && B.stages.size() - stripe_a.back() >= kAStagesPerStripe)
                         stripe_a.push_back(static_cast<uint32_t>(B.stages.size()));
-                        stages_in_stripe = 0;
-                    }
-                    it.nseg = static_cast<uint16_t>(ng);
+                    it.nseg = static_cast<uint8_t>(ng);
                     it.nf = static_cast<uint16_t>(nf);
                     it.xcol = L.colbase + g;
-                    it.xidx = static_cast<uint32_t>(d.col0[l] + f0);
                     it.leaf = static_cast<uint32_t>(lr_id[l]);
                     it.chunk = static_cast<uint16_t>(ch);
                     it.icol0 = static_cast<uint16_t>(g);
-                    for (uint32_t i = g; i < g + ng; ++i) B.put_fields(d.buf0[l] + L.k + i, f0, nf, keep_map);
-                    B.aitems.push_back(it);
+                    for (uint32_t i = g; i < g + ng; ++i) B.put_fields(d.buf0[l] + L.k + i, f0, nf);
+                    P.add(it, nf * ng);
                 }
             }
         }
@@ -690,28 +1001,39 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     }
     rep.stages_a = B.stages.size();
 
-    // ---- phase B items / stages, one stripe per row block
+    // ---- phase B: one stripe per block of kR rows
+    const uint64_t nblocks = (h->re - h->rb + kR - 1) / kR;
+    std::vector<std::vector<uint32_t>> block_leaves(nblocks);
+    for (uint64_t l : leaves) {
+        const uint64_t a = std::max<uint64_t>(d.row0[l], h->rb) - h->rb;
+        const uint64_t b = std::min<uint64_t>(d.row1[l], h->re) - h->rb;
+        for (uint64_t blk = a / kR; blk * kR < b; ++blk) block_leaves[blk].push_back(static_cast<uint32_t>(l));
+    }
     std::vector<uint32_t> stripe_b = {static_cast<uint32_t>(B.stages.size())};
-    for (uint32_t blk = 0; blk < nblocks; ++blk) {
-        Builder::Packer P(B);
-        const uint64_t r0 = rfirst[blk], nr = rcount[blk];
+    for (uint64_t blk = 0; blk < nblocks; ++blk) {
+        StagePacker<BItem> P(B.arena, B.stages, B.wb, B.bitems);
+        const uint64_t b0 = h->rb + blk * kR, b1 = std::min<uint64_t>(b0 + kR, h->re);
         for (uint32_t l : block_leaves[blk]) {
             const int64_t rows = d.row1[l] - d.row0[l], cols = d.col1[l] - d.col0[l];
-            const uint64_t roff = r0 - d.row0[l];
+            const uint64_t r0 = std::max<uint64_t>(d.row0[l], b0), r1 = std::min<uint64_t>(d.row1[l], b1);
+            const uint64_t nr = r1 - r0, roff = r0 - d.row0[l];
             if (d.kind[l] == 0) {
                 const uint64_t b = d.buf0[l];
                 const unsigned w = B.width(b);
                 for (int64_t c0 = 0; c0 < cols; c0 += kBDenseGroup) {
                     const uint32_t nc = static_cast<uint32_t>(std::min<int64_t>(kBDenseGroup, cols - c0));
                     BItem it{};
-                    it.word_off = P.place(nc * ((nr * w + 31) / 32), static_cast<uint32_t>(B.bitems.size()));
-                    it.nseg = static_cast<uint16_t>(nc);
+                    it.src = static_cast<uint32_t>(d.col0[l] + c0);
+                    it.shift = it.src & 1u;
+                    it.word_off = P.place(nc * ((nr * w + 31) / 32), r16((nc + it.shift) * 8), &it.coef_off);
+                    it.nseg = static_cast<uint8_t>(nc);
                     it.kind = 0;
-                    it.e = d.desc[b].exp_bits;
-                    it.a = static_cast<uint32_t>(d.col0[l] + c0);
-                    it.b = static_cast<uint32_t>(dense_id[l]);
-                    for (uint32_t c = 0; c < nc; ++c) B.put_fields(b, (c0 + c) * rows + roff, nr, keep_map);
-                    B.bitems.push_back(it);
+                    it.ra = static_cast<uint8_t>(r0 - b0);
+                    it.nr = static_cast<uint8_t>(nr);
+                    it.par = col_par(d.desc[b]);
+                    it.scale = d.desc[b].scale;
+                    for (uint32_t c = 0; c < nc; ++c) B.put_fields(b, (c0 + c) * rows + roff, nr);
+                    P.add(it, nc * nr);
                 }
             } else {
                 const LeafA& L = leafa[lr_id[l]];
@@ -720,14 +1042,14 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                     uint64_t words = 0;
                     for (uint32_t i = g; i < g + ng; ++i) words += (nr * B.width(d.buf0[l] + i) + 31) / 32;
                     BItem it{};
-                    it.word_off = P.place(words, static_cast<uint32_t>(B.bitems.size()));
-                    it.nseg = static_cast<uint16_t>(ng);
+                    it.word_off = P.place(words, r16(ng * 8) + ng * 16, &it.coef_off);
+                    it.nseg = static_cast<uint8_t>(ng);
                     it.kind = 1;
-                    it.e = L.k ? d.desc[d.buf0[l]].exp_bits : 2;
-                    it.a = L.colbase + g;
-                    it.b = 0;
-                    for (uint32_t i = g; i < g + ng; ++i) B.put_fields(d.buf0[l] + i, roff, nr, keep_map);
-                    B.bitems.push_back(it);
+                    it.ra = static_cast<uint8_t>(r0 - b0);
+                    it.nr = static_cast<uint8_t>(nr);
+                    it.src = L.colbase + g;
+                    for (uint32_t i = g; i < g + ng; ++i) B.put_fields(d.buf0[l] + i, roff, nr);
+                    P.add(it, ng * nr);
                 }
             }
         }
@@ -735,10 +1057,9 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         stripe_b.push_back(static_cast<uint32_t>(B.stages.size()));
     }
     rep.stages_b = B.stages.size() - rep.stages_a;
-    // B items index their own array: rebase B stage item0 (A and B share `stages`)
-    // (A stages reference aitems, B stages reference bitems -- item0 is per array)
     while (B.arena.size() % 4) B.arena.push_back(0u);
     B.arena.resize(B.arena.size() + 8, 0u);  // tail slack
+    if (B.stages.size() >= (1ull << 31)) throw invalid_argument("hmat: too many stages");
 
     // ---- upload
     cudaStream_t s = h->stream;
@@ -748,28 +1069,29 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     };
     up(h->arena, B.arena.data(), B.arena.size() * 4);
     up(h->stages, B.stages.data(), B.stages.size() * sizeof(Stage));
+    up(h->stage_wb, B.wb.data(), B.wb.size() * sizeof(uint16_t));
     up(h->bitems, B.bitems.data(), B.bitems.size() * sizeof(BItem));
     up(h->aitems, B.aitems.data(), B.aitems.size() * sizeof(AItem));
     up(h->stripe_a, stripe_a.data(), stripe_a.size() * 4);
     up(h->stripe_b, stripe_b.data(), stripe_b.size() * 4);
-    up(h->row_first, rfirst.data(), rfirst.size() * 4);
-    up(h->row_count, rcount.data(), rcount.size() * 4);
     up(h->leafa, leafa.data(), leafa.size() * sizeof(LeafA));
-    up(h->dense, dense.data(), dense.size() * sizeof(DenseInfo));
-    up(h->colw, colw.data(), colw.size() * 2);
-    up(h->colx, colx.data(), colx.size() * 2);
+    up(h->colw, colw.data(), colw.size() * sizeof(ColPar));
+    up(h->colx, colx.data(), colx.size() * sizeof(ColPar));
+    h->xpad.alloc((d.n_cols + 4) * 8);
+    check_cuda(cudaMemsetAsync(h->xpad.p, 0, h->xpad.bytes, s), "memset");
     up(h->coef, coef.data(), coef.size() * 8);
     h->c.alloc(std::max<size_t>(16, coef.size() * 8));
+    check_cuda(cudaMemsetAsync(h->c.p, 0, h->c.bytes, s), "memset");
     h->partial.alloc(std::max<size_t>(16, npartial * 8));
     h->counter.alloc(std::max<size_t>(16, leafa.size() * 4));
     check_cuda(cudaMemsetAsync(h->counter.p, 0, h->counter.bytes, s), "memset");
     stream_sync(s);
     h->nstripe_a = static_cast<uint32_t>(stripe_a.size() - 1);
-    h->nblocks = nblocks;
+    h->nblocks = static_cast<uint32_t>(nblocks);
     rep.device_arena_bytes = B.arena.size() * 4;
-    rep.device_table_bytes = B.stages.size() * sizeof(Stage) + B.bitems.size() * sizeof(BItem) +
-                             B.aitems.size() * sizeof(AItem) + leafa.size() * sizeof(LeafA) +
-                             dense.size() * sizeof(DenseInfo) + colw.size() * 12 + coef.size() * 16;
+    rep.device_table_bytes = B.stages.size() * sizeof(Stage) + B.wb.size() * 2 + B.bitems.size() * sizeof(BItem) +
+                             B.aitems.size() * sizeof(AItem) + leafa.size() * sizeof(LeafA) + colw.size() * 2 * sizeof(ColPar) +
+                             coef.size() * 16;
     rep.overhead = rep.device_table_bytes;
 }
 
@@ -777,22 +1099,23 @@ Params make_params(hcmx_hmat* h, double alpha, const double* x, double beta, dou
     Params p{};
     p.arena = h->arena.as<uint8_t>();
     p.stages = h->stages.as<Stage>();
+    p.stage_wb = h->stage_wb.as<uint16_t>();
     p.bitems = h->bitems.as<BItem>();
     p.aitems = h->aitems.as<AItem>();
     p.stripe_a = h->stripe_a.as<uint32_t>();
     p.stripe_b = h->stripe_b.as<uint32_t>();
-    p.row_first = h->row_first.as<uint32_t>();
-    p.row_count = h->row_count.as<uint32_t>();
     p.leafa = h->leafa.as<LeafA>();
-    p.dense = h->dense.as<DenseInfo>();
-    p.colw_wm = h->colw.as<uint16_t>();
-    p.colx_wm = h->colx.as<uint16_t>();
+    p.colw_par = h->colw.as<ColPar>();
+    p.colx_par = h->colx.as<ColPar>();
     p.coef = h->coef.as<double>();
     p.c = h->c.as<double>();
     p.partial = h->partial.as<double>();
     p.counter = h->counter.as<unsigned>();
-    p.x = x;
+    p.x = h->xpad.as<double>();  // padded, 16-byte aligned copy of x (bulk copies)
+    (void)x;
     p.y = y;
+    p.row_begin = static_cast<uint32_t>(h->rb);
+    p.row_end = static_cast<uint32_t>(h->re);
     p.alpha = alpha;
     p.beta = beta;
     return p;
@@ -815,6 +1138,7 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
         h->last_launches = 1;
         return;
     }
+    check_cuda(cudaMemcpyAsync(h->xpad.p, dx, h->n_cols * 8, cudaMemcpyDeviceToDevice, s), "x copy");
     Params p = make_params(h, alpha, dx, beta, dy);
     hcmx_hmat::Rec rec{};
     if (h->timing) {
@@ -822,12 +1146,12 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
         check_cuda(cudaEventRecord(rec.a0, s), "event");
     }
     if (h->nlr && h->nstripe_a) {
-        k_phase_a<<<h->nstripe_a, kNW * 32, kSmemBytes, s>>>(p);
+        k_phase_a<<<h->nstripe_a, kThreads, kSmemBytes, s>>>(p);
         h->last_launches++;
     }
     if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
     if (h->nblocks) {
-        k_phase_b<<<h->nblocks, kNW * 32, kSmemBytes, s>>>(p);
+        k_phase_b<<<h->nblocks, kThreads, kSmemBytes, s>>>(p);
         h->last_launches++;
     }
     check_cuda(cudaGetLastError(), "matvec launch");
