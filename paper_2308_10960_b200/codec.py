@@ -222,6 +222,14 @@ class BatchBuffers:
     poff: np.ndarray          # uint64 [nbuf] (16-byte aligned byte offsets)
     payload: torch.Tensor     # uint8 cuda arena
     total: int                # arena bytes used
+    _dev: dict = field(default_factory=dict, repr=False)  # cached device copies of the tables
+
+    def dev(self, name: str, host: np.ndarray) -> torch.Tensor:
+        t = self._dev.get(name)
+        if t is None:
+            t = torch.as_tensor(np.ascontiguousarray(host).view(np.uint8)).cuda()
+            self._dev[name] = t
+        return t
 
     def __len__(self):
         return self.count.size
@@ -275,12 +283,14 @@ def compress_batch(values: torch.Tensor, counts, eps: float, scheme, capacity: i
 def decompress_batch(bb: BatchBuffers, out: torch.Tensor | None = None, voff=None) -> torch.Tensor:
     """codec::decompress_into for every buffer of a batch (device -> device)"""
     _lib.ensure_device()
-    vo = _offsets(bb.count) if voff is None else np.ascontiguousarray(voff, dtype=np.uint64)
     if out is None:
         out = torch.empty(int(bb.count.sum()), dtype=torch.float64, device="cuda")
-    d_voff = torch.as_tensor(vo.view(np.int64)).cuda()
-    d_poff = torch.as_tensor(bb.poff.view(np.int64)).cuda()
-    d_desc = torch.as_tensor(bb.desc.view(np.uint8)).cuda()
+    if voff is None:
+        d_voff = bb.dev("voff", _offsets(bb.count))
+    else:
+        d_voff = torch.as_tensor(np.ascontiguousarray(voff, dtype=np.uint64).view(np.int64)).cuda()
+    d_poff = bb.dev("poff", bb.poff)
+    d_desc = bb.dev("desc", bb.desc)
     check(lib().hcmx_gpu_codec_unpack(ptr(bb.payload), ptr(d_poff), u64p(bb.count), ptr(d_desc),
                                       ptr(d_voff), len(bb), ptr(out), _stream()), "decompress")
     return out

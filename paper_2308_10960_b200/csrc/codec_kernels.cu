@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "internal.h"
@@ -40,9 +41,37 @@ void require_device() {
     }
 }
 
+// Small device buffers (job lists, descriptors, offsets) come from a
+// process-wide cache of power-of-two blocks: cudaMalloc/cudaFree synchronise
+// the device and cost more than the kernels of a batched codec call.  Every
+// user of a cached block synchronises its stream before releasing it.
+namespace {
+constexpr size_t kPoolMax = size_t(64) << 20;
+std::mutex g_pool_mu;
+std::vector<std::vector<void*>> g_pool(40);
+int size_class(size_t n) {
+    int c = 8;  // 256 B minimum
+    while ((size_t(1) << c) < n) ++c;
+    return c;
+}
+}  // namespace
+
 void DevBuf::alloc(size_t n) {
     release();
     if (n == 0) return;
+    if (n <= kPoolMax) {
+        const int c = size_class(n);
+        {
+            std::lock_guard<std::mutex> g(g_pool_mu);
+            if (!g_pool[c].empty()) {
+                p = g_pool[c].back();
+                g_pool[c].pop_back();
+                bytes = n;
+                return;
+            }
+        }
+        n = size_t(1) << c;
+    }
     cudaError_t e = cudaMalloc(&p, n);
     if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();
@@ -54,7 +83,14 @@ void DevBuf::alloc(size_t n) {
 }
 
 void DevBuf::release() {
-    if (p) cudaFree(p);
+    if (p) {
+        if (bytes <= kPoolMax) {
+            std::lock_guard<std::mutex> g(g_pool_mu);
+            g_pool[size_class(bytes)].push_back(p);
+        } else {
+            cudaFree(p);
+        }
+    }
     p = nullptr;
     bytes = 0;
 }
@@ -73,7 +109,7 @@ void stream_sync(void* stream) {
 
 namespace {
 
-constexpr unsigned kGroupsPerJob = 64;  // 2048 values per warp job
+constexpr unsigned kGroupsPerJob = 32;  // 1024 values per warp job
 constexpr int kWarpsPerBlock = 8;
 
 struct Job {
@@ -215,11 +251,22 @@ k_pack(const double* __restrict__ values, const uint64_t* __restrict__ voff,
         // output words K = lane and K = lane + 32: first overlapping field and its bit shift
         const unsigned i0a = (32 * lane) / w, i0b = (32 * (lane + 32)) / w;
         int nf_bad = 0;
-        for (uint32_t g = jb.g0; g < jb.g0 + jb.ng; ++g) {
+        const uint32_t gend = jb.g0 + jb.ng;
+        for (uint32_t g4 = jb.g0; g4 < gend; g4 += 4) {
+          double xs[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+              const uint64_t idx = (uint64_t)(g4 + i) * 32 + lane;
+              xs[i] = (g4 + i < gend && idx < n) ? __ldcs(v + idx) : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t g = g4 + i;
+            if (g >= gend) break;
             const uint64_t idx = (uint64_t)g * 32 + lane;
             uint64_t f = 0;
             if (idx < n) {
-                const double x = __ldcs(v + idx);
+                const double x = xs[i];
                 if (!isfinite(x)) nf_bad = 1;
                 else f = encode_value(x, e, m, inv_scale, max_offset, round_add, mant_mask);
             }
@@ -243,6 +290,7 @@ k_pack(const double* __restrict__ values, const uint64_t* __restrict__ voff,
                 }
                 if (K < nwords) __stcs(o + K, word);
             }
+          }
         }
         if (__any_sync(0xffffffffu, nf_bad) && lane == 0) *err = 1;
     }
@@ -284,10 +332,10 @@ k_unpack(const uint8_t* __restrict__ payload, const uint64_t* __restrict__ poff,
         const unsigned bit = lane * w, q = bit >> 5, sh = bit & 31;
         const uint64_t wmask = (w == 64) ? ~0ull : ((1ull << w) - 1);
         const uint32_t gend = jb.g0 + jb.ng;
-        for (uint32_t g = jb.g0; g < gend; g += 4) {
-            uint32_t wa[4], wb[4];
+        for (uint32_t g = jb.g0; g < gend; g += 8) {
+            uint32_t wa[8], wb[8];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < 8; ++i) {
                 const uint32_t gi = g + i;
                 wa[i] = wb[i] = 0;
                 if (gi < gend) {
@@ -298,7 +346,7 @@ k_unpack(const uint8_t* __restrict__ payload, const uint64_t* __restrict__ poff,
                 }
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < 8; ++i) {
                 const uint32_t gi = g + i;
                 if (gi >= gend) break;
                 uint32_t w0, w1, w2 = 0;

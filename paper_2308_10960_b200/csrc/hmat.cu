@@ -3,28 +3,32 @@
 //
 // Layout (built once on the host by hcmx_gpu_hmat_create):
 //   The packed codec streams of every leaf are re-tiled, field-for-field and
-//   bit-identical, into one HBM arena of 16-byte aligned "stages" (<= 24 KB).
+//   bit-identical, into one HBM arena.  Work is cut into items; items are
+//   grouped into CTA "stripes", spread over the CTA's warps by LPT on their
+//   field counts, and each warp's items are packed into its own sequence of
+//   16-byte aligned warp-stages (<= 3 KB of packed data each).
 //
-//   phase A (lowrank X^T x): item = (APLR leaf, <= 256 consecutive columns of
-//     the block, <= 16 rank columns); its data is, for each rank column, the
-//     fields of that X column over the column chunk, word aligned.  One warp
-//     decodes an item with the x values in registers (8 per lane), reduces
-//     per rank column with shuffles, and either writes t_i directly (one chunk)
-//     or a partial that the last-arriving warp sums in fixed chunk order.
+//   phase A (lowrank X^T x): item = (APLR leaf, <= 128 consecutive columns of
+//     the block, <= 4 rank columns); its data is, for each rank column, the
+//     fields of that X column over the column chunk, word aligned.  The items
+//     of one chunk go to one warp and share one staged x slice.  A warp reduces
+//     each rank column with shuffles and writes t_i directly (one chunk) or a
+//     partial that the last-arriving warp sums in fixed chunk order.
 //   phase B (row-stationary): one CTA owns one block of 128 rows and streams
-//     the "stripe" of everything that writes those rows: dense leaves (column
-//     groups of 16) and the W slices of every APLR leaf covering the block.
-//     Lane l owns rows 32 g + l (4 accumulators); y is written once per row.
+//     every item that writes those rows: dense leaves (groups of 8 columns)
+//     and the W slices of every APLR leaf covering the block (<= 8 rank
+//     columns).  Lane l owns rows 32 g + l (4 accumulators per warp); the CTA
+//     sums its warps once at the end and writes y once per row -- no atomics.
 //
-//   Each CTA = 16 consumer warps + 1 producer warp.  The producer moves stages
-//   HBM -> shared memory with cp.async.bulk (the TMA bulk engine, L2
-//   evict_first) into a 4-deep ring; full/empty mbarriers replace CTA-wide
-//   barriers.  Items of a stage are assigned to warps by LPT on their field
-//   counts.  Per item, one round of independent loads fetches the column
-//   widths and coefficients (x, or the phase-A results) -- nothing in the
-//   per-column loop waits on global memory.  A field costs two LDS, a funnel
-//   shift, ~4 integer ops to rebuild the FP64 pattern (32-bit fast paths for
-//   w <= 32), one DADD and one DFMA.
+//   Every warp runs its own 3-deep ring of warp-stages in shared memory, fed
+//   by cp.async.bulk (the TMA bulk engine; packed data with L2 evict_first):
+//   the packed data, the item descriptors, and per item the coefficient slice
+//   (x, or the phase-A results) plus the column parameters.  The warp refills a
+//   slot right after consuming it, with metadata it prefetched while decoding,
+//   so there is no cross-warp coupling and nothing in the decode loop waits on
+//   global memory.  A field costs two LDS, a funnel shift, ~4 integer ops to
+//   rebuild the FP64 pattern (32-bit fast paths for w <= 32), one DADD and one
+//   DFMA.
 //
 // Numerics: decoded values are bit-identical to codec::decompress_into; the
 // multiply by the buffer scale is folded into the coefficients (dense: alpha *
@@ -38,15 +42,18 @@
 #include <vector>
 
 #include "internal.h"
+#include <type_traits>
 
 namespace hcmx_gpu {
 namespace {
 
-constexpr int kNW = 16;                   // consumer warps per CTA
-constexpr int kThreads = (kNW + 1) * 32;  // + one producer warp (bulk copies)
+constexpr int kNWB = 16;                  // phase-B consumer warps per CTA
+constexpr int kNWA = 12;                  // phase-A consumer warps (more registers per thread)
+constexpr int kThreadsB = (kNWB + 1) * 32;  // + one producer warp (bulk copies)
+constexpr int kThreadsA = (kNWA + 1) * 32;
 constexpr int kStageBytes = 24576;        // packed data per stage
 constexpr int kMaxItems = 32;             // items per stage (one per producer lane)
-constexpr int kItemBytes = 48;            // descriptor size (A and B)
+constexpr int kItemBytes = 32;            // descriptor size (A and B)
 constexpr int kCoefBytes = 8192;          // staged coefficients + column params per stage
 constexpr int kNStage = 3;                // ring depth
 constexpr int kSlack = 16;                // decode reads up to 2 words past a segment
@@ -57,14 +64,15 @@ constexpr int kSlotBytes = kOffCoef + kCoefBytes;
 constexpr int kR = 128;               // rows per phase-B CTA
 constexpr int kG = kR / 32;           // row groups (accumulators) per lane
 constexpr int kAChunk = 256;          // X fields per A item (8 per lane)
-constexpr int kAGroup = 16;           // rank columns per A item
-constexpr int kBDenseGroup = 16;      // dense columns per B item
-constexpr int kBLRGroup = 32;         // rank columns per B item
-constexpr int kAStagesPerStripe = 8;  // phase-A stages per CTA
+constexpr int kAGroup = 4;            // max rank columns per A item
+constexpr int kBDenseGroup = 8;       // max dense columns per B item
+constexpr int kBLRGroup = 8;          // max rank columns per B item
+constexpr uint64_t kAStripeBytes = 8 * kStageBytes;  // target packed bytes per phase-A CTA
+constexpr uint64_t kItemTarget = 1536;          // packed bytes per item (columns grouped up to this)
 constexpr size_t kRingBytes = static_cast<size_t>(kNStage) * kSlotBytes;
 constexpr size_t kSmemBytes = kRingBytes + 2 * kNStage * sizeof(uint64_t);
 static_assert(kOffDesc % 16 == 0 && kOffCoef % 16 == 0 && kSlotBytes % 16 == 0, "slot alignment");
-static_assert(kNW * kR * sizeof(double) <= kRingBytes, "reduction reuses the ring");
+static_assert(kNWB * kR * sizeof(double) <= kRingBytes, "reduction reuses the ring");
 
 struct Stage {
     uint64_t byte_off;   // packed data in the arena
@@ -85,15 +93,14 @@ struct ColPar {
 };
 
 struct BItem {
-    uint32_t word_off;   // packed data, from the stage start
+    uint32_t word_off;   // packed data, from the warp-stage start
     uint8_t nseg;        // columns in this item
     uint8_t kind;        // 0 dense, 1 lowrank
     uint8_t ra;          // first row of the item inside the row block
     uint8_t nr;          // rows (fields per column segment)
-    uint32_t coef_off;   // staged coefficients in the slot's coef area (bytes)
+    uint32_t coef_off;   // staged coefficients: dense x slice | lowrank C slice, then column params
     uint32_t src;        // dense: x index of first column; lowrank: global W column id (even)
-    ColPar par;          // dense: the leaf's layout
-    uint32_t shift;      // dense: x slice starts at x[src & ~1], first value at + shift
+    uint32_t dpacked;    // dense: w | m << 8 | e << 16 | mode << 24
     uint32_t pad;
     double scale;        // dense: buffer scale
 };
@@ -102,16 +109,15 @@ static_assert(sizeof(BItem) == kItemBytes, "BItem layout");
 struct AItem {
     uint32_t word_off;
     uint8_t nseg;        // rank columns
-    uint8_t pad0;
+    uint8_t owns_x;      // this item's copy stages the x slice (shared by the chunk's items)
     uint16_t nf;         // fields per column (<= kAChunk)
-    uint32_t coef_off;   // staged x slice then X column params
+    uint32_t x_off;      // staged x slice (coef area bytes)
+    uint32_t par_off;    // staged X column params
     uint32_t xidx;       // x index of field 0
     uint32_t xcol;       // global X column id of the first rank column
     uint32_t leaf;       // lowrank-leaf id
     uint16_t chunk;      // column-chunk index within the leaf
     uint16_t icol0;      // first rank column within the leaf
-    uint32_t shift;      // x slice starts at x[xidx & ~1], first value at + shift
-    uint64_t pad1, pad2;
 };
 static_assert(sizeof(AItem) == kItemBytes, "AItem layout");
 
@@ -127,11 +133,11 @@ struct LeafA {
 struct Params {
     const uint8_t* arena;
     const Stage* stages;
-    const uint16_t* stage_wb;   // [nstages * 24] per-warp item ranges (kNW + 1 used)
-    const BItem* bitems;
-    const AItem* aitems;
+    const uint16_t* stage_wb;   // [nstages * 24] per-warp item ranges (NW + 1 used)
     const uint32_t* stripe_a;   // [nstripe_a + 1] stage ranges
     const uint32_t* stripe_b;   // [nblocks + 1]
+    const BItem* bitems;
+    const AItem* aitems;
     const LeafA* leafa;
     const ColPar* colw_par;
     const ColPar* colx_par;
@@ -182,9 +188,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
     asm volatile(
         "{\n .reg .pred p;\n"
         "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(1000000u)  // suspend (not spin) up to 1 ms: idle warps leave issue slots to busy ones
         : "memory");
 }
 
@@ -234,6 +240,16 @@ __device__ __forceinline__ double dec(const uint32_t* sp, const ColPar& c, unsig
 }
 
 __device__ __forceinline__ unsigned par_w(const ColPar& c) { return c.packed & 0xffu; }
+
+__device__ __forceinline__ ColPar make_par(uint32_t packed) {
+    ColPar c;
+    const unsigned m = (packed >> 8) & 0xffu, e = (packed >> 16) & 0xffu, mode = packed >> 24, em = e + m;
+    c.mask_em = em >= 32 ? 0xffffffffu : ((1u << em) - 1u);
+    c.mul_rsh = mode == 0 ? (1u << (20 - m)) : (mode == 1 ? m - 20 : 0u);
+    c.packed = packed;
+    c.sgn_sh = em <= 31 ? 31 - em : 0u;
+    return c;
+}
 __device__ __forceinline__ unsigned par_mode(const ColPar& c) { return c.packed >> 24; }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -244,18 +260,19 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 __device__ __forceinline__ unsigned round16u(unsigned x) { return (x + 15u) & ~15u; }
 
-// ---------------------------------------------------- producer warp ----
-// One warp fills the ring: the stage's packed data, its item descriptors and
-// per-warp ranges, and -- per item -- the coefficient slice (x or the phase-A
-// results) plus the column parameters, all as cp.async.bulk copies completing
-// on the slot's full barrier.  Consumers never wait on global memory.
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+
+// ------------------------------------------------------- warp pipeline ----
 // staged copies of one item (sizes must match the host's coef_bytes):
 // copy 0 = coefficient slice (x, or the phase-A results C), copy 1 = column params
 struct ProdItem {
-    uint32_t coef_off;
-    uint32_t sizes;   // n0 | n1 << 16 (bytes)
-    uint32_t i0;      // element index of copy 0 in x (or C when lowrank)
-    uint32_t i1;      // column id of copy 1; bit 31 set: copy 0 reads C
+    uint32_t dst0, dst1;  // coef-area offsets of the two copies
+    uint32_t sizes;       // n0 | n1 << 16 (bytes; 0 = no copy)
+    uint32_t i0;          // element index of copy 0 in x (or C when bit 31 of i1)
+    uint32_t i1;          // column id of copy 1 (params)
 };
 
 template <bool PHASE_A>
@@ -263,19 +280,22 @@ __device__ __forceinline__ ProdItem prod_item(const Params& p, uint32_t idx) {
     ProdItem r{};
     if (PHASE_A) {
         const AItem a = p.aitems[idx];
-        r.coef_off = a.coef_off;
-        r.sizes = round16u((a.nf + a.shift) * 8u) | ((a.nseg * 16u) << 16);
+        r.dst0 = a.x_off;
+        r.dst1 = a.par_off;
+        r.sizes = (a.owns_x ? round16u((a.nf + (a.xidx & 1u)) * 8u) : 0u) | ((a.nseg * 16u) << 16);
         r.i0 = a.xidx & ~1u;
         r.i1 = a.xcol;
     } else {
         const BItem b = p.bitems[idx];
-        r.coef_off = b.coef_off;
+        r.dst0 = b.coef_off;
         if (b.kind == 0) {
-            r.sizes = round16u((b.nseg + b.shift) * 8u);
+            r.sizes = round16u((b.nseg + (b.src & 1u)) * 8u);
             r.i0 = b.src & ~1u;
         } else {
-            r.sizes = round16u(b.nseg * 8u) | ((b.nseg * 16u) << 16);
-            r.i0 = b.src;
+            const unsigned n0 = round16u((b.nseg + (b.src & 1u)) * 8u);
+            r.dst1 = b.coef_off + n0;
+            r.sizes = n0 | ((b.nseg * 16u) << 16);
+            r.i0 = b.src & ~1u;
             r.i1 = b.src | 0x80000000u;
         }
     }
@@ -316,18 +336,46 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
         }
         __syncwarp();
         if (lane < st.nitems) {
-            uint8_t* cdst = base + kOffCoef + pi.coef_off;
+            uint8_t* cdst = base + kOffCoef;
             const unsigned n0 = pi.sizes & 0xffffu, n1 = pi.sizes >> 16;
             const bool from_c = !PHASE_A && (pi.i1 & 0x80000000u);
-            bulk_g2s_plain(cdst, (from_c ? p.c : p.x) + pi.i0, n0, &full[slot]);
+            if (n0) bulk_g2s_plain(cdst + pi.dst0, (from_c ? p.c : p.x) + pi.i0, n0, &full[slot]);
             if (n1) {
                 const ColPar* par = PHASE_A ? p.colx_par : p.colw_par;
-                bulk_g2s_plain(cdst + n0, par + (pi.i1 & 0x7fffffffu), n1, &full[slot]);
+                bulk_g2s_plain(cdst + pi.dst1, par + (pi.i1 & 0x7fffffffu), n1, &full[slot]);
             }
         }
         st = nst;
         pi = npi;
     }
+}
+
+// consumer warps of a CTA ring: body(slot_base, first, end) for the warp's items
+template <int NW, class Body>
+__device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t* empty, uint32_t s0, uint32_t s1,
+                                        unsigned warp, unsigned lane, Body&& body) {
+    for (uint32_t s = s0; s < s1; ++s) {
+        const uint32_t it = s - s0;
+        const int slot = static_cast<int>(it % kNStage);
+        mbar_wait(&full[slot], (it / kNStage) & 1u);
+        const uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
+        const uint16_t* wb = reinterpret_cast<const uint16_t*>(base + kOffWb);
+        body(base, wb[warp], wb[warp + 1]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+}
+
+template <int NW>
+__device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < kNStage; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&empty[b], NW);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
 }
 
 // ------------------------------------------------------------ phase A ----
@@ -385,8 +433,8 @@ __device__ __forceinline__ double a_dispatch_u(const uint32_t* seg, const ColPar
 
 __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const uint8_t* slot, unsigned lane) {
     const unsigned nseg = it.nseg, nf = it.nf;
-    const double* xs = reinterpret_cast<const double*>(slot + kOffCoef + it.coef_off) + it.shift;
-    const ColPar* par = reinterpret_cast<const ColPar*>(slot + kOffCoef + it.coef_off + round16u((nf + it.shift) * 8u));
+    const double* xs = reinterpret_cast<const double*>(slot + kOffCoef + it.x_off) + (it.xidx & 1u);
+    const ColPar* par = reinterpret_cast<const ColPar*>(slot + kOffCoef + it.par_off);
     double xv[kAChunk / 32];
     const unsigned U = (nf + 31) >> 5;
 #pragma unroll
@@ -414,51 +462,21 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
         return;
     }
     if (lane < nseg) p.partial[L.pbase + static_cast<uint32_t>(it.chunk) * L.k + it.icol0 + lane] = res;
-    __threadfence();
     __syncwarp();
     unsigned last = 0;
-    if (lane == 0) last = atomicAdd(p.counter + it.leaf, 1u) == L.nitems - 1;
+    if (lane == 0) {  // release our partials, acquire everyone else's (partials are read from L2)
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.counter + it.leaf) : "memory");
+        last = old == L.nitems - 1;
+    }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {  // every chunk is in: sum in fixed chunk order (deterministic)
-        __threadfence();
         for (unsigned i = lane; i < L.k; i += 32) {
             double s = 0.0;
             for (unsigned ch = 0; ch < L.nchunks; ++ch) s += __ldcg(p.partial + L.pbase + ch * L.k + i);
             p.c[L.colbase + i] = p.alpha * __ldg(p.coef + L.colbase + i) * s;
         }
         if (lane == 0) p.counter[it.leaf] = 0u;  // re-armed for the next product
-    }
-}
-
-__global__ void __launch_bounds__(kThreads, 2) k_phase_a(Params p) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
-    uint64_t* empty = full + kNStage;
-    const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint32_t s0 = p.stripe_a[blockIdx.x], s1 = p.stripe_a[blockIdx.x + 1];
-    if (tid == 0) {
-        for (int b = 0; b < kNStage; ++b) {
-            mbar_init(&full[b], 1);
-            mbar_init(&empty[b], kNW);
-        }
-        fence_barrier_init();
-    }
-    __syncthreads();
-    if (warp == kNW) {
-        producer<true>(p, smem, full, empty, s0, s1, lane);
-        return;
-    }
-    for (uint32_t s = s0; s < s1; ++s) {
-        const uint32_t it = s - s0;
-        const int slot = static_cast<int>(it % kNStage);
-        mbar_wait(&full[slot], (it / kNStage) & 1u);
-        const uint8_t* base = smem + static_cast<size_t>(slot) * kSlotBytes;
-        const uint16_t* wb = reinterpret_cast<const uint16_t*>(base + kOffWb);
-        const AItem* items = reinterpret_cast<const AItem*>(base + kOffDesc);
-        const unsigned b = wb[warp], e = wb[warp + 1];
-        for (unsigned i = b; i < e; ++i) a_item(p, items[i], base, lane);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
     }
 }
 
@@ -497,31 +515,37 @@ __device__ __forceinline__ void b_column_full(const uint32_t* sp, const ColPar& 
     }
 }
 
+// dense item, one layout: the mode is fixed for the whole column loop
+template <int MODE, int GLO, int GHI>
+__device__ __forceinline__ void b_dense_full(const uint32_t* sp, const ColPar& col, unsigned sh, unsigned segw,
+                                             const double* cf, double dmul, unsigned nseg, double (&acc)[kG]) {
+#pragma unroll 2
+    for (unsigned c = 0; c < nseg; ++c) {
+        b_column_full<MODE, GLO, GHI>(sp, col, sh, dmul * cf[c], acc);
+        sp += segw;
+    }
+}
+
 template <int GLO, int GHI>
 __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg, const uint8_t* cbase,
                                             unsigned lane, double dmul, double (&acc)[kG]) {
     const unsigned nseg = it.nseg;
     constexpr unsigned nr = 32 * (GHI - GLO);
+    const double* cf = reinterpret_cast<const double*>(cbase) + (it.src & 1u);
     if (it.kind == 0) {  // dense: one layout for the whole item
-        const ColPar col = it.par;
-        const double* cf = reinterpret_cast<const double*>(cbase) + it.shift;
-        const double mul = dmul;
+        const ColPar col = make_par(it.dpacked);
         const unsigned w = par_w(col);
         const unsigned bit = lane * w;
         const uint32_t* sp = seg + (bit >> 5);
         const unsigned sh = bit & 31u;
         const unsigned segw = (nr * w + 31) >> 5;
-        const unsigned mode = par_mode(col);
-        for (unsigned c = 0; c < nseg; ++c) {
-            const double cc = mul * cf[c];
-            if (mode == 0) b_column_full<0, GLO, GHI>(sp, col, sh, cc, acc);
-            else if (mode == 1) b_column_full<1, GLO, GHI>(sp, col, sh, cc, acc);
-            else b_column_full<2, GLO, GHI>(sp, col, sh, cc, acc);
-            sp += segw;
+        switch (par_mode(col)) {
+            case 0: b_dense_full<0, GLO, GHI>(sp, col, sh, segw, cf, dmul, nseg, acc); break;
+            case 1: b_dense_full<1, GLO, GHI>(sp, col, sh, segw, cf, dmul, nseg, acc); break;
+            default: b_dense_full<2, GLO, GHI>(sp, col, sh, segw, cf, dmul, nseg, acc); break;
         }
     } else {
-        const double* cf = reinterpret_cast<const double*>(cbase);
-        const ColPar* par = reinterpret_cast<const ColPar*>(cbase + round16u(nseg * 8u));
+        const ColPar* par = reinterpret_cast<const ColPar*>(cbase + round16u((nseg + (it.src & 1u)) * 8u));
         for (unsigned c = 0; c < nseg; ++c) {
             const ColPar col = par[c];
             const double cc = cf[c];
@@ -529,11 +553,10 @@ __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg
             const unsigned bit = lane * w;
             const uint32_t* sp = seg + (bit >> 5);
             const unsigned sh = bit & 31u;
-            switch (par_mode(col)) {
-                case 0: b_column_full<0, GLO, GHI>(sp, col, sh, cc, acc); break;
-                case 1: b_column_full<1, GLO, GHI>(sp, col, sh, cc, acc); break;
-                default: b_column_full<2, GLO, GHI>(sp, col, sh, cc, acc); break;
-            }
+            const unsigned mode = par_mode(col);
+            if (mode == 0) b_column_full<0, GLO, GHI>(sp, col, sh, cc, acc);
+            else if (mode == 1) b_column_full<1, GLO, GHI>(sp, col, sh, cc, acc);
+            else b_column_full<2, GLO, GHI>(sp, col, sh, cc, acc);
             seg += (nr * w + 31) >> 5;
         }
     }
@@ -567,10 +590,11 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
             default: break;
         }
     }
-    const double* cf = reinterpret_cast<const double*>(cbase) + (it.kind == 0 ? it.shift : 0u);
-    const ColPar* par = reinterpret_cast<const ColPar*>(cbase + round16u(nseg * 8u));
+    const double* cf = reinterpret_cast<const double*>(cbase) + (it.src & 1u);
+    const ColPar* par = reinterpret_cast<const ColPar*>(cbase + round16u((nseg + (it.src & 1u)) * 8u));
+    const ColPar dpar = make_par(it.dpacked);
     for (unsigned c = 0; c < nseg; ++c) {
-        const ColPar col = it.kind == 0 ? it.par : par[c];
+        const ColPar col = it.kind == 0 ? dpar : par[c];
         const double cc = it.kind == 0 ? dmul * cf[c] : cf[c];
         switch (par_mode(col)) {
             case 0: b_column<0>(seg, col, f0, vmask, umask, cc, acc); break;
@@ -581,54 +605,56 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 2) k_phase_b(Params p) {
+__global__ void __launch_bounds__(kThreadsA, 2) k_phase_a(Params p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
+    uint64_t* empty = full + kNStage;
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t s0 = p.stripe_a[blockIdx.x], s1 = p.stripe_a[blockIdx.x + 1];
+    ring_init<kNWA>(full, empty);
+    if (warp == kNWA) {
+        producer<true>(p, smem, full, empty, s0, s1, lane);
+        return;
+    }
+    consume<kNWA>(smem, full, empty, s0, s1, warp, lane, [&](const uint8_t* base, unsigned b, unsigned e) {
+        const AItem* items = reinterpret_cast<const AItem*>(base + kOffDesc);
+        for (unsigned i = b; i < e; ++i) a_item(p, items[i], base, lane);
+    });
+}
+
+__global__ void __launch_bounds__(kThreadsB, 2) k_phase_b(Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
     uint64_t* empty = full + kNStage;
     const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t blk = blockIdx.x;
     const uint32_t s0 = p.stripe_b[blk], s1 = p.stripe_b[blk + 1];
-    if (tid == 0) {
-        for (int b = 0; b < kNStage; ++b) {
-            mbar_init(&full[b], 1);
-            mbar_init(&empty[b], kNW);
-        }
-        fence_barrier_init();
-    }
-    __syncthreads();
+    ring_init<kNWB>(full, empty);
     double acc[kG];
 #pragma unroll
     for (int g = 0; g < kG; ++g) acc[g] = 0.0;
-    if (warp == kNW) {
+    if (warp == kNWB) {
         producer<false>(p, smem, full, empty, s0, s1, lane);
     } else {
-        for (uint32_t s = s0; s < s1; ++s) {
-            const uint32_t it = s - s0;
-            const int slot = static_cast<int>(it % kNStage);
-            mbar_wait(&full[slot], (it / kNStage) & 1u);
-            const uint8_t* base = smem + static_cast<size_t>(slot) * kSlotBytes;
-            const uint16_t* wb = reinterpret_cast<const uint16_t*>(base + kOffWb);
+        consume<kNWB>(smem, full, empty, s0, s1, warp, lane, [&](const uint8_t* base, unsigned b, unsigned e) {
             const BItem* items = reinterpret_cast<const BItem*>(base + kOffDesc);
-            const unsigned b = wb[warp], e = wb[warp + 1];
             for (unsigned i = b; i < e; ++i) b_item(p, items[i], base, lane, acc);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[slot]);
-        }
+        });
     }
     __syncthreads();  // ring drained: reuse it for the cross-warp reduction
     double* red = reinterpret_cast<double*>(smem);
-    if (warp < kNW) {
+    if (warp < kNWB) {
 #pragma unroll
         for (int g = 0; g < kG; ++g) red[warp * kR + 32 * g + lane] = acc[g];
     }
     __syncthreads();
     const uint32_t r0 = p.row_begin + blk * kR;
     const uint32_t nrows = min(static_cast<uint32_t>(kR), p.row_end - r0);
-    for (uint32_t r = tid; r < nrows; r += kThreads) {
+    for (uint32_t q = tid; q < nrows; q += kThreadsB) {
         double sum = 0.0;
 #pragma unroll
-        for (int wv = 0; wv < kNW; ++wv) sum += red[wv * kR + r];
-        double* yp = p.y + r0 + r;
+        for (int wv = 0; wv < kNWB; ++wv) sum += red[wv * kR + q];
+        double* yp = p.y + r0 + q;
         *yp = p.beta == 0.0 ? sum : fma(p.beta, *yp, sum);
     }
 }
@@ -672,8 +698,8 @@ using namespace hcmx_gpu;
 
 struct hcmx_hmat {
     uint64_t n_rows = 0, n_cols = 0, rb = 0, re = 0;
-    DevBuf arena, stages, stage_wb, bitems, aitems, stripe_a, stripe_b, leafa, colw, colx, coef, c, partial, xpad,
-        counter, xbuf, ybuf;
+    DevBuf arena, stages, stage_wb, stripe_a, stripe_b, bitems, aitems, leafa, colw, colx, coef, c, partial,
+        counter, xpad, xbuf, ybuf;
     uint32_t nstripe_a = 0, nblocks = 0, nlr = 0;
     hcmx_memory_report report{};
     std::vector<std::vector<SegRef>> segs;  // per buffer (export); empty if too big
@@ -719,85 +745,6 @@ void drain_timing(hcmx_hmat* h) {
     h->pending.clear();
 }
 
-
-
-// Stage packing: items are appended (data written to the arena as they come);
-// when a stage is full it is closed, its items are assigned to the kNW consumer
-// warps by LPT on their field counts, and the descriptors are emitted grouped
-// by warp (data stays where it is: word offsets are stage-relative).
-template <class Item>
-struct StagePacker {
-    std::vector<uint32_t>& arena;
-    std::vector<Stage>& stages;
-    std::vector<uint16_t>& wb;
-    std::vector<Item>& out;
-    std::vector<std::pair<Item, uint64_t>> pending;  // item, cost
-    uint64_t start = 0;
-    uint32_t coef = 0;  // staged coefficient bytes of the open stage
-    bool open = false;
-
-    StagePacker(std::vector<uint32_t>& a, std::vector<Stage>& s, std::vector<uint16_t>& w, std::vector<Item>& o)
-        : arena(a), stages(s), wb(w), out(o) {}
-
-    // reserve room for an item of `words` packed words and `cbytes` staged
-    // coefficient bytes; returns the stage-relative word offset of its data and
-    // sets *coef_off to its offset in the slot's coefficient area
-    uint32_t place(uint64_t words, uint32_t cbytes, uint32_t* coef_off) {
-        if (words * 4 > static_cast<uint64_t>(kStageBytes) || cbytes > static_cast<uint32_t>(kCoefBytes))
-            throw invalid_argument("hmat: item exceeds a stage");
-        if (open && ((arena.size() - start + words) * 4 > static_cast<uint64_t>(kStageBytes) ||
-                     coef + cbytes > static_cast<uint32_t>(kCoefBytes) || pending.size() >= kMaxItems))
-            close();
-        if (!open) {
-            while (arena.size() % 4) arena.push_back(0u);  // 16-byte aligned stages
-            start = arena.size();
-            coef = 0;
-            open = true;
-        }
-        *coef_off = coef;
-        coef += cbytes;
-        return static_cast<uint32_t>(arena.size() - start);
-    }
-    void add(const Item& it, uint64_t cost) { pending.emplace_back(it, cost); }
-    void close() {
-        if (!open) return;
-        open = false;
-        while (arena.size() % 4) arena.push_back(0u);
-        if (pending.empty()) return;
-        // LPT: biggest item first onto the least-loaded warp; keep arrival order per warp
-        std::vector<size_t> order(pending.size());
-        for (size_t i = 0; i < order.size(); ++i) order[i] = i;
-        std::stable_sort(order.begin(), order.end(),
-                         [&](size_t a, size_t b) { return pending[a].second > pending[b].second; });
-        std::vector<uint64_t> load(kNW, 0);
-        std::vector<int> owner(pending.size());
-        for (size_t i : order) {
-            const int wv = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-            owner[i] = wv;
-            load[wv] += pending[i].second + 64;
-        }
-        Stage s{};
-        s.byte_off = start * 4;
-        s.bytes = static_cast<uint32_t>((arena.size() - start) * 4);
-        s.item0 = static_cast<uint32_t>(out.size());
-        s.nitems = static_cast<uint32_t>(pending.size());
-        s.coef_bytes = coef;
-        stages.push_back(s);
-        uint16_t cnt = 0;
-        for (int wv = 0; wv < kNW; ++wv) {
-            wb.push_back(cnt);
-            for (size_t i = 0; i < pending.size(); ++i)
-                if (owner[i] == wv) {
-                    out.push_back(pending[i].first);
-                    ++cnt;
-                }
-        }
-        wb.push_back(cnt);
-        while (wb.size() % 24) wb.push_back(cnt);  // 48 bytes per stage (one bulk copy)
-        pending.clear();
-    }
-};
-
 // host-side column parameters for the decoder (see dec<MODE>)
 ColPar col_par(const hcmx_descriptor& x) {
     ColPar c{};
@@ -812,6 +759,40 @@ ColPar col_par(const hcmx_descriptor& x) {
 
 inline uint32_t r16(uint64_t x) { return static_cast<uint32_t>((x + 15) & ~uint64_t(15)); }
 
+// A run of fields of one codec buffer that an item needs (copied word aligned)
+struct Seg {
+    uint64_t buf, f0, nf;
+};
+
+// An item before placement: descriptor + the field runs it streams
+template <class Item>
+struct Spec {
+    Item it;
+    uint32_t seg0, nseg;   // range in Builder::segs
+    uint64_t words;        // packed words
+    uint32_t coef_x;       // A: x slice bytes (shareable by the chunk's items)
+    uint32_t coef_p;       // coefficient / params bytes owned by the item
+    uint64_t cost;         // fields (LPT weight)
+    uint64_t unit;         // LPT unit (A: one chunk of one leaf; B: the item)
+    uint32_t xidx, nf;     // A: x slice key
+};
+
+// split columns [0, n) into consecutive groups of <= maxcols columns and,
+// beyond the first column, <= kItemTarget packed bytes
+template <class WordsOf>
+std::vector<std::pair<uint32_t, uint32_t>> column_groups(uint32_t n, uint32_t maxcols, WordsOf words_of) {
+    std::vector<std::pair<uint32_t, uint32_t>> g;
+    uint32_t c0 = 0;
+    while (c0 < n) {
+        uint32_t c1 = c0 + 1;
+        uint64_t bytes = words_of(c0) * 4;
+        while (c1 < n && c1 - c0 < maxcols && bytes + words_of(c1) * 4 <= kItemTarget) bytes += words_of(c1++) * 4;
+        g.emplace_back(c0, c1 - c0);
+        c0 = c1;
+    }
+    return g;
+}
+
 struct Builder {
     const hcmx_hmat_desc& d;
     hcmx_hmat* h;
@@ -821,22 +802,117 @@ struct Builder {
 
     std::vector<uint32_t> arena;  // words
     std::vector<Stage> stages;
-    std::vector<uint16_t> wb;
+    std::vector<uint16_t> wb;     // 24 entries per stage
     std::vector<BItem> bitems;
     std::vector<AItem> aitems;
+    std::vector<Seg> segs;
 
     Builder(const hcmx_hmat_desc& dd, hcmx_hmat* hh) : d(dd), h(hh) {}
 
     unsigned width(uint64_t b) const { return d.desc[b].bit_width; }
+    uint64_t words_of(uint64_t b, uint64_t nf) const { return (nf * width(b) + 31) / 32; }
 
     // append the words of fields [f0, f0+nf) of buffer b (word aligned)
-    void put_fields(uint64_t b, uint64_t f0, uint64_t nf) {
-        const unsigned w = width(b);
-        const uint64_t nw = (nf * w + 31) / 32;
+    void put_fields(const Seg& s) {
+        const unsigned w = width(s.buf);
+        const uint64_t nw = (s.nf * w + 31) / 32;
         const uint64_t at = arena.size();
         arena.resize(at + nw);
-        copy_bits(blob + d.poff[b], static_cast<uint64_t>(d.plen[b]), f0 * w, nf * w, arena.data() + at);
-        if (keep_map) h->segs[b].push_back({at, static_cast<uint32_t>(f0), static_cast<uint32_t>(nf)});
+        copy_bits(blob + d.poff[s.buf], static_cast<uint64_t>(d.plen[s.buf]), s.f0 * w, s.nf * w, arena.data() + at);
+        if (keep_map) h->segs[s.buf].push_back({at, static_cast<uint32_t>(s.f0), static_cast<uint32_t>(s.nf)});
+    }
+
+    // One CTA stripe: items packed in order into CTA stages (<= kStageBytes of
+    // data, <= kMaxItems items, <= kCoefBytes staged); each closed stage's items
+    // go to the NW consumer warps by LPT on the warps' CUMULATIVE load over the
+    // stripe (so warps progress through the ring at the same pace), and the
+    // descriptors are emitted grouped by warp.  Phase-A items of one chunk in a
+    // stage share one staged x slice.
+    template <class Item, int NW>
+    void emit_stripe(std::vector<Spec<Item>>& specs, std::vector<Item>& items) {
+        constexpr bool IS_A = std::is_same<Item, AItem>::value;
+        std::vector<uint64_t> load(NW, 0);
+        std::vector<std::pair<Item, uint64_t>> pending;
+        bool open = false;
+        uint64_t start = 0;
+        uint32_t coef = 0;
+        uint32_t x_idx = 0xffffffffu, x_nf = 0, x_at = 0;
+        auto close = [&]() {
+            if (!open) return;
+            open = false;
+            while (arena.size() % 4) arena.push_back(0u);
+            if (pending.empty()) return;
+            std::vector<size_t> order(pending.size());
+            for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+            std::stable_sort(order.begin(), order.end(),
+                             [&](size_t a, size_t b) { return pending[a].second > pending[b].second; });
+            std::vector<int> owner(pending.size());
+            for (size_t i : order) {
+                const int wv = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+                owner[i] = wv;
+                load[wv] += pending[i].second;
+            }
+            Stage st{};
+            st.byte_off = start * 4;
+            st.bytes = static_cast<uint32_t>((arena.size() - start) * 4);
+            st.item0 = static_cast<uint32_t>(items.size());
+            st.nitems = static_cast<uint32_t>(pending.size());
+            st.coef_bytes = coef;
+            stages.push_back(st);
+            uint16_t cnt = 0;
+            for (int wv = 0; wv < NW; ++wv) {
+                wb.push_back(cnt);
+                for (size_t i = 0; i < pending.size(); ++i)
+                    if (owner[i] == wv) {
+                        items.push_back(pending[i].first);
+                        ++cnt;
+                    }
+            }
+            while (wb.size() % 24) wb.push_back(cnt);  // 48 bytes per stage (one bulk copy)
+            pending.clear();
+        };
+        for (Spec<Item>& sp : specs) {
+            if (sp.words * 4 > static_cast<uint64_t>(kStageBytes) ||
+                sp.coef_x + sp.coef_p > static_cast<uint32_t>(kCoefBytes))
+                throw invalid_argument("hmat: item exceeds a stage");
+            bool shared = IS_A && open && x_idx == sp.xidx && sp.nf <= x_nf;
+            const uint32_t need = (shared ? 0u : sp.coef_x) + sp.coef_p;
+            if (open && ((arena.size() - start + sp.words) * 4 > static_cast<uint64_t>(kStageBytes) ||
+                         coef + need > static_cast<uint32_t>(kCoefBytes) || pending.size() >= kMaxItems)) {
+                close();
+                shared = false;
+            }
+            if (!open) {
+                while (arena.size() % 4) arena.push_back(0u);  // 16-byte aligned stages
+                start = arena.size();
+                coef = 0;
+                x_idx = 0xffffffffu;
+                open = true;
+            }
+            Item it = sp.it;
+            it.word_off = static_cast<uint32_t>(arena.size() - start);
+            if constexpr (IS_A) {
+                if (shared) {
+                    it.owns_x = 0;
+                    it.x_off = x_at;
+                } else {
+                    it.owns_x = 1;
+                    it.x_off = coef;
+                    x_at = coef;
+                    x_idx = sp.xidx;
+                    x_nf = sp.nf;
+                    coef += sp.coef_x;
+                }
+                it.par_off = coef;
+                coef += sp.coef_p;
+            } else {
+                it.coef_off = coef;
+                coef += sp.coef_p;
+            }
+            for (uint32_t k = 0; k < sp.nseg; ++k) put_fields(segs[sp.seg0 + k]);
+            pending.emplace_back(it, sp.cost + 64);
+        }
+        close();
     }
 };
 
@@ -875,8 +951,6 @@ void validate(const hcmx_hmat_desc& d) {
             throw corrupt_buffer("bitstream: payload ends inside a value");
     }
 }
-
-
 
 void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     validate(d);
@@ -963,41 +1037,62 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         coef.push_back(0.0);
     }
 
-    // ---- phase A: items (leaf, <= 256 columns of the block, <= 16 rank columns)
+    // ---- phase A: items (leaf, <= 128 columns of the block, <= 4 rank columns),
+    // stripes of ~kAStripeBytes, one chunk (all its rank-column groups) per warp
+    uint32_t nstripe_a = 0;
     std::vector<uint32_t> stripe_a = {0};
     {
-        StagePacker<AItem> P(B.arena, B.stages, B.wb, B.aitems);
+        std::vector<Spec<AItem>> specs;
+        uint64_t stripe_bytes = 0, unit = 0;
+        auto flush = [&]() {
+            if (specs.empty()) return;
+            B.emit_stripe<AItem, kNWA>(specs, B.aitems);
+            stripe_a.push_back(static_cast<uint32_t>(B.stages.size()));
+            ++nstripe_a;
+            specs.clear();
+            stripe_bytes = 0;
+        };
         for (uint64_t l : leaves) {
             if (d.kind[l] != 1) continue;
             const LeafA& L = leafa[lr_id[l]];
             const int64_t cols = d.col1[l] - d.col0[l];
-            for (uint32_t ch = 0; ch < L.nchunks; ++ch) {
+            LeafA& Lw = leafa[lr_id[l]];
+            Lw.nitems = 0;
+            for (uint32_t ch = 0; ch < L.nchunks; ++ch, ++unit) {
                 const uint64_t f0 = static_cast<uint64_t>(ch) * kAChunk;
                 const uint64_t nf = std::min<uint64_t>(kAChunk, cols - f0);
-                for (uint32_t g = 0; g < L.k; g += kAGroup) {
-                    const uint32_t ng = std::min<uint32_t>(kAGroup, L.k - g);
-                    uint64_t words = 0;
-                    for (uint32_t i = g; i < g + ng; ++i) words += (nf * B.width(d.buf0[l] + L.k + i) + 31) / 32;
-                    const size_t nst = B.stages.size();
-                    AItem it{};
-                    it.xidx = static_cast<uint32_t>(d.col0[l] + f0);
-                    it.shift = it.xidx & 1u;
-                    it.word_off = P.place(words, r16((nf + it.shift) * 8) + ng * 16, &it.coef_off);
-                    if (B.stages.size() != nst && B.stages.size() - stripe_a.back() >= kAStagesPerStripe)
-                        stripe_a.push_back(static_cast<uint32_t>(B.stages.size()));
+                const auto groups = column_groups(L.k, kAGroup, [&](uint32_t i) { return B.words_of(d.buf0[l] + L.k + i, nf); });
+                Lw.nitems += static_cast<uint32_t>(groups.size());
+                for (const auto& gr : groups) {
+                    const uint32_t g = gr.first, ng = gr.second;
+                    Spec<AItem> sp{};
+                    sp.seg0 = static_cast<uint32_t>(B.segs.size());
+                    sp.nseg = ng;
+                    for (uint32_t i = g; i < g + ng; ++i) {
+                        B.segs.push_back({static_cast<uint64_t>(d.buf0[l] + L.k + i), f0, nf});
+                        sp.words += B.words_of(d.buf0[l] + L.k + i, nf);
+                    }
+                    AItem& it = sp.it;
                     it.nseg = static_cast<uint8_t>(ng);
                     it.nf = static_cast<uint16_t>(nf);
+                    it.xidx = static_cast<uint32_t>(d.col0[l] + f0);
                     it.xcol = L.colbase + g;
                     it.leaf = static_cast<uint32_t>(lr_id[l]);
                     it.chunk = static_cast<uint16_t>(ch);
                     it.icol0 = static_cast<uint16_t>(g);
-                    for (uint32_t i = g; i < g + ng; ++i) B.put_fields(d.buf0[l] + L.k + i, f0, nf);
-                    P.add(it, nf * ng);
+                    sp.coef_x = r16((nf + (it.xidx & 1u)) * 8);
+                    sp.coef_p = ng * 16;
+                    sp.cost = nf * ng;
+                    sp.unit = unit;
+                    sp.xidx = it.xidx;
+                    sp.nf = static_cast<uint32_t>(nf);
+                    stripe_bytes += sp.words * 4;
+                    specs.push_back(sp);
                 }
+                if (stripe_bytes >= kAStripeBytes) flush();
             }
         }
-        P.close();
-        if (stripe_a.back() != B.stages.size()) stripe_a.push_back(static_cast<uint32_t>(B.stages.size()));
+        flush();
     }
     rep.stages_a = B.stages.size();
 
@@ -1009,54 +1104,77 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         const uint64_t b = std::min<uint64_t>(d.row1[l], h->re) - h->rb;
         for (uint64_t blk = a / kR; blk * kR < b; ++blk) block_leaves[blk].push_back(static_cast<uint32_t>(l));
     }
+    const size_t b_ws0 = B.stages.size();
     std::vector<uint32_t> stripe_b = {static_cast<uint32_t>(B.stages.size())};
-    for (uint64_t blk = 0; blk < nblocks; ++blk) {
-        StagePacker<BItem> P(B.arena, B.stages, B.wb, B.bitems);
-        const uint64_t b0 = h->rb + blk * kR, b1 = std::min<uint64_t>(b0 + kR, h->re);
-        for (uint32_t l : block_leaves[blk]) {
-            const int64_t rows = d.row1[l] - d.row0[l], cols = d.col1[l] - d.col0[l];
-            const uint64_t r0 = std::max<uint64_t>(d.row0[l], b0), r1 = std::min<uint64_t>(d.row1[l], b1);
-            const uint64_t nr = r1 - r0, roff = r0 - d.row0[l];
-            if (d.kind[l] == 0) {
-                const uint64_t b = d.buf0[l];
-                const unsigned w = B.width(b);
-                for (int64_t c0 = 0; c0 < cols; c0 += kBDenseGroup) {
-                    const uint32_t nc = static_cast<uint32_t>(std::min<int64_t>(kBDenseGroup, cols - c0));
-                    BItem it{};
-                    it.src = static_cast<uint32_t>(d.col0[l] + c0);
-                    it.shift = it.src & 1u;
-                    it.word_off = P.place(nc * ((nr * w + 31) / 32), r16((nc + it.shift) * 8), &it.coef_off);
-                    it.nseg = static_cast<uint8_t>(nc);
-                    it.kind = 0;
-                    it.ra = static_cast<uint8_t>(r0 - b0);
-                    it.nr = static_cast<uint8_t>(nr);
-                    it.par = col_par(d.desc[b]);
-                    it.scale = d.desc[b].scale;
-                    for (uint32_t c = 0; c < nc; ++c) B.put_fields(b, (c0 + c) * rows + roff, nr);
-                    P.add(it, nc * nr);
-                }
-            } else {
-                const LeafA& L = leafa[lr_id[l]];
-                for (uint32_t g = 0; g < L.k; g += kBLRGroup) {
-                    const uint32_t ng = std::min<uint32_t>(kBLRGroup, L.k - g);
-                    uint64_t words = 0;
-                    for (uint32_t i = g; i < g + ng; ++i) words += (nr * B.width(d.buf0[l] + i) + 31) / 32;
-                    BItem it{};
-                    it.word_off = P.place(words, r16(ng * 8) + ng * 16, &it.coef_off);
-                    it.nseg = static_cast<uint8_t>(ng);
-                    it.kind = 1;
-                    it.ra = static_cast<uint8_t>(r0 - b0);
-                    it.nr = static_cast<uint8_t>(nr);
-                    it.src = L.colbase + g;
-                    for (uint32_t i = g; i < g + ng; ++i) B.put_fields(d.buf0[l] + i, roff, nr);
-                    P.add(it, ng * nr);
+    {
+        std::vector<Spec<BItem>> specs;
+        uint64_t unit = 0;
+        for (uint64_t blk = 0; blk < nblocks; ++blk) {
+            specs.clear();
+            const uint64_t b0 = h->rb + blk * kR, b1 = std::min<uint64_t>(b0 + kR, h->re);
+            for (uint32_t l : block_leaves[blk]) {
+                const int64_t rows = d.row1[l] - d.row0[l], cols = d.col1[l] - d.col0[l];
+                const uint64_t r0 = std::max<uint64_t>(d.row0[l], b0), r1 = std::min<uint64_t>(d.row1[l], b1);
+                const uint64_t nr = r1 - r0, roff = r0 - d.row0[l];
+                if (d.kind[l] == 0) {
+                    const uint64_t b = d.buf0[l];
+                    const auto groups = column_groups(static_cast<uint32_t>(cols), kBDenseGroup,
+                                                      [&](uint32_t) { return B.words_of(b, nr); });
+                    for (const auto& gr : groups) {
+                        const int64_t c0 = gr.first;
+                        const uint32_t nc = gr.second;
+                        Spec<BItem> sp{};
+                        sp.seg0 = static_cast<uint32_t>(B.segs.size());
+                        sp.nseg = nc;
+                        for (uint32_t c = 0; c < nc; ++c) {
+                            B.segs.push_back({b, static_cast<uint64_t>((c0 + c) * rows + roff), nr});
+                            sp.words += B.words_of(b, nr);
+                        }
+                        BItem& it = sp.it;
+                        it.src = static_cast<uint32_t>(d.col0[l] + c0);
+                        it.nseg = static_cast<uint8_t>(nc);
+                        it.kind = 0;
+                        it.ra = static_cast<uint8_t>(r0 - b0);
+                        it.nr = static_cast<uint8_t>(nr);
+                        it.dpacked = col_par(d.desc[b]).packed;
+                        it.scale = d.desc[b].scale;
+                        sp.coef_p = r16((nc + (it.src & 1u)) * 8);
+                        sp.cost = nc * nr;
+                        sp.unit = unit++;
+                        specs.push_back(sp);
+                    }
+                } else {
+                    const LeafA& L = leafa[lr_id[l]];
+                    const auto groups = column_groups(L.k, kBLRGroup, [&](uint32_t i) { return B.words_of(d.buf0[l] + i, nr); });
+                    for (const auto& gr : groups) {
+                        const uint32_t g = gr.first, ng = gr.second;
+                        Spec<BItem> sp{};
+                        sp.seg0 = static_cast<uint32_t>(B.segs.size());
+                        sp.nseg = ng;
+                        for (uint32_t i = g; i < g + ng; ++i) {
+                            B.segs.push_back({static_cast<uint64_t>(d.buf0[l] + i), roff, nr});
+                            sp.words += B.words_of(d.buf0[l] + i, nr);
+                        }
+                        BItem& it = sp.it;
+                        it.nseg = static_cast<uint8_t>(ng);
+                        it.kind = 1;
+                        it.ra = static_cast<uint8_t>(r0 - b0);
+                        it.nr = static_cast<uint8_t>(nr);
+                        it.src = L.colbase + g;
+                        sp.coef_p = r16((ng + (it.src & 1u)) * 8) + ng * 16;
+                        sp.cost = ng * nr;
+                        sp.unit = unit++;
+                        specs.push_back(sp);
+                    }
                 }
             }
+            B.emit_stripe<BItem, kNWB>(specs, B.bitems);
+            stripe_b.push_back(static_cast<uint32_t>(B.stages.size()));
         }
-        P.close();
-        stripe_b.push_back(static_cast<uint32_t>(B.stages.size()));
     }
-    rep.stages_b = B.stages.size() - rep.stages_a;
+    rep.stages_b = B.stages.size() - b_ws0;
+    B.segs.clear();
+    B.segs.shrink_to_fit();
     while (B.arena.size() % 4) B.arena.push_back(0u);
     B.arena.resize(B.arena.size() + 8, 0u);  // tail slack
     if (B.stages.size() >= (1ull << 31)) throw invalid_argument("hmat: too many stages");
@@ -1070,40 +1188,40 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     up(h->arena, B.arena.data(), B.arena.size() * 4);
     up(h->stages, B.stages.data(), B.stages.size() * sizeof(Stage));
     up(h->stage_wb, B.wb.data(), B.wb.size() * sizeof(uint16_t));
-    up(h->bitems, B.bitems.data(), B.bitems.size() * sizeof(BItem));
-    up(h->aitems, B.aitems.data(), B.aitems.size() * sizeof(AItem));
     up(h->stripe_a, stripe_a.data(), stripe_a.size() * 4);
     up(h->stripe_b, stripe_b.data(), stripe_b.size() * 4);
+    up(h->bitems, B.bitems.data(), B.bitems.size() * sizeof(BItem));
+    up(h->aitems, B.aitems.data(), B.aitems.size() * sizeof(AItem));
     up(h->leafa, leafa.data(), leafa.size() * sizeof(LeafA));
     up(h->colw, colw.data(), colw.size() * sizeof(ColPar));
     up(h->colx, colx.data(), colx.size() * sizeof(ColPar));
+    up(h->coef, coef.data(), coef.size() * 8);
     h->xpad.alloc((d.n_cols + 4) * 8);
     check_cuda(cudaMemsetAsync(h->xpad.p, 0, h->xpad.bytes, s), "memset");
-    up(h->coef, coef.data(), coef.size() * 8);
     h->c.alloc(std::max<size_t>(16, coef.size() * 8));
     check_cuda(cudaMemsetAsync(h->c.p, 0, h->c.bytes, s), "memset");
     h->partial.alloc(std::max<size_t>(16, npartial * 8));
     h->counter.alloc(std::max<size_t>(16, leafa.size() * 4));
     check_cuda(cudaMemsetAsync(h->counter.p, 0, h->counter.bytes, s), "memset");
     stream_sync(s);
-    h->nstripe_a = static_cast<uint32_t>(stripe_a.size() - 1);
+    h->nstripe_a = nstripe_a;
     h->nblocks = static_cast<uint32_t>(nblocks);
     rep.device_arena_bytes = B.arena.size() * 4;
-    rep.device_table_bytes = B.stages.size() * sizeof(Stage) + B.wb.size() * 2 + B.bitems.size() * sizeof(BItem) +
-                             B.aitems.size() * sizeof(AItem) + leafa.size() * sizeof(LeafA) + colw.size() * 2 * sizeof(ColPar) +
-                             coef.size() * 16;
+    rep.device_table_bytes = B.stages.size() * (sizeof(Stage) + 48) + B.bitems.size() * sizeof(BItem) +
+                             B.aitems.size() * sizeof(AItem) + leafa.size() * sizeof(LeafA) +
+                             colw.size() * 2 * sizeof(ColPar) + coef.size() * 16;
     rep.overhead = rep.device_table_bytes;
 }
 
-Params make_params(hcmx_hmat* h, double alpha, const double* x, double beta, double* y) {
+Params make_params(hcmx_hmat* h, double alpha, double beta, double* y) {
     Params p{};
     p.arena = h->arena.as<uint8_t>();
     p.stages = h->stages.as<Stage>();
     p.stage_wb = h->stage_wb.as<uint16_t>();
-    p.bitems = h->bitems.as<BItem>();
-    p.aitems = h->aitems.as<AItem>();
     p.stripe_a = h->stripe_a.as<uint32_t>();
     p.stripe_b = h->stripe_b.as<uint32_t>();
+    p.bitems = h->bitems.as<BItem>();
+    p.aitems = h->aitems.as<AItem>();
     p.leafa = h->leafa.as<LeafA>();
     p.colw_par = h->colw.as<ColPar>();
     p.colx_par = h->colx.as<ColPar>();
@@ -1112,7 +1230,6 @@ Params make_params(hcmx_hmat* h, double alpha, const double* x, double beta, dou
     p.partial = h->partial.as<double>();
     p.counter = h->counter.as<unsigned>();
     p.x = h->xpad.as<double>();  // padded, 16-byte aligned copy of x (bulk copies)
-    (void)x;
     p.y = y;
     p.row_begin = static_cast<uint32_t>(h->rb);
     p.row_end = static_cast<uint32_t>(h->re);
@@ -1139,19 +1256,19 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
         return;
     }
     check_cuda(cudaMemcpyAsync(h->xpad.p, dx, h->n_cols * 8, cudaMemcpyDeviceToDevice, s), "x copy");
-    Params p = make_params(h, alpha, dx, beta, dy);
+    Params p = make_params(h, alpha, beta, dy);
     hcmx_hmat::Rec rec{};
     if (h->timing) {
         rec = {take_event(h), take_event(h), take_event(h)};
         check_cuda(cudaEventRecord(rec.a0, s), "event");
     }
     if (h->nlr && h->nstripe_a) {
-        k_phase_a<<<h->nstripe_a, kThreads, kSmemBytes, s>>>(p);
+        k_phase_a<<<h->nstripe_a, kThreadsA, kSmemBytes, s>>>(p);
         h->last_launches++;
     }
     if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
     if (h->nblocks) {
-        k_phase_b<<<h->nblocks, kThreads, kSmemBytes, s>>>(p);
+        k_phase_b<<<h->nblocks, kThreadsB, kSmemBytes, s>>>(p);
         h->last_launches++;
     }
     check_cuda(cudaGetLastError(), "matvec launch");
