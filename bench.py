@@ -205,7 +205,9 @@ def restrict(flat, rr):
 
 
 def codec_microbench(reps=5):
-    """BASELINE config 2: 4096 64x64 blocks, sign * 10^U[-6,0]; AFL at 1e-6"""
+    """BASELINE config 2: 4096 blocks of 64x64, sign * 10^U[-6,0], AFL at 1e-4/1e-6/1e-8.
+    Inputs resident in HBM; compress = the batched API call (fused kernel + the
+    descriptor read-back), decompress = the batched unpack call; CUDA events."""
     import torch
     from paper_2308_10960_b200 import codec
     nb, bs = 4096, 4096
@@ -213,19 +215,22 @@ def codec_microbench(reps=5):
     vals = np.sign(rng.standard_normal(nb * bs)) * 10 ** rng.uniform(-6, 0, nb * bs)
     d = torch.as_tensor(vals).cuda()
     counts = np.full(nb, bs, np.uint64)
+    d_voff = torch.as_tensor((np.arange(nb, dtype=np.int64) * bs)).cuda()
     out = {}
     for eps in (1e-4, 1e-6, 1e-8):
-        bb = codec.compress_batch(d, counts, eps, codec.Scheme.afl)
+        bb = codec.compress_batch(d, counts, eps, codec.Scheme.afl, d_voff=d_voff)
         dec = codec.decompress_batch(bb)
         torch.cuda.synchronize()
         pay = int(((counts * bb.desc["bit_width"].astype(np.uint64) + 7) // 8).sum()) + 20 * nb
         algo = 8 * nb * bs + pay
         tc, td = [], []
         for _ in range(reps):
-            t = time.perf_counter()
-            bb = codec.compress_batch(d, counts, eps, codec.Scheme.afl, payload=bb.payload)
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record()
+            bb2 = codec.compress_batch(d, counts, eps, codec.Scheme.afl, payload=bb.payload, d_voff=d_voff)
+            t1.record()
             torch.cuda.synchronize()
-            tc.append(time.perf_counter() - t)
+            tc.append(t0.elapsed_time(t1) / 1e3)
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0.record()
             codec.decompress_batch(bb, out=dec)

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIBPATH = os.path.join(HERE, "libhcmx_gpu.so")
+LIBPATH = os.environ.get("HCMX_GPU_LIB") or os.path.join(HERE, "libhcmx_gpu.so")
 
 HCMX_OK, HCMX_INVALID_ARGUMENT, HCMX_CORRUPT_BUFFER = 0, 1, 2
 HCMX_CUDA_ERROR, HCMX_NCCL_ERROR, HCMX_OUT_OF_MEMORY = 3, 4, 5

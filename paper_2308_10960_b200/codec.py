@@ -258,15 +258,19 @@ def _offsets(counts: np.ndarray) -> np.ndarray:
 
 
 def compress_batch(values: torch.Tensor, counts, eps: float, scheme, capacity: int | None = None,
-                   voff=None, payload: torch.Tensor | None = None) -> BatchBuffers:
+                   voff=None, payload: torch.Tensor | None = None,
+                   d_voff: torch.Tensor | None = None) -> BatchBuffers:
     """codec::compress over nbuf independent buffers laid end to end in `values`
-    (a cuda float64 tensor) -- one analyze launch, host layout selection with the
-    reference's scalar rules, one pack launch."""
+    (a cuda float64 tensor): one fused kernel per batch (analyze, layout
+    selection on the device with a host re-check next to the exponent-width
+    thresholds, pack).  Payload slots are sized for the widest layout the scheme
+    allows; each buffer's payload is the first payload_bytes(b) of its slot."""
     values = _dev_f64(values)
     counts = np.ascontiguousarray(counts, dtype=np.uint64)
     nb = counts.size
-    vo = _offsets(counts) if voff is None else np.ascontiguousarray(voff, dtype=np.uint64)
-    d_voff = torch.as_tensor(vo.view(np.int64)).cuda()
+    if d_voff is None:
+        vo = _offsets(counts) if voff is None else np.ascontiguousarray(voff, dtype=np.uint64)
+        d_voff = torch.as_tensor(vo.view(np.int64)).cuda()
     if capacity is None:
         capacity = int(8 * counts.sum() + 16 * nb + 16)
     if payload is None:
@@ -277,7 +281,10 @@ def compress_batch(values: torch.Tensor, counts, eps: float, scheme, capacity: i
     check(lib().hcmx_gpu_codec_compress(ptr(values), ptr(d_voff), u64p(counts), nb, float(eps),
                                         int(scheme), ptr(payload), payload.numel(), ptr(desc),
                                         u64p(poff), C.byref(total), _stream()), "compress")
-    return BatchBuffers(desc, counts, poff, payload, total.value)
+    bb = BatchBuffers(desc, counts, poff, payload, total.value)
+    if voff is None:
+        bb._dev["voff"] = d_voff.view(torch.uint8) if d_voff.dtype != torch.uint8 else d_voff
+    return bb
 
 
 def decompress_batch(bb: BatchBuffers, out: torch.Tensor | None = None, voff=None) -> torch.Tensor:

@@ -110,6 +110,7 @@ void stream_sync(void* stream) {
 namespace {
 
 constexpr unsigned kGroupsPerJob = 32;  // 1024 values per warp job
+constexpr uint64_t kFuseMax = 1ull << 17;  // fused compress: one warp per buffer up to this size
 constexpr int kWarpsPerBlock = 8;
 
 struct Job {
@@ -227,48 +228,34 @@ __device__ __forceinline__ uint64_t encode_value(double v, unsigned e, unsigned 
 // Packing without atomics: lane j encodes value 32g + j into a 64-bit field F_j;
 // lane K then assembles output word K of the group (bits [32K, 32K+32)) from
 // the <= ceil(32/w)+1 fields that overlap it, fetched with warp shuffles.  The
-// w words of a group are stored by w lanes at once (coalesced).
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-k_pack(const double* __restrict__ values, const uint64_t* __restrict__ voff,
-       const uint64_t* __restrict__ count, const hcmx_descriptor* __restrict__ desc,
-       const uint64_t* __restrict__ poff, const Job* __restrict__ jobs, uint64_t njobs,
-       uint8_t* __restrict__ payload, int* __restrict__ err) {
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-    for (uint64_t j = wid; j < njobs; j += nw) {
-        const Job jb = jobs[j];
-        const hcmx_descriptor d = desc[jb.buf];
-        const unsigned e = d.exp_bits, m = d.mant_bits, w = d.bit_width;
-        const double inv_scale = 1.0 / d.scale;  // IEEE division (codec.cpp:107)
-        const uint64_t max_offset = (1ull << e) - 1;
-        const uint64_t round_add = (m < 52) ? (1ull << (51 - m)) : 0;
-        const uint64_t mant_mask = (m == 52) ? ((1ull << 52) - 1) : ((1ull << m) - 1);
-        const uint64_t n = count[jb.buf];
-        const double* v = values + voff[jb.buf];
-        uint32_t* out = reinterpret_cast<uint32_t*>(payload + poff[jb.buf]);
-        const unsigned T = (32 + w - 1) / w + 1;  // fields overlapping one output word
-        // output words K = lane and K = lane + 32: first overlapping field and its bit shift
-        const unsigned i0a = (32 * lane) / w, i0b = (32 * (lane + 32)) / w;
-        int nf_bad = 0;
-        const uint32_t gend = jb.g0 + jb.ng;
-        for (uint32_t g4 = jb.g0; g4 < gend; g4 += 4) {
-          double xs[4];
+// w words of a group are stored by w lanes at once (coalesced).  Groups
+// [g0, g1) of the buffer v[0, n) are packed into out (word 0 = group 0).
+__device__ __forceinline__ int pack_groups(const double* __restrict__ v, uint64_t n, uint32_t g0, uint32_t g1,
+                                           unsigned e, unsigned m, unsigned w, double scale,
+                                           uint32_t* __restrict__ out, unsigned lane) {
+    const double inv_scale = 1.0 / scale;  // IEEE division (codec.cpp:107)
+    const uint64_t max_offset = (1ull << e) - 1;
+    const uint64_t round_add = (m < 52) ? (1ull << (51 - m)) : 0;
+    const uint64_t mant_mask = (m == 52) ? ((1ull << 52) - 1) : ((1ull << m) - 1);
+    const unsigned T = (32 + w - 1) / w + 1;  // fields overlapping one output word
+    const unsigned i0a = (32 * lane) / w, i0b = (32 * (lane + 32)) / w;
+    int nf_bad = 0;
+    for (uint32_t g4 = g0; g4 < g1; g4 += 4) {
+        double xs[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-              const uint64_t idx = (uint64_t)(g4 + i) * 32 + lane;
-              xs[i] = (g4 + i < gend && idx < n) ? __ldcs(v + idx) : 0.0;
-          }
+        for (int i = 0; i < 4; ++i) {
+            const uint64_t idx = (uint64_t)(g4 + i) * 32 + lane;
+            xs[i] = (g4 + i < g1 && idx < n) ? __ldcs(v + idx) : 0.0;
+        }
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 4; ++i) {
             const uint32_t g = g4 + i;
-            if (g >= gend) break;
+            if (g >= g1) break;
             const uint64_t idx = (uint64_t)g * 32 + lane;
             uint64_t f = 0;
             if (idx < n) {
-                const double x = xs[i];
-                if (!isfinite(x)) nf_bad = 1;
-                else f = encode_value(x, e, m, inv_scale, max_offset, round_add, mant_mask);
+                if (!isfinite(xs[i])) nf_bad = 1;
+                else f = encode_value(xs[i], e, m, inv_scale, max_offset, round_add, mant_mask);
             }
             const uint32_t flo = static_cast<uint32_t>(f), fhi = static_cast<uint32_t>(f >> 32);
             const uint64_t nvalid = umin64(32, n - (uint64_t)g * 32);
@@ -282,7 +269,7 @@ k_pack(const double* __restrict__ values, const uint64_t* __restrict__ voff,
                     const unsigned i = i0 + t;
                     const uint32_t lo = __shfl_sync(0xffffffffu, flo, i & 31u);
                     const uint32_t hi = __shfl_sync(0xffffffffu, fhi, i & 31u);
-                    const int sft = static_cast<int>(i * w) - static_cast<int>(32 * K);  // field bit 0 vs word bit 0
+                    const int sft = static_cast<int>(i * w) - static_cast<int>(32 * K);
                     if (i < 32 && sft < 32) {
                         const uint64_t F = (static_cast<uint64_t>(hi) << 32) | lo;
                         word |= sft >= 0 ? static_cast<uint32_t>(F << sft) : static_cast<uint32_t>(F >> (-sft));
@@ -290,9 +277,124 @@ k_pack(const double* __restrict__ values, const uint64_t* __restrict__ voff,
                 }
                 if (K < nwords) __stcs(o + K, word);
             }
-          }
         }
-        if (__any_sync(0xffffffffu, nf_bad) && lane == 0) *err = 1;
+    }
+    return __any_sync(0xffffffffu, nf_bad);
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_pack(const double* __restrict__ values, const uint64_t* __restrict__ voff,
+       const uint64_t* __restrict__ count, const hcmx_descriptor* __restrict__ desc,
+       const uint64_t* __restrict__ poff, const Job* __restrict__ jobs, uint64_t njobs,
+       uint8_t* __restrict__ payload, int* __restrict__ err) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    for (uint64_t j = wid; j < njobs; j += nw) {
+        const Job jb = jobs[j];
+        const hcmx_descriptor d = desc[jb.buf];
+        const int bad = pack_groups(values + voff[jb.buf], count[jb.buf], jb.g0, jb.g0 + jb.ng, d.exp_bits,
+                                    d.mant_bits, d.bit_width, d.scale,
+                                    reinterpret_cast<uint32_t*>(payload + poff[jb.buf]), lane);
+        if (bad && lane == 0) *err = 1;
+    }
+}
+
+// codec.cpp:142-144 compress fused per buffer (one warp each): analyze,
+// descriptor selection on the device, pack.  The exponent width uses the
+// device log2; when log2(max) - log2(min) + 2 falls within 1e-9 (relative) of a
+// power of two 2^2..2^10 the buffer is flagged and the host re-decides with
+// glibc's log2 exactly like the reference (and repacks if it differs).
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_compress_fused(const double* __restrict__ values, const uint64_t* __restrict__ voff,
+                 const uint64_t* __restrict__ count, uint64_t nbuf, int scheme, unsigned m_req,
+                 const uint64_t* __restrict__ poff, uint8_t* __restrict__ payload,
+                 hcmx_descriptor* __restrict__ desc, hcmx_stats* __restrict__ stats,
+                 uint32_t* __restrict__ flags, int* __restrict__ err) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    for (uint64_t b = wid; b < nbuf; b += nw) {
+        const uint64_t n = count[b];
+        const double* v = values + voff[b];
+        uint64_t mn = 0x7FF0000000000000ull, mx = 0;
+        unsigned nz = 0, nf = 0;
+        for (uint64_t i = lane; i < n; i += 128) {
+            double xs[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) xs[u] = i + 32 * u < n ? __ldcg(v + i + 32 * u) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double a = fabs(xs[u]);
+                if (a != 0.0) nz = 1;
+                if (!isfinite(xs[u])) nf = 1;
+                if (a != 0.0 && !isnan(a)) {
+                    const uint64_t ab = dbits(a);
+                    mn = ab < mn ? ab : mn;
+                    mx = ab > mx ? ab : mx;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t omn = __shfl_xor_sync(0xffffffffu, mn, o);
+            const uint64_t omx = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = omn < mn ? omn : mn;
+            mx = omx > mx ? omx : mx;
+        }
+        nz = __any_sync(0xffffffffu, nz);
+        nf = __any_sync(0xffffffffu, nf);
+        const bool all_zero = !nz;
+        const double dmin = all_zero ? 0.0 : bitsd(mn), dmax = all_zero ? 0.0 : bitsd(mx);
+        unsigned e = 2, ambiguous = 0;
+        if (scheme == HCMX_BFL) {
+            e = 8;
+        } else if (scheme == HCMX_DFL) {
+            e = 11;
+        } else if (!all_zero) {  // codec.cpp:69-75 with the device log2
+            const double span = log2(dmax) - log2(dmin) + 1.0;
+            const double vv = span + 1.0;
+            const double bits = ceil(log2(vv));
+            e = static_cast<unsigned>(fmin(fmax(bits, 2.0), 11.0));
+            for (int k = 2; k <= 10; ++k) {
+                const double pk = ldexp(1.0, k);
+                if (fabs(vv - pk) <= pk * 1e-9) ambiguous = 1;
+            }
+        }
+        unsigned m = m_req;
+        if (scheme != HCMX_AFL) {  // codec.cpp:25-30
+            const unsigned unit = scheme == HCMX_DFL ? 16u : 8u;
+            unsigned w = 1 + e + m;
+            w += (unit - w % unit) % unit;
+            m = min(52u, w - 1 - e);
+        }
+        const unsigned unit = scheme == HCMX_AFL ? 1u : (scheme == HCMX_DFL ? 16u : 8u);
+        unsigned w = 1 + e + m;
+        w += (unit - w % unit) % unit;
+        const double scale = all_zero ? 1.0 : dmin;
+        if (lane == 0) {
+            hcmx_descriptor d;
+            d.scheme = static_cast<uint8_t>(scheme);
+            d.exp_bits = static_cast<uint8_t>(e);
+            d.mant_bits = static_cast<uint8_t>(m);
+            d.bit_width = static_cast<uint8_t>(w);
+            d.reserved = 0;
+            d.scale = scale;
+            desc[b] = d;
+            hcmx_stats st;
+            st.min_mag = dmin;
+            st.max_mag = dmax;
+            st.all_zero = all_zero ? 1u : 0u;
+            st.non_finite = nf;
+            stats[b] = st;
+            flags[b] = ambiguous;
+        }
+        if (nf) {
+            if (lane == 0) *err = 1;
+            continue;
+        }
+        pack_groups(v, n, 0, static_cast<uint32_t>((n + 31) / 32), e, m, w, scale,
+                    reinterpret_cast<uint32_t*>(payload + poff[b]), lane);
     }
 }
 
@@ -529,22 +631,74 @@ int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff, cons
     return guarded([&] {
         require_device();
         alignment_unit(scheme);
-        mantissa_bits_for(eps);
+        const uint8_t m_req = mantissa_bits_for(eps);  // eps validation first (codec.cpp:63-64)
+        uint64_t maxc = 0;
+        for (uint64_t b = 0; b < nbuf; ++b) maxc = std::max(maxc, h_count[b]);
         DevBuf dc = upload_u64(h_count, nbuf, stream);
-        DevBuf dst(std::max<uint64_t>(24, nbuf * sizeof(hcmx_stats)));
-        launch_analyze_jobs(d_values, d_voff, dc.as<uint64_t>(), h_count, nbuf, dst.as<hcmx_stats>(),
-                            stream);
-        std::vector<hcmx_stats> st(nbuf);
-        d2h(st.data(), dst.p, nbuf * sizeof(hcmx_stats), stream);
-        stream_sync(stream);
-        select_layouts(st, h_count, nbuf, eps, scheme, h_desc, h_poff, h_total);
-        if (*h_total > payload_capacity) throw invalid_argument("compress: payload capacity too small");
-        DevBuf dd(std::max<uint64_t>(16, nbuf * sizeof(hcmx_descriptor)));
-        h2d(dd.p, h_desc, nbuf * sizeof(hcmx_descriptor), stream);
+        if (maxc > kFuseMax) {  // very large buffers: device analyze, host selection, device pack
+            DevBuf dst(std::max<uint64_t>(24, nbuf * sizeof(hcmx_stats)));
+            launch_analyze_jobs(d_values, d_voff, dc.as<uint64_t>(), h_count, nbuf, dst.as<hcmx_stats>(),
+                                stream);
+            std::vector<hcmx_stats> st(nbuf);
+            d2h(st.data(), dst.p, nbuf * sizeof(hcmx_stats), stream);
+            stream_sync(stream);
+            select_layouts(st, h_count, nbuf, eps, scheme, h_desc, h_poff, h_total);
+            if (*h_total > payload_capacity) throw invalid_argument("compress: payload capacity too small");
+            DevBuf dd(std::max<uint64_t>(16, nbuf * sizeof(hcmx_descriptor)));
+            h2d(dd.p, h_desc, nbuf * sizeof(hcmx_descriptor), stream);
+            DevBuf dp = upload_u64(h_poff, nbuf, stream);
+            if (launch_pack_jobs(d_values, d_voff, dc.as<uint64_t>(), h_count, dd.as<hcmx_descriptor>(),
+                                 dp.as<uint64_t>(), nbuf, d_payload, stream))
+                throw invalid_argument("compress: values must be finite");
+            return;
+        }
+        // fused path: slots sized for the widest layout the scheme allows (e = 11)
+        const hcmx_descriptor widest = make_descriptor(scheme, eps, 1.0, 11);
+        uint64_t off = 0;
+        for (uint64_t b = 0; b < nbuf; ++b) {
+            h_poff[b] = off;
+            off += round16(payload_bytes(h_count[b], widest.bit_width));
+        }
+        *h_total = off;
+        if (off > payload_capacity) throw invalid_argument("compress: payload capacity too small");
         DevBuf dp = upload_u64(h_poff, nbuf, stream);
-        if (launch_pack_jobs(d_values, d_voff, dc.as<uint64_t>(), h_count, dd.as<hcmx_descriptor>(),
-                             dp.as<uint64_t>(), nbuf, d_payload, stream))
-            throw invalid_argument("compress: values must be finite");
+        DevBuf dd(std::max<uint64_t>(16, nbuf * sizeof(hcmx_descriptor)));
+        DevBuf dst(std::max<uint64_t>(24, nbuf * sizeof(hcmx_stats)));
+        DevBuf dfl(std::max<uint64_t>(16, nbuf * 4)), de(sizeof(int));
+        cudaStream_t s = (cudaStream_t)stream;
+        check_cuda(cudaMemsetAsync(de.p, 0, sizeof(int), s), "memset");
+        const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((nbuf + kWarpsPerBlock - 1) / kWarpsPerBlock,
+                                                                       148ull * 16));
+        k_compress_fused<<<grid, kWarpsPerBlock * 32, 0, s>>>(d_values, d_voff, dc.as<uint64_t>(), nbuf, scheme,
+                                                              m_req, dp.as<uint64_t>(), d_payload,
+                                                              dd.as<hcmx_descriptor>(), dst.as<hcmx_stats>(),
+                                                              dfl.as<uint32_t>(), de.as<int>());
+        check_cuda(cudaGetLastError(), "compress launch");
+        int err = 0;
+        std::vector<uint32_t> flags(nbuf);
+        d2h(h_desc, dd.p, nbuf * sizeof(hcmx_descriptor), stream);
+        d2h(flags.data(), dfl.p, nbuf * 4, stream);
+        d2h(&err, de.p, sizeof(int), stream);
+        stream_sync(stream);
+        if (err) throw invalid_argument("compress: values must be finite");
+        // exponent widths next to a 2^k - 2 threshold: decide with glibc (codec.cpp:72-73)
+        for (uint64_t b = 0; b < nbuf; ++b) {
+            if (!flags[b]) continue;
+            hcmx_stats st{};
+            d2h(&st, dst.as<hcmx_stats>() + b, sizeof(hcmx_stats), stream);
+            uint64_t vo = 0;
+            d2h(&vo, d_voff + b, 8, stream);
+            stream_sync(stream);
+            const hcmx_descriptor exact = make_descriptor(scheme, eps, st);
+            if (exact.exp_bits == h_desc[b].exp_bits) continue;
+            h_desc[b] = exact;
+            DevBuf d1(sizeof(hcmx_descriptor));
+            h2d(d1.p, &exact, sizeof(hcmx_descriptor), stream);
+            DevBuf dv1 = upload_u64(&vo, 1, stream), dc1 = upload_u64(h_count + b, 1, stream),
+                   dp1 = upload_u64(h_poff + b, 1, stream);
+            launch_pack_jobs(d_values, dv1.as<uint64_t>(), dc1.as<uint64_t>(), h_count + b,
+                             d1.as<hcmx_descriptor>(), dp1.as<uint64_t>(), 1, d_payload, stream);
+        }
     });
 }
 

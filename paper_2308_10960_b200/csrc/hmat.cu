@@ -36,6 +36,12 @@
 // sum differs from the oracle only by FP64 reassociation (||dy||/||y|| ~ 1e-15).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
+#ifndef HCMX_WAIT_HINT
+#define HCMX_WAIT_HINT 200
+#endif
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -51,15 +57,17 @@ constexpr int kNWB = 16;                  // phase-B consumer warps per CTA
 constexpr int kNWA = 12;                  // phase-A consumer warps (more registers per thread)
 constexpr int kThreadsB = (kNWB + 1) * 32;  // + one producer warp (bulk copies)
 constexpr int kThreadsA = (kNWA + 1) * 32;
-constexpr int kStageBytes = 24576;        // packed data per stage
+constexpr int kStageBytes = 26624;        // packed data per stage
 constexpr int kMaxItems = 32;             // items per stage (one per producer lane)
 constexpr int kItemBytes = 32;            // descriptor size (A and B)
-constexpr int kCoefBytes = 8192;          // staged coefficients + column params per stage
+constexpr int kCoefBytes = 6144;          // staged coefficients + column params per stage
 constexpr int kNStage = 3;                // ring depth
 constexpr int kSlack = 16;                // decode reads up to 2 words past a segment
+constexpr unsigned kWaitHintNs = HCMX_WAIT_HINT;  // mbarrier try_wait suspend hint (ns)
 constexpr int kOffDesc = kStageBytes + kSlack;
 constexpr int kOffWb = kOffDesc + kMaxItems * kItemBytes;
-constexpr int kOffCoef = kOffWb + 48;
+constexpr int kOffHdr = kOffWb + 48;     // slot header written by the producer: stripe id, flags
+constexpr int kOffCoef = kOffHdr + 16;
 constexpr int kSlotBytes = kOffCoef + kCoefBytes;
 constexpr int kR = 128;               // rows per phase-B CTA
 constexpr int kG = kR / 32;           // row groups (accumulators) per lane
@@ -70,9 +78,13 @@ constexpr int kBLRGroup = 8;          // max rank columns per B item
 constexpr uint64_t kAStripeBytes = 8 * kStageBytes;  // target packed bytes per phase-A CTA
 constexpr uint64_t kItemTarget = 1536;          // packed bytes per item (columns grouped up to this)
 constexpr size_t kRingBytes = static_cast<size_t>(kNStage) * kSlotBytes;
-constexpr size_t kSmemBytes = kRingBytes + 2 * kNStage * sizeof(uint64_t);
+constexpr size_t kRedBytes = (kNWB / 2) * kR * sizeof(double);  // phase-B cross-warp reduction
+constexpr size_t kSmemBytes = kRingBytes + kRedBytes + 2 * kNStage * sizeof(uint64_t);  // + full, empty barriers
+constexpr int kCopies = 2 * kMaxItems;  // coefficient copies per stage (two per producer lane)
+// copy entry (u64): [0,32) source element index, [32,48) dst / 16 in the coef area,
+// [48,60) bytes / 16, [60,62) source table (0 x, 1 C, 2 W params, 3 X params), bit 63 valid
 static_assert(kOffDesc % 16 == 0 && kOffCoef % 16 == 0 && kSlotBytes % 16 == 0, "slot alignment");
-static_assert(kNWB * kR * sizeof(double) <= kRingBytes, "reduction reuses the ring");
+constexpr uint32_t kHdrLast = 1u, kHdrEnd = 2u, kHdrEmpty = 4u;  // slot header flags
 
 struct Stage {
     uint64_t byte_off;   // packed data in the arena
@@ -98,8 +110,8 @@ struct BItem {
     uint8_t kind;        // 0 dense, 1 lowrank
     uint8_t ra;          // first row of the item inside the row block
     uint8_t nr;          // rows (fields per column segment)
-    uint32_t coef_off;   // staged coefficients: dense x slice | lowrank C slice, then column params
-    uint32_t src;        // dense: x index of first column; lowrank: global W column id (even)
+    uint32_t coef_off;   // staged coefficient of the first column (x or phase-A result), coef-area bytes
+    uint32_t src;        // dense: x index of first column; lowrank: global W column id
     uint32_t dpacked;    // dense: w | m << 8 | e << 16 | mode << 24
     uint32_t pad;
     double scale;        // dense: buffer scale
@@ -109,10 +121,10 @@ static_assert(sizeof(BItem) == kItemBytes, "BItem layout");
 struct AItem {
     uint32_t word_off;
     uint8_t nseg;        // rank columns
-    uint8_t owns_x;      // this item's copy stages the x slice (shared by the chunk's items)
+    uint8_t pad0;
     uint16_t nf;         // fields per column (<= kAChunk)
-    uint32_t x_off;      // staged x slice (coef area bytes)
-    uint32_t par_off;    // staged X column params
+    uint32_t x_off;      // staged x value of field 0 (coef-area bytes)
+    uint32_t pad1;
     uint32_t xidx;       // x index of field 0
     uint32_t xcol;       // global X column id of the first rank column
     uint32_t leaf;       // lowrank-leaf id
@@ -136,6 +148,9 @@ struct Params {
     const uint16_t* stage_wb;   // [nstages * 24] per-warp item ranges (NW + 1 used)
     const uint32_t* stripe_a;   // [nstripe_a + 1] stage ranges
     const uint32_t* stripe_b;   // [nblocks + 1]
+    const uint64_t* copies;     // [nstages * kCopies] staged coefficient copies (see CopyEntry)
+    unsigned* work;             // [2] stripe counters of the persistent kernels (A, B), zeroed per product
+    uint32_t nstripe_a, nblocks;
     const BItem* bitems;
     const AItem* aitems;
     const LeafA* leafa;
@@ -149,6 +164,7 @@ struct Params {
     double* y;
     uint32_t row_begin, row_end;
     double alpha, beta;
+    int debug;                  // profiling knob (HCMX_DEBUG): 1 = consumers skip the decode
 };
 
 // ----------------------------------------------------------- PTX glue ----
@@ -185,13 +201,23 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     return p;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+#if HCMX_WAIT_HINT > 0
     asm volatile(
         "{\n .reg .pred p;\n"
         "WAIT_%=:\n"
         " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(1000000u)  // suspend (not spin) up to 1 ms: idle warps leave issue slots to busy ones
+        "r"(parity), "r"(kWaitHintNs)  // short suspend instead of a hot spin
         : "memory");
+#else
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+#endif
 }
 
 
@@ -266,103 +292,166 @@ __device__ __forceinline__ void fence_proxy_async() {
 
 
 // ------------------------------------------------------- warp pipeline ----
-// staged copies of one item (sizes must match the host's coef_bytes):
-// copy 0 = coefficient slice (x, or the phase-A results C), copy 1 = column params
-struct ProdItem {
-    uint32_t dst0, dst1;  // coef-area offsets of the two copies
-    uint32_t sizes;       // n0 | n1 << 16 (bytes; 0 = no copy)
-    uint32_t i0;          // element index of copy 0 in x (or C when bit 31 of i1)
-    uint32_t i1;          // column id of copy 1 (params)
-};
 
-template <bool PHASE_A>
-__device__ __forceinline__ ProdItem prod_item(const Params& p, uint32_t idx) {
-    ProdItem r{};
-    if (PHASE_A) {
-        const AItem a = p.aitems[idx];
-        r.dst0 = a.x_off;
-        r.dst1 = a.par_off;
-        r.sizes = (a.owns_x ? round16u((a.nf + (a.xidx & 1u)) * 8u) : 0u) | ((a.nseg * 16u) << 16);
-        r.i0 = a.xidx & ~1u;
-        r.i1 = a.xcol;
-    } else {
-        const BItem b = p.bitems[idx];
-        r.dst0 = b.coef_off;
-        if (b.kind == 0) {
-            r.sizes = round16u((b.nseg + (b.src & 1u)) * 8u);
-            r.i0 = b.src & ~1u;
-        } else {
-            const unsigned n0 = round16u((b.nseg + (b.src & 1u)) * 8u);
-            r.dst1 = b.coef_off + n0;
-            r.sizes = n0 | ((b.nseg * 16u) << 16);
-            r.i0 = b.src & ~1u;
-            r.i1 = b.src | 0x80000000u;
-        }
-    }
-    return r;
-}
 
 // One warp fills the ring: the stage's packed data, its item descriptors and
 // per-warp ranges, and -- per item, one item per lane -- the coefficient slice
 // (x or the phase-A results) plus the column parameters, all as cp.async.bulk
 // copies completing on the slot's full barrier.  Consumers never wait on global
 // memory.  The metadata of stage s+1 is fetched while waiting for a free slot.
+__device__ __forceinline__ void issue_copy(const Params& p, uint64_t c, uint8_t* cdst, uint64_t* bar) {
+    if (!(c >> 63)) return;
+    const uint32_t idx = static_cast<uint32_t>(c);
+    const unsigned dst = static_cast<unsigned>((c >> 32) & 0xffffu) * 16u;
+    const unsigned bytes = static_cast<unsigned>((c >> 48) & 0xfffu) * 16u;
+    const void* src;
+    switch (static_cast<unsigned>((c >> 60) & 3u)) {
+        case 0: src = p.x + idx; break;
+        case 1: src = p.c + idx; break;
+        case 2: src = p.colw_par + idx; break;
+        default: src = p.colx_par + idx; break;
+    }
+    bulk_g2s_plain(cdst + dst, src, bytes, bar);
+}
+
+// Stage sequence of a persistent CTA: stripes are claimed one at a time from a
+// global counter (any CTA may take any stripe; every stripe's result is the
+// same whoever computes it, so the product stays deterministic).  cur() is the
+// stage the producer issues next; the sequence is walked two stages ahead so
+// the metadata of a stage is loaded two iterations before its copies.
+struct StageSeq {
+    uint32_t stripe = 0, s = 0, e = 0;  // stage s of stripe [.., e)
+    bool done = false;
+};
+
 template <bool PHASE_A>
-__device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_t* full, uint64_t* empty,
-                                         uint32_t s0, uint32_t s1, unsigned lane) {
-    if (s0 >= s1) return;
-    const uint64_t policy = evict_first_policy();
-    Stage st = p.stages[s0];
-    ProdItem pi{};
-    if (lane < st.nitems) pi = prod_item<PHASE_A>(p, st.item0 + lane);
-    for (uint32_t s = s0; s < s1; ++s) {
-        const uint32_t it = s - s0;
-        const int slot = static_cast<int>(it % kNStage);
-        Stage nst{};
-        ProdItem npi{};
-        if (s + 1 < s1) {
-            nst = p.stages[s + 1];
-            if (lane < nst.nitems) npi = prod_item<PHASE_A>(p, nst.item0 + lane);
+__device__ __forceinline__ void seq_next(const Params& p, StageSeq& q, unsigned lane) {
+    if (q.done) return;
+    if (q.s + 1 < q.e) {
+        ++q.s;
+        return;
+    }
+    const uint32_t nstripes = PHASE_A ? p.nstripe_a : p.nblocks;
+    for (;;) {
+        uint32_t id = 0;
+        if (lane == 0) id = atomicAdd(p.work + (PHASE_A ? 0 : 1), 1u);
+        id = __shfl_sync(0xffffffffu, id, 0);
+        if (id >= nstripes) {
+            q.done = true;
+            return;
         }
-        if (it >= kNStage) mbar_wait(&empty[slot], ((it / kNStage) - 1) & 1u);
-        uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
-        if (lane == 0) {
-            mbar_expect_tx(&full[slot], st.bytes + st.nitems * kItemBytes + 48 + st.coef_bytes);
-            bulk_g2s(base, p.arena + st.byte_off, st.bytes, &full[slot], policy);
-            const void* d = PHASE_A ? static_cast<const void*>(p.aitems + st.item0)
-                                    : static_cast<const void*>(p.bitems + st.item0);
-            bulk_g2s_plain(base + kOffDesc, d, st.nitems * kItemBytes, &full[slot]);
-            bulk_g2s_plain(base + kOffWb, p.stage_wb + static_cast<size_t>(s) * 24, 48, &full[slot]);
+        const uint32_t* range = PHASE_A ? p.stripe_a : p.stripe_b;
+        const uint32_t s0 = range[id], s1 = range[id + 1];
+        if (s0 < s1 || !PHASE_A) {  // phase B visits empty row blocks too (y = beta y)
+            q.stripe = id;
+            q.s = s0;
+            q.e = s1;
+            return;
         }
-        __syncwarp();
-        if (lane < st.nitems) {
-            uint8_t* cdst = base + kOffCoef;
-            const unsigned n0 = pi.sizes & 0xffffu, n1 = pi.sizes >> 16;
-            const bool from_c = !PHASE_A && (pi.i1 & 0x80000000u);
-            if (n0) bulk_g2s_plain(cdst + pi.dst0, (from_c ? p.c : p.x) + pi.i0, n0, &full[slot]);
-            if (n1) {
-                const ColPar* par = PHASE_A ? p.colx_par : p.colw_par;
-                bulk_g2s_plain(cdst + pi.dst1, par + (pi.i1 & 0x7fffffffu), n1, &full[slot]);
-            }
-        }
-        st = nst;
-        pi = npi;
     }
 }
 
-// consumer warps of a CTA ring: body(slot_base, first, end) for the warp's items
-template <int NW, class Body>
-__device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t* empty, uint32_t s0, uint32_t s1,
-                                        unsigned warp, unsigned lane, Body&& body) {
-    for (uint32_t s = s0; s < s1; ++s) {
-        const uint32_t it = s - s0;
+struct StageMeta {  // what the producer needs for one stage, loaded ahead
+    Stage st;
+    uint64_t c0, c1;
+    uint32_t stripe;
+    uint32_t flags;  // kHdrLast / kHdrEnd
+    bool empty;      // a row block without stages: header only
+};
+
+template <bool PHASE_A>
+__device__ __forceinline__ StageMeta seq_meta(const Params& p, const StageSeq& q, unsigned lane) {
+    StageMeta m{};
+    if (q.done) {
+        m.flags = kHdrEnd;
+        return m;
+    }
+    m.stripe = q.stripe;
+    if (q.s >= q.e) {  // empty phase-B row block
+        m.empty = true;
+        m.flags = kHdrLast | kHdrEmpty;
+        return m;
+    }
+    m.st = p.stages[q.s];
+    m.c0 = __ldg(p.copies + static_cast<size_t>(q.s) * kCopies + lane);
+    m.c1 = __ldg(p.copies + static_cast<size_t>(q.s) * kCopies + 32 + lane);
+    m.flags = q.s + 1 == q.e ? kHdrLast : 0u;
+    return m;
+}
+
+// One warp fills the ring: per stage the packed data, the item descriptors,
+// the per-warp ranges and the coefficient / column-parameter copies (a fixed
+// stride list of <= 64 copy entries per stage, two per lane), all completing
+// on the slot's full barrier, plus a small header (stripe id, last-stage and
+// end flags) written before the copies.  The metadata of every stage is loaded
+// two stages ahead, so no global load sits on the producer's critical path.
+template <bool PHASE_A>
+__device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_t* full, uint64_t* empty,
+                                         unsigned lane) {
+    const uint64_t policy = evict_first_policy();
+    StageSeq q;
+    q.s = q.e = 0;
+    seq_next<PHASE_A>(p, q, lane);
+    StageMeta m0 = seq_meta<PHASE_A>(p, q, lane);
+    seq_next<PHASE_A>(p, q, lane);
+    StageMeta m1 = seq_meta<PHASE_A>(p, q, lane);
+    for (uint32_t it = 0;; ++it) {
+        seq_next<PHASE_A>(p, q, lane);
+        const StageMeta m2 = seq_meta<PHASE_A>(p, q, lane);
+        const int slot = static_cast<int>(it % kNStage);
+        if (it >= kNStage) mbar_wait(&empty[slot], ((it / kNStage) - 1) & 1u);
+        uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
+        if (lane == 0) {
+            uint32_t* hdr = reinterpret_cast<uint32_t*>(base + kOffHdr);
+            hdr[0] = m0.stripe;
+            hdr[1] = m0.flags;
+        }
+        __syncwarp();
+        if (m0.flags & kHdrEnd || m0.empty) {  // header only
+            if (lane == 0) mbar_arrive(&full[slot]);
+        } else {
+            const bool no_coef = p.debug >= 2, no_meta = p.debug >= 3;  // profiling knobs
+            if (lane == 0) {
+                mbar_expect_tx(&full[slot], m0.st.bytes + (no_meta ? 0u : m0.st.nitems * kItemBytes + 48) +
+                                                (no_coef ? 0u : m0.st.coef_bytes));
+                bulk_g2s(base, p.arena + m0.st.byte_off, m0.st.bytes, &full[slot], policy);
+                if (!no_meta) {
+                    const void* d = PHASE_A ? static_cast<const void*>(p.aitems + m0.st.item0)
+                                            : static_cast<const void*>(p.bitems + m0.st.item0);
+                    bulk_g2s_plain(base + kOffDesc, d, m0.st.nitems * kItemBytes, &full[slot]);
+                    const uint32_t sidx = static_cast<uint32_t>(m0.st.pad);  // global stage index
+                    bulk_g2s_plain(base + kOffWb, p.stage_wb + static_cast<size_t>(sidx) * 24, 48, &full[slot]);
+                }
+            }
+            __syncwarp();
+            if (!no_coef) {
+                issue_copy(p, m0.c0, base + kOffCoef, &full[slot]);
+                issue_copy(p, m0.c1, base + kOffCoef, &full[slot]);
+            }
+        }
+        if (m0.flags & kHdrEnd) return;
+        m0 = m1;
+        m1 = m2;
+    }
+}
+
+// consumer warps of a persistent CTA: body(slot_base, first, end) for the
+// warp's items of every stage; at the last stage of a stripe, stripe_end(id)
+template <int NW, class Body, class End>
+__device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t* empty, unsigned warp,
+                                        unsigned lane, int debug, Body&& body, End&& stripe_end) {
+    for (uint32_t it = 0;; ++it) {
         const int slot = static_cast<int>(it % kNStage);
         mbar_wait(&full[slot], (it / kNStage) & 1u);
         const uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
+        const uint32_t* hdr = reinterpret_cast<const uint32_t*>(base + kOffHdr);
+        const uint32_t stripe = hdr[0], flags = hdr[1];
+        if (flags & kHdrEnd) return;
         const uint16_t* wb = reinterpret_cast<const uint16_t*>(base + kOffWb);
-        body(base, wb[warp], wb[warp + 1]);
+        if (!debug && !(flags & kHdrEmpty)) body(base, wb[warp], wb[warp + 1]);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
+        if (flags & kHdrLast) stripe_end(stripe);
     }
 }
 
@@ -433,8 +522,8 @@ __device__ __forceinline__ double a_dispatch_u(const uint32_t* seg, const ColPar
 
 __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const uint8_t* slot, unsigned lane) {
     const unsigned nseg = it.nseg, nf = it.nf;
-    const double* xs = reinterpret_cast<const double*>(slot + kOffCoef + it.x_off) + (it.xidx & 1u);
-    const ColPar* par = reinterpret_cast<const ColPar*>(slot + kOffCoef + it.par_off);
+    const double* xs = reinterpret_cast<const double*>(slot + kOffCoef + it.x_off);
+    const uint32_t* pk = reinterpret_cast<const uint32_t*>(slot) + it.word_off;  // packed column layouts
     double xv[kAChunk / 32];
     const unsigned U = (nf + 31) >> 5;
 #pragma unroll
@@ -442,10 +531,10 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
         const unsigned f = lane + 32u * u;
         xv[u] = (static_cast<unsigned>(u) < U && f < nf) ? xs[f] : 0.0;
     }
-    const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
+    const uint32_t* seg = pk + nseg;
     double res = 0.0;
     for (unsigned c = 0; c < nseg; ++c) {
-        const ColPar col = par[c];
+        const ColPar col = make_par(pk[c]);
         double acc;
         switch (par_mode(col)) {
             case 0: acc = a_dispatch_u<0>(seg, col, lane, nf, xv); break;
@@ -531,7 +620,7 @@ __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg
                                             unsigned lane, double dmul, double (&acc)[kG]) {
     const unsigned nseg = it.nseg;
     constexpr unsigned nr = 32 * (GHI - GLO);
-    const double* cf = reinterpret_cast<const double*>(cbase) + (it.src & 1u);
+    const double* cf = reinterpret_cast<const double*>(cbase);
     if (it.kind == 0) {  // dense: one layout for the whole item
         const ColPar col = make_par(it.dpacked);
         const unsigned w = par_w(col);
@@ -545,9 +634,9 @@ __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg
             default: b_dense_full<2, GLO, GHI>(sp, col, sh, segw, cf, dmul, nseg, acc); break;
         }
     } else {
-        const ColPar* par = reinterpret_cast<const ColPar*>(cbase + round16u((nseg + (it.src & 1u)) * 8u));
+        const uint32_t* pk = seg - nseg;  // packed column layouts precede the segments
         for (unsigned c = 0; c < nseg; ++c) {
-            const ColPar col = par[c];
+            const ColPar col = make_par(pk[c]);
             const double cc = cf[c];
             const unsigned w = par_w(col);
             const unsigned bit = lane * w;
@@ -576,7 +665,7 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
         if (f >= 0 && f < static_cast<int>(nr)) vmask |= 1u << g;
     }
     const unsigned umask = __reduce_or_sync(0xffffffffu, vmask);
-    const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
+    const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off + (it.kind ? nseg : 0u);
     if (__all_sync(0xffffffffu, vmask == umask)) {
         static_assert(kG == 4, "fast-path table assumes 128-row blocks");
         switch (umask) {
@@ -590,11 +679,11 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
             default: break;
         }
     }
-    const double* cf = reinterpret_cast<const double*>(cbase) + (it.src & 1u);
-    const ColPar* par = reinterpret_cast<const ColPar*>(cbase + round16u((nseg + (it.src & 1u)) * 8u));
+    const double* cf = reinterpret_cast<const double*>(cbase);
+    const uint32_t* pk = seg - nseg;
     const ColPar dpar = make_par(it.dpacked);
     for (unsigned c = 0; c < nseg; ++c) {
-        const ColPar col = it.kind == 0 ? dpar : par[c];
+        const ColPar col = it.kind == 0 ? dpar : make_par(pk[c]);
         const double cc = it.kind == 0 ? dmul * cf[c] : cf[c];
         switch (par_mode(col)) {
             case 0: b_column<0>(seg, col, f0, vmask, umask, cc, acc); break;
@@ -605,58 +694,81 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
     }
 }
 
+__device__ __forceinline__ void consumer_bar() {  // the consumer warps of phase B only
+    asm volatile("bar.sync 1, %0;" ::"n"(kNWB * 32) : "memory");
+}
+
+// Persistent kernels: one CTA per resident slot, stripes claimed dynamically.
 __global__ void __launch_bounds__(kThreadsA, 2) k_phase_a(Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kRedBytes);
     uint64_t* empty = full + kNStage;
     const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t s0 = p.stripe_a[blockIdx.x], s1 = p.stripe_a[blockIdx.x + 1];
     ring_init<kNWA>(full, empty);
     if (warp == kNWA) {
-        producer<true>(p, smem, full, empty, s0, s1, lane);
+        producer<true>(p, smem, full, empty, lane);
         return;
     }
-    consume<kNWA>(smem, full, empty, s0, s1, warp, lane, [&](const uint8_t* base, unsigned b, unsigned e) {
-        const AItem* items = reinterpret_cast<const AItem*>(base + kOffDesc);
-        for (unsigned i = b; i < e; ++i) a_item(p, items[i], base, lane);
-    });
+    consume<kNWA>(
+        smem, full, empty, warp, lane, p.debug,
+        [&](const uint8_t* base, unsigned b, unsigned e) {
+            const AItem* items = reinterpret_cast<const AItem*>(base + kOffDesc);
+            for (unsigned i = b; i < e; ++i) a_item(p, items[i], base, lane);
+        },
+        [](uint32_t) {});
 }
 
 __global__ void __launch_bounds__(kThreadsB, 2) k_phase_b(Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
+    double* red = reinterpret_cast<double*>(smem + kRingBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kRedBytes);
     uint64_t* empty = full + kNStage;
     const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint32_t blk = blockIdx.x;
-    const uint32_t s0 = p.stripe_b[blk], s1 = p.stripe_b[blk + 1];
     ring_init<kNWB>(full, empty);
+    if (warp == kNWB) {
+        producer<false>(p, smem, full, empty, lane);
+        return;
+    }
     double acc[kG];
 #pragma unroll
     for (int g = 0; g < kG; ++g) acc[g] = 0.0;
-    if (warp == kNWB) {
-        producer<false>(p, smem, full, empty, s0, s1, lane);
-    } else {
-        consume<kNWB>(smem, full, empty, s0, s1, warp, lane, [&](const uint8_t* base, unsigned b, unsigned e) {
+    constexpr unsigned H = kNWB / 2;
+    consume<kNWB>(
+        smem, full, empty, warp, lane, p.debug,
+        [&](const uint8_t* base, unsigned b, unsigned e) {
             const BItem* items = reinterpret_cast<const BItem*>(base + kOffDesc);
             for (unsigned i = b; i < e; ++i) b_item(p, items[i], base, lane, acc);
+        },
+        [&](uint32_t blk) {  // block done: fixed-order pairwise sum of the warps, then y
+            consumer_bar();
+            if (warp >= H) {
+#pragma unroll
+                for (int g = 0; g < kG; ++g) red[(warp - H) * kR + 32 * g + lane] = acc[g];
+            }
+            consumer_bar();
+            if (warp < H) {
+#pragma unroll
+                for (int g = 0; g < kG; ++g) acc[g] += red[warp * kR + 32 * g + lane];
+            }
+            consumer_bar();
+            if (warp < H) {
+#pragma unroll
+                for (int g = 0; g < kG; ++g) red[warp * kR + 32 * g + lane] = acc[g];
+            }
+            consumer_bar();
+            const uint32_t r0 = p.row_begin + blk * kR;
+            const uint32_t nrows = min(static_cast<uint32_t>(kR), p.row_end - r0);
+            if (tid < nrows) {
+                double sum = 0.0;
+#pragma unroll
+                for (unsigned wv = 0; wv < H; ++wv) sum += red[wv * kR + tid];
+                double* yp = p.y + r0 + tid;
+                *yp = p.beta == 0.0 ? sum : fma(p.beta, *yp, sum);
+            }
+            consumer_bar();
+#pragma unroll
+            for (int g = 0; g < kG; ++g) acc[g] = 0.0;
         });
-    }
-    __syncthreads();  // ring drained: reuse it for the cross-warp reduction
-    double* red = reinterpret_cast<double*>(smem);
-    if (warp < kNWB) {
-#pragma unroll
-        for (int g = 0; g < kG; ++g) red[warp * kR + 32 * g + lane] = acc[g];
-    }
-    __syncthreads();
-    const uint32_t r0 = p.row_begin + blk * kR;
-    const uint32_t nrows = min(static_cast<uint32_t>(kR), p.row_end - r0);
-    for (uint32_t q = tid; q < nrows; q += kThreadsB) {
-        double sum = 0.0;
-#pragma unroll
-        for (int wv = 0; wv < kNWB; ++wv) sum += red[wv * kR + q];
-        double* yp = p.y + r0 + q;
-        *yp = p.beta == 0.0 ? sum : fma(p.beta, *yp, sum);
-    }
 }
 
 __global__ void k_scale(double* y, uint64_t n, double beta) {
@@ -698,7 +810,7 @@ using namespace hcmx_gpu;
 
 struct hcmx_hmat {
     uint64_t n_rows = 0, n_cols = 0, rb = 0, re = 0;
-    DevBuf arena, stages, stage_wb, stripe_a, stripe_b, bitems, aitems, leafa, colw, colx, coef, c, partial,
+    DevBuf arena, stages, stage_wb, stripe_a, stripe_b, copies, work, bitems, aitems, leafa, colw, colx, coef, c, partial,
         counter, xpad, xbuf, ybuf;
     uint32_t nstripe_a = 0, nblocks = 0, nlr = 0;
     hcmx_memory_report report{};
@@ -773,8 +885,11 @@ struct Spec {
     uint32_t coef_x;       // A: x slice bytes (shareable by the chunk's items)
     uint32_t coef_p;       // coefficient / params bytes owned by the item
     uint64_t cost;         // fields (LPT weight)
-    uint64_t unit;         // LPT unit (A: one chunk of one leaf; B: the item)
+    uint64_t unit;         // item key: consecutive columns with the same key may merge
     uint32_t xidx, nf;     // A: x slice key
+    uint32_t param;        // lowrank / phase A: packed column layout stored ahead of the segments
+    uint32_t elem;         // this column's coefficient index (x or C)
+    uint32_t sl_table, sl_start, sl_count;  // staged coefficient slice (deduplicated per stage)
 };
 
 // split columns [0, n) into consecutive groups of <= maxcols columns and,
@@ -806,6 +921,12 @@ struct Builder {
     std::vector<BItem> bitems;
     std::vector<AItem> aitems;
     std::vector<Seg> segs;
+    std::vector<uint64_t> copies;  // kCopies per stage
+
+    static uint64_t copy_entry(uint32_t idx, uint32_t dst, uint32_t bytes, unsigned table) {
+        return (1ull << 63) | (static_cast<uint64_t>(table) << 60) | (static_cast<uint64_t>(bytes / 16) << 48) |
+               (static_cast<uint64_t>(dst / 16) << 32) | idx;
+    }
 
     Builder(const hcmx_hmat_desc& dd, hcmx_hmat* hh) : d(dd), h(hh) {}
 
@@ -822,97 +943,129 @@ struct Builder {
         if (keep_map) h->segs[s.buf].push_back({at, static_cast<uint32_t>(s.f0), static_cast<uint32_t>(s.nf)});
     }
 
-    // One CTA stripe: items packed in order into CTA stages (<= kStageBytes of
-    // data, <= kMaxItems items, <= kCoefBytes staged); each closed stage's items
-    // go to the NW consumer warps by LPT on the warps' CUMULATIVE load over the
-    // stripe (so warps progress through the ring at the same pace), and the
-    // descriptors are emitted grouped by warp.  Phase-A items of one chunk in a
-    // stage share one staged x slice.
-    template <class Item, int NW>
+    // One CTA stripe.  Specs are single columns.  Stages take columns in order
+    // up to kStageBytes; each stage's columns are split into NW contiguous
+    // pieces of (nearly) equal packed bytes, one per consumer warp, so every
+    // warp has the same amount of decoding per stage (the ring advances at the
+    // pace of the slowest warp).  Inside a piece, consecutive columns of one
+    // leaf / row range (B) or leaf chunk (A) merge into items of <= MAXC
+    // columns.  Phase-A items of one chunk in a stage share one staged x slice.
+    std::vector<uint32_t> a_items_per_leaf;
+
+    template <class Item, int NW, int MAXC>
     void emit_stripe(std::vector<Spec<Item>>& specs, std::vector<Item>& items) {
         constexpr bool IS_A = std::is_same<Item, AItem>::value;
-        std::vector<uint64_t> load(NW, 0);
-        std::vector<std::pair<Item, uint64_t>> pending;
-        bool open = false;
-        uint64_t start = 0;
-        uint32_t coef = 0;
-        uint32_t x_idx = 0xffffffffu, x_nf = 0, x_at = 0;
-        auto close = [&]() {
-            if (!open) return;
-            open = false;
-            while (arena.size() % 4) arena.push_back(0u);
-            if (pending.empty()) return;
-            std::vector<size_t> order(pending.size());
-            for (size_t i = 0; i < order.size(); ++i) order[i] = i;
-            std::stable_sort(order.begin(), order.end(),
-                             [&](size_t a, size_t b) { return pending[a].second > pending[b].second; });
-            std::vector<int> owner(pending.size());
-            for (size_t i : order) {
-                const int wv = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-                owner[i] = wv;
-                load[wv] += pending[i].second;
+        size_t pos = 0;
+        while (pos < specs.size()) {
+            // columns of this stage by data budget
+            size_t end = pos;
+            uint64_t bytes = 0;
+            while (end < specs.size() && bytes + specs[end].words * 4 <= static_cast<uint64_t>(kStageBytes))
+                bytes += specs[end++].words * 4;
+            if (end == pos) throw invalid_argument("hmat: column exceeds a stage");
+            for (;;) {
+                if (try_stage<Item, NW, MAXC>(specs, pos, end, items)) break;
+                end = pos + std::max<size_t>(1, (end - pos) * 3 / 4);  // too many items / coefficients
             }
-            Stage st{};
-            st.byte_off = start * 4;
-            st.bytes = static_cast<uint32_t>((arena.size() - start) * 4);
-            st.item0 = static_cast<uint32_t>(items.size());
-            st.nitems = static_cast<uint32_t>(pending.size());
-            st.coef_bytes = coef;
-            stages.push_back(st);
-            uint16_t cnt = 0;
-            for (int wv = 0; wv < NW; ++wv) {
-                wb.push_back(cnt);
-                for (size_t i = 0; i < pending.size(); ++i)
-                    if (owner[i] == wv) {
-                        items.push_back(pending[i].first);
-                        ++cnt;
-                    }
-            }
-            while (wb.size() % 24) wb.push_back(cnt);  // 48 bytes per stage (one bulk copy)
-            pending.clear();
-        };
-        for (Spec<Item>& sp : specs) {
-            if (sp.words * 4 > static_cast<uint64_t>(kStageBytes) ||
-                sp.coef_x + sp.coef_p > static_cast<uint32_t>(kCoefBytes))
-                throw invalid_argument("hmat: item exceeds a stage");
-            bool shared = IS_A && open && x_idx == sp.xidx && sp.nf <= x_nf;
-            const uint32_t need = (shared ? 0u : sp.coef_x) + sp.coef_p;
-            if (open && ((arena.size() - start + sp.words) * 4 > static_cast<uint64_t>(kStageBytes) ||
-                         coef + need > static_cast<uint32_t>(kCoefBytes) || pending.size() >= kMaxItems)) {
-                close();
-                shared = false;
-            }
-            if (!open) {
-                while (arena.size() % 4) arena.push_back(0u);  // 16-byte aligned stages
-                start = arena.size();
-                coef = 0;
-                x_idx = 0xffffffffu;
-                open = true;
-            }
-            Item it = sp.it;
-            it.word_off = static_cast<uint32_t>(arena.size() - start);
-            if constexpr (IS_A) {
-                if (shared) {
-                    it.owns_x = 0;
-                    it.x_off = x_at;
-                } else {
-                    it.owns_x = 1;
-                    it.x_off = coef;
-                    x_at = coef;
-                    x_idx = sp.xidx;
-                    x_nf = sp.nf;
-                    coef += sp.coef_x;
-                }
-                it.par_off = coef;
-                coef += sp.coef_p;
-            } else {
-                it.coef_off = coef;
-                coef += sp.coef_p;
-            }
-            for (uint32_t k = 0; k < sp.nseg; ++k) put_fields(segs[sp.seg0 + k]);
-            pending.emplace_back(it, sp.cost + 64);
+            pos = end;
         }
-        close();
+    }
+
+    // pieces + items for specs[pos, end); false (nothing emitted) if over budget
+    template <class Item, int NW, int MAXC>
+    bool try_stage(std::vector<Spec<Item>>& specs, size_t pos, size_t end, std::vector<Item>& items) {
+        constexpr bool IS_A = std::is_same<Item, AItem>::value;
+        uint64_t total = 0;
+        for (size_t i = pos; i < end; ++i) total += specs[i].words;
+        // piece boundaries: warp p gets specs [cut[p], cut[p+1])
+        std::vector<size_t> cut(NW + 1, end);
+        cut[0] = pos;
+        {
+            size_t i = pos;
+            uint64_t acc = 0;
+            for (int p = 1; p < NW; ++p) {
+                const uint64_t target = total * p / NW;
+                while (i < end && acc + specs[i].words / 2 <= target) acc += specs[i++].words;
+                cut[p] = i;
+            }
+        }
+        // items (per warp, in order); coefficient slices deduplicated per stage
+        struct Built {
+            Item it;
+            size_t first, n;
+        };
+        std::vector<std::vector<Built>> per(NW);
+        struct Slice {
+            uint32_t table, start, count, off;
+        };
+        std::vector<Slice> slices;
+        uint32_t coef = 0, nit = 0;
+        auto slice_of = [&](const Spec<Item>& sp) -> const Slice& {
+            for (const Slice& sl : slices)
+                if (sl.table == sp.sl_table && sl.start == sp.sl_start && sl.count >= sp.sl_count) return sl;
+            slices.push_back({sp.sl_table, sp.sl_start, sp.sl_count, coef});
+            coef += r16((sp.sl_count + (sp.sl_start & 1u)) * 8);
+            return slices.back();
+        };
+        for (int p = 0; p < NW; ++p) {
+            size_t i = cut[p];
+            while (i < cut[p + 1]) {
+                size_t j = i + 1;
+                while (j < cut[p + 1] && j - i < static_cast<size_t>(MAXC) && specs[j].unit == specs[i].unit) ++j;
+                const uint32_t n = static_cast<uint32_t>(j - i);
+                Item it = specs[i].it;
+                it.nseg = static_cast<uint8_t>(n);
+                const Slice sl = slice_of(specs[i]);
+                const uint32_t off = sl.off + (specs[i].elem - (sl.start & ~1u)) * 8;
+                if constexpr (IS_A) it.x_off = off;
+                else it.coef_off = off;
+                per[p].push_back({it, i, n});
+                ++nit;
+                i = j;
+            }
+        }
+        if (nit > static_cast<uint32_t>(kMaxItems) || coef > static_cast<uint32_t>(kCoefBytes) ||
+            slices.size() > static_cast<size_t>(kCopies)) {
+            if (end - pos == 1) throw invalid_argument("hmat: column exceeds a stage");
+            return false;
+        }
+        // emit: data in warp order (packed column layouts ahead of the segments
+        // for lowrank / phase-A items), descriptors grouped by warp, copy list
+        const size_t c0 = copies.size();
+        copies.resize(c0 + kCopies, 0);
+        for (size_t q = 0; q < slices.size(); ++q)
+            copies[c0 + q] = copy_entry(slices[q].start & ~1u, slices[q].off,
+                                        r16((slices[q].count + (slices[q].start & 1u)) * 8), slices[q].table);
+        while (arena.size() % 4) arena.push_back(0u);  // 16-byte aligned stages
+        const uint64_t start = arena.size();
+        Stage st{};
+        st.item0 = static_cast<uint32_t>(items.size());
+        uint16_t cnt = 0;
+        for (int p = 0; p < NW; ++p) {
+            wb.push_back(cnt);
+            for (Built& b : per[p]) {
+                b.it.word_off = static_cast<uint32_t>(arena.size() - start);
+                bool packed = IS_A;
+                if constexpr (!IS_A) packed = b.it.kind != 0;
+                if (packed)
+                    for (size_t k = b.first; k < b.first + b.n; ++k) arena.push_back(specs[k].param);
+                for (size_t k = b.first; k < b.first + b.n; ++k)
+                    for (uint32_t q = 0; q < specs[k].nseg; ++q) put_fields(segs[specs[k].seg0 + q]);
+                if constexpr (IS_A) a_items_per_leaf[b.it.leaf]++;
+                items.push_back(b.it);
+                ++cnt;
+            }
+        }
+        wb.push_back(cnt);
+        while (wb.size() % 24) wb.push_back(cnt);  // 48 bytes per stage (one bulk copy)
+        while (arena.size() % 4) arena.push_back(0u);
+        st.byte_off = start * 4;
+        st.bytes = static_cast<uint32_t>((arena.size() - start) * 4);
+        st.nitems = nit;
+        st.coef_bytes = coef;
+        st.pad = stages.size();  // global stage index (the producer fetches its per-warp ranges)
+        stages.push_back(st);
+        return true;
     }
 };
 
@@ -1041,12 +1194,13 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     // stripes of ~kAStripeBytes, one chunk (all its rank-column groups) per warp
     uint32_t nstripe_a = 0;
     std::vector<uint32_t> stripe_a = {0};
+    B.a_items_per_leaf.assign(leafa.size(), 0);
     {
         std::vector<Spec<AItem>> specs;
         uint64_t stripe_bytes = 0, unit = 0;
         auto flush = [&]() {
             if (specs.empty()) return;
-            B.emit_stripe<AItem, kNWA>(specs, B.aitems);
+            B.emit_stripe<AItem, kNWA, kAGroup>(specs, B.aitems);
             stripe_a.push_back(static_cast<uint32_t>(B.stages.size()));
             ++nstripe_a;
             specs.clear();
@@ -1056,13 +1210,10 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
             if (d.kind[l] != 1) continue;
             const LeafA& L = leafa[lr_id[l]];
             const int64_t cols = d.col1[l] - d.col0[l];
-            LeafA& Lw = leafa[lr_id[l]];
-            Lw.nitems = 0;
             for (uint32_t ch = 0; ch < L.nchunks; ++ch, ++unit) {
                 const uint64_t f0 = static_cast<uint64_t>(ch) * kAChunk;
                 const uint64_t nf = std::min<uint64_t>(kAChunk, cols - f0);
-                const auto groups = column_groups(L.k, kAGroup, [&](uint32_t i) { return B.words_of(d.buf0[l] + L.k + i, nf); });
-                Lw.nitems += static_cast<uint32_t>(groups.size());
+                const auto groups = column_groups(L.k, 1, [&](uint32_t i) { return B.words_of(d.buf0[l] + L.k + i, nf); });
                 for (const auto& gr : groups) {
                     const uint32_t g = gr.first, ng = gr.second;
                     Spec<AItem> sp{};
@@ -1080,8 +1231,12 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                     it.leaf = static_cast<uint32_t>(lr_id[l]);
                     it.chunk = static_cast<uint16_t>(ch);
                     it.icol0 = static_cast<uint16_t>(g);
-                    sp.coef_x = r16((nf + (it.xidx & 1u)) * 8);
-                    sp.coef_p = ng * 16;
+                    sp.words += ng;  // packed column layout word
+                    sp.param = col_par(d.desc[d.buf0[l] + L.k + g]).packed;
+                    sp.elem = it.xidx;
+                    sp.sl_table = 0;  // x slice of the chunk
+                    sp.sl_start = it.xidx;
+                    sp.sl_count = static_cast<uint32_t>(nf);
                     sp.cost = nf * ng;
                     sp.unit = unit;
                     sp.xidx = it.xidx;
@@ -1095,6 +1250,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         flush();
     }
     rep.stages_a = B.stages.size();
+    for (size_t i = 0; i < leafa.size(); ++i) leafa[i].nitems = B.a_items_per_leaf[i];
 
     // ---- phase B: one stripe per block of kR rows
     const uint64_t nblocks = (h->re - h->rb + kR - 1) / kR;
@@ -1113,12 +1269,13 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
             specs.clear();
             const uint64_t b0 = h->rb + blk * kR, b1 = std::min<uint64_t>(b0 + kR, h->re);
             for (uint32_t l : block_leaves[blk]) {
+                ++unit;  // one item key per (leaf, row block)
                 const int64_t rows = d.row1[l] - d.row0[l], cols = d.col1[l] - d.col0[l];
                 const uint64_t r0 = std::max<uint64_t>(d.row0[l], b0), r1 = std::min<uint64_t>(d.row1[l], b1);
                 const uint64_t nr = r1 - r0, roff = r0 - d.row0[l];
                 if (d.kind[l] == 0) {
                     const uint64_t b = d.buf0[l];
-                    const auto groups = column_groups(static_cast<uint32_t>(cols), kBDenseGroup,
+                    const auto groups = column_groups(static_cast<uint32_t>(cols), 1,
                                                       [&](uint32_t) { return B.words_of(b, nr); });
                     for (const auto& gr : groups) {
                         const int64_t c0 = gr.first;
@@ -1138,14 +1295,17 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                         it.nr = static_cast<uint8_t>(nr);
                         it.dpacked = col_par(d.desc[b]).packed;
                         it.scale = d.desc[b].scale;
-                        sp.coef_p = r16((nc + (it.src & 1u)) * 8);
+                        sp.elem = it.src;
+                        sp.sl_table = 0;  // x slice of the dense leaf's columns
+                        sp.sl_start = static_cast<uint32_t>(d.col0[l]);
+                        sp.sl_count = static_cast<uint32_t>(cols);
                         sp.cost = nc * nr;
-                        sp.unit = unit++;
+                        sp.unit = unit;
                         specs.push_back(sp);
                     }
                 } else {
                     const LeafA& L = leafa[lr_id[l]];
-                    const auto groups = column_groups(L.k, kBLRGroup, [&](uint32_t i) { return B.words_of(d.buf0[l] + i, nr); });
+                    const auto groups = column_groups(L.k, 1, [&](uint32_t i) { return B.words_of(d.buf0[l] + i, nr); });
                     for (const auto& gr : groups) {
                         const uint32_t g = gr.first, ng = gr.second;
                         Spec<BItem> sp{};
@@ -1161,14 +1321,19 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                         it.ra = static_cast<uint8_t>(r0 - b0);
                         it.nr = static_cast<uint8_t>(nr);
                         it.src = L.colbase + g;
-                        sp.coef_p = r16((ng + (it.src & 1u)) * 8) + ng * 16;
+                        sp.words += ng;  // packed column layout word
+                        sp.param = col_par(d.desc[d.buf0[l] + g]).packed;
+                        sp.elem = it.src;
+                        sp.sl_table = 1;  // phase-A results of the leaf
+                        sp.sl_start = L.colbase;
+                        sp.sl_count = L.k;
                         sp.cost = ng * nr;
-                        sp.unit = unit++;
+                        sp.unit = unit;
                         specs.push_back(sp);
                     }
                 }
             }
-            B.emit_stripe<BItem, kNWB>(specs, B.bitems);
+            B.emit_stripe<BItem, kNWB, kBLRGroup>(specs, B.bitems);
             stripe_b.push_back(static_cast<uint32_t>(B.stages.size()));
         }
     }
@@ -1188,6 +1353,8 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     up(h->arena, B.arena.data(), B.arena.size() * 4);
     up(h->stages, B.stages.data(), B.stages.size() * sizeof(Stage));
     up(h->stage_wb, B.wb.data(), B.wb.size() * sizeof(uint16_t));
+    up(h->copies, B.copies.data(), B.copies.size() * sizeof(uint64_t));
+    h->work.alloc(16);
     up(h->stripe_a, stripe_a.data(), stripe_a.size() * 4);
     up(h->stripe_b, stripe_b.data(), stripe_b.size() * 4);
     up(h->bitems, B.bitems.data(), B.bitems.size() * sizeof(BItem));
@@ -1207,7 +1374,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     h->nstripe_a = nstripe_a;
     h->nblocks = static_cast<uint32_t>(nblocks);
     rep.device_arena_bytes = B.arena.size() * 4;
-    rep.device_table_bytes = B.stages.size() * (sizeof(Stage) + 48) + B.bitems.size() * sizeof(BItem) +
+    rep.device_table_bytes = B.stages.size() * (sizeof(Stage) + 48 + kCopies * 8) + B.bitems.size() * sizeof(BItem) +
                              B.aitems.size() * sizeof(AItem) + leafa.size() * sizeof(LeafA) +
                              colw.size() * 2 * sizeof(ColPar) + coef.size() * 16;
     rep.overhead = rep.device_table_bytes;
@@ -1220,6 +1387,10 @@ Params make_params(hcmx_hmat* h, double alpha, double beta, double* y) {
     p.stage_wb = h->stage_wb.as<uint16_t>();
     p.stripe_a = h->stripe_a.as<uint32_t>();
     p.stripe_b = h->stripe_b.as<uint32_t>();
+    p.copies = h->copies.as<uint64_t>();
+    p.work = h->work.as<unsigned>();
+    p.nstripe_a = h->nstripe_a;
+    p.nblocks = h->nblocks;
     p.bitems = h->bitems.as<BItem>();
     p.aitems = h->aitems.as<AItem>();
     p.leafa = h->leafa.as<LeafA>();
@@ -1257,18 +1428,30 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
     }
     check_cuda(cudaMemcpyAsync(h->xpad.p, dx, h->n_cols * 8, cudaMemcpyDeviceToDevice, s), "x copy");
     Params p = make_params(h, alpha, beta, dy);
+    static const int debug_knob = [] {
+        const char* e = std::getenv("HCMX_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    p.debug = debug_knob;
     hcmx_hmat::Rec rec{};
     if (h->timing) {
         rec = {take_event(h), take_event(h), take_event(h)};
         check_cuda(cudaEventRecord(rec.a0, s), "event");
     }
+    static int nsm = [] {
+        int dev = 0, n = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n;
+    }();
+    check_cuda(cudaMemsetAsync(h->work.p, 0, 8, s), "work counters");
     if (h->nlr && h->nstripe_a) {
-        k_phase_a<<<h->nstripe_a, kThreadsA, kSmemBytes, s>>>(p);
+        k_phase_a<<<std::min<uint32_t>(h->nstripe_a, 2 * nsm), kThreadsA, kSmemBytes, s>>>(p);
         h->last_launches++;
     }
     if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
     if (h->nblocks) {
-        k_phase_b<<<h->nblocks, kThreadsB, kSmemBytes, s>>>(p);
+        k_phase_b<<<std::min<uint32_t>(h->nblocks, 2 * nsm), kThreadsB, kSmemBytes, s>>>(p);
         h->last_launches++;
     }
     check_cuda(cudaGetLastError(), "matvec launch");

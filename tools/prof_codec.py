@@ -21,9 +21,10 @@ def main():
     vals = np.sign(rng.standard_normal(nb * bs)) * 10 ** rng.uniform(-6, 0, nb * bs)
     d = torch.as_tensor(vals).cuda()
     counts = np.full(nb, bs, np.uint64)
+    dv = torch.as_tensor(np.arange(nb, dtype=np.int64) * bs).cuda()
     for eps in (1e-4, 1e-6, 1e-8):
         for s in range(4):
-            bb = codec.compress_batch(d, counts, eps, s)
+            bb = codec.compress_batch(d, counts, eps, s, d_voff=dv)
             out = codec.decompress_batch(bb)
             torch.cuda.synchronize()
             w = int(bb.desc["bit_width"][0])
@@ -33,7 +34,7 @@ def main():
             for _ in range(5):
                 torch.cuda.synchronize()
                 t = time.perf_counter()
-                bb = codec.compress_batch(d, counts, eps, s, payload=bb.payload)
+                bb = codec.compress_batch(d, counts, eps, s, payload=bb.payload, d_voff=dv)
                 torch.cuda.synchronize()
                 tc.append(time.perf_counter() - t)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
