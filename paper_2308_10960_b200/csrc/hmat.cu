@@ -113,33 +113,34 @@ struct BItem {
     uint32_t coef_off;   // staged coefficient of the first column (x or phase-A result), coef-area bytes
     uint32_t src;        // dense: x index of first column; lowrank: global W column id
     uint32_t dpacked;    // dense: w | m << 8 | e << 16 | mode << 24
-    uint32_t pad;
+    uint8_t mode;        // decode mode shared by every column of the item
+    uint8_t fcase;       // GLO << 4 | GHI when the item covers whole row groups [GLO, GHI), else 0
+    uint16_t pad;
     double scale;        // dense: buffer scale
 };
 static_assert(sizeof(BItem) == kItemBytes, "BItem layout");
 
 struct AItem {
     uint32_t word_off;
-    uint8_t nseg;        // rank columns
-    uint8_t pad0;
+    uint8_t nseg;        // rank columns (<= kAGroup)
+    uint8_t mode;        // decode mode shared by every column of the item
     uint16_t nf;         // fields per column (<= kAChunk)
     uint32_t x_off;      // staged x value of field 0 (coef-area bytes)
-    uint32_t pad1;
-    uint32_t xidx;       // x index of field 0
+    uint32_t pbase;      // partials of the leaf (nchunks > 1)
     uint32_t xcol;       // global X column id of the first rank column
-    uint32_t leaf;       // lowrank-leaf id
+    uint32_t leaf;       // lowrank-leaf id (arrival counter)
+    uint16_t k;          // leaf rank
+    uint16_t nchunks;    // column chunks of the leaf
     uint16_t chunk;      // column-chunk index within the leaf
     uint16_t icol0;      // first rank column within the leaf
 };
 static_assert(sizeof(AItem) == kItemBytes, "AItem layout");
 
-struct LeafA {
+struct LeafA {  // host-side only
     uint32_t colbase;   // global column id of rank column 0
     uint32_t k;
     uint32_t pbase;     // partials base (nchunks > 1)
-    uint32_t nitems;    // A items of this leaf
     uint32_t nchunks;
-    uint32_t pad;
 };
 
 struct Params {
@@ -153,7 +154,6 @@ struct Params {
     uint32_t nstripe_a, nblocks;
     const BItem* bitems;
     const AItem* aitems;
-    const LeafA* leafa;
     const ColPar* colw_par;
     const ColPar* colx_par;
     const double* coef;         // sigma_i * scale_X_i * scale_W_i
@@ -231,26 +231,25 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // ------------------------------------------------------------- decode ----
 // A field of width w sits at bit sh of the word pair sp[0..1] (sp[2] too when
 // w > 32).  Layout [mant m][offset e][sign] (codec.cpp:118-137).  Each mode
-// returns (1.mant * 2^offset) - 1 -- exactly the codec's value / scale
-// (codec.cpp:161-169) -- and xors the sign into the coefficient's high word.
-//   mode 0: w <= 32, m <= 20, e < 11   (the whole double lives in the high word)
-//   mode 1: w <= 32, m  > 20, e < 11
+// returns +-((1.mant * 2^offset) - 1) -- exactly the codec's value / scale
+// (codec.cpp:161-169); the sign is xored into the result's high word.
+//   mode 0: w == 1 + e + m <= 32, m <= 20, e < 11 (the double lives in the high word)
+//   mode 1: w == 1 + e + m <= 32, m  > 20, e < 11
 //   mode 2: anything else (64-bit window, min(offset + 1023, 2046) clamp)
+// Every column of an item shares one mode, so the mode is dispatched per item.
 template <int MODE>
-__device__ __forceinline__ double dec(const uint32_t* sp, const ColPar& c, unsigned sh, double coef, double& cs) {
+__device__ __forceinline__ double dec(const uint32_t* sp, const ColPar& c, unsigned sh) {
     if (MODE == 0) {
         const uint32_t t = __funnelshift_r(sp[0], sp[1], sh);
-        const uint32_t sgn = (t << c.sgn_sh) & 0x80000000u;
         const uint32_t hi = (t & c.mask_em) * c.mul_rsh + (1023u << 20);
-        cs = __hiloint2double(__double2hiint(coef) ^ sgn, __double2loint(coef));
-        return __hiloint2double(hi, 0) - 1.0;
+        const double d = __hiloint2double(hi, 0) - 1.0;
+        return __hiloint2double(__double2hiint(d) ^ ((t << c.sgn_sh) & 0x80000000u), __double2loint(d));
     } else if (MODE == 1) {
         const uint32_t t = __funnelshift_r(sp[0], sp[1], sh);
-        const uint32_t sgn = (t << c.sgn_sh) & 0x80000000u;
         const uint32_t hi = ((t & c.mask_em) >> c.mul_rsh) + (1023u << 20);
         const uint32_t lo = t << (32u - c.mul_rsh);
-        cs = __hiloint2double(__double2hiint(coef) ^ sgn, __double2loint(coef));
-        return __hiloint2double(hi, lo) - 1.0;
+        const double d = __hiloint2double(hi, lo) - 1.0;
+        return __hiloint2double(__double2hiint(d) ^ ((t << c.sgn_sh) & 0x80000000u), __double2loint(d));
     } else {
         const unsigned w = c.packed & 0xffu, m = (c.packed >> 8) & 0xffu, e = (c.packed >> 16) & 0xffu;
         uint64_t win = ((static_cast<uint64_t>(sp[1]) << 32) | sp[0]) >> sh;
@@ -260,28 +259,22 @@ __device__ __forceinline__ double dec(const uint32_t* sp, const ColPar& c, unsig
         const uint64_t fem = win & ((1ull << em) - 1);
         uint64_t bits = (fem << (52 - m)) + (1023ull << 52);
         if ((fem >> m) >= 1024) bits = (2046ull << 52) | ((fem << (52 - m)) & ((1ull << 52) - 1));
-        cs = __longlong_as_double(__double_as_longlong(coef) ^ static_cast<long long>(sgn << 63));
-        return __longlong_as_double(static_cast<long long>(bits)) - 1.0;
+        const double d = __longlong_as_double(static_cast<long long>(bits)) - 1.0;
+        return __longlong_as_double(__double_as_longlong(d) ^ static_cast<long long>(sgn << 63));
     }
 }
 
-__device__ __forceinline__ unsigned par_w(const ColPar& c) { return c.packed & 0xffu; }
-
-__device__ __forceinline__ ColPar make_par(uint32_t packed) {
+// decoder constants of one column from its packed layout word (w | m << 8 |
+// e << 16 | mode << 24); modes 0/1 have w == 1 + e + m
+template <int MODE>
+__device__ __forceinline__ ColPar col_of(uint32_t packed) {
     ColPar c;
-    const unsigned m = (packed >> 8) & 0xffu, e = (packed >> 16) & 0xffu, mode = packed >> 24, em = e + m;
-    c.mask_em = em >= 32 ? 0xffffffffu : ((1u << em) - 1u);
-    c.mul_rsh = mode == 0 ? (1u << (20 - m)) : (mode == 1 ? m - 20 : 0u);
     c.packed = packed;
-    c.sgn_sh = em <= 31 ? 31 - em : 0u;
+    const unsigned w = packed & 0xffu, m = (packed >> 8) & 0xffu;
+    c.mask_em = 0xffffffffu >> (33u - w);  // e + m = w - 1 bits
+    c.mul_rsh = MODE == 0 ? (1u << (20u - m)) : m - 20u;
+    c.sgn_sh = 32u - w;                    // sign bit (w - 1) to bit 31
     return c;
-}
-__device__ __forceinline__ unsigned par_mode(const ColPar& c) { return c.packed >> 24; }
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
 }
 
 __device__ __forceinline__ unsigned round16u(unsigned x) { return (x + 15u) & ~15u; }
@@ -468,62 +461,109 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
 }
 
 // ------------------------------------------------------------ phase A ----
-// U = fields per lane (nf = 32 U) known at compile time: no predication
+// One rank column of an A item: this lane's share of X_i^T x over the chunk.
+// U = fields per lane (nf == 32 U) known at compile time, or 0 (predicated).
 template <int MODE, int U>
-__device__ __forceinline__ double a_column_full(const uint32_t* seg, const ColPar& c, unsigned lane,
-                                                const double (&xv)[kAChunk / 32]) {
-    const unsigned w = par_w(c);
+__device__ __forceinline__ double a_col(const uint32_t* seg, uint32_t pw, unsigned lane, unsigned nf,
+                                        const double (&xv)[kAChunk / 32]) {
+    const ColPar c = col_of<MODE>(pw);
+    const unsigned w = pw & 0xffu;
     const unsigned bit = lane * w;
     const uint32_t* sp = seg + (bit >> 5);
     const unsigned sh = bit & 31u;
     double acc0 = 0.0, acc1 = 0.0;
+    if (U > 0) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-        double cs;
-        const double d = dec<MODE>(sp + u * w, c, sh, xv[u], cs);
-        if (u & 1) acc1 = fma(d, cs, acc1);
-        else acc0 = fma(d, cs, acc0);
+        for (int u = 0; u < U; ++u) {
+            const double d = dec<MODE>(sp + u * w, c, sh);
+            if (u & 1) acc1 = fma(d, xv[u], acc1);
+            else acc0 = fma(d, xv[u], acc0);
+        }
+    } else {
+        const unsigned nu = (nf + 31) >> 5;
+#pragma unroll
+        for (int u = 0; u < kAChunk / 32; ++u) {
+            if (static_cast<unsigned>(u) < nu && lane + 32u * u < nf) acc0 = fma(dec<MODE>(sp + u * w, c, sh), xv[u], acc0);
+        }
     }
     return acc0 + acc1;
 }
 
-template <int MODE>
-__device__ __forceinline__ double a_column(const uint32_t* seg, const ColPar& c, unsigned lane, unsigned nf,
-                                           const double (&xv)[kAChunk / 32]) {
-    const unsigned w = par_w(c);
-    const unsigned bit = lane * w;
-    const uint32_t* sp = seg + (bit >> 5);
-    const unsigned sh = bit & 31u;
-    double acc = 0.0;
-    const unsigned U = (nf + 31) >> 5;
+// the item's columns (<= kAGroup, unrolled so the sums stay in registers)
+template <int MODE, int U>
+__device__ __forceinline__ void a_cols(const uint32_t* pk, unsigned nseg, unsigned nf, unsigned lane,
+                                       const double (&xv)[kAChunk / 32], double (&a)[kAGroup]) {
+    const uint32_t* seg = pk + nseg;  // packed column layouts precede the segments
 #pragma unroll
-    for (int u = 0; u < kAChunk / 32; ++u) {
-        if (static_cast<unsigned>(u) < U) {
-            if (lane + 32u * u < nf) {
-                double cs;
-                const double d = dec<MODE>(sp + u * w, c, sh, xv[u], cs);
-                acc = fma(d, cs, acc);
-            }
+    for (int c = 0; c < kAGroup; ++c) {
+        if (static_cast<unsigned>(c) < nseg) {
+            const uint32_t pw = pk[c];
+            a[c] = a_col<MODE, U>(seg, pw, lane, nf, xv);
+            seg += (nf * (pw & 0xffu) + 31) >> 5;
         }
     }
-    return acc;
 }
 
 template <int MODE>
-__device__ __forceinline__ double a_dispatch_u(const uint32_t* seg, const ColPar& c, unsigned lane, unsigned nf,
-                                               const double (&xv)[kAChunk / 32]) {
+__device__ __forceinline__ void a_cols_u(const uint32_t* pk, unsigned nseg, unsigned nf, unsigned lane,
+                                         const double (&xv)[kAChunk / 32], double (&a)[kAGroup]) {
     switch (nf) {
-        case 256: return a_column_full<MODE, 8>(seg, c, lane, xv);
-        case 128: return a_column_full<MODE, 4>(seg, c, lane, xv);
-        case 64: return a_column_full<MODE, 2>(seg, c, lane, xv);
-        default: return a_column<MODE>(seg, c, lane, nf, xv);
+        case 256: a_cols<MODE, 8>(pk, nseg, nf, lane, xv, a); break;
+        case 128: a_cols<MODE, 4>(pk, nseg, nf, lane, xv, a); break;
+        case 64: a_cols<MODE, 2>(pk, nseg, nf, lane, xv, a); break;
+        default: a_cols<MODE, 0>(pk, nseg, nf, lane, xv, a); break;
     }
 }
 
-__device__ __forceinline__ void a_item(const Params& p, const AItem& it, const uint8_t* slot, unsigned lane) {
+// Transposed warp reduction of four per-lane sums: afterwards lane 8 c holds
+// the warp total of a[c] (fixed order: deterministic).
+__device__ __forceinline__ double reduce4(const double (&a)[kAGroup], unsigned lane) {
+    static_assert(kAGroup == 4, "reduce4 assumes four columns per A item");
+    const bool up = lane & 16u;
+    double k0 = up ? a[2] : a[0], k1 = up ? a[3] : a[1];
+    const double s0 = up ? a[0] : a[2], s1 = up ? a[1] : a[3];
+    k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+    k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+    const bool b3 = lane & 8u;
+    double k = b3 ? k1 : k0;
+    k += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+    k += __shfl_xor_sync(0xffffffffu, k, 4);
+    k += __shfl_xor_sync(0xffffffffu, k, 2);
+    k += __shfl_xor_sync(0xffffffffu, k, 1);
+    return k;
+}
+
+// A multi-chunk leaf's arrival (atom issued by lane 0); resolved one item
+// later so the atomic's latency hides behind the next item's decode.
+struct APend {
+    unsigned old = 0, need = 0, leaf = 0, colbase = 0, k = 0, nchunks = 0, pbase = 0;
+    bool on = false;
+};
+
+__device__ __forceinline__ void a_resolve(const Params& p, APend& q, unsigned lane) {
+    if (!q.on) return;
+    q.on = false;
+    const unsigned last = __shfl_sync(0xffffffffu, q.old == q.need ? 1u : 0u, 0);
+    if (!last) return;
+    __syncwarp();
+    // every chunk is in: sum in fixed chunk order (deterministic)
+    for (unsigned i = lane; i < q.k; i += 32) {
+        double s = 0.0;
+        for (unsigned ch = 0; ch < q.nchunks; ++ch) s += __ldcg(p.partial + q.pbase + ch * q.k + i);
+        p.c[q.colbase + i] = p.alpha * __ldg(p.coef + q.colbase + i) * s;
+    }
+    if (lane == 0) p.counter[q.leaf] = 0u;  // re-armed for the next product
+}
+
+__device__ __forceinline__ void a_item(const Params& p, const AItem& it, const uint8_t* slot, unsigned lane,
+                                       APend& pend) {
     const unsigned nseg = it.nseg, nf = it.nf;
+    const unsigned cl = lane >> 3;
+    const bool writer = (lane & 7u) == 0 && cl < nseg;
+    double cf = 0.0;
+    if (writer && it.nchunks == 1) cf = __ldg(p.coef + it.xcol + cl);  // in flight during the decode
     const double* xs = reinterpret_cast<const double*>(slot + kOffCoef + it.x_off);
-    const uint32_t* pk = reinterpret_cast<const uint32_t*>(slot) + it.word_off;  // packed column layouts
+    const uint32_t* pk = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
     double xv[kAChunk / 32];
     const unsigned U = (nf + 31) >> 5;
 #pragma unroll
@@ -531,131 +571,59 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
         const unsigned f = lane + 32u * u;
         xv[u] = (static_cast<unsigned>(u) < U && f < nf) ? xs[f] : 0.0;
     }
-    const uint32_t* seg = pk + nseg;
-    double res = 0.0;
-    for (unsigned c = 0; c < nseg; ++c) {
-        const ColPar col = make_par(pk[c]);
-        double acc;
-        switch (par_mode(col)) {
-            case 0: acc = a_dispatch_u<0>(seg, col, lane, nf, xv); break;
-            case 1: acc = a_dispatch_u<1>(seg, col, lane, nf, xv); break;
-            default: acc = a_dispatch_u<2>(seg, col, lane, nf, xv); break;
-        }
-        acc = warp_sum(acc);
-        if (lane == c) res = acc;
-        seg += (nf * par_w(col) + 31) >> 5;
+    double a[kAGroup];
+#pragma unroll
+    for (int c = 0; c < kAGroup; ++c) a[c] = 0.0;
+    switch (it.mode) {
+        case 0: a_cols_u<0>(pk, nseg, nf, lane, xv, a); break;
+        case 1: a_cols_u<1>(pk, nseg, nf, lane, xv, a); break;
+        default: a_cols_u<2>(pk, nseg, nf, lane, xv, a); break;
     }
-    const LeafA L = p.leafa[it.leaf];
-    if (L.nchunks == 1) {
-        if (lane < nseg) p.c[it.xcol + lane] = p.alpha * __ldg(p.coef + it.xcol + lane) * res;
+    const double r = reduce4(a, lane);
+    a_resolve(p, pend, lane);  // the previous item's arrival, long since returned
+    if (it.nchunks == 1) {
+        if (writer) p.c[it.xcol + cl] = p.alpha * cf * r;
         return;
     }
-    if (lane < nseg) p.partial[L.pbase + static_cast<uint32_t>(it.chunk) * L.k + it.icol0 + lane] = res;
+    if (writer) p.partial[it.pbase + static_cast<uint32_t>(it.chunk) * it.k + it.icol0 + cl] = r;
     __syncwarp();
-    unsigned last = 0;
-    if (lane == 0) {  // release our partials, acquire everyone else's (partials are read from L2)
+    if (lane == 0) {  // release our partials; acquire everyone else's when we turn out last
         unsigned old;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.counter + it.leaf) : "memory");
-        last = old == L.nitems - 1;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;"
+                     : "=r"(old)
+                     : "l"(p.counter + it.leaf), "r"(nseg)
+                     : "memory");
+        pend.old = old + nseg;
     }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) {  // every chunk is in: sum in fixed chunk order (deterministic)
-        for (unsigned i = lane; i < L.k; i += 32) {
-            double s = 0.0;
-            for (unsigned ch = 0; ch < L.nchunks; ++ch) s += __ldcg(p.partial + L.pbase + ch * L.k + i);
-            p.c[L.colbase + i] = p.alpha * __ldg(p.coef + L.colbase + i) * s;
-        }
-        if (lane == 0) p.counter[it.leaf] = 0u;  // re-armed for the next product
-    }
+    pend.need = static_cast<unsigned>(it.k) * it.nchunks;
+    pend.leaf = it.leaf;
+    pend.colbase = it.xcol - it.icol0;
+    pend.k = it.k;
+    pend.nchunks = it.nchunks;
+    pend.pbase = it.pbase;
+    pend.on = true;
 }
 
 // ------------------------------------------------------------ phase B ----
 // generic path: any row offset / count (lanes individually predicated)
 template <int MODE>
-__device__ __forceinline__ void b_column(const uint32_t* seg, const ColPar& c, int f0, unsigned vmask,
+__device__ __forceinline__ void b_column(const uint32_t* seg, const ColPar& c, unsigned w, int f0, unsigned vmask,
                                          unsigned umask, double coef, double (&acc)[kG]) {
-    const unsigned w = par_w(c);
     const int bit0 = f0 * static_cast<int>(w);
     const uint32_t* sp = seg + (bit0 >> 5);
     const unsigned sh = static_cast<unsigned>(bit0) & 31u;
 #pragma unroll
     for (int g = 0; g < kG; ++g) {
         if (umask & (1u << g)) {
-            if (vmask & (1u << g)) {
-                double cs;
-                const double d = dec<MODE>(sp + g * w, c, sh, coef, cs);
-                acc[g] = fma(d, cs, acc[g]);
-            }
+            if (vmask & (1u << g)) acc[g] = fma(dec<MODE>(sp + g * w, c, sh), coef, acc[g]);
         }
     }
 }
 
-// fast path: the item covers row groups [GLO, GHI) of the block completely, so
-// every lane decodes one field per group with no predication
-template <int MODE, int GLO, int GHI>
-__device__ __forceinline__ void b_column_full(const uint32_t* sp, const ColPar& c, unsigned sh, double coef,
-                                              double (&acc)[kG]) {
-    const unsigned w = par_w(c);
-#pragma unroll
-    for (int g = GLO; g < GHI; ++g) {
-        double cs;
-        const double d = dec<MODE>(sp + (g - GLO) * w, c, sh, coef, cs);
-        acc[g] = fma(d, cs, acc[g]);
-    }
-}
-
-// dense item, one layout: the mode is fixed for the whole column loop
-template <int MODE, int GLO, int GHI>
-__device__ __forceinline__ void b_dense_full(const uint32_t* sp, const ColPar& col, unsigned sh, unsigned segw,
-                                             const double* cf, double dmul, unsigned nseg, double (&acc)[kG]) {
-#pragma unroll 2
-    for (unsigned c = 0; c < nseg; ++c) {
-        b_column_full<MODE, GLO, GHI>(sp, col, sh, dmul * cf[c], acc);
-        sp += segw;
-    }
-}
-
-template <int GLO, int GHI>
-__device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg, const uint8_t* cbase,
-                                            unsigned lane, double dmul, double (&acc)[kG]) {
-    const unsigned nseg = it.nseg;
-    constexpr unsigned nr = 32 * (GHI - GLO);
-    const double* cf = reinterpret_cast<const double*>(cbase);
-    if (it.kind == 0) {  // dense: one layout for the whole item
-        const ColPar col = make_par(it.dpacked);
-        const unsigned w = par_w(col);
-        const unsigned bit = lane * w;
-        const uint32_t* sp = seg + (bit >> 5);
-        const unsigned sh = bit & 31u;
-        const unsigned segw = (nr * w + 31) >> 5;
-        switch (par_mode(col)) {
-            case 0: b_dense_full<0, GLO, GHI>(sp, col, sh, segw, cf, dmul, nseg, acc); break;
-            case 1: b_dense_full<1, GLO, GHI>(sp, col, sh, segw, cf, dmul, nseg, acc); break;
-            default: b_dense_full<2, GLO, GHI>(sp, col, sh, segw, cf, dmul, nseg, acc); break;
-        }
-    } else {
-        const uint32_t* pk = seg - nseg;  // packed column layouts precede the segments
-        for (unsigned c = 0; c < nseg; ++c) {
-            const ColPar col = make_par(pk[c]);
-            const double cc = cf[c];
-            const unsigned w = par_w(col);
-            const unsigned bit = lane * w;
-            const uint32_t* sp = seg + (bit >> 5);
-            const unsigned sh = bit & 31u;
-            const unsigned mode = par_mode(col);
-            if (mode == 0) b_column_full<0, GLO, GHI>(sp, col, sh, cc, acc);
-            else if (mode == 1) b_column_full<1, GLO, GHI>(sp, col, sh, cc, acc);
-            else b_column_full<2, GLO, GHI>(sp, col, sh, cc, acc);
-            seg += (nr * w + 31) >> 5;
-        }
-    }
-}
-
-__device__ __forceinline__ void b_item(const Params& p, const BItem& it, const uint8_t* slot, unsigned lane,
-                                       double (&acc)[kG]) {
+template <int MODE>
+__device__ __forceinline__ void b_item_generic(const BItem& it, const uint32_t* seg, const double* cf, unsigned lane,
+                                               double dmul, double (&acc)[kG]) {
     const unsigned nseg = it.nseg, nr = it.nr;
-    const uint8_t* cbase = slot + kOffCoef + it.coef_off;
-    const double dmul = p.alpha * it.scale;  // dense: alpha * buffer scale folded into x
     // lane owns rows 32 g + lane of the block; field index f0 + 32 g in each segment
     const int f0 = static_cast<int>(lane) - static_cast<int>(it.ra);
     unsigned vmask = 0;
@@ -665,32 +633,79 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
         if (f >= 0 && f < static_cast<int>(nr)) vmask |= 1u << g;
     }
     const unsigned umask = __reduce_or_sync(0xffffffffu, vmask);
-    const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off + (it.kind ? nseg : 0u);
-    if (__all_sync(0xffffffffu, vmask == umask)) {
-        static_assert(kG == 4, "fast-path table assumes 128-row blocks");
-        switch (umask) {
-            case 0x3: b_item_full<0, 2>(it, seg, cbase, lane, dmul, acc); return;
-            case 0xc: b_item_full<2, 4>(it, seg, cbase, lane, dmul, acc); return;
-            case 0xf: b_item_full<0, 4>(it, seg, cbase, lane, dmul, acc); return;
-            case 0x1: b_item_full<0, 1>(it, seg, cbase, lane, dmul, acc); return;
-            case 0x2: b_item_full<1, 2>(it, seg, cbase, lane, dmul, acc); return;
-            case 0x4: b_item_full<2, 3>(it, seg, cbase, lane, dmul, acc); return;
-            case 0x8: b_item_full<3, 4>(it, seg, cbase, lane, dmul, acc); return;
-            default: break;
+    const uint32_t* pk = seg - nseg;
+    for (unsigned c = 0; c < nseg; ++c) {
+        const uint32_t pw = it.kind == 0 ? it.dpacked : pk[c];
+        const ColPar col = col_of<MODE>(pw);
+        const unsigned w = pw & 0xffu;
+        const double cc = it.kind == 0 ? dmul * cf[c] : cf[c];
+        b_column<MODE>(seg, col, w, f0, vmask, umask, cc, acc);
+        seg += (nr * w + 31) >> 5;
+    }
+}
+
+// fast path: the item covers row groups [GLO, GHI) of the block completely, so
+// every lane decodes one field per group with no predication
+template <int MODE, int GLO, int GHI>
+__device__ __forceinline__ void b_column_full(const uint32_t* sp, const ColPar& c, unsigned w, unsigned sh,
+                                              double coef, double (&acc)[kG]) {
+#pragma unroll
+    for (int g = GLO; g < GHI; ++g) acc[g] = fma(dec<MODE>(sp + (g - GLO) * w, c, sh), coef, acc[g]);
+}
+
+template <int MODE, int GLO, int GHI>
+__device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg, const double* cf, unsigned lane,
+                                            double dmul, double (&acc)[kG]) {
+    const unsigned nseg = it.nseg;
+    if (it.kind == 0) {  // dense: one layout for the whole item
+        const ColPar col = col_of<MODE>(it.dpacked);
+        const unsigned w = it.dpacked & 0xffu;
+        const unsigned bit = lane * w;
+        const uint32_t* sp = seg + (bit >> 5);
+        const unsigned sh = bit & 31u, segw = (GHI - GLO) * w;
+#pragma unroll 2
+        for (unsigned c = 0; c < nseg; ++c) {
+            b_column_full<MODE, GLO, GHI>(sp, col, w, sh, dmul * cf[c], acc);
+            sp += segw;
+        }
+    } else {
+        const uint32_t* pk = seg - nseg;  // packed column layouts precede the segments
+        for (unsigned c = 0; c < nseg; ++c) {
+            const uint32_t pw = pk[c];
+            const ColPar col = col_of<MODE>(pw);
+            const unsigned w = pw & 0xffu;
+            const unsigned bit = lane * w;
+            b_column_full<MODE, GLO, GHI>(seg + (bit >> 5), col, w, bit & 31u, cf[c], acc);
+            seg += (GHI - GLO) * w;
         }
     }
-    const double* cf = reinterpret_cast<const double*>(cbase);
-    const uint32_t* pk = seg - nseg;
-    const ColPar dpar = make_par(it.dpacked);
-    for (unsigned c = 0; c < nseg; ++c) {
-        const ColPar col = it.kind == 0 ? dpar : make_par(pk[c]);
-        const double cc = it.kind == 0 ? dmul * cf[c] : cf[c];
-        switch (par_mode(col)) {
-            case 0: b_column<0>(seg, col, f0, vmask, umask, cc, acc); break;
-            case 1: b_column<1>(seg, col, f0, vmask, umask, cc, acc); break;
-            default: b_column<2>(seg, col, f0, vmask, umask, cc, acc); break;
-        }
-        seg += (nr * par_w(col) + 31) >> 5;
+}
+
+template <int MODE>
+__device__ __forceinline__ void b_item_mode(const BItem& it, const uint32_t* seg, const double* cf, unsigned lane,
+                                            double dmul, double (&acc)[kG]) {
+    static_assert(kG == 4, "fast-path table assumes 128-row blocks");
+    switch (it.fcase) {
+        case 0x04: b_item_full<MODE, 0, 4>(it, seg, cf, lane, dmul, acc); return;
+        case 0x02: b_item_full<MODE, 0, 2>(it, seg, cf, lane, dmul, acc); return;
+        case 0x24: b_item_full<MODE, 2, 4>(it, seg, cf, lane, dmul, acc); return;
+        case 0x01: b_item_full<MODE, 0, 1>(it, seg, cf, lane, dmul, acc); return;
+        case 0x12: b_item_full<MODE, 1, 2>(it, seg, cf, lane, dmul, acc); return;
+        case 0x23: b_item_full<MODE, 2, 3>(it, seg, cf, lane, dmul, acc); return;
+        case 0x34: b_item_full<MODE, 3, 4>(it, seg, cf, lane, dmul, acc); return;
+        default: b_item_generic<MODE>(it, seg, cf, lane, dmul, acc); return;
+    }
+}
+
+__device__ __forceinline__ void b_item(const Params& p, const BItem& it, const uint8_t* slot, unsigned lane,
+                                       double (&acc)[kG]) {
+    const double* cf = reinterpret_cast<const double*>(slot + kOffCoef + it.coef_off);
+    const double dmul = p.alpha * it.scale;  // dense: alpha * buffer scale folded into x
+    const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off + (it.kind ? it.nseg : 0u);
+    switch (it.mode) {
+        case 0: b_item_mode<0>(it, seg, cf, lane, dmul, acc); break;
+        case 1: b_item_mode<1>(it, seg, cf, lane, dmul, acc); break;
+        default: b_item_mode<2>(it, seg, cf, lane, dmul, acc); break;
     }
 }
 
@@ -709,13 +724,15 @@ __global__ void __launch_bounds__(kThreadsA, 2) k_phase_a(Params p) {
         producer<true>(p, smem, full, empty, lane);
         return;
     }
+    APend pend;
     consume<kNWA>(
         smem, full, empty, warp, lane, p.debug,
         [&](const uint8_t* base, unsigned b, unsigned e) {
             const AItem* items = reinterpret_cast<const AItem*>(base + kOffDesc);
-            for (unsigned i = b; i < e; ++i) a_item(p, items[i], base, lane);
+            for (unsigned i = b; i < e; ++i) a_item(p, items[i], base, lane, pend);
         },
         [](uint32_t) {});
+    a_resolve(p, pend, lane);
 }
 
 __global__ void __launch_bounds__(kThreadsB, 2) k_phase_b(Params p) {
@@ -810,7 +827,7 @@ using namespace hcmx_gpu;
 
 struct hcmx_hmat {
     uint64_t n_rows = 0, n_cols = 0, rb = 0, re = 0;
-    DevBuf arena, stages, stage_wb, stripe_a, stripe_b, copies, work, bitems, aitems, leafa, colw, colx, coef, c, partial,
+    DevBuf arena, stages, stage_wb, stripe_a, stripe_b, copies, work, bitems, aitems, colw, colx, coef, c, partial,
         counter, xpad, xbuf, ybuf;
     uint32_t nstripe_a = 0, nblocks = 0, nlr = 0;
     hcmx_memory_report report{};
@@ -861,12 +878,23 @@ void drain_timing(hcmx_hmat* h) {
 ColPar col_par(const hcmx_descriptor& x) {
     ColPar c{};
     const unsigned w = x.bit_width, m = x.mant_bits, e = x.exp_bits, em = e + m;
-    const unsigned mode = (w > 32 || e == 11) ? 2u : (m <= 20 ? 0u : 1u);
+    const unsigned mode = (w > 32 || e >= 11 || w != 1 + em) ? 2u : (m <= 20 ? 0u : 1u);
     c.mask_em = em >= 32 ? 0xffffffffu : ((1u << em) - 1u);
     c.mul_rsh = mode == 0 ? (1u << (20 - m)) : (mode == 1 ? m - 20 : 0u);
     c.packed = w | (m << 8) | (e << 16) | (mode << 24);
     c.sgn_sh = em <= 31 ? 31 - em : 0u;
     return c;
+}
+
+// fast-path case of a phase-B item covering rows [ra, ra + nr) of its block
+uint8_t fcase_of(uint64_t ra, uint64_t nr) {
+    if (ra % 32 || nr % 32) return 0;
+    const unsigned lo = static_cast<unsigned>(ra / 32), hi = static_cast<unsigned>((ra + nr) / 32);
+    const unsigned c = lo << 4 | hi;
+    switch (c) {
+        case 0x04: case 0x02: case 0x24: case 0x01: case 0x12: case 0x23: case 0x34: return static_cast<uint8_t>(c);
+        default: return 0;
+    }
 }
 
 inline uint32_t r16(uint64_t x) { return static_cast<uint32_t>((x + 15) & ~uint64_t(15)); }
@@ -950,8 +978,6 @@ struct Builder {
     // pace of the slowest warp).  Inside a piece, consecutive columns of one
     // leaf / row range (B) or leaf chunk (A) merge into items of <= MAXC
     // columns.  Phase-A items of one chunk in a stage share one staged x slice.
-    std::vector<uint32_t> a_items_per_leaf;
-
     template <class Item, int NW, int MAXC>
     void emit_stripe(std::vector<Spec<Item>>& specs, std::vector<Item>& items) {
         constexpr bool IS_A = std::is_same<Item, AItem>::value;
@@ -1051,7 +1077,6 @@ struct Builder {
                     for (size_t k = b.first; k < b.first + b.n; ++k) arena.push_back(specs[k].param);
                 for (size_t k = b.first; k < b.first + b.n; ++k)
                     for (uint32_t q = 0; q < specs[k].nseg; ++q) put_fields(segs[specs[k].seg0 + q]);
-                if constexpr (IS_A) a_items_per_leaf[b.it.leaf]++;
                 items.push_back(b.it);
                 ++cnt;
             }
@@ -1162,7 +1187,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
             L.colbase = static_cast<uint32_t>(colw.size());
             L.k = k;
             L.nchunks = static_cast<uint32_t>((cols + kAChunk - 1) / kAChunk);
-            L.nitems = L.nchunks * ((k + kAGroup - 1) / kAGroup);
+            if (k >= (1u << 16) || L.nchunks >= (1u << 16)) throw invalid_argument("hmat: lowrank leaf too large");
             L.pbase = static_cast<uint32_t>(npartial);
             if (L.nchunks > 1) npartial += static_cast<uint64_t>(L.nchunks) * k;
             leafa.push_back(L);
@@ -1194,7 +1219,6 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     // stripes of ~kAStripeBytes, one chunk (all its rank-column groups) per warp
     uint32_t nstripe_a = 0;
     std::vector<uint32_t> stripe_a = {0};
-    B.a_items_per_leaf.assign(leafa.size(), 0);
     {
         std::vector<Spec<AItem>> specs;
         uint64_t stripe_bytes = 0, unit = 0;
@@ -1226,20 +1250,24 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                     AItem& it = sp.it;
                     it.nseg = static_cast<uint8_t>(ng);
                     it.nf = static_cast<uint16_t>(nf);
-                    it.xidx = static_cast<uint32_t>(d.col0[l] + f0);
+                    const uint32_t xidx = static_cast<uint32_t>(d.col0[l] + f0);
                     it.xcol = L.colbase + g;
                     it.leaf = static_cast<uint32_t>(lr_id[l]);
                     it.chunk = static_cast<uint16_t>(ch);
                     it.icol0 = static_cast<uint16_t>(g);
+                    it.k = static_cast<uint16_t>(L.k);
+                    it.nchunks = static_cast<uint16_t>(L.nchunks);
+                    it.pbase = L.pbase;
                     sp.words += ng;  // packed column layout word
                     sp.param = col_par(d.desc[d.buf0[l] + L.k + g]).packed;
-                    sp.elem = it.xidx;
+                    it.mode = static_cast<uint8_t>(sp.param >> 24);
+                    sp.elem = xidx;
                     sp.sl_table = 0;  // x slice of the chunk
-                    sp.sl_start = it.xidx;
+                    sp.sl_start = xidx;
                     sp.sl_count = static_cast<uint32_t>(nf);
                     sp.cost = nf * ng;
-                    sp.unit = unit;
-                    sp.xidx = it.xidx;
+                    sp.unit = unit * 4 + it.mode;  // items never mix decode modes
+                    sp.xidx = xidx;
                     sp.nf = static_cast<uint32_t>(nf);
                     stripe_bytes += sp.words * 4;
                     specs.push_back(sp);
@@ -1250,7 +1278,6 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         flush();
     }
     rep.stages_a = B.stages.size();
-    for (size_t i = 0; i < leafa.size(); ++i) leafa[i].nitems = B.a_items_per_leaf[i];
 
     // ---- phase B: one stripe per block of kR rows
     const uint64_t nblocks = (h->re - h->rb + kR - 1) / kR;
@@ -1294,13 +1321,15 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                         it.ra = static_cast<uint8_t>(r0 - b0);
                         it.nr = static_cast<uint8_t>(nr);
                         it.dpacked = col_par(d.desc[b]).packed;
+                        it.mode = static_cast<uint8_t>(it.dpacked >> 24);
+                        it.fcase = fcase_of(r0 - b0, nr);
                         it.scale = d.desc[b].scale;
                         sp.elem = it.src;
                         sp.sl_table = 0;  // x slice of the dense leaf's columns
                         sp.sl_start = static_cast<uint32_t>(d.col0[l]);
                         sp.sl_count = static_cast<uint32_t>(cols);
                         sp.cost = nc * nr;
-                        sp.unit = unit;
+                        sp.unit = unit * 4 + it.mode;
                         specs.push_back(sp);
                     }
                 } else {
@@ -1323,12 +1352,14 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                         it.src = L.colbase + g;
                         sp.words += ng;  // packed column layout word
                         sp.param = col_par(d.desc[d.buf0[l] + g]).packed;
+                        it.mode = static_cast<uint8_t>(sp.param >> 24);
+                        it.fcase = fcase_of(r0 - b0, nr);
                         sp.elem = it.src;
                         sp.sl_table = 1;  // phase-A results of the leaf
                         sp.sl_start = L.colbase;
                         sp.sl_count = L.k;
                         sp.cost = ng * nr;
-                        sp.unit = unit;
+                        sp.unit = unit * 4 + it.mode;  // items never mix decode modes
                         specs.push_back(sp);
                     }
                 }
@@ -1359,7 +1390,6 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     up(h->stripe_b, stripe_b.data(), stripe_b.size() * 4);
     up(h->bitems, B.bitems.data(), B.bitems.size() * sizeof(BItem));
     up(h->aitems, B.aitems.data(), B.aitems.size() * sizeof(AItem));
-    up(h->leafa, leafa.data(), leafa.size() * sizeof(LeafA));
     up(h->colw, colw.data(), colw.size() * sizeof(ColPar));
     up(h->colx, colx.data(), colx.size() * sizeof(ColPar));
     up(h->coef, coef.data(), coef.size() * 8);
@@ -1375,7 +1405,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     h->nblocks = static_cast<uint32_t>(nblocks);
     rep.device_arena_bytes = B.arena.size() * 4;
     rep.device_table_bytes = B.stages.size() * (sizeof(Stage) + 48 + kCopies * 8) + B.bitems.size() * sizeof(BItem) +
-                             B.aitems.size() * sizeof(AItem) + leafa.size() * sizeof(LeafA) +
+                             B.aitems.size() * sizeof(AItem) +
                              colw.size() * 2 * sizeof(ColPar) + coef.size() * 16;
     rep.overhead = rep.device_table_bytes;
 }
@@ -1393,7 +1423,6 @@ Params make_params(hcmx_hmat* h, double alpha, double beta, double* y) {
     p.nblocks = h->nblocks;
     p.bitems = h->bitems.as<BItem>();
     p.aitems = h->aitems.as<AItem>();
-    p.leafa = h->leafa.as<LeafA>();
     p.colw_par = h->colw.as<ColPar>();
     p.colx_par = h->colx.as<ColPar>();
     p.coef = h->coef.as<double>();
