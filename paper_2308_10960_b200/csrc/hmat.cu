@@ -128,7 +128,7 @@ struct AItem {
     uint32_t x_off;      // staged x value of field 0 (coef-area bytes)
     uint32_t pbase;      // partials of the leaf (nchunks > 1)
     uint32_t xcol;       // global X column id of the first rank column
-    uint32_t leaf;       // lowrank-leaf id (arrival counter)
+    uint32_t leaf;       // lowrank-leaf id
     uint16_t k;          // leaf rank
     uint16_t nchunks;    // column chunks of the leaf
     uint16_t chunk;      // column-chunk index within the leaf
@@ -159,7 +159,6 @@ struct Params {
     const double* coef;         // sigma_i * scale_X_i * scale_W_i
     double* c;                  // alpha * coef * (X^T x)_i, written by phase A
     double* partial;
-    unsigned* counter;
     const double* x;            // padded internal copy (16-byte aligned, readable + 16 B)
     double* y;
     uint32_t row_begin, row_end;
@@ -504,17 +503,6 @@ __device__ __forceinline__ void a_cols(const uint32_t* pk, unsigned nseg, unsign
     }
 }
 
-template <int MODE>
-__device__ __forceinline__ void a_cols_u(const uint32_t* pk, unsigned nseg, unsigned nf, unsigned lane,
-                                         const double (&xv)[kAChunk / 32], double (&a)[kAGroup]) {
-    switch (nf) {
-        case 256: a_cols<MODE, 8>(pk, nseg, nf, lane, xv, a); break;
-        case 128: a_cols<MODE, 4>(pk, nseg, nf, lane, xv, a); break;
-        case 64: a_cols<MODE, 2>(pk, nseg, nf, lane, xv, a); break;
-        default: a_cols<MODE, 0>(pk, nseg, nf, lane, xv, a); break;
-    }
-}
-
 // Transposed warp reduction of four per-lane sums: afterwards lane 8 c holds
 // the warp total of a[c] (fixed order: deterministic).
 __device__ __forceinline__ double reduce4(const double (&a)[kAGroup], unsigned lane) {
@@ -533,30 +521,16 @@ __device__ __forceinline__ double reduce4(const double (&a)[kAGroup], unsigned l
     return k;
 }
 
-// A multi-chunk leaf's arrival (atom issued by lane 0); resolved one item
-// later so the atomic's latency hides behind the next item's decode.
-struct APend {
-    unsigned old = 0, need = 0, leaf = 0, colbase = 0, k = 0, nchunks = 0, pbase = 0;
-    bool on = false;
+// A leaf wider than one chunk: every chunk item writes partial sums, k_reduce
+// (launched between the phases) adds them in fixed chunk order.
+struct RedCol {
+    uint32_t col;      // global column id (C index)
+    uint32_t p0;       // partial of chunk 0
+    uint32_t stride;   // leaf rank k (partials are chunk-major)
+    uint32_t nchunks;
 };
 
-__device__ __forceinline__ void a_resolve(const Params& p, APend& q, unsigned lane) {
-    if (!q.on) return;
-    q.on = false;
-    const unsigned last = __shfl_sync(0xffffffffu, q.old == q.need ? 1u : 0u, 0);
-    if (!last) return;
-    __syncwarp();
-    // every chunk is in: sum in fixed chunk order (deterministic)
-    for (unsigned i = lane; i < q.k; i += 32) {
-        double s = 0.0;
-        for (unsigned ch = 0; ch < q.nchunks; ++ch) s += __ldcg(p.partial + q.pbase + ch * q.k + i);
-        p.c[q.colbase + i] = p.alpha * __ldg(p.coef + q.colbase + i) * s;
-    }
-    if (lane == 0) p.counter[q.leaf] = 0u;  // re-armed for the next product
-}
-
-__device__ __forceinline__ void a_item(const Params& p, const AItem& it, const uint8_t* slot, unsigned lane,
-                                       APend& pend) {
+__device__ __forceinline__ void a_item(const Params& p, const AItem& it, const uint8_t* slot, unsigned lane) {
     const unsigned nseg = it.nseg, nf = it.nf;
     const unsigned cl = lane >> 3;
     const bool writer = (lane & 7u) == 0 && cl < nseg;
@@ -574,34 +548,32 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
     double a[kAGroup];
 #pragma unroll
     for (int c = 0; c < kAGroup; ++c) a[c] = 0.0;
-    switch (it.mode) {
-        case 0: a_cols_u<0>(pk, nseg, nf, lane, xv, a); break;
-        case 1: a_cols_u<1>(pk, nseg, nf, lane, xv, a); break;
-        default: a_cols_u<2>(pk, nseg, nf, lane, xv, a); break;
+    // fast bodies for modes 0/1 at the chunk sizes 64-row leaf clusters give;
+    // mode 2 (e = 11 or w > 32) and ragged chunks take one generic body (the
+    // mode-2 decoder is exact for every layout; keeps the kernel small)
+    const unsigned ui = nf == 256 ? 3u : nf == 128 ? 2u : nf == 64 ? 1u : 0u;
+    switch (it.mode == 2 || ui == 0 ? 0u : ui + 3u * it.mode) {
+        case 3: a_cols<0, 8>(pk, nseg, nf, lane, xv, a); break;
+        case 2: a_cols<0, 4>(pk, nseg, nf, lane, xv, a); break;
+        case 1: a_cols<0, 2>(pk, nseg, nf, lane, xv, a); break;
+        case 6: a_cols<1, 8>(pk, nseg, nf, lane, xv, a); break;
+        case 5: a_cols<1, 4>(pk, nseg, nf, lane, xv, a); break;
+        case 4: a_cols<1, 2>(pk, nseg, nf, lane, xv, a); break;
+        default: a_cols<2, 0>(pk, nseg, nf, lane, xv, a); break;
     }
     const double r = reduce4(a, lane);
-    a_resolve(p, pend, lane);  // the previous item's arrival, long since returned
-    if (it.nchunks == 1) {
-        if (writer) p.c[it.xcol + cl] = p.alpha * cf * r;
-        return;
+    if (!writer) return;
+    if (it.nchunks == 1) p.c[it.xcol + cl] = p.alpha * cf * r;
+    else p.partial[it.pbase + static_cast<uint32_t>(it.chunk) * it.k + it.icol0 + cl] = r;
+}
+
+__global__ void k_reduce(Params p, const RedCol* rc, uint32_t n) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const RedCol r = rc[i];
+        double s = 0.0;
+        for (uint32_t ch = 0; ch < r.nchunks; ++ch) s += p.partial[r.p0 + ch * r.stride];
+        p.c[r.col] = p.alpha * p.coef[r.col] * s;
     }
-    if (writer) p.partial[it.pbase + static_cast<uint32_t>(it.chunk) * it.k + it.icol0 + cl] = r;
-    __syncwarp();
-    if (lane == 0) {  // release our partials; acquire everyone else's when we turn out last
-        unsigned old;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;"
-                     : "=r"(old)
-                     : "l"(p.counter + it.leaf), "r"(nseg)
-                     : "memory");
-        pend.old = old + nseg;
-    }
-    pend.need = static_cast<unsigned>(it.k) * it.nchunks;
-    pend.leaf = it.leaf;
-    pend.colbase = it.xcol - it.icol0;
-    pend.k = it.k;
-    pend.nchunks = it.nchunks;
-    pend.pbase = it.pbase;
-    pend.on = true;
 }
 
 // ------------------------------------------------------------ phase B ----
@@ -681,31 +653,24 @@ __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg
     }
 }
 
-template <int MODE>
-__device__ __forceinline__ void b_item_mode(const BItem& it, const uint32_t* seg, const double* cf, unsigned lane,
-                                            double dmul, double (&acc)[kG]) {
-    static_assert(kG == 4, "fast-path table assumes 128-row blocks");
-    switch (it.fcase) {
-        case 0x04: b_item_full<MODE, 0, 4>(it, seg, cf, lane, dmul, acc); return;
-        case 0x02: b_item_full<MODE, 0, 2>(it, seg, cf, lane, dmul, acc); return;
-        case 0x24: b_item_full<MODE, 2, 4>(it, seg, cf, lane, dmul, acc); return;
-        case 0x01: b_item_full<MODE, 0, 1>(it, seg, cf, lane, dmul, acc); return;
-        case 0x12: b_item_full<MODE, 1, 2>(it, seg, cf, lane, dmul, acc); return;
-        case 0x23: b_item_full<MODE, 2, 3>(it, seg, cf, lane, dmul, acc); return;
-        case 0x34: b_item_full<MODE, 3, 4>(it, seg, cf, lane, dmul, acc); return;
-        default: b_item_generic<MODE>(it, seg, cf, lane, dmul, acc); return;
-    }
-}
-
 __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const uint8_t* slot, unsigned lane,
                                        double (&acc)[kG]) {
     const double* cf = reinterpret_cast<const double*>(slot + kOffCoef + it.coef_off);
     const double dmul = p.alpha * it.scale;  // dense: alpha * buffer scale folded into x
     const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off + (it.kind ? it.nseg : 0u);
-    switch (it.mode) {
-        case 0: b_item_mode<0>(it, seg, cf, lane, dmul, acc); break;
-        case 1: b_item_mode<1>(it, seg, cf, lane, dmul, acc); break;
-        default: b_item_mode<2>(it, seg, cf, lane, dmul, acc); break;
+    // fast bodies for modes 0/1 at the shapes 64-row leaf clusters produce;
+    // everything else takes one generic body with the mode-2 decoder (exact for
+    // every layout), which keeps the kernel inside the instruction cache
+    static_assert(kG == 4, "fast-path table assumes 128-row blocks");
+    const unsigned fc = it.mode == 2 ? 0u : it.fcase;
+    switch (fc | (it.mode << 8)) {
+        case 0x004: b_item_full<0, 0, 4>(it, seg, cf, lane, dmul, acc); break;
+        case 0x002: b_item_full<0, 0, 2>(it, seg, cf, lane, dmul, acc); break;
+        case 0x024: b_item_full<0, 2, 4>(it, seg, cf, lane, dmul, acc); break;
+        case 0x104: b_item_full<1, 0, 4>(it, seg, cf, lane, dmul, acc); break;
+        case 0x102: b_item_full<1, 0, 2>(it, seg, cf, lane, dmul, acc); break;
+        case 0x124: b_item_full<1, 2, 4>(it, seg, cf, lane, dmul, acc); break;
+        default: b_item_generic<2>(it, seg, cf, lane, dmul, acc); break;
     }
 }
 
@@ -724,15 +689,13 @@ __global__ void __launch_bounds__(kThreadsA, 2) k_phase_a(Params p) {
         producer<true>(p, smem, full, empty, lane);
         return;
     }
-    APend pend;
     consume<kNWA>(
         smem, full, empty, warp, lane, p.debug,
         [&](const uint8_t* base, unsigned b, unsigned e) {
             const AItem* items = reinterpret_cast<const AItem*>(base + kOffDesc);
-            for (unsigned i = b; i < e; ++i) a_item(p, items[i], base, lane, pend);
+            for (unsigned i = b; i < e; ++i) a_item(p, items[i], base, lane);
         },
         [](uint32_t) {});
-    a_resolve(p, pend, lane);
 }
 
 __global__ void __launch_bounds__(kThreadsB, 2) k_phase_b(Params p) {
@@ -828,8 +791,8 @@ using namespace hcmx_gpu;
 struct hcmx_hmat {
     uint64_t n_rows = 0, n_cols = 0, rb = 0, re = 0;
     DevBuf arena, stages, stage_wb, stripe_a, stripe_b, copies, work, bitems, aitems, colw, colx, coef, c, partial,
-        counter, xpad, xbuf, ybuf;
-    uint32_t nstripe_a = 0, nblocks = 0, nlr = 0;
+        redcols, xpad, xbuf, ybuf;
+    uint32_t nstripe_a = 0, nblocks = 0, nlr = 0, nred = 0;
     hcmx_memory_report report{};
     std::vector<std::vector<SegRef>> segs;  // per buffer (export); empty if too big
     std::vector<hcmx_descriptor> desc;
@@ -892,7 +855,7 @@ uint8_t fcase_of(uint64_t ra, uint64_t nr) {
     const unsigned lo = static_cast<unsigned>(ra / 32), hi = static_cast<unsigned>((ra + nr) / 32);
     const unsigned c = lo << 4 | hi;
     switch (c) {
-        case 0x04: case 0x02: case 0x24: case 0x01: case 0x12: case 0x23: case 0x34: return static_cast<uint8_t>(c);
+        case 0x04: case 0x02: case 0x24: return static_cast<uint8_t>(c);
         default: return 0;
     }
 }
@@ -1165,6 +1128,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     std::vector<ColPar> colw, colx;
     std::vector<double> coef;
     uint64_t npartial = 0;
+    std::vector<RedCol> redcols;
     hcmx_memory_report& rep = h->report;
     rep = hcmx_memory_report{};
     for (uint64_t l : leaves) {
@@ -1189,7 +1153,11 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
             L.nchunks = static_cast<uint32_t>((cols + kAChunk - 1) / kAChunk);
             if (k >= (1u << 16) || L.nchunks >= (1u << 16)) throw invalid_argument("hmat: lowrank leaf too large");
             L.pbase = static_cast<uint32_t>(npartial);
-            if (L.nchunks > 1) npartial += static_cast<uint64_t>(L.nchunks) * k;
+            if (L.nchunks > 1) {
+                for (uint32_t i = 0; i < k; ++i)
+                    redcols.push_back({L.colbase + i, static_cast<uint32_t>(npartial) + i, k, L.nchunks});
+                npartial += static_cast<uint64_t>(L.nchunks) * k;
+            }
             leafa.push_back(L);
             uint64_t bytes = 8 + 8ull * k;  // APLRLowrank::byte_size (mixedprec.cpp:210-217)
             for (uint32_t i = 0; i < k; ++i) {
@@ -1398,8 +1366,8 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     h->c.alloc(std::max<size_t>(16, coef.size() * 8));
     check_cuda(cudaMemsetAsync(h->c.p, 0, h->c.bytes, s), "memset");
     h->partial.alloc(std::max<size_t>(16, npartial * 8));
-    h->counter.alloc(std::max<size_t>(16, leafa.size() * 4));
-    check_cuda(cudaMemsetAsync(h->counter.p, 0, h->counter.bytes, s), "memset");
+    up(h->redcols, redcols.data(), redcols.size() * sizeof(RedCol));
+    h->nred = static_cast<uint32_t>(redcols.size());
     stream_sync(s);
     h->nstripe_a = nstripe_a;
     h->nblocks = static_cast<uint32_t>(nblocks);
@@ -1428,7 +1396,6 @@ Params make_params(hcmx_hmat* h, double alpha, double beta, double* y) {
     p.coef = h->coef.as<double>();
     p.c = h->c.as<double>();
     p.partial = h->partial.as<double>();
-    p.counter = h->counter.as<unsigned>();
     p.x = h->xpad.as<double>();  // padded, 16-byte aligned copy of x (bulk copies)
     p.y = y;
     p.row_begin = static_cast<uint32_t>(h->rb);
@@ -1476,6 +1443,10 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
     check_cuda(cudaMemsetAsync(h->work.p, 0, 8, s), "work counters");
     if (h->nlr && h->nstripe_a) {
         k_phase_a<<<std::min<uint32_t>(h->nstripe_a, 2 * nsm), kThreadsA, kSmemBytes, s>>>(p);
+        h->last_launches++;
+    }
+    if (h->nred) {
+        k_reduce<<<(h->nred + 255) / 256, 256, 0, s>>>(p, h->redcols.as<RedCol>(), h->nred);
         h->last_launches++;
     }
     if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
