@@ -65,8 +65,9 @@ constexpr int kNStage = 3;                // ring depth
 constexpr int kSlack = 16;                // decode reads up to 2 words past a segment
 constexpr unsigned kWaitHintNs = HCMX_WAIT_HINT;  // mbarrier try_wait suspend hint (ns)
 constexpr int kOffDesc = kStageBytes + kSlack;
-constexpr int kOffWb = kOffDesc + kMaxItems * kItemBytes;
-constexpr int kOffHdr = kOffWb + 48;     // slot header written by the producer: stripe id, flags
+constexpr int kOffWb = kOffDesc + kMaxItems * kItemBytes;  // phase B: per-warp item ranges (48 B)
+constexpr int kOffHdr = kOffWb + 48;  // slot header written by the producer: stripe id, flags,
+                                      // item claim counter (phase A), items
 constexpr int kOffCoef = kOffHdr + 16;
 constexpr int kSlotBytes = kOffCoef + kCoefBytes;
 constexpr int kR = 128;               // rows per phase-B CTA
@@ -77,6 +78,7 @@ constexpr int kBDenseGroup = 8;       // max dense columns per B item
 constexpr int kBLRGroup = 8;          // max rank columns per B item
 constexpr uint64_t kAStripeBytes = 8 * kStageBytes;  // target packed bytes per phase-A CTA
 constexpr uint64_t kItemTarget = 1536;          // packed bytes per item (columns grouped up to this)
+constexpr uint64_t kItemMaxBytes = 2048;        // items merge columns up to this many packed bytes
 constexpr size_t kRingBytes = static_cast<size_t>(kNStage) * kSlotBytes;
 constexpr size_t kRedBytes = (kNWB / 2) * kR * sizeof(double);  // phase-B cross-warp reduction
 constexpr size_t kSmemBytes = kRingBytes + kRedBytes + 2 * kNStage * sizeof(uint64_t);  // + full, empty barriers
@@ -146,7 +148,7 @@ struct LeafA {  // host-side only
 struct Params {
     const uint8_t* arena;
     const Stage* stages;
-    const uint16_t* stage_wb;   // [nstages * 24] per-warp item ranges (NW + 1 used)
+    const uint16_t* stage_wb;   // phase B: [nstages * 24] per-warp item ranges (NW + 1 used)
     const uint32_t* stripe_a;   // [nstripe_a + 1] stage ranges
     const uint32_t* stripe_b;   // [nblocks + 1]
     const uint64_t* copies;     // [nstages * kCopies] staged coefficient copies (see CopyEntry)
@@ -397,6 +399,8 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
             uint32_t* hdr = reinterpret_cast<uint32_t*>(base + kOffHdr);
             hdr[0] = m0.stripe;
             hdr[1] = m0.flags;
+            hdr[2] = 0u;  // item claim counter
+            hdr[3] = (m0.flags & kHdrEnd || m0.empty) ? 0u : m0.st.nitems;
         }
         __syncwarp();
         if (m0.flags & kHdrEnd || m0.empty) {  // header only
@@ -404,15 +408,16 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
         } else {
             const bool no_coef = p.debug >= 2, no_meta = p.debug >= 3;  // profiling knobs
             if (lane == 0) {
-                mbar_expect_tx(&full[slot], m0.st.bytes + (no_meta ? 0u : m0.st.nitems * kItemBytes + 48) +
+                mbar_expect_tx(&full[slot], m0.st.bytes + (no_meta ? 0u : m0.st.nitems * kItemBytes + (PHASE_A ? 0u : 48u)) +
                                                 (no_coef ? 0u : m0.st.coef_bytes));
                 bulk_g2s(base, p.arena + m0.st.byte_off, m0.st.bytes, &full[slot], policy);
                 if (!no_meta) {
                     const void* d = PHASE_A ? static_cast<const void*>(p.aitems + m0.st.item0)
                                             : static_cast<const void*>(p.bitems + m0.st.item0);
                     bulk_g2s_plain(base + kOffDesc, d, m0.st.nitems * kItemBytes, &full[slot]);
-                    const uint32_t sidx = static_cast<uint32_t>(m0.st.pad);  // global stage index
-                    bulk_g2s_plain(base + kOffWb, p.stage_wb + static_cast<size_t>(sidx) * 24, 48, &full[slot]);
+                    if (!PHASE_A)
+                        bulk_g2s_plain(base + kOffWb, p.stage_wb + static_cast<size_t>(m0.st.pad) * 24, 48,
+                                       &full[slot]);
                 }
             }
             __syncwarp();
@@ -429,18 +434,34 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
 
 // consumer warps of a persistent CTA: body(slot_base, first, end) for the
 // warp's items of every stage; at the last stage of a stripe, stripe_end(id)
-template <int NW, class Body, class End>
+// DYN: warps claim a stage's items one at a time (phase A: every item writes
+// its own results, so any assignment gives the same bits).  Otherwise each
+// warp takes its precomputed contiguous range (phase B: a warp's row sums
+// must see the same items in the same order on every run: deterministic y).
+template <int NW, bool DYN, class Body, class End>
 __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t* empty, unsigned warp,
                                         unsigned lane, int debug, Body&& body, End&& stripe_end) {
     for (uint32_t it = 0;; ++it) {
         const int slot = static_cast<int>(it % kNStage);
         mbar_wait(&full[slot], (it / kNStage) & 1u);
         const uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
-        const uint32_t* hdr = reinterpret_cast<const uint32_t*>(base + kOffHdr);
+        uint32_t* hdr = reinterpret_cast<uint32_t*>(ring + static_cast<size_t>(slot) * kSlotBytes + kOffHdr);
         const uint32_t stripe = hdr[0], flags = hdr[1];
         if (flags & kHdrEnd) return;
-        const uint16_t* wb = reinterpret_cast<const uint16_t*>(base + kOffWb);
-        if (!debug && !(flags & kHdrEmpty)) body(base, wb[warp], wb[warp + 1]);
+        if (debug) {
+        } else if (DYN) {
+            const unsigned n = hdr[3];
+            for (;;) {
+                unsigned i = 0;
+                if (lane == 0) i = atomicAdd(hdr + 2, 1u);
+                i = __shfl_sync(0xffffffffu, i, 0);
+                if (i >= n) break;
+                body(base, i);
+            }
+        } else if (!(flags & kHdrEmpty)) {
+            const uint16_t* wb = reinterpret_cast<const uint16_t*>(base + kOffWb);
+            for (unsigned i = wb[warp], e = wb[warp + 1]; i < e; ++i) body(base, i);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
         if (flags & kHdrLast) stripe_end(stripe);
@@ -570,9 +591,14 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
 __global__ void k_reduce(Params p, const RedCol* rc, uint32_t n) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const RedCol r = rc[i];
-        double s = 0.0;
-        for (uint32_t ch = 0; ch < r.nchunks; ++ch) s += p.partial[r.p0 + ch * r.stride];
-        p.c[r.col] = p.alpha * p.coef[r.col] * s;
+        double s[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains, fixed order
+        uint32_t ch = 0;
+        for (; ch + 4 <= r.nchunks; ch += 4) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s[q] += p.partial[r.p0 + (ch + q) * r.stride];
+        }
+        for (; ch < r.nchunks; ++ch) s[ch & 3u] += p.partial[r.p0 + ch * r.stride];
+        p.c[r.col] = p.alpha * p.coef[r.col] * ((s[0] + s[1]) + (s[2] + s[3]));
     }
 }
 
@@ -689,11 +715,10 @@ __global__ void __launch_bounds__(kThreadsA, 2) k_phase_a(Params p) {
         producer<true>(p, smem, full, empty, lane);
         return;
     }
-    consume<kNWA>(
+    consume<kNWA, true>(
         smem, full, empty, warp, lane, p.debug,
-        [&](const uint8_t* base, unsigned b, unsigned e) {
-            const AItem* items = reinterpret_cast<const AItem*>(base + kOffDesc);
-            for (unsigned i = b; i < e; ++i) a_item(p, items[i], base, lane);
+        [&](const uint8_t* base, unsigned i) {
+            a_item(p, reinterpret_cast<const AItem*>(base + kOffDesc)[i], base, lane);
         },
         [](uint32_t) {});
 }
@@ -713,11 +738,10 @@ __global__ void __launch_bounds__(kThreadsB, 2) k_phase_b(Params p) {
 #pragma unroll
     for (int g = 0; g < kG; ++g) acc[g] = 0.0;
     constexpr unsigned H = kNWB / 2;
-    consume<kNWB>(
+    consume<kNWB, false>(
         smem, full, empty, warp, lane, p.debug,
-        [&](const uint8_t* base, unsigned b, unsigned e) {
-            const BItem* items = reinterpret_cast<const BItem*>(base + kOffDesc);
-            for (unsigned i = b; i < e; ++i) b_item(p, items[i], base, lane, acc);
+        [&](const uint8_t* base, unsigned i) {
+            b_item(p, reinterpret_cast<const BItem*>(base + kOffDesc)[i], base, lane, acc);
         },
         [&](uint32_t blk) {  // block done: fixed-order pairwise sum of the warps, then y
             consumer_bar();
@@ -908,7 +932,7 @@ struct Builder {
 
     std::vector<uint32_t> arena;  // words
     std::vector<Stage> stages;
-    std::vector<uint16_t> wb;     // 24 entries per stage
+    std::vector<uint16_t> wb;     // phase B: 24 entries per stage (NW + 1 used)
     std::vector<BItem> bitems;
     std::vector<AItem> aitems;
     std::vector<Seg> segs;
@@ -935,15 +959,13 @@ struct Builder {
     }
 
     // One CTA stripe.  Specs are single columns.  Stages take columns in order
-    // up to kStageBytes; each stage's columns are split into NW contiguous
-    // pieces of (nearly) equal packed bytes, one per consumer warp, so every
-    // warp has the same amount of decoding per stage (the ring advances at the
-    // pace of the slowest warp).  Inside a piece, consecutive columns of one
-    // leaf / row range (B) or leaf chunk (A) merge into items of <= MAXC
-    // columns.  Phase-A items of one chunk in a stage share one staged x slice.
-    template <class Item, int NW, int MAXC>
+    // up to kStageBytes; consecutive columns of one leaf / row range (B) or leaf
+    // chunk (A) with one decode mode merge into items of <= MAXC columns and
+    // <= kItemMaxBytes.  Consumer warps claim a stage's items one at a time
+    // (largest first), so no per-warp shares are precomputed.  Items of one
+    // stage share deduplicated coefficient slices (x or phase-A results).
+    template <class Item, int MAXC, int NW>
     void emit_stripe(std::vector<Spec<Item>>& specs, std::vector<Item>& items) {
-        constexpr bool IS_A = std::is_same<Item, AItem>::value;
         size_t pos = 0;
         while (pos < specs.size()) {
             // columns of this stage by data budget
@@ -953,42 +975,31 @@ struct Builder {
                 bytes += specs[end++].words * 4;
             if (end == pos) throw invalid_argument("hmat: column exceeds a stage");
             for (;;) {
-                if (try_stage<Item, NW, MAXC>(specs, pos, end, items)) break;
+                if (try_stage<Item, MAXC, NW>(specs, pos, end, items)) break;
                 end = pos + std::max<size_t>(1, (end - pos) * 3 / 4);  // too many items / coefficients
             }
             pos = end;
         }
     }
 
-    // pieces + items for specs[pos, end); false (nothing emitted) if over budget
-    template <class Item, int NW, int MAXC>
+    // items for specs[pos, end); false (nothing emitted) if over budget.
+    // NW == 0: items claimed dynamically, largest first.  NW > 0: the stage's
+    // columns are cut into NW contiguous pieces of (nearly) equal decode cost,
+    // one per consumer warp, and items never straddle a piece.
+    template <class Item, int MAXC, int NW>
     bool try_stage(std::vector<Spec<Item>>& specs, size_t pos, size_t end, std::vector<Item>& items) {
         constexpr bool IS_A = std::is_same<Item, AItem>::value;
-        uint64_t total = 0;
-        for (size_t i = pos; i < end; ++i) total += specs[i].words;
-        // piece boundaries: warp p gets specs [cut[p], cut[p+1])
-        std::vector<size_t> cut(NW + 1, end);
-        cut[0] = pos;
-        {
-            size_t i = pos;
-            uint64_t acc = 0;
-            for (int p = 1; p < NW; ++p) {
-                const uint64_t target = total * p / NW;
-                while (i < end && acc + specs[i].words / 2 <= target) acc += specs[i++].words;
-                cut[p] = i;
-            }
-        }
-        // items (per warp, in order); coefficient slices deduplicated per stage
         struct Built {
             Item it;
             size_t first, n;
+            uint64_t words;
         };
-        std::vector<std::vector<Built>> per(NW);
+        std::vector<Built> built;
         struct Slice {
             uint32_t table, start, count, off;
         };
         std::vector<Slice> slices;
-        uint32_t coef = 0, nit = 0;
+        uint32_t coef = 0;
         auto slice_of = [&](const Spec<Item>& sp) -> const Slice& {
             for (const Slice& sl : slices)
                 if (sl.table == sp.sl_table && sl.start == sp.sl_start && sl.count >= sp.sl_count) return sl;
@@ -996,30 +1007,56 @@ struct Builder {
             coef += r16((sp.sl_count + (sp.sl_start & 1u)) * 8);
             return slices.back();
         };
-        for (int p = 0; p < NW; ++p) {
-            size_t i = cut[p];
-            while (i < cut[p + 1]) {
-                size_t j = i + 1;
-                while (j < cut[p + 1] && j - i < static_cast<size_t>(MAXC) && specs[j].unit == specs[i].unit) ++j;
-                const uint32_t n = static_cast<uint32_t>(j - i);
-                Item it = specs[i].it;
-                it.nseg = static_cast<uint8_t>(n);
-                const Slice sl = slice_of(specs[i]);
-                const uint32_t off = sl.off + (specs[i].elem - (sl.start & ~1u)) * 8;
-                if constexpr (IS_A) it.x_off = off;
-                else it.coef_off = off;
-                per[p].push_back({it, i, n});
-                ++nit;
-                i = j;
+        std::vector<size_t> cut = {pos, end};
+        if (NW > 0) {
+            uint64_t total = 0;
+            for (size_t i = pos; i < end; ++i) total += specs[i].cost;
+            cut.assign(NW + 1, end);
+            cut[0] = pos;
+            size_t i = pos;
+            uint64_t acc = 0;
+            for (int q = 1; q < NW; ++q) {
+                const uint64_t target = total * q / NW;
+                while (i < end && acc + specs[i].cost / 2 <= target) acc += specs[i++].cost;
+                cut[q] = i;
             }
         }
-        if (nit > static_cast<uint32_t>(kMaxItems) || coef > static_cast<uint32_t>(kCoefBytes) ||
+        std::vector<uint32_t> piece_end;  // items per piece, cumulative
+        for (size_t q = 0; q + 1 < cut.size(); ++q) {
+          size_t i = cut[q];
+          const size_t pend = cut[q + 1];
+          while (i < pend) {
+            size_t j = i + 1;
+            uint64_t words = specs[i].words;
+            while (j < pend && j - i < static_cast<size_t>(MAXC) && specs[j].unit == specs[i].unit &&
+                   (words + specs[j].words) * 4 <= kItemMaxBytes)
+                words += specs[j++].words;
+            Item it = specs[i].it;
+            it.nseg = static_cast<uint8_t>(j - i);
+            const Slice sl = slice_of(specs[i]);
+            const uint32_t off = sl.off + (specs[i].elem - (sl.start & ~1u)) * 8;
+            if constexpr (IS_A) it.x_off = off;
+            else it.coef_off = off;
+            built.push_back({it, i, j - i, words});
+            i = j;
+          }
+          piece_end.push_back(static_cast<uint32_t>(built.size()));
+        }
+        if (built.size() > static_cast<size_t>(kMaxItems) || coef > static_cast<uint32_t>(kCoefBytes) ||
             slices.size() > static_cast<size_t>(kCopies)) {
             if (end - pos == 1) throw invalid_argument("hmat: column exceeds a stage");
             return false;
         }
-        // emit: data in warp order (packed column layouts ahead of the segments
-        // for lowrank / phase-A items), descriptors grouped by warp, copy list
+        if (NW == 0)  // claimed largest first: the last items to finish are the small ones
+            std::stable_sort(built.begin(), built.end(),
+                             [](const Built& x, const Built& y) { return x.words > y.words; });
+        uint32_t wb_index = 0;
+        if (NW > 0) {
+            wb_index = static_cast<uint32_t>(wb.size() / 24);
+            wb.push_back(0);
+            for (uint32_t e : piece_end) wb.push_back(static_cast<uint16_t>(e));
+            while (wb.size() % 24) wb.push_back(static_cast<uint16_t>(built.size()));  // 48 B per stage
+        }
         const size_t c0 = copies.size();
         copies.resize(c0 + kCopies, 0);
         for (size_t q = 0; q < slices.size(); ++q)
@@ -1029,29 +1066,22 @@ struct Builder {
         const uint64_t start = arena.size();
         Stage st{};
         st.item0 = static_cast<uint32_t>(items.size());
-        uint16_t cnt = 0;
-        for (int p = 0; p < NW; ++p) {
-            wb.push_back(cnt);
-            for (Built& b : per[p]) {
-                b.it.word_off = static_cast<uint32_t>(arena.size() - start);
-                bool packed = IS_A;
-                if constexpr (!IS_A) packed = b.it.kind != 0;
-                if (packed)
-                    for (size_t k = b.first; k < b.first + b.n; ++k) arena.push_back(specs[k].param);
-                for (size_t k = b.first; k < b.first + b.n; ++k)
-                    for (uint32_t q = 0; q < specs[k].nseg; ++q) put_fields(segs[specs[k].seg0 + q]);
-                items.push_back(b.it);
-                ++cnt;
-            }
+        for (Built& b : built) {
+            b.it.word_off = static_cast<uint32_t>(arena.size() - start);
+            bool packed = IS_A;
+            if constexpr (!IS_A) packed = b.it.kind != 0;
+            if (packed)  // packed column layouts ahead of the segments
+                for (size_t k = b.first; k < b.first + b.n; ++k) arena.push_back(specs[k].param);
+            for (size_t k = b.first; k < b.first + b.n; ++k)
+                for (uint32_t q = 0; q < specs[k].nseg; ++q) put_fields(segs[specs[k].seg0 + q]);
+            items.push_back(b.it);
         }
-        wb.push_back(cnt);
-        while (wb.size() % 24) wb.push_back(cnt);  // 48 bytes per stage (one bulk copy)
         while (arena.size() % 4) arena.push_back(0u);
         st.byte_off = start * 4;
         st.bytes = static_cast<uint32_t>((arena.size() - start) * 4);
-        st.nitems = nit;
+        st.nitems = static_cast<uint32_t>(built.size());
+        st.pad = wb_index;  // phase B: where the producer fetches this stage's warp ranges
         st.coef_bytes = coef;
-        st.pad = stages.size();  // global stage index (the producer fetches its per-warp ranges)
         stages.push_back(st);
         return true;
     }
@@ -1192,7 +1222,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         uint64_t stripe_bytes = 0, unit = 0;
         auto flush = [&]() {
             if (specs.empty()) return;
-            B.emit_stripe<AItem, kNWA, kAGroup>(specs, B.aitems);
+            B.emit_stripe<AItem, kAGroup, 0>(specs, B.aitems);
             stripe_a.push_back(static_cast<uint32_t>(B.stages.size()));
             ++nstripe_a;
             specs.clear();
@@ -1296,7 +1326,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                         sp.sl_table = 0;  // x slice of the dense leaf's columns
                         sp.sl_start = static_cast<uint32_t>(d.col0[l]);
                         sp.sl_count = static_cast<uint32_t>(cols);
-                        sp.cost = nc * nr;
+                        sp.cost = 3 * nr + 128;  // ~decode instructions (x8) of one column segment
                         sp.unit = unit * 4 + it.mode;
                         specs.push_back(sp);
                     }
@@ -1326,13 +1356,13 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                         sp.sl_table = 1;  // phase-A results of the leaf
                         sp.sl_start = L.colbase;
                         sp.sl_count = L.k;
-                        sp.cost = ng * nr;
+                        sp.cost = 3 * nr + 128;
                         sp.unit = unit * 4 + it.mode;  // items never mix decode modes
                         specs.push_back(sp);
                     }
                 }
             }
-            B.emit_stripe<BItem, kNWB, kBLRGroup>(specs, B.bitems);
+            B.emit_stripe<BItem, kBLRGroup, kNWB>(specs, B.bitems);
             stripe_b.push_back(static_cast<uint32_t>(B.stages.size()));
         }
     }
@@ -1351,6 +1381,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     };
     up(h->arena, B.arena.data(), B.arena.size() * 4);
     up(h->stages, B.stages.data(), B.stages.size() * sizeof(Stage));
+    B.wb.resize(std::max<size_t>(B.wb.size(), 24));
     up(h->stage_wb, B.wb.data(), B.wb.size() * sizeof(uint16_t));
     up(h->copies, B.copies.data(), B.copies.size() * sizeof(uint64_t));
     h->work.alloc(16);
@@ -1372,7 +1403,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     h->nstripe_a = nstripe_a;
     h->nblocks = static_cast<uint32_t>(nblocks);
     rep.device_arena_bytes = B.arena.size() * 4;
-    rep.device_table_bytes = B.stages.size() * (sizeof(Stage) + 48 + kCopies * 8) + B.bitems.size() * sizeof(BItem) +
+    rep.device_table_bytes = B.stages.size() * (sizeof(Stage) + kCopies * 8) + B.bitems.size() * sizeof(BItem) +
                              B.aitems.size() * sizeof(AItem) +
                              colw.size() * 2 * sizeof(ColPar) + coef.size() * 16;
     rep.overhead = rep.device_table_bytes;

@@ -112,3 +112,39 @@ def test_compute_without_gpu_fails_loudly(L):
     assert st == _lib.HCMX_CUDA_ERROR
     assert b"no CUDA device" in L.hcmx_gpu_last_error()
     assert L.hcmx_gpu_init(0) == _lib.HCMX_CUDA_ERROR
+
+
+def test_cpp_shim_compiles_and_maps_exceptions(tmp_path):
+    """include/hcmx_gpu.hpp (the binding INTEGRATION.md shows) builds against the
+    library and keeps the reference's names and exception types (host-only calls)"""
+    import shutil
+    import subprocess
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "shim.cpp"
+    src.write_text(r'''
+#include <hcmx_gpu.hpp>
+#include <cstdio>
+int main() {
+    namespace codec = hcmx_gpu::codec;
+    const auto d = codec::make_descriptor(codec::Scheme::aflp, 1e-6, 0.5, 5);
+    std::printf("%d %d %u %zu\n", (int)codec::mantissa_bits_for(1e-6), (int)d.mant_bits, d.bit_width(),
+                codec::compressed_size(64, d));
+    try { codec::mantissa_bits_for(2.0); } catch (const std::invalid_argument&) { std::printf("invalid_argument\n"); }
+    std::vector<std::uint8_t> wire;
+    codec::CompressedBuffer b{d, 0, {}};
+    codec::serialize(b, wire);
+    std::size_t off = 0;
+    try { codec::deserialize(wire.data(), 10, off); } catch (const hcmx_gpu::corrupt_buffer_error&) { std::printf("corrupt\n"); }
+    return 0;
+}
+''')
+    libdir = os.path.join(root, "paper_2308_10960_b200")
+    exe = tmp_path / "shim"
+    subprocess.run(["g++", "-std=c++20", "-I" + os.path.join(root, "include"), str(src), "-L" + libdir,
+                    "-lhcmx_gpu", "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    m, mant, w, size = out[0].split()
+    assert (m, mant, w, size) == ("19", "26", "32", str(20 + 64 * 4))  # AFLP widens m to a byte multiple
+    assert out[1] == "invalid_argument" and out[2] == "corrupt"
