@@ -60,7 +60,7 @@ constexpr int kThreadsA = (kNWA + 1) * 32;
 constexpr int kStageBytes = 26624;        // packed data per stage
 constexpr int kMaxItems = 32;             // items per stage (one per producer lane)
 constexpr int kItemBytes = 32;            // descriptor size (A and B)
-constexpr int kCoefBytes = 6144;          // staged coefficients + column params per stage
+constexpr int kCoefBytes = 7936;          // staged coefficients + column params per stage
 constexpr int kNStage = 3;                // ring depth
 constexpr int kSlack = 16;                // decode reads up to 2 words past a segment
 constexpr unsigned kWaitHintNs = HCMX_WAIT_HINT;  // mbarrier try_wait suspend hint (ns)
@@ -105,6 +105,16 @@ struct ColPar {
     uint32_t packed;     // w | m << 8 | e << 16 | mode << 24
     uint32_t sgn_sh;     // 31 - e - m (mode 0/1)
 };
+
+// One rank column of a lowrank leaf as phase B needs it (32 bytes, two
+// LDS.128): the phase-A result c_i = alpha coef_i (X_i^T x), written each
+// product, and the W column's decoder constants, precomputed at build time.
+// A leaf's records are contiguous, so one bulk copy stages a whole leaf.
+struct WCol {
+    double c;
+    uint32_t mask_em, mul_rsh, sgn_sh, packed, w, pad;
+};
+static_assert(sizeof(WCol) == 32, "WCol layout");
 
 struct BItem {
     uint32_t word_off;   // packed data, from the warp-stage start
@@ -156,10 +166,8 @@ struct Params {
     uint32_t nstripe_a, nblocks;
     const BItem* bitems;
     const AItem* aitems;
-    const ColPar* colw_par;
-    const ColPar* colx_par;
     const double* coef;         // sigma_i * scale_X_i * scale_W_i
-    double* c;                  // alpha * coef * (X^T x)_i, written by phase A
+    WCol* wcol;                 // per rank column: alpha * coef * (X^T x)_i (phase A) + W decoder constants
     double* partial;
     const double* x;            // padded internal copy (16-byte aligned, readable + 16 B)
     double* y;
@@ -301,9 +309,7 @@ __device__ __forceinline__ void issue_copy(const Params& p, uint64_t c, uint8_t*
     const void* src;
     switch (static_cast<unsigned>((c >> 60) & 3u)) {
         case 0: src = p.x + idx; break;
-        case 1: src = p.c + idx; break;
-        case 2: src = p.colw_par + idx; break;
-        default: src = p.colx_par + idx; break;
+        default: src = p.wcol + idx; break;
     }
     bulk_g2s_plain(cdst + dst, src, bytes, bar);
 }
@@ -584,7 +590,7 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
     }
     const double r = reduce4(a, lane);
     if (!writer) return;
-    if (it.nchunks == 1) p.c[it.xcol + cl] = p.alpha * cf * r;
+    if (it.nchunks == 1) p.wcol[it.xcol + cl].c = p.alpha * cf * r;
     else p.partial[it.pbase + static_cast<uint32_t>(it.chunk) * it.k + it.icol0 + cl] = r;
 }
 
@@ -598,7 +604,7 @@ __global__ void k_reduce(Params p, const RedCol* rc, uint32_t n) {
             for (int q = 0; q < 4; ++q) s[q] += p.partial[r.p0 + (ch + q) * r.stride];
         }
         for (; ch < r.nchunks; ++ch) s[ch & 3u] += p.partial[r.p0 + ch * r.stride];
-        p.c[r.col] = p.alpha * p.coef[r.col] * ((s[0] + s[1]) + (s[2] + s[3]));
+        p.wcol[r.col].c = p.alpha * p.coef[r.col] * ((s[0] + s[1]) + (s[2] + s[3]));
     }
 }
 
@@ -631,12 +637,12 @@ __device__ __forceinline__ void b_item_generic(const BItem& it, const uint32_t* 
         if (f >= 0 && f < static_cast<int>(nr)) vmask |= 1u << g;
     }
     const unsigned umask = __reduce_or_sync(0xffffffffu, vmask);
-    const uint32_t* pk = seg - nseg;
+    const WCol* wc = reinterpret_cast<const WCol*>(cf);
     for (unsigned c = 0; c < nseg; ++c) {
-        const uint32_t pw = it.kind == 0 ? it.dpacked : pk[c];
+        const uint32_t pw = it.kind == 0 ? it.dpacked : wc[c].packed;
         const ColPar col = col_of<MODE>(pw);
         const unsigned w = pw & 0xffu;
-        const double cc = it.kind == 0 ? dmul * cf[c] : cf[c];
+        const double cc = it.kind == 0 ? dmul * cf[c] : wc[c].c;
         b_column<MODE>(seg, col, w, f0, vmask, umask, cc, acc);
         seg += (nr * w + 31) >> 5;
     }
@@ -667,14 +673,13 @@ __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg
             sp += segw;
         }
     } else {
-        const uint32_t* pk = seg - nseg;  // packed column layouts precede the segments
+        const WCol* wc = reinterpret_cast<const WCol*>(cf);  // staged records of the leaf's columns
         for (unsigned c = 0; c < nseg; ++c) {
-            const uint32_t pw = pk[c];
-            const ColPar col = col_of<MODE>(pw);
-            const unsigned w = pw & 0xffu;
-            const unsigned bit = lane * w;
-            b_column_full<MODE, GLO, GHI>(seg + (bit >> 5), col, w, bit & 31u, cf[c], acc);
-            seg += (GHI - GLO) * w;
+            const WCol q = wc[c];
+            const ColPar col{q.mask_em, q.mul_rsh, q.packed, q.sgn_sh};
+            const unsigned bit = lane * q.w;
+            b_column_full<MODE, GLO, GHI>(seg + (bit >> 5), col, q.w, bit & 31u, q.c, acc);
+            seg += (GHI - GLO) * q.w;
         }
     }
 }
@@ -683,7 +688,7 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
                                        double (&acc)[kG]) {
     const double* cf = reinterpret_cast<const double*>(slot + kOffCoef + it.coef_off);
     const double dmul = p.alpha * it.scale;  // dense: alpha * buffer scale folded into x
-    const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off + (it.kind ? it.nseg : 0u);
+    const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
     // fast bodies for modes 0/1 at the shapes 64-row leaf clusters produce;
     // everything else takes one generic body with the mode-2 decoder (exact for
     // every layout), which keeps the kernel inside the instruction cache
@@ -814,7 +819,7 @@ using namespace hcmx_gpu;
 
 struct hcmx_hmat {
     uint64_t n_rows = 0, n_cols = 0, rb = 0, re = 0;
-    DevBuf arena, stages, stage_wb, stripe_a, stripe_b, copies, work, bitems, aitems, colw, colx, coef, c, partial,
+    DevBuf arena, stages, stage_wb, stripe_a, stripe_b, copies, work, bitems, aitems, wcol, coef, partial,
         redcols, xpad, xbuf, ybuf;
     uint32_t nstripe_a = 0, nblocks = 0, nlr = 0, nred = 0;
     hcmx_memory_report report{};
@@ -1000,11 +1005,15 @@ struct Builder {
         };
         std::vector<Slice> slices;
         uint32_t coef = 0;
+        // table 0: x (8-byte entries, copied from an even index), table 1: WCol records
+        auto slice_bytes = [](uint32_t table, uint32_t start, uint32_t count) {
+            return table == 0 ? r16((count + (start & 1u)) * 8) : count * static_cast<uint32_t>(sizeof(WCol));
+        };
         auto slice_of = [&](const Spec<Item>& sp) -> const Slice& {
             for (const Slice& sl : slices)
                 if (sl.table == sp.sl_table && sl.start == sp.sl_start && sl.count >= sp.sl_count) return sl;
             slices.push_back({sp.sl_table, sp.sl_start, sp.sl_count, coef});
-            coef += r16((sp.sl_count + (sp.sl_start & 1u)) * 8);
+            coef += slice_bytes(sp.sl_table, sp.sl_start, sp.sl_count);
             return slices.back();
         };
         std::vector<size_t> cut = {pos, end};
@@ -1034,7 +1043,8 @@ struct Builder {
             Item it = specs[i].it;
             it.nseg = static_cast<uint8_t>(j - i);
             const Slice sl = slice_of(specs[i]);
-            const uint32_t off = sl.off + (specs[i].elem - (sl.start & ~1u)) * 8;
+            const uint32_t off = sl.table == 0 ? sl.off + (specs[i].elem - (sl.start & ~1u)) * 8
+                                               : sl.off + (specs[i].elem - sl.start) * static_cast<uint32_t>(sizeof(WCol));
             if constexpr (IS_A) it.x_off = off;
             else it.coef_off = off;
             built.push_back({it, i, j - i, words});
@@ -1060,17 +1070,16 @@ struct Builder {
         const size_t c0 = copies.size();
         copies.resize(c0 + kCopies, 0);
         for (size_t q = 0; q < slices.size(); ++q)
-            copies[c0 + q] = copy_entry(slices[q].start & ~1u, slices[q].off,
-                                        r16((slices[q].count + (slices[q].start & 1u)) * 8), slices[q].table);
+            copies[c0 + q] = copy_entry(slices[q].table == 0 ? slices[q].start & ~1u : slices[q].start, slices[q].off,
+                                        slice_bytes(slices[q].table, slices[q].start, slices[q].count),
+                                        slices[q].table);
         while (arena.size() % 4) arena.push_back(0u);  // 16-byte aligned stages
         const uint64_t start = arena.size();
         Stage st{};
         st.item0 = static_cast<uint32_t>(items.size());
         for (Built& b : built) {
             b.it.word_off = static_cast<uint32_t>(arena.size() - start);
-            bool packed = IS_A;
-            if constexpr (!IS_A) packed = b.it.kind != 0;
-            if (packed)  // packed column layouts ahead of the segments
+            if (IS_A)  // packed column layouts ahead of the segments
                 for (size_t k = b.first; k < b.first + b.n; ++k) arena.push_back(specs[k].param);
             for (size_t k = b.first; k < b.first + b.n; ++k)
                 for (uint32_t q = 0; q < specs[k].nseg; ++q) put_fields(segs[specs[k].seg0 + q]);
@@ -1155,7 +1164,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     // per-leaf tables
     std::vector<int64_t> lr_id(d.nleaves, -1);
     std::vector<LeafA> leafa;
-    std::vector<ColPar> colw, colx;
+    std::vector<WCol> wcol;
     std::vector<double> coef;
     uint64_t npartial = 0;
     std::vector<RedCol> redcols;
@@ -1172,13 +1181,12 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         } else {
             const uint32_t k = static_cast<uint32_t>(d.rank[l]);
             lr_id[l] = static_cast<int64_t>(leafa.size());
-            if (colw.size() % 2) {  // even column bases: 16-byte aligned bulk copies of C
-                colw.push_back(ColPar{});
-                colx.push_back(ColPar{});
+            if (wcol.size() % 2) {  // even column bases (x-style 16-byte alignment of coef)
+                wcol.push_back(WCol{});
                 coef.push_back(0.0);
             }
             LeafA L{};
-            L.colbase = static_cast<uint32_t>(colw.size());
+            L.colbase = static_cast<uint32_t>(wcol.size());
             L.k = k;
             L.nchunks = static_cast<uint32_t>((cols + kAChunk - 1) / kAChunk);
             if (k >= (1u << 16) || L.nchunks >= (1u << 16)) throw invalid_argument("hmat: lowrank leaf too large");
@@ -1193,8 +1201,8 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
             for (uint32_t i = 0; i < k; ++i) {
                 const hcmx_descriptor& xw = d.desc[d.buf0[l] + i];
                 const hcmx_descriptor& xx = d.desc[d.buf0[l] + k + i];
-                colw.push_back(col_par(xw));
-                colx.push_back(col_par(xx));
+                const ColPar cp = col_par(xw);
+                wcol.push_back({0.0, cp.mask_em, cp.mul_rsh, cp.sgn_sh, cp.packed, xw.bit_width, 0u});
                 coef.push_back(d.sigma[d.sig0[l] + i] * xx.scale * xw.scale);
                 bytes += 40 + d.plen[d.buf0[l] + i] + d.plen[d.buf0[l] + k + i];
                 rep.algorithmic_bytes += 40 + payload_bytes(rows, xw.bit_width) + payload_bytes(cols, xx.bit_width);
@@ -1208,8 +1216,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     rep.algorithmic_bytes += 8ull * d.n_cols + 8ull * (h->re - h->rb);
     h->nlr = static_cast<uint32_t>(leafa.size());
     for (int pad = 0; pad < 4; ++pad) {  // bulk copies may round up past the last column
-        colw.push_back(ColPar{});
-        colx.push_back(ColPar{});
+        wcol.push_back(WCol{});
         coef.push_back(0.0);
     }
 
@@ -1348,9 +1355,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                         it.ra = static_cast<uint8_t>(r0 - b0);
                         it.nr = static_cast<uint8_t>(nr);
                         it.src = L.colbase + g;
-                        sp.words += ng;  // packed column layout word
-                        sp.param = col_par(d.desc[d.buf0[l] + g]).packed;
-                        it.mode = static_cast<uint8_t>(sp.param >> 24);
+                        it.mode = static_cast<uint8_t>(col_par(d.desc[d.buf0[l] + g]).packed >> 24);
                         it.fcase = fcase_of(r0 - b0, nr);
                         sp.elem = it.src;
                         sp.sl_table = 1;  // phase-A results of the leaf
@@ -1389,13 +1394,10 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     up(h->stripe_b, stripe_b.data(), stripe_b.size() * 4);
     up(h->bitems, B.bitems.data(), B.bitems.size() * sizeof(BItem));
     up(h->aitems, B.aitems.data(), B.aitems.size() * sizeof(AItem));
-    up(h->colw, colw.data(), colw.size() * sizeof(ColPar));
-    up(h->colx, colx.data(), colx.size() * sizeof(ColPar));
+    up(h->wcol, wcol.data(), wcol.size() * sizeof(WCol));
     up(h->coef, coef.data(), coef.size() * 8);
     h->xpad.alloc((d.n_cols + 4) * 8);
     check_cuda(cudaMemsetAsync(h->xpad.p, 0, h->xpad.bytes, s), "memset");
-    h->c.alloc(std::max<size_t>(16, coef.size() * 8));
-    check_cuda(cudaMemsetAsync(h->c.p, 0, h->c.bytes, s), "memset");
     h->partial.alloc(std::max<size_t>(16, npartial * 8));
     up(h->redcols, redcols.data(), redcols.size() * sizeof(RedCol));
     h->nred = static_cast<uint32_t>(redcols.size());
@@ -1405,7 +1407,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     rep.device_arena_bytes = B.arena.size() * 4;
     rep.device_table_bytes = B.stages.size() * (sizeof(Stage) + kCopies * 8) + B.bitems.size() * sizeof(BItem) +
                              B.aitems.size() * sizeof(AItem) +
-                             colw.size() * 2 * sizeof(ColPar) + coef.size() * 16;
+                             wcol.size() * sizeof(WCol) + coef.size() * 8;
     rep.overhead = rep.device_table_bytes;
 }
 
@@ -1422,10 +1424,8 @@ Params make_params(hcmx_hmat* h, double alpha, double beta, double* y) {
     p.nblocks = h->nblocks;
     p.bitems = h->bitems.as<BItem>();
     p.aitems = h->aitems.as<AItem>();
-    p.colw_par = h->colw.as<ColPar>();
-    p.colx_par = h->colx.as<ColPar>();
     p.coef = h->coef.as<double>();
-    p.c = h->c.as<double>();
+    p.wcol = h->wcol.as<WCol>();
     p.partial = h->partial.as<double>();
     p.x = h->xpad.as<double>();  // padded, 16-byte aligned copy of x (bulk copies)
     p.y = y;
