@@ -515,10 +515,17 @@ __device__ __forceinline__ double a_col(const uint32_t* seg, uint32_t pw, unsign
     return acc0 + acc1;
 }
 
-// the item's columns (<= kAGroup, unrolled so the sums stay in registers)
+// the item's columns (<= kAGroup, unrolled so the sums stay in registers);
+// x of this lane's fields is loaded once per item (U known: no predication)
 template <int MODE, int U>
 __device__ __forceinline__ void a_cols(const uint32_t* pk, unsigned nseg, unsigned nf, unsigned lane,
-                                       const double (&xv)[kAChunk / 32], double (&a)[kAGroup]) {
+                                       const double* xs, double (&a)[kAGroup]) {
+    double xv[kAChunk / 32];
+#pragma unroll
+    for (int u = 0; u < kAChunk / 32; ++u) {
+        if (U > 0) xv[u] = u < U ? xs[lane + 32u * u] : 0.0;
+        else xv[u] = (lane + 32u * u < nf) ? xs[lane + 32u * u] : 0.0;
+    }
     const uint32_t* seg = pk + nseg;  // packed column layouts precede the segments
 #pragma unroll
     for (int c = 0; c < kAGroup; ++c) {
@@ -565,13 +572,6 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
     if (writer && it.nchunks == 1) cf = __ldg(p.coef + it.xcol + cl);  // in flight during the decode
     const double* xs = reinterpret_cast<const double*>(slot + kOffCoef + it.x_off);
     const uint32_t* pk = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
-    double xv[kAChunk / 32];
-    const unsigned U = (nf + 31) >> 5;
-#pragma unroll
-    for (int u = 0; u < kAChunk / 32; ++u) {
-        const unsigned f = lane + 32u * u;
-        xv[u] = (static_cast<unsigned>(u) < U && f < nf) ? xs[f] : 0.0;
-    }
     double a[kAGroup];
 #pragma unroll
     for (int c = 0; c < kAGroup; ++c) a[c] = 0.0;
@@ -580,13 +580,13 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
     // mode-2 decoder is exact for every layout; keeps the kernel small)
     const unsigned ui = nf == 256 ? 3u : nf == 128 ? 2u : nf == 64 ? 1u : 0u;
     switch (it.mode == 2 || ui == 0 ? 0u : ui + 3u * it.mode) {
-        case 3: a_cols<0, 8>(pk, nseg, nf, lane, xv, a); break;
-        case 2: a_cols<0, 4>(pk, nseg, nf, lane, xv, a); break;
-        case 1: a_cols<0, 2>(pk, nseg, nf, lane, xv, a); break;
-        case 6: a_cols<1, 8>(pk, nseg, nf, lane, xv, a); break;
-        case 5: a_cols<1, 4>(pk, nseg, nf, lane, xv, a); break;
-        case 4: a_cols<1, 2>(pk, nseg, nf, lane, xv, a); break;
-        default: a_cols<2, 0>(pk, nseg, nf, lane, xv, a); break;
+        case 3: a_cols<0, 8>(pk, nseg, nf, lane, xs, a); break;
+        case 2: a_cols<0, 4>(pk, nseg, nf, lane, xs, a); break;
+        case 1: a_cols<0, 2>(pk, nseg, nf, lane, xs, a); break;
+        case 6: a_cols<1, 8>(pk, nseg, nf, lane, xs, a); break;
+        case 5: a_cols<1, 4>(pk, nseg, nf, lane, xs, a); break;
+        case 4: a_cols<1, 2>(pk, nseg, nf, lane, xs, a); break;
+        default: a_cols<2, 0>(pk, nseg, nf, lane, xs, a); break;
     }
     const double r = reduce4(a, lane);
     if (!writer) return;
