@@ -232,7 +232,7 @@ __device__ __forceinline__ uint64_t encode_value(double v, unsigned e, unsigned 
 // [g0, g1) of the buffer v[0, n) are packed into out (word 0 = group 0).
 __device__ __forceinline__ int pack_groups(const double* __restrict__ v, uint64_t n, uint32_t g0, uint32_t g1,
                                            unsigned e, unsigned m, unsigned w, double scale,
-                                           uint32_t* __restrict__ out, unsigned lane) {
+                                           uint32_t* __restrict__ out, unsigned lane, uint32_t gstride = 1) {
     const double inv_scale = 1.0 / scale;  // IEEE division (codec.cpp:107)
     const uint64_t max_offset = (1ull << e) - 1;
     const uint64_t round_add = (m < 52) ? (1ull << (51 - m)) : 0;
@@ -240,16 +240,17 @@ __device__ __forceinline__ int pack_groups(const double* __restrict__ v, uint64_
     const unsigned T = (32 + w - 1) / w + 1;  // fields overlapping one output word
     const unsigned i0a = (32 * lane) / w, i0b = (32 * (lane + 32)) / w;
     int nf_bad = 0;
-    for (uint32_t g4 = g0; g4 < g1; g4 += 4) {
+    for (uint32_t g4 = g0; g4 < g1; g4 += 4 * gstride) {
         double xs[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const uint64_t idx = (uint64_t)(g4 + i) * 32 + lane;
-            xs[i] = (g4 + i < g1 && idx < n) ? __ldcs(v + idx) : 0.0;
+            const uint32_t g = g4 + i * gstride;
+            const uint64_t idx = (uint64_t)g * 32 + lane;
+            xs[i] = (g < g1 && idx < n) ? __ldcs(v + idx) : 0.0;
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const uint32_t g = g4 + i;
+            const uint32_t g = g4 + i * gstride;
             if (g >= g1) break;
             const uint64_t idx = (uint64_t)g * 32 + lane;
             uint64_t f = 0;
@@ -277,6 +278,69 @@ __device__ __forceinline__ int pack_groups(const double* __restrict__ v, uint64_
                 }
                 if (K < nwords) __stcs(o + K, word);
             }
+        }
+    }
+    return __any_sync(0xffffffffu, nf_bad);
+}
+
+// Packing of 32-bit fields (w <= 32): lane j encodes value 32g + j into field
+// f at bit j w of the group; its low part goes to word q = j w / 32, its high
+// part (if it straddles) to word q + 1, ORed into a per-warp shared buffer of
+// w + 1 words (shared atomics; a word has <= ceil(32 / w) + 1 writers), then
+// the w words are stored coalesced.  Same bits as encode_value / pack_groups.
+__device__ __forceinline__ int pack_groups32(const double* __restrict__ v, uint32_t n, uint32_t g0, uint32_t g1,
+                                             unsigned e, unsigned m, unsigned w, double scale,
+                                             uint32_t* __restrict__ out, unsigned lane, uint32_t gstride,
+                                             uint32_t* __restrict__ sw) {
+    const double inv_scale = 1.0 / scale;  // IEEE division (codec.cpp:107)
+    const uint32_t max_offset = (1u << e) - 1u;
+    const uint64_t round_add = 1ull << (51 - m);
+    const uint32_t mant_mask = (1u << m) - 1u;
+    const unsigned bit = lane * w, q = bit >> 5, s = bit & 31u;
+    int nf_bad = 0;
+    for (uint32_t g4 = g0; g4 < g1; g4 += 4 * gstride) {
+        double xs[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t g = g4 + i * gstride;
+            const uint32_t idx = g * 32 + lane;
+            xs[i] = (g < g1 && idx < n) ? __ldcs(v + idx) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t g = g4 + i * gstride;
+            if (g >= g1) break;
+            const uint32_t idx = g * 32 + lane;
+            const double x = xs[i];
+            uint32_t f = 0;
+            if (idx < n) {
+                const uint32_t sign = static_cast<uint32_t>(__double2hiint(x)) >> 31;
+                f = sign << (e + m);
+                if (!isfinite(x)) {
+                    nf_bad = 1;
+                    f = 0;
+                } else if (x != 0.0) {
+                    const double vp = __dadd_rn(__dmul_rn(fabs(x), inv_scale), 1.0);  // >= 2, no FMA
+                    const uint64_t u = dbits(vp) + round_add;
+                    uint32_t offset = static_cast<uint32_t>(u >> 52) - 1023u;
+                    uint32_t mant = static_cast<uint32_t>(u >> (52 - m)) & mant_mask;
+                    if (offset > max_offset || !isfinite(vp)) {
+                        offset = max_offset;
+                        mant = mant_mask;
+                    }
+                    f |= (offset << m) | mant;
+                }
+            }
+            sw[lane] = 0u;
+            if (lane == 0) sw[32] = 0u;
+            __syncwarp();
+            atomicOr(sw + q, f << s);
+            if (s + w > 32) atomicOr(sw + q + 1, f >> (32u - s));
+            __syncwarp();
+            const uint32_t nvalid = min(32u, n - g * 32);
+            const unsigned nwords = (nvalid * w + 31) / 32;
+            if (lane < nwords) __stcs(out + g * w + lane, sw[lane]);
+            __syncwarp();
         }
     }
     return __any_sync(0xffffffffu, nf_bad);
@@ -398,6 +462,127 @@ k_compress_fused(const double* __restrict__ values, const uint64_t* __restrict__
     }
 }
 
+// codec.cpp:142-144 fused per buffer, one CTA of kCtaWarps warps per buffer:
+// pass 1 (min/max, every thread, 8 loads in flight), block reduction, the
+// layout rules (device log2 + ambiguity flag as in k_compress_fused), pass 2
+// packs groups warp-strided (the values come back from L2).
+constexpr int kCtaWarps = 4;
+
+__global__ void __launch_bounds__(kCtaWarps * 32)
+k_compress_cta(const double* __restrict__ values, const uint64_t* __restrict__ voff,
+               const uint64_t* __restrict__ count, uint64_t nbuf, int scheme, unsigned m_req,
+               const uint64_t* __restrict__ poff, uint8_t* __restrict__ payload,
+               hcmx_descriptor* __restrict__ desc, hcmx_stats* __restrict__ stats,
+               uint32_t* __restrict__ flags, int* __restrict__ err) {
+    __shared__ uint64_t s_mn[kCtaWarps], s_mx[kCtaWarps];
+    __shared__ unsigned s_nz[kCtaWarps], s_nf[kCtaWarps];
+    __shared__ uint32_t s_words[kCtaWarps][40];
+    const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    for (uint64_t b = blockIdx.x; b < nbuf; b += gridDim.x) {
+        const uint64_t n = count[b];
+        const double* v = values + voff[b];
+        uint64_t mn = 0x7FF0000000000000ull, mx = 0;
+        unsigned nz = 0, nf = 0;
+        constexpr unsigned T = kCtaWarps * 32;
+        for (uint64_t i = tid; i < n; i += 8 * T) {
+            double xs[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) xs[u] = i + T * u < n ? __ldcg(v + i + T * u) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double a = fabs(xs[u]);
+                if (a != 0.0) nz = 1;
+                if (!isfinite(xs[u])) nf = 1;
+                if (a != 0.0 && !isnan(a)) {
+                    const uint64_t ab = dbits(a);
+                    mn = ab < mn ? ab : mn;
+                    mx = ab > mx ? ab : mx;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t omn = __shfl_xor_sync(0xffffffffu, mn, o);
+            const uint64_t omx = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = omn < mn ? omn : mn;
+            mx = omx > mx ? omx : mx;
+        }
+        nz = __any_sync(0xffffffffu, nz);
+        nf = __any_sync(0xffffffffu, nf);
+        if (lane == 0) {
+            s_mn[warp] = mn;
+            s_mx[warp] = mx;
+            s_nz[warp] = nz;
+            s_nf[warp] = nf;
+        }
+        __syncthreads();
+        mn = s_mn[0];
+        mx = s_mx[0];
+        nz = s_nz[0];
+        nf = s_nf[0];
+#pragma unroll
+        for (int q = 1; q < kCtaWarps; ++q) {
+            mn = s_mn[q] < mn ? s_mn[q] : mn;
+            mx = s_mx[q] > mx ? s_mx[q] : mx;
+            nz |= s_nz[q];
+            nf |= s_nf[q];
+        }
+        __syncthreads();  // s_* reused by the next buffer
+        const bool all_zero = !nz;
+        const double dmin = all_zero ? 0.0 : bitsd(mn), dmax = all_zero ? 0.0 : bitsd(mx);
+        unsigned e = 2, ambiguous = 0;
+        if (scheme == HCMX_BFL) {
+            e = 8;
+        } else if (scheme == HCMX_DFL) {
+            e = 11;
+        } else if (!all_zero) {  // codec.cpp:69-75 with the device log2
+            const double span = log2(dmax) - log2(dmin) + 1.0;
+            const double vv = span + 1.0;
+            const double bits = ceil(log2(vv));
+            e = static_cast<unsigned>(fmin(fmax(bits, 2.0), 11.0));
+            for (int k = 2; k <= 10; ++k) {
+                const double pk = ldexp(1.0, k);
+                if (fabs(vv - pk) <= pk * 1e-9) ambiguous = 1;
+            }
+        }
+        unsigned m = m_req;
+        const unsigned unit = scheme == HCMX_AFL ? 1u : (scheme == HCMX_DFL ? 16u : 8u);
+        if (scheme != HCMX_AFL) {  // codec.cpp:25-30
+            unsigned w0 = 1 + e + m;
+            w0 += (unit - w0 % unit) % unit;
+            m = min(52u, w0 - 1 - e);
+        }
+        unsigned w = 1 + e + m;
+        w += (unit - w % unit) % unit;
+        const double scale = all_zero ? 1.0 : dmin;
+        if (tid == 0) {
+            hcmx_descriptor d;
+            d.scheme = static_cast<uint8_t>(scheme);
+            d.exp_bits = static_cast<uint8_t>(e);
+            d.mant_bits = static_cast<uint8_t>(m);
+            d.bit_width = static_cast<uint8_t>(w);
+            d.reserved = 0;
+            d.scale = scale;
+            desc[b] = d;
+            hcmx_stats st;
+            st.min_mag = dmin;
+            st.max_mag = dmax;
+            st.all_zero = all_zero ? 1u : 0u;
+            st.non_finite = nf;
+            stats[b] = st;
+            flags[b] = ambiguous;
+            if (nf) *err = 1;
+        }
+        if (nf) continue;
+        if (w <= 32)
+            pack_groups32(v, static_cast<uint32_t>(n), warp, static_cast<uint32_t>((n + 31) / 32), e, m, w, scale,
+                          reinterpret_cast<uint32_t*>(payload + poff[b]), lane, kCtaWarps, s_words[warp]);
+        else
+            pack_groups(v, n, warp, static_cast<uint32_t>((n + 31) / 32), e, m, w, scale,
+                        reinterpret_cast<uint32_t*>(payload + poff[b]), lane, kCtaWarps);
+    }
+}
+
 // ------------------------------------------------------------- unpack ----
 __device__ __forceinline__ double decode_field(uint64_t field, unsigned e, unsigned m, double scale) {
     const uint64_t exp_mask = (1ull << e) - 1;
@@ -475,16 +660,191 @@ k_unpack(const uint8_t* __restrict__ payload, const uint64_t* __restrict__ poff,
     }
 }
 
+// Job-free unpacking: warp chunks of 32 groups (1024 values); chunk c belongs
+// to the buffer found by binary search over coff (cumulative chunks per
+// buffer).  A chunk's packed words are first copied to a per-warp shared
+// buffer with 16-byte loads (all in flight at once: the warp's memory-level
+// parallelism), then every lane decodes its field of each group from shared
+// memory and the doubles are stored coalesced.  w > 32 goes in two halves.
+constexpr int kUnpackWarps = 8;
+constexpr unsigned kStageWords = 1024;  // per warp: 16 groups at w <= 64, 32 at w <= 32
+
+// per-chunk metadata, loaded one chunk ahead
+struct ChunkMeta {
+    hcmx_descriptor d;
+    uint64_t n, poff, voff, c0;
+};
+__device__ __forceinline__ ChunkMeta chunk_meta(uint64_t c, const uint32_t* cbuf, const uint64_t* coff,
+                                                const hcmx_descriptor* desc, const uint64_t* count,
+                                                const uint64_t* poff, const uint64_t* voff) {
+    const uint32_t b = __ldg(cbuf + c);
+    ChunkMeta m;
+    m.d = desc[b];
+    m.n = count[b];
+    m.poff = poff[b];
+    m.voff = voff[b];
+    m.c0 = __ldg(coff + b);
+    return m;
+}
+
+__global__ void __launch_bounds__(kUnpackWarps * 32)
+k_unpack_chunks(const uint8_t* __restrict__ payload, const uint64_t* __restrict__ poff,
+                const uint64_t* __restrict__ count, const hcmx_descriptor* __restrict__ desc,
+                const uint64_t* __restrict__ voff, const uint64_t* __restrict__ coff,
+                const uint32_t* __restrict__ cbuf, uint64_t nchunks, double* __restrict__ out) {
+    __shared__ __align__(16) uint32_t stage[kUnpackWarps][kStageWords + 8];
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t* sw = stage[warp];
+    const uint64_t gw = blockIdx.x * (uint64_t)kUnpackWarps + warp;
+    const uint64_t nw = gridDim.x * (uint64_t)kUnpackWarps;
+    ChunkMeta next{};
+    if (gw < nchunks) next = chunk_meta(gw, cbuf, coff, desc, count, poff, voff);
+    for (uint64_t c = gw; c < nchunks; c += nw) {
+        const ChunkMeta cm = next;
+        if (c + nw < nchunks) next = chunk_meta(c + nw, cbuf, coff, desc, count, poff, voff);
+        const hcmx_descriptor d = cm.d;
+        const unsigned e = d.exp_bits, m = d.mant_bits, w = d.bit_width;
+        const uint64_t n = cm.n;
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(payload + cm.poff);
+        double* o = out + cm.voff;
+        const uint64_t ngroups = (n + 31) / 32, nwords_all = (n * w + 31) / 32;
+        const uint32_t gc0 = static_cast<uint32_t>((c - cm.c0) * 32);
+        const uint32_t gc1 = static_cast<uint32_t>(umin64(gc0 + 32, ngroups));
+        const uint32_t step = w > 32 ? 16u : 32u;
+        const unsigned bit = lane * w, q = bit >> 5, sh = bit & 31u;
+        const uint64_t wmask = (w == 64) ? ~0ull : ((1ull << w) - 1);
+        for (uint32_t g0 = gc0; g0 < gc1; g0 += step) {
+            const uint32_t g1 = min(g0 + step, gc1);
+            const uint64_t wb = (uint64_t)g0 * w, we = umin64((uint64_t)g1 * w, nwords_all);
+            const unsigned nvec = static_cast<unsigned>((we - wb + 3) / 4);  // the slot is 16-byte padded
+            const uint4* src = reinterpret_cast<const uint4*>(p + wb);
+            uint4 r[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const unsigned i = lane + 32u * u;
+                if (i < nvec) r[u] = __ldcs(src + i);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const unsigned i = lane + 32u * u;
+                if (i < nvec) reinterpret_cast<uint4*>(sw)[i] = r[u];
+            }
+            __syncwarp();
+            if (w <= 32 && e <= 10 && w == 1 + e + m) {
+                // 32-bit fields, no 2046 clamp: the double is built with integer ops
+                // (exactly the codec's bits - 1.0, one rounding in * scale)
+                const uint32_t mask = 0xffffffffu >> (33u - w);
+                const bool lo_m = m <= 20;
+                const unsigned s1 = lo_m ? 20u - m : m - 20u;
+                const uint32_t nfull = static_cast<uint32_t>(umin64(g1, n / 32));
+                uint32_t g = g0;
+                for (; g < nfull; ++g) {
+                    const uint32_t* gp = sw + (g - g0) * w + q;
+                    const uint32_t t = __funnelshift_r(gp[0], gp[1], sh);
+                    const uint32_t pay = t & mask;
+                    const uint32_t hi = (lo_m ? pay << s1 : pay >> s1) + (1023u << 20);
+                    const uint32_t lo = lo_m ? 0u : pay << (32u - s1);
+                    const double v = __dmul_rn(__hiloint2double(hi, lo) - 1.0, d.scale);
+                    const double sv = __hiloint2double(__double2hiint(v) ^ ((t << (32u - w)) & 0x80000000u),
+                                                       __double2loint(v));
+                    __stcs(o + (uint64_t)g * 32 + lane, sv);
+                }
+                for (; g < g1; ++g) {  // ragged last group
+                    const uint32_t* gp = sw + (g - g0) * w + q;
+                    uint64_t win = ((uint64_t)gp[1] << 32 | gp[0]) >> sh;
+                    const uint64_t idx = (uint64_t)g * 32 + lane;
+                    if (idx < n) __stcs(o + idx, decode_field(win & wmask, e, m, d.scale));
+                }
+            } else {
+                for (uint32_t g = g0; g < g1; ++g) {
+                    const uint32_t* gp = sw + (g - g0) * w + q;
+                    uint64_t win = ((uint64_t)gp[1] << 32 | gp[0]) >> sh;
+                    if (sh + w > 64) win |= (uint64_t)gp[2] << (64 - sh);
+                    const uint64_t idx = (uint64_t)g * 32 + lane;
+                    if (idx < n) __stcs(o + idx, decode_field(win & wmask, e, m, d.scale));
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
 int grid_for(uint64_t njobs) {
     const uint64_t blocks = (njobs + kWarpsPerBlock - 1) / kWarpsPerBlock;
     return (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, 148ull * 16));
 }
 
-struct Scratch {
-    DevBuf jobs, err;
+// Device copies of a batch layout (counts, cumulative unpack chunks, payload
+// slot offsets), uploaded once per distinct layout: repeated batched calls on
+// the same layout do no host-to-device traffic and no synchronisation.
+struct LayoutCache {
+    std::mutex mu;
+    uint64_t nbuf = ~0ull, hash = 0, nchunks = 0;
+    DevBuf count, coff, cbuf;
+    uint64_t poff_hash = 0;
+    DevBuf poff;
 };
+LayoutCache g_layout;
+
+uint64_t fnv(const uint64_t* a, uint64_t n, uint64_t h = 1469598103934665603ull) {
+    for (uint64_t i = 0; i < n; ++i) h = (h ^ a[i]) * 1099511628211ull;
+    return h;
+}
+
+// pinned staging for small device-to-host results (descriptors, flags)
+struct Pinned {
+    std::mutex mu;
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* get(size_t n) {
+        if (n > bytes) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            bytes = 0;
+            check_cuda(cudaMallocHost(&p, n), "cudaMallocHost");
+            bytes = n;
+        }
+        return p;
+    }
+};
+Pinned g_pinned;
 
 }  // namespace
+
+// layout arrays for h_count (caller holds g_layout.mu)
+static void layout_arrays(const uint64_t* h_count, uint64_t nbuf, void* stream) {
+    const uint64_t h = fnv(h_count, nbuf);
+    if (g_layout.nbuf == nbuf && g_layout.hash == h) return;
+    check_cuda(cudaDeviceSynchronize(), "layout cache");  // kernels may still read the old arrays
+    std::vector<uint64_t> coff(nbuf + 1, 0);
+    for (uint64_t b = 0; b < nbuf; ++b) coff[b + 1] = coff[b] + (h_count[b] + 1023) / 1024;
+    std::vector<uint32_t> cbuf(coff[nbuf]);
+    for (uint64_t b = 0; b < nbuf; ++b)
+        for (uint64_t c = coff[b]; c < coff[b + 1]; ++c) cbuf[c] = static_cast<uint32_t>(b);
+    g_layout.count.alloc(std::max<uint64_t>(16, nbuf * 8));
+    g_layout.coff.alloc((nbuf + 1) * 8);
+    g_layout.cbuf.alloc(std::max<uint64_t>(16, cbuf.size() * 4));
+    h2d(g_layout.count.p, h_count, nbuf * 8, stream);
+    h2d(g_layout.coff.p, coff.data(), (nbuf + 1) * 8, stream);
+    h2d(g_layout.cbuf.p, cbuf.data(), cbuf.size() * 4, stream);
+    stream_sync(stream);
+    g_layout.nbuf = nbuf;
+    g_layout.hash = h;
+    g_layout.nchunks = coff[nbuf];
+    g_layout.poff_hash = 0;
+}
+
+static const uint64_t* layout_poff(const uint64_t* h_poff, uint64_t nbuf, void* stream) {
+    const uint64_t h = fnv(h_poff, nbuf, 7);
+    if (g_layout.poff_hash != h || !g_layout.poff.p) {
+        check_cuda(cudaDeviceSynchronize(), "layout cache");
+        g_layout.poff.alloc(std::max<uint64_t>(16, nbuf * 8));
+        h2d(g_layout.poff.p, h_poff, nbuf * 8, stream);
+        stream_sync(stream);
+        g_layout.poff_hash = h;
+    }
+    return g_layout.poff.as<uint64_t>();
+}
 
 static void upload_jobs(const std::vector<Job>& jobs, DevBuf& dj, void* stream) {
     dj.alloc(std::max<size_t>(16, jobs.size() * sizeof(Job)));
@@ -527,18 +887,19 @@ int launch_pack_jobs(const double* values, const uint64_t* voff, const uint64_t*
     return err;
 }
 
-void launch_unpack_jobs(const uint8_t* payload, const uint64_t* poff, const uint64_t* d_count,
+void launch_unpack_jobs(const uint8_t* payload, const uint64_t* poff, const uint64_t* /*d_count*/,
                         const uint64_t* h_count, const hcmx_descriptor* desc, const uint64_t* voff,
                         uint64_t nbuf, double* out, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    const auto jobs = make_jobs(h_count, nbuf);
-    if (jobs.empty()) return;
-    DevBuf dj;
-    upload_jobs(jobs, dj, stream);
-    k_unpack<<<grid_for(jobs.size()), kWarpsPerBlock * 32, 0, s>>>(payload, poff, d_count, desc, voff,
-                                                                   dj.as<Job>(), jobs.size(), out);
+    std::lock_guard<std::mutex> g(g_layout.mu);
+    layout_arrays(h_count, nbuf, stream);
+    const uint64_t nch = g_layout.nchunks;
+    if (!nch) return;
+    const int grid = (int)std::min<uint64_t>((nch + kUnpackWarps - 1) / kUnpackWarps, 148ull * 8);
+    k_unpack_chunks<<<grid, kUnpackWarps * 32, 0, s>>>(payload, poff, g_layout.count.as<uint64_t>(), desc, voff,
+                                                       g_layout.coff.as<uint64_t>(), g_layout.cbuf.as<uint32_t>(),
+                                                       nch, out);
     check_cuda(cudaGetLastError(), "unpack launch");
-    stream_sync(stream);
 }
 
 }  // namespace hcmx_gpu
@@ -618,9 +979,7 @@ int hcmx_gpu_codec_unpack(const uint8_t* d_payload, const uint64_t* d_poff, cons
                           double* d_out, void* stream) {
     return guarded([&] {
         require_device();
-        DevBuf dc = upload_u64(h_count, nbuf, stream);
-        launch_unpack_jobs(d_payload, d_poff, dc.as<uint64_t>(), h_count, d_desc, d_voff, nbuf, d_out,
-                           stream);
+        launch_unpack_jobs(d_payload, d_poff, nullptr, h_count, d_desc, d_voff, nbuf, d_out, stream);
     });
 }
 
@@ -634,8 +993,8 @@ int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff, cons
         const uint8_t m_req = mantissa_bits_for(eps);  // eps validation first (codec.cpp:63-64)
         uint64_t maxc = 0;
         for (uint64_t b = 0; b < nbuf; ++b) maxc = std::max(maxc, h_count[b]);
-        DevBuf dc = upload_u64(h_count, nbuf, stream);
         if (maxc > kFuseMax) {  // very large buffers: device analyze, host selection, device pack
+            DevBuf dc = upload_u64(h_count, nbuf, stream);
             DevBuf dst(std::max<uint64_t>(24, nbuf * sizeof(hcmx_stats)));
             launch_analyze_jobs(d_values, d_voff, dc.as<uint64_t>(), h_count, nbuf, dst.as<hcmx_stats>(),
                                 stream);
@@ -661,26 +1020,30 @@ int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff, cons
         }
         *h_total = off;
         if (off > payload_capacity) throw invalid_argument("compress: payload capacity too small");
-        DevBuf dp = upload_u64(h_poff, nbuf, stream);
-        DevBuf dd(std::max<uint64_t>(16, nbuf * sizeof(hcmx_descriptor)));
+        std::lock_guard<std::mutex> g(g_layout.mu);
+        layout_arrays(h_count, nbuf, stream);
+        const uint64_t* dp = layout_poff(h_poff, nbuf, stream);
+        // one device block for descriptors | flags | error, one pinned block for the read-back
+        const size_t o_fl = round16(nbuf * sizeof(hcmx_descriptor)), o_err = o_fl + round16(nbuf * 4);
+        DevBuf out(o_err + 16);
         DevBuf dst(std::max<uint64_t>(24, nbuf * sizeof(hcmx_stats)));
-        DevBuf dfl(std::max<uint64_t>(16, nbuf * 4)), de(sizeof(int));
         cudaStream_t s = (cudaStream_t)stream;
-        check_cuda(cudaMemsetAsync(de.p, 0, sizeof(int), s), "memset");
-        const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((nbuf + kWarpsPerBlock - 1) / kWarpsPerBlock,
-                                                                       148ull * 16));
-        k_compress_fused<<<grid, kWarpsPerBlock * 32, 0, s>>>(d_values, d_voff, dc.as<uint64_t>(), nbuf, scheme,
-                                                              m_req, dp.as<uint64_t>(), d_payload,
-                                                              dd.as<hcmx_descriptor>(), dst.as<hcmx_stats>(),
-                                                              dfl.as<uint32_t>(), de.as<int>());
+        uint8_t* ob = out.as<uint8_t>();
+        check_cuda(cudaMemsetAsync(ob + o_err, 0, sizeof(int), s), "memset");
+        const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(nbuf, 148ull * 16));
+        k_compress_cta<<<grid, kCtaWarps * 32, 0, s>>>(d_values, d_voff, g_layout.count.as<uint64_t>(), nbuf,
+                                                       scheme, m_req, dp, d_payload,
+                                                       reinterpret_cast<hcmx_descriptor*>(ob), dst.as<hcmx_stats>(),
+                                                       reinterpret_cast<uint32_t*>(ob + o_fl),
+                                                       reinterpret_cast<int*>(ob + o_err));
         check_cuda(cudaGetLastError(), "compress launch");
-        int err = 0;
-        std::vector<uint32_t> flags(nbuf);
-        d2h(h_desc, dd.p, nbuf * sizeof(hcmx_descriptor), stream);
-        d2h(flags.data(), dfl.p, nbuf * 4, stream);
-        d2h(&err, de.p, sizeof(int), stream);
+        std::lock_guard<std::mutex> gp(g_pinned.mu);
+        uint8_t* hb = static_cast<uint8_t*>(g_pinned.get(o_err + 16));
+        d2h(hb, ob, o_err + sizeof(int), stream);
         stream_sync(stream);
-        if (err) throw invalid_argument("compress: values must be finite");
+        std::memcpy(h_desc, hb, nbuf * sizeof(hcmx_descriptor));
+        const uint32_t* flags = reinterpret_cast<const uint32_t*>(hb + o_fl);
+        if (*reinterpret_cast<const int*>(hb + o_err)) throw invalid_argument("compress: values must be finite");
         // exponent widths next to a 2^k - 2 threshold: decide with glibc (codec.cpp:72-73)
         for (uint64_t b = 0; b < nbuf; ++b) {
             if (!flags[b]) continue;
