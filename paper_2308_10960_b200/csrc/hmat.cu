@@ -456,13 +456,16 @@ __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t*
         if (flags & kHdrEnd) return;
         if (debug) {
         } else if (DYN) {
+            // the next claim is issued before the current item is decoded, so the
+            // shared atomic's latency hides behind it
             const unsigned n = hdr[3];
-            for (;;) {
-                unsigned i = 0;
-                if (lane == 0) i = atomicAdd(hdr + 2, 1u);
-                i = __shfl_sync(0xffffffffu, i, 0);
-                if (i >= n) break;
+            unsigned nl = 0;
+            if (lane == 0) nl = atomicAdd(hdr + 2, 1u);
+            unsigned i = __shfl_sync(0xffffffffu, nl, 0);
+            while (i < n) {
+                if (lane == 0) nl = atomicAdd(hdr + 2, 1u);
                 body(base, i);
+                i = __shfl_sync(0xffffffffu, nl, 0);
             }
         } else if (!(flags & kHdrEmpty)) {
             const uint16_t* wb = reinterpret_cast<const uint16_t*>(base + kOffWb);
