@@ -64,9 +64,10 @@ constexpr int kCoefBytes = 7936;          // staged coefficients + column params
 constexpr int kNStage = 3;                // ring depth
 constexpr int kSlack = 16;                // decode reads up to 2 words past a segment
 constexpr unsigned kWaitHintNs = HCMX_WAIT_HINT;  // mbarrier try_wait suspend hint (ns)
-constexpr int kOffDesc = kStageBytes + kSlack;
-constexpr int kOffWb = kOffDesc + kMaxItems * kItemBytes;  // phase B: per-warp item ranges (48 B)
-constexpr int kOffHdr = kOffWb + 48;  // slot header written by the producer: stripe id, flags,
+// A stage is one contiguous arena range, copied by ONE bulk copy into the slot:
+// [items (32 B each)][phase B: per-warp item ranges, 48 B][packed data]
+constexpr int kStageMax = kMaxItems * kItemBytes + 48 + kStageBytes;
+constexpr int kOffHdr = kStageMax + kSlack;  // slot header written by the producer: stripe id, flags,
                                       // item claim counter (phase A), items
 constexpr int kOffCoef = kOffHdr + 16;
 constexpr int kSlotBytes = kOffCoef + kCoefBytes;
@@ -85,7 +86,7 @@ constexpr size_t kSmemBytes = kRingBytes + kRedBytes + 2 * kNStage * sizeof(uint
 constexpr int kCopies = 2 * kMaxItems;  // coefficient copies per stage (two per producer lane)
 // copy entry (u64): [0,32) source element index, [32,48) dst / 16 in the coef area,
 // [48,60) bytes / 16, [60,62) source table (0 x, 1 C, 2 W params, 3 X params), bit 63 valid
-static_assert(kOffDesc % 16 == 0 && kOffCoef % 16 == 0 && kSlotBytes % 16 == 0, "slot alignment");
+static_assert(kOffHdr % 16 == 0 && kOffCoef % 16 == 0 && kSlotBytes % 16 == 0, "slot alignment");
 constexpr uint32_t kHdrLast = 1u, kHdrEnd = 2u, kHdrEmpty = 4u;  // slot header flags
 
 struct Stage {
@@ -158,14 +159,11 @@ struct LeafA {  // host-side only
 struct Params {
     const uint8_t* arena;
     const Stage* stages;
-    const uint16_t* stage_wb;   // phase B: [nstages * 24] per-warp item ranges (NW + 1 used)
     const uint32_t* stripe_a;   // [nstripe_a + 1] stage ranges
     const uint32_t* stripe_b;   // [nblocks + 1]
     const uint64_t* copies;     // [nstages * kCopies] staged coefficient copies (see CopyEntry)
     unsigned* work;             // [2] stripe counters of the persistent kernels (A, B), zeroed per product
     uint32_t nstripe_a, nblocks;
-    const BItem* bitems;
-    const AItem* aitems;
     const double* coef;         // sigma_i * scale_X_i * scale_W_i
     WCol* wcol;                 // per rank column: alpha * coef * (X^T x)_i (phase A) + W decoder constants
     double* partial;
@@ -414,17 +412,9 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
         } else {
             const bool no_coef = p.debug >= 2, no_meta = p.debug >= 3;  // profiling knobs
             if (lane == 0) {
-                mbar_expect_tx(&full[slot], m0.st.bytes + (no_meta ? 0u : m0.st.nitems * kItemBytes + (PHASE_A ? 0u : 48u)) +
-                                                (no_coef ? 0u : m0.st.coef_bytes));
+                (void)no_meta;
+                mbar_expect_tx(&full[slot], m0.st.bytes + (no_coef ? 0u : m0.st.coef_bytes));
                 bulk_g2s(base, p.arena + m0.st.byte_off, m0.st.bytes, &full[slot], policy);
-                if (!no_meta) {
-                    const void* d = PHASE_A ? static_cast<const void*>(p.aitems + m0.st.item0)
-                                            : static_cast<const void*>(p.bitems + m0.st.item0);
-                    bulk_g2s_plain(base + kOffDesc, d, m0.st.nitems * kItemBytes, &full[slot]);
-                    if (!PHASE_A)
-                        bulk_g2s_plain(base + kOffWb, p.stage_wb + static_cast<size_t>(m0.st.pad) * 24, 48,
-                                       &full[slot]);
-                }
             }
             __syncwarp();
             if (!no_coef) {
@@ -468,7 +458,7 @@ __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t*
                 i = __shfl_sync(0xffffffffu, nl, 0);
             }
         } else if (!(flags & kHdrEmpty)) {
-            const uint16_t* wb = reinterpret_cast<const uint16_t*>(base + kOffWb);
+            const uint16_t* wb = reinterpret_cast<const uint16_t*>(base + hdr[3] * kItemBytes);
             for (unsigned i = wb[warp], e = wb[warp + 1]; i < e; ++i) body(base, i);
         }
         __syncwarp();
@@ -726,7 +716,7 @@ __global__ void __launch_bounds__(kThreadsA, 2) k_phase_a(Params p) {
     consume<kNWA, true>(
         smem, full, empty, warp, lane, p.debug,
         [&](const uint8_t* base, unsigned i) {
-            a_item(p, reinterpret_cast<const AItem*>(base + kOffDesc)[i], base, lane);
+            a_item(p, reinterpret_cast<const AItem*>(base)[i], base, lane);
         },
         [](uint32_t) {});
 }
@@ -749,7 +739,7 @@ __global__ void __launch_bounds__(kThreadsB, 2) k_phase_b(Params p) {
     consume<kNWB, false>(
         smem, full, empty, warp, lane, p.debug,
         [&](const uint8_t* base, unsigned i) {
-            b_item(p, reinterpret_cast<const BItem*>(base + kOffDesc)[i], base, lane, acc);
+            b_item(p, reinterpret_cast<const BItem*>(base)[i], base, lane, acc);
         },
         [&](uint32_t blk) {  // block done: fixed-order pairwise sum of the warps, then y
             consumer_bar();
@@ -822,7 +812,7 @@ using namespace hcmx_gpu;
 
 struct hcmx_hmat {
     uint64_t n_rows = 0, n_cols = 0, rb = 0, re = 0;
-    DevBuf arena, stages, stage_wb, stripe_a, stripe_b, copies, work, bitems, aitems, wcol, coef, partial,
+    DevBuf arena, stages, stripe_a, stripe_b, copies, work, wcol, coef, partial,
         redcols, xpad, xbuf, ybuf;
     uint32_t nstripe_a = 0, nblocks = 0, nlr = 0, nred = 0;
     hcmx_memory_report report{};
@@ -1080,6 +1070,9 @@ struct Builder {
         const uint64_t start = arena.size();
         Stage st{};
         st.item0 = static_cast<uint32_t>(items.size());
+        // [items][warp ranges (B)][data]: item word offsets count from the stage start
+        const size_t meta_words = built.size() * (kItemBytes / 4) + (NW > 0 ? 12 : 0);
+        arena.resize(start + ((meta_words + 3) & ~size_t(3)), 0u);
         for (Built& b : built) {
             b.it.word_off = static_cast<uint32_t>(arena.size() - start);
             if (IS_A)  // packed column layouts ahead of the segments
@@ -1088,6 +1081,9 @@ struct Builder {
                 for (uint32_t q = 0; q < specs[k].nseg; ++q) put_fields(segs[specs[k].seg0 + q]);
             items.push_back(b.it);
         }
+        for (size_t i = 0; i < built.size(); ++i)
+            std::memcpy(arena.data() + start + i * (kItemBytes / 4), &built[i].it, kItemBytes);
+        if (NW > 0) std::memcpy(arena.data() + start + built.size() * (kItemBytes / 4), &wb[wb_index * 24], 48);
         while (arena.size() % 4) arena.push_back(0u);
         st.byte_off = start * 4;
         st.bytes = static_cast<uint32_t>((arena.size() - start) * 4);
@@ -1390,13 +1386,10 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     up(h->arena, B.arena.data(), B.arena.size() * 4);
     up(h->stages, B.stages.data(), B.stages.size() * sizeof(Stage));
     B.wb.resize(std::max<size_t>(B.wb.size(), 24));
-    up(h->stage_wb, B.wb.data(), B.wb.size() * sizeof(uint16_t));
     up(h->copies, B.copies.data(), B.copies.size() * sizeof(uint64_t));
     h->work.alloc(16);
     up(h->stripe_a, stripe_a.data(), stripe_a.size() * 4);
     up(h->stripe_b, stripe_b.data(), stripe_b.size() * 4);
-    up(h->bitems, B.bitems.data(), B.bitems.size() * sizeof(BItem));
-    up(h->aitems, B.aitems.data(), B.aitems.size() * sizeof(AItem));
     up(h->wcol, wcol.data(), wcol.size() * sizeof(WCol));
     up(h->coef, coef.data(), coef.size() * 8);
     h->xpad.alloc((d.n_cols + 4) * 8);
@@ -1418,15 +1411,12 @@ Params make_params(hcmx_hmat* h, double alpha, double beta, double* y) {
     Params p{};
     p.arena = h->arena.as<uint8_t>();
     p.stages = h->stages.as<Stage>();
-    p.stage_wb = h->stage_wb.as<uint16_t>();
     p.stripe_a = h->stripe_a.as<uint32_t>();
     p.stripe_b = h->stripe_b.as<uint32_t>();
     p.copies = h->copies.as<uint64_t>();
     p.work = h->work.as<unsigned>();
     p.nstripe_a = h->nstripe_a;
     p.nblocks = h->nblocks;
-    p.bitems = h->bitems.as<BItem>();
-    p.aitems = h->aitems.as<AItem>();
     p.coef = h->coef.as<double>();
     p.wcol = h->wcol.as<WCol>();
     p.partial = h->partial.as<double>();
