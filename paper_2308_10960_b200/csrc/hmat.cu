@@ -36,6 +36,7 @@
 // sum differs from the oracle only by FP64 reassociation (||dy||/||y|| ~ 1e-15).
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #ifndef HCMX_WAIT_HINT
@@ -43,6 +44,7 @@
 #endif
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -159,8 +161,8 @@ struct LeafA {  // host-side only
 struct Params {
     const uint8_t* arena;
     const Stage* stages;
-    const uint32_t* stripe_a;   // [nstripe_a + 1] stage ranges
-    const uint32_t* stripe_b;   // [nblocks + 1]
+    const uint4* stripe_a;      // [nstripe_a] {stage begin, end, -, -}, most expensive first
+    const uint4* stripe_b;      // [nblocks] {stage begin, end, row block, -}, most expensive first
     const uint64_t* copies;     // [nstages * kCopies] staged coefficient copies (see CopyEntry)
     unsigned* work;             // [2] stripe counters of the persistent kernels (A, B), zeroed per product
     uint32_t nstripe_a, nblocks;
@@ -173,6 +175,25 @@ struct Params {
     double alpha, beta;
     int debug;                  // profiling knob (HCMX_DEBUG): 1 = consumers skip the decode
 };
+
+// ------------------------------------------------------- instrumentation --
+// HCMX_PROF builds only: per-phase cycle counters (consumer wait / busy,
+// producer wait on free slots / total), read back by the host when HCMX_PROF is
+// set in the environment.  [phase][0 wait_full, 1 busy, 2 prod_wait_empty,
+// 3 prod_total, 4 consumer warps, 5 stripe-end cycles, 6 CTA ns, 7 CTAs]
+#ifdef HCMX_PROF
+__device__ unsigned long long g_prof[2][8];
+__device__ unsigned long long g_ts[2][4];  // min start, max end, sum end, sum start (ns, globaltimer)
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define PROF_ADD(ph, i, v) atomicAdd(&g_prof[ph][i], static_cast<unsigned long long>(v))
+#else
+#define PROF_ADD(ph, i, v) ((void)0)
+#endif
+__device__ __forceinline__ long long clk() { return clock64(); }
 
 // ----------------------------------------------------------- PTX glue ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -338,8 +359,8 @@ __device__ __forceinline__ void seq_next(const Params& p, StageSeq& q, unsigned 
             q.done = true;
             return;
         }
-        const uint32_t* range = PHASE_A ? p.stripe_a : p.stripe_b;
-        const uint32_t s0 = range[id], s1 = range[id + 1];
+        const uint4 r = (PHASE_A ? p.stripe_a : p.stripe_b)[id];
+        const uint32_t s0 = r.x, s1 = r.y;
         if (s0 < s1 || !PHASE_A) {  // phase B visits empty row blocks too (y = beta y)
             q.stripe = id;
             q.s = s0;
@@ -393,11 +414,18 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
     StageMeta m0 = seq_meta<PHASE_A>(p, q, lane);
     seq_next<PHASE_A>(p, q, lane);
     StageMeta m1 = seq_meta<PHASE_A>(p, q, lane);
+    const long long t_start = clk();
+#ifdef HCMX_PROF
+    const unsigned long long g0 = gtime();
+#endif
+    long long t_wait = 0;
     for (uint32_t it = 0;; ++it) {
         seq_next<PHASE_A>(p, q, lane);
         const StageMeta m2 = seq_meta<PHASE_A>(p, q, lane);
         const int slot = static_cast<int>(it % kNStage);
+        const long long t0 = clk();
         if (it >= kNStage) mbar_wait(&empty[slot], ((it / kNStage) - 1) & 1u);
+        t_wait += clk() - t0;
         uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
         if (lane == 0) {
             uint32_t* hdr = reinterpret_cast<uint32_t*>(base + kOffHdr);
@@ -422,7 +450,21 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
                 issue_copy(p, m0.c1, base + kOffCoef, &full[slot]);
             }
         }
-        if (m0.flags & kHdrEnd) return;
+        if (m0.flags & kHdrEnd) {
+            if (lane == 0) {
+                PROF_ADD(PHASE_A ? 0 : 1, 2, t_wait);
+                PROF_ADD(PHASE_A ? 0 : 1, 3, clk() - t_start);
+                PROF_ADD(PHASE_A ? 0 : 1, 7, 1);
+#ifdef HCMX_PROF
+                const unsigned long long g1 = gtime();
+                atomicMin(&g_ts[PHASE_A ? 0 : 1][0], g0);
+                atomicMax(&g_ts[PHASE_A ? 0 : 1][1], g1);
+                atomicAdd(&g_ts[PHASE_A ? 0 : 1][2], g1 >> 8);
+                atomicAdd(&g_ts[PHASE_A ? 0 : 1][3], g0 >> 8);
+#endif
+            }
+            return;
+        }
         m0 = m1;
         m1 = m2;
     }
@@ -437,13 +479,25 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
 template <int NW, bool DYN, class Body, class End>
 __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t* empty, unsigned warp,
                                         unsigned lane, int debug, Body&& body, End&& stripe_end) {
+    long long t_wait = 0, t_busy = 0, t_end = 0;
     for (uint32_t it = 0;; ++it) {
         const int slot = static_cast<int>(it % kNStage);
+        const long long t0 = clk();
         mbar_wait(&full[slot], (it / kNStage) & 1u);
+        const long long t1 = clk();
+        t_wait += t1 - t0;
         const uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
         uint32_t* hdr = reinterpret_cast<uint32_t*>(ring + static_cast<size_t>(slot) * kSlotBytes + kOffHdr);
         const uint32_t stripe = hdr[0], flags = hdr[1];
-        if (flags & kHdrEnd) return;
+        if (flags & kHdrEnd) {
+            if (lane == 0) {
+                PROF_ADD(DYN ? 0 : 1, 0, t_wait);
+                PROF_ADD(DYN ? 0 : 1, 1, t_busy);
+                PROF_ADD(DYN ? 0 : 1, 4, 1);
+                PROF_ADD(DYN ? 0 : 1, 5, t_end);
+            }
+            return;
+        }
         if (debug) {
         } else if (DYN) {
             // the next claim is issued before the current item is decoded, so the
@@ -463,7 +517,12 @@ __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t*
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
-        if (flags & kHdrLast) stripe_end(stripe);
+        const long long t2 = clk();
+        t_busy += t2 - t1;
+        if (flags & kHdrLast) {
+            stripe_end(stripe);
+            t_end += clk() - t2;
+        }
     }
 }
 
@@ -741,7 +800,8 @@ __global__ void __launch_bounds__(kThreadsB, 2) k_phase_b(Params p) {
         [&](const uint8_t* base, unsigned i) {
             b_item(p, reinterpret_cast<const BItem*>(base)[i], base, lane, acc);
         },
-        [&](uint32_t blk) {  // block done: fixed-order pairwise sum of the warps, then y
+        [&](uint32_t sid) {  // block done: fixed-order pairwise sum of the warps, then y
+            const uint32_t blk = p.stripe_b[sid].z;
             consumer_bar();
             if (warp >= H) {
 #pragma unroll
@@ -1088,7 +1148,17 @@ struct Builder {
         st.byte_off = start * 4;
         st.bytes = static_cast<uint32_t>((arena.size() - start) * 4);
         st.nitems = static_cast<uint32_t>(built.size());
-        st.pad = wb_index;  // phase B: where the producer fetches this stage's warp ranges
+        // estimated consumer cost (warp instructions): per item, per column, per field
+        uint64_t cost = 0;
+        for (const Built& b : built) {
+            cost += 100;
+            for (size_t k = b.first; k < b.first + b.n; ++k) {
+                uint64_t fields = 0;
+                for (uint32_t q = 0; q < specs[k].nseg; ++q) fields += segs[specs[k].seg0 + q].nf;
+                cost += 15 + 12 * ((fields + 31) / 32);
+            }
+        }
+        st.pad = cost;
         st.coef_bytes = coef;
         stages.push_back(st);
         return true;
@@ -1388,8 +1458,28 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     B.wb.resize(std::max<size_t>(B.wb.size(), 24));
     up(h->copies, B.copies.data(), B.copies.size() * sizeof(uint64_t));
     h->work.alloc(16);
-    up(h->stripe_a, stripe_a.data(), stripe_a.size() * 4);
-    up(h->stripe_b, stripe_b.data(), stripe_b.size() * 4);
+    // stripes in decreasing estimated cost: the persistent CTAs claim the big ones
+    // first, so they finish together (every stripe's result is independent of
+    // which CTA computes it, so the order is free)
+    auto lpt = [&](const std::vector<uint32_t>& range, bool with_block) {
+        std::vector<std::array<uint32_t, 4>> v;
+        std::vector<uint64_t> cost;
+        for (size_t i = 0; i + 1 < range.size(); ++i) {
+            uint64_t c = 0;
+            for (uint32_t s2 = range[i]; s2 < range[i + 1]; ++s2) c += B.stages[s2].pad;
+            v.push_back({range[i], range[i + 1], with_block ? static_cast<uint32_t>(i) : 0u, 0u});
+            cost.push_back(c);
+        }
+        std::vector<size_t> ord(v.size());
+        for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+        std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return cost[a] > cost[b]; });
+        std::vector<std::array<uint32_t, 4>> out;
+        for (size_t i : ord) out.push_back(v[i]);
+        return out;
+    };
+    const auto sa = lpt(stripe_a, false), sb = lpt(stripe_b, true);
+    up(h->stripe_a, sa.data(), sa.size() * 16);
+    up(h->stripe_b, sb.data(), sb.size() * 16);
     up(h->wcol, wcol.data(), wcol.size() * sizeof(WCol));
     up(h->coef, coef.data(), coef.size() * 8);
     h->xpad.alloc((d.n_cols + 4) * 8);
@@ -1411,8 +1501,8 @@ Params make_params(hcmx_hmat* h, double alpha, double beta, double* y) {
     Params p{};
     p.arena = h->arena.as<uint8_t>();
     p.stages = h->stages.as<Stage>();
-    p.stripe_a = h->stripe_a.as<uint32_t>();
-    p.stripe_b = h->stripe_b.as<uint32_t>();
+    p.stripe_a = h->stripe_a.as<uint4>();
+    p.stripe_b = h->stripe_b.as<uint4>();
     p.copies = h->copies.as<uint64_t>();
     p.work = h->work.as<unsigned>();
     p.nstripe_a = h->nstripe_a;
@@ -1479,6 +1569,31 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
         h->last_launches++;
     }
     check_cuda(cudaGetLastError(), "matvec launch");
+#ifdef HCMX_PROF
+    static const bool prof_env = std::getenv("HCMX_PROF") != nullptr;
+    if (prof_env) {
+        unsigned long long v[2][8], ts[2][4];
+        check_cuda(cudaStreamSynchronize(s), "prof sync");
+        check_cuda(cudaMemcpyFromSymbol(v, g_prof, sizeof(v)), "prof read");
+        check_cuda(cudaMemcpyFromSymbol(ts, g_ts, sizeof(ts)), "prof read");
+        const unsigned long long z[2][8] = {};
+        check_cuda(cudaMemcpyToSymbol(g_prof, z, sizeof(z)), "prof reset");
+        const unsigned long long zt[2][4] = {{~0ull, 0, 0, 0}, {~0ull, 0, 0, 0}};
+        check_cuda(cudaMemcpyToSymbol(g_ts, zt, sizeof(zt)), "prof reset");
+        for (int ph = 0; ph < 2; ++ph) {
+            const double w = v[ph][4] ? double(v[ph][4]) : 1.0, c = v[ph][7] ? double(v[ph][7]) : 1.0;
+            std::fprintf(stderr,
+                         "[prof %c] per consumer warp: wait_full %.1f us busy %.1f us stripe_end %.1f us | per producer: "
+                         "wait_empty %.1f us total %.1f us (1.965 GHz)\n",
+                         ph ? 'B' : 'A', v[ph][0] / w / 1965.0, v[ph][1] / w / 1965.0, v[ph][5] / w / 1965.0,
+                         v[ph][2] / c / 1965.0, v[ph][3] / c / 1965.0);
+            if (ts[ph][0] != ~0ull)
+                std::fprintf(stderr, "[prof %c] CTA start: avg +%.1f us; CTA end: avg +%.1f us, last +%.1f us\n",
+                             ph ? 'B' : 'A', (ts[ph][3] / c * 256.0 - ts[ph][0]) / 1e3, (ts[ph][2] / c * 256.0 - ts[ph][0]) / 1e3,
+                             (ts[ph][1] - ts[ph][0]) / 1e3);
+        }
+    }
+#endif
     if (h->timing) {
         check_cuda(cudaEventRecord(rec.b1, s), "event");
         h->pending.push_back(rec);
