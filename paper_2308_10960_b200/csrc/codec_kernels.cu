@@ -285,9 +285,10 @@ __device__ __forceinline__ int pack_groups(const double* __restrict__ v, uint64_
 
 // Packing of 32-bit fields (w <= 32): lane j encodes value 32g + j into field
 // f at bit j w of the group; its low part goes to word q = j w / 32, its high
-// part (if it straddles) to word q + 1, ORed into a per-warp shared buffer of
-// w + 1 words (shared atomics; a word has <= ceil(32 / w) + 1 writers), then
-// the w words are stored coalesced.  Same bits as encode_value / pack_groups.
+// part (if it straddles) to word q + 1, ORed into a per-warp shared buffer
+// (shared atomics; a word has <= ceil(32 / w) + 1 writers); the w words are
+// then stored coalesced.  Four groups share each round of warp barriers.  The
+// field arithmetic is encode_value's in 32 bits (e + m <= 31): same bits.
 __device__ __forceinline__ int pack_groups32(const double* __restrict__ v, uint32_t n, uint32_t g0, uint32_t g1,
                                              unsigned e, unsigned m, unsigned w, double scale,
                                              uint32_t* __restrict__ out, unsigned lane, uint32_t gstride,
@@ -296,7 +297,12 @@ __device__ __forceinline__ int pack_groups32(const double* __restrict__ v, uint3
     const uint32_t max_offset = (1u << e) - 1u;
     const uint64_t round_add = 1ull << (51 - m);
     const uint32_t mant_mask = (1u << m) - 1u;
+    const unsigned sgn_sh = e + m;
+    const bool m_lo = m <= 20;
+    const unsigned msh = m_lo ? 20u - m : 52u - m;
     const unsigned bit = lane * w, q = bit >> 5, s = bit & 31u;
+    const bool straddle = s + w > 32;
+    const uint32_t nfull = n / 32;
     int nf_bad = 0;
     for (uint32_t g4 = g0; g4 < g1; g4 += 4 * gstride) {
         double xs[4];
@@ -306,42 +312,40 @@ __device__ __forceinline__ int pack_groups32(const double* __restrict__ v, uint3
             const uint32_t idx = g * 32 + lane;
             xs[i] = (g < g1 && idx < n) ? __ldcs(v + idx) : 0.0;
         }
+        uint32_t f[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            // the caller rejected non-finite input; zeros keep only their sign
+            // (selected, not branched: 1 / scale may be inf for a subnormal scale)
+            const double x = xs[i];
+            const uint32_t sign = static_cast<uint32_t>(__double2hiint(x)) >> 31;
+            const double vp = __dadd_rn(__dmul_rn(fabs(x), inv_scale), 1.0);  // no FMA (codec.cpp:124)
+            const uint64_t u = dbits(vp) + round_add;
+            const uint32_t uh = static_cast<uint32_t>(u >> 32), ul = static_cast<uint32_t>(u);
+            uint32_t offset = (uh >> 20) - 1023u;
+            uint32_t mant = (m_lo ? uh >> msh : __funnelshift_r(ul, uh, msh)) & mant_mask;
+            const bool sat = offset > max_offset || static_cast<uint32_t>(__double2hiint(vp)) >= 0x7ff00000u;
+            offset = sat ? max_offset : offset;
+            mant = sat ? mant_mask : mant;
+            f[i] = (sign << sgn_sh) | (x != 0.0 ? (offset << m) | mant : 0u);
+            sw[i * 36 + lane] = 0u;
+            if (lane == 0) sw[i * 36 + 32] = 0u;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            atomicOr(sw + i * 36 + q, f[i] << s);
+            if (straddle) atomicOr(sw + i * 36 + q + 1, f[i] >> (32u - s));
+        }
+        __syncwarp();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const uint32_t g = g4 + i * gstride;
             if (g >= g1) break;
-            const uint32_t idx = g * 32 + lane;
-            const double x = xs[i];
-            uint32_t f = 0;
-            if (idx < n) {
-                const uint32_t sign = static_cast<uint32_t>(__double2hiint(x)) >> 31;
-                f = sign << (e + m);
-                if (!isfinite(x)) {
-                    nf_bad = 1;
-                    f = 0;
-                } else if (x != 0.0) {
-                    const double vp = __dadd_rn(__dmul_rn(fabs(x), inv_scale), 1.0);  // >= 2, no FMA
-                    const uint64_t u = dbits(vp) + round_add;
-                    uint32_t offset = static_cast<uint32_t>(u >> 52) - 1023u;
-                    uint32_t mant = static_cast<uint32_t>(u >> (52 - m)) & mant_mask;
-                    if (offset > max_offset || !isfinite(vp)) {
-                        offset = max_offset;
-                        mant = mant_mask;
-                    }
-                    f |= (offset << m) | mant;
-                }
-            }
-            sw[lane] = 0u;
-            if (lane == 0) sw[32] = 0u;
-            __syncwarp();
-            atomicOr(sw + q, f << s);
-            if (s + w > 32) atomicOr(sw + q + 1, f >> (32u - s));
-            __syncwarp();
-            const uint32_t nvalid = min(32u, n - g * 32);
-            const unsigned nwords = (nvalid * w + 31) / 32;
-            if (lane < nwords) __stcs(out + g * w + lane, sw[lane]);
-            __syncwarp();
+            const unsigned nwords = g < nfull ? w : ((n - g * 32) * w + 31) / 32;
+            if (lane < nwords) __stcs(out + g * w + lane, sw[i * 36 + lane]);
         }
+        __syncwarp();
     }
     return __any_sync(0xffffffffu, nf_bad);
 }
@@ -476,57 +480,62 @@ k_compress_cta(const double* __restrict__ values, const uint64_t* __restrict__ v
                uint32_t* __restrict__ flags, int* __restrict__ err) {
     __shared__ uint64_t s_mn[kCtaWarps], s_mx[kCtaWarps];
     __shared__ unsigned s_nz[kCtaWarps], s_nf[kCtaWarps];
-    __shared__ uint32_t s_words[kCtaWarps][40];
+    __shared__ uint32_t s_words[kCtaWarps][4][36];
     const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     for (uint64_t b = blockIdx.x; b < nbuf; b += gridDim.x) {
-        const uint64_t n = count[b];
+        const uint64_t n = count[b];  // <= kFuseMax
+        const uint32_t n32 = static_cast<uint32_t>(n);
         const double* v = values + voff[b];
-        uint64_t mn = 0x7FF0000000000000ull, mx = 0;
-        unsigned nz = 0, nf = 0;
+        // min / max of the nonzero |v| on the bit patterns (non-negative doubles
+        // order like their bits).  |v| - 1 wraps a zero to the largest value, so
+        // the min skips zeros without a test; a non-finite value shows up as a
+        // max at or above +inf (the buffer is then rejected, codec.cpp:119-120).
+        uint64_t mnm1 = ~0ull, mx = 0;
+        uint32_t orv = 0;
         constexpr unsigned T = kCtaWarps * 32;
-        for (uint64_t i = tid; i < n; i += 8 * T) {
-            double xs[8];
+        for (uint32_t i = tid; i < n32; i += 8 * T) {
+            uint64_t xs[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) xs[u] = i + T * u < n ? __ldcg(v + i + T * u) : 0.0;
+            for (int u = 0; u < 8; ++u)
+                xs[u] = i + T * u < n32 ? static_cast<uint64_t>(__ldcg(reinterpret_cast<const long long*>(v) + i + T * u))
+                                        : 0ull;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const double a = fabs(xs[u]);
-                if (a != 0.0) nz = 1;
-                if (!isfinite(xs[u])) nf = 1;
-                if (a != 0.0 && !isnan(a)) {
-                    const uint64_t ab = dbits(a);
-                    mn = ab < mn ? ab : mn;
-                    mx = ab > mx ? ab : mx;
-                }
+                const uint64_t a = xs[u] & 0x7fffffffffffffffull;
+                orv |= static_cast<uint32_t>(a >> 32) | static_cast<uint32_t>(a);
+                const uint64_t am1 = a - 1;
+                mnm1 = am1 < mnm1 ? am1 : mnm1;
+                mx = a > mx ? a : mx;
             }
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
-            const uint64_t omn = __shfl_xor_sync(0xffffffffu, mn, o);
+            const uint64_t omn = __shfl_xor_sync(0xffffffffu, mnm1, o);
             const uint64_t omx = __shfl_xor_sync(0xffffffffu, mx, o);
-            mn = omn < mn ? omn : mn;
+            mnm1 = omn < mnm1 ? omn : mnm1;
             mx = omx > mx ? omx : mx;
         }
-        nz = __any_sync(0xffffffffu, nz);
-        nf = __any_sync(0xffffffffu, nf);
+        unsigned nz = __any_sync(0xffffffffu, orv != 0);
+        unsigned nf = mx >= 0x7FF0000000000000ull ? 1u : 0u;
         if (lane == 0) {
-            s_mn[warp] = mn;
+            s_mn[warp] = mnm1;
             s_mx[warp] = mx;
             s_nz[warp] = nz;
             s_nf[warp] = nf;
         }
         __syncthreads();
-        mn = s_mn[0];
+        mnm1 = s_mn[0];
         mx = s_mx[0];
         nz = s_nz[0];
         nf = s_nf[0];
 #pragma unroll
         for (int q = 1; q < kCtaWarps; ++q) {
-            mn = s_mn[q] < mn ? s_mn[q] : mn;
+            mnm1 = s_mn[q] < mnm1 ? s_mn[q] : mnm1;
             mx = s_mx[q] > mx ? s_mx[q] : mx;
             nz |= s_nz[q];
             nf |= s_nf[q];
         }
+        const uint64_t mn = mnm1 + 1;
         __syncthreads();  // s_* reused by the next buffer
         const bool all_zero = !nz;
         const double dmin = all_zero ? 0.0 : bitsd(mn), dmax = all_zero ? 0.0 : bitsd(mx);
@@ -575,8 +584,8 @@ k_compress_cta(const double* __restrict__ values, const uint64_t* __restrict__ v
         }
         if (nf) continue;
         if (w <= 32)
-            pack_groups32(v, static_cast<uint32_t>(n), warp, static_cast<uint32_t>((n + 31) / 32), e, m, w, scale,
-                          reinterpret_cast<uint32_t*>(payload + poff[b]), lane, kCtaWarps, s_words[warp]);
+            pack_groups32(v, n32, warp, (n32 + 31) / 32, e, m, w, scale,
+                          reinterpret_cast<uint32_t*>(payload + poff[b]), lane, kCtaWarps, &s_words[warp][0][0]);
         else
             pack_groups(v, n, warp, static_cast<uint32_t>((n + 31) / 32), e, m, w, scale,
                         reinterpret_cast<uint32_t*>(payload + poff[b]), lane, kCtaWarps);
