@@ -90,6 +90,8 @@ class BlockStats:
 def _dev_f64(values) -> torch.Tensor:
     _lib.ensure_device()
     if isinstance(values, torch.Tensor):
+        if values.is_cuda and values.dtype == torch.float64 and values.is_contiguous():
+            return values.detach()
         return values.detach().to(device="cuda", dtype=torch.float64).contiguous()
     return torch.as_tensor(np.ascontiguousarray(values, dtype=np.float64)).cuda()
 

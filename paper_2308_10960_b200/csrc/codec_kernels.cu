@@ -17,6 +17,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -477,7 +480,7 @@ k_compress_cta(const double* __restrict__ values, const uint64_t* __restrict__ v
                const uint64_t* __restrict__ count, uint64_t nbuf, int scheme, unsigned m_req,
                const uint64_t* __restrict__ poff, uint8_t* __restrict__ payload,
                hcmx_descriptor* __restrict__ desc, hcmx_stats* __restrict__ stats,
-               uint32_t* __restrict__ flags, int* __restrict__ err) {
+               uint32_t* __restrict__ flags) {
     __shared__ uint64_t s_mn[kCtaWarps], s_mx[kCtaWarps];
     __shared__ unsigned s_nz[kCtaWarps], s_nf[kCtaWarps];
     __shared__ uint32_t s_words[kCtaWarps][4][36];
@@ -579,8 +582,7 @@ k_compress_cta(const double* __restrict__ values, const uint64_t* __restrict__ v
             st.all_zero = all_zero ? 1u : 0u;
             st.non_finite = nf;
             stats[b] = st;
-            flags[b] = ambiguous;
-            if (nf) *err = 1;
+            flags[b] = ambiguous | (nf ? 2u : 0u);  // bit 1: non-finite input (rejected)
         }
         if (nf) continue;
         if (w <= 32)
@@ -788,17 +790,12 @@ int grid_for(uint64_t njobs) {
 // the same layout do no host-to-device traffic and no synchronisation.
 struct LayoutCache {
     std::mutex mu;
-    uint64_t nbuf = ~0ull, hash = 0, nchunks = 0;
+    uint64_t nbuf = ~0ull, nchunks = 0;
+    std::vector<uint64_t> h_count, h_poff;  // host copies the device arrays were made from
     DevBuf count, coff, cbuf;
-    uint64_t poff_hash = 0;
     DevBuf poff;
 };
 LayoutCache g_layout;
-
-uint64_t fnv(const uint64_t* a, uint64_t n, uint64_t h = 1469598103934665603ull) {
-    for (uint64_t i = 0; i < n; ++i) h = (h ^ a[i]) * 1099511628211ull;
-    return h;
-}
 
 // pinned staging for small device-to-host results (descriptors, flags)
 struct Pinned {
@@ -822,8 +819,7 @@ Pinned g_pinned;
 
 // layout arrays for h_count (caller holds g_layout.mu)
 static void layout_arrays(const uint64_t* h_count, uint64_t nbuf, void* stream) {
-    const uint64_t h = fnv(h_count, nbuf);
-    if (g_layout.nbuf == nbuf && g_layout.hash == h) return;
+    if (g_layout.nbuf == nbuf && std::memcmp(g_layout.h_count.data(), h_count, nbuf * 8) == 0) return;
     check_cuda(cudaDeviceSynchronize(), "layout cache");  // kernels may still read the old arrays
     std::vector<uint64_t> coff(nbuf + 1, 0);
     for (uint64_t b = 0; b < nbuf; ++b) coff[b + 1] = coff[b] + (h_count[b] + 1023) / 1024;
@@ -838,19 +834,18 @@ static void layout_arrays(const uint64_t* h_count, uint64_t nbuf, void* stream) 
     h2d(g_layout.cbuf.p, cbuf.data(), cbuf.size() * 4, stream);
     stream_sync(stream);
     g_layout.nbuf = nbuf;
-    g_layout.hash = h;
+    g_layout.h_count.assign(h_count, h_count + nbuf);
     g_layout.nchunks = coff[nbuf];
-    g_layout.poff_hash = 0;
+    g_layout.h_poff.clear();
 }
 
 static const uint64_t* layout_poff(const uint64_t* h_poff, uint64_t nbuf, void* stream) {
-    const uint64_t h = fnv(h_poff, nbuf, 7);
-    if (g_layout.poff_hash != h || !g_layout.poff.p) {
+    if (g_layout.h_poff.size() != nbuf || std::memcmp(g_layout.h_poff.data(), h_poff, nbuf * 8) != 0) {
         check_cuda(cudaDeviceSynchronize(), "layout cache");
         g_layout.poff.alloc(std::max<uint64_t>(16, nbuf * 8));
         h2d(g_layout.poff.p, h_poff, nbuf * 8, stream);
         stream_sync(stream);
-        g_layout.poff_hash = h;
+        g_layout.h_poff.assign(h_poff, h_poff + nbuf);
     }
     return g_layout.poff.as<uint64_t>();
 }
@@ -996,6 +991,14 @@ int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff, cons
                             uint64_t nbuf, double eps, int scheme, uint8_t* d_payload,
                             uint64_t payload_capacity, hcmx_descriptor* h_desc, uint64_t* h_poff,
                             uint64_t* h_total, void* stream) {
+    static const bool trace = std::getenv("HCMX_TRACE") != nullptr;
+    auto T0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "%s %.1f us\n", what, std::chrono::duration<double, std::micro>(t - T0).count());
+        T0 = t;
+    };
     return guarded([&] {
         require_device();
         alignment_unit(scheme);
@@ -1029,33 +1032,37 @@ int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff, cons
         }
         *h_total = off;
         if (off > payload_capacity) throw invalid_argument("compress: payload capacity too small");
+        mark("pre");
         std::lock_guard<std::mutex> g(g_layout.mu);
         layout_arrays(h_count, nbuf, stream);
         const uint64_t* dp = layout_poff(h_poff, nbuf, stream);
-        // one device block for descriptors | flags | error, one pinned block for the read-back
-        const size_t o_fl = round16(nbuf * sizeof(hcmx_descriptor)), o_err = o_fl + round16(nbuf * 4);
-        DevBuf out(o_err + 16);
+        mark("layout");
+        // one device block for descriptors | flags, one pinned block for the read-back
+        const size_t o_fl = round16(nbuf * sizeof(hcmx_descriptor)), o_end = o_fl + round16(nbuf * 4);
+        DevBuf out(o_end);
         DevBuf dst(std::max<uint64_t>(24, nbuf * sizeof(hcmx_stats)));
         cudaStream_t s = (cudaStream_t)stream;
         uint8_t* ob = out.as<uint8_t>();
-        check_cuda(cudaMemsetAsync(ob + o_err, 0, sizeof(int), s), "memset");
         const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(nbuf, 148ull * 16));
         k_compress_cta<<<grid, kCtaWarps * 32, 0, s>>>(d_values, d_voff, g_layout.count.as<uint64_t>(), nbuf,
                                                        scheme, m_req, dp, d_payload,
                                                        reinterpret_cast<hcmx_descriptor*>(ob), dst.as<hcmx_stats>(),
-                                                       reinterpret_cast<uint32_t*>(ob + o_fl),
-                                                       reinterpret_cast<int*>(ob + o_err));
+                                                       reinterpret_cast<uint32_t*>(ob + o_fl));
         check_cuda(cudaGetLastError(), "compress launch");
+        mark("launch");
         std::lock_guard<std::mutex> gp(g_pinned.mu);
-        uint8_t* hb = static_cast<uint8_t*>(g_pinned.get(o_err + 16));
-        d2h(hb, ob, o_err + sizeof(int), stream);
+        uint8_t* hb = static_cast<uint8_t*>(g_pinned.get(o_end));
+        d2h(hb, ob, o_fl + nbuf * 4, stream);
+        mark("d2h issue");
         stream_sync(stream);
+        mark("sync");
         std::memcpy(h_desc, hb, nbuf * sizeof(hcmx_descriptor));
         const uint32_t* flags = reinterpret_cast<const uint32_t*>(hb + o_fl);
-        if (*reinterpret_cast<const int*>(hb + o_err)) throw invalid_argument("compress: values must be finite");
+        for (uint64_t b = 0; b < nbuf; ++b)
+            if (flags[b] & 2u) throw invalid_argument("compress: values must be finite");
         // exponent widths next to a 2^k - 2 threshold: decide with glibc (codec.cpp:72-73)
         for (uint64_t b = 0; b < nbuf; ++b) {
-            if (!flags[b]) continue;
+            if (!(flags[b] & 1u)) continue;
             hcmx_stats st{};
             d2h(&st, dst.as<hcmx_stats>() + b, sizeof(hcmx_stats), stream);
             uint64_t vo = 0;
