@@ -78,10 +78,10 @@ constexpr int kG = kR / 32;           // row groups (accumulators) per lane
 constexpr int kAChunk = 256;          // X fields per A item (8 per lane)
 constexpr int kAGroup = 4;            // max rank columns per A item
 constexpr int kBDenseGroup = 8;       // max dense columns per B item
-constexpr int kBLRGroup = 8;          // max rank columns per B item
+constexpr int kBLRGroup = 16;         // max rank columns per B item
 constexpr uint64_t kAStripeBytes = 8 * kStageBytes;  // target packed bytes per phase-A CTA
 constexpr uint64_t kItemTarget = 1536;          // packed bytes per item (columns grouped up to this)
-constexpr uint64_t kItemMaxBytes = 2048;        // items merge columns up to this many packed bytes
+constexpr uint64_t kItemMaxBytes = 4096;        // items merge columns up to this many packed bytes
 constexpr size_t kRingBytes = static_cast<size_t>(kNStage) * kSlotBytes;
 constexpr size_t kRedBytes = (kNWB / 2) * kR * sizeof(double);  // phase-B cross-warp reduction
 constexpr size_t kSmemBytes = kRingBytes + kRedBytes + 2 * kNStage * sizeof(uint64_t);  // + full, empty barriers
