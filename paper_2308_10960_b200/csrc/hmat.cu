@@ -1053,22 +1053,17 @@ struct Builder {
             uint64_t words;
         };
         std::vector<Built> built;
+        // Coefficient ranges the stage's items read (table 0: x, 8-byte entries,
+        // copied from an even index; table 1: WCol records).  Ranges of one table
+        // that overlap or lie close together merge into one bulk copy: each copy
+        // costs the producer far more than the few extra bytes it brings.
         struct Slice {
-            uint32_t table, start, count, off;
+            uint32_t table, start, end, off;  // [start, end) elements; start even for table 0
         };
         std::vector<Slice> slices;
         uint32_t coef = 0;
-        // table 0: x (8-byte entries, copied from an even index), table 1: WCol records
-        auto slice_bytes = [](uint32_t table, uint32_t start, uint32_t count) {
-            return table == 0 ? r16((count + (start & 1u)) * 8) : count * static_cast<uint32_t>(sizeof(WCol));
-        };
-        auto slice_of = [&](const Spec<Item>& sp) -> const Slice& {
-            for (const Slice& sl : slices)
-                if (sl.table == sp.sl_table && sl.start == sp.sl_start && sl.count >= sp.sl_count) return sl;
-            slices.push_back({sp.sl_table, sp.sl_start, sp.sl_count, coef});
-            coef += slice_bytes(sp.sl_table, sp.sl_start, sp.sl_count);
-            return slices.back();
-        };
+        auto esize = [](uint32_t table) { return table == 0 ? 8u : static_cast<uint32_t>(sizeof(WCol)); };
+        auto slice_bytes = [&](const Slice& s) { return r16((s.end - s.start) * esize(s.table)); };
         std::vector<size_t> cut = {pos, end};
         if (NW > 0) {
             uint64_t total = 0;
@@ -1095,15 +1090,44 @@ struct Builder {
                 words += specs[j++].words;
             Item it = specs[i].it;
             it.nseg = static_cast<uint8_t>(j - i);
-            const Slice sl = slice_of(specs[i]);
-            const uint32_t off = sl.table == 0 ? sl.off + (specs[i].elem - (sl.start & ~1u)) * 8
-                                               : sl.off + (specs[i].elem - sl.start) * static_cast<uint32_t>(sizeof(WCol));
-            if constexpr (IS_A) it.x_off = off;
-            else it.coef_off = off;
+            const uint32_t t = specs[i].sl_table;
+            slices.push_back({t, t == 0 ? specs[i].sl_start & ~1u : specs[i].sl_start,
+                              specs[i].sl_start + specs[i].sl_count, 0});
             built.push_back({it, i, j - i, words});
             i = j;
           }
           piece_end.push_back(static_cast<uint32_t>(built.size()));
+        }
+        {  // merge: sort by (table, start); join ranges whose gap is small
+            std::sort(slices.begin(), slices.end(), [](const Slice& a, const Slice& b) {
+                return a.table != b.table ? a.table < b.table : a.start < b.start;
+            });
+            std::vector<Slice> merged;
+            for (const Slice& s : slices) {
+                const uint32_t gap = s.table == 0 ? 32u : 4u;  // elements (256 B of x, 128 B of records)
+                if (!merged.empty() && merged.back().table == s.table && s.start <= merged.back().end + gap) {
+                    merged.back().end = std::max(merged.back().end, s.end);
+                } else {
+                    merged.push_back(s);
+                }
+            }
+            slices.swap(merged);
+            for (Slice& s : slices) {
+                s.off = coef;
+                coef += slice_bytes(s);
+            }
+            for (Built& b : built) {  // item offsets into the merged ranges
+                const Spec<Item>& sp = specs[b.first];
+                const uint32_t t = sp.sl_table;
+                for (const Slice& s : slices) {
+                    if (s.table == t && s.start <= sp.sl_start && sp.sl_start + sp.sl_count <= s.end) {
+                        const uint32_t off = s.off + (sp.elem - s.start) * esize(t);
+                        if constexpr (IS_A) b.it.x_off = off;
+                        else b.it.coef_off = off;
+                        break;
+                    }
+                }
+            }
         }
         if (built.size() > static_cast<size_t>(kMaxItems) || coef > static_cast<uint32_t>(kCoefBytes) ||
             slices.size() > static_cast<size_t>(kCopies)) {
@@ -1123,9 +1147,7 @@ struct Builder {
         const size_t c0 = copies.size();
         copies.resize(c0 + kCopies, 0);
         for (size_t q = 0; q < slices.size(); ++q)
-            copies[c0 + q] = copy_entry(slices[q].table == 0 ? slices[q].start & ~1u : slices[q].start, slices[q].off,
-                                        slice_bytes(slices[q].table, slices[q].start, slices[q].count),
-                                        slices[q].table);
+            copies[c0 + q] = copy_entry(slices[q].start, slices[q].off, slice_bytes(slices[q]), slices[q].table);
         while (arena.size() % 4) arena.push_back(0u);  // 16-byte aligned stages
         const uint64_t start = arena.size();
         Stage st{};
