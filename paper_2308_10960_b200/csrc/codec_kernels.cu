@@ -371,108 +371,13 @@ k_pack(const double* __restrict__ values, const uint64_t* __restrict__ voff,
     }
 }
 
-// codec.cpp:142-144 compress fused per buffer (one warp each): analyze,
-// descriptor selection on the device, pack.  The exponent width uses the
-// device log2; when log2(max) - log2(min) + 2 falls within 1e-9 (relative) of a
-// power of two 2^2..2^10 the buffer is flagged and the host re-decides with
-// glibc's log2 exactly like the reference (and repacks if it differs).
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-k_compress_fused(const double* __restrict__ values, const uint64_t* __restrict__ voff,
-                 const uint64_t* __restrict__ count, uint64_t nbuf, int scheme, unsigned m_req,
-                 const uint64_t* __restrict__ poff, uint8_t* __restrict__ payload,
-                 hcmx_descriptor* __restrict__ desc, hcmx_stats* __restrict__ stats,
-                 uint32_t* __restrict__ flags, int* __restrict__ err) {
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-    for (uint64_t b = wid; b < nbuf; b += nw) {
-        const uint64_t n = count[b];
-        const double* v = values + voff[b];
-        uint64_t mn = 0x7FF0000000000000ull, mx = 0;
-        unsigned nz = 0, nf = 0;
-        for (uint64_t i = lane; i < n; i += 128) {
-            double xs[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) xs[u] = i + 32 * u < n ? __ldcg(v + i + 32 * u) : 0.0;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const double a = fabs(xs[u]);
-                if (a != 0.0) nz = 1;
-                if (!isfinite(xs[u])) nf = 1;
-                if (a != 0.0 && !isnan(a)) {
-                    const uint64_t ab = dbits(a);
-                    mn = ab < mn ? ab : mn;
-                    mx = ab > mx ? ab : mx;
-                }
-            }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            const uint64_t omn = __shfl_xor_sync(0xffffffffu, mn, o);
-            const uint64_t omx = __shfl_xor_sync(0xffffffffu, mx, o);
-            mn = omn < mn ? omn : mn;
-            mx = omx > mx ? omx : mx;
-        }
-        nz = __any_sync(0xffffffffu, nz);
-        nf = __any_sync(0xffffffffu, nf);
-        const bool all_zero = !nz;
-        const double dmin = all_zero ? 0.0 : bitsd(mn), dmax = all_zero ? 0.0 : bitsd(mx);
-        unsigned e = 2, ambiguous = 0;
-        if (scheme == HCMX_BFL) {
-            e = 8;
-        } else if (scheme == HCMX_DFL) {
-            e = 11;
-        } else if (!all_zero) {  // codec.cpp:69-75 with the device log2
-            const double span = log2(dmax) - log2(dmin) + 1.0;
-            const double vv = span + 1.0;
-            const double bits = ceil(log2(vv));
-            e = static_cast<unsigned>(fmin(fmax(bits, 2.0), 11.0));
-            for (int k = 2; k <= 10; ++k) {
-                const double pk = ldexp(1.0, k);
-                if (fabs(vv - pk) <= pk * 1e-9) ambiguous = 1;
-            }
-        }
-        unsigned m = m_req;
-        if (scheme != HCMX_AFL) {  // codec.cpp:25-30
-            const unsigned unit = scheme == HCMX_DFL ? 16u : 8u;
-            unsigned w = 1 + e + m;
-            w += (unit - w % unit) % unit;
-            m = min(52u, w - 1 - e);
-        }
-        const unsigned unit = scheme == HCMX_AFL ? 1u : (scheme == HCMX_DFL ? 16u : 8u);
-        unsigned w = 1 + e + m;
-        w += (unit - w % unit) % unit;
-        const double scale = all_zero ? 1.0 : dmin;
-        if (lane == 0) {
-            hcmx_descriptor d;
-            d.scheme = static_cast<uint8_t>(scheme);
-            d.exp_bits = static_cast<uint8_t>(e);
-            d.mant_bits = static_cast<uint8_t>(m);
-            d.bit_width = static_cast<uint8_t>(w);
-            d.reserved = 0;
-            d.scale = scale;
-            desc[b] = d;
-            hcmx_stats st;
-            st.min_mag = dmin;
-            st.max_mag = dmax;
-            st.all_zero = all_zero ? 1u : 0u;
-            st.non_finite = nf;
-            stats[b] = st;
-            flags[b] = ambiguous;
-        }
-        if (nf) {
-            if (lane == 0) *err = 1;
-            continue;
-        }
-        pack_groups(v, n, 0, static_cast<uint32_t>((n + 31) / 32), e, m, w, scale,
-                    reinterpret_cast<uint32_t*>(payload + poff[b]), lane);
-    }
-}
-
 // codec.cpp:142-144 fused per buffer, one CTA of kCtaWarps warps per buffer:
 // pass 1 (min/max, every thread, 8 loads in flight), block reduction, the
-// layout rules (device log2 + ambiguity flag as in k_compress_fused), pass 2
-// packs groups warp-strided (the values come back from L2).
+// layout rules, pass 2 packs groups warp-strided (the values come back from
+// L2).  The exponent width uses the device log2; when log2(max) - log2(min) + 2
+// falls within 1e-9 (relative) of a power of two 2^2..2^10 the buffer is
+// flagged and the host re-decides with glibc's log2 exactly like the reference
+// (and repacks if it differs).
 constexpr int kCtaWarps = 4;
 
 __global__ void __launch_bounds__(kCtaWarps * 32)
@@ -607,68 +512,6 @@ __device__ __forceinline__ double decode_field(uint64_t field, unsigned e, unsig
         v = __dmul_rn(bitsd((biased << 52) | (mant << (52 - m))) - 1.0, scale);
     }
     return sign ? -v : v;
-}
-
-// Unpacking: the w words of a group are loaded by w lanes (coalesced, four
-// groups in flight per warp); lane j pulls the 2-3 words holding field j with
-// shuffles and decodes it; the 32 doubles are stored coalesced.
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-k_unpack(const uint8_t* __restrict__ payload, const uint64_t* __restrict__ poff,
-         const uint64_t* __restrict__ count, const hcmx_descriptor* __restrict__ desc,
-         const uint64_t* __restrict__ voff, const Job* __restrict__ jobs, uint64_t njobs,
-         double* __restrict__ out) {
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-    for (uint64_t j = wid; j < njobs; j += nw) {
-        const Job jb = jobs[j];
-        const hcmx_descriptor d = desc[jb.buf];
-        const unsigned e = d.exp_bits, m = d.mant_bits, w = d.bit_width;
-        const uint64_t n = count[jb.buf];
-        const uint32_t* p = reinterpret_cast<const uint32_t*>(payload + poff[jb.buf]);
-        double* o = out + voff[jb.buf];
-        const unsigned bit = lane * w, q = bit >> 5, sh = bit & 31;
-        const uint64_t wmask = (w == 64) ? ~0ull : ((1ull << w) - 1);
-        const uint32_t gend = jb.g0 + jb.ng;
-        for (uint32_t g = jb.g0; g < gend; g += 8) {
-            uint32_t wa[8], wb[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const uint32_t gi = g + i;
-                wa[i] = wb[i] = 0;
-                if (gi < gend) {
-                    const uint64_t nvalid = umin64(32, n - (uint64_t)gi * 32);
-                    const unsigned nwords = (unsigned)((nvalid * w + 31) / 32);
-                    if (lane < nwords) wa[i] = __ldcs(p + (uint64_t)gi * w + lane);
-                    if (lane + 32 < nwords) wb[i] = __ldcs(p + (uint64_t)gi * w + 32 + lane);
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const uint32_t gi = g + i;
-                if (gi >= gend) break;
-                uint32_t w0, w1, w2 = 0;
-                if (w <= 32) {
-                    w0 = __shfl_sync(0xffffffffu, wa[i], q);
-                    w1 = __shfl_sync(0xffffffffu, wa[i], (q + 1) & 31u);
-                } else {
-                    const uint32_t a0 = __shfl_sync(0xffffffffu, wa[i], q & 31u);
-                    const uint32_t b0 = __shfl_sync(0xffffffffu, wb[i], q & 31u);
-                    const uint32_t a1 = __shfl_sync(0xffffffffu, wa[i], (q + 1) & 31u);
-                    const uint32_t b1 = __shfl_sync(0xffffffffu, wb[i], (q + 1) & 31u);
-                    const uint32_t a2 = __shfl_sync(0xffffffffu, wa[i], (q + 2) & 31u);
-                    const uint32_t b2 = __shfl_sync(0xffffffffu, wb[i], (q + 2) & 31u);
-                    w0 = q < 32 ? a0 : b0;
-                    w1 = q + 1 < 32 ? a1 : b1;
-                    w2 = q + 2 < 32 ? a2 : b2;
-                }
-                uint64_t win = ((uint64_t)w1 << 32 | w0) >> sh;
-                if (sh + w > 64) win |= (uint64_t)w2 << (64 - sh);
-                const uint64_t idx = (uint64_t)gi * 32 + lane;
-                if (idx < n) __stcs(o + idx, decode_field(win & wmask, e, m, d.scale));
-            }
-        }
-    }
 }
 
 // Job-free unpacking: warp chunks of 32 groups (1024 values); chunk c belongs
