@@ -202,3 +202,27 @@ def test_analyze_matches_reference(gpu, oracle):
               np.array([0.0, np.inf, 2.0])):
         st = codec.analyze(v)
         assert (st.min_mag, st.max_mag, st.all_zero) == oracle.analyze(v)
+
+
+def test_large_buffers_unfused_path(gpu, oracle):
+    """buffers above the fused kernel's 2^17 values go through device analyze +
+    host layout selection + device pack; mixed with small ones in one batch"""
+    from paper_2308_10960_b200 import codec
+    rng = np.random.default_rng(11)
+    counts = np.array([300000, 5, 140000, 0, 4096], np.uint64)
+    n = int(counts.sum())
+    v = np.sign(rng.standard_normal(n)) * 10 ** rng.uniform(-9, 3, n)
+    v[::97] = 0.0
+    for eps, s in ((1e-6, 0), (1e-9, 2), (1e-3, 3)):
+        bb = codec.compress_batch(torch.as_tensor(v).cuda(), counts, eps, s)
+        host = bb.payload.cpu().numpy()
+        dec = codec.decompress_batch(bb).cpu().numpy()
+        o = 0
+        for b in range(counts.size):
+            c = int(counts[b])
+            ob = oracle.compress(v[o: o + c], eps, s)
+            g = bb.buffer(b, host)
+            assert (g.descriptor.exp_bits, g.descriptor.mant_bits) == (ob.e, ob.m), (eps, s, b)
+            assert g.payload == ob.payload, (eps, s, b)
+            assert (dec[o: o + c].view(np.uint64) == oracle.decompress(ob).view(np.uint64)).all()
+            o += c

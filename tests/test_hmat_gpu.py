@@ -150,3 +150,32 @@ def test_config1_full_size(gpu, oracle):
     assert rep.dense_leaves == info["dense_leaves"]
     rate = rep.uncompressed_equivalent / (rep.dense_compressed + rep.lowrank_compressed)
     assert rate > 3.0  # ~29% of FP64 storage
+
+
+@pytest.mark.parametrize("eps,scheme", [(1e-12, 3), (1e-9, 2), (1e-14, 0)])
+def test_wide_fields(gpu, oracle, eps, scheme):
+    """w > 32 / e = 11 layouts take the generic 64-bit decoder in both phases"""
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    f, x = build_small_flat(n=1024, eps=eps, scheme=scheme)
+    assert int(f.e.max()) == 11 or (f.e.astype(int) + f.m.astype(int) + 1).max() > 32
+    H = HMatrix(f.to_product())
+    y = np.zeros(1024)
+    H.matvec(1.0, x, 0.0, y)
+    assert rel(y, oracle.hmat_matvec(f, 1.0, x, 0.0, np.zeros(1024), threads=4)) <= TOL
+
+
+def test_rank_zero_and_zero_blocks(gpu, oracle):
+    """lowrank leaves of rank 0 and all-zero dense blocks contribute nothing"""
+    from dataclasses import replace
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    f, x = build_small_flat(n=768, eps=1e-6, scheme=0)
+    lr = np.nonzero((f.kind == 1) & (f.rank > 0))[0]
+    rank = f.rank.copy()
+    rank[lr[::3]] = 0  # drop every third lowrank leaf (its buffers stay unused)
+    f0 = replace(f, rank=rank)
+    H = HMatrix(f0.to_product())
+    y = np.zeros(768)
+    H.matvec(1.0, x, 0.0, y)
+    assert rel(y, oracle.hmat_matvec(f0, 1.0, x, 0.0, np.zeros(768), threads=4)) <= TOL
