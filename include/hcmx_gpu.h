@@ -113,6 +113,12 @@ int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff,
                             uint8_t* d_payload, uint64_t payload_capacity, hcmx_descriptor* h_desc,
                             uint64_t* h_poff, uint64_t* h_total, void* stream);
 
+/* Device time of the batched codec kernels (CUDA events around the fused compress
+ * and the unpack launches), accumulated since the last reset.  enable: 1 on, 0 off,
+ * < 0 query only (no reset).  Instrumentation for the benchmark, not a reference API. */
+int hcmx_gpu_codec_timing(int enable, double* ms_compress, uint64_t* n_compress, double* ms_decompress,
+                          uint64_t* n_decompress);
+
 /* Single-buffer, HOST-pointer forms of codec::compress / decompress_into
  * (codec.cpp:142-171): the reference-facing call.  Copies in, runs the device
  * kernels, copies out. */

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -658,6 +659,63 @@ struct Pinned {
 };
 Pinned g_pinned;
 
+// optional device timing of the batched codec kernels (CUDA events on the
+// launching stream), queried through hcmx_gpu_codec_timing
+struct CodecTiming {
+    std::mutex mu;
+    bool on = false;
+    double ms[2] = {0, 0};
+    uint64_t n[2] = {0, 0};
+    std::vector<std::array<cudaEvent_t, 2>> pend[2];
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t take() {
+        if (pool.empty()) {
+            cudaEvent_t e;
+            check_cuda(cudaEventCreate(&e), "event");
+            return e;
+        }
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    void drain() {
+        for (int k = 0; k < 2; ++k) {
+            for (auto& pr : pend[k]) {
+                float t = 0;
+                check_cuda(cudaEventSynchronize(pr[1]), "event");
+                check_cuda(cudaEventElapsedTime(&t, pr[0], pr[1]), "event");
+                ms[k] += t;
+                ++n[k];
+                pool.push_back(pr[0]);
+                pool.push_back(pr[1]);
+            }
+            pend[k].clear();
+        }
+    }
+};
+CodecTiming g_ct;
+
+// brackets a kernel launch with events when timing is on (kind 0 compress, 1 decompress)
+struct KernelTimer {
+    int kind;
+    cudaStream_t s;
+    cudaEvent_t e0 = nullptr;
+    KernelTimer(int k, cudaStream_t st) : kind(k), s(st) {
+        std::lock_guard<std::mutex> g(g_ct.mu);
+        if (!g_ct.on) return;
+        e0 = g_ct.take();
+        check_cuda(cudaEventRecord(e0, s), "event");
+    }
+    void stop() {
+        if (!e0) return;
+        std::lock_guard<std::mutex> g(g_ct.mu);
+        cudaEvent_t e1 = g_ct.take();
+        check_cuda(cudaEventRecord(e1, s), "event");
+        g_ct.pend[kind].push_back({e0, e1});
+        e0 = nullptr;
+    }
+};
+
 }  // namespace
 
 // layout arrays for h_count (caller holds g_layout.mu)
@@ -743,10 +801,12 @@ void launch_unpack_jobs(const uint8_t* payload, const uint64_t* poff, const uint
     const uint64_t nch = g_layout.nchunks;
     if (!nch) return;
     const int grid = (int)std::min<uint64_t>((nch + kUnpackWarps - 1) / kUnpackWarps, 148ull * 8);
+    KernelTimer kt(1, s);
     k_unpack_chunks<<<grid, kUnpackWarps * 32, 0, s>>>(payload, poff, g_layout.count.as<uint64_t>(), desc, voff,
                                                        g_layout.coff.as<uint64_t>(), g_layout.cbuf.as<uint32_t>(),
                                                        nch, out);
     check_cuda(cudaGetLastError(), "unpack launch");
+    kt.stop();
 }
 
 }  // namespace hcmx_gpu
@@ -834,14 +894,6 @@ int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff, cons
                             uint64_t nbuf, double eps, int scheme, uint8_t* d_payload,
                             uint64_t payload_capacity, hcmx_descriptor* h_desc, uint64_t* h_poff,
                             uint64_t* h_total, void* stream) {
-    static const bool trace = std::getenv("HCMX_TRACE") != nullptr;
-    auto T0 = std::chrono::steady_clock::now();
-    auto mark = [&](const char* what) {
-        if (!trace) return;
-        const auto t = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "%s %.1f us\n", what, std::chrono::duration<double, std::micro>(t - T0).count());
-        T0 = t;
-    };
     return guarded([&] {
         require_device();
         alignment_unit(scheme);
@@ -875,11 +927,9 @@ int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff, cons
         }
         *h_total = off;
         if (off > payload_capacity) throw invalid_argument("compress: payload capacity too small");
-        mark("pre");
         std::lock_guard<std::mutex> g(g_layout.mu);
         layout_arrays(h_count, nbuf, stream);
         const uint64_t* dp = layout_poff(h_poff, nbuf, stream);
-        mark("layout");
         // one device block for descriptors | flags, one pinned block for the read-back
         const size_t o_fl = round16(nbuf * sizeof(hcmx_descriptor)), o_end = o_fl + round16(nbuf * 4);
         DevBuf out(o_end);
@@ -887,18 +937,17 @@ int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff, cons
         cudaStream_t s = (cudaStream_t)stream;
         uint8_t* ob = out.as<uint8_t>();
         const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(nbuf, 148ull * 16));
+        KernelTimer kt(0, s);
         k_compress_cta<<<grid, kCtaWarps * 32, 0, s>>>(d_values, d_voff, g_layout.count.as<uint64_t>(), nbuf,
                                                        scheme, m_req, dp, d_payload,
                                                        reinterpret_cast<hcmx_descriptor*>(ob), dst.as<hcmx_stats>(),
                                                        reinterpret_cast<uint32_t*>(ob + o_fl));
         check_cuda(cudaGetLastError(), "compress launch");
-        mark("launch");
+        kt.stop();
         std::lock_guard<std::mutex> gp(g_pinned.mu);
         uint8_t* hb = static_cast<uint8_t*>(g_pinned.get(o_end));
         d2h(hb, ob, o_fl + nbuf * 4, stream);
-        mark("d2h issue");
         stream_sync(stream);
-        mark("sync");
         std::memcpy(h_desc, hb, nbuf * sizeof(hcmx_descriptor));
         const uint32_t* flags = reinterpret_cast<const uint32_t*>(hb + o_fl);
         for (uint64_t b = 0; b < nbuf; ++b)
@@ -920,6 +969,23 @@ int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff, cons
                    dp1 = upload_u64(h_poff + b, 1, stream);
             launch_pack_jobs(d_values, dv1.as<uint64_t>(), dc1.as<uint64_t>(), h_count + b,
                              d1.as<hcmx_descriptor>(), dp1.as<uint64_t>(), 1, d_payload, stream);
+        }
+    });
+}
+
+int hcmx_gpu_codec_timing(int enable, double* ms_compress, uint64_t* n_compress, double* ms_decompress,
+                          uint64_t* n_decompress) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(g_ct.mu);
+        g_ct.drain();
+        if (ms_compress) *ms_compress = g_ct.ms[0];
+        if (n_compress) *n_compress = g_ct.n[0];
+        if (ms_decompress) *ms_decompress = g_ct.ms[1];
+        if (n_decompress) *n_decompress = g_ct.n[1];
+        if (enable >= 0) {  // enable < 0: query only
+            g_ct.on = enable != 0;
+            g_ct.ms[0] = g_ct.ms[1] = 0;
+            g_ct.n[0] = g_ct.n[1] = 0;
         }
     });
 }
