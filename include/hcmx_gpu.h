@@ -38,8 +38,14 @@ enum hcmx_status {
     HCMX_OUT_OF_MEMORY = 5
 };
 
-/* codec::Scheme (codec.hpp:22) */
-enum hcmx_scheme { HCMX_AFL = 0, HCMX_AFLP = 1, HCMX_BFL = 2, HCMX_DFL = 3 };
+/* codec::Scheme (codec.hpp:22).  The matvec also accepts buffers of uncompressed
+ * IEEE words (StorageMode fp64, hmatrix.hpp:32-40, and the FP64/FP32/FP16 groups
+ * of mp::MPLowrank, mixedprec.hpp:20-43): bit_width 64/32/16, scale 1.  The codec
+ * entry points reject these. */
+enum hcmx_scheme {
+    HCMX_AFL = 0, HCMX_AFLP = 1, HCMX_BFL = 2, HCMX_DFL = 3,
+    HCMX_RAW_F64 = 4, HCMX_RAW_F32 = 5, HCMX_RAW_F16 = 6
+};
 
 /* codec::FormatDescriptor (codec.hpp:35-56), 16 bytes */
 typedef struct hcmx_descriptor {
@@ -157,7 +163,12 @@ int hcmx_gpu_aplr_compress(uint64_t nleaves, const uint64_t* h_rows, const uint6
  * (clustering.cpp:159-166, children row-major 2i+j), internal index space.
  *   kind 0 CodecDense  (hmatrix.hpp:42-44): buffer buf0, column-major scan
  *   kind 1 APLRLowrank (mixedprec.hpp:68-82): buffers buf0..buf0+k-1 = W columns,
- *          buf0+k..buf0+2k-1 = X columns, sigma[sig0 .. sig0+k)
+ *          buf0+k..buf0+2k-1 = X columns, sigma[sig0 .. sig0+k).  With raw FP64 /
+ *          FP32 / FP16 column buffers the same kind holds mp::MPLowrank
+ *          (mixedprec.hpp:46-64: W Sigma X^H, columns grouped by format).
+ *   kind 2 CodecLowrank (hmatrix.hpp:46-49) / LowrankBlock (lowrank.hpp:17-29):
+ *          buffer buf0 = U (rows x k, column-major), buf0+1 = V (cols x k),
+ *          y += U (V^T x); codec-compressed or raw FP64 words
  * Buffers: descriptor, value count, payload at blob[poff .. poff+plen). */
 typedef struct hcmx_hmat_desc {
     uint64_t n_rows, n_cols, nleaves, nbuffers, nsigma, blob_bytes;

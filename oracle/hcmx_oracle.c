@@ -363,14 +363,97 @@ int orc_aplr_compress(const double* W, int64_t rows, const double* X, int64_t co
     return ORC_OK;
 }
 
+/* ------------------------------------------ uncompressed storage ------- */
+/* half.hpp:14-45 float_to_half: round to nearest even, denormals kept,
+ * overflow -> inf; double_to_half = float_to_half((float)v) (half.hpp:75) */
+uint16_t orc_float_to_half(float value) {
+    uint32_t bits;
+    memcpy(&bits, &value, 4);
+    const uint32_t sign = (bits >> 16) & 0x8000u;
+    const int32_t exp = (int32_t)((bits >> 23) & 0xffu) - 127 + 15;
+    uint32_t mant = bits & 0x7fffffu;
+    if (exp >= 31) return (uint16_t)(sign | 0x7c00u);
+    if (exp <= 0) {
+        if (exp < -10) return (uint16_t)sign;
+        mant |= 0x800000u;
+        const unsigned shift = (unsigned)(14 - exp);
+        const uint32_t lsb = 1u << shift, rest = mant & (lsb - 1);
+        uint32_t hm = mant >> shift;
+        if (rest > (lsb >> 1) || (rest == (lsb >> 1) && (hm & 1u))) ++hm;
+        return (uint16_t)(sign | hm);
+    }
+    uint32_t hm = mant >> 13;
+    const uint32_t rest = mant & 0x1fffu;
+    if (rest > 0x1000u || (rest == 0x1000u && (hm & 1u))) ++hm;
+    return (uint16_t)(sign | (((uint32_t)exp << 10) + hm));
+}
+
+/* half.hpp:47-72 half_to_float */
+float orc_half_to_float(uint16_t h) {
+    const uint32_t sign = (uint32_t)(h & 0x8000u) << 16, exp = (h >> 10) & 0x1fu, mant = h & 0x3ffu;
+    uint32_t bits;
+    if (exp == 0) {
+        if (mant == 0) {
+            bits = sign;
+        } else {
+            int e = -1;
+            uint32_t mm = mant;
+            while (!(mm & 0x400u)) { mm <<= 1; ++e; }
+            bits = sign | ((127u - 15u - (uint32_t)e) << 23) | ((mm & 0x3ffu) << 13);
+        }
+    } else if (exp == 31) {
+        bits = sign | 0x7f800000u | (mant << 13);
+    } else {
+        bits = sign | ((exp - 15u + 127u) << 23) | (mant << 13);
+    }
+    float f;
+    memcpy(&f, &bits, 4);
+    return f;
+}
+
+/* mixedprec.cpp:16-41 PackedSlice::pack for n values (format 4 fp64, 5 fp32,
+ * 6 fp16 in the hcmx_gpu raw-scheme numbering) */
+void orc_pack_raw(const double* v, int64_t n, int fmt, uint8_t* out) {
+    for (int64_t i = 0; i < n; ++i) {
+        if (fmt == 4) {
+            memcpy(out + 8 * i, &v[i], 8);
+        } else if (fmt == 5) {
+            const float f = (float)v[i];
+            memcpy(out + 4 * i, &f, 4);
+        } else {
+            const uint16_t hv = orc_float_to_half((float)v[i]);
+            memcpy(out + 2 * i, &hv, 2);
+        }
+    }
+}
+
+/* mixedprec.cpp:66-82 mp_partition: ranks of the FP64 / FP32 / FP16 groups */
+void orc_mp_partition(const double* sigma, int64_t k, double delta, int64_t* ranks) {
+    static const double rho[3] = {1.1e-16, 6.0e-8, 4.9e-4}; /* mixedprec.hpp:23 */
+    ranks[0] = ranks[1] = ranks[2] = 0;
+    for (int64_t j = 0; j < k; ++j) {
+        const double s = sigma[j];
+        if (s <= delta) continue;
+        int group = 0;
+        for (int i = 2; i >= 1; --i)
+            if (s * rho[i] <= delta) { group = i; break; }
+        ++ranks[group];
+    }
+}
+
 /* ----------------------------------------------------------- matvec ----- */
 /* Flattened H-matrix (the declared-only hmatrix.hpp:51-78 payload tree, leaves in
  * for_each_leaf preorder, clustering.cpp:159-166, children row-major 2i+j):
- *   leaf l: rows [row0,row1), cols [col0,col1), kind 0 = CodecDense (one buffer,
- *   column-major scan, hmatrix.hpp:42-44), kind 1 = APLRLowrank (2k buffers:
- *   W columns then X columns, sigma[sig0 .. sig0+k), mixedprec.hpp:68-82),
- *   kind 2 = raw FP64 dense (values in `raw` at buf0 as a double offset).
- *   buffer b: scheme/e/m/scale/count, payload at blob[poff[b] .. poff[b]+plen[b]).
+ *   leaf l: rows [row0,row1), cols [col0,col1), kind 0 = dense (one buffer,
+ *   column-major scan: CodecDense hmatrix.hpp:42-44, or raw FP64), kind 1 = W
+ *   Sigma X^H with one buffer per column (2k buffers: W columns then X columns,
+ *   sigma[sig0 .. sig0+k): APLRLowrank mixedprec.hpp:68-82, or the MP groups of
+ *   mixedprec.hpp:46-64 as raw FP64/FP32/FP16 columns), kind 2 = U V^T with one
+ *   U and one V buffer (CodecLowrank hmatrix.hpp:46-49, LowrankBlock
+ *   lowrank.hpp:17-29).
+ *   buffer b: scheme/e/m/scale/count, payload at blob[poff[b] .. poff[b]+plen[b]);
+ *   schemes 4/5/6 = uncompressed FP64/FP32/FP16 words (PackedSlice::unpack,
+ *   mixedprec.cpp:43-62).
  * matvec follows hmatrix.hpp:126-128 + SPEC.md:458-466: y := alpha*M*x + beta*y
  * (beta == 0 overwrites y), alpha == 0 leaves M untouched. */
 typedef struct {
@@ -393,8 +476,28 @@ typedef struct {
 } mv_job;
 
 static int decode_buf(const orc_hmat* h, int64_t b, double* out) {
-    return orc_decompress(h->scheme[b], h->e[b], h->m[b], h->scale[b], h->count[b],
-                          h->blob + h->poff[b], h->plen[b], out);
+    const int sc = h->scheme[b];
+    if (sc >= 4) { /* uncompressed words */
+        const uint8_t* p = h->blob + h->poff[b];
+        const int64_t n = h->count[b], esz = sc == 4 ? 8 : sc == 5 ? 4 : 2;
+        if (sc > 6 || n * esz > h->plen[b]) return ORC_CORRUPT_BUFFER;
+        for (int64_t i = 0; i < n; ++i) {
+            if (sc == 4) {
+                memcpy(&out[i], p + 8 * i, 8);
+            } else if (sc == 5) {
+                float f;
+                memcpy(&f, p + 4 * i, 4);
+                out[i] = (double)f;
+            } else {
+                uint16_t hv;
+                memcpy(&hv, p + 2 * i, 2);
+                out[i] = (double)orc_half_to_float(hv);
+            }
+        }
+        return ORC_OK;
+    }
+    return orc_decompress(sc, h->e[b], h->m[b], h->scale[b], h->count[b], h->blob + h->poff[b], h->plen[b],
+                          out);
 }
 
 static void* mv_worker(void* arg) {
@@ -403,22 +506,17 @@ static void* mv_worker(void* arg) {
     int64_t maxe = 0;
     for (int64_t l = j->l0; l < j->l1; ++l) {
         int64_t r = h->row1[l] - h->row0[l], c = h->col1[l] - h->col0[l];
-        int64_t need = h->kind[l] == 1 ? (r + c) * h->rank[l] + h->rank[l] : r * c;
+        int64_t need = h->kind[l] != 0 ? (r + c) * h->rank[l] + h->rank[l] : r * c;
         if (need > maxe) maxe = need;
     }
     double* tmp = (double*)malloc(sizeof(double) * (size_t)(maxe + 1));
     for (int64_t l = j->l0; l < j->l1 && j->status == 0; ++l) {
         const int64_t r0 = h->row0[l], c0 = h->col0[l];
         const int64_t rows = h->row1[l] - r0, cols = h->col1[l] - c0;
-        if (h->kind[l] == 0 || h->kind[l] == 2) {
-            const double* A;
-            if (h->kind[l] == 0) {
-                if (h->count[h->buf0[l]] != rows * cols) { j->status = ORC_INVALID_ARGUMENT; break; }
-                j->status = decode_buf(h, h->buf0[l], tmp);
-                A = tmp;
-            } else {
-                A = h->raw + h->buf0[l];
-            }
+        if (h->kind[l] == 0) {
+            if (h->count[h->buf0[l]] != rows * cols) { j->status = ORC_INVALID_ARGUMENT; break; }
+            j->status = decode_buf(h, h->buf0[l], tmp);
+            const double* A = tmp;
             for (int64_t cc = 0; cc < cols; ++cc) {
                 const double xv = j->x[c0 + cc];
                 const double* a = A + cc * rows;
@@ -429,16 +527,24 @@ static void* mv_worker(void* arg) {
             double* Wd = tmp;
             double* Xd = tmp + rows * k;
             double* t = Xd + cols * k;
-            for (int64_t i = 0; i < k && j->status == 0; ++i) {
-                j->status |= decode_buf(h, h->buf0[l] + i, Wd + i * rows);
-                j->status |= decode_buf(h, h->buf0[l] + k + i, Xd + i * cols);
+            if (h->kind[l] == 2) { /* one U and one V buffer, column-major */
+                if (k > 0) {
+                    j->status |= decode_buf(h, h->buf0[l], Wd);
+                    j->status |= decode_buf(h, h->buf0[l] + 1, Xd);
+                }
+            } else {
+                for (int64_t i = 0; i < k && j->status == 0; ++i) {
+                    j->status |= decode_buf(h, h->buf0[l] + i, Wd + i * rows);
+                    j->status |= decode_buf(h, h->buf0[l] + k + i, Xd + i * cols);
+                }
             }
-            /* mixedprec.cpp:203-208: U = W diag(sigma), V = X; y_t += U (V^T x_s) */
+            /* mixedprec.cpp:203-208: U = W diag(sigma), V = X; y_t += U (V^T x_s)
+             * (sigma = 1 for U V^T leaves) */
             for (int64_t i = 0; i < k; ++i) {
                 double s = 0.0;
                 const double* xc = Xd + i * cols;
                 for (int64_t cc = 0; cc < cols; ++cc) s += xc[cc] * j->x[c0 + cc];
-                t[i] = s * h->sigma[h->sig0[l] + i];
+                t[i] = h->kind[l] == 2 ? s : s * h->sigma[h->sig0[l] + i];
             }
             for (int64_t i = 0; i < k; ++i) {
                 const double* wc = Wd + i * rows;
@@ -461,7 +567,7 @@ int orc_hmat_matvec(const orc_hmat* h, double alpha, const double* x, double bet
     double total = 0.0;
     for (int64_t l = 0; l < h->nleaves; ++l) {
         double r = (double)(h->row1[l] - h->row0[l]), c = (double)(h->col1[l] - h->col0[l]);
-        work[l] = h->kind[l] == 1 ? (r + c) * (double)h->rank[l] : r * c;
+        work[l] = h->kind[l] != 0 ? (r + c) * (double)h->rank[l] : r * c;
         total += work[l];
     }
     mv_job* jobs = (mv_job*)calloc((size_t)threads, sizeof(mv_job));

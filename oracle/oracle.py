@@ -139,6 +139,32 @@ class Oracle(_Base):
                               _pi32, _pi32, _pd, _pd, _i32)
         self._lus = self._fn("log_uniform_signed", None, _u64, _i64, _d, _d, _pd)
         self._c2 = self._fn("config2_values", None, _u64, _i64, _pd)
+        self._f2h = self._fn("float_to_half", C.c_uint16, C.c_float)
+        self._h2f = self._fn("half_to_float", C.c_float, C.c_uint16)
+        self._praw = self._fn("pack_raw", None, _pd, _i64, _i32, _pu8)
+        self._mpp = self._fn("mp_partition", None, _pd, _i64, _d, _pi64)
+
+    def float_to_half(self, f: float) -> int:
+        """half.hpp:14-45"""
+        return int(self._f2h(f))
+
+    def half_to_float(self, h: int) -> float:
+        """half.hpp:47-72"""
+        return float(self._h2f(h))
+
+    def pack_raw(self, v, fmt: int) -> bytes:
+        """PackedSlice::pack (mixedprec.cpp:16-41); fmt 4 fp64, 5 fp32, 6 fp16"""
+        v = np.ascontiguousarray(v, np.float64)
+        out = np.zeros(v.size * {4: 8, 5: 4, 6: 2}[fmt] + 1, np.uint8)
+        self._praw(_p(v, _d), v.size, fmt, _p(out, _u8))
+        return out[:-1].tobytes()
+
+    def mp_partition(self, sigma, delta: float):
+        """mixedprec.cpp:66-82: ranks of the FP64 / FP32 / FP16 groups"""
+        sigma = np.ascontiguousarray(sigma, np.float64)
+        out = np.zeros(3, np.int64)
+        self._mpp(_p(sigma, _d), sigma.size, float(delta), _p(out, _i64))
+        return out
 
     def log_uniform_signed(self, seed, n, lo, hi):
         out = np.empty(n)
@@ -221,8 +247,16 @@ class RefOracle(_Base):
     def available(path: str | None = None) -> bool:
         return os.path.exists(path or RefOracle.libpath)
 
+    def float_to_half(self, f: float) -> int:
+        return int(self._f2h(f))
+
+    def half_to_float(self, h: int) -> float:
+        return float(self._h2f(h))
+
     def _bind(self):
         super()._bind()
+        self._f2h = self._fn("float_to_half", C.c_uint16, C.c_float)
+        self._h2f = self._fn("half_to_float", C.c_float, C.c_uint16)
         self._mkd = self._fn("make_descriptor", _i32, _i32, _d, _d, _i32, _pi32, _pi32)
         self._mkds = self._fn("make_descriptor_stats", _i32, _i32, _d, _d, _d, _i32, _pi32,
                               _pi32, _pd)

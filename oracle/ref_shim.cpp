@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "hcmx/codec.hpp"
+#include "hcmx/half.hpp"
 
 using namespace hcmx;
 using codec::Scheme;
@@ -81,6 +82,10 @@ int fan_out(std::int64_t n, int threads, F&& body) {
 } // namespace
 
 extern "C" {
+
+// half.hpp conversions, header-only reference code (pins the restatement)
+std::uint16_t ref_float_to_half(float v) { return hcmx::mp::float_to_half(v); }
+float ref_half_to_float(std::uint16_t h) { return hcmx::mp::half_to_float(h); }
 
 void ref_mt64_raw(std::uint64_t seed, std::int64_t n, std::uint64_t* out) {
     std::mt19937_64 g(seed);

@@ -34,6 +34,7 @@
 // multiply by the buffer scale is folded into the coefficients (dense: alpha *
 // scale * x_j, lowrank: alpha * sigma_i * scale_X_i * scale_W_i * t_i), so the
 // sum differs from the oracle only by FP64 reassociation (||dy||/||y|| ~ 1e-15).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -264,6 +265,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 //   mode 0: w == 1 + e + m <= 32, m <= 20, e < 11 (the double lives in the high word)
 //   mode 1: w == 1 + e + m <= 32, m  > 20, e < 11
 //   mode 2: anything else (64-bit window, min(offset + 1023, 2046) clamp)
+//   modes 3, 4, 5 (decoded by the mode-2 body): uncompressed FP64 / FP32 / FP16
+//   storage (StorageMode fp64 and the MP-D-S-H groups, mixedprec.hpp:20-43): the
+//   value itself (scale 1)
 // Every column of an item shares one mode, so the mode is dispatched per item.
 template <int MODE>
 __device__ __forceinline__ double dec(const uint32_t* sp, const ColPar& c, unsigned sh) {
@@ -279,6 +283,16 @@ __device__ __forceinline__ double dec(const uint32_t* sp, const ColPar& c, unsig
         const double d = __hiloint2double(hi, lo) - 1.0;
         return __hiloint2double(__double2hiint(d) ^ ((t << c.sgn_sh) & 0x80000000u), __double2loint(d));
     } else {
+        const unsigned fmt = c.packed >> 24;
+        if (fmt >= 3) {  // uncompressed words (uniform per item, so the branch is too)
+            if (fmt == 3)  // FP64 (64-bit fields are word aligned: sh == 0)
+                return __hiloint2double(static_cast<int>(sp[1]), static_cast<int>(sp[0]));
+            if (fmt == 4)  // FP32 (word aligned)
+                return static_cast<double>(__int_as_float(static_cast<int>(sp[0])));
+            // binary16 (the half.hpp:47-72 widening is exact)
+            const uint32_t t = __funnelshift_r(sp[0], sp[1], sh) & 0xffffu;
+            return static_cast<double>(__half2float(__ushort_as_half(static_cast<unsigned short>(t))));
+        }
         const unsigned w = c.packed & 0xffu, m = (c.packed >> 8) & 0xffu, e = (c.packed >> 16) & 0xffu;
         uint64_t win = ((static_cast<uint64_t>(sp[1]) << 32) | sp[0]) >> sh;
         if (w > 32 && sh + w > 64) win |= static_cast<uint64_t>(sp[2]) << (64 - sh);
@@ -631,14 +645,16 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
     // mode 2 (e = 11 or w > 32) and ragged chunks take one generic body (the
     // mode-2 decoder is exact for every layout; keeps the kernel small)
     const unsigned ui = nf == 256 ? 3u : nf == 128 ? 2u : nf == 64 ? 1u : 0u;
-    switch (it.mode == 2 || ui == 0 ? 0u : ui + 3u * it.mode) {
+    switch (it.mode >= 2 || ui == 0 ? 0u : ui + 3u * it.mode) {
         case 3: a_cols<0, 8>(pk, nseg, nf, lane, xs, a); break;
         case 2: a_cols<0, 4>(pk, nseg, nf, lane, xs, a); break;
         case 1: a_cols<0, 2>(pk, nseg, nf, lane, xs, a); break;
         case 6: a_cols<1, 8>(pk, nseg, nf, lane, xs, a); break;
         case 5: a_cols<1, 4>(pk, nseg, nf, lane, xs, a); break;
         case 4: a_cols<1, 2>(pk, nseg, nf, lane, xs, a); break;
-        default: a_cols<2, 0>(pk, nseg, nf, lane, xs, a); break;
+        default:
+            a_cols<2, 0>(pk, nseg, nf, lane, xs, a);  // also uncompressed words (modes 3-5)
+            break;
     }
     const double r = reduce4(a, lane);
     if (!writer) return;
@@ -745,7 +761,7 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
     // everything else takes one generic body with the mode-2 decoder (exact for
     // every layout), which keeps the kernel inside the instruction cache
     static_assert(kG == 4, "fast-path table assumes 128-row blocks");
-    const unsigned fc = it.mode == 2 ? 0u : it.fcase;
+    const unsigned fc = it.mode >= 2 ? 0u : it.fcase;
     switch (fc | (it.mode << 8)) {
         case 0x004: b_item_full<0, 0, 4>(it, seg, cf, lane, dmul, acc); break;
         case 0x002: b_item_full<0, 0, 2>(it, seg, cf, lane, dmul, acc); break;
@@ -753,7 +769,9 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
         case 0x104: b_item_full<1, 0, 4>(it, seg, cf, lane, dmul, acc); break;
         case 0x102: b_item_full<1, 0, 2>(it, seg, cf, lane, dmul, acc); break;
         case 0x124: b_item_full<1, 2, 4>(it, seg, cf, lane, dmul, acc); break;
-        default: b_item_generic<2>(it, seg, cf, lane, dmul, acc); break;
+        default:
+            b_item_generic<2>(it, seg, cf, lane, dmul, acc);  // also uncompressed words (modes 3-5)
+            break;
     }
 }
 
@@ -923,7 +941,8 @@ void drain_timing(hcmx_hmat* h) {
 ColPar col_par(const hcmx_descriptor& x) {
     ColPar c{};
     const unsigned w = x.bit_width, m = x.mant_bits, e = x.exp_bits, em = e + m;
-    const unsigned mode = (w > 32 || e >= 11 || w != 1 + em) ? 2u : (m <= 20 ? 0u : 1u);
+    unsigned mode = (w > 32 || e >= 11 || w != 1 + em) ? 2u : (m <= 20 ? 0u : 1u);
+    if (x.scheme >= HCMX_RAW_F64) mode = 3u + (x.scheme - HCMX_RAW_F64);  // uncompressed storage
     c.mask_em = em >= 32 ? 0xffffffffu : ((1u << em) - 1u);
     c.mul_rsh = mode == 0 ? (1u << (20 - m)) : (mode == 1 ? m - 20 : 0u);
     c.packed = w | (m << 8) | (e << 16) | (mode << 24);
@@ -1207,15 +1226,29 @@ void validate(const hcmx_hmat_desc& d) {
                 if (d.count[d.buf0[l] + i] != rows || d.count[d.buf0[l] + k + i] != cols)
                     throw invalid_argument("hmat: lowrank factor size mismatch");
             }
+        } else if (d.kind[l] == 2) {
+            const int64_t k = d.rank[l];
+            if (k < 0) throw invalid_argument("hmat: lowrank leaf indices");
+            if (k > 0) {  // a rank-0 leaf has no buffers
+                if (d.buf0[l] < 0 || d.buf0[l] + 2 > (int64_t)d.nbuffers)
+                    throw invalid_argument("hmat: lowrank leaf indices");
+                if (d.count[d.buf0[l]] != rows * k || d.count[d.buf0[l] + 1] != cols * k)
+                    throw invalid_argument("hmat: lowrank factor size mismatch");
+            }
         } else {
-            throw invalid_argument("hmat: unsupported leaf kind (only CodecDense and APLRLowrank)");
+            throw invalid_argument("hmat: unsupported leaf kind (CodecDense, APLR / MP lowrank, CodecLowrank)");
         }
     }
     for (uint64_t b = 0; b < d.nbuffers; ++b) {
         const hcmx_descriptor& x = d.desc[b];
-        if (x.scheme > 3 || x.exp_bits < 2 || x.exp_bits > 11 || x.mant_bits < 2 || x.mant_bits > 52 ||
-            x.bit_width != bit_width(x.scheme, x.exp_bits, x.mant_bits))
+        if (x.scheme >= HCMX_RAW_F64) {  // uncompressed storage: 64 / 32 / 16-bit IEEE words
+            static const unsigned rw[3] = {64, 32, 16};
+            if (x.scheme > HCMX_RAW_F16 || x.bit_width != rw[x.scheme - HCMX_RAW_F64] || x.scale != 1.0)
+                throw invalid_argument("hmat: invalid raw-storage descriptor");
+        } else if (x.scheme > 3 || x.exp_bits < 2 || x.exp_bits > 11 || x.mant_bits < 2 || x.mant_bits > 52 ||
+                   x.bit_width != bit_width(x.scheme, x.exp_bits, x.mant_bits)) {
             throw invalid_argument("hmat: invalid buffer descriptor");
+        }
         if (d.poff[b] < 0 || d.plen[b] < 0 || (uint64_t)(d.poff[b] + d.plen[b]) > d.blob_bytes)
             throw corrupt_buffer("hmat: payload outside the blob");
         if ((uint64_t)d.plen[b] < payload_bytes(d.count[b], x.bit_width))
@@ -1252,6 +1285,18 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     B.keep_map = total_fields <= (1ull << 28);
     if (B.keep_map) h->segs.assign(d.nbuffers, {});
 
+    // (buffer, first field) of rank column i of a lowrank leaf: one buffer per
+    // column (APLR / MP, kind 1) or a slice of the U / V buffer (CodecLowrank, kind 2)
+    auto wbuf = [&](uint64_t l, uint32_t i) -> std::pair<uint64_t, uint64_t> {
+        if (d.kind[l] == 2) return {static_cast<uint64_t>(d.buf0[l]), static_cast<uint64_t>(i) * (d.row1[l] - d.row0[l])};
+        return {static_cast<uint64_t>(d.buf0[l] + i), 0};
+    };
+    auto xbuf = [&](uint64_t l, uint32_t i) -> std::pair<uint64_t, uint64_t> {
+        if (d.kind[l] == 2)
+            return {static_cast<uint64_t>(d.buf0[l] + 1), static_cast<uint64_t>(i) * (d.col1[l] - d.col0[l])};
+        return {static_cast<uint64_t>(d.buf0[l] + d.rank[l] + i), 0};
+    };
+
     // per-leaf tables
     std::vector<int64_t> lr_id(d.nleaves, -1);
     std::vector<LeafA> leafa;
@@ -1265,10 +1310,12 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         const int64_t rows = d.row1[l] - d.row0[l], cols = d.col1[l] - d.col0[l];
         if (d.kind[l] == 0) {
             const hcmx_descriptor& x = d.desc[d.buf0[l]];
+            const bool raw = x.scheme >= HCMX_RAW_F64;  // uncompressed FP64 leaf (StorageMode fp64 / MP)
             rep.dense_leaves++;
-            rep.dense_compressed += 20 + d.plen[d.buf0[l]];
+            if (raw) rep.dense_raw += d.plen[d.buf0[l]];
+            else rep.dense_compressed += 20 + d.plen[d.buf0[l]];
             rep.uncompressed_equivalent += 8ull * rows * cols;
-            rep.algorithmic_bytes += 20 + payload_bytes(rows * cols, x.bit_width);
+            rep.algorithmic_bytes += (raw ? 0 : 20) + payload_bytes(rows * cols, x.bit_width);
         } else {
             const uint32_t k = static_cast<uint32_t>(d.rank[l]);
             lr_id[l] = static_cast<int64_t>(leafa.size());
@@ -1288,17 +1335,30 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                 npartial += static_cast<uint64_t>(L.nchunks) * k;
             }
             leafa.push_back(L);
-            uint64_t bytes = 8 + 8ull * k;  // APLRLowrank::byte_size (mixedprec.cpp:210-217)
+            const bool uniform = d.kind[l] == 2;  // CodecLowrank: one U and one V buffer, sigma = 1
+            uint64_t bytes = uniform ? 4 : 8 + 8ull * k;  // APLRLowrank::byte_size (mixedprec.cpp:210-217)
+            if (uniform && k > 0) {
+                for (int f = 0; f < 2; ++f) {
+                    const hcmx_descriptor& x = d.desc[d.buf0[l] + f];
+                    const uint64_t n = f ? cols * k : rows * k;
+                    const uint64_t hdr = x.scheme >= HCMX_RAW_F64 ? 0 : 20;
+                    bytes += hdr + d.plen[d.buf0[l] + f];
+                    rep.algorithmic_bytes += hdr + payload_bytes(n, x.bit_width);
+                }
+            }
             for (uint32_t i = 0; i < k; ++i) {
-                const hcmx_descriptor& xw = d.desc[d.buf0[l] + i];
-                const hcmx_descriptor& xx = d.desc[d.buf0[l] + k + i];
+                const hcmx_descriptor& xw = d.desc[wbuf(l, i).first];
+                const hcmx_descriptor& xx = d.desc[xbuf(l, i).first];
                 const ColPar cp = col_par(xw);
                 wcol.push_back({0.0, cp.mask_em, cp.mul_rsh, cp.sgn_sh, cp.packed, xw.bit_width, 0u});
-                coef.push_back(d.sigma[d.sig0[l] + i] * xx.scale * xw.scale);
-                bytes += 40 + d.plen[d.buf0[l] + i] + d.plen[d.buf0[l] + k + i];
-                rep.algorithmic_bytes += 40 + payload_bytes(rows, xw.bit_width) + payload_bytes(cols, xx.bit_width);
+                coef.push_back((uniform ? 1.0 : d.sigma[d.sig0[l] + i]) * xx.scale * xw.scale);
+                if (!uniform) {
+                    const uint64_t hdr = xw.scheme >= HCMX_RAW_F64 ? 0 : 20;
+                    bytes += 2 * hdr + d.plen[d.buf0[l] + i] + d.plen[d.buf0[l] + k + i];
+                    rep.algorithmic_bytes += 2 * hdr + payload_bytes(rows, xw.bit_width) + payload_bytes(cols, xx.bit_width);
+                }
             }
-            rep.algorithmic_bytes += 8ull * k;
+            if (!uniform) rep.algorithmic_bytes += 8ull * k;
             rep.lowrank_leaves++;
             rep.lowrank_compressed += bytes;
             rep.uncompressed_equivalent += 8ull * (rows + cols) * k;
@@ -1327,21 +1387,22 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
             stripe_bytes = 0;
         };
         for (uint64_t l : leaves) {
-            if (d.kind[l] != 1) continue;
+            if (d.kind[l] == 0) continue;
             const LeafA& L = leafa[lr_id[l]];
             const int64_t cols = d.col1[l] - d.col0[l];
             for (uint32_t ch = 0; ch < L.nchunks; ++ch, ++unit) {
                 const uint64_t f0 = static_cast<uint64_t>(ch) * kAChunk;
                 const uint64_t nf = std::min<uint64_t>(kAChunk, cols - f0);
-                const auto groups = column_groups(L.k, 1, [&](uint32_t i) { return B.words_of(d.buf0[l] + L.k + i, nf); });
+                const auto groups = column_groups(L.k, 1, [&](uint32_t i) { return B.words_of(xbuf(l, i).first, nf); });
                 for (const auto& gr : groups) {
                     const uint32_t g = gr.first, ng = gr.second;
                     Spec<AItem> sp{};
                     sp.seg0 = static_cast<uint32_t>(B.segs.size());
                     sp.nseg = ng;
                     for (uint32_t i = g; i < g + ng; ++i) {
-                        B.segs.push_back({static_cast<uint64_t>(d.buf0[l] + L.k + i), f0, nf});
-                        sp.words += B.words_of(d.buf0[l] + L.k + i, nf);
+                        const auto xb = xbuf(l, i);
+                        B.segs.push_back({xb.first, xb.second + f0, nf});
+                        sp.words += B.words_of(xb.first, nf);
                     }
                     AItem& it = sp.it;
                     it.nseg = static_cast<uint8_t>(ng);
@@ -1355,14 +1416,14 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                     it.nchunks = static_cast<uint16_t>(L.nchunks);
                     it.pbase = L.pbase;
                     sp.words += ng;  // packed column layout word
-                    sp.param = col_par(d.desc[d.buf0[l] + L.k + g]).packed;
+                    sp.param = col_par(d.desc[xbuf(l, g).first]).packed;
                     it.mode = static_cast<uint8_t>(sp.param >> 24);
                     sp.elem = xidx;
                     sp.sl_table = 0;  // x slice of the chunk
                     sp.sl_start = xidx;
                     sp.sl_count = static_cast<uint32_t>(nf);
                     sp.cost = nf * ng;
-                    sp.unit = unit * 4 + it.mode;  // items never mix decode modes
+                    sp.unit = unit * 8 + it.mode;  // items never mix decode modes
                     sp.xidx = xidx;
                     sp.nf = static_cast<uint32_t>(nf);
                     stripe_bytes += sp.words * 4;
@@ -1425,20 +1486,21 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                         sp.sl_start = static_cast<uint32_t>(d.col0[l]);
                         sp.sl_count = static_cast<uint32_t>(cols);
                         sp.cost = 3 * nr + 128;  // ~decode instructions (x8) of one column segment
-                        sp.unit = unit * 4 + it.mode;
+                        sp.unit = unit * 8 + it.mode;
                         specs.push_back(sp);
                     }
                 } else {
                     const LeafA& L = leafa[lr_id[l]];
-                    const auto groups = column_groups(L.k, 1, [&](uint32_t i) { return B.words_of(d.buf0[l] + i, nr); });
+                    const auto groups = column_groups(L.k, 1, [&](uint32_t i) { return B.words_of(wbuf(l, i).first, nr); });
                     for (const auto& gr : groups) {
                         const uint32_t g = gr.first, ng = gr.second;
                         Spec<BItem> sp{};
                         sp.seg0 = static_cast<uint32_t>(B.segs.size());
                         sp.nseg = ng;
                         for (uint32_t i = g; i < g + ng; ++i) {
-                            B.segs.push_back({static_cast<uint64_t>(d.buf0[l] + i), roff, nr});
-                            sp.words += B.words_of(d.buf0[l] + i, nr);
+                            const auto wb2 = wbuf(l, i);
+                            B.segs.push_back({wb2.first, wb2.second + roff, nr});
+                            sp.words += B.words_of(wb2.first, nr);
                         }
                         BItem& it = sp.it;
                         it.nseg = static_cast<uint8_t>(ng);
@@ -1446,14 +1508,14 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                         it.ra = static_cast<uint8_t>(r0 - b0);
                         it.nr = static_cast<uint8_t>(nr);
                         it.src = L.colbase + g;
-                        it.mode = static_cast<uint8_t>(col_par(d.desc[d.buf0[l] + g]).packed >> 24);
+                        it.mode = static_cast<uint8_t>(col_par(d.desc[wbuf(l, g).first]).packed >> 24);
                         it.fcase = fcase_of(r0 - b0, nr);
                         sp.elem = it.src;
                         sp.sl_table = 1;  // phase-A results of the leaf
                         sp.sl_start = L.colbase;
                         sp.sl_count = L.k;
                         sp.cost = 3 * nr + 128;
-                        sp.unit = unit * 4 + it.mode;  // items never mix decode modes
+                        sp.unit = unit * 8 + it.mode;  // items never mix decode modes
                         specs.push_back(sp);
                     }
                 }

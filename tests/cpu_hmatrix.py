@@ -60,9 +60,12 @@ class Flat:
         from paper_2308_10960_b200.hmatrix import FlatHMatrix
         desc = np.zeros(self.count.size, DESC_DTYPE)
         desc["scheme"], desc["exp_bits"], desc["mant_bits"] = self.scheme, self.e, self.m
-        unit = np.array([1, 8, 8, 16])[self.scheme.astype(np.int64)]
+        sc = self.scheme.astype(np.int64)
+        unit = np.array([1, 8, 8, 16, 1, 1, 1])[sc]
         w = 1 + self.e.astype(np.int64) + self.m.astype(np.int64)
-        desc["bit_width"] = w + (unit - w % unit) % unit
+        w = w + (unit - w % unit) % unit
+        w = np.where(sc >= 4, np.array([0, 0, 0, 0, 64, 32, 16])[sc], w)  # raw FP64 / FP32 / FP16
+        desc["bit_width"] = w
         desc["scale"] = self.scale
         return FlatHMatrix(self.n_rows, self.n_cols, self.row0, self.row1, self.col0, self.col1,
                            self.kind, self.rank, self.buf0, self.sig0, self.sigma, desc, self.count,
@@ -90,14 +93,22 @@ class Flat:
 
 
 def build_small_flat(n=1024, eps=1e-6, scheme=0, use_ref=False, geometry="fibonacci",
-                     kernel="laplace", seed=1, leaf=64, eta=2.0):
-    """points -> trees -> FP64 assembly (torch CPU) -> CPU codec -> Flat, x"""
+                     kernel="laplace", seed=1, leaf=64, eta=2.0, mode="aplr", dense_too=True,
+                     return_assembled=False):
+    """points -> trees -> FP64 assembly (torch CPU) -> CPU codec -> Flat, x.
+    mode (StorageMode kind, hmatrix.hpp:32-40): 'aplr' (default), 'codec'
+    (CodecDense + CodecLowrank of U = W diag(sigma), V = X), 'mp' (FP64 dense +
+    MP-D-S-H column groups), 'fp64' (uncompressed)"""
     from paper_2308_10960_b200 import assemble, problems, tree
     o = RefOracle() if use_ref else Oracle()
     pts = problems.make_points(geometry, n, seed)
     ct = tree.build_cluster_tree(pts, leaf)
     lv = tree.build_block_tree(ct, ct, eta)
     A = assemble.assemble(pts[ct.i2e], lv, problems.make_kernel(kernel), eps, device="cpu")
+    if mode != "aplr":
+        flat = _build_mode_flat(o, A, lv, n, eps, scheme, mode, dense_too)
+        x = np.random.default_rng(seed + 100).uniform(-1.0, 1.0, n)
+        return (flat, x, A) if return_assembled else (flat, x)
     dense = A.dense.numpy()
     W, X = A.W.numpy(), A.X.numpy()
     L = len(lv)
@@ -133,4 +144,68 @@ def build_small_flat(n=1024, eps=1e-6, scheme=0, use_ref=False, geometry="fibona
                 np.array(poff, np.int64), np.array([len(b.payload) for b in bufs], np.int64),
                 np.concatenate(parts) if parts else np.zeros(16, np.uint8))
     x = np.random.default_rng(seed + 100).uniform(-1.0, 1.0, n)
-    return flat, x
+    return (flat, x, A) if return_assembled else (flat, x)
+
+
+def _raw_buf(o, v, fmt):
+    from oracle import Buf
+    return Buf(fmt, 0, 0, 1.0, int(np.asarray(v).size), o.pack_raw(v, fmt))
+
+
+def _build_mode_flat(o, A, lv, n, eps, scheme, mode, dense_too):
+    """CPU construction of the other StorageModes with the checkers' codec and
+    the restated PackedSlice / mp_partition (oracle/hcmx_oracle.c)"""
+    dense = A.dense.numpy()
+    W, X = A.W.numpy(), A.X.numpy()
+    L = len(lv)
+    rows = (lv.row1 - lv.row0).astype(np.int64)
+    cols = (lv.col1 - lv.col0).astype(np.int64)
+    kind = A.kind.astype(np.int64).copy()
+    rank = A.rank.astype(np.int64).copy()
+    bufs, buf0 = [], np.zeros(L, np.int64)
+    for l in range(L):
+        buf0[l] = len(bufs)
+        if A.kind[l] == 0:
+            v = dense[A.dense_off[l]: A.dense_off[l] + rows[l] * cols[l]]
+            if mode == "codec" and dense_too:
+                bufs.append(o.compress(v, eps, scheme))
+            else:
+                bufs.append(_raw_buf(o, v, 4))
+            continue
+        k = int(A.rank[l])
+        if mode in ("codec", "fp64"):
+            kind[l] = 2
+        if k == 0:
+            continue
+        Wl = W[A.w_off[l]: A.w_off[l] + rows[l] * k]            # column-major rows x k
+        Xl = X[A.x_off[l]: A.x_off[l] + cols[l] * k]
+        s = A.sigma[A.sig_off[l]: A.sig_off[l] + k]
+        if mode in ("codec", "fp64"):
+            U = (Wl.reshape(k, rows[l]) * s[:, None]).reshape(-1)  # W diag(sigma), one product each
+            if mode == "codec":
+                bufs += [o.compress(U, eps, scheme), o.compress(Xl, eps, scheme)]
+            else:
+                bufs += [_raw_buf(o, U, 4), _raw_buf(o, Xl, 4)]
+        else:  # mp
+            r = o.mp_partition(s, eps * s[0])
+            assert r.sum() == k
+            fmt = np.repeat([4, 5, 6], r)
+            for i in range(k):
+                bufs.append(_raw_buf(o, Wl[i * rows[l]:(i + 1) * rows[l]], int(fmt[i])))
+            for i in range(k):
+                bufs.append(_raw_buf(o, Xl[i * cols[l]:(i + 1) * cols[l]], int(fmt[i])))
+    poff, off, parts = [], 0, []
+    for b in bufs:
+        poff.append(off)
+        pad = (-len(b.payload)) % 16
+        parts.append(np.frombuffer(b.payload + b"\0" * pad, np.uint8))
+        off += len(b.payload) + pad
+    sig0 = A.sig_off.copy()
+    sig0[sig0 < 0] = 0
+    return Flat(n, n, lv.row0.astype(np.int64), lv.row1.astype(np.int64), lv.col0.astype(np.int64),
+                lv.col1.astype(np.int64), kind, rank, buf0, sig0, A.sigma.astype(np.float64),
+                np.array([b.scheme for b in bufs], np.uint8), np.array([b.e for b in bufs], np.uint8),
+                np.array([b.m for b in bufs], np.uint8), np.array([b.scale for b in bufs]),
+                np.array([b.count for b in bufs], np.int64), np.array(poff, np.int64),
+                np.array([len(b.payload) for b in bufs], np.int64),
+                np.concatenate(parts) if parts else np.zeros(16, np.uint8))

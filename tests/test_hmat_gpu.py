@@ -179,3 +179,35 @@ def test_rank_zero_and_zero_blocks(gpu, oracle):
     y = np.zeros(768)
     H.matvec(1.0, x, 0.0, y)
     assert rel(y, oracle.hmat_matvec(f0, 1.0, x, 0.0, np.zeros(768), threads=4)) <= TOL
+
+
+@pytest.mark.parametrize("mode,scheme,dense_too", [
+    ("codec", 0, True),    # CodecDense + CodecLowrank (AFL)
+    ("codec", 2, False),   # BFL lowrank factors, FP64 dense leaves
+    ("mp", 0, True),       # FP64 dense + MP-D-S-H lowrank groups
+    ("fp64", 0, True),     # uncompressed
+])
+def test_storage_modes(gpu, oracle, mode, scheme, dense_too):
+    """every StorageMode kind (hmatrix.hpp:32-40) through the fused matvec, and the
+    device compress_in_place producing the same buffers as the CPU construction"""
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200.hmatrix import HMatrix, compress_in_place
+    eps = 1e-6
+    f, x, A = build_small_flat(n=1024, eps=eps, scheme=scheme, mode=mode, dense_too=dense_too,
+                               return_assembled=True)
+    H = HMatrix(f.to_product())
+    y0 = np.random.default_rng(3).standard_normal(1024)
+    for alpha, beta in ((1.0, 0.0), (0.7, -1.5)):
+        y = y0.copy()
+        H.matvec(alpha, x, beta, y)
+        assert rel(y, oracle.hmat_matvec(f, alpha, x, beta, y0, threads=4)) <= TOL, (alpha, beta)
+    name = {"codec": ["afl", "aflp", "bfl", "dfl"][scheme]}.get(mode, mode)
+    g = compress_in_place(A, eps, name, dense_too=dense_too).host()
+    assert (g.kind == f.kind).all() and (g.count == f.count).all()
+    assert (g.desc["scheme"] == f.scheme).all()
+    for b in range(f.count.size):
+        assert g.blob[g.poff[b]: g.poff[b] + g.plen[b]].tobytes() == \
+            f.blob[f.poff[b]: f.poff[b] + f.plen[b]].tobytes(), b
+    y = np.zeros(1024)
+    HMatrix(g).matvec(1.0, x, 0.0, y)
+    assert rel(y, oracle.hmat_matvec(f, 1.0, x, 0.0, np.zeros(1024), threads=4)) <= TOL

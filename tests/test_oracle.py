@@ -108,3 +108,36 @@ def test_oracle_matvec_vs_reference_glue(oracle, ref):
         a = oracle.hmat_matvec(f, alpha, x, beta, y0, threads=2)
         b = ref.hmat_matvec(f, alpha, x, beta, y0, threads=1)
         assert np.linalg.norm(a - b) <= 1e-13 * max(np.linalg.norm(b), 1e-300)
+
+
+def test_half_conversions_match_reference(oracle, ref):
+    """half.hpp float_to_half / half_to_float restated bit for bit (MP storage):
+    every binary16 pattern, and floats around every rounding boundary"""
+    import struct
+    for h in range(0, 1 << 16, 7):
+        a, b = oracle.half_to_float(h), ref.half_to_float(h)
+        assert struct.pack("<f", a) == struct.pack("<f", b), h
+    rng = np.random.default_rng(4)
+    bits = np.concatenate([rng.integers(0, 1 << 32, 20000, dtype=np.uint64),
+                           np.arange(0x33000000, 0x33800000, 997, dtype=np.uint64),   # denormal range
+                           np.arange(0x477fe000, 0x47800100, 1, dtype=np.uint64)])   # overflow boundary
+    for u in bits:
+        f = struct.unpack("<f", struct.pack("<I", int(u)))[0]
+        if f != f:  # NaN: both map it to inf; skip payload details
+            continue
+        assert oracle.float_to_half(f) == ref.float_to_half(f), hex(int(u))
+
+
+def test_mp_partition_rule(oracle):
+    """mixedprec.cpp:66-82 with the D-S-H roundoffs (mixedprec.hpp:23)"""
+    delta = 1e-6
+    sigma = np.array([1.0, 1e-3, 1e-5, 1.5e-6, 1e-6, 5e-7])
+    # s*rho_i <= delta picks the cheapest group: 1.0 -> fp64 (6e-8 > 1e-6? no: 1*6e-8 <= 1e-6 -> fp32)
+    r = oracle.mp_partition(sigma, delta)
+    exp = [0, 0, 0]
+    for s_ in sigma:
+        if s_ <= delta:
+            continue
+        g = 2 if s_ * 4.9e-4 <= delta else (1 if s_ * 6.0e-8 <= delta else 0)
+        exp[g] += 1
+    assert list(r) == exp
