@@ -181,6 +181,8 @@ typedef struct hcmx_hmat_desc {
     /* block-row partition (multi-GPU): only leaves with row0 in [row_begin,row_end)
      * are loaded; matvec then writes y[row_begin,row_end) only. 0,0 = all rows */
     uint64_t row_begin, row_end;
+    /* nonzero: also build M^T (hmatrix.hpp:128 transpose; whole matrix only) */
+    int with_transpose;
 } hcmx_hmat_desc;
 
 typedef struct hcmx_hmat hcmx_hmat; /* opaque, device resident */
@@ -200,15 +202,19 @@ int hcmx_gpu_hmat_destroy(hcmx_hmat* h);
 int hcmx_gpu_hmat_memory(const hcmx_hmat* h, hcmx_memory_report* out);
 
 /* hmatrix.hpp:126-128 matvec: y := alpha * M * x + beta * y (beta == 0 overwrites
- * y; alpha == 0 gives beta * y without touching M).  transpose != 0 is not
- * supported yet (HCMX_INVALID_ARGUMENT).  Host-pointer form: copies x in and y
- * out (the reference-facing call). */
+ * y; alpha == 0 gives beta * y without touching M).  Host-pointer form: copies x in
+ * and y out (the reference-facing call).  transpose != 0: y (n_cols) := alpha M^T x
+ * + beta y, for handles created with with_transpose (else HCMX_INVALID_ARGUMENT). */
 int hcmx_gpu_hmat_matvec(hcmx_hmat* h, double alpha, const double* h_x, double beta, double* h_y,
                          int transpose);
 /* device-pointer form on a stream; d_x has n_cols entries, d_y n_rows entries
  * (for a partitioned handle only d_y[row_begin,row_end) is written) */
 int hcmx_gpu_hmat_matvec_device(hcmx_hmat* h, double alpha, const double* d_x, double beta,
                                 double* d_y, void* stream);
+
+/* the handle of M^T inside a handle created with with_transpose (owned by h;
+ * use it with the _device / _timing calls) */
+int hcmx_gpu_hmat_transposed(hcmx_hmat* h, hcmx_hmat** out);
 
 /* rebuild buffer b's verbatim payload from the device arena (layout check) */
 int hcmx_gpu_hmat_export_buffer(const hcmx_hmat* h, uint64_t b, uint8_t* h_payload,

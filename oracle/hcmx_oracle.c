@@ -470,9 +470,10 @@ typedef struct {
 typedef struct {
     const orc_hmat* h;
     const double* x;
-    double* z; /* private accumulator n_rows */
+    double* z; /* private accumulator n_rows (n_cols when transposed) */
     int64_t l0, l1;
     int status;
+    int transpose; /* hmatrix.hpp:128: y := alpha M^T x + beta y */
 } mv_job;
 
 static int decode_buf(const orc_hmat* h, int64_t b, double* out) {
@@ -517,10 +518,19 @@ static void* mv_worker(void* arg) {
             if (h->count[h->buf0[l]] != rows * cols) { j->status = ORC_INVALID_ARGUMENT; break; }
             j->status = decode_buf(h, h->buf0[l], tmp);
             const double* A = tmp;
-            for (int64_t cc = 0; cc < cols; ++cc) {
-                const double xv = j->x[c0 + cc];
-                const double* a = A + cc * rows;
-                for (int64_t rr = 0; rr < rows; ++rr) j->z[r0 + rr] += a[rr] * xv;
+            if (j->transpose) {
+                for (int64_t cc = 0; cc < cols; ++cc) {
+                    const double* a = A + cc * rows;
+                    double s = 0.0;
+                    for (int64_t rr = 0; rr < rows; ++rr) s += a[rr] * j->x[r0 + rr];
+                    j->z[c0 + cc] += s;
+                }
+            } else {
+                for (int64_t cc = 0; cc < cols; ++cc) {
+                    const double xv = j->x[c0 + cc];
+                    const double* a = A + cc * rows;
+                    for (int64_t rr = 0; rr < rows; ++rr) j->z[r0 + rr] += a[rr] * xv;
+                }
             }
         } else {
             const int64_t k = h->rank[l];
@@ -539,16 +549,20 @@ static void* mv_worker(void* arg) {
                 }
             }
             /* mixedprec.cpp:203-208: U = W diag(sigma), V = X; y_t += U (V^T x_s)
-             * (sigma = 1 for U V^T leaves) */
+             * (sigma = 1 for U V^T leaves); transposed: y_s += V (U^T x_t) */
+            const double* in = j->transpose ? Wd : Xd;
+            const double* outf = j->transpose ? Xd : Wd;
+            const int64_t nin = j->transpose ? rows : cols, nout = j->transpose ? cols : rows;
+            const int64_t oin = j->transpose ? r0 : c0, oout = j->transpose ? c0 : r0;
             for (int64_t i = 0; i < k; ++i) {
                 double s = 0.0;
-                const double* xc = Xd + i * cols;
-                for (int64_t cc = 0; cc < cols; ++cc) s += xc[cc] * j->x[c0 + cc];
+                const double* xc = in + i * nin;
+                for (int64_t cc = 0; cc < nin; ++cc) s += xc[cc] * j->x[oin + cc];
                 t[i] = h->kind[l] == 2 ? s : s * h->sigma[h->sig0[l] + i];
             }
             for (int64_t i = 0; i < k; ++i) {
-                const double* wc = Wd + i * rows;
-                for (int64_t rr = 0; rr < rows; ++rr) j->z[r0 + rr] += wc[rr] * t[i];
+                const double* wc = outf + i * nout;
+                for (int64_t rr = 0; rr < nout; ++rr) j->z[oout + rr] += wc[rr] * t[i];
             }
         }
     }
@@ -558,10 +572,11 @@ static void* mv_worker(void* arg) {
 
 /* leaf ranges split by cumulative value count so threads get even work; the
  * private accumulators are summed in thread order (deterministic for fixed T). */
-int orc_hmat_matvec(const orc_hmat* h, double alpha, const double* x, double beta, double* y,
-                    int threads) {
+int orc_hmat_matvec_t(const orc_hmat* h, double alpha, const double* x, double beta, double* y,
+                      int threads, int transpose) {
     if (threads < 1) threads = 1;
-    for (int64_t i = 0; i < h->n_rows; ++i) y[i] = beta == 0.0 ? 0.0 : beta * y[i];
+    const int64_t ny = transpose ? h->n_cols : h->n_rows;
+    for (int64_t i = 0; i < ny; ++i) y[i] = beta == 0.0 ? 0.0 : beta * y[i];
     if (alpha == 0.0) return ORC_OK;
     double* work = (double*)malloc(sizeof(double) * (size_t)h->nleaves + 8);
     double total = 0.0;
@@ -575,11 +590,11 @@ int orc_hmat_matvec(const orc_hmat* h, double alpha, const double* x, double bet
     int64_t l = 0;
     double acc = 0.0;
     for (int t = 0; t < threads; ++t) {
-        jobs[t].h = h; jobs[t].x = x; jobs[t].l0 = l;
+        jobs[t].h = h; jobs[t].x = x; jobs[t].l0 = l; jobs[t].transpose = transpose;
         double target = total * (double)(t + 1) / (double)threads;
         while (l < h->nleaves && (t == threads - 1 || acc + work[l] * 0.5 <= target)) acc += work[l++];
         jobs[t].l1 = l;
-        jobs[t].z = (double*)calloc((size_t)h->n_rows, sizeof(double));
+        jobs[t].z = (double*)calloc((size_t)ny, sizeof(double));
     }
     for (int t = 1; t < threads; ++t) pthread_create(&tid[t], NULL, mv_worker, &jobs[t]);
     mv_worker(&jobs[0]);
@@ -587,11 +602,16 @@ int orc_hmat_matvec(const orc_hmat* h, double alpha, const double* x, double bet
     int st = ORC_OK;
     for (int t = 0; t < threads; ++t) {
         if (jobs[t].status) st = jobs[t].status;
-        for (int64_t i = 0; i < h->n_rows; ++i) y[i] += alpha * jobs[t].z[i];
+        for (int64_t i = 0; i < ny; ++i) y[i] += alpha * jobs[t].z[i];
         free(jobs[t].z);
     }
     free(jobs); free(tid); free(work);
     return st;
+}
+
+int orc_hmat_matvec(const orc_hmat* h, double alpha, const double* x, double beta, double* y,
+                    int threads) {
+    return orc_hmat_matvec_t(h, alpha, x, beta, y, threads, 0);
 }
 
 /* flat-argument wrapper for ctypes */
@@ -606,6 +626,20 @@ int orc_hmat_matvec_flat(int64_t n_rows, int64_t n_cols, int64_t nleaves, const 
     orc_hmat h = {n_rows, n_cols, nleaves, row0, row1, col0, col1, kind, rank, buf0, sig0,
                   sigma, scheme, e, m, scale, count, poff, plen, blob, raw};
     return orc_hmat_matvec(&h, alpha, x, beta, y, threads);
+}
+
+/* transpose = 1: y (n_cols) := alpha M^T x + beta y (hmatrix.hpp:128) */
+int orc_hmat_matvec_t_flat(int64_t n_rows, int64_t n_cols, int64_t nleaves, const int64_t* row0,
+                           const int64_t* row1, const int64_t* col0, const int64_t* col1,
+                           const int64_t* kind, const int64_t* rank, const int64_t* buf0,
+                           const int64_t* sig0, const double* sigma, const uint8_t* scheme,
+                           const uint8_t* e, const uint8_t* m, const double* scale,
+                           const int64_t* count, const int64_t* poff, const int64_t* plen,
+                           const uint8_t* blob, const double* raw, double alpha, const double* x,
+                           double beta, double* y, int threads, int transpose) {
+    orc_hmat h = {n_rows, n_cols, nleaves, row0, row1, col0, col1, kind, rank, buf0, sig0,
+                  sigma, scheme, e, m, scale, count, poff, plen, blob, raw};
+    return orc_hmat_matvec_t(&h, alpha, x, beta, y, threads, transpose);
 }
 
 /* ------------------------------------------------- batched codec (CPU) --- */

@@ -133,6 +133,9 @@ class Oracle(_Base):
         self._mv = self._fn("hmat_matvec_flat", _i32, _i64, _i64, _i64, *([_pi64] * 8), _pd,
                             _pu8, _pu8, _pu8, _pd, _pi64, _pi64, _pi64, _pu8, _pd, _d, _pd, _d,
                             _pd, _i32)
+        self._mvt = self._fn("hmat_matvec_t_flat", _i32, _i64, _i64, _i64, *([_pi64] * 8), _pd,
+                             _pu8, _pu8, _pu8, _pd, _pi64, _pi64, _pi64, _pu8, _pd, _d, _pd, _d,
+                             _pd, _i32, _i32)
         self._cbat = self._fn("compress_batch", _i32, _pd, _pi64, _pi64, _i64, _d, _i32, _pi32,
                               _pi32, _pd, _pi64, _pu8, _i32)
         self._dbat = self._fn("decompress_batch", _i32, _pu8, _pi64, _pi64, _pi64, _i64, _i32,
@@ -209,7 +212,10 @@ class Oracle(_Base):
     def aplr_compress(self, W, X, sigma, eps, scheme):
         return _aplr(self._aplr, W, X, sigma, eps, scheme)
 
-    def hmat_matvec(self, h, alpha, x, beta, y, threads=1):
+    def hmat_matvec(self, h, alpha, x, beta, y, threads=1, transpose=False):
+        """hmatrix.hpp:126-128 (transpose: y := alpha M^T x + beta y)"""
+        if transpose:
+            return _matvec(self._mvt, h, alpha, x, beta, y, threads, transpose=True)
         return _matvec(self._mv, h, alpha, x, beta, y, threads)
 
     def compress_batch(self, values, counts, eps, scheme, threads=1):
@@ -385,7 +391,7 @@ def _aplr(fn, W, X, sigma, eps, scheme):
     return bufs
 
 
-def _matvec(fn, h, alpha, x, beta, y, threads):
+def _matvec(fn, h, alpha, x, beta, y, threads, transpose=None):
     """h: any object with the flat H-matrix arrays (see hcmx_oracle.c)"""
     x = _f64(x)
     y = np.array(y, dtype=np.float64, copy=True)
@@ -407,5 +413,5 @@ def _matvec(fn, h, alpha, x, beta, y, threads):
               _p(sigma, _d), _p(u8["scheme"], _u8), _p(u8["e"], _u8), _p(u8["m"], _u8),
               _p(scale, _d), _p(arrs["count"], _i64), _p(arrs["poff"], _i64),
               _p(arrs["plen"], _i64), _p(blob, _u8), _p(raw, _d), alpha, _p(x, _d), beta,
-              _p(y, _d), threads), "hmat_matvec")
+              _p(y, _d), threads, *([] if transpose is None else [int(transpose)])), "hmat_matvec")
     return y

@@ -907,6 +907,7 @@ struct hcmx_hmat {
     std::vector<Rec> pending;
     double ms_a = 0, ms_b = 0;
     uint64_t calls = 0;
+    hcmx_hmat* trans = nullptr;  // M^T (hmatrix.hpp:128 transpose), built on request
 };
 
 namespace {
@@ -1686,6 +1687,139 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
     }
 }
 
+// w-bit field at bit `pos` of a byte stream padded by >= 16 readable bytes
+inline uint64_t get_field(const uint8_t* src, uint64_t pos, unsigned w) {
+    uint64_t lo, hi;
+    std::memcpy(&lo, src + (pos >> 3), 8);
+    std::memcpy(&hi, src + (pos >> 3) + 8, 8);
+    const unsigned sh = pos & 7u;
+    uint64_t v = sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+    return w == 64 ? v : v & ((1ull << w) - 1);
+}
+inline void put_field(uint8_t* dst, uint64_t pos, unsigned w, uint64_t v) {  // dst zeroed, padded
+    const unsigned sh = pos & 7u;
+    uint64_t lo, hi;
+    std::memcpy(&lo, dst + (pos >> 3), 8);
+    std::memcpy(&hi, dst + (pos >> 3) + 8, 8);
+    lo |= v << sh;
+    if (sh) hi |= v >> (64 - sh);
+    std::memcpy(dst + (pos >> 3), &lo, 8);
+    std::memcpy(dst + (pos >> 3) + 8, &hi, 8);
+}
+
+// The flattened M^T of a descriptor (hmatrix.hpp:128 transpose = true): row and
+// column ranges swap; a per-column lowrank leaf W Sigma X^H becomes X Sigma W^H
+// and U V^T becomes V U^T (buffer order permuted, bytes shared); a dense leaf's
+// column-major fields are re-ordered into the transposed block's column-major
+// scan (every field keeps its bits; appended to the blob copy).
+struct Transposed {
+    std::vector<int64_t> row0, row1, col0, col1, count, poff, plen;
+    std::vector<hcmx_descriptor> desc;
+    std::vector<uint8_t> blob;
+    hcmx_hmat_desc d{};
+};
+
+void make_transposed(const hcmx_hmat_desc& d, Transposed& t) {
+    const uint64_t L = d.nleaves, nb = d.nbuffers;
+    t.row0.assign(d.col0, d.col0 + L);
+    t.row1.assign(d.col1, d.col1 + L);
+    t.col0.assign(d.row0, d.row0 + L);
+    t.col1.assign(d.row1, d.row1 + L);
+    t.desc.assign(d.desc, d.desc + nb);
+    t.count.assign(d.count, d.count + nb);
+    t.poff.assign(d.poff, d.poff + nb);
+    t.plen.assign(d.plen, d.plen + nb);
+    uint64_t extra = 0;
+    for (uint64_t l = 0; l < L; ++l)
+        if (d.kind[l] == 0) extra += static_cast<uint64_t>(d.plen[d.buf0[l]]) + 16;
+    t.blob.assign(d.blob_bytes + extra + 32, 0);
+    if (d.blob_on_device)
+        check_cuda(cudaMemcpy(t.blob.data(), d.blob, d.blob_bytes, cudaMemcpyDeviceToHost), "blob d2h");
+    else
+        std::memcpy(t.blob.data(), d.blob, d.blob_bytes);
+    uint64_t at = (d.blob_bytes + 15) & ~uint64_t(15);
+    auto take = [&](uint64_t dst, uint64_t src) {
+        t.desc[dst] = d.desc[src];
+        t.count[dst] = d.count[src];
+        t.poff[dst] = d.poff[src];
+        t.plen[dst] = d.plen[src];
+    };
+    for (uint64_t l = 0; l < L; ++l) {
+        const uint64_t b0 = static_cast<uint64_t>(d.buf0[l]);
+        const int64_t k = d.rank[l];
+        if (d.kind[l] == 1) {
+            for (int64_t i = 0; i < k; ++i) {
+                take(b0 + i, b0 + k + i);
+                take(b0 + k + i, b0 + i);
+            }
+        } else if (d.kind[l] == 2) {
+            if (k > 0) {
+                take(b0, b0 + 1);
+                take(b0 + 1, b0);
+            }
+        } else {
+            const uint64_t rows = d.row1[l] - d.row0[l], cols = d.col1[l] - d.col0[l];
+            const unsigned w = d.desc[b0].bit_width;
+            const uint8_t* src = t.blob.data() + d.poff[b0];
+            uint8_t* dst = t.blob.data() + at;
+            for (uint64_t c = 0; c < cols; ++c)
+                for (uint64_t r = 0; r < rows; ++r)
+                    put_field(dst, (c + r * cols) * w, w, get_field(src, (r + c * rows) * w, w));
+            t.poff[b0] = static_cast<int64_t>(at);
+            at += (static_cast<uint64_t>(d.plen[b0]) + 15) & ~uint64_t(15);
+        }
+    }
+    t.d = d;
+    t.d.n_rows = d.n_cols;
+    t.d.n_cols = d.n_rows;
+    t.d.row0 = t.row0.data();
+    t.d.row1 = t.row1.data();
+    t.d.col0 = t.col0.data();
+    t.d.col1 = t.col1.data();
+    t.d.desc = t.desc.data();
+    t.d.count = t.count.data();
+    t.d.poff = t.poff.data();
+    t.d.plen = t.plen.data();
+    t.d.blob = t.blob.data();
+    t.d.blob_bytes = at;
+    t.d.blob_on_device = 0;
+    t.d.row_begin = t.d.row_end = 0;
+    t.d.with_transpose = 0;
+}
+
+void destroy_handle(hcmx_hmat* h) {
+    if (!h) return;
+    destroy_handle(h->trans);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    for (auto& r : h->pending) {
+        cudaEventDestroy(r.a0);
+        cudaEventDestroy(r.a1);
+        cudaEventDestroy(r.b1);
+    }
+    for (auto e : h->ev_pool) cudaEventDestroy(e);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+hcmx_hmat* create_handle(const hcmx_hmat_desc& d) {
+    auto* h = new hcmx_hmat();
+    try {
+        check_cuda(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        build(d, h);
+        if (d.with_transpose) {
+            if (d.row_begin != 0 || d.row_end != 0)
+                throw invalid_argument("hmat: the transpose needs the whole matrix (no row partition)");
+            Transposed t;
+            make_transposed(d, t);
+            h->trans = create_handle(t.d);
+        }
+    } catch (...) {
+        destroy_handle(h);
+        throw;
+    }
+    return h;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1693,32 +1827,19 @@ extern "C" {
 int hcmx_gpu_hmat_create(const hcmx_hmat_desc* desc, hcmx_hmat** out) {
     return guarded([&] {
         require_device();
-        auto* h = new hcmx_hmat();
-        try {
-            check_cuda(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
-            build(*desc, h);
-        } catch (...) {
-            if (h->stream) cudaStreamDestroy(h->stream);
-            delete h;
-            throw;
-        }
-        *out = h;
+        *out = create_handle(*desc);
+    });
+}
+
+int hcmx_gpu_hmat_transposed(hcmx_hmat* h, hcmx_hmat** out) {
+    return guarded([&] {
+        if (!h->trans) throw invalid_argument("hmat: created without with_transpose");
+        *out = h->trans;
     });
 }
 
 int hcmx_gpu_hmat_destroy(hcmx_hmat* h) {
-    return guarded([&] {
-        if (!h) return;
-        cudaStreamSynchronize(h->stream);
-        for (auto& r : h->pending) {
-            cudaEventDestroy(r.a0);
-            cudaEventDestroy(r.a1);
-            cudaEventDestroy(r.b1);
-        }
-        for (auto e : h->ev_pool) cudaEventDestroy(e);
-        cudaStreamDestroy(h->stream);
-        delete h;
-    });
+    return guarded([&] { destroy_handle(h); });
 }
 
 int hcmx_gpu_hmat_memory(const hcmx_hmat* h, hcmx_memory_report* out) {
@@ -1733,7 +1854,10 @@ int hcmx_gpu_hmat_matvec_device(hcmx_hmat* h, double alpha, const double* d_x, d
 int hcmx_gpu_hmat_matvec(hcmx_hmat* h, double alpha, const double* h_x, double beta, double* h_y,
                          int transpose) {
     return guarded([&] {
-        if (transpose) throw invalid_argument("matvec: transpose is not supported");
+        if (transpose) {  // hmatrix.hpp:128: y (n_cols) := alpha M^T x + beta y
+            if (!h->trans) throw invalid_argument("matvec: transpose needs a handle created with with_transpose");
+            h = h->trans;
+        }
         if (!h->xbuf.p) h->xbuf.alloc(h->n_cols * 8);
         if (!h->ybuf.p) h->ybuf.alloc(h->n_rows * 8);
         const uint64_t nr = h->re - h->rb;

@@ -379,7 +379,8 @@ def build_config(cfg, scheme="afl", device=None, n=None, seed=1, eps=None) -> tu
 class HMatrix:
     """Device-resident compressed H-matrix (handle over hcmx_gpu_hmat_*)."""
 
-    def __init__(self, flat: FlatHMatrix, row_range: tuple[int, int] | None = None):
+    def __init__(self, flat: FlatHMatrix, row_range: tuple[int, int] | None = None,
+                 with_transpose: bool = False):
         _lib.ensure_device()
         self.n_rows, self.n_cols = int(flat.n_rows), int(flat.n_cols)
         self.row_range = row_range or (0, self.n_rows)
@@ -405,6 +406,7 @@ class HMatrix:
         d.blob = ptr(blob)
         d.blob_on_device = int(on_dev)
         d.row_begin, d.row_end = (0, 0) if row_range is None else row_range
+        d.with_transpose = int(with_transpose)
         h = C.c_void_p()
         check(lib().hcmx_gpu_hmat_create(C.byref(d), C.byref(h)), "hmat_create")
         self._h = h
@@ -439,18 +441,18 @@ class HMatrix:
         return y
 
     def matvec(self, alpha: float, x, beta: float, y, transpose: bool = False):
-        """hmatrix.hpp:126-128 with host vectors (copies in/out inside)"""
-        if transpose:
-            raise ValueError("matvec: transpose is not supported by the GPU path yet")
-        if isinstance(x, torch.Tensor) and x.is_cuda:
+        """hmatrix.hpp:126-128 with host vectors (copies in/out inside); transpose:
+        y := alpha M^T x + beta y (handle built with with_transpose=True)"""
+        if isinstance(x, torch.Tensor) and x.is_cuda and not transpose:
             return self.matvec_device(alpha, x, beta, y)
         xa = np.ascontiguousarray(x, dtype=np.float64)
-        if xa.size != self.n_cols or np.asarray(y).size != self.n_rows:
+        nx, ny = (self.n_rows, self.n_cols) if transpose else (self.n_cols, self.n_rows)
+        if xa.size != nx or np.asarray(y).size != ny:
             raise ValueError("matvec: dimension mismatch")
         if not (isinstance(y, np.ndarray) and y.dtype == np.float64 and y.flags.c_contiguous):
             raise ValueError("matvec: y must be a contiguous float64 array")
-        check(lib().hcmx_gpu_hmat_matvec(self._h, float(alpha), ptr(xa), float(beta), ptr(y), 0),
-              "matvec")
+        check(lib().hcmx_gpu_hmat_matvec(self._h, float(alpha), ptr(xa), float(beta), ptr(y),
+                                         int(bool(transpose))), "matvec")
         return y
 
     def launches(self) -> int:

@@ -211,3 +211,25 @@ def test_storage_modes(gpu, oracle, mode, scheme, dense_too):
     y = np.zeros(1024)
     HMatrix(g).matvec(1.0, x, 0.0, y)
     assert rel(y, oracle.hmat_matvec(f, 1.0, x, 0.0, np.zeros(1024), threads=4)) <= TOL
+
+
+@pytest.mark.parametrize("mode,scheme", [("aplr", 0), ("codec", 1), ("mp", 0), ("aplr", 3)])
+def test_transpose(gpu, oracle, mode, scheme):
+    """hmatrix.hpp:128 matvec(..., transpose = true) vs the oracle's M^T product;
+    ragged clusters (n = 1100) and every leaf kind"""
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    n = 1100
+    f, x = build_small_flat(n=n, eps=1e-6, scheme=scheme, mode=mode, geometry="sphere")
+    H = HMatrix(f.to_product(), with_transpose=True)
+    y0 = np.random.default_rng(5).standard_normal(n)
+    for alpha, beta in ((1.0, 0.0), (-0.4, 2.0)):
+        ref = oracle.hmat_matvec(f, alpha, x, beta, y0, threads=4, transpose=True)
+        y = y0.copy()
+        H.matvec(alpha, x, beta, y, transpose=True)
+        assert rel(y, ref) <= TOL, (alpha, beta)
+        y = y0.copy()  # the forward product is unchanged by the extra handle
+        H.matvec(alpha, x, beta, y)
+        assert rel(y, oracle.hmat_matvec(f, alpha, x, beta, y0, threads=4)) <= TOL
+    with pytest.raises(ValueError):
+        HMatrix(f.to_product()).matvec(1.0, x, 0.0, np.zeros(n), transpose=True)
