@@ -207,6 +207,11 @@ int hcmx_gpu_hmat_memory(const hcmx_hmat* h, hcmx_memory_report* out);
  * + beta y, for handles created with with_transpose (else HCMX_INVALID_ARGUMENT). */
 int hcmx_gpu_hmat_matvec(hcmx_hmat* h, double alpha, const double* h_x, double beta, double* h_y,
                          int transpose);
+/* several right-hand sides: Y := alpha op(M) X +
+ * beta Y for nrhs host columns (column-major, leading dimensions ldx / ldy); one
+ * copy of X in and of Y out, one device product per column */
+int hcmx_gpu_hmat_matmat(hcmx_hmat* h, double alpha, const double* h_x, uint64_t ldx, uint64_t nrhs,
+                         double beta, double* h_y, uint64_t ldy, int transpose);
 /* device-pointer form on a stream; d_x has n_cols entries, d_y n_rows entries
  * (for a partitioned handle only d_y[row_begin,row_end) is written) */
 int hcmx_gpu_hmat_matvec_device(hcmx_hmat* h, double alpha, const double* d_x, double beta,

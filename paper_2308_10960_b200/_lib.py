@@ -97,6 +97,7 @@ PROTOTYPES = {
     "hcmx_gpu_hmat_destroy": (_i, [_vp]),
     "hcmx_gpu_hmat_memory": (_i, [_vp, C.POINTER(hcmx_memory_report)]),
     "hcmx_gpu_hmat_matvec": (_i, [_vp, _d, _vp, _d, _vp, _i]),
+    "hcmx_gpu_hmat_matmat": (_i, [_vp, _d, _vp, _u64, _u64, _d, _vp, _u64, _i]),
     "hcmx_gpu_hmat_matvec_device": (_i, [_vp, _d, _vp, _d, _vp, _vp]),
     "hcmx_gpu_hmat_transposed": (_i, [_vp, C.POINTER(_vp)]),
     "hcmx_gpu_hmat_export_buffer": (_i, [_vp, _u64, _vp, _u64, _pu64]),

@@ -1846,6 +1846,29 @@ int hcmx_gpu_hmat_memory(const hcmx_hmat* h, hcmx_memory_report* out) {
     return guarded([&] { *out = h->report; });
 }
 
+int hcmx_gpu_hmat_matmat(hcmx_hmat* h, double alpha, const double* h_x, uint64_t ldx, uint64_t nrhs,
+                         double beta, double* h_y, uint64_t ldy, int transpose) {
+    return guarded([&] {
+        if (transpose) {
+            if (!h->trans) throw invalid_argument("matmat: transpose needs a handle created with with_transpose");
+            h = h->trans;
+        }
+        if (ldx < h->n_cols || ldy < h->n_rows) throw invalid_argument("matmat: leading dimension too small");
+        if (!nrhs) return;
+        // all right-hand sides in one copy each way; one product per column
+        DevBuf dx(h->n_cols * nrhs * 8), dy(h->n_rows * nrhs * 8);
+        for (uint64_t j = 0; j < nrhs; ++j) h2d(dx.as<double>() + j * h->n_cols, h_x + j * ldx, h->n_cols * 8, h->stream);
+        const uint64_t nr = h->re - h->rb;
+        if (beta != 0.0)
+            for (uint64_t j = 0; j < nrhs; ++j)
+                h2d(dy.as<double>() + j * h->n_rows + h->rb, h_y + j * ldy + h->rb, nr * 8, h->stream);
+        for (uint64_t j = 0; j < nrhs; ++j)
+            run_matvec(h, alpha, dx.as<double>() + j * h->n_cols, beta, dy.as<double>() + j * h->n_rows, h->stream);
+        for (uint64_t j = 0; j < nrhs; ++j) d2h(h_y + j * ldy + h->rb, dy.as<double>() + j * h->n_rows + h->rb, nr * 8, h->stream);
+        stream_sync(h->stream);
+    });
+}
+
 int hcmx_gpu_hmat_matvec_device(hcmx_hmat* h, double alpha, const double* d_x, double beta, double* d_y,
                                 void* stream) {
     return guarded([&] { run_matvec(h, alpha, d_x, beta, d_y, (cudaStream_t)stream); });

@@ -455,6 +455,19 @@ class HMatrix:
                                          int(bool(transpose))), "matvec")
         return y
 
+    def matmat(self, alpha: float, X, beta: float, Y, transpose: bool = False):
+        """Y := alpha op(M) X + beta Y for the columns of X (host, float64; C5's
+        multi-RHS products)"""
+        X = np.asfortranarray(X, dtype=np.float64)
+        nx, ny = (self.n_rows, self.n_cols) if transpose else (self.n_cols, self.n_rows)
+        if X.ndim != 2 or X.shape[0] != nx or Y.shape != (ny, X.shape[1]):
+            raise ValueError("matmat: dimension mismatch")
+        if not (isinstance(Y, np.ndarray) and Y.dtype == np.float64 and Y.flags.f_contiguous):
+            raise ValueError("matmat: Y must be a Fortran-ordered float64 array")
+        check(lib().hcmx_gpu_hmat_matmat(self._h, float(alpha), ptr(X), nx, X.shape[1], float(beta), ptr(Y), ny,
+                                         int(bool(transpose))), "matmat")
+        return Y
+
     def launches(self) -> int:
         return lib().hcmx_gpu_hmat_last_launches(self._h)
 

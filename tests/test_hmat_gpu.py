@@ -233,3 +233,21 @@ def test_transpose(gpu, oracle, mode, scheme):
         assert rel(y, oracle.hmat_matvec(f, alpha, x, beta, y0, threads=4)) <= TOL
     with pytest.raises(ValueError):
         HMatrix(f.to_product()).matvec(1.0, x, 0.0, np.zeros(n), transpose=True)
+
+
+def test_matmat_multi_rhs(gpu, oracle):
+    """several right-hand sides (forward and transposed) == column-wise oracle products"""
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    n = 1024
+    f, _ = build_small_flat(n=n, eps=1e-6, scheme=0)
+    H = HMatrix(f.to_product(), with_transpose=True)
+    rng = np.random.default_rng(6)
+    X = np.asfortranarray(rng.uniform(-1, 1, (n, 5)))
+    Y0 = np.asfortranarray(rng.standard_normal((n, 5)))
+    for tr in (False, True):
+        Y = Y0.copy(order="F")
+        H.matmat(0.5, X, -1.0, Y, transpose=tr)
+        for j in range(5):
+            ref = oracle.hmat_matvec(f, 0.5, X[:, j], -1.0, Y0[:, j], threads=4, transpose=tr)
+            assert rel(Y[:, j], ref) <= TOL, (tr, j)
