@@ -22,7 +22,8 @@ INC = os.path.join(ROOT, "include")
 NVCC = os.environ.get("NVCC", "nvcc")
 CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVFLAGS = ARCH + [*(["-DHCMX_PROF"] if os.environ.get("HCMX_PROF_BUILD") else []), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
+NVFLAGS = ARCH + [*(["-DHCMX_PROF"] if os.environ.get("HCMX_PROF_BUILD") else []),
+                  *os.environ.get("HCMX_NVCC_DEFS", "").split(), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
                   "-I" + INC, "-I" + CSRC]
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-I" + INC, "-I" + CSRC]
 

@@ -105,7 +105,7 @@ static_assert(sizeof(Stage) == 32, "Stage layout");
 // Column layout parameters, precomputed on the host (16 bytes, one LDS.128)
 struct ColPar {
     uint32_t mask_em;    // (1 << (e + m)) - 1, all ones for e + m >= 32
-    uint32_t mul_rsh;    // mode 0: 1 << (20 - m); mode 1: m - 20
+    uint32_t mul_rsh;    // mode 0: 1 << (20 - m); mode 1: 1 << (52 - m)
     uint32_t packed;     // w | m << 8 | e << 16 | mode << 24
     uint32_t sgn_sh;     // 31 - e - m (mode 0/1)
 };
@@ -194,7 +194,11 @@ __device__ __forceinline__ unsigned long long gtime() {
 #else
 #define PROF_ADD(ph, i, v) ((void)0)
 #endif
+#ifdef HCMX_PROF
 __device__ __forceinline__ long long clk() { return clock64(); }
+#else
+__device__ __forceinline__ long long clk() { return 0; }  // no clock reads in product builds
+#endif
 
 // ----------------------------------------------------------- PTX glue ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -277,10 +281,11 @@ __device__ __forceinline__ double dec(const uint32_t* sp, const ColPar& c, unsig
         const double d = __hiloint2double(hi, 0) - 1.0;
         return __hiloint2double(__double2hiint(d) ^ ((t << c.sgn_sh) & 0x80000000u), __double2loint(d));
     } else if (MODE == 1) {
+        // mul = 2^(52 - m): the double's bits are (t & mask) * mul + (1023 << 52),
+        // one wide IMAD with a loop-invariant addend
         const uint32_t t = __funnelshift_r(sp[0], sp[1], sh);
-        const uint32_t hi = ((t & c.mask_em) >> c.mul_rsh) + (1023u << 20);
-        const uint32_t lo = t << (32u - c.mul_rsh);
-        const double d = __hiloint2double(hi, lo) - 1.0;
+        const uint64_t bits = static_cast<uint64_t>(t & c.mask_em) * c.mul_rsh + (1023ull << 52);
+        const double d = __longlong_as_double(static_cast<long long>(bits)) - 1.0;
         return __hiloint2double(__double2hiint(d) ^ ((t << c.sgn_sh) & 0x80000000u), __double2loint(d));
     } else {
         const unsigned fmt = c.packed >> 24;
@@ -308,13 +313,28 @@ __device__ __forceinline__ double dec(const uint32_t* sp, const ColPar& c, unsig
 
 // decoder constants of one column from its packed layout word (w | m << 8 |
 // e << 16 | mode << 24); modes 0/1 have w == 1 + e + m
+// decoder multiplier of a column with m mantissa bits: 2^(20 - m) (mode 0,
+// m <= 20) or 2^(52 - m) (mode 1, 20 < m <= 31), read from a table: a
+// multiplier the compiler cannot see is a power of two stays an IMAD (fused
+// with the exponent bias) instead of a shift plus an add on the integer ALU,
+// the decode's tightest pipe
+struct Pow2Table {
+    uint32_t v[32];
+};
+constexpr Pow2Table make_pow2() {
+    Pow2Table t{};
+    for (int m = 0; m < 32; ++m) t.v[m] = m <= 20 ? (1u << (20 - m)) : (1u << (52 - m));
+    return t;
+}
+__constant__ Pow2Table c_pow2 = make_pow2();
+
 template <int MODE>
 __device__ __forceinline__ ColPar col_of(uint32_t packed) {
     ColPar c;
     c.packed = packed;
     const unsigned w = packed & 0xffu, m = (packed >> 8) & 0xffu;
     c.mask_em = 0xffffffffu >> (33u - w);  // e + m = w - 1 bits
-    c.mul_rsh = MODE == 0 ? (1u << (20u - m)) : m - 20u;
+    c.mul_rsh = c_pow2.v[m & 31u];
     c.sgn_sh = 32u - w;                    // sign bit (w - 1) to bit 31
     return c;
 }
@@ -433,12 +453,12 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
     const unsigned long long g0 = gtime();
 #endif
     long long t_wait = 0;
+    unsigned slot = 0, phase = 0;  // it % kNStage, parity of the slot's previous use
     for (uint32_t it = 0;; ++it) {
         seq_next<PHASE_A>(p, q, lane);
         const StageMeta m2 = seq_meta<PHASE_A>(p, q, lane);
-        const int slot = static_cast<int>(it % kNStage);
         const long long t0 = clk();
-        if (it >= kNStage) mbar_wait(&empty[slot], ((it / kNStage) - 1) & 1u);
+        if (it >= kNStage) mbar_wait(&empty[slot], phase);
         t_wait += clk() - t0;
         uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
         if (lane == 0) {
@@ -481,6 +501,10 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
         }
         m0 = m1;
         m1 = m2;
+        if (++slot == kNStage) {
+            slot = 0;
+            if (it + 1 > kNStage) phase ^= 1u;
+        }
     }
 }
 
@@ -490,14 +514,22 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
 // its own results, so any assignment gives the same bits).  Otherwise each
 // warp takes its precomputed contiguous range (phase B: a warp's row sums
 // must see the same items in the same order on every run: deterministic y).
+// one item claim: a plain shared-memory atomic from one lane (atomicAdd from a
+// lane-0 branch compiles to the warp-aggregated sequence, ~12 instructions)
+__device__ __forceinline__ unsigned claim(uint32_t* counter) {
+    unsigned v;
+    asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(v) : "r"(smem_u32(counter)) : "memory");
+    return v;
+}
+
 template <int NW, bool DYN, class Body, class End>
 __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t* empty, unsigned warp,
                                         unsigned lane, int debug, Body&& body, End&& stripe_end) {
     long long t_wait = 0, t_busy = 0, t_end = 0;
-    for (uint32_t it = 0;; ++it) {
-        const int slot = static_cast<int>(it % kNStage);
+    unsigned slot = 0, phase = 0;  // ring position of stage it: it % kNStage, (it / kNStage) & 1
+    for (;;) {
         const long long t0 = clk();
-        mbar_wait(&full[slot], (it / kNStage) & 1u);
+        mbar_wait(&full[slot], phase);
         const long long t1 = clk();
         t_wait += t1 - t0;
         const uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
@@ -518,10 +550,10 @@ __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t*
             // shared atomic's latency hides behind it
             const unsigned n = hdr[3];
             unsigned nl = 0;
-            if (lane == 0) nl = atomicAdd(hdr + 2, 1u);
+            if (lane == 0) nl = claim(hdr + 2);
             unsigned i = __shfl_sync(0xffffffffu, nl, 0);
             while (i < n) {
-                if (lane == 0) nl = atomicAdd(hdr + 2, 1u);
+                if (lane == 0) nl = claim(hdr + 2);
                 body(base, i);
                 i = __shfl_sync(0xffffffffu, nl, 0);
             }
@@ -536,6 +568,10 @@ __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t*
         if (flags & kHdrLast) {
             stripe_end(stripe);
             t_end += clk() - t2;
+        }
+        if (++slot == kNStage) {
+            slot = 0;
+            phase ^= 1u;
         }
     }
 }
@@ -945,7 +981,7 @@ ColPar col_par(const hcmx_descriptor& x) {
     unsigned mode = (w > 32 || e >= 11 || w != 1 + em) ? 2u : (m <= 20 ? 0u : 1u);
     if (x.scheme >= HCMX_RAW_F64) mode = 3u + (x.scheme - HCMX_RAW_F64);  // uncompressed storage
     c.mask_em = em >= 32 ? 0xffffffffu : ((1u << em) - 1u);
-    c.mul_rsh = mode == 0 ? (1u << (20 - m)) : (mode == 1 ? m - 20 : 0u);
+    c.mul_rsh = mode == 0 ? (1u << (20 - m)) : (mode == 1 ? 1u << (52 - m) : 0u);
     c.packed = w | (m << 8) | (e << 16) | (mode << 24);
     c.sgn_sh = em <= 31 ? 31 - em : 0u;
     return c;
