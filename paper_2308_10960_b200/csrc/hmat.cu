@@ -130,7 +130,7 @@ struct BItem {
     uint32_t src;        // dense: x index of first column; lowrank: global W column id
     uint32_t dpacked;    // dense: w | m << 8 | e << 16 | mode << 24
     uint8_t mode;        // decode mode shared by every column of the item
-    uint8_t fcase;       // GLO << 4 | GHI when the item covers whole row groups [GLO, GHI), else 0
+    uint8_t fcase;       // decode body (bcase_of): 1-6 fast (mode 0/1 x whole row groups), 0 generic
     uint16_t pad;
     double scale;        // dense: buffer scale
 };
@@ -139,7 +139,7 @@ static_assert(sizeof(BItem) == kItemBytes, "BItem layout");
 struct AItem {
     uint32_t word_off;
     uint8_t nseg;        // rank columns (<= kAGroup)
-    uint8_t mode;        // decode mode shared by every column of the item
+    uint8_t mode;        // decode body (acase_of): 1-6 fast (2/4/8 fields per lane x mode 0/1), 0 generic
     uint16_t nf;         // fields per column (<= kAChunk)
     uint32_t x_off;      // staged x value of field 0 (coef-area bytes)
     uint32_t pbase;      // partials of the leaf (nchunks > 1)
@@ -198,6 +198,13 @@ __device__ __forceinline__ unsigned long long gtime() {
 __device__ __forceinline__ long long clk() { return clock64(); }
 #else
 __device__ __forceinline__ long long clk() { return 0; }  // no clock reads in product builds
+#endif
+
+// the HCMX_DEBUG profiling knob reaches the kernels in HCMX_PROF builds only
+#ifdef HCMX_PROF
+#define dbg(p) ((p).debug)
+#else
+#define dbg(p) 0
 #endif
 
 // ----------------------------------------------------------- PTX glue ----
@@ -472,7 +479,7 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
         if (m0.flags & kHdrEnd || m0.empty) {  // header only
             if (lane == 0) mbar_arrive(&full[slot]);
         } else {
-            const bool no_coef = p.debug >= 2, no_meta = p.debug >= 3;  // profiling knobs
+            const bool no_coef = dbg(p) >= 2, no_meta = dbg(p) >= 3;  // profiling knobs
             if (lane == 0) {
                 (void)no_meta;
                 mbar_expect_tx(&full[slot], m0.st.bytes + (no_coef ? 0u : m0.st.coef_bytes));
@@ -680,8 +687,7 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
     // fast bodies for modes 0/1 at the chunk sizes 64-row leaf clusters give;
     // mode 2 (e = 11 or w > 32) and ragged chunks take one generic body (the
     // mode-2 decoder is exact for every layout; keeps the kernel small)
-    const unsigned ui = nf == 256 ? 3u : nf == 128 ? 2u : nf == 64 ? 1u : 0u;
-    switch (it.mode >= 2 || ui == 0 ? 0u : ui + 3u * it.mode) {
+    switch (it.mode) {  // the body index, precomputed by acase_of
         case 3: a_cols<0, 8>(pk, nseg, nf, lane, xs, a); break;
         case 2: a_cols<0, 4>(pk, nseg, nf, lane, xs, a); break;
         case 1: a_cols<0, 2>(pk, nseg, nf, lane, xs, a); break;
@@ -797,14 +803,13 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
     // everything else takes one generic body with the mode-2 decoder (exact for
     // every layout), which keeps the kernel inside the instruction cache
     static_assert(kG == 4, "fast-path table assumes 128-row blocks");
-    const unsigned fc = it.mode >= 2 ? 0u : it.fcase;
-    switch (fc | (it.mode << 8)) {
-        case 0x004: b_item_full<0, 0, 4>(it, seg, cf, lane, dmul, acc); break;
-        case 0x002: b_item_full<0, 0, 2>(it, seg, cf, lane, dmul, acc); break;
-        case 0x024: b_item_full<0, 2, 4>(it, seg, cf, lane, dmul, acc); break;
-        case 0x104: b_item_full<1, 0, 4>(it, seg, cf, lane, dmul, acc); break;
-        case 0x102: b_item_full<1, 0, 2>(it, seg, cf, lane, dmul, acc); break;
-        case 0x124: b_item_full<1, 2, 4>(it, seg, cf, lane, dmul, acc); break;
+    switch (it.fcase) {  // the body index, precomputed by bcase_of (a dense jump table)
+        case 1: b_item_full<0, 0, 4>(it, seg, cf, lane, dmul, acc); break;
+        case 2: b_item_full<0, 0, 2>(it, seg, cf, lane, dmul, acc); break;
+        case 3: b_item_full<0, 2, 4>(it, seg, cf, lane, dmul, acc); break;
+        case 4: b_item_full<1, 0, 4>(it, seg, cf, lane, dmul, acc); break;
+        case 5: b_item_full<1, 0, 2>(it, seg, cf, lane, dmul, acc); break;
+        case 6: b_item_full<1, 2, 4>(it, seg, cf, lane, dmul, acc); break;
         default:
             b_item_generic<2>(it, seg, cf, lane, dmul, acc);  // also uncompressed words (modes 3-5)
             break;
@@ -827,7 +832,7 @@ __global__ void __launch_bounds__(kThreadsA, 2) k_phase_a(Params p) {
         return;
     }
     consume<kNWA, true>(
-        smem, full, empty, warp, lane, p.debug,
+        smem, full, empty, warp, lane, dbg(p),
         [&](const uint8_t* base, unsigned i) {
             a_item(p, reinterpret_cast<const AItem*>(base)[i], base, lane);
         },
@@ -850,7 +855,7 @@ __global__ void __launch_bounds__(kThreadsB, 2) k_phase_b(Params p) {
     for (int g = 0; g < kG; ++g) acc[g] = 0.0;
     constexpr unsigned H = kNWB / 2;
     consume<kNWB, false>(
-        smem, full, empty, warp, lane, p.debug,
+        smem, full, empty, warp, lane, dbg(p),
         [&](const uint8_t* base, unsigned i) {
             b_item(p, reinterpret_cast<const BItem*>(base)[i], base, lane, acc);
         },
@@ -996,6 +1001,20 @@ uint8_t fcase_of(uint64_t ra, uint64_t nr) {
         case 0x04: case 0x02: case 0x24: return static_cast<uint8_t>(c);
         default: return 0;
     }
+}
+
+// phase-B body index: whole row groups [0,4) / [0,2) / [2,4) x decode mode 0 / 1
+uint8_t bcase_of(uint64_t ra, uint64_t nr, unsigned mode) {
+    const uint8_t f = fcase_of(ra, nr);
+    if (mode >= 2 || f == 0) return 0;
+    return static_cast<uint8_t>((f == 0x04 ? 1 : f == 0x02 ? 2 : 3) + 3 * mode);
+}
+
+// phase-A body index: fields per lane 2 / 4 / 8 (64 / 128 / 256-field chunks) x
+// decode mode 0 / 1 -> 1-6; anything else 0 (the generic body)
+uint8_t acase_of(uint64_t nf, unsigned mode) {
+    const unsigned ui = nf == 256 ? 3u : nf == 128 ? 2u : nf == 64 ? 1u : 0u;
+    return static_cast<uint8_t>(mode >= 2 || ui == 0 ? 0u : ui + 3u * mode);
 }
 
 inline uint32_t r16(uint64_t x) { return static_cast<uint32_t>((x + 15) & ~uint64_t(15)); }
@@ -1454,13 +1473,14 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                     it.pbase = L.pbase;
                     sp.words += ng;  // packed column layout word
                     sp.param = col_par(d.desc[xbuf(l, g).first]).packed;
-                    it.mode = static_cast<uint8_t>(sp.param >> 24);
+                    const unsigned mode = sp.param >> 24;
+                    it.mode = acase_of(nf, mode);
                     sp.elem = xidx;
                     sp.sl_table = 0;  // x slice of the chunk
                     sp.sl_start = xidx;
                     sp.sl_count = static_cast<uint32_t>(nf);
                     sp.cost = nf * ng;
-                    sp.unit = unit * 8 + it.mode;  // items never mix decode modes
+                    sp.unit = unit * 8 + mode;  // items never mix decode modes
                     sp.xidx = xidx;
                     sp.nf = static_cast<uint32_t>(nf);
                     stripe_bytes += sp.words * 4;
@@ -1516,7 +1536,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                         it.nr = static_cast<uint8_t>(nr);
                         it.dpacked = col_par(d.desc[b]).packed;
                         it.mode = static_cast<uint8_t>(it.dpacked >> 24);
-                        it.fcase = fcase_of(r0 - b0, nr);
+                        it.fcase = bcase_of(r0 - b0, nr, it.mode);
                         it.scale = d.desc[b].scale;
                         sp.elem = it.src;
                         sp.sl_table = 0;  // x slice of the dense leaf's columns
@@ -1546,7 +1566,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                         it.nr = static_cast<uint8_t>(nr);
                         it.src = L.colbase + g;
                         it.mode = static_cast<uint8_t>(col_par(d.desc[wbuf(l, g).first]).packed >> 24);
-                        it.fcase = fcase_of(r0 - b0, nr);
+                        it.fcase = bcase_of(r0 - b0, nr, it.mode);
                         sp.elem = it.src;
                         sp.sl_table = 1;  // phase-A results of the leaf
                         sp.sl_start = L.colbase;
