@@ -262,6 +262,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 
 
 
+// Programmatic dependent launch: k_reduce and k_phase_b are launched while the
+// kernel before them still runs (their CTAs take SMs as phase-A CTAs retire)
+// and wait for its completion only where they first read what it wrote.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -460,6 +466,7 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
     const unsigned long long g0 = gtime();
 #endif
     long long t_wait = 0;
+    bool waited = false;           // phase B: griddepcontrol.wait done
     unsigned slot = 0, phase = 0;  // it % kNStage, parity of the slot's previous use
     for (uint32_t it = 0;; ++it) {
         seq_next<PHASE_A>(p, q, lane);
@@ -479,6 +486,17 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
         if (m0.flags & kHdrEnd || m0.empty) {  // header only
             if (lane == 0) mbar_arrive(&full[slot]);
         } else {
+            if (!PHASE_A && !waited) {
+                // the first stage that copies phase-A column coefficients (table
+                // 1) waits for phase A and k_reduce to complete; dense stages
+                // before it run while they drain
+                const bool needs_a = ((m0.c0 >> 63) && ((m0.c0 >> 60) & 3u) == 1u) ||
+                                     ((m0.c1 >> 63) && ((m0.c1 >> 60) & 3u) == 1u);
+                if (__any_sync(0xffffffffu, needs_a)) {
+                    pdl_wait();
+                    waited = true;
+                }
+            }
             const bool no_coef = dbg(p) >= 2, no_meta = dbg(p) >= 3;  // profiling knobs
             if (lane == 0) {
                 (void)no_meta;
@@ -492,6 +510,10 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
             }
         }
         if (m0.flags & kHdrEnd) {
+            if (!PHASE_A && blockIdx.x == 0 && lane == 0) {
+                if (!waited) pdl_wait();
+                p.work[0] = 0u;  // phase A's stripe counter, for the next product
+            }
             if (lane == 0) {
                 PROF_ADD(PHASE_A ? 0 : 1, 2, t_wait);
                 PROF_ADD(PHASE_A ? 0 : 1, 3, clk() - t_start);
@@ -705,6 +727,8 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
 }
 
 __global__ void k_reduce(Params p, const RedCol* rc, uint32_t n) {
+    pdl_trigger();
+    pdl_wait();  // the partials of phase A
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const RedCol r = rc[i];
         double s[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains, fixed order
@@ -826,7 +850,14 @@ __global__ void __launch_bounds__(kThreadsA, 2) k_phase_a(Params p) {
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kRedBytes);
     uint64_t* empty = full + kNStage;
     const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    // phase B's stripe counter for this product (A runs first, B claims only
+    // after its griddepcontrol.wait, so the store is visible by then)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        p.work[1] = 0u;
+        __threadfence();  // visible before this CTA triggers phase B's launch
+    }
     ring_init<kNWA>(full, empty);
+    pdl_trigger();
     if (warp == kNWA) {
         producer<true>(p, smem, full, empty, lane);
         return;
@@ -1501,6 +1532,11 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         const uint64_t b = std::min<uint64_t>(d.row1[l], h->re) - h->rb;
         for (uint64_t blk = a / kR; blk * kR < b; ++blk) block_leaves[blk].push_back(static_cast<uint32_t>(l));
     }
+    // dense leaves first in every row block: their stages need nothing from
+    // phase A, so a phase-B CTA that starts while phase A drains (programmatic
+    // dependent launch) has work before it must wait for the coefficients
+    for (auto& bl : block_leaves)
+        std::stable_partition(bl.begin(), bl.end(), [&](uint32_t l) { return d.kind[l] == 0; });
     const size_t b_ws0 = B.stages.size();
     std::vector<uint32_t> stripe_b = {static_cast<uint32_t>(B.stages.size())};
     {
@@ -1599,6 +1635,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     B.wb.resize(std::max<size_t>(B.wb.size(), 24));
     up(h->copies, B.copies.data(), B.copies.size() * sizeof(uint64_t));
     h->work.alloc(16);
+    check_cuda(cudaMemsetAsync(h->work.p, 0, 16, s), "memset");
     // stripes in decreasing estimated cost: the persistent CTAs claim the big ones
     // first, so they finish together (every stripe's result is independent of
     // which CTA computes it, so the order is free)
@@ -1677,8 +1714,14 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
         h->last_launches = 1;
         return;
     }
-    check_cuda(cudaMemcpyAsync(h->xpad.p, dx, h->n_cols * 8, cudaMemcpyDeviceToDevice, s), "x copy");
+    // x slices are bulk-copied from an even index in 16-byte units: read x in
+    // place when that stays inside it (16-byte aligned, even length), else from
+    // the padded copy
+    const bool direct = dx == h->xpad.as<double>() ||
+                        (reinterpret_cast<uintptr_t>(dx) % 16 == 0 && h->n_cols % 2 == 0);
+    if (!direct) check_cuda(cudaMemcpyAsync(h->xpad.p, dx, h->n_cols * 8, cudaMemcpyDeviceToDevice, s), "x copy");
     Params p = make_params(h, alpha, beta, dy);
+    if (direct) p.x = dx;
     static const int debug_knob = [] {
         const char* e = std::getenv("HCMX_DEBUG");
         return e ? std::atoi(e) : 0;
@@ -1695,20 +1738,28 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
         return n;
     }();
-    check_cuda(cudaMemsetAsync(h->work.p, 0, 8, s), "work counters");
-    if (h->nlr && h->nstripe_a) {
-        k_phase_a<<<std::min<uint32_t>(h->nstripe_a, 2 * nsm), kThreadsA, kSmemBytes, s>>>(p);
+    // the stripe counters: phase A resets B's and B resets A's for the next
+    // product (both start at zero); a product without phase A resets here
+    const bool run_a = h->nlr && h->nstripe_a;
+    if (!run_a) check_cuda(cudaMemsetAsync(h->work.p, 0, 8, s), "work counters");
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    auto launch = [&](auto kernel, uint32_t grid, int threads, size_t smem, bool after_kernel, auto... args) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cfg.attrs = pdl;
+        cfg.numAttrs = after_kernel && !h->timing ? 1 : 0;  // events between kernels: plain launches
+        check_cuda(cudaLaunchKernelEx(&cfg, kernel, args...), "matvec launch");
         h->last_launches++;
-    }
-    if (h->nred) {
-        k_reduce<<<(h->nred + 255) / 256, 256, 0, s>>>(p, h->redcols.as<RedCol>(), h->nred);
-        h->last_launches++;
-    }
+    };
+    if (run_a) launch(k_phase_a, std::min<uint32_t>(h->nstripe_a, 2 * nsm), kThreadsA, kSmemBytes, false, p);
+    if (h->nred) launch(k_reduce, (h->nred + 255) / 256, 256, 0, true, p, h->redcols.as<RedCol>(), h->nred);
     if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
-    if (h->nblocks) {
-        k_phase_b<<<std::min<uint32_t>(h->nblocks, 2 * nsm), kThreadsB, kSmemBytes, s>>>(p);
-        h->last_launches++;
-    }
+    if (h->nblocks) launch(k_phase_b, std::min<uint32_t>(h->nblocks, 2 * nsm), kThreadsB, kSmemBytes, run_a, p);
     check_cuda(cudaGetLastError(), "matvec launch");
 #ifdef HCMX_PROF
     static const bool prof_env = std::getenv("HCMX_PROF") != nullptr;
