@@ -809,11 +809,14 @@ __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg
     } else {
         const WCol* wc = reinterpret_cast<const WCol*>(cf);  // staged records of the leaf's columns
         for (unsigned c = 0; c < nseg; ++c) {
-            const WCol q = wc[c];
-            const ColPar col{q.mask_em, q.mul_rsh, q.packed, q.sgn_sh};
-            const unsigned bit = lane * q.w;
-            b_column_full<MODE, GLO, GHI>(seg + (bit >> 5), col, q.w, bit & 31u, q.c, acc);
-            seg += (GHI - GLO) * q.w;
+            // the record as two 16-byte loads: {c, mask, mul}, {sgn, packed, w, -}
+            const uint4 q0 = reinterpret_cast<const uint4*>(wc + c)[0];
+            const uint4 q1 = reinterpret_cast<const uint4*>(wc + c)[1];
+            const ColPar col{q0.z, q0.w, q1.y, q1.x};
+            const double cc = __hiloint2double(static_cast<int>(q0.y), static_cast<int>(q0.x));
+            const unsigned w = q1.z, bit = lane * w;
+            b_column_full<MODE, GLO, GHI>(seg + (bit >> 5), col, w, bit & 31u, cc, acc);
+            seg += (GHI - GLO) * w;
         }
     }
 }
