@@ -57,27 +57,47 @@ namespace hcmx_gpu {
 namespace {
 
 constexpr int kNWB = 16;                  // phase-B consumer warps per CTA
-constexpr int kNWA = 12;                  // phase-A consumer warps (more registers per thread)
+#ifndef HCMX_NWA
+#define HCMX_NWA 8
+#endif
+#ifndef HCMX_NSTAGE
+#define HCMX_NSTAGE 3
+#endif
+#ifndef HCMX_STAGE_BYTES
+#define HCMX_STAGE_BYTES 26624
+#endif
+constexpr int kNWA = HCMX_NWA;            // phase-A consumer warps (more registers per thread)
 constexpr int kThreadsB = (kNWB + 1) * 32;  // + one producer warp (bulk copies)
 constexpr int kThreadsA = (kNWA + 1) * 32;
-constexpr int kStageBytes = 26624;        // packed data per stage
+constexpr int kStageBytes = HCMX_STAGE_BYTES;  // packed data per stage
 constexpr int kMaxItems = 32;             // items per stage (one per producer lane)
 constexpr int kItemBytes = 32;            // descriptor size (A and B)
 constexpr int kCoefBytes = 7936;          // staged coefficients + column params per stage
-constexpr int kNStage = 3;                // ring depth
+constexpr int kNStage = HCMX_NSTAGE;      // ring depth
 constexpr int kSlack = 16;                // decode reads up to 2 words past a segment
 constexpr unsigned kWaitHintNs = HCMX_WAIT_HINT;  // mbarrier try_wait suspend hint (ns)
 // A stage is one contiguous arena range, copied by ONE bulk copy into the slot:
-// [items (32 B each)][phase B: per-warp item ranges, 48 B][packed data]
+// [items (32 B each)][phase B: per-warp item ranges, 48 B][packed data]; its
+// staged coefficients (x slices, phase-A results) follow it in the same slot,
+// at the 16-byte aligned end of the stage, so a stage may trade packed data
+// for coefficients (phase A's x slices are ~1/3 of its packed bytes).  The
+// builder bakes slot-relative coefficient offsets into the items.
 constexpr int kStageMax = kMaxItems * kItemBytes + 48 + kStageBytes;
-constexpr int kOffHdr = kStageMax + kSlack;  // slot header written by the producer: stripe id, flags,
+constexpr int kSlotData = kStageMax + kSlack + kCoefBytes;  // stage + coefficients
+constexpr int kOffHdr = kSlotData;    // slot header written by the producer: stripe id, flags,
                                       // item claim counter (phase A), items
-constexpr int kOffCoef = kOffHdr + 16;
-constexpr int kSlotBytes = kOffCoef + kCoefBytes;
+constexpr int kSlotBytes = kOffHdr + 16;
 constexpr int kR = 128;               // rows per phase-B CTA
 constexpr int kG = kR / 32;           // row groups (accumulators) per lane
-constexpr int kAChunk = 256;          // X fields per A item (8 per lane)
-constexpr int kAGroup = 4;            // max rank columns per A item
+constexpr int kAChunk = 64;           // rows of a leaf's X columns per phase-A chunk
+constexpr int kARows = 4;             // rows per word-padded group of a phase-A item
+constexpr int kALanes = 32;           // rank columns per phase-A item
+constexpr int kAGroupMax = 8;         // chunks of one rank column summed in-warp
+#ifndef HCMX_AITEM
+#define HCMX_AITEM 8192
+#endif
+constexpr uint64_t kAItemBytes = HCMX_AITEM;  // packed data per phase-A item
+constexpr uint32_t kAItemXBytes = 12288;  // staged x slices per phase-A item
 constexpr int kBDenseGroup = 8;       // max dense columns per B item
 constexpr int kBLRGroup = 16;         // max rank columns per B item
 constexpr uint64_t kAStripeBytes = 8 * kStageBytes;  // target packed bytes per phase-A CTA
@@ -87,9 +107,9 @@ constexpr size_t kRingBytes = static_cast<size_t>(kNStage) * kSlotBytes;
 constexpr size_t kRedBytes = (kNWB / 2) * kR * sizeof(double);  // phase-B cross-warp reduction
 constexpr size_t kSmemBytes = kRingBytes + kRedBytes + 2 * kNStage * sizeof(uint64_t);  // + full, empty barriers
 constexpr int kCopies = 2 * kMaxItems;  // coefficient copies per stage (two per producer lane)
-// copy entry (u64): [0,32) source element index, [32,48) dst / 16 in the coef area,
-// [48,60) bytes / 16, [60,62) source table (0 x, 1 C, 2 W params, 3 X params), bit 63 valid
-static_assert(kOffHdr % 16 == 0 && kOffCoef % 16 == 0 && kSlotBytes % 16 == 0, "slot alignment");
+// copy entry (u64): [0,32) source element index, [32,48) dst / 16 in the slot,
+// [48,60) bytes / 16, [60,62) source table (0 x, 1 wcol records), bit 63 valid
+static_assert(kOffHdr % 16 == 0 && kSlotBytes % 16 == 0, "slot alignment");
 constexpr uint32_t kHdrLast = 1u, kHdrEnd = 2u, kHdrEmpty = 4u;  // slot header flags
 
 struct Stage {
@@ -136,19 +156,27 @@ struct BItem {
 };
 static_assert(sizeof(BItem) == kItemBytes, "BItem layout");
 
+// A phase-A item: up to 32 rank columns ("lanes") with the same number of rows
+// nf -- the X columns of one or more leaf chunks.  Lane l owns column l and
+// sums X_l^T x over its rows by itself (no cross-lane reduction).  The data is
+// row-interleaved: row j holds the fields of lanes 0..nl-1 back to back (row
+// width rowbits = sum of the lane widths), and every group of kARows rows is
+// padded to whole words, so a lane's field sits at the same (word, shift) in
+// every group.  Ahead of the data: one 32-bit record per lane (aligned to 16
+// bytes): w | e << 7 | m << 11 | fmt << 17 | x offset in the slot (doubles) << 19,
+// fmt 0 codec field, 1-3 uncompressed FP64 / FP32 / FP16.
 struct AItem {
-    uint32_t word_off;
-    uint8_t nseg;        // rank columns (<= kAGroup)
-    uint8_t mode;        // decode body (acase_of): 1-6 fast (2/4/8 fields per lane x mode 0/1), 0 generic
-    uint16_t nf;         // fields per column (<= kAChunk)
-    uint32_t x_off;      // staged x value of field 0 (coef-area bytes)
-    uint32_t pbase;      // partials of the leaf (nchunks > 1)
-    uint32_t xcol;       // global X column id of the first rank column
-    uint32_t leaf;       // lowrank-leaf id
-    uint16_t k;          // leaf rank
-    uint16_t nchunks;    // column chunks of the leaf
-    uint16_t chunk;      // column-chunk index within the leaf
-    uint16_t icol0;      // first rank column within the leaf
+    uint32_t word_off;   // lane records, then the data groups (words from the stage start)
+    uint16_t nf;         // rows (fields per lane)
+    uint8_t nl;          // lanes, 1..32
+    uint8_t body;        // 1: fast body (every lane w <= 32, e <= 10, codec fields), 0: generic
+    uint32_t dest0;      // lane l writes element dest0 + l (wcol record or partial)
+    uint16_t rowbits;    // bits per row (sum of the lane widths)
+    uint16_t gwords;     // words per group of kARows rows
+    uint8_t final_;      // 1: c = alpha coef (X^T x) into wcol; 0: partial sum (k_reduce)
+    uint8_t cshift;      // 2^cshift column slots; lane l = g * 2^cshift + slot holds chunk g of
+                         // its slot's rank column (the chunks are summed in-warp)
+    uint8_t pad[14];
 };
 static_assert(sizeof(AItem) == kItemBytes, "AItem layout");
 
@@ -240,27 +268,36 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
+    uint32_t ok;
 #if HCMX_WAIT_HINT > 0
     asm volatile(
         "{\n .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(kWaitHintNs)  // short suspend instead of a hot spin
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(kWaitHintNs)  // short suspend instead of a hot spin
         : "memory");
 #else
     asm volatile(
         "{\n .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
 #endif
+    return ok != 0;
 }
 
-
+// A wait that never completes (a byte count the copies do not deliver) traps
+// after ~seconds instead of hanging the device: the launch fails with an error.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    uint32_t n = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        if (++n == (1u << 26)) __trap();
+    }
+}
 
 // Programmatic dependent launch: k_reduce and k_phase_b are launched while the
 // kernel before them still runs (their CTAs take SMs as phase-A CTAs retire)
@@ -302,18 +339,18 @@ __device__ __forceinline__ double dec(const uint32_t* sp, const ColPar& c, unsig
         return __hiloint2double(__double2hiint(d) ^ ((t << c.sgn_sh) & 0x80000000u), __double2loint(d));
     } else {
         const unsigned fmt = c.packed >> 24;
-        if (fmt >= 3) {  // uncompressed words (uniform per item, so the branch is too)
-            if (fmt == 3)  // FP64 (64-bit fields are word aligned: sh == 0)
-                return __hiloint2double(static_cast<int>(sp[1]), static_cast<int>(sp[0]));
-            if (fmt == 4)  // FP32 (word aligned)
-                return static_cast<double>(__int_as_float(static_cast<int>(sp[0])));
-            // binary16 (the half.hpp:47-72 widening is exact)
-            const uint32_t t = __funnelshift_r(sp[0], sp[1], sh) & 0xffffu;
-            return static_cast<double>(__half2float(__ushort_as_half(static_cast<unsigned short>(t))));
-        }
         const unsigned w = c.packed & 0xffu, m = (c.packed >> 8) & 0xffu, e = (c.packed >> 16) & 0xffu;
         uint64_t win = ((static_cast<uint64_t>(sp[1]) << 32) | sp[0]) >> sh;
         if (w > 32 && sh + w > 64) win |= static_cast<uint64_t>(sp[2]) << (64 - sh);
+        if (fmt >= 3) {  // uncompressed words (uniform per item, so the branch is too)
+            if (fmt == 3)  // FP64
+                return __longlong_as_double(static_cast<long long>(win));
+            if (fmt == 4)  // FP32
+                return static_cast<double>(__int_as_float(static_cast<int>(static_cast<uint32_t>(win))));
+            // binary16 (the half.hpp:47-72 widening is exact)
+            const uint32_t t = static_cast<uint32_t>(win) & 0xffffu;
+            return static_cast<double>(__half2float(__ushort_as_half(static_cast<unsigned short>(t))));
+        }
         const unsigned em = e + m;
         const uint64_t sgn = (win >> em) & 1ull;
         const uint64_t fem = win & ((1ull << em) - 1);
@@ -340,6 +377,14 @@ constexpr Pow2Table make_pow2() {
     return t;
 }
 __constant__ Pow2Table c_pow2 = make_pow2();
+// phase-A fast body: 2^(21 + e) (same reason: an opaque power of two stays one
+// wide IMAD instead of a 64-bit shift pair plus a 64-bit add)
+constexpr Pow2Table make_pow2e() {
+    Pow2Table t{};
+    for (int e = 0; e < 32; ++e) t.v[e] = e <= 10 ? (1u << (21 + e)) : 0u;
+    return t;
+}
+__constant__ Pow2Table c_pow2e = make_pow2e();
 
 template <int MODE>
 __device__ __forceinline__ ColPar col_of(uint32_t packed) {
@@ -382,9 +427,9 @@ __device__ __forceinline__ void issue_copy(const Params& p, uint64_t c, uint8_t*
 
 // Stage sequence of a persistent CTA: stripes are claimed one at a time from a
 // global counter (any CTA may take any stripe; every stripe's result is the
-// same whoever computes it, so the product stays deterministic).  cur() is the
-// stage the producer issues next; the sequence is walked two stages ahead so
-// the metadata of a stage is loaded two iterations before its copies.
+// same whoever computes it, so the product stays deterministic).  A stripe is
+// claimed only when the previous one is exhausted (claiming ahead would hold
+// stripes back from idle CTAs at the tail).
 struct StageSeq {
     uint32_t stripe = 0, s = 0, e = 0;  // stage s of stripe [.., e)
     bool done = false;
@@ -407,11 +452,10 @@ __device__ __forceinline__ void seq_next(const Params& p, StageSeq& q, unsigned 
             return;
         }
         const uint4 r = (PHASE_A ? p.stripe_a : p.stripe_b)[id];
-        const uint32_t s0 = r.x, s1 = r.y;
-        if (s0 < s1 || !PHASE_A) {  // phase B visits empty row blocks too (y = beta y)
+        if (r.x < r.y || !PHASE_A) {  // phase B visits empty row blocks too (y = beta y)
             q.stripe = id;
-            q.s = s0;
-            q.e = s1;
+            q.s = r.x;
+            q.e = r.y;
             return;
         }
     }
@@ -458,9 +502,10 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
     StageSeq q;
     q.s = q.e = 0;
     seq_next<PHASE_A>(p, q, lane);
-    StageMeta m0 = seq_meta<PHASE_A>(p, q, lane);
+    StageMeta mx = seq_meta<PHASE_A>(p, q, lane);
     seq_next<PHASE_A>(p, q, lane);
-    StageMeta m1 = seq_meta<PHASE_A>(p, q, lane);
+    StageMeta my = seq_meta<PHASE_A>(p, q, lane);
+    StageMeta mz;
     const long long t_start = clk();
 #ifdef HCMX_PROF
     const unsigned long long g0 = gtime();
@@ -468,48 +513,50 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
     long long t_wait = 0;
     bool waited = false;           // phase B: griddepcontrol.wait done
     unsigned slot = 0, phase = 0;  // it % kNStage, parity of the slot's previous use
-    for (uint32_t it = 0;; ++it) {
+    uint32_t it = 0;
+    // one stage: issue `cur`, load the metadata of the stage two ahead into
+    // `ahead` (three rotating registers sets: no register copy waits on a load)
+    auto step = [&](const StageMeta& cur, StageMeta& ahead) -> bool {
         seq_next<PHASE_A>(p, q, lane);
-        const StageMeta m2 = seq_meta<PHASE_A>(p, q, lane);
+        ahead = seq_meta<PHASE_A>(p, q, lane);
         const long long t0 = clk();
         if (it >= kNStage) mbar_wait(&empty[slot], phase);
         t_wait += clk() - t0;
         uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
         if (lane == 0) {
             uint32_t* hdr = reinterpret_cast<uint32_t*>(base + kOffHdr);
-            hdr[0] = m0.stripe;
-            hdr[1] = m0.flags;
+            hdr[0] = cur.stripe;
+            hdr[1] = cur.flags;
             hdr[2] = 0u;  // item claim counter
-            hdr[3] = (m0.flags & kHdrEnd || m0.empty) ? 0u : m0.st.nitems;
+            hdr[3] = (cur.flags & kHdrEnd || cur.empty) ? 0u : cur.st.nitems;
         }
         __syncwarp();
-        if (m0.flags & kHdrEnd || m0.empty) {  // header only
+        if (cur.flags & kHdrEnd || cur.empty) {  // header only
             if (lane == 0) mbar_arrive(&full[slot]);
         } else {
             if (!PHASE_A && !waited) {
                 // the first stage that copies phase-A column coefficients (table
                 // 1) waits for phase A and k_reduce to complete; dense stages
                 // before it run while they drain
-                const bool needs_a = ((m0.c0 >> 63) && ((m0.c0 >> 60) & 3u) == 1u) ||
-                                     ((m0.c1 >> 63) && ((m0.c1 >> 60) & 3u) == 1u);
+                const bool needs_a = ((cur.c0 >> 63) && ((cur.c0 >> 60) & 3u) == 1u) ||
+                                     ((cur.c1 >> 63) && ((cur.c1 >> 60) & 3u) == 1u);
                 if (__any_sync(0xffffffffu, needs_a)) {
                     pdl_wait();
                     waited = true;
                 }
             }
-            const bool no_coef = dbg(p) >= 2, no_meta = dbg(p) >= 3;  // profiling knobs
+            const bool no_coef = dbg(p) >= 2;  // profiling knob
             if (lane == 0) {
-                (void)no_meta;
-                mbar_expect_tx(&full[slot], m0.st.bytes + (no_coef ? 0u : m0.st.coef_bytes));
-                bulk_g2s(base, p.arena + m0.st.byte_off, m0.st.bytes, &full[slot], policy);
+                mbar_expect_tx(&full[slot], cur.st.bytes + (no_coef ? 0u : cur.st.coef_bytes));
+                bulk_g2s(base, p.arena + cur.st.byte_off, cur.st.bytes, &full[slot], policy);
             }
             __syncwarp();
             if (!no_coef) {
-                issue_copy(p, m0.c0, base + kOffCoef, &full[slot]);
-                issue_copy(p, m0.c1, base + kOffCoef, &full[slot]);
+                issue_copy(p, cur.c0, base, &full[slot]);
+                issue_copy(p, cur.c1, base, &full[slot]);
             }
         }
-        if (m0.flags & kHdrEnd) {
+        if (cur.flags & kHdrEnd) {
             if (!PHASE_A && blockIdx.x == 0 && lane == 0) {
                 if (!waited) pdl_wait();
                 p.work[0] = 0u;  // phase A's stripe counter, for the next product
@@ -526,14 +573,19 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
                 atomicAdd(&g_ts[PHASE_A ? 0 : 1][3], g0 >> 8);
 #endif
             }
-            return;
+            return true;
         }
-        m0 = m1;
-        m1 = m2;
+        ++it;
         if (++slot == kNStage) {
             slot = 0;
-            if (it + 1 > kNStage) phase ^= 1u;
+            if (it > kNStage) phase ^= 1u;
         }
+        return false;
+    };
+    for (;;) {
+        if (step(mx, mz)) return;
+        if (step(my, mx)) return;
+        if (step(mz, my)) return;
     }
 }
 
@@ -618,72 +670,90 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
 }
 
 // ------------------------------------------------------------ phase A ----
-// One rank column of an A item: this lane's share of X_i^T x over the chunk.
-// U = fields per lane (nf == 32 U) known at compile time, or 0 (predicated).
-template <int MODE, int U>
-__device__ __forceinline__ double a_col(const uint32_t* seg, uint32_t pw, unsigned lane, unsigned nf,
-                                        const double (&xv)[kAChunk / 32]) {
-    const ColPar c = col_of<MODE>(pw);
-    const unsigned w = pw & 0xffu;
-    const unsigned bit = lane * w;
-    const uint32_t* sp = seg + (bit >> 5);
-    const unsigned sh = bit & 31u;
+// Fast body: every lane's field is a codec field with w <= 32 and e <= 10, the
+// item has whole row groups and every lane's x slice is 16-byte aligned.  The
+// funnel shift left-aligns the field (sign in bit 31); the exponent offset and
+// mantissa bits times 2^(21 + e) land at bits [52 - m, 52 + e) of the double,
+// so one wide IMAD with the bias 1023 << 52 rebuilds 1.mant * 2^offset
+// (codec.cpp:161-169; offset + 1023 <= 2046 needs no clamp for e <= 10).
+__device__ __forceinline__ double a_fast(const uint32_t* data, unsigned P, unsigned w, unsigned e, const double* xs,
+                                         unsigned ngroups, unsigned rowbits, unsigned gwords) {
+    const uint32_t mask = 0x7fffffffu & ~((0xffffffffu >> (w - 1)) >> 1);  // the field's e + m bits
+    const uint32_t mul = c_pow2e.v[e & 31u];
+    const uint32_t* q[kARows];
+    unsigned s[kARows];
+#pragma unroll
+    for (int r = 0; r < kARows; ++r) {
+        const unsigned top = P + r * rowbits + w;  // one past the field's sign bit
+        q[r] = data + ((top - 1) >> 5) - 1;        // the word below the one holding the sign
+        s[r] = (0u - top) & 31u;
+    }
     double acc0 = 0.0, acc1 = 0.0;
-    if (U > 0) {
+#pragma unroll 2
+    for (unsigned g = 0; g < ngroups; ++g) {
+        const double2 x01 = reinterpret_cast<const double2*>(xs)[2 * g];
+        const double2 x23 = reinterpret_cast<const double2*>(xs)[2 * g + 1];
+        const double xv[kARows] = {x01.x, x01.y, x23.x, x23.y};
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const double d = dec<MODE>(sp + u * w, c, sh);
-            if (u & 1) acc1 = fma(d, xv[u], acc1);
-            else acc0 = fma(d, xv[u], acc0);
-        }
-    } else {
-        const unsigned nu = (nf + 31) >> 5;
-#pragma unroll
-        for (int u = 0; u < kAChunk / 32; ++u) {
-            if (static_cast<unsigned>(u) < nu && lane + 32u * u < nf) acc0 = fma(dec<MODE>(sp + u * w, c, sh), xv[u], acc0);
+        for (int r = 0; r < kARows; ++r) {
+            const uint32_t t = __funnelshift_l(q[r][0], q[r][1], s[r]);
+            const uint64_t bits = static_cast<uint64_t>(t & mask) * mul + (1023ull << 52);
+            const double v = __longlong_as_double(static_cast<long long>(bits)) - 1.0;
+            const double d = __hiloint2double(__double2hiint(v) ^ static_cast<int>(t & 0x80000000u), __double2loint(v));
+            if (r & 1) acc1 = fma(d, xv[r], acc1);
+            else acc0 = fma(d, xv[r], acc0);
+            q[r] += gwords;
         }
     }
     return acc0 + acc1;
 }
 
-// the item's columns (<= kAGroup, unrolled so the sums stay in registers);
-// x of this lane's fields is loaded once per item (U known: no predication)
-template <int MODE, int U>
-__device__ __forceinline__ void a_cols(const uint32_t* pk, unsigned nseg, unsigned nf, unsigned lane,
-                                       const double* xs, double (&a)[kAGroup]) {
-    double xv[kAChunk / 32];
-#pragma unroll
-    for (int u = 0; u < kAChunk / 32; ++u) {
-        if (U > 0) xv[u] = u < U ? xs[lane + 32u * u] : 0.0;
-        else xv[u] = (lane + 32u * u < nf) ? xs[lane + 32u * u] : 0.0;
+// Generic body: any layout (e = 11, w > 32, uncompressed words), any row count,
+// any x alignment -- the mode-2 decoder per field.
+__device__ __forceinline__ double a_generic(const uint32_t* data, unsigned P, uint32_t rec, const double* xs,
+                                            unsigned nf, unsigned rowbits, unsigned gwords) {
+    const unsigned w = rec & 127u, e = (rec >> 7) & 15u, m = (rec >> 11) & 63u, fmt = (rec >> 17) & 3u;
+    ColPar c{};
+    c.packed = w | (m << 8) | (e << 16) | ((fmt ? fmt + 2u : 2u) << 24);  // 1-3: uncompressed f64 / f32 / f16
+    double acc = 0.0;
+    for (unsigned j = 0; j < nf; ++j) {
+        const unsigned bit = P + (j % kARows) * rowbits;
+        const uint32_t* sp = data + (j / kARows) * gwords + (bit >> 5);
+        acc = fma(dec<2>(sp, c, bit & 31u), xs[j], acc);
     }
-    const uint32_t* seg = pk + nseg;  // packed column layouts precede the segments
-#pragma unroll
-    for (int c = 0; c < kAGroup; ++c) {
-        if (static_cast<unsigned>(c) < nseg) {
-            const uint32_t pw = pk[c];
-            a[c] = a_col<MODE, U>(seg, pw, lane, nf, xv);
-            seg += (nf * (pw & 0xffu) + 31) >> 5;
-        }
-    }
+    return acc;
 }
 
-// Transposed warp reduction of four per-lane sums: afterwards lane 8 c holds
-// the warp total of a[c] (fixed order: deterministic).
-__device__ __forceinline__ double reduce4(const double (&a)[kAGroup], unsigned lane) {
-    static_assert(kAGroup == 4, "reduce4 assumes four columns per A item");
-    const bool up = lane & 16u;
-    double k0 = up ? a[2] : a[0], k1 = up ? a[3] : a[1];
-    const double s0 = up ? a[0] : a[2], s1 = up ? a[1] : a[3];
-    k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
-    k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
-    const bool b3 = lane & 8u;
-    double k = b3 ? k1 : k0;
-    k += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
-    k += __shfl_xor_sync(0xffffffffu, k, 4);
-    k += __shfl_xor_sync(0xffffffffu, k, 2);
-    k += __shfl_xor_sync(0xffffffffu, k, 1);
-    return k;
+__device__ __forceinline__ void a_item(const Params& p, const AItem& it, const uint8_t* slot, unsigned lane) {
+    const unsigned nl = it.nl;  // lane records
+    const uint32_t* recs = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
+    const uint32_t r0 = recs[lane < nl ? lane : 0u];
+    const bool act = lane < nl && (r0 & 127u) != 0u;
+    const uint32_t rec = act ? r0 : recs[0];  // idle lanes shadow lane 0 (results dropped)
+    const unsigned nslot = 1u << it.cshift;
+    const unsigned dest = it.dest0 + lane;      // written by the slot lanes (g == 0) only
+    double cf = 0.0;
+    if (act && lane < nslot && it.final_) cf = __ldg(p.coef + dest);  // in flight during the decode
+    // this lane's bit offset inside a row: exclusive prefix sum of the widths
+    const unsigned w = rec & 127u;
+    unsigned P = act ? w : 0u;
+#pragma unroll
+    for (unsigned o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, P, o);
+        if (lane >= o) P += v;
+    }
+    P = act ? P - w : 0u;
+    const uint32_t* data = recs + ((nl + 3u) & ~3u);
+    const double* xs = reinterpret_cast<const double*>(slot) + (rec >> 19);
+    double r = it.body ? a_fast(data, P, w, (rec >> 7) & 15u, xs, it.nf / kARows, it.rowbits, it.gwords)
+                       : a_generic(data, P, rec, xs, it.nf, it.rowbits, it.gwords);
+    // the chunks of a slot's rank column (lanes slot, slot + nslot, ...): fixed
+    // butterfly (lane `slot` gets the same order on every run); idle lanes add 0
+    if (!act) r = 0.0;
+    for (unsigned o = nslot; o < 32u; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (!act || lane >= nslot) return;
+    if (it.final_) p.wcol[dest].c = p.alpha * cf * r;
+    else p.partial[dest] = r;
 }
 
 // A leaf wider than one chunk: every chunk item writes partial sums, k_reduce
@@ -695,51 +765,40 @@ struct RedCol {
     uint32_t nchunks;
 };
 
-__device__ __forceinline__ void a_item(const Params& p, const AItem& it, const uint8_t* slot, unsigned lane) {
-    const unsigned nseg = it.nseg, nf = it.nf;
-    const unsigned cl = lane >> 3;
-    const bool writer = (lane & 7u) == 0 && cl < nseg;
-    double cf = 0.0;
-    if (writer && it.nchunks == 1) cf = __ldg(p.coef + it.xcol + cl);  // in flight during the decode
-    const double* xs = reinterpret_cast<const double*>(slot + kOffCoef + it.x_off);
-    const uint32_t* pk = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
-    double a[kAGroup];
-#pragma unroll
-    for (int c = 0; c < kAGroup; ++c) a[c] = 0.0;
-    // fast bodies for modes 0/1 at the chunk sizes 64-row leaf clusters give;
-    // mode 2 (e = 11 or w > 32) and ragged chunks take one generic body (the
-    // mode-2 decoder is exact for every layout; keeps the kernel small)
-    switch (it.mode) {  // the body index, precomputed by acase_of
-        case 3: a_cols<0, 8>(pk, nseg, nf, lane, xs, a); break;
-        case 2: a_cols<0, 4>(pk, nseg, nf, lane, xs, a); break;
-        case 1: a_cols<0, 2>(pk, nseg, nf, lane, xs, a); break;
-        case 6: a_cols<1, 8>(pk, nseg, nf, lane, xs, a); break;
-        case 5: a_cols<1, 4>(pk, nseg, nf, lane, xs, a); break;
-        case 4: a_cols<1, 2>(pk, nseg, nf, lane, xs, a); break;
-        default:
-            a_cols<2, 0>(pk, nseg, nf, lane, xs, a);  // also uncompressed words (modes 3-5)
-            break;
-    }
-    const double r = reduce4(a, lane);
-    if (!writer) return;
-    if (it.nchunks == 1) p.wcol[it.xcol + cl].c = p.alpha * cf * r;
-    else p.partial[it.pbase + static_cast<uint32_t>(it.chunk) * it.k + it.icol0 + cl] = r;
-}
-
-__global__ void k_reduce(Params p, const RedCol* rc, uint32_t n) {
+// Chunk partials -> c_i = alpha coef_i sum_ch partial.  Columns with many
+// chunks (the first nlong entries) take one warp each: lane j adds chunks j,
+// j + 32, ... and a fixed butterfly finishes the sum (lane 0's order is the
+// same on every run).  The rest take one thread each with independent loads.
+constexpr uint32_t kRedLong = 16;  // chunks from which a column gets a warp
+__global__ void k_reduce(Params p, const RedCol* rc, uint32_t nlong, uint32_t n) {
     pdl_trigger();
     pdl_wait();  // the partials of phase A
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t long_blocks = (nlong + 7) / 8;
+    if (blockIdx.x < long_blocks) {
+        const uint32_t i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31u;
+        if (i >= nlong) return;
         const RedCol r = rc[i];
-        double s[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains, fixed order
-        uint32_t ch = 0;
-        for (; ch + 4 <= r.nchunks; ch += 4) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) s[q] += p.partial[r.p0 + (ch + q) * r.stride];
+        double s0 = 0.0, s1 = 0.0;
+        uint32_t ch = lane;
+        for (; ch + 32 < r.nchunks; ch += 64) {
+            s0 += p.partial[r.p0 + ch * r.stride];
+            s1 += p.partial[r.p0 + (ch + 32) * r.stride];
         }
-        for (; ch < r.nchunks; ++ch) s[ch & 3u] += p.partial[r.p0 + ch * r.stride];
-        p.wcol[r.col].c = p.alpha * p.coef[r.col] * ((s[0] + s[1]) + (s[2] + s[3]));
+        if (ch < r.nchunks) s0 += p.partial[r.p0 + ch * r.stride];
+        double s = s0 + s1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) p.wcol[r.col].c = p.alpha * p.coef[r.col] * s;
+        return;
     }
+    const uint32_t i = nlong + (blockIdx.x - long_blocks) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const RedCol r = rc[i];
+    double s[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains, fixed order
+#pragma unroll
+    for (uint32_t ch = 0; ch < kRedLong; ++ch)
+        if (ch < r.nchunks) s[ch & 3u] += p.partial[r.p0 + ch * r.stride];
+    p.wcol[r.col].c = p.alpha * p.coef[r.col] * ((s[0] + s[1]) + (s[2] + s[3]));
 }
 
 // ------------------------------------------------------------ phase B ----
@@ -823,7 +882,7 @@ __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg
 
 __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const uint8_t* slot, unsigned lane,
                                        double (&acc)[kG]) {
-    const double* cf = reinterpret_cast<const double*>(slot + kOffCoef + it.coef_off);
+    const double* cf = reinterpret_cast<const double*>(slot + it.coef_off);
     const double dmul = p.alpha * it.scale;  // dense: alpha * buffer scale folded into x
     const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
     // fast bodies for modes 0/1 at the shapes 64-row leaf clusters produce;
@@ -956,6 +1015,45 @@ void copy_bits(const uint8_t* src, uint64_t len, uint64_t bit, uint64_t nbits, u
 struct SegRef {  // where a run of a buffer's fields landed in the arena (export)
     uint64_t word;  // arena word index
     uint32_t f0, nf;
+    // phase-A items (gwords > 0): field j at bit (j / kARows) * 32 gwords +
+    // pbit + (j % kARows) * rowbits from `word`; else the fields are contiguous
+    uint32_t pbit;
+    uint16_t rowbits, gwords;
+};
+
+// w (<= 64) bits at bit offset `bit` of the LSB-first stream src[0, len)
+// (bytes past len read as 0)
+uint64_t get_bits(const uint8_t* src, uint64_t len, uint64_t bit, unsigned w) {
+    const uint64_t byte = bit >> 3;
+    uint8_t tmp[16] = {};
+    if (byte + 16 <= len) std::memcpy(tmp, src + byte, 16);
+    else if (byte < len) std::memcpy(tmp, src + byte, static_cast<size_t>(len - byte));
+    unsigned __int128 v;
+    std::memcpy(&v, tmp, 16);
+    const uint64_t r = static_cast<uint64_t>(v >> (bit & 7));
+    return w >= 64 ? r : (r & ((1ull << w) - 1));
+}
+
+// OR the low w bits of v into the word stream dst at bit offset `bit`
+void put_bits(uint32_t* dst, uint64_t bit, uint64_t v, unsigned w) {
+    while (w) {
+        const unsigned sh = static_cast<unsigned>(bit & 31), take = std::min(32u - sh, w);
+        const uint64_t part = take == 64 ? v : (v & ((1ull << take) - 1));
+        dst[bit >> 5] |= static_cast<uint32_t>(part << sh);
+        v = take >= 64 ? 0 : v >> take;
+        bit += take;
+        w -= take;
+    }
+}
+
+// one lane of a phase-A item: fields [f0, f0 + nf) of codec buffer `buf`
+// (a chunk of one X column), x elements [xidx, xidx + nf).  Lanes come in
+// segments of G (a power of two) chunks of one rank column, summed in-warp
+// into result element `dest` (wcol record if final_, else a partial); g is
+// the lane's place in its segment.
+struct ALane {
+    uint64_t buf, f0;
+    uint32_t nf, xidx, dest, final_, G, g;
 };
 
 }  // namespace
@@ -967,7 +1065,7 @@ struct hcmx_hmat {
     uint64_t n_rows = 0, n_cols = 0, rb = 0, re = 0;
     DevBuf arena, stages, stripe_a, stripe_b, copies, work, wcol, coef, partial,
         redcols, xpad, xbuf, ybuf;
-    uint32_t nstripe_a = 0, nblocks = 0, nlr = 0, nred = 0;
+    uint32_t nstripe_a = 0, nblocks = 0, nlr = 0, nred = 0, nred_long = 0;
     hcmx_memory_report report{};
     std::vector<std::vector<SegRef>> segs;  // per buffer (export); empty if too big
     std::vector<hcmx_descriptor> desc;
@@ -1044,13 +1142,6 @@ uint8_t bcase_of(uint64_t ra, uint64_t nr, unsigned mode) {
     return static_cast<uint8_t>((f == 0x04 ? 1 : f == 0x02 ? 2 : 3) + 3 * mode);
 }
 
-// phase-A body index: fields per lane 2 / 4 / 8 (64 / 128 / 256-field chunks) x
-// decode mode 0 / 1 -> 1-6; anything else 0 (the generic body)
-uint8_t acase_of(uint64_t nf, unsigned mode) {
-    const unsigned ui = nf == 256 ? 3u : nf == 128 ? 2u : nf == 64 ? 1u : 0u;
-    return static_cast<uint8_t>(mode >= 2 || ui == 0 ? 0u : ui + 3u * mode);
-}
-
 inline uint32_t r16(uint64_t x) { return static_cast<uint32_t>((x + 15) & ~uint64_t(15)); }
 
 // A run of fields of one codec buffer that an item needs (copied word aligned)
@@ -1101,7 +1192,6 @@ struct Builder {
     std::vector<Stage> stages;
     std::vector<uint16_t> wb;     // phase B: 24 entries per stage (NW + 1 used)
     std::vector<BItem> bitems;
-    std::vector<AItem> aitems;
     std::vector<Seg> segs;
     std::vector<uint64_t> copies;  // kCopies per stage
 
@@ -1111,6 +1201,15 @@ struct Builder {
     }
 
     Builder(const hcmx_hmat_desc& dd, hcmx_hmat* hh) : d(dd), h(hh) {}
+
+    // the bytes a stage's copies deliver must be exactly what its full barrier
+    // expects, or the consumers would wait forever
+    void check_copies(size_t c0, uint32_t expect) const {
+        uint64_t sum = 0;
+        for (size_t q = c0; q < c0 + kCopies; ++q)
+            if (copies[q] >> 63) sum += ((copies[q] >> 48) & 0xfffu) * 16u;
+        if (sum != expect) throw std::logic_error("hmat: stage copy bytes mismatch");
+    }
 
     unsigned width(uint64_t b) const { return d.desc[b].bit_width; }
     uint64_t words_of(uint64_t b, uint64_t nf) const { return (nf * width(b) + 31) / 32; }
@@ -1170,7 +1269,7 @@ struct Builder {
             uint32_t table, start, end, off;  // [start, end) elements; start even for table 0
         };
         std::vector<Slice> slices;
-        uint32_t coef = 0;
+        uint32_t coef = 0, data_bytes = 0;
         auto esize = [](uint32_t table) { return table == 0 ? 8u : static_cast<uint32_t>(sizeof(WCol)); };
         auto slice_bytes = [&](const Slice& s) { return r16((s.end - s.start) * esize(s.table)); };
         std::vector<size_t> cut = {pos, end};
@@ -1221,6 +1320,11 @@ struct Builder {
                 }
             }
             slices.swap(merged);
+            // the coefficients follow the stage in the slot (slot-relative offsets)
+            size_t data_words = (built.size() * (kItemBytes / 4) + (NW > 0 ? 12 : 0) + 3) & ~size_t(3);
+            for (const Built& b : built) data_words += b.words;
+            data_bytes = static_cast<uint32_t>(((data_words + 3) & ~size_t(3)) * 4);
+            coef = data_bytes;
             for (Slice& s : slices) {
                 s.off = coef;
                 coef += slice_bytes(s);
@@ -1238,7 +1342,7 @@ struct Builder {
                 }
             }
         }
-        if (built.size() > static_cast<size_t>(kMaxItems) || coef > static_cast<uint32_t>(kCoefBytes) ||
+        if (built.size() > static_cast<size_t>(kMaxItems) || coef > static_cast<uint32_t>(kSlotData) ||
             slices.size() > static_cast<size_t>(kCopies)) {
             if (end - pos == 1) throw invalid_argument("hmat: column exceeds a stage");
             return false;
@@ -1290,8 +1394,215 @@ struct Builder {
             }
         }
         st.pad = cost;
-        st.coef_bytes = coef;
+        if (st.bytes != data_bytes) throw std::logic_error("hmat: stage size");
+        st.coef_bytes = coef - data_bytes;
+        check_copies(c0, st.coef_bytes);
         stages.push_back(st);
+        return true;
+    }
+
+    // ---- phase A --------------------------------------------------------
+    uint64_t a_items = 0;
+
+    struct AIt {
+        size_t l0, nl;
+        uint32_t rowbits, gwords, ngroups;
+        uint64_t bytes;  // lane records + data, 16-byte aligned
+    };
+
+    // A stripe's lanes -> items (<= kALanes lanes with one row count, one
+    // result kind and consecutive result elements, <= kAItemBytes of data) ->
+    // stages.
+    void emit_stripe_a(const std::vector<ALane>& lanes) {
+        std::vector<AIt> its;
+        for (size_t i = 0; i < lanes.size();) {
+            // whole segments only; one row count, result kind and segment size;
+            // consecutive results
+            // the x slices the item needs must fit one stage's coefficient area
+            uint32_t rb = 0, xbytes = 0, nslices = 0;
+            size_t j = i;
+            while (j < lanes.size()) {
+                const ALane& L = lanes[j];
+                const size_t seg = L.G;
+                if (j + seg - i > static_cast<size_t>(kALanes)) break;
+                if (j > i && (L.nf != lanes[i].nf || L.final_ != lanes[i].final_ || L.G != lanes[i].G ||
+                              L.dest != lanes[j - 1].dest + 1))
+                    break;
+                uint32_t sb = 0, xb = 0, ns = 0;
+                for (size_t q = j; q < j + seg; ++q) {
+                    sb += width(lanes[q].buf);
+                    bool seen = false;  // x slice already counted for this item
+                    for (size_t u = i; u < q && !seen; ++u) seen = lanes[u].xidx == lanes[q].xidx && lanes[u].nf == lanes[q].nf;
+                    if (!seen) {
+                        xb += r16((lanes[q].nf + 2) * 8ull);
+                        ++ns;
+                    }
+                }
+                if (j > i && (static_cast<uint64_t>(rb + sb) * L.nf > 8 * kAItemBytes ||
+                              xbytes + xb > kAItemXBytes || nslices + ns > static_cast<uint32_t>(kCopies)))
+                    break;
+                rb += sb;
+                xbytes += xb;
+                nslices += ns;
+                j += seg;
+            }
+            AIt t{};
+            t.l0 = i;
+            t.nl = j - i;
+            t.rowbits = rb;
+            t.gwords = (kARows * rb + 31) / 32;
+            t.ngroups = (lanes[i].nf + kARows - 1) / kARows;
+            const size_t nrec = lanes[i].G == 1 ? t.nl : static_cast<size_t>(kALanes);  // lane records
+            t.bytes = r16(4 * (((nrec + 3) & ~size_t(3)) + static_cast<uint64_t>(t.ngroups) * t.gwords));
+            if (rb >= (1u << 16) || t.gwords >= (1u << 16)) throw invalid_argument("hmat: phase-A item too wide");
+            its.push_back(t);
+            i = j;
+        }
+        for (size_t pos = 0; pos < its.size();) {
+            size_t end = pos;
+            uint64_t bytes = 0;
+            while (end < its.size() && end - pos < static_cast<size_t>(kMaxItems) &&
+                   bytes + its[end].bytes + kItemBytes * (end - pos + 1) <= static_cast<uint64_t>(kStageMax))
+                bytes += its[end++].bytes;
+            if (end == pos) throw invalid_argument("hmat: phase-A item exceeds a stage");
+            while (!try_stage_a(lanes, its, pos, end)) {  // too many x slices: one item fewer
+                if (end - pos == 1) throw invalid_argument("hmat: phase-A item exceeds a stage");
+                --end;
+            }
+            pos = end;
+        }
+    }
+
+    bool try_stage_a(const std::vector<ALane>& lanes, std::vector<AIt>& its, size_t pos, size_t end) {
+        // x slices of the stage's lanes, merged like phase B's coefficient ranges
+        // Lanes of a chunk segment (G > 1) read G different x chunks in the same
+        // step: each chunk gets its own slice, 16 bytes apart modulo 128, so
+        // their LDS.128 hit different banks (merged ranges would put them 512 B
+        // apart: one bank group).  Other slices merge as in phase B.
+        struct Slice {
+            uint32_t start, end, off, pad;
+        };
+        std::vector<Slice> sl;
+        for (size_t t = pos; t < end; ++t)
+            for (size_t q = its[t].l0; q < its[t].l0 + its[t].nl; ++q) {
+                const ALane& L = lanes[q];
+                const uint32_t pad = L.G > 1 ? 1u : 0u;
+                const Slice x{pad ? L.xidx : (L.xidx & ~1u), L.xidx + L.nf, 0, pad};
+                bool dup = false;
+                for (size_t u = sl.size(); u-- > 0 && !dup && sl.size() - u <= 8;)
+                    dup = sl[u].start == x.start && sl[u].end == x.end && sl[u].pad == x.pad;
+                if (!dup) sl.push_back(x);
+            }
+        std::sort(sl.begin(), sl.end(), [](const Slice& a2, const Slice& b2) {
+            return a2.start != b2.start ? a2.start < b2.start : a2.pad < b2.pad;
+        });
+        std::vector<Slice> merged;
+        for (const Slice& x : sl) {
+            if (!merged.empty() && merged.back().start == x.start && merged.back().end == x.end && merged.back().pad == x.pad)
+                continue;
+            if (!x.pad && !merged.empty() && !merged.back().pad && x.start <= merged.back().end + 32u)
+                merged.back().end = std::max(merged.back().end, x.end);
+            else
+                merged.push_back(x);
+        }
+        // the x slices follow the stage in the slot (slot-relative offsets)
+        uint32_t data_bytes = static_cast<uint32_t>((end - pos) * kItemBytes);
+        for (size_t t = pos; t < end; ++t) data_bytes += static_cast<uint32_t>(its[t].bytes);
+        uint32_t coef = data_bytes, copied = 0;  // slot bytes used / bytes the copies bring
+        for (Slice& x : merged) {
+            if (x.pad && (x.start & 1u)) {  // bulk copies start at an even element
+                x.start -= 1;
+            }
+            x.off = coef;
+            copied += r16((x.end - x.start) * 8ull);
+            coef += r16((x.end - x.start) * 8ull) + (x.pad ? 16u : 0u);
+        }
+        if (coef > static_cast<uint32_t>(kSlotData) || merged.size() > static_cast<size_t>(kCopies)) return false;
+        auto xoff = [&](const ALane& L) -> uint32_t {  // coef-area offset of x[xidx], in doubles
+            const uint32_t pad = L.G > 1 ? 1u : 0u;
+            for (const Slice& x : merged)
+                if (x.pad == pad && x.start <= L.xidx && L.xidx + L.nf <= x.end) return x.off / 8 + (L.xidx - x.start);
+            throw std::logic_error("hmat: x slice");
+        };
+        // descriptors largest first (warps claim a stage's items in order)
+        std::vector<size_t> ord;
+        for (size_t t = pos; t < end; ++t) ord.push_back(t);
+        std::stable_sort(ord.begin(), ord.end(), [&](size_t a2, size_t b2) { return its[a2].bytes > its[b2].bytes; });
+        const size_t c0 = copies.size();
+        copies.resize(c0 + kCopies, 0);
+        for (size_t q = 0; q < merged.size(); ++q)
+            copies[c0 + q] = copy_entry(merged[q].start, merged[q].off, r16((merged[q].end - merged[q].start) * 8ull), 0);
+        while (arena.size() % 4) arena.push_back(0u);
+        const uint64_t start = arena.size();
+        arena.resize(start + ord.size() * (kItemBytes / 4), 0u);
+        uint64_t cost = 0;
+        for (size_t n = 0; n < ord.size(); ++n) {
+            const AIt& t = its[ord[n]];
+            AItem it{};
+            it.word_off = static_cast<uint32_t>(arena.size() - start);
+            it.nf = static_cast<uint16_t>(lanes[t.l0].nf);
+            it.nl = static_cast<uint8_t>(t.nl);
+            it.dest0 = lanes[t.l0].dest;
+            it.rowbits = static_cast<uint16_t>(t.rowbits);
+            it.gwords = static_cast<uint16_t>(t.gwords);
+            it.final_ = static_cast<uint8_t>(lanes[t.l0].final_);
+            const uint32_t G = lanes[t.l0].G, C = static_cast<uint32_t>(kALanes) / G;
+            it.cshift = static_cast<uint8_t>(__builtin_ctz(G == 1 ? static_cast<uint32_t>(kALanes) : C));
+            const size_t nrec = G == 1 ? t.nl : static_cast<size_t>(kALanes);
+            it.nl = static_cast<uint8_t>(nrec);
+            // physical lane l <- segment l % C, chunk l / C (G > 1): one 8-lane
+            // shared-memory phase of the x loads reads two x chunks, not eight
+            auto src_of = [&](size_t l) -> long {
+                if (G == 1) return static_cast<long>(t.l0 + l);
+                const size_t sg = l % C, g = l / C;
+                return sg * G < t.nl ? static_cast<long>(t.l0 + sg * G + g) : -1L;
+            };
+            bool fast = it.nf % kARows == 0;
+            const uint64_t rec0 = arena.size();
+            arena.resize(rec0 + ((nrec + 3) & ~size_t(3)), 0u);
+            const uint64_t data0 = arena.size();
+            arena.resize(data0 + static_cast<uint64_t>(t.ngroups) * t.gwords, 0u);
+            uint32_t P = 0;
+            for (size_t q = 0; q < nrec; ++q) {
+                const long li = src_of(q);
+                if (li < 0) continue;  // idle lane: record 0
+                const ALane& L = lanes[static_cast<size_t>(li)];
+                const hcmx_descriptor& x = d.desc[L.buf];
+                const unsigned w = x.bit_width, e = x.exp_bits, m = x.mant_bits;
+                const unsigned fmt = x.scheme >= HCMX_RAW_F64 ? 3u + (x.scheme - HCMX_RAW_F64) : 0u;
+                const uint32_t xo = xoff(L);
+                if (xo >= 8192u || w > 64) throw std::logic_error("hmat: phase-A lane record");
+                fast = fast && fmt == 0 && w <= 32 && e <= 10 && w == 1 + e + m && xo % 2 == 0;
+                arena[rec0 + q] = w | (e << 7) | ((fmt ? 0u : m) << 11) | ((fmt ? fmt - 2u : 0u) << 17) | (xo << 19);
+                const uint8_t* src = blob + d.poff[L.buf];
+                const uint64_t len = static_cast<uint64_t>(d.plen[L.buf]);
+                for (uint32_t j = 0; j < L.nf; ++j) {
+                    const uint64_t v = get_bits(src, len, (L.f0 + j) * w, w);
+                    put_bits(arena.data() + data0,
+                             static_cast<uint64_t>(j / kARows) * t.gwords * 32 + P + (j % kARows) * t.rowbits, v, w);
+                }
+                if (keep_map)
+                    h->segs[L.buf].push_back({data0, static_cast<uint32_t>(L.f0), L.nf, P,
+                                              static_cast<uint16_t>(t.rowbits), static_cast<uint16_t>(t.gwords)});
+                P += w;
+            }
+            it.body = fast ? 1 : 0;
+            std::memcpy(arena.data() + start + n * (kItemBytes / 4), &it, kItemBytes);
+            while (arena.size() % 4) arena.push_back(0u);
+            cost += 60 + 40ull * t.ngroups * (fast ? 1 : 3);  // ~warp instructions
+        }
+        while (arena.size() % 4) arena.push_back(0u);
+        Stage st{};
+        st.item0 = static_cast<uint32_t>(a_items);
+        st.byte_off = start * 4;
+        st.bytes = static_cast<uint32_t>((arena.size() - start) * 4);
+        st.nitems = static_cast<uint32_t>(ord.size());
+        st.pad = cost;
+        if (st.bytes != data_bytes) throw std::logic_error("hmat: phase-A stage size");
+        st.coef_bytes = copied;  // what the copies complete on the barrier (expect_tx)
+        check_copies(c0, copied);
+        stages.push_back(st);
+        a_items += ord.size();
         return true;
     }
 };
@@ -1387,12 +1698,13 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         return {static_cast<uint64_t>(d.buf0[l] + d.rank[l] + i), 0};
     };
 
-    // per-leaf tables
+    // per-leaf tables; rank-column ids (wcol / coef) and partial ranges are
+    // assigned by the phase-A layout below, in the order its items' lanes take
     std::vector<int64_t> lr_id(d.nleaves, -1);
     std::vector<LeafA> leafa;
-    std::vector<WCol> wcol;
-    std::vector<double> coef;
+    std::vector<uint64_t> lr_leaf;  // leaf index of each lowrank leaf
     uint64_t npartial = 0;
+    uint32_t ncols = 0;
     std::vector<RedCol> redcols;
     hcmx_memory_report& rep = h->report;
     rep = hcmx_memory_report{};
@@ -1409,22 +1721,12 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         } else {
             const uint32_t k = static_cast<uint32_t>(d.rank[l]);
             lr_id[l] = static_cast<int64_t>(leafa.size());
-            if (wcol.size() % 2) {  // even column bases (x-style 16-byte alignment of coef)
-                wcol.push_back(WCol{});
-                coef.push_back(0.0);
-            }
             LeafA L{};
-            L.colbase = static_cast<uint32_t>(wcol.size());
             L.k = k;
             L.nchunks = static_cast<uint32_t>((cols + kAChunk - 1) / kAChunk);
             if (k >= (1u << 16) || L.nchunks >= (1u << 16)) throw invalid_argument("hmat: lowrank leaf too large");
-            L.pbase = static_cast<uint32_t>(npartial);
-            if (L.nchunks > 1) {
-                for (uint32_t i = 0; i < k; ++i)
-                    redcols.push_back({L.colbase + i, static_cast<uint32_t>(npartial) + i, k, L.nchunks});
-                npartial += static_cast<uint64_t>(L.nchunks) * k;
-            }
             leafa.push_back(L);
+            lr_leaf.push_back(l);
             const bool uniform = d.kind[l] == 2;  // CodecLowrank: one U and one V buffer, sigma = 1
             uint64_t bytes = uniform ? 4 : 8 + 8ull * k;  // APLRLowrank::byte_size (mixedprec.cpp:210-217)
             if (uniform && k > 0) {
@@ -1436,17 +1738,12 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                     rep.algorithmic_bytes += hdr + payload_bytes(n, x.bit_width);
                 }
             }
-            for (uint32_t i = 0; i < k; ++i) {
+            for (uint32_t i = 0; i < k && !uniform; ++i) {
                 const hcmx_descriptor& xw = d.desc[wbuf(l, i).first];
                 const hcmx_descriptor& xx = d.desc[xbuf(l, i).first];
-                const ColPar cp = col_par(xw);
-                wcol.push_back({0.0, cp.mask_em, cp.mul_rsh, cp.sgn_sh, cp.packed, xw.bit_width, 0u});
-                coef.push_back((uniform ? 1.0 : d.sigma[d.sig0[l] + i]) * xx.scale * xw.scale);
-                if (!uniform) {
-                    const uint64_t hdr = xw.scheme >= HCMX_RAW_F64 ? 0 : 20;
-                    bytes += 2 * hdr + d.plen[d.buf0[l] + i] + d.plen[d.buf0[l] + k + i];
-                    rep.algorithmic_bytes += 2 * hdr + payload_bytes(rows, xw.bit_width) + payload_bytes(cols, xx.bit_width);
-                }
+                const uint64_t hdr = xw.scheme >= HCMX_RAW_F64 ? 0 : 20;
+                bytes += 2 * hdr + d.plen[d.buf0[l] + i] + d.plen[d.buf0[l] + k + i];
+                rep.algorithmic_bytes += 2 * hdr + payload_bytes(rows, xw.bit_width) + payload_bytes(cols, xx.bit_width);
             }
             if (!uniform) rep.algorithmic_bytes += 8ull * k;
             rep.lowrank_leaves++;
@@ -1456,74 +1753,101 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     }
     rep.algorithmic_bytes += 8ull * d.n_cols + 8ull * (h->re - h->rb);
     h->nlr = static_cast<uint32_t>(leafa.size());
-    for (int pad = 0; pad < 4; ++pad) {  // bulk copies may round up past the last column
-        wcol.push_back(WCol{});
-        coef.push_back(0.0);
-    }
 
-    // ---- phase A: items (leaf, <= 128 columns of the block, <= 4 rank columns),
-    // stripes of ~kAStripeBytes, one chunk (all its rank-column groups) per warp
+    // ---- phase A: stripes of ~kAStripeBytes of X factors.  In a stripe, the
+    // leaves that fit one chunk come first, grouped by width (so lanes of
+    // several leaves fill an item and write consecutive wcol records), then the
+    // chunked leaves, whose lanes run over (chunk, rank column) and write
+    // consecutive partials.
     uint32_t nstripe_a = 0;
     std::vector<uint32_t> stripe_a = {0};
     {
-        std::vector<Spec<AItem>> specs;
-        uint64_t stripe_bytes = 0, unit = 0;
+        std::vector<uint32_t> pend;  // lowrank ids of the current stripe
+        uint64_t stripe_bytes = 0;
+        std::vector<ALane> lanes;
         auto flush = [&]() {
-            if (specs.empty()) return;
-            B.emit_stripe<AItem, kAGroup, 0>(specs, B.aitems);
+            if (pend.empty()) return;
+            lanes.clear();
+            std::vector<uint32_t> single, chunked;
+            for (uint32_t id : pend) (leafa[id].nchunks == 1 ? single : chunked).push_back(id);
+            auto cols_of = [&](uint32_t id) { return d.col1[lr_leaf[id]] - d.col0[lr_leaf[id]]; };
+            std::stable_sort(single.begin(), single.end(), [&](uint32_t a2, uint32_t b2) { return cols_of(a2) < cols_of(b2); });
+            for (uint32_t id : single) {
+                LeafA& L = leafa[id];
+                const uint64_t l = lr_leaf[id];
+                L.colbase = ncols;
+                ncols += L.k;
+                for (uint32_t i = 0; i < L.k; ++i) {
+                    const auto xb = xbuf(l, i);
+                    lanes.push_back({xb.first, xb.second, static_cast<uint32_t>(cols_of(id)),
+                                     static_cast<uint32_t>(d.col0[l]), L.colbase + i, 1, 1, 0});
+                }
+            }
+            for (uint32_t id : chunked) {
+                // whole 64-row chunks in groups of G (a power of two <= kAGroupMax
+                // dividing their count) summed in-warp; a ragged last chunk is a
+                // group of its own.  One group: the result is final.
+                LeafA& L = leafa[id];
+                const uint64_t l = lr_leaf[id];
+                const uint64_t cols = static_cast<uint64_t>(cols_of(id));
+                const uint32_t nfull = static_cast<uint32_t>(cols / kAChunk), rag = static_cast<uint32_t>(cols % kAChunk);
+                uint32_t G = 1;
+                while (2 * G <= static_cast<uint32_t>(kAGroupMax) && nfull % (2 * G) == 0) G *= 2;
+                const uint32_t ngrp = nfull / G + (rag ? 1u : 0u);
+                L.colbase = ncols;
+                ncols += L.k;
+                L.nchunks = ngrp;
+                const uint32_t fin = ngrp == 1 ? 1u : 0u;
+                if (!fin) {
+                    L.pbase = static_cast<uint32_t>(npartial);
+                    for (uint32_t i = 0; i < L.k; ++i) redcols.push_back({L.colbase + i, L.pbase + i, L.k, ngrp});
+                    npartial += static_cast<uint64_t>(ngrp) * L.k;
+                }
+                for (uint32_t grp = 0; grp < ngrp; ++grp) {
+                    const bool ragged = grp * G >= nfull;
+                    const uint32_t gs = ragged ? 1u : G;
+                    for (uint32_t i = 0; i < L.k; ++i) {
+                        const auto xb = xbuf(l, i);
+                        const uint32_t dest = fin ? L.colbase + i : L.pbase + grp * L.k + i;
+                        for (uint32_t g = 0; g < gs; ++g) {
+                            const uint64_t f0 = static_cast<uint64_t>(ragged ? nfull : grp * G + g) * kAChunk;
+                            const uint32_t nf = ragged ? rag : static_cast<uint32_t>(kAChunk);
+                            lanes.push_back({xb.first, xb.second + f0, nf, static_cast<uint32_t>(d.col0[l] + f0), dest,
+                                             fin, gs, g});
+                        }
+                    }
+                }
+            }
+            if (npartial >= (1ull << 32) || ncols >= (1u << 31)) throw invalid_argument("hmat: too many rank columns");
+            B.emit_stripe_a(lanes);
             stripe_a.push_back(static_cast<uint32_t>(B.stages.size()));
             ++nstripe_a;
-            specs.clear();
+            pend.clear();
             stripe_bytes = 0;
         };
         for (uint64_t l : leaves) {
             if (d.kind[l] == 0) continue;
-            const LeafA& L = leafa[lr_id[l]];
-            const int64_t cols = d.col1[l] - d.col0[l];
-            for (uint32_t ch = 0; ch < L.nchunks; ++ch, ++unit) {
-                const uint64_t f0 = static_cast<uint64_t>(ch) * kAChunk;
-                const uint64_t nf = std::min<uint64_t>(kAChunk, cols - f0);
-                const auto groups = column_groups(L.k, 1, [&](uint32_t i) { return B.words_of(xbuf(l, i).first, nf); });
-                for (const auto& gr : groups) {
-                    const uint32_t g = gr.first, ng = gr.second;
-                    Spec<AItem> sp{};
-                    sp.seg0 = static_cast<uint32_t>(B.segs.size());
-                    sp.nseg = ng;
-                    for (uint32_t i = g; i < g + ng; ++i) {
-                        const auto xb = xbuf(l, i);
-                        B.segs.push_back({xb.first, xb.second + f0, nf});
-                        sp.words += B.words_of(xb.first, nf);
-                    }
-                    AItem& it = sp.it;
-                    it.nseg = static_cast<uint8_t>(ng);
-                    it.nf = static_cast<uint16_t>(nf);
-                    const uint32_t xidx = static_cast<uint32_t>(d.col0[l] + f0);
-                    it.xcol = L.colbase + g;
-                    it.leaf = static_cast<uint32_t>(lr_id[l]);
-                    it.chunk = static_cast<uint16_t>(ch);
-                    it.icol0 = static_cast<uint16_t>(g);
-                    it.k = static_cast<uint16_t>(L.k);
-                    it.nchunks = static_cast<uint16_t>(L.nchunks);
-                    it.pbase = L.pbase;
-                    sp.words += ng;  // packed column layout word
-                    sp.param = col_par(d.desc[xbuf(l, g).first]).packed;
-                    const unsigned mode = sp.param >> 24;
-                    it.mode = acase_of(nf, mode);
-                    sp.elem = xidx;
-                    sp.sl_table = 0;  // x slice of the chunk
-                    sp.sl_start = xidx;
-                    sp.sl_count = static_cast<uint32_t>(nf);
-                    sp.cost = nf * ng;
-                    sp.unit = unit * 8 + mode;  // items never mix decode modes
-                    sp.xidx = xidx;
-                    sp.nf = static_cast<uint32_t>(nf);
-                    stripe_bytes += sp.words * 4;
-                    specs.push_back(sp);
-                }
-                if (stripe_bytes >= kAStripeBytes) flush();
-            }
+            const uint32_t id = static_cast<uint32_t>(lr_id[l]);
+            pend.push_back(id);
+            for (uint32_t i = 0; i < leafa[id].k; ++i)
+                stripe_bytes += B.words_of(xbuf(l, i).first, d.col1[l] - d.col0[l]) * 4;
+            if (stripe_bytes >= kAStripeBytes) flush();
         }
         flush();
+    }
+    // rank-column tables in the order phase A assigned
+    std::vector<WCol> wcol(ncols + 4);  // + 4: bulk copies may round up past the last column
+    std::vector<double> coef(ncols + 4, 0.0);
+    for (uint32_t id = 0; id < leafa.size(); ++id) {
+        const uint64_t l = lr_leaf[id];
+        const bool uniform = d.kind[l] == 2;
+        for (uint32_t i = 0; i < leafa[id].k; ++i) {
+            const hcmx_descriptor& xw = d.desc[wbuf(l, i).first];
+            const hcmx_descriptor& xx = d.desc[xbuf(l, i).first];
+            const ColPar cp = col_par(xw);
+            wcol[leafa[id].colbase + i] = {0.0, cp.mask_em, cp.mul_rsh, cp.sgn_sh, cp.packed, xw.bit_width, 0u};
+            coef[leafa[id].colbase + i] = (uniform ? 1.0 : d.sigma[d.sig0[l] + i]) * xx.scale * xw.scale;
+        }
     }
     rep.stages_a = B.stages.size();
 
@@ -1666,6 +1990,10 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     h->xpad.alloc((d.n_cols + 4) * 8);
     check_cuda(cudaMemsetAsync(h->xpad.p, 0, h->xpad.bytes, s), "memset");
     h->partial.alloc(std::max<size_t>(16, npartial * 8));
+    // columns with >= kRedLong chunks first (one warp each in k_reduce)
+    std::stable_partition(redcols.begin(), redcols.end(), [](const RedCol& r) { return r.nchunks >= kRedLong; });
+    h->nred_long = static_cast<uint32_t>(
+        std::count_if(redcols.begin(), redcols.end(), [](const RedCol& r) { return r.nchunks >= kRedLong; }));
     up(h->redcols, redcols.data(), redcols.size() * sizeof(RedCol));
     h->nred = static_cast<uint32_t>(redcols.size());
     stream_sync(s);
@@ -1673,7 +2001,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     h->nblocks = static_cast<uint32_t>(nblocks);
     rep.device_arena_bytes = B.arena.size() * 4;
     rep.device_table_bytes = B.stages.size() * (sizeof(Stage) + kCopies * 8) + B.bitems.size() * sizeof(BItem) +
-                             B.aitems.size() * sizeof(AItem) +
+                             B.a_items * sizeof(AItem) +
                              wcol.size() * sizeof(WCol) + coef.size() * 8;
     rep.overhead = rep.device_table_bytes;
 }
@@ -1760,7 +2088,9 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
         h->last_launches++;
     };
     if (run_a) launch(k_phase_a, std::min<uint32_t>(h->nstripe_a, 2 * nsm), kThreadsA, kSmemBytes, false, p);
-    if (h->nred) launch(k_reduce, (h->nred + 255) / 256, 256, 0, true, p, h->redcols.as<RedCol>(), h->nred);
+    if (h->nred)
+        launch(k_reduce, (h->nred_long + 7) / 8 + (h->nred - h->nred_long + 255) / 256, 256, 0, true, p,
+               h->redcols.as<RedCol>(), h->nred_long, h->nred);
     if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
     if (h->nblocks) launch(k_phase_b, std::min<uint32_t>(h->nblocks, 2 * nsm), kThreadsB, kSmemBytes, run_a, p);
     check_cuda(cudaGetLastError(), "matvec launch");
@@ -2010,19 +2340,20 @@ int hcmx_gpu_hmat_export_buffer(const hcmx_hmat* h, uint64_t b, uint8_t* h_paylo
         const unsigned w = h->desc[b].bit_width;
         const uint64_t n = payload_bytes(h->count[b], w);
         if (n > capacity) throw invalid_argument("export: capacity");
-        std::vector<uint8_t> bits(n + 16, 0);
+        std::vector<uint8_t> bits(((n + 16) & ~uint64_t(3)) + 16, 0);
         for (const SegRef& sref : h->segs[b]) {
-            const uint64_t nw = (static_cast<uint64_t>(sref.nf) * w + 31) / 32;
-            std::vector<uint32_t> words(nw);
+            const uint64_t nbits = sref.gwords ? static_cast<uint64_t>((sref.nf + kARows - 1) / kARows) * sref.gwords * 32
+                                               : static_cast<uint64_t>(sref.nf) * w;
+            const uint64_t nw = (nbits + 31) / 32;
+            std::vector<uint32_t> words(nw + 2, 0u);
             check_cuda(cudaMemcpy(words.data(), h->arena.as<uint32_t>() + sref.word, nw * 4, cudaMemcpyDeviceToHost),
                        "export d2h");
-            // OR the fields back at their original bit offset
-            const uint64_t base = static_cast<uint64_t>(sref.f0) * w;
-            for (uint64_t bit = 0; bit < static_cast<uint64_t>(sref.nf) * w; ++bit) {
-                if ((words[bit >> 5] >> (bit & 31)) & 1u) {
-                    const uint64_t o = base + bit;
-                    bits[o >> 3] |= static_cast<uint8_t>(1u << (o & 7));
-                }
+            const uint8_t* wb = reinterpret_cast<const uint8_t*>(words.data());
+            for (uint64_t j = 0; j < sref.nf; ++j) {
+                // the field's bit in the arena run, written back at its original offset
+                const uint64_t from = sref.gwords ? (j / kARows) * sref.gwords * 32ull + sref.pbit + (j % kARows) * sref.rowbits
+                                                  : j * w;
+                put_bits(reinterpret_cast<uint32_t*>(bits.data()), (sref.f0 + j) * w, get_bits(wb, words.size() * 4, from, w), w);
             }
         }
         std::memcpy(h_payload, bits.data(), n);
