@@ -122,12 +122,14 @@ struct Stage {
 };
 static_assert(sizeof(Stage) == 32, "Stage layout");
 
-// Column layout parameters, precomputed on the host (16 bytes, one LDS.128)
+// Column layout parameters of the fast decoder (dec_fast), precomputed on the
+// host: the field's e + m bits once it is left-aligned (bits [32 - w, 31)) and
+// the multiplier 2^(21 + e) that moves them to bits [52 - m, 52 + e)
 struct ColPar {
-    uint32_t mask_em;    // (1 << (e + m)) - 1, all ones for e + m >= 32
-    uint32_t mul_rsh;    // mode 0: 1 << (20 - m); mode 1: 1 << (52 - m)
-    uint32_t packed;     // w | m << 8 | e << 16 | mode << 24
-    uint32_t sgn_sh;     // 31 - e - m (mode 0/1)
+    uint32_t mask;       // ((1 << (w - 1)) - 1) << (32 - w)
+    uint32_t mul;        // 1 << (21 + e)
+    uint32_t packed;     // w | m << 8 | e << 16 | mode << 24 (mode 0 fast, 2 generic, 3-5 raw)
+    uint32_t w;
 };
 
 // One rank column of a lowrank leaf as phase B needs it (32 bytes, two
@@ -136,7 +138,7 @@ struct ColPar {
 // A leaf's records are contiguous, so one bulk copy stages a whole leaf.
 struct WCol {
     double c;
-    uint32_t mask_em, mul_rsh, sgn_sh, packed, w, pad;
+    uint32_t mask, mul, packed, w, pad0, pad1;
 };
 static_assert(sizeof(WCol) == 32, "WCol layout");
 
@@ -150,7 +152,7 @@ struct BItem {
     uint32_t src;        // dense: x index of first column; lowrank: global W column id
     uint32_t dpacked;    // dense: w | m << 8 | e << 16 | mode << 24
     uint8_t mode;        // decode mode shared by every column of the item
-    uint8_t fcase;       // decode body (bcase_of): 1-6 fast (mode 0/1 x whole row groups), 0 generic
+    uint8_t fcase;       // decode body (bcase_of): 1-3 fast (whole row groups), 0 generic
     uint16_t pad;
     double scale;        // dense: buffer scale
 };
@@ -312,73 +314,57 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 
 // ------------------------------------------------------------- decode ----
-// A field of width w sits at bit sh of the word pair sp[0..1] (sp[2] too when
-// w > 32).  Layout [mant m][offset e][sign] (codec.cpp:118-137).  Each mode
-// returns +-((1.mant * 2^offset) - 1) -- exactly the codec's value / scale
-// (codec.cpp:161-169); the sign is xored into the result's high word.
-//   mode 0: w == 1 + e + m <= 32, m <= 20, e < 11 (the double lives in the high word)
-//   mode 1: w == 1 + e + m <= 32, m  > 20, e < 11
-//   mode 2: anything else (64-bit window, min(offset + 1023, 2046) clamp)
-//   modes 3, 4, 5 (decoded by the mode-2 body): uncompressed FP64 / FP32 / FP16
-//   storage (StorageMode fp64 and the MP-D-S-H groups, mixedprec.hpp:20-43): the
-//   value itself (scale 1)
-// Every column of an item shares one mode, so the mode is dispatched per item.
-template <int MODE>
-__device__ __forceinline__ double dec(const uint32_t* sp, const ColPar& c, unsigned sh) {
-    if (MODE == 0) {
-        const uint32_t t = __funnelshift_r(sp[0], sp[1], sh);
-        const uint32_t hi = (t & c.mask_em) * c.mul_rsh + (1023u << 20);
-        const double d = __hiloint2double(hi, 0) - 1.0;
-        return __hiloint2double(__double2hiint(d) ^ ((t << c.sgn_sh) & 0x80000000u), __double2loint(d));
-    } else if (MODE == 1) {
-        // mul = 2^(52 - m): the double's bits are (t & mask) * mul + (1023 << 52),
-        // one wide IMAD with a loop-invariant addend
-        const uint32_t t = __funnelshift_r(sp[0], sp[1], sh);
-        const uint64_t bits = static_cast<uint64_t>(t & c.mask_em) * c.mul_rsh + (1023ull << 52);
-        const double d = __longlong_as_double(static_cast<long long>(bits)) - 1.0;
-        return __hiloint2double(__double2hiint(d) ^ ((t << c.sgn_sh) & 0x80000000u), __double2loint(d));
-    } else {
-        const unsigned fmt = c.packed >> 24;
-        const unsigned w = c.packed & 0xffu, m = (c.packed >> 8) & 0xffu, e = (c.packed >> 16) & 0xffu;
-        uint64_t win = ((static_cast<uint64_t>(sp[1]) << 32) | sp[0]) >> sh;
-        if (w > 32 && sh + w > 64) win |= static_cast<uint64_t>(sp[2]) << (64 - sh);
-        if (fmt >= 3) {  // uncompressed words (uniform per item, so the branch is too)
-            if (fmt == 3)  // FP64
-                return __longlong_as_double(static_cast<long long>(win));
-            if (fmt == 4)  // FP32
-                return static_cast<double>(__int_as_float(static_cast<int>(static_cast<uint32_t>(win))));
-            // binary16 (the half.hpp:47-72 widening is exact)
-            const uint32_t t = static_cast<uint32_t>(win) & 0xffffu;
-            return static_cast<double>(__half2float(__ushort_as_half(static_cast<unsigned short>(t))));
-        }
-        const unsigned em = e + m;
-        const uint64_t sgn = (win >> em) & 1ull;
-        const uint64_t fem = win & ((1ull << em) - 1);
-        uint64_t bits = (fem << (52 - m)) + (1023ull << 52);
-        if ((fem >> m) >= 1024) bits = (2046ull << 52) | ((fem << (52 - m)) & ((1ull << 52) - 1));
-        const double d = __longlong_as_double(static_cast<long long>(bits)) - 1.0;
-        return __longlong_as_double(__double_as_longlong(d) ^ static_cast<long long>(sgn << 63));
-    }
+// A field's layout is [mant m][offset e][sign] (codec.cpp:118-137); every
+// decoder returns +-((1.mant * 2^offset) - 1) -- exactly the codec's value /
+// scale (codec.cpp:161-169).
+//
+// Fast decoder (w == 1 + e + m <= 32, e <= 10, codec fields): sp[1] is the
+// word holding the field's sign bit, sp[0] the word below it; the funnel shift
+// by s left-aligns the field (sign in bit 31).  The offset and mantissa bits
+// times 2^(21 + e) land at bits [52 - m, 52 + e) of the double, so one wide
+// IMAD with the bias 1023 << 52 rebuilds 1.mant * 2^offset (offset + 1023 <=
+// 2046: no clamp for e <= 10); one DADD takes the 1 off and the sign is xored
+// into the high word.  About 8 instructions per value with the FMA.
+__device__ __forceinline__ double dec_fast(const uint32_t* sp, unsigned s, uint32_t mask, uint32_t mul) {
+    const uint32_t t = __funnelshift_l(sp[0], sp[1], s);
+    const uint64_t bits = static_cast<uint64_t>(t & mask) * mul + (1023ull << 52);
+    const double v = __longlong_as_double(static_cast<long long>(bits)) - 1.0;
+    return __hiloint2double(__double2hiint(v) ^ static_cast<int>(t & 0x80000000u), __double2loint(v));
 }
 
-// decoder constants of one column from its packed layout word (w | m << 8 |
-// e << 16 | mode << 24); modes 0/1 have w == 1 + e + m
-// decoder multiplier of a column with m mantissa bits: 2^(20 - m) (mode 0,
-// m <= 20) or 2^(52 - m) (mode 1, 20 < m <= 31), read from a table: a
-// multiplier the compiler cannot see is a power of two stays an IMAD (fused
-// with the exponent bias) instead of a shift plus an add on the integer ALU,
-// the decode's tightest pipe
+// Generic decoder: the field at bit sh of sp[0..2] (64-bit window, the
+// min(offset + 1023, 2046) clamp), for e = 11, w > 32 and padded layouts;
+// modes 3, 4, 5: uncompressed FP64 / FP32 / FP16 storage (StorageMode fp64 and
+// the MP-D-S-H groups, mixedprec.hpp:20-43), the value itself (scale 1).
+__device__ __forceinline__ double dec_generic(const uint32_t* sp, uint32_t packed, unsigned sh) {
+    const unsigned fmt = packed >> 24;
+    const unsigned w = packed & 0xffu, m = (packed >> 8) & 0xffu, e = (packed >> 16) & 0xffu;
+    uint64_t win = ((static_cast<uint64_t>(sp[1]) << 32) | sp[0]) >> sh;
+    if (w > 32 && sh + w > 64) win |= static_cast<uint64_t>(sp[2]) << (64 - sh);
+    if (fmt >= 3) {  // uncompressed words (uniform per item, so the branch is too)
+        if (fmt == 3)  // FP64
+            return __longlong_as_double(static_cast<long long>(win));
+        if (fmt == 4)  // FP32
+            return static_cast<double>(__int_as_float(static_cast<int>(static_cast<uint32_t>(win))));
+        // binary16 (the half.hpp:47-72 widening is exact)
+        const uint32_t t = static_cast<uint32_t>(win) & 0xffffu;
+        return static_cast<double>(__half2float(__ushort_as_half(static_cast<unsigned short>(t))));
+    }
+    const unsigned em = e + m;
+    const uint64_t sgn = (win >> em) & 1ull;
+    const uint64_t fem = win & ((1ull << em) - 1);
+    uint64_t bits = (fem << (52 - m)) + (1023ull << 52);
+    if ((fem >> m) >= 1024) bits = (2046ull << 52) | ((fem << (52 - m)) & ((1ull << 52) - 1));
+    const double d = __longlong_as_double(static_cast<long long>(bits)) - 1.0;
+    return __longlong_as_double(__double_as_longlong(d) ^ static_cast<long long>(sgn << 63));
+}
+
+// 2^(21 + e), read from a table: a multiplier the compiler cannot see is a
+// power of two stays one wide IMAD (fused with the exponent bias) instead of a
+// 64-bit shift pair plus a 64-bit add on the integer pipe
 struct Pow2Table {
     uint32_t v[32];
 };
-constexpr Pow2Table make_pow2() {
-    Pow2Table t{};
-    for (int m = 0; m < 32; ++m) t.v[m] = m <= 20 ? (1u << (20 - m)) : (1u << (52 - m));
-    return t;
-}
-__constant__ Pow2Table c_pow2 = make_pow2();
-// phase-A fast body: 2^(21 + e) (same reason: an opaque power of two stays one
-// wide IMAD instead of a 64-bit shift pair plus a 64-bit add)
 constexpr Pow2Table make_pow2e() {
     Pow2Table t{};
     for (int e = 0; e < 32; ++e) t.v[e] = e <= 10 ? (1u << (21 + e)) : 0u;
@@ -386,16 +372,8 @@ constexpr Pow2Table make_pow2e() {
 }
 __constant__ Pow2Table c_pow2e = make_pow2e();
 
-template <int MODE>
-__device__ __forceinline__ ColPar col_of(uint32_t packed) {
-    ColPar c;
-    c.packed = packed;
-    const unsigned w = packed & 0xffu, m = (packed >> 8) & 0xffu;
-    c.mask_em = 0xffffffffu >> (33u - w);  // e + m = w - 1 bits
-    c.mul_rsh = c_pow2.v[m & 31u];
-    c.sgn_sh = 32u - w;                    // sign bit (w - 1) to bit 31
-    return c;
-}
+// fast-decoder constants from a layout word (w <= 32)
+__device__ __forceinline__ uint32_t fast_mask(unsigned w) { return 0x7fffffffu & ~((0xffffffffu >> (w - 1)) >> 1); }
 
 __device__ __forceinline__ unsigned round16u(unsigned x) { return (x + 15u) & ~15u; }
 
@@ -670,15 +648,13 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
 }
 
 // ------------------------------------------------------------ phase A ----
-// Fast body: every lane's field is a codec field with w <= 32 and e <= 10, the
-// item has whole row groups and every lane's x slice is 16-byte aligned.  The
-// funnel shift left-aligns the field (sign in bit 31); the exponent offset and
-// mantissa bits times 2^(21 + e) land at bits [52 - m, 52 + e) of the double,
-// so one wide IMAD with the bias 1023 << 52 rebuilds 1.mant * 2^offset
-// (codec.cpp:161-169; offset + 1023 <= 2046 needs no clamp for e <= 10).
+// Fast body: every lane's field is a codec field with w <= 32 and e <= 10
+// (dec_fast), the item has whole row groups and every lane's x slice is
+// 16-byte aligned.  Lane-constant (word, shift) per row of a group; the group
+// stride is gwords.
 __device__ __forceinline__ double a_fast(const uint32_t* data, unsigned P, unsigned w, unsigned e, const double* xs,
                                          unsigned ngroups, unsigned rowbits, unsigned gwords) {
-    const uint32_t mask = 0x7fffffffu & ~((0xffffffffu >> (w - 1)) >> 1);  // the field's e + m bits
+    const uint32_t mask = fast_mask(w);
     const uint32_t mul = c_pow2e.v[e & 31u];
     const uint32_t* q[kARows];
     unsigned s[kARows];
@@ -696,10 +672,7 @@ __device__ __forceinline__ double a_fast(const uint32_t* data, unsigned P, unsig
         const double xv[kARows] = {x01.x, x01.y, x23.x, x23.y};
 #pragma unroll
         for (int r = 0; r < kARows; ++r) {
-            const uint32_t t = __funnelshift_l(q[r][0], q[r][1], s[r]);
-            const uint64_t bits = static_cast<uint64_t>(t & mask) * mul + (1023ull << 52);
-            const double v = __longlong_as_double(static_cast<long long>(bits)) - 1.0;
-            const double d = __hiloint2double(__double2hiint(v) ^ static_cast<int>(t & 0x80000000u), __double2loint(v));
+            const double d = dec_fast(q[r], s[r], mask, mul);
             if (r & 1) acc1 = fma(d, xv[r], acc1);
             else acc0 = fma(d, xv[r], acc0);
             q[r] += gwords;
@@ -713,13 +686,12 @@ __device__ __forceinline__ double a_fast(const uint32_t* data, unsigned P, unsig
 __device__ __forceinline__ double a_generic(const uint32_t* data, unsigned P, uint32_t rec, const double* xs,
                                             unsigned nf, unsigned rowbits, unsigned gwords) {
     const unsigned w = rec & 127u, e = (rec >> 7) & 15u, m = (rec >> 11) & 63u, fmt = (rec >> 17) & 3u;
-    ColPar c{};
-    c.packed = w | (m << 8) | (e << 16) | ((fmt ? fmt + 2u : 2u) << 24);  // 1-3: uncompressed f64 / f32 / f16
+    const uint32_t packed = w | (m << 8) | (e << 16) | ((fmt ? fmt + 2u : 2u) << 24);  // 1-3: raw f64 / f32 / f16
     double acc = 0.0;
     for (unsigned j = 0; j < nf; ++j) {
         const unsigned bit = P + (j % kARows) * rowbits;
         const uint32_t* sp = data + (j / kARows) * gwords + (bit >> 5);
-        acc = fma(dec<2>(sp, c, bit & 31u), xs[j], acc);
+        acc = fma(dec_generic(sp, packed, bit & 31u), xs[j], acc);
     }
     return acc;
 }
@@ -802,9 +774,8 @@ __global__ void k_reduce(Params p, const RedCol* rc, uint32_t nlong, uint32_t n)
 }
 
 // ------------------------------------------------------------ phase B ----
-// generic path: any row offset / count (lanes individually predicated)
-template <int MODE>
-__device__ __forceinline__ void b_column(const uint32_t* seg, const ColPar& c, unsigned w, int f0, unsigned vmask,
+// generic path: any layout, any row offset / count (lanes individually predicated)
+__device__ __forceinline__ void b_column(const uint32_t* seg, uint32_t packed, unsigned w, int f0, unsigned vmask,
                                          unsigned umask, double coef, double (&acc)[kG]) {
     const int bit0 = f0 * static_cast<int>(w);
     const uint32_t* sp = seg + (bit0 >> 5);
@@ -812,12 +783,11 @@ __device__ __forceinline__ void b_column(const uint32_t* seg, const ColPar& c, u
 #pragma unroll
     for (int g = 0; g < kG; ++g) {
         if (umask & (1u << g)) {
-            if (vmask & (1u << g)) acc[g] = fma(dec<MODE>(sp + g * w, c, sh), coef, acc[g]);
+            if (vmask & (1u << g)) acc[g] = fma(dec_generic(sp + g * w, packed, sh), coef, acc[g]);
         }
     }
 }
 
-template <int MODE>
 __device__ __forceinline__ void b_item_generic(const BItem& it, const uint32_t* seg, const double* cf, unsigned lane,
                                                double dmul, double (&acc)[kG]) {
     const unsigned nseg = it.nseg, nr = it.nr;
@@ -833,48 +803,48 @@ __device__ __forceinline__ void b_item_generic(const BItem& it, const uint32_t* 
     const WCol* wc = reinterpret_cast<const WCol*>(cf);
     for (unsigned c = 0; c < nseg; ++c) {
         const uint32_t pw = it.kind == 0 ? it.dpacked : wc[c].packed;
-        const ColPar col = col_of<MODE>(pw);
         const unsigned w = pw & 0xffu;
         const double cc = it.kind == 0 ? dmul * cf[c] : wc[c].c;
-        b_column<MODE>(seg, col, w, f0, vmask, umask, cc, acc);
+        b_column(seg, pw, w, f0, vmask, umask, cc, acc);
         seg += (nr * w + 31) >> 5;
     }
 }
 
-// fast path: the item covers row groups [GLO, GHI) of the block completely, so
-// every lane decodes one field per group with no predication
-template <int MODE, int GLO, int GHI>
-__device__ __forceinline__ void b_column_full(const uint32_t* sp, const ColPar& c, unsigned w, unsigned sh,
-                                              double coef, double (&acc)[kG]) {
+// fast path: the item covers row groups [GLO, GHI) of the block completely and
+// every column decodes with dec_fast: lane l takes field l + 32 (g - GLO) of
+// each column segment, at the same shift in every group (32 fields = w words)
+template <int GLO, int GHI>
+__device__ __forceinline__ void b_column_full(const uint32_t* seg, unsigned lane, unsigned w, uint32_t mask,
+                                              uint32_t mul, double coef, double (&acc)[kG]) {
+    const unsigned top = (lane + 1) * w;  // one past the sign bit of field `lane`
+    const uint32_t* sp = seg + ((top - 1) >> 5) - 1;
+    const unsigned s = (0u - top) & 31u;
 #pragma unroll
-    for (int g = GLO; g < GHI; ++g) acc[g] = fma(dec<MODE>(sp + (g - GLO) * w, c, sh), coef, acc[g]);
+    for (int g = GLO; g < GHI; ++g) acc[g] = fma(dec_fast(sp + (g - GLO) * w, s, mask, mul), coef, acc[g]);
 }
 
-template <int MODE, int GLO, int GHI>
+template <int GLO, int GHI>
 __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg, const double* cf, unsigned lane,
                                             double dmul, double (&acc)[kG]) {
     const unsigned nseg = it.nseg;
     if (it.kind == 0) {  // dense: one layout for the whole item
-        const ColPar col = col_of<MODE>(it.dpacked);
-        const unsigned w = it.dpacked & 0xffu;
-        const unsigned bit = lane * w;
-        const uint32_t* sp = seg + (bit >> 5);
-        const unsigned sh = bit & 31u, segw = (GHI - GLO) * w;
+        const unsigned w = it.dpacked & 0xffu, e = (it.dpacked >> 16) & 0xffu;
+        const uint32_t mask = fast_mask(w), mul = c_pow2e.v[e & 31u];
+        const unsigned segw = (GHI - GLO) * w;
 #pragma unroll 2
         for (unsigned c = 0; c < nseg; ++c) {
-            b_column_full<MODE, GLO, GHI>(sp, col, w, sh, dmul * cf[c], acc);
-            sp += segw;
+            b_column_full<GLO, GHI>(seg, lane, w, mask, mul, dmul * cf[c], acc);
+            seg += segw;
         }
     } else {
         const WCol* wc = reinterpret_cast<const WCol*>(cf);  // staged records of the leaf's columns
         for (unsigned c = 0; c < nseg; ++c) {
-            // the record as two 16-byte loads: {c, mask, mul}, {sgn, packed, w, -}
+            // the record as two 16-byte loads: {c, mask, mul}, {packed, w, -, -}
             const uint4 q0 = reinterpret_cast<const uint4*>(wc + c)[0];
             const uint4 q1 = reinterpret_cast<const uint4*>(wc + c)[1];
-            const ColPar col{q0.z, q0.w, q1.y, q1.x};
             const double cc = __hiloint2double(static_cast<int>(q0.y), static_cast<int>(q0.x));
-            const unsigned w = q1.z, bit = lane * w;
-            b_column_full<MODE, GLO, GHI>(seg + (bit >> 5), col, w, bit & 31u, cc, acc);
+            const unsigned w = q1.y;
+            b_column_full<GLO, GHI>(seg, lane, w, q0.z, q0.w, cc, acc);
             seg += (GHI - GLO) * w;
         }
     }
@@ -885,19 +855,16 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
     const double* cf = reinterpret_cast<const double*>(slot + it.coef_off);
     const double dmul = p.alpha * it.scale;  // dense: alpha * buffer scale folded into x
     const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
-    // fast bodies for modes 0/1 at the shapes 64-row leaf clusters produce;
-    // everything else takes one generic body with the mode-2 decoder (exact for
-    // every layout), which keeps the kernel inside the instruction cache
+    // fast bodies for dec_fast layouts at the shapes 64-row leaf clusters
+    // produce; everything else takes one generic body (exact for every layout),
+    // which keeps the kernel inside the instruction cache
     static_assert(kG == 4, "fast-path table assumes 128-row blocks");
     switch (it.fcase) {  // the body index, precomputed by bcase_of (a dense jump table)
-        case 1: b_item_full<0, 0, 4>(it, seg, cf, lane, dmul, acc); break;
-        case 2: b_item_full<0, 0, 2>(it, seg, cf, lane, dmul, acc); break;
-        case 3: b_item_full<0, 2, 4>(it, seg, cf, lane, dmul, acc); break;
-        case 4: b_item_full<1, 0, 4>(it, seg, cf, lane, dmul, acc); break;
-        case 5: b_item_full<1, 0, 2>(it, seg, cf, lane, dmul, acc); break;
-        case 6: b_item_full<1, 2, 4>(it, seg, cf, lane, dmul, acc); break;
+        case 1: b_item_full<0, 4>(it, seg, cf, lane, dmul, acc); break;
+        case 2: b_item_full<0, 2>(it, seg, cf, lane, dmul, acc); break;
+        case 3: b_item_full<2, 4>(it, seg, cf, lane, dmul, acc); break;
         default:
-            b_item_generic<2>(it, seg, cf, lane, dmul, acc);  // also uncompressed words (modes 3-5)
+            b_item_generic(it, seg, cf, lane, dmul, acc);  // also uncompressed words (modes 3-5)
             break;
     }
 }
@@ -1111,16 +1078,18 @@ void drain_timing(hcmx_hmat* h) {
     h->pending.clear();
 }
 
-// host-side column parameters for the decoder (see dec<MODE>)
+// host-side column parameters of the decoders (dec_fast / dec_generic)
 ColPar col_par(const hcmx_descriptor& x) {
     ColPar c{};
-    const unsigned w = x.bit_width, m = x.mant_bits, e = x.exp_bits, em = e + m;
-    unsigned mode = (w > 32 || e >= 11 || w != 1 + em) ? 2u : (m <= 20 ? 0u : 1u);
+    const unsigned w = x.bit_width, m = x.mant_bits, e = x.exp_bits;
+    unsigned mode = (w > 32 || e >= 11 || w != 1 + e + m) ? 2u : 0u;
     if (x.scheme >= HCMX_RAW_F64) mode = 3u + (x.scheme - HCMX_RAW_F64);  // uncompressed storage
-    c.mask_em = em >= 32 ? 0xffffffffu : ((1u << em) - 1u);
-    c.mul_rsh = mode == 0 ? (1u << (20 - m)) : (mode == 1 ? 1u << (52 - m) : 0u);
+    if (mode == 0) {
+        c.mask = ((1u << (w - 1)) - 1u) << (32 - w);
+        c.mul = 1u << (21 + e);
+    }
     c.packed = w | (m << 8) | (e << 16) | (mode << 24);
-    c.sgn_sh = em <= 31 ? 31 - em : 0u;
+    c.w = w;
     return c;
 }
 
@@ -1135,11 +1104,11 @@ uint8_t fcase_of(uint64_t ra, uint64_t nr) {
     }
 }
 
-// phase-B body index: whole row groups [0,4) / [0,2) / [2,4) x decode mode 0 / 1
+// phase-B body index: whole row groups [0,4) / [0,2) / [2,4) with the fast decoder
 uint8_t bcase_of(uint64_t ra, uint64_t nr, unsigned mode) {
     const uint8_t f = fcase_of(ra, nr);
-    if (mode >= 2 || f == 0) return 0;
-    return static_cast<uint8_t>((f == 0x04 ? 1 : f == 0x02 ? 2 : 3) + 3 * mode);
+    if (mode != 0 || f == 0) return 0;
+    return static_cast<uint8_t>(f == 0x04 ? 1 : f == 0x02 ? 2 : 3);
 }
 
 inline uint32_t r16(uint64_t x) { return static_cast<uint32_t>((x + 15) & ~uint64_t(15)); }
@@ -1845,7 +1814,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
             const hcmx_descriptor& xw = d.desc[wbuf(l, i).first];
             const hcmx_descriptor& xx = d.desc[xbuf(l, i).first];
             const ColPar cp = col_par(xw);
-            wcol[leafa[id].colbase + i] = {0.0, cp.mask_em, cp.mul_rsh, cp.sgn_sh, cp.packed, xw.bit_width, 0u};
+            wcol[leafa[id].colbase + i] = {0.0, cp.mask, cp.mul, cp.packed, xw.bit_width, 0u, 0u};
             coef[leafa[id].colbase + i] = (uniform ? 1.0 : d.sigma[d.sig0[l] + i]) * xx.scale * xw.scale;
         }
     }
@@ -1945,6 +1914,21 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         }
     }
     rep.stages_b = B.stages.size() - b_ws0;
+    if (std::getenv("HCMX_BUILD_STATS")) {  // profiling aid: copies / items / bytes per stage
+        for (int ph = 0; ph < 2; ++ph) {
+            const size_t s0 = ph ? b_ws0 : 0, s1 = ph ? B.stages.size() : b_ws0;
+            uint64_t nc = 0, cb = 0, db = 0, ni = 0;
+            for (size_t st = s0; st < s1; ++st) {
+                for (size_t q = 0; q < kCopies; ++q) nc += B.copies[st * kCopies + q] >> 63;
+                cb += B.stages[st].coef_bytes;
+                db += B.stages[st].bytes;
+                ni += B.stages[st].nitems;
+            }
+            const double n = std::max<double>(1.0, double(s1 - s0));
+            std::fprintf(stderr, "[build %c] stages %zu: per stage %.1f copies, %.1f items, %.0f data B, %.0f coef B\n",
+                         ph ? 'B' : 'A', s1 - s0, nc / n, ni / n, db / n, cb / n);
+        }
+    }
     B.segs.clear();
     B.segs.shrink_to_fit();
     while (B.arena.size() % 4) B.arena.push_back(0u);
