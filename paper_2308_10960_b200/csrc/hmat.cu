@@ -56,7 +56,10 @@
 namespace hcmx_gpu {
 namespace {
 
-constexpr int kNWB = 16;                  // phase-B consumer warps per CTA
+#ifndef HCMX_NWB
+#define HCMX_NWB 16
+#endif
+constexpr int kNWB = HCMX_NWB;            // phase-B consumer warps per CTA
 #ifndef HCMX_NWA
 #define HCMX_NWA 8
 #endif
@@ -93,9 +96,13 @@ constexpr int kAChunk = 64;           // rows of a leaf's X columns per phase-A 
 constexpr int kARows = 4;             // rows per word-padded group of a phase-A item
 constexpr int kALanes = 32;           // rank columns per phase-A item
 constexpr int kAGroupMax = 8;         // chunks of one rank column summed in-warp
+#ifndef HCMX_AUNROLL
+#define HCMX_AUNROLL 4
+#endif
 #ifndef HCMX_AITEM
 #define HCMX_AITEM 8192
 #endif
+constexpr int kAUnroll = HCMX_AUNROLL;   // row groups per iteration of the phase-A fast body
 constexpr uint64_t kAItemBytes = HCMX_AITEM;  // packed data per phase-A item
 constexpr uint32_t kAItemXBytes = 12288;  // staged x slices per phase-A item
 constexpr int kBDenseGroup = 8;       // max dense columns per B item
@@ -664,21 +671,19 @@ __device__ __forceinline__ double a_fast(const uint32_t* data, unsigned P, unsig
         q[r] = data + ((top - 1) >> 5) - 1;        // the word below the one holding the sign
         s[r] = (0u - top) & 31u;
     }
-    double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll 2
+    double acc[kARows] = {0.0, 0.0, 0.0, 0.0};  // one chain per row of the group
+#pragma unroll kAUnroll
     for (unsigned g = 0; g < ngroups; ++g) {
         const double2 x01 = reinterpret_cast<const double2*>(xs)[2 * g];
         const double2 x23 = reinterpret_cast<const double2*>(xs)[2 * g + 1];
         const double xv[kARows] = {x01.x, x01.y, x23.x, x23.y};
 #pragma unroll
         for (int r = 0; r < kARows; ++r) {
-            const double d = dec_fast(q[r], s[r], mask, mul);
-            if (r & 1) acc1 = fma(d, xv[r], acc1);
-            else acc0 = fma(d, xv[r], acc0);
+            acc[r] = fma(dec_fast(q[r], s[r], mask, mul), xv[r], acc[r]);
             q[r] += gwords;
         }
     }
-    return acc0 + acc1;
+    return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 // Generic body: any layout (e = 11, w > 32, uncompressed words), any row count,
