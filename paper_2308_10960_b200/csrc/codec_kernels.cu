@@ -305,49 +305,68 @@ __device__ __forceinline__ int pack_groups32(const double* __restrict__ v, uint3
     const bool m_lo = m <= 20;
     const unsigned msh = m_lo ? 20u - m : 52u - m;
     const unsigned bit = lane * w, q = bit >> 5, s = bit & 31u;
-    const bool straddle = s + w > 32;
     const uint32_t nfull = n / 32;
     int nf_bad = 0;
+    auto encode = [&](double x) -> uint32_t {
+        // the caller rejected non-finite input; zeros keep only their sign
+        // (selected, not branched: 1 / scale may be inf for a subnormal scale)
+        const uint32_t sign = static_cast<uint32_t>(__double2hiint(x)) >> 31;
+        const double vp = __dadd_rn(__dmul_rn(fabs(x), inv_scale), 1.0);  // no FMA (codec.cpp:124)
+        const uint64_t u = dbits(vp) + round_add;
+        const uint32_t uh = static_cast<uint32_t>(u >> 32), ul = static_cast<uint32_t>(u);
+        uint32_t offset = (uh >> 20) - 1023u;
+        uint32_t mant = (m_lo ? uh >> msh : __funnelshift_r(ul, uh, msh)) & mant_mask;
+        const bool sat = offset > max_offset || static_cast<uint32_t>(__double2hiint(vp)) >= 0x7ff00000u;
+        offset = sat ? max_offset : offset;
+        mant = sat ? mant_mask : mant;
+        return (sign << sgn_sh) | (x != 0.0 ? (offset << m) | mant : 0u);
+    };
     for (uint32_t g4 = g0; g4 < g1; g4 += 4 * gstride) {
+        // four whole groups (warp-uniform): no bounds on loads or stores
+        const bool whole = g4 + 3 * gstride < nfull;
         double xs[4];
+        if (whole) {
+            const double* vp = v + g4 * 32 + lane;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint32_t g = g4 + i * gstride;
-            const uint32_t idx = g * 32 + lane;
-            xs[i] = (g < g1 && idx < n) ? __ldcs(v + idx) : 0.0;
+            for (int i = 0; i < 4; ++i) xs[i] = __ldcs(vp + i * gstride * 32);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t g = g4 + i * gstride;
+                const uint32_t idx = g * 32 + lane;
+                xs[i] = (g < g1 && idx < n) ? __ldcs(v + idx) : 0.0;
+            }
         }
         uint32_t f[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            // the caller rejected non-finite input; zeros keep only their sign
-            // (selected, not branched: 1 / scale may be inf for a subnormal scale)
-            const double x = xs[i];
-            const uint32_t sign = static_cast<uint32_t>(__double2hiint(x)) >> 31;
-            const double vp = __dadd_rn(__dmul_rn(fabs(x), inv_scale), 1.0);  // no FMA (codec.cpp:124)
-            const uint64_t u = dbits(vp) + round_add;
-            const uint32_t uh = static_cast<uint32_t>(u >> 32), ul = static_cast<uint32_t>(u);
-            uint32_t offset = (uh >> 20) - 1023u;
-            uint32_t mant = (m_lo ? uh >> msh : __funnelshift_r(ul, uh, msh)) & mant_mask;
-            const bool sat = offset > max_offset || static_cast<uint32_t>(__double2hiint(vp)) >= 0x7ff00000u;
-            offset = sat ? max_offset : offset;
-            mant = sat ? mant_mask : mant;
-            f[i] = (sign << sgn_sh) | (x != 0.0 ? (offset << m) | mant : 0u);
+            f[i] = encode(xs[i]);
             sw[i * 36 + lane] = 0u;
             if (lane == 0) sw[i * 36 + 32] = 0u;
         }
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
+            // the high part is 0 when the field does not straddle (ORing 0 into
+            // word q + 1 <= 32 is harmless): no divergent branch
             atomicOr(sw + i * 36 + q, f[i] << s);
-            if (straddle) atomicOr(sw + i * 36 + q + 1, f[i] >> (32u - s));
+            atomicOr(sw + i * 36 + q + 1, __funnelshift_l(f[i], 0u, s));
         }
         __syncwarp();
+        if (whole) {
+            if (lane < w) {
+                uint32_t* op = out + g4 * w + lane;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint32_t g = g4 + i * gstride;
-            if (g >= g1) break;
-            const unsigned nwords = g < nfull ? w : ((n - g * 32) * w + 31) / 32;
-            if (lane < nwords) __stcs(out + g * w + lane, sw[i * 36 + lane]);
+                for (int i = 0; i < 4; ++i) __stcs(op + i * gstride * w, sw[i * 36 + lane]);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t g = g4 + i * gstride;
+                if (g >= g1) break;
+                const unsigned nwords = g < nfull ? w : ((n - g * 32) * w + 31) / 32;
+                if (lane < nwords) __stcs(out + g * w + lane, sw[i * 36 + lane]);
+            }
         }
         __syncwarp();
     }
