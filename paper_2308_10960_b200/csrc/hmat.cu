@@ -2,33 +2,28 @@
 // decompress + matrix-vector product (hmatrix.hpp:126-128).
 //
 // Layout (built once on the host by hcmx_gpu_hmat_create):
-//   The packed codec streams of every leaf are re-tiled, field-for-field and
-//   bit-identical, into one HBM arena.  Work is cut into items; items are
-//   grouped into CTA "stripes", spread over the CTA's warps by LPT on their
-//   field counts, and each warp's items are packed into its own sequence of
-//   16-byte aligned warp-stages (<= 3 KB of packed data each).
+//   The packed codec fields of every leaf are re-tiled, each field keeping its
+//   bits, into one HBM arena of 16-byte aligned stages.  A stage is one bulk
+//   copy (TMA engine) into a shared-memory ring slot; its staged coefficients
+//   follow it in the slot.  Stages are grouped into stripes that persistent
+//   CTAs claim from a global counter (largest estimated cost first).
 //
-//   phase A (lowrank X^T x): item = (APLR leaf, <= 128 consecutive columns of
-//     the block, <= 4 rank columns); its data is, for each rank column, the
-//     fields of that X column over the column chunk, word aligned.  The items
-//     of one chunk go to one warp and share one staged x slice.  A warp reduces
-//     each rank column with shuffles and writes t_i directly (one chunk) or a
-//     partial that the last-arriving warp sums in fixed chunk order.
-//   phase B (row-stationary): one CTA owns one block of 128 rows and streams
-//     every item that writes those rows: dense leaves (groups of 8 columns)
-//     and the W slices of every APLR leaf covering the block (<= 8 rank
-//     columns).  Lane l owns rows 32 g + l (4 accumulators per warp); the CTA
-//     sums its warps once at the end and writes y once per row -- no atomics.
+//   phase A (lowrank X^T x): item = up to 32 lanes, one 64-row chunk of one X
+//     column per lane, row-interleaved (row j = the lanes' fields back to
+//     back, groups of 4 rows padded to whole words).  Each lane sums its own
+//     column -- no cross-lane reduction; consecutive chunks of one column
+//     (<= 8, a segment) are summed by a fixed in-warp butterfly, wider leaves
+//     leave one partial per segment for k_reduce.
+//   phase B (row-stationary): one stripe = one block of 128 rows and every
+//     item that writes those rows: dense leaves and the W slices of every
+//     lowrank leaf covering the block, column-major.  Lane l owns rows
+//     32 g + l (4 accumulators per warp); the CTA sums its warps once at the
+//     end and writes y once per row -- no atomics.
 //
-//   Every warp runs its own 3-deep ring of warp-stages in shared memory, fed
-//   by cp.async.bulk (the TMA bulk engine; packed data with L2 evict_first):
-//   the packed data, the item descriptors, and per item the coefficient slice
-//   (x, or the phase-A results) plus the column parameters.  The warp refills a
-//   slot right after consuming it, with metadata it prefetched while decoding,
-//   so there is no cross-warp coupling and nothing in the decode loop waits on
-//   global memory.  A field costs two LDS, a funnel shift, ~4 integer ops to
-//   rebuild the FP64 pattern (32-bit fast paths for w <= 32), one DADD and one
-//   DFMA.
+//   One producer warp per CTA fills a 3-slot ring (stage data with L2
+//   evict_first, coefficient copies); consumer warps decode from shared
+//   memory only.  A field costs two LDS, one funnel shift, a mask, one wide
+//   IMAD, one DADD, one LOP3 for the sign and one DFMA (dec_fast).
 //
 // Numerics: decoded values are bit-identical to codec::decompress_into; the
 // multiply by the buffer scale is folded into the coefficients (dense: alpha *
