@@ -54,9 +54,9 @@ def _cpu_svd(M: torch.Tensor):
     from concurrent.futures import ThreadPoolExecutor
     a = M.detach().cpu().numpy()
     B = a.shape[0]
-    U = np.empty(a.shape[:-1] + (min(a.shape[-2:]),))
+    U = np.empty(a.shape[:-1] + (min(a.shape[-2:]),), a.dtype)
     S = np.empty((B, min(a.shape[-2:])))
-    Vh = np.empty((B, min(a.shape[-2:]), a.shape[-1]))
+    Vh = np.empty((B, min(a.shape[-2:]), a.shape[-1]), a.dtype)
     nt = min(32, os.cpu_count() or 1)
     cuts = np.linspace(0, B, nt + 1).astype(int)
 
@@ -81,13 +81,13 @@ def _svd_batch(A: torch.Tensor, eps: float):
     while True:
         omega = torch.randn(B, n, p, dtype=A.dtype, device=A.device, generator=g)
         Q, _ = torch.linalg.qr(A @ omega)
-        Q, _ = torch.linalg.qr(A.transpose(1, 2) @ Q)   # one power iteration
+        Q, _ = torch.linalg.qr(A.mH @ Q)                  # one power iteration
         Q, _ = torch.linalg.qr(A @ Q)
-        Bt = A.transpose(1, 2) @ Q                        # (Q^T A)^T, n x p
-        Q2, R2 = torch.linalg.qr(Bt)                      # Q^T A = R2^T Q2^T
-        Ur, S, Vrh = _cpu_svd(R2.transpose(1, 2))         # p x p
+        Bt = A.mH @ Q                                     # (Q^H A)^H, n x p
+        Q2, R2 = torch.linalg.qr(Bt)                      # Q^H A = R2^H Q2^H
+        Ur, S, Vrh = _cpu_svd(R2.mH)                      # p x p
         if p >= min(m, n) or bool((S[:, -1] <= 1e-3 * eps * S[:, 0]).all()):
-            return Q @ Ur, S, (Q2 @ Vrh.transpose(1, 2)).transpose(1, 2)
+            return Q @ Ur, S, (Q2 @ Vrh.mH).mH
         p = min(min(m, n), 2 * p)
 
 
@@ -182,3 +182,80 @@ def _fill_blocks(P, leaves, ids, kernel, out, off, batch_bytes):
             o = torch.as_tensor(off[chunk], device=P.device)
             idx = o[:, None] + torch.arange(m * n, device=P.device)[None, :]
             out[idx.reshape(-1)] = colmaj.reshape(-1)
+
+
+def assemble_complex(points_internal: np.ndarray, leaves: BlockLeaves, kernel: PointKernel, eps: float,
+                     device: str | None = None, batch_bytes: int | None = None) -> tuple[Assembled, Assembled]:
+    """Complex kernels (config 5): A = Ar + i Ai as two real H-matrices on the same
+    tree, so every factor's real and imaginary parts are separate codec streams.
+
+    Dense leaves: Re / Im of the block.  Lowrank leaves: complex SVD A ~= U S V^H
+    truncated by the same rank rule; with U = Ur + i Ui, V = Vr + i Vi,
+        Re(A) = [Ur Ui] diag(S, S) [Vr Vi]^T,   Im(A) = [Ui -Ur] diag(S, S) [Vr Vi]^T,
+    i.e. real APLR leaves of rank 2k whose column precisions follow S (the
+    reference is real-only)."""
+    dev = torch.device(device or ("cuda" if torch.cuda.is_available() else "cpu"))
+    if batch_bytes is None:
+        batch_bytes = (4 << 30) if dev.type == "cuda" else (1 << 30)
+    P = torch.as_tensor(np.ascontiguousarray(points_internal, dtype=np.float64), device=dev)
+    L = len(leaves)
+    kind = np.where(leaves.admissible, 1, 0).astype(np.int64)
+    rows = (leaves.row1 - leaves.row0).astype(np.int64)
+    cols = (leaves.col1 - leaves.col0).astype(np.int64)
+    rank = np.zeros(L, np.int64)
+    dense_off = np.full(L, -1, np.int64)
+    didx = np.nonzero(kind == 0)[0]
+    sizes = rows[didx] * cols[didx]
+    dense_off[didx] = np.concatenate([[0], np.cumsum(sizes)[:-1]]) if didx.size else []
+    dre = torch.empty(int(sizes.sum()), dtype=torch.float64, device=dev)
+    dim = torch.empty_like(dre)
+    groups = {}
+    for l in didx:
+        groups.setdefault((int(rows[l]), int(cols[l])), []).append(int(l))
+    for (m, n), g in groups.items():
+        per = max(1, batch_bytes // (16 * m * n * 2))
+        for c0 in range(0, len(g), per):
+            chunk = np.array(g[c0: c0 + per])
+            A = _blocks(P, leaves, chunk, kernel).transpose(1, 2).reshape(len(chunk), -1)  # column-major
+            o = torch.as_tensor(dense_off[chunk], device=dev)
+            idx = (o[:, None] + torch.arange(m * n, device=dev)[None, :]).reshape(-1)
+            dre[idx] = A.real.reshape(-1)
+            dim[idx] = A.imag.reshape(-1)
+    lidx = np.nonzero(kind == 1)[0]
+    w_off = np.full(L, -1, np.int64)
+    x_off = np.full(L, -1, np.int64)
+    sig_off = np.full(L, -1, np.int64)
+    wr, wi, xl, sl = [], [], [], []
+    wo = xo = so = 0
+    shapes = {}
+    for l in lidx:
+        shapes.setdefault((int(rows[l]), int(cols[l])), []).append(int(l))
+    for (m, n), ids in shapes.items():
+        per = max(1, batch_bytes // (16 * m * n * 3))
+        for c0 in range(0, len(ids), per):
+            chunk = np.array(ids[c0: c0 + per])
+            A = _blocks(P, leaves, chunk, kernel)
+            U, S, Vh = _svd_batch(A, eps)
+            ks_t = rank_from_singular_values(S, eps)
+            keep = torch.arange(S.shape[1], device=S.device)[None, :] < ks_t[:, None]
+            keep2 = keep[:, None, :].expand(-1, 2, -1)                # (B, 2, p): [real part, imag part]
+            Ut = U.mT                                                  # rows = columns of U
+            Wre = torch.stack([Ut.real, Ut.imag], 1)[keep2].reshape(-1)   # [Ur Ui]
+            Wim = torch.stack([Ut.imag, -Ut.real], 1)[keep2].reshape(-1)  # [Ui -Ur]
+            Xc = torch.stack([Vh.real, -Vh.imag], 1)[keep2].reshape(-1)   # [Vr Vi], V = Vh^H
+            Sc = torch.stack([S, S], 1)[keep2].cpu().numpy()
+            ks = 2 * ks_t.cpu().numpy().astype(np.int64)
+            rank[chunk] = ks
+            w_off[chunk] = wo + np.concatenate([[0], np.cumsum(ks * m)[:-1]])
+            x_off[chunk] = xo + np.concatenate([[0], np.cumsum(ks * n)[:-1]])
+            sig_off[chunk] = so + np.concatenate([[0], np.cumsum(ks)[:-1]])
+            wr.append(Wre); wi.append(Wim); xl.append(Xc); sl.append(Sc)
+            wo += Wre.numel(); xo += Xc.numel(); so += Sc.size
+    z = torch.zeros(0, dtype=torch.float64, device=dev)
+    Wr = torch.cat(wr) if wr else z
+    Wi = torch.cat(wi) if wi else z
+    X = torch.cat(xl) if xl else z
+    sigma = np.concatenate(sl) if sl else np.zeros(0)
+    n = points_internal.shape[0]
+    mk = lambda dense, W: Assembled(n, leaves, kind, rank, dense, dense_off, W, X, w_off, x_off, sigma, sig_off)
+    return mk(dre, Wr), mk(dim, Wi)

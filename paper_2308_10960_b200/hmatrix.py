@@ -25,7 +25,7 @@ import torch
 
 from . import _lib
 from ._lib import DESC_DTYPE, check, lib, ptr, u64p
-from .assemble import Assembled, assemble
+from .assemble import Assembled, assemble, assemble_complex
 from .codec import Scheme, compress_batch
 from .problems import config as problem_config, make_kernel, make_points
 from .tree import build_block_tree, build_cluster_tree
@@ -487,3 +487,62 @@ class HMatrix:
 def matvec(alpha: float, M: HMatrix, x, beta: float, y, transpose: bool = False):
     """hmatrix.hpp:126-128: y := alpha * op(M) * x + beta * y"""
     return M.matvec(alpha, x, beta, y, transpose)
+
+
+def build_config_complex(cfg, scheme="afl", device=None, n=None, seed=1, eps=None):
+    """setup for config 5 (complex kernel): the real and imaginary H-matrices
+    (assemble_complex), each compressed on the GPU with APLR leaves"""
+    c = problem_config(cfg) if not isinstance(cfg, dict) else dict(cfg)
+    if n is not None:
+        c["n"] = n
+    if eps is not None:
+        c["eps"] = eps
+    pts = make_points(c["geometry"], c["n"], seed)
+    ct = build_cluster_tree(pts, c["leaf"])
+    leaves = build_block_tree(ct, ct, c["eta"])
+    Ar, Ai = assemble_complex(pts[ct.i2e], leaves, make_kernel(c["kernel"]), c["eps"], device=device)
+    mode = f"{Scheme[scheme].name if isinstance(scheme, str) else Scheme(scheme).name}-aplr"
+    fr = compress_in_place(Ar, c["eps"], mode)
+    fi = compress_in_place(Ai, c["eps"], mode)
+    info = dict(c, leaves=len(leaves), dense_leaves=int((Ar.kind == 0).sum()),
+                lowrank_leaves=int((Ar.kind == 1).sum()))
+    return fr, fi, info
+
+
+class ComplexHMatrix:
+    """A = Ar + i Ai (config 5): two device-resident real H-matrices on one tree
+    whose factors hold the real and imaginary parts as separate codec streams.
+    Y = A X for complex X (n x r): [Ar; Ai] applied to [Re X, Im X] (one fused
+    product per real column), combined as Re Y = Ar Re X - Ai Im X,
+    Im Y = Ar Im X + Ai Re X."""
+
+    def __init__(self, fr: FlatHMatrix, fi: FlatHMatrix):
+        self.re, self.im = HMatrix(fr), HMatrix(fi)
+        self.n_rows, self.n_cols = self.re.n_rows, self.re.n_cols
+
+    def close(self):
+        self.re.close()
+        self.im.close()
+
+    def matmat(self, alpha: complex, X, beta: complex, Y):
+        """Y := alpha A X + beta Y (host complex128, X: n x r or n)"""
+        X = np.asarray(X, dtype=np.complex128)
+        Y = np.asarray(Y)
+        vec = X.ndim == 1
+        X2 = X[:, None] if vec else X
+        if X2.shape[0] != self.n_cols or Y.shape != ((self.n_rows,) if vec else (self.n_rows, X2.shape[1])):
+            raise ValueError("matmat: dimension mismatch")
+        r = X2.shape[1]
+        XX = np.asfortranarray(np.concatenate([X2.real, X2.imag], axis=1))   # [Re X, Im X]
+        Pr = np.zeros((self.n_rows, 2 * r), order="F")
+        Pi = np.zeros((self.n_rows, 2 * r), order="F")
+        self.re.matmat(1.0, XX, 0.0, Pr)
+        self.im.matmat(1.0, XX, 0.0, Pi)
+        AX = (Pr[:, :r] - Pi[:, r:]) + 1j * (Pr[:, r:] + Pi[:, :r])
+        out = alpha * AX + (beta * (Y[:, None] if vec else Y) if beta != 0 else 0.0)
+        out = out[:, 0] if vec else out
+        Y[...] = out
+        return Y
+
+    def matvec(self, alpha: complex, x, beta: complex, y):
+        return self.matmat(alpha, x, beta, y)

@@ -79,6 +79,22 @@ class Matern15(PointKernel):
         return self.sigma2 * (1.0 + t) * torch.exp(-t)
 
 
+class Helmholtz(PointKernel):
+    """exp(i kappa |x - y|) / (4 pi |x - y|), self term 0 (BASELINE config 5;
+    complex FP64 -- assemble_complex splits it into real / imaginary parts)"""
+    name = "helmholtz"
+    complex = True
+
+    def __init__(self, kappa: float = 16.0):
+        self.kappa = kappa
+
+    def block(self, a, b):
+        d = torch.cdist(a, b, compute_mode="donot_use_mm_for_euclid_dist")
+        inv = torch.where(d > 0, 1.0 / (4.0 * math.pi * torch.where(d > 0, d, torch.ones_like(d))),
+                          torch.zeros_like(d))
+        return torch.polar(inv, self.kappa * d)
+
+
 def config(name: str) -> dict:
     """BASELINE.json configs (index 0..4) as build parameters"""
     name = str(name)
@@ -86,6 +102,7 @@ def config(name: str) -> dict:
         "1": dict(geometry="fibonacci", n=8192, kernel="laplace", eps=1e-6, leaf=64, eta=2.0),
         "3": dict(geometry="fibonacci", n=131072, kernel="laplace", eps=1e-8, leaf=64, eta=2.0),
         "4": dict(geometry="cube", n=524288, kernel="matern", eps=1e-6, leaf=64, eta=2.0),
+        "5": dict(geometry="fibonacci", n=262144, kernel="helmholtz", eps=1e-6, leaf=64, eta=2.0, nrhs=16),
     }
     return dict(table[name])
 
@@ -105,4 +122,6 @@ def make_kernel(name: str) -> PointKernel:
         return Laplace()
     if name == "matern":
         return Matern15(0.1, 1.0)
+    if name == "helmholtz":
+        return Helmholtz(16.0)
     raise ValueError(f"unknown kernel {name}")
