@@ -664,7 +664,7 @@ __device__ __forceinline__ double a_fast(const uint32_t* data, unsigned P, unsig
     for (int r = 0; r < kARows; ++r) {
         const unsigned top = P + r * rowbits + w;  // one past the field's sign bit
         q[r] = data + ((top - 1) >> 5) - 1;        // the word below the one holding the sign
-        s[r] = (0u - top) & 31u;
+        s[r] = 0u - top;                           // the funnel shift takes it modulo 32
     }
     double acc[kARows] = {0.0, 0.0, 0.0, 0.0};  // one chain per row of the group
 #pragma unroll kAUnroll
@@ -818,7 +818,7 @@ __device__ __forceinline__ void b_column_full(const uint32_t* seg, unsigned lane
                                               uint32_t mul, double coef, double (&acc)[kG]) {
     const unsigned top = (lane + 1) * w;  // one past the sign bit of field `lane`
     const uint32_t* sp = seg + ((top - 1) >> 5) - 1;
-    const unsigned s = (0u - top) & 31u;
+    const unsigned s = 0u - top;          // the funnel shift takes it modulo 32
 #pragma unroll
     for (int g = GLO; g < GHI; ++g) acc[g] = fma(dec_fast(sp + (g - GLO) * w, s, mask, mul), coef, acc[g]);
 }
@@ -831,11 +831,17 @@ __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg
         const unsigned w = it.dpacked & 0xffu, e = (it.dpacked >> 16) & 0xffu;
         const uint32_t mask = fast_mask(w), mul = c_pow2e.v[e & 31u];
         const unsigned segw = (GHI - GLO) * w;
+        // sum d * x_c over the item's columns, then one alpha * scale multiply
+        double t[kG];
+#pragma unroll
+        for (int g = 0; g < kG; ++g) t[g] = 0.0;
 #pragma unroll 2
         for (unsigned c = 0; c < nseg; ++c) {
-            b_column_full<GLO, GHI>(seg, lane, w, mask, mul, dmul * cf[c], acc);
+            b_column_full<GLO, GHI>(seg, lane, w, mask, mul, cf[c], t);
             seg += segw;
         }
+#pragma unroll
+        for (int g = GLO; g < GHI; ++g) acc[g] = fma(dmul, t[g], acc[g]);
     } else {
         const WCol* wc = reinterpret_cast<const WCol*>(cf);  // staged records of the leaf's columns
         for (unsigned c = 0; c < nseg; ++c) {
