@@ -101,10 +101,16 @@ constexpr int kAUnroll = HCMX_AUNROLL;   // row groups per iteration of the phas
 constexpr uint64_t kAItemBytes = HCMX_AITEM;  // packed data per phase-A item
 constexpr uint32_t kAItemXBytes = 12288;  // staged x slices per phase-A item
 constexpr int kBDenseGroup = 8;       // max dense columns per B item
-constexpr int kBLRGroup = 16;         // max rank columns per B item
+#ifndef HCMX_BGROUP
+#define HCMX_BGROUP 16
+#endif
+#ifndef HCMX_BITEM
+#define HCMX_BITEM 4096
+#endif
+constexpr int kBLRGroup = HCMX_BGROUP;  // max columns per B item
 constexpr uint64_t kAStripeBytes = 8 * kStageBytes;  // target packed bytes per phase-A CTA
 constexpr uint64_t kItemTarget = 1536;          // packed bytes per item (columns grouped up to this)
-constexpr uint64_t kItemMaxBytes = 4096;        // items merge columns up to this many packed bytes
+constexpr uint64_t kItemMaxBytes = HCMX_BITEM;  // items merge columns up to this many packed bytes
 constexpr size_t kRingBytes = static_cast<size_t>(kNStage) * kSlotBytes;
 constexpr size_t kRedBytes = (kNWB / 2) * kR * sizeof(double);  // phase-B cross-warp reduction
 constexpr size_t kSmemBytes = kRingBytes + kRedBytes + 2 * kNStage * sizeof(uint64_t);  // + full, empty barriers
