@@ -183,6 +183,9 @@ typedef struct hcmx_hmat_desc {
     uint64_t row_begin, row_end;
     /* nonzero: also build M^T (hmatrix.hpp:128 transpose; whole matrix only) */
     int with_transpose;
+    /* 4: also lay the matrix out for products with 4 right-hand sides at once
+     * (hcmx_gpu_hmat_matmat decodes every field once for 4 columns); 0: off */
+    int nrhs_block;
 } hcmx_hmat_desc;
 
 typedef struct hcmx_hmat hcmx_hmat; /* opaque, device resident */
@@ -216,6 +219,14 @@ int hcmx_gpu_hmat_matmat(hcmx_hmat* h, double alpha, const double* h_x, uint64_t
  * (for a partitioned handle only d_y[row_begin,row_end) is written) */
 int hcmx_gpu_hmat_matvec_device(hcmx_hmat* h, double alpha, const double* d_x, double beta,
                                 double* d_y, void* stream);
+
+/* Four right-hand sides at once through the multi-RHS arena (handles created
+ * with nrhs_block = 4): Y := alpha M X + beta Y with X (n_cols x 4) and Y
+ * (n_rows x 4) ROW-major on the device (the 4 columns interleaved), every
+ * packed field decoded once for the 4 columns.  Same stream rules as
+ * hcmx_gpu_hmat_matvec_device.  C5's multi-RHS products. */
+int hcmx_gpu_hmat_matmat4_device(hcmx_hmat* h, double alpha, const double* d_x4, double beta, double* d_y4,
+                                 void* stream);
 
 /* the handle of M^T inside a handle created with with_transpose (owned by h;
  * use it with the _device / _timing calls) */

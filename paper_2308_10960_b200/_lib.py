@@ -46,7 +46,8 @@ class hcmx_hmat_desc(C.Structure):
                 ("sigma", C.POINTER(C.c_double)), ("desc", C.POINTER(hcmx_descriptor)),
                 ("count", _pi64), ("poff", _pi64), ("plen", _pi64),
                 ("blob", C.c_void_p), ("blob_on_device", C.c_int),
-                ("row_begin", C.c_uint64), ("row_end", C.c_uint64), ("with_transpose", C.c_int)]
+                ("row_begin", C.c_uint64), ("row_end", C.c_uint64), ("with_transpose", C.c_int),
+                ("nrhs_block", C.c_int)]
 
 
 class hcmx_memory_report(C.Structure):
@@ -99,6 +100,7 @@ PROTOTYPES = {
     "hcmx_gpu_hmat_matvec": (_i, [_vp, _d, _vp, _d, _vp, _i]),
     "hcmx_gpu_hmat_matmat": (_i, [_vp, _d, _vp, _u64, _u64, _d, _vp, _u64, _i]),
     "hcmx_gpu_hmat_matvec_device": (_i, [_vp, _d, _vp, _d, _vp, _vp]),
+    "hcmx_gpu_hmat_matmat4_device": (_i, [_vp, _d, _vp, _d, _vp, _vp]),
     "hcmx_gpu_hmat_transposed": (_i, [_vp, C.POINTER(_vp)]),
     "hcmx_gpu_hmat_export_buffer": (_i, [_vp, _u64, _vp, _u64, _pu64]),
     "hcmx_gpu_hmat_last_launches": (_i, [_vp]),

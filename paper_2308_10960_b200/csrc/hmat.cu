@@ -91,6 +91,10 @@ constexpr int kAChunk = 64;           // rows of a leaf's X columns per phase-A 
 constexpr int kARows = 4;             // rows per word-padded group of a phase-A item
 constexpr int kALanes = 32;           // rank columns per phase-A item
 constexpr int kAGroupMax = 8;         // chunks of one rank column summed in-warp
+#ifndef HCMX_AGROUP_MULTI
+#define HCMX_AGROUP_MULTI 2
+#endif
+constexpr uint32_t kAGroupMaxMulti = HCMX_AGROUP_MULTI;  // the same for multi-RHS arenas
 #ifndef HCMX_AUNROLL
 #define HCMX_AUNROLL 4
 #endif
@@ -150,6 +154,17 @@ struct WCol {
 };
 static_assert(sizeof(WCol) == 32, "WCol layout");
 
+// Products with R right-hand sides at once (decode once, R FMAs per value):
+// rank-column records carry R phase-A results, {double c[R]; mask, mul,
+// packed, w}, 16-byte aligned; R = 1 is the WCol layout above.
+template <int R>
+__host__ __device__ constexpr int rec_bytes() { return R == 1 ? 32 : (8 * R + 16 + 15) / 16 * 16; }
+constexpr int kMultiR = 4;    // right-hand sides per product of a multi-RHS arena
+constexpr int kNWBMulti = 8;  // phase-B consumer warps for R > 1 (R x 4 accumulators per lane)
+inline uint32_t rec_bytes_rt(int R) { return R == 1 ? 32u : static_cast<uint32_t>((8 * R + 16 + 15) / 16 * 16); }
+template <int R>
+__host__ __device__ constexpr int nwb() { return R == 1 ? HCMX_NWB : kNWBMulti; }
+
 struct BItem {
     uint32_t word_off;   // packed data, from the warp-stage start
     uint8_t nseg;        // columns in this item
@@ -206,10 +221,12 @@ struct Params {
     unsigned* work;             // [2] stripe counters of the persistent kernels (A, B), zeroed per product
     uint32_t nstripe_a, nblocks;
     const double* coef;         // sigma_i * scale_X_i * scale_W_i
-    WCol* wcol;                 // per rank column: alpha * coef * (X^T x)_i (phase A) + W decoder constants
+    uint8_t* wrec;              // per rank column: record {c[R], mask, mul, packed, w} (rec_bytes<R>):
+                                // c = alpha * coef * (X^T x) per right-hand side (phase A) + W decoder constants
     double* partial;
-    const double* x;            // padded internal copy (16-byte aligned, readable + 16 B)
-    double* y;
+    const double* x;            // R = 1: padded internal copy (16-byte aligned, readable + 16 B);
+                                // R > 1: n x R, row-major (the R right-hand sides interleaved)
+    double* y;                  // R > 1: n x R, row-major
     uint32_t row_begin, row_end;
     double alpha, beta;
     int debug;                  // profiling knob (HCMX_DEBUG): 1 = consumers skip the decode
@@ -398,6 +415,7 @@ __device__ __forceinline__ void fence_proxy_async() {
 // (x or the phase-A results) plus the column parameters, all as cp.async.bulk
 // copies completing on the slot's full barrier.  Consumers never wait on global
 // memory.  The metadata of stage s+1 is fetched while waiting for a free slot.
+template <int R>
 __device__ __forceinline__ void issue_copy(const Params& p, uint64_t c, uint8_t* cdst, uint64_t* bar) {
     if (!(c >> 63)) return;
     const uint32_t idx = static_cast<uint32_t>(c);
@@ -405,8 +423,8 @@ __device__ __forceinline__ void issue_copy(const Params& p, uint64_t c, uint8_t*
     const unsigned bytes = static_cast<unsigned>((c >> 48) & 0xfffu) * 16u;
     const void* src;
     switch (static_cast<unsigned>((c >> 60) & 3u)) {
-        case 0: src = p.x + idx; break;
-        default: src = p.wcol + idx; break;
+        case 0: src = p.x + static_cast<size_t>(idx) * R; break;
+        default: src = p.wrec + static_cast<size_t>(idx) * rec_bytes<R>(); break;
     }
     bulk_g2s_plain(cdst + dst, src, bytes, bar);
 }
@@ -481,7 +499,7 @@ __device__ __forceinline__ StageMeta seq_meta(const Params& p, const StageSeq& q
 // on the slot's full barrier, plus a small header (stripe id, last-stage and
 // end flags) written before the copies.  The metadata of every stage is loaded
 // two stages ahead, so no global load sits on the producer's critical path.
-template <bool PHASE_A>
+template <bool PHASE_A, int R>
 __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_t* full, uint64_t* empty,
                                          unsigned lane) {
     const uint64_t policy = evict_first_policy();
@@ -538,8 +556,8 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
             }
             __syncwarp();
             if (!no_coef) {
-                issue_copy(p, cur.c0, base, &full[slot]);
-                issue_copy(p, cur.c1, base, &full[slot]);
+                issue_copy<R>(p, cur.c0, base, &full[slot]);
+                issue_copy<R>(p, cur.c1, base, &full[slot]);
             }
         }
         if (cur.flags & kHdrEnd) {
@@ -659,9 +677,11 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
 // Fast body: every lane's field is a codec field with w <= 32 and e <= 10
 // (dec_fast), the item has whole row groups and every lane's x slice is
 // 16-byte aligned.  Lane-constant (word, shift) per row of a group; the group
-// stride is gwords.
-__device__ __forceinline__ double a_fast(const uint32_t* data, unsigned P, unsigned w, unsigned e, const double* xs,
-                                         unsigned ngroups, unsigned rowbits, unsigned gwords) {
+// stride is gwords.  xs: this lane's x rows, R values per row.  R = 1 keeps one
+// FMA chain per row of the group, R > 1 one chain per right-hand side.
+template <int R>
+__device__ __forceinline__ void a_fast(const uint32_t* data, unsigned P, unsigned w, unsigned e, const double* xs,
+                                       unsigned ngroups, unsigned rowbits, unsigned gwords, double (&res)[R]) {
     const uint32_t mask = fast_mask(w);
     const uint32_t mul = c_pow2e.v[e & 31u];
     const uint32_t* q[kARows];
@@ -672,36 +692,62 @@ __device__ __forceinline__ double a_fast(const uint32_t* data, unsigned P, unsig
         q[r] = data + ((top - 1) >> 5) - 1;        // the word below the one holding the sign
         s[r] = 0u - top;                           // the funnel shift takes it modulo 32
     }
-    double acc[kARows] = {0.0, 0.0, 0.0, 0.0};  // one chain per row of the group
+    constexpr int NA = R == 1 ? kARows : R;
+    double acc[NA];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) acc[i] = 0.0;
 #pragma unroll kAUnroll
     for (unsigned g = 0; g < ngroups; ++g) {
-        const double2 x01 = reinterpret_cast<const double2*>(xs)[2 * g];
-        const double2 x23 = reinterpret_cast<const double2*>(xs)[2 * g + 1];
-        const double xv[kARows] = {x01.x, x01.y, x23.x, x23.y};
+        double xv[kARows * R];
+#pragma unroll
+        for (int i = 0; i < kARows * R / 2; ++i) {
+            const double2 t = reinterpret_cast<const double2*>(xs)[2 * R * g + i];
+            xv[2 * i] = t.x;
+            xv[2 * i + 1] = t.y;
+        }
 #pragma unroll
         for (int r = 0; r < kARows; ++r) {
-            acc[r] = fma(dec_fast(q[r], s[r], mask, mul), xv[r], acc[r]);
+            const double d = dec_fast(q[r], s[r], mask, mul);
+            if (R == 1) {
+                acc[r] = fma(d, xv[r], acc[r]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < R; ++c) acc[c % NA] = fma(d, xv[r * R + c], acc[c % NA]);
+            }
             q[r] += gwords;
         }
     }
-    return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    if (R == 1) res[0] = (acc[0] + acc[1]) + (acc[2 % NA] + acc[3 % NA]);
+    else {
+#pragma unroll
+        for (int c = 0; c < R; ++c) res[c] = acc[c % NA];
+    }
 }
 
 // Generic body: any layout (e = 11, w > 32, uncompressed words), any row count,
 // any x alignment -- the mode-2 decoder per field.
-__device__ __forceinline__ double a_generic(const uint32_t* data, unsigned P, uint32_t rec, const double* xs,
-                                            unsigned nf, unsigned rowbits, unsigned gwords) {
+template <int R>
+__device__ __forceinline__ void a_generic(const uint32_t* data, unsigned P, uint32_t rec, const double* xs,
+                                          unsigned nf, unsigned rowbits, unsigned gwords, double (&res)[R]) {
     const unsigned w = rec & 127u, e = (rec >> 7) & 15u, m = (rec >> 11) & 63u, fmt = (rec >> 17) & 3u;
     const uint32_t packed = w | (m << 8) | (e << 16) | ((fmt ? fmt + 2u : 2u) << 24);  // 1-3: raw f64 / f32 / f16
-    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < R; ++c) res[c] = 0.0;
     for (unsigned j = 0; j < nf; ++j) {
         const unsigned bit = P + (j % kARows) * rowbits;
         const uint32_t* sp = data + (j / kARows) * gwords + (bit >> 5);
-        acc = fma(dec_generic(sp, packed, bit & 31u), xs[j], acc);
+        const double d = dec_generic(sp, packed, bit & 31u);
+#pragma unroll
+        for (int c = 0; c < R; ++c) res[c] = fma(d, xs[j * R + c], res[c]);
     }
-    return acc;
 }
 
+template <int R>
+__device__ __forceinline__ double* rec_c(const Params& p, uint32_t col) {
+    return reinterpret_cast<double*>(p.wrec + static_cast<size_t>(col) * rec_bytes<R>());
+}
+
+template <int R>
 __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const uint8_t* slot, unsigned lane) {
     const unsigned nl = it.nl;  // lane records
     const uint32_t* recs = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
@@ -723,15 +769,25 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
     P = act ? P - w : 0u;
     const uint32_t* data = recs + ((nl + 3u) & ~3u);
     const double* xs = reinterpret_cast<const double*>(slot) + (rec >> 19);
-    double r = it.body ? a_fast(data, P, w, (rec >> 7) & 15u, xs, it.nf / kARows, it.rowbits, it.gwords)
-                       : a_generic(data, P, rec, xs, it.nf, it.rowbits, it.gwords);
+    double r[R];
+    if (it.body) a_fast<R>(data, P, w, (rec >> 7) & 15u, xs, it.nf / kARows, it.rowbits, it.gwords, r);
+    else a_generic<R>(data, P, rec, xs, it.nf, it.rowbits, it.gwords, r);
     // the chunks of a slot's rank column (lanes slot, slot + nslot, ...): fixed
     // butterfly (lane `slot` gets the same order on every run); idle lanes add 0
-    if (!act) r = 0.0;
-    for (unsigned o = nslot; o < 32u; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+        if (!act) r[c] = 0.0;
+        for (unsigned o = nslot; o < 32u; o <<= 1) r[c] += __shfl_xor_sync(0xffffffffu, r[c], o);
+    }
     if (!act || lane >= nslot) return;
-    if (it.final_) p.wcol[dest].c = p.alpha * cf * r;
-    else p.partial[dest] = r;
+    if (it.final_) {
+        double* out = rec_c<R>(p, dest);
+#pragma unroll
+        for (int c = 0; c < R; ++c) out[c] = p.alpha * cf * r[c];
+    } else {
+#pragma unroll
+        for (int c = 0; c < R; ++c) p.partial[static_cast<size_t>(dest) * R + c] = r[c];
+    }
 }
 
 // A leaf wider than one chunk: every chunk item writes partial sums, k_reduce
@@ -748,6 +804,7 @@ struct RedCol {
 // j + 32, ... and a fixed butterfly finishes the sum (lane 0's order is the
 // same on every run).  The rest take one thread each with independent loads.
 constexpr uint32_t kRedLong = 16;  // chunks from which a column gets a warp
+template <int R>
 __global__ void k_reduce(Params p, const RedCol* rc, uint32_t nlong, uint32_t n) {
     pdl_trigger();
     pdl_wait();  // the partials of phase A
@@ -756,46 +813,63 @@ __global__ void k_reduce(Params p, const RedCol* rc, uint32_t nlong, uint32_t n)
         const uint32_t i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31u;
         if (i >= nlong) return;
         const RedCol r = rc[i];
-        double s0 = 0.0, s1 = 0.0;
-        uint32_t ch = lane;
-        for (; ch + 32 < r.nchunks; ch += 64) {
-            s0 += p.partial[r.p0 + ch * r.stride];
-            s1 += p.partial[r.p0 + (ch + 32) * r.stride];
-        }
-        if (ch < r.nchunks) s0 += p.partial[r.p0 + ch * r.stride];
-        double s = s0 + s1;
+        const double cf = p.alpha * p.coef[r.col];
+        double* out = rec_c<R>(p, r.col);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) p.wcol[r.col].c = p.alpha * p.coef[r.col] * s;
+        for (int c = 0; c < R; ++c) {
+            double s0 = 0.0, s1 = 0.0;
+            uint32_t ch = lane;
+            for (; ch + 32 < r.nchunks; ch += 64) {
+                s0 += p.partial[static_cast<size_t>(r.p0 + ch * r.stride) * R + c];
+                s1 += p.partial[static_cast<size_t>(r.p0 + (ch + 32) * r.stride) * R + c];
+            }
+            if (ch < r.nchunks) s0 += p.partial[static_cast<size_t>(r.p0 + ch * r.stride) * R + c];
+            double s = s0 + s1;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) out[c] = cf * s;
+        }
         return;
     }
     const uint32_t i = nlong + (blockIdx.x - long_blocks) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const RedCol r = rc[i];
-    double s[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains, fixed order
+    const double cf = p.alpha * p.coef[r.col];
+    double* out = rec_c<R>(p, r.col);
 #pragma unroll
-    for (uint32_t ch = 0; ch < kRedLong; ++ch)
-        if (ch < r.nchunks) s[ch & 3u] += p.partial[r.p0 + ch * r.stride];
-    p.wcol[r.col].c = p.alpha * p.coef[r.col] * ((s[0] + s[1]) + (s[2] + s[3]));
+    for (int c = 0; c < R; ++c) {
+        double s[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains, fixed order
+#pragma unroll
+        for (uint32_t ch = 0; ch < kRedLong; ++ch)
+            if (ch < r.nchunks) s[ch & 3u] += p.partial[static_cast<size_t>(r.p0 + ch * r.stride) * R + c];
+        out[c] = cf * ((s[0] + s[1]) + (s[2] + s[3]));
+    }
 }
 
 // ------------------------------------------------------------ phase B ----
+// acc[g * R + c]: rows 32 g + lane of the block, right-hand side c.
 // generic path: any layout, any row offset / count (lanes individually predicated)
+template <int R>
 __device__ __forceinline__ void b_column(const uint32_t* seg, uint32_t packed, unsigned w, int f0, unsigned vmask,
-                                         unsigned umask, double coef, double (&acc)[kG]) {
+                                         unsigned umask, const double (&coef)[R], double (&acc)[kG * R]) {
     const int bit0 = f0 * static_cast<int>(w);
     const uint32_t* sp = seg + (bit0 >> 5);
     const unsigned sh = static_cast<unsigned>(bit0) & 31u;
 #pragma unroll
     for (int g = 0; g < kG; ++g) {
         if (umask & (1u << g)) {
-            if (vmask & (1u << g)) acc[g] = fma(dec_generic(sp + g * w, packed, sh), coef, acc[g]);
+            if (vmask & (1u << g)) {
+                const double d = dec_generic(sp + g * w, packed, sh);
+#pragma unroll
+                for (int c = 0; c < R; ++c) acc[g * R + c] = fma(d, coef[c], acc[g * R + c]);
+            }
         }
     }
 }
 
+template <int R>
 __device__ __forceinline__ void b_item_generic(const BItem& it, const uint32_t* seg, const double* cf, unsigned lane,
-                                               double dmul, double (&acc)[kG]) {
+                                               double dmul, double (&acc)[kG * R]) {
     const unsigned nseg = it.nseg, nr = it.nr;
     // lane owns rows 32 g + lane of the block; field index f0 + 32 g in each segment
     const int f0 = static_cast<int>(lane) - static_cast<int>(it.ra);
@@ -806,12 +880,15 @@ __device__ __forceinline__ void b_item_generic(const BItem& it, const uint32_t* 
         if (f >= 0 && f < static_cast<int>(nr)) vmask |= 1u << g;
     }
     const unsigned umask = __reduce_or_sync(0xffffffffu, vmask);
-    const WCol* wc = reinterpret_cast<const WCol*>(cf);
+    const uint8_t* wc = reinterpret_cast<const uint8_t*>(cf);
     for (unsigned c = 0; c < nseg; ++c) {
-        const uint32_t pw = it.kind == 0 ? it.dpacked : wc[c].packed;
+        const double* rc = reinterpret_cast<const double*>(wc + c * rec_bytes<R>());
+        const uint32_t pw = it.kind == 0 ? it.dpacked : reinterpret_cast<const uint32_t*>(rc + R)[2];
         const unsigned w = pw & 0xffu;
-        const double cc = it.kind == 0 ? dmul * cf[c] : wc[c].c;
-        b_column(seg, pw, w, f0, vmask, umask, cc, acc);
+        double cc[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) cc[q] = it.kind == 0 ? dmul * cf[c * R + q] : rc[q];
+        b_column<R>(seg, pw, w, f0, vmask, umask, cc, acc);
         seg += (nr * w + 31) >> 5;
     }
 }
@@ -819,51 +896,81 @@ __device__ __forceinline__ void b_item_generic(const BItem& it, const uint32_t* 
 // fast path: the item covers row groups [GLO, GHI) of the block completely and
 // every column decodes with dec_fast: lane l takes field l + 32 (g - GLO) of
 // each column segment, at the same shift in every group (32 fields = w words)
-template <int GLO, int GHI>
+template <int GLO, int GHI, int R>
 __device__ __forceinline__ void b_column_full(const uint32_t* seg, unsigned lane, unsigned w, uint32_t mask,
-                                              uint32_t mul, double coef, double (&acc)[kG]) {
+                                              uint32_t mul, const double (&coef)[R], double (&acc)[kG * R]) {
     const unsigned top = (lane + 1) * w;  // one past the sign bit of field `lane`
     const uint32_t* sp = seg + ((top - 1) >> 5) - 1;
     const unsigned s = 0u - top;          // the funnel shift takes it modulo 32
 #pragma unroll
-    for (int g = GLO; g < GHI; ++g) acc[g] = fma(dec_fast(sp + (g - GLO) * w, s, mask, mul), coef, acc[g]);
+    for (int g = GLO; g < GHI; ++g) {
+        const double d = dec_fast(sp + (g - GLO) * w, s, mask, mul);
+#pragma unroll
+        for (int c = 0; c < R; ++c) acc[g * R + c] = fma(d, coef[c], acc[g * R + c]);
+    }
 }
 
-template <int GLO, int GHI>
+template <int GLO, int GHI, int R>
 __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg, const double* cf, unsigned lane,
-                                            double dmul, double (&acc)[kG]) {
+                                            double dmul, double (&acc)[kG * R]) {
     const unsigned nseg = it.nseg;
     if (it.kind == 0) {  // dense: one layout for the whole item
         const unsigned w = it.dpacked & 0xffu, e = (it.dpacked >> 16) & 0xffu;
         const uint32_t mask = fast_mask(w), mul = c_pow2e.v[e & 31u];
         const unsigned segw = (GHI - GLO) * w;
-        // sum d * x_c over the item's columns, then one alpha * scale multiply
-        double t[kG];
+        if (R == 1) {
+            // sum d * x_c over the item's columns, then one alpha * scale multiply
+            double t[kG * R];
 #pragma unroll
-        for (int g = 0; g < kG; ++g) t[g] = 0.0;
+            for (int g = 0; g < kG * R; ++g) t[g] = 0.0;
 #pragma unroll 2
-        for (unsigned c = 0; c < nseg; ++c) {
-            b_column_full<GLO, GHI>(seg, lane, w, mask, mul, cf[c], t);
-            seg += segw;
-        }
+            for (unsigned c = 0; c < nseg; ++c) {
+                const double xc[R] = {cf[c]};
+                b_column_full<GLO, GHI, R>(seg, lane, w, mask, mul, xc, t);
+                seg += segw;
+            }
 #pragma unroll
-        for (int g = GLO; g < GHI; ++g) acc[g] = fma(dmul, t[g], acc[g]);
+            for (int g = GLO; g < GHI; ++g) acc[g] = fma(dmul, t[g], acc[g]);
+        } else {
+            for (unsigned c = 0; c < nseg; ++c) {
+                double xc[R];
+#pragma unroll
+                for (int q = 0; q < R; ++q) xc[q] = dmul * cf[c * R + q];
+                b_column_full<GLO, GHI, R>(seg, lane, w, mask, mul, xc, acc);
+                seg += segw;
+            }
+        }
     } else {
-        const WCol* wc = reinterpret_cast<const WCol*>(cf);  // staged records of the leaf's columns
+        const uint8_t* wc = reinterpret_cast<const uint8_t*>(cf);  // staged records of the leaf's columns
         for (unsigned c = 0; c < nseg; ++c) {
-            // the record as two 16-byte loads: {c, mask, mul}, {packed, w, -, -}
-            const uint4 q0 = reinterpret_cast<const uint4*>(wc + c)[0];
-            const uint4 q1 = reinterpret_cast<const uint4*>(wc + c)[1];
-            const double cc = __hiloint2double(static_cast<int>(q0.y), static_cast<int>(q0.x));
-            const unsigned w = q1.y;
-            b_column_full<GLO, GHI>(seg, lane, w, q0.z, q0.w, cc, acc);
+            const uint8_t* rp = wc + c * rec_bytes<R>();
+            double cc[R];
+            uint32_t mask, mul, w;
+            if (R == 1) {
+                // the record as two 16-byte loads: {c, mask, mul}, {packed, w, -, -}
+                const uint4 q0 = reinterpret_cast<const uint4*>(rp)[0];
+                const uint4 q1 = reinterpret_cast<const uint4*>(rp)[1];
+                cc[0] = __hiloint2double(static_cast<int>(q0.y), static_cast<int>(q0.x));
+                mask = q0.z;
+                mul = q0.w;
+                w = q1.y;
+            } else {
+#pragma unroll
+                for (int q = 0; q < R; ++q) cc[q] = reinterpret_cast<const double*>(rp)[q];
+                const uint4 pr = *reinterpret_cast<const uint4*>(rp + 8 * R);  // {mask, mul, packed, w}
+                mask = pr.x;
+                mul = pr.y;
+                w = pr.w;
+            }
+            b_column_full<GLO, GHI, R>(seg, lane, w, mask, mul, cc, acc);
             seg += (GHI - GLO) * w;
         }
     }
 }
 
+template <int R>
 __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const uint8_t* slot, unsigned lane,
-                                       double (&acc)[kG]) {
+                                       double (&acc)[kG * R]) {
     const double* cf = reinterpret_cast<const double*>(slot + it.coef_off);
     const double dmul = p.alpha * it.scale;  // dense: alpha * buffer scale folded into x
     const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
@@ -872,20 +979,22 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
     // which keeps the kernel inside the instruction cache
     static_assert(kG == 4, "fast-path table assumes 128-row blocks");
     switch (it.fcase) {  // the body index, precomputed by bcase_of (a dense jump table)
-        case 1: b_item_full<0, 4>(it, seg, cf, lane, dmul, acc); break;
-        case 2: b_item_full<0, 2>(it, seg, cf, lane, dmul, acc); break;
-        case 3: b_item_full<2, 4>(it, seg, cf, lane, dmul, acc); break;
+        case 1: b_item_full<0, 4, R>(it, seg, cf, lane, dmul, acc); break;
+        case 2: b_item_full<0, 2, R>(it, seg, cf, lane, dmul, acc); break;
+        case 3: b_item_full<2, 4, R>(it, seg, cf, lane, dmul, acc); break;
         default:
-            b_item_generic(it, seg, cf, lane, dmul, acc);  // also uncompressed words (modes 3-5)
+            b_item_generic<R>(it, seg, cf, lane, dmul, acc);  // also uncompressed words (modes 3-5)
             break;
     }
 }
 
+template <int NW>
 __device__ __forceinline__ void consumer_bar() {  // the consumer warps of phase B only
-    asm volatile("bar.sync 1, %0;" ::"n"(kNWB * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
 }
 
 // Persistent kernels: one CTA per resident slot, stripes claimed dynamically.
+template <int R>
 __global__ void __launch_bounds__(kThreadsA, 2) k_phase_a(Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kRedBytes);
@@ -900,67 +1009,73 @@ __global__ void __launch_bounds__(kThreadsA, 2) k_phase_a(Params p) {
     ring_init<kNWA>(full, empty);
     pdl_trigger();
     if (warp == kNWA) {
-        producer<true>(p, smem, full, empty, lane);
+        producer<true, R>(p, smem, full, empty, lane);
         return;
     }
     consume<kNWA, true>(
         smem, full, empty, warp, lane, dbg(p),
         [&](const uint8_t* base, unsigned i) {
-            a_item(p, reinterpret_cast<const AItem*>(base)[i], base, lane);
+            a_item<R>(p, reinterpret_cast<const AItem*>(base)[i], base, lane);
         },
         [](uint32_t) {});
 }
 
-__global__ void __launch_bounds__(kThreadsB, 2) k_phase_b(Params p) {
+template <int R>
+__global__ void __launch_bounds__((nwb<R>() + 1) * 32, 2) k_phase_b(Params p) {
+    constexpr int NW = nwb<R>();
     extern __shared__ __align__(128) uint8_t smem[];
     double* red = reinterpret_cast<double*>(smem + kRingBytes);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kRedBytes);
     uint64_t* empty = full + kNStage;
     const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    ring_init<kNWB>(full, empty);
-    if (warp == kNWB) {
-        producer<false>(p, smem, full, empty, lane);
+    ring_init<NW>(full, empty);
+    if (warp == NW) {
+        producer<false, R>(p, smem, full, empty, lane);
         return;
     }
-    double acc[kG];
+    double acc[kG * R];
 #pragma unroll
-    for (int g = 0; g < kG; ++g) acc[g] = 0.0;
-    constexpr unsigned H = kNWB / 2;
-    consume<kNWB, false>(
+    for (int g = 0; g < kG * R; ++g) acc[g] = 0.0;
+    constexpr unsigned H = NW / 2;
+    static_assert(H * kR * sizeof(double) <= kRedBytes, "phase-B reduction buffer");
+    consume<NW, false>(
         smem, full, empty, warp, lane, dbg(p),
         [&](const uint8_t* base, unsigned i) {
-            b_item(p, reinterpret_cast<const BItem*>(base)[i], base, lane, acc);
+            b_item<R>(p, reinterpret_cast<const BItem*>(base)[i], base, lane, acc);
         },
         [&](uint32_t sid) {  // block done: fixed-order pairwise sum of the warps, then y
             const uint32_t blk = p.stripe_b[sid].z;
-            consumer_bar();
-            if (warp >= H) {
-#pragma unroll
-                for (int g = 0; g < kG; ++g) red[(warp - H) * kR + 32 * g + lane] = acc[g];
-            }
-            consumer_bar();
-            if (warp < H) {
-#pragma unroll
-                for (int g = 0; g < kG; ++g) acc[g] += red[warp * kR + 32 * g + lane];
-            }
-            consumer_bar();
-            if (warp < H) {
-#pragma unroll
-                for (int g = 0; g < kG; ++g) red[warp * kR + 32 * g + lane] = acc[g];
-            }
-            consumer_bar();
             const uint32_t r0 = p.row_begin + blk * kR;
             const uint32_t nrows = min(static_cast<uint32_t>(kR), p.row_end - r0);
-            if (tid < nrows) {
-                double sum = 0.0;
 #pragma unroll
-                for (unsigned wv = 0; wv < H; ++wv) sum += red[wv * kR + tid];
-                double* yp = p.y + r0 + tid;
-                *yp = p.beta == 0.0 ? sum : fma(p.beta, *yp, sum);
+            for (int c = 0; c < R; ++c) {  // one right-hand side at a time through the buffer
+                consumer_bar<NW>();
+                if (warp >= H) {
+#pragma unroll
+                    for (int g = 0; g < kG; ++g) red[(warp - H) * kR + 32 * g + lane] = acc[g * R + c];
+                }
+                consumer_bar<NW>();
+                if (warp < H) {
+#pragma unroll
+                    for (int g = 0; g < kG; ++g) acc[g * R + c] += red[warp * kR + 32 * g + lane];
+                }
+                consumer_bar<NW>();
+                if (warp < H) {
+#pragma unroll
+                    for (int g = 0; g < kG; ++g) red[warp * kR + 32 * g + lane] = acc[g * R + c];
+                }
+                consumer_bar<NW>();
+                if (tid < nrows) {
+                    double sum = 0.0;
+#pragma unroll
+                    for (unsigned wv = 0; wv < H; ++wv) sum += red[wv * kR + tid];
+                    double* yp = p.y + static_cast<size_t>(r0 + tid) * R + c;
+                    *yp = p.beta == 0.0 ? sum : fma(p.beta, *yp, sum);
+                }
             }
-            consumer_bar();
+            consumer_bar<NW>();
 #pragma unroll
-            for (int g = 0; g < kG; ++g) acc[g] = 0.0;
+            for (int g = 0; g < kG * R; ++g) acc[g] = 0.0;
         });
 }
 
@@ -1042,6 +1157,7 @@ using namespace hcmx_gpu;
 
 struct hcmx_hmat {
     uint64_t n_rows = 0, n_cols = 0, rb = 0, re = 0;
+    int R = 1;                   // right-hand sides per product of this arena (1 or kMultiR)
     DevBuf arena, stages, stripe_a, stripe_b, copies, work, wcol, coef, partial,
         redcols, xpad, xbuf, ybuf;
     uint32_t nstripe_a = 0, nblocks = 0, nlr = 0, nred = 0, nred_long = 0;
@@ -1060,6 +1176,7 @@ struct hcmx_hmat {
     double ms_a = 0, ms_b = 0;
     uint64_t calls = 0;
     hcmx_hmat* trans = nullptr;  // M^T (hmatrix.hpp:128 transpose), built on request
+    hcmx_hmat* multi = nullptr;  // the same matrix laid out for kMultiR right-hand sides (matmat)
 };
 
 namespace {
@@ -1181,7 +1298,9 @@ struct Builder {
                (static_cast<uint64_t>(dst / 16) << 32) | idx;
     }
 
-    Builder(const hcmx_hmat_desc& dd, hcmx_hmat* hh) : d(dd), h(hh) {}
+    int R = 1;  // right-hand sides: x / coefficient elements are R doubles wide
+
+    Builder(const hcmx_hmat_desc& dd, hcmx_hmat* hh) : d(dd), h(hh), R(hh->R) {}
 
     // the bytes a stage's copies deliver must be exactly what its full barrier
     // expects, or the consumers would wait forever
@@ -1251,7 +1370,7 @@ struct Builder {
         };
         std::vector<Slice> slices;
         uint32_t coef = 0, data_bytes = 0;
-        auto esize = [](uint32_t table) { return table == 0 ? 8u : static_cast<uint32_t>(sizeof(WCol)); };
+        auto esize = [&](uint32_t table) { return table == 0 ? 8u * R : rec_bytes_rt(R); };
         auto slice_bytes = [&](const Slice& s) { return r16((s.end - s.start) * esize(s.table)); };
         std::vector<size_t> cut = {pos, end};
         if (NW > 0) {
@@ -1415,7 +1534,7 @@ struct Builder {
                     bool seen = false;  // x slice already counted for this item
                     for (size_t u = i; u < q && !seen; ++u) seen = lanes[u].xidx == lanes[q].xidx && lanes[u].nf == lanes[q].nf;
                     if (!seen) {
-                        xb += r16((lanes[q].nf + 2) * 8ull);
+                        xb += r16((lanes[q].nf + 2) * 8ull * R);
                         ++ns;
                     }
                 }
@@ -1495,14 +1614,14 @@ struct Builder {
                 x.start -= 1;
             }
             x.off = coef;
-            copied += r16((x.end - x.start) * 8ull);
-            coef += r16((x.end - x.start) * 8ull) + (x.pad ? 16u : 0u);
+            copied += r16((x.end - x.start) * 8ull * R);
+            coef += r16((x.end - x.start) * 8ull * R) + (x.pad ? 16u : 0u);
         }
         if (coef > static_cast<uint32_t>(kSlotData) || merged.size() > static_cast<size_t>(kCopies)) return false;
         auto xoff = [&](const ALane& L) -> uint32_t {  // coef-area offset of x[xidx], in doubles
             const uint32_t pad = L.G > 1 ? 1u : 0u;
             for (const Slice& x : merged)
-                if (x.pad == pad && x.start <= L.xidx && L.xidx + L.nf <= x.end) return x.off / 8 + (L.xidx - x.start);
+                if (x.pad == pad && x.start <= L.xidx && L.xidx + L.nf <= x.end) return x.off / 8 + (L.xidx - x.start) * static_cast<uint32_t>(R);
             throw std::logic_error("hmat: x slice");
         };
         // descriptors largest first (warps claim a stage's items in order)
@@ -1512,7 +1631,7 @@ struct Builder {
         const size_t c0 = copies.size();
         copies.resize(c0 + kCopies, 0);
         for (size_t q = 0; q < merged.size(); ++q)
-            copies[c0 + q] = copy_entry(merged[q].start, merged[q].off, r16((merged[q].end - merged[q].start) * 8ull), 0);
+            copies[c0 + q] = copy_entry(merged[q].start, merged[q].off, r16((merged[q].end - merged[q].start) * 8ull * R), 0);
         while (arena.size() % 4) arena.push_back(0u);
         const uint64_t start = arena.size();
         arena.resize(start + ord.size() * (kItemBytes / 4), 0u);
@@ -1773,7 +1892,10 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                 const uint64_t cols = static_cast<uint64_t>(cols_of(id));
                 const uint32_t nfull = static_cast<uint32_t>(cols / kAChunk), rag = static_cast<uint32_t>(cols % kAChunk);
                 uint32_t G = 1;
-                while (2 * G <= static_cast<uint32_t>(kAGroupMax) && nfull % (2 * G) == 0) G *= 2;
+                // R right-hand sides stage R x slices per chunk: smaller segments
+                // keep a segment's x (G chunks x 64 rows x R doubles) a fraction of a slot
+                const uint32_t gmax = h->R == 1 ? static_cast<uint32_t>(kAGroupMax) : kAGroupMaxMulti;
+                while (2 * G <= gmax && nfull % (2 * G) == 0) G *= 2;
                 const uint32_t ngrp = nfull / G + (rag ? 1u : 0u);
                 L.colbase = ncols;
                 ncols += L.k;
@@ -1817,7 +1939,8 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         flush();
     }
     // rank-column tables in the order phase A assigned
-    std::vector<WCol> wcol(ncols + 4);  // + 4: bulk copies may round up past the last column
+    const uint32_t rb = rec_bytes_rt(h->R);
+    std::vector<uint8_t> wrec(static_cast<size_t>(ncols + 4) * rb, 0);  // + 4: bulk copies may round up
     std::vector<double> coef(ncols + 4, 0.0);
     for (uint32_t id = 0; id < leafa.size(); ++id) {
         const uint64_t l = lr_leaf[id];
@@ -1826,7 +1949,9 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
             const hcmx_descriptor& xw = d.desc[wbuf(l, i).first];
             const hcmx_descriptor& xx = d.desc[xbuf(l, i).first];
             const ColPar cp = col_par(xw);
-            wcol[leafa[id].colbase + i] = {0.0, cp.mask, cp.mul, cp.packed, xw.bit_width, 0u, 0u};
+            // record {c[R] (phase A writes it), mask, mul, packed, w}
+            const uint32_t par[4] = {cp.mask, cp.mul, cp.packed, xw.bit_width};
+            std::memcpy(wrec.data() + static_cast<size_t>(leafa[id].colbase + i) * rb + 8 * h->R, par, sizeof(par));
             coef[leafa[id].colbase + i] = (uniform ? 1.0 : d.sigma[d.sig0[l] + i]) * xx.scale * xw.scale;
         }
     }
@@ -1921,7 +2046,8 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                     }
                 }
             }
-            B.emit_stripe<BItem, kBLRGroup, kNWB>(specs, B.bitems);
+            if (h->R == 1) B.emit_stripe<BItem, kBLRGroup, kNWB>(specs, B.bitems);
+            else B.emit_stripe<BItem, kBLRGroup, kNWBMulti>(specs, B.bitems);
             stripe_b.push_back(static_cast<uint32_t>(B.stages.size()));
         }
     }
@@ -1981,11 +2107,11 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     const auto sa = lpt(stripe_a, false), sb = lpt(stripe_b, true);
     up(h->stripe_a, sa.data(), sa.size() * 16);
     up(h->stripe_b, sb.data(), sb.size() * 16);
-    up(h->wcol, wcol.data(), wcol.size() * sizeof(WCol));
+    up(h->wcol, wrec.data(), wrec.size());
     up(h->coef, coef.data(), coef.size() * 8);
     h->xpad.alloc((d.n_cols + 4) * 8);
     check_cuda(cudaMemsetAsync(h->xpad.p, 0, h->xpad.bytes, s), "memset");
-    h->partial.alloc(std::max<size_t>(16, npartial * 8));
+    h->partial.alloc(std::max<size_t>(16, npartial * 8 * h->R));
     // columns with >= kRedLong chunks first (one warp each in k_reduce)
     std::stable_partition(redcols.begin(), redcols.end(), [](const RedCol& r) { return r.nchunks >= kRedLong; });
     h->nred_long = static_cast<uint32_t>(
@@ -1998,7 +2124,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     rep.device_arena_bytes = B.arena.size() * 4;
     rep.device_table_bytes = B.stages.size() * (sizeof(Stage) + kCopies * 8) + B.bitems.size() * sizeof(BItem) +
                              B.a_items * sizeof(AItem) +
-                             wcol.size() * sizeof(WCol) + coef.size() * 8;
+                             wrec.size() + coef.size() * 8;
     rep.overhead = rep.device_table_bytes;
 }
 
@@ -2013,7 +2139,7 @@ Params make_params(hcmx_hmat* h, double alpha, double beta, double* y) {
     p.nstripe_a = h->nstripe_a;
     p.nblocks = h->nblocks;
     p.coef = h->coef.as<double>();
-    p.wcol = h->wcol.as<WCol>();
+    p.wrec = h->wcol.as<uint8_t>();
     p.partial = h->partial.as<double>();
     p.x = h->xpad.as<double>();  // padded, 16-byte aligned copy of x (bulk copies)
     p.y = y;
@@ -2024,27 +2150,32 @@ Params make_params(hcmx_hmat* h, double alpha, double beta, double* y) {
     return p;
 }
 
+// dx, dy: n-vectors (h->R == 1) or n x R row-major blocks (h->R == kMultiR)
 void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, double* dy, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        check_cuda(cudaFuncSetAttribute(k_phase_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
+        const int sm = static_cast<int>(kSmemBytes);
+        check_cuda(cudaFuncSetAttribute(k_phase_a<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        check_cuda(cudaFuncSetAttribute(k_phase_b<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        check_cuda(cudaFuncSetAttribute(k_phase_a<kMultiR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
                    "smem attr");
-        check_cuda(cudaFuncSetAttribute(k_phase_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
+        check_cuda(cudaFuncSetAttribute(k_phase_b<kMultiR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
                    "smem attr");
         attr_set = true;
     }
+    const int R = h->R;
     h->last_launches = 0;
     if (alpha == 0.0) {  // y = beta y without touching M
-        const uint64_t n = h->re - h->rb;
-        k_scale<<<(int)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, s>>>(dy + h->rb, n, beta);
+        const uint64_t n = (h->re - h->rb) * R;
+        k_scale<<<(int)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, s>>>(dy + h->rb * R, n, beta);
         check_cuda(cudaGetLastError(), "scale launch");
         h->last_launches = 1;
         return;
     }
     // x slices are bulk-copied from an even index in 16-byte units: read x in
     // place when that stays inside it (16-byte aligned, even length), else from
-    // the padded copy
-    const bool direct = dx == h->xpad.as<double>() ||
+    // the padded copy (R > 1: the caller's n x R block, allocated aligned)
+    const bool direct = R > 1 || dx == h->xpad.as<double>() ||
                         (reinterpret_cast<uintptr_t>(dx) % 16 == 0 && h->n_cols % 2 == 0);
     if (!direct) check_cuda(cudaMemcpyAsync(h->xpad.p, dx, h->n_cols * 8, cudaMemcpyDeviceToDevice, s), "x copy");
     Params p = make_params(h, alpha, beta, dy);
@@ -2083,12 +2214,20 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
         check_cuda(cudaLaunchKernelEx(&cfg, kernel, args...), "matvec launch");
         h->last_launches++;
     };
-    if (run_a) launch(k_phase_a, std::min<uint32_t>(h->nstripe_a, 2 * nsm), kThreadsA, kSmemBytes, false, p);
-    if (h->nred)
-        launch(k_reduce, (h->nred_long + 7) / 8 + (h->nred - h->nred_long + 255) / 256, 256, 0, true, p,
-               h->redcols.as<RedCol>(), h->nred_long, h->nred);
-    if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
-    if (h->nblocks) launch(k_phase_b, std::min<uint32_t>(h->nblocks, 2 * nsm), kThreadsB, kSmemBytes, run_a, p);
+    const uint32_t ga = std::min<uint32_t>(h->nstripe_a, 2 * nsm), gb = std::min<uint32_t>(h->nblocks, 2 * nsm);
+    const uint32_t gr = (h->nred_long + 7) / 8 + (h->nred - h->nred_long + 255) / 256;
+    const RedCol* rc = h->redcols.as<RedCol>();
+    if (R == 1) {
+        if (run_a) launch(k_phase_a<1>, ga, kThreadsA, kSmemBytes, false, p);
+        if (h->nred) launch(k_reduce<1>, gr, 256, 0, true, p, rc, h->nred_long, h->nred);
+        if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
+        if (h->nblocks) launch(k_phase_b<1>, gb, (nwb<1>() + 1) * 32, kSmemBytes, run_a, p);
+    } else {
+        if (run_a) launch(k_phase_a<kMultiR>, ga, kThreadsA, kSmemBytes, false, p);
+        if (h->nred) launch(k_reduce<kMultiR>, gr, 256, 0, true, p, rc, h->nred_long, h->nred);
+        if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
+        if (h->nblocks) launch(k_phase_b<kMultiR>, gb, (nwb<kMultiR>() + 1) * 32, kSmemBytes, run_a, p);
+    }
     check_cuda(cudaGetLastError(), "matvec launch");
 #ifdef HCMX_PROF
     static const bool prof_env = std::getenv("HCMX_PROF") != nullptr;
@@ -2226,6 +2365,7 @@ void make_transposed(const hcmx_hmat_desc& d, Transposed& t) {
 void destroy_handle(hcmx_hmat* h) {
     if (!h) return;
     destroy_handle(h->trans);
+    destroy_handle(h->multi);
     if (h->stream) cudaStreamSynchronize(h->stream);
     for (auto& r : h->pending) {
         cudaEventDestroy(r.a0);
@@ -2242,6 +2382,13 @@ hcmx_hmat* create_handle(const hcmx_hmat_desc& d) {
     try {
         check_cuda(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
         build(d, h);
+        if (d.nrhs_block) {
+            if (d.nrhs_block != kMultiR) throw invalid_argument("hmat: nrhs_block must be 0 or 4");
+            h->multi = new hcmx_hmat();
+            h->multi->R = kMultiR;
+            check_cuda(cudaStreamCreateWithFlags(&h->multi->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            build(d, h->multi);
+        }
         if (d.with_transpose) {
             if (d.row_begin != 0 || d.row_end != 0)
                 throw invalid_argument("hmat: the transpose needs the whole matrix (no row partition)");
@@ -2291,6 +2438,33 @@ int hcmx_gpu_hmat_matmat(hcmx_hmat* h, double alpha, const double* h_x, uint64_t
         }
         if (ldx < h->n_cols || ldy < h->n_rows) throw invalid_argument("matmat: leading dimension too small");
         if (!nrhs) return;
+        if (h->multi && nrhs >= 2) {
+            // blocks of kMultiR columns through the multi-RHS arena: each field is
+            // decoded once for the block (x and y interleaved n x kMultiR; a short
+            // last block is padded with zero columns)
+            hcmx_hmat* mh = h->multi;
+            constexpr uint64_t B = kMultiR;
+            const uint64_t n = h->n_cols, nr = h->re - h->rb;
+            DevBuf dx(n * B * 8), dy(h->n_rows * B * 8);
+            std::vector<double> hx(n * B), hy(nr * B);
+            for (uint64_t j0 = 0; j0 < nrhs; j0 += B) {
+                const uint64_t cnt = std::min<uint64_t>(B, nrhs - j0);
+                for (uint64_t i = 0; i < n; ++i)
+                    for (uint64_t c = 0; c < B; ++c) hx[i * B + c] = c < cnt ? h_x[(j0 + c) * ldx + i] : 0.0;
+                h2d(dx.p, hx.data(), n * B * 8, mh->stream);
+                if (beta != 0.0) {
+                    for (uint64_t i = 0; i < nr; ++i)
+                        for (uint64_t c = 0; c < B; ++c) hy[i * B + c] = c < cnt ? h_y[(j0 + c) * ldy + h->rb + i] : 0.0;
+                    h2d(dy.as<double>() + h->rb * B, hy.data(), nr * B * 8, mh->stream);
+                }
+                run_matvec(mh, alpha, dx.as<double>(), beta, dy.as<double>(), mh->stream);
+                d2h(hy.data(), dy.as<double>() + h->rb * B, nr * B * 8, mh->stream);
+                stream_sync(mh->stream);
+                for (uint64_t i = 0; i < nr; ++i)
+                    for (uint64_t c = 0; c < cnt; ++c) h_y[(j0 + c) * ldy + h->rb + i] = hy[i * B + c];
+            }
+            return;
+        }
         // all right-hand sides in one copy each way; one product per column
         DevBuf dx(h->n_cols * nrhs * 8), dy(h->n_rows * nrhs * 8);
         for (uint64_t j = 0; j < nrhs; ++j) h2d(dx.as<double>() + j * h->n_cols, h_x + j * ldx, h->n_cols * 8, h->stream);
@@ -2308,6 +2482,15 @@ int hcmx_gpu_hmat_matmat(hcmx_hmat* h, double alpha, const double* h_x, uint64_t
 int hcmx_gpu_hmat_matvec_device(hcmx_hmat* h, double alpha, const double* d_x, double beta, double* d_y,
                                 void* stream) {
     return guarded([&] { run_matvec(h, alpha, d_x, beta, d_y, (cudaStream_t)stream); });
+}
+
+int hcmx_gpu_hmat_matmat4_device(hcmx_hmat* h, double alpha, const double* d_x4, double beta, double* d_y4,
+                                 void* stream) {
+    return guarded([&] {
+        if (!h->multi) throw invalid_argument("matmat4: handle created without nrhs_block = 4");
+        if (reinterpret_cast<uintptr_t>(d_x4) % 16) throw invalid_argument("matmat4: x must be 16-byte aligned");
+        run_matvec(h->multi, alpha, d_x4, beta, d_y4, (cudaStream_t)stream);
+    });
 }
 
 int hcmx_gpu_hmat_matvec(hcmx_hmat* h, double alpha, const double* h_x, double beta, double* h_y,

@@ -380,7 +380,7 @@ class HMatrix:
     """Device-resident compressed H-matrix (handle over hcmx_gpu_hmat_*)."""
 
     def __init__(self, flat: FlatHMatrix, row_range: tuple[int, int] | None = None,
-                 with_transpose: bool = False):
+                 with_transpose: bool = False, nrhs_block: int = 0):
         _lib.ensure_device()
         self.n_rows, self.n_cols = int(flat.n_rows), int(flat.n_cols)
         self.row_range = row_range or (0, self.n_rows)
@@ -407,6 +407,7 @@ class HMatrix:
         d.blob_on_device = int(on_dev)
         d.row_begin, d.row_end = (0, 0) if row_range is None else row_range
         d.with_transpose = int(with_transpose)
+        d.nrhs_block = int(nrhs_block)  # 4: matmat decodes once for 4 right-hand sides
         h = C.c_void_p()
         check(lib().hcmx_gpu_hmat_create(C.byref(d), C.byref(h)), "hmat_create")
         self._h = h
@@ -439,6 +440,17 @@ class HMatrix:
         check(lib().hcmx_gpu_hmat_matvec_device(self._h, float(alpha), ptr(x), float(beta), ptr(y), s),
               "matvec")
         return y
+
+    def matmat4_device(self, alpha: float, X4: torch.Tensor, beta: float, Y4: torch.Tensor):
+        """Y4 := alpha M X4 + beta Y4 with X4 (n_cols, 4), Y4 (n_rows, 4) row-major
+        cuda float64 tensors, every field decoded once for the 4 columns (handle
+        built with nrhs_block=4), on the current stream"""
+        if X4.shape != (self.n_cols, 4) or Y4.shape != (self.n_rows, 4) or not (X4.is_contiguous() and
+                                                                             Y4.is_contiguous()):
+            raise ValueError("matmat4: contiguous (n, 4) float64 tensors required")
+        check(lib().hcmx_gpu_hmat_matmat4_device(self._h, float(alpha), ptr(X4), float(beta), ptr(Y4),
+                                                 torch.cuda.current_stream().cuda_stream), "matmat4")
+        return Y4
 
     def matvec(self, alpha: float, x, beta: float, y, transpose: bool = False):
         """hmatrix.hpp:126-128 with host vectors (copies in/out inside); transpose:
@@ -516,8 +528,8 @@ class ComplexHMatrix:
     product per real column), combined as Re Y = Ar Re X - Ai Im X,
     Im Y = Ar Im X + Ai Re X."""
 
-    def __init__(self, fr: FlatHMatrix, fi: FlatHMatrix):
-        self.re, self.im = HMatrix(fr), HMatrix(fi)
+    def __init__(self, fr: FlatHMatrix, fi: FlatHMatrix, nrhs_block: int = 4):
+        self.re, self.im = HMatrix(fr, nrhs_block=nrhs_block), HMatrix(fi, nrhs_block=nrhs_block)
         self.n_rows, self.n_cols = self.re.n_rows, self.re.n_cols
 
     def close(self):

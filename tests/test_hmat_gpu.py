@@ -254,3 +254,25 @@ def test_matmat_multi_rhs(gpu, oracle):
         for j in range(5):
             ref = oracle.hmat_matvec(f, 0.5, X[:, j], -1.0, Y0[:, j], threads=4, transpose=tr)
             assert rel(Y[:, j], ref) <= TOL, (tr, j)
+
+
+@pytest.mark.parametrize("mode,scheme,nrhs", [("aplr", 0, 4), ("aplr", 1, 7), ("codec", 2, 5), ("mp", 0, 2)])
+def test_multi_rhs_decode_once(gpu, oracle, mode, scheme, nrhs):
+    """matmat through the 4-right-hand-side arena (every field decoded once per
+    block of 4 columns; a short last block padded): each column equals the
+    oracle's product (ragged clusters, every leaf kind, alpha / beta)"""
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    n = 1100
+    f, _ = build_small_flat(n=n, eps=1e-6, scheme=scheme, mode=mode, geometry="sphere")
+    H = HMatrix(f.to_product(), nrhs_block=4)
+    rng = np.random.default_rng(11)
+    X = np.asfortranarray(rng.uniform(-1, 1, (n, nrhs)))
+    Y0 = np.asfortranarray(rng.standard_normal((n, nrhs)))
+    for alpha, beta in ((1.0, 0.0), (-0.7, 1.5)):
+        Y = Y0.copy(order="F")
+        H.matmat(alpha, X, beta, Y)
+        for j in range(nrhs):
+            ref = oracle.hmat_matvec(f, alpha, X[:, j], beta, Y0[:, j], threads=4)
+            assert rel(Y[:, j], ref) <= TOL, (alpha, beta, j)
+    H.close()

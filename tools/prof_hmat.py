@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--scheme", default="afl")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--cache", default=None)
+    ap.add_argument("--rhs4", action="store_true", help="also time the 4-right-hand-side arena")
     a = ap.parse_args()
     c = problems.config(a.config)
     if a.n:
@@ -53,7 +54,7 @@ def main():
             pickle.dump(h, open(a.cache, "wb"))
         del A
     t = time.time()
-    H = HMatrix(flat)
+    H = HMatrix(flat, nrhs_block=4 if a.rhs4 else 0)
     T["hmat_create"] = time.time() - t
     n = flat.n_rows
     x = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, n)).cuda()
@@ -80,7 +81,24 @@ def main():
           f"stagesA={r.stages_a} stagesB={r.stages_b} phaseA={ms_a/calls:.4f}ms phaseB={ms_b/calls:.4f}ms "
           f"total={(ms_a+ms_b)/calls:.4f}ms -> {r.algorithmic_bytes/((ms_a+ms_b)/calls)/1e6:.1f} GB/s "
           f"wall={wall:.4f}ms -> {r.algorithmic_bytes/wall/1e6:.1f} GB/s")
+    if a.rhs4:  # 4 right-hand sides decoded once vs 4 single products
+        X4 = torch.as_tensor(np.random.default_rng(1).uniform(-1, 1, (n, 4))).cuda().contiguous()
+        Y4 = torch.zeros(n, 4, dtype=torch.float64, device="cuda")
+        for _ in range(3):
+            H.matmat4_device(1.0, X4, 0.0, Y4)
+        e0.record()
+        for _ in range(a.iters):
+            H.matmat4_device(1.0, X4, 0.0, Y4)
+        e1.record()
+        torch.cuda.synchronize()
+        t4 = e0.elapsed_time(e1) / a.iters
+        ref = torch.stack([H.matvec_device(1.0, X4[:, c].contiguous(), 0.0, torch.zeros(n, dtype=torch.float64,
+                                                                                      device="cuda")) for c in range(4)], 1)
+        err = float((Y4 - ref).norm() / ref.norm())
+        print(f"rhs4: {t4:.4f} ms per 4-RHS product vs {4 * wall:.4f} ms for 4 products "
+              f"({4 * wall / t4:.2f}x), rel diff {err:.2e}")
 
 
 if __name__ == "__main__":
     main()
+
