@@ -942,6 +942,7 @@ __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg
         }
     } else {
         const uint8_t* wc = reinterpret_cast<const uint8_t*>(cf);  // staged records of the leaf's columns
+#pragma unroll 2
         for (unsigned c = 0; c < nseg; ++c) {
             const uint8_t* rp = wc + c * rec_bytes<R>();
             double cc[R];
