@@ -159,6 +159,7 @@ static_assert(sizeof(WCol) == 32, "WCol layout");
 // packed, w}, 16-byte aligned; R = 1 is the WCol layout above.
 template <int R>
 __host__ __device__ constexpr int rec_bytes() { return R == 1 ? 32 : (8 * R + 16 + 15) / 16 * 16; }
+constexpr uint32_t kMaxPieces = 4;  // pieces a phase-B row block may be split into
 constexpr int kMultiR = 4;    // right-hand sides per product of a multi-RHS arena
 constexpr int kNWBMulti = 8;  // phase-B consumer warps for R > 1 (R x 4 accumulators per lane)
 inline uint32_t rec_bytes_rt(int R) { return R == 1 ? 32u : static_cast<uint32_t>((8 * R + 16 + 15) / 16 * 16); }
@@ -216,10 +217,13 @@ struct Params {
     const uint8_t* arena;
     const Stage* stages;
     const uint4* stripe_a;      // [nstripe_a] {stage begin, end, -, -}, most expensive first
-    const uint4* stripe_b;      // [nblocks] {stage begin, end, row block, -}, most expensive first
+    const uint4* stripe_b;      // [nstripe_b] {stage begin, end, row block, piece}, most expensive first;
+                                // piece 0: the whole block, writes y; piece q > 0: part q - 1 of a
+                                // block split across CTAs, writes ypart (k_combine adds the parts)
     const uint64_t* copies;     // [nstages * kCopies] staged coefficient copies (see CopyEntry)
     unsigned* work;             // [2] stripe counters of the persistent kernels (A, B), zeroed per product
-    uint32_t nstripe_a, nblocks;
+    uint32_t nstripe_a, nblocks;  // nblocks: phase-B stripes (row blocks or their pieces)
+    double* ypart;              // [pieces][local rows][R] partial row sums of split blocks
     const double* coef;         // sigma_i * scale_X_i * scale_W_i
     uint8_t* wrec;              // per rank column: record {c[R], mask, mul, packed, w} (rec_bytes<R>):
                                 // c = alpha * coef * (X^T x) per right-hand side (phase A) + W decoder constants
@@ -1045,7 +1049,8 @@ __global__ void __launch_bounds__((nwb<R>() + 1) * 32, 2) k_phase_b(Params p) {
             b_item<R>(p, reinterpret_cast<const BItem*>(base)[i], base, lane, acc);
         },
         [&](uint32_t sid) {  // block done: fixed-order pairwise sum of the warps, then y
-            const uint32_t blk = p.stripe_b[sid].z;
+            const uint4 sr = p.stripe_b[sid];
+            const uint32_t blk = sr.z, piece = sr.w;
             const uint32_t r0 = p.row_begin + blk * kR;
             const uint32_t nrows = min(static_cast<uint32_t>(kR), p.row_end - r0);
 #pragma unroll
@@ -1070,14 +1075,38 @@ __global__ void __launch_bounds__((nwb<R>() + 1) * 32, 2) k_phase_b(Params p) {
                     double sum = 0.0;
 #pragma unroll
                     for (unsigned wv = 0; wv < H; ++wv) sum += red[wv * kR + tid];
-                    double* yp = p.y + static_cast<size_t>(r0 + tid) * R + c;
-                    *yp = p.beta == 0.0 ? sum : fma(p.beta, *yp, sum);
+                    if (piece == 0) {
+                        double* yp = p.y + static_cast<size_t>(r0 + tid) * R + c;
+                        *yp = p.beta == 0.0 ? sum : fma(p.beta, *yp, sum);
+                    } else {  // one part of a split block: k_combine adds the parts and beta y
+                        const size_t nl = p.row_end - p.row_begin;
+                        p.ypart[((piece - 1) * nl + (r0 - p.row_begin + tid)) * R + c] = sum;
+                    }
                 }
             }
             consumer_bar<NW>();
 #pragma unroll
             for (int g = 0; g < kG * R; ++g) acc[g] = 0.0;
         });
+}
+
+// Row blocks split into pieces (few blocks per GPU, e.g. one rank of a block-row
+// partition): y = beta y + sum of the pieces' partial sums, in piece order.
+template <int R>
+__global__ void k_combine(Params p, const uint8_t* npieces) {
+    pdl_trigger();
+    pdl_wait();  // phase B's partial sums
+    const size_t nl = p.row_end - p.row_begin;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < nl * R;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t row = i / R;
+        const unsigned q = npieces[row / kR];
+        if (q == 0) continue;
+        double sum = 0.0;
+        for (unsigned j = 0; j < q; ++j) sum += p.ypart[j * nl * R + i];
+        double* yp = p.y + p.row_begin * static_cast<size_t>(R) + i;
+        *yp = p.beta == 0.0 ? sum : fma(p.beta, *yp, sum);
+    }
 }
 
 __global__ void k_scale(double* y, uint64_t n, double beta) {
@@ -1161,7 +1190,8 @@ struct hcmx_hmat {
     int R = 1;                   // right-hand sides per product of this arena (1 or kMultiR)
     DevBuf arena, stages, stripe_a, stripe_b, copies, work, wcol, coef, partial,
         redcols, xpad, xbuf, ybuf;
-    uint32_t nstripe_a = 0, nblocks = 0, nlr = 0, nred = 0, nred_long = 0;
+    uint32_t nstripe_a = 0, nblocks = 0, nlr = 0, nred = 0, nred_long = 0, pieces = 0;
+    DevBuf npieces, ypart;  // split row blocks (pieces > 0): pieces per block, partial row sums
     hcmx_memory_report report{};
     std::vector<std::vector<SegRef>> segs;  // per buffer (export); empty if too big
     std::vector<hcmx_descriptor> desc;
@@ -2105,7 +2135,64 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         for (size_t i : ord) out.push_back(v[i]);
         return out;
     };
-    const auto sa = lpt(stripe_a, false), sb = lpt(stripe_b, true);
+    const auto sa = lpt(stripe_a, false);
+    // phase-B stripes: one row block each.  With too few blocks to keep every CTA
+    // slot busy (one rank of a block-row partition), a block is cut into up to
+    // kMaxPieces stage ranges of similar cost; their partial row sums go to
+    // ypart and k_combine adds them (fixed order, beta y once).
+    const uint64_t nb_rows = stripe_b.size() - 1;
+    const uint64_t want = 2ull * 148;  // one stripe per CTA slot
+    const char* mp_env = std::getenv("HCMX_MAX_PIECES");  // test / profiling knob (1: never split)
+    const uint64_t max_pieces = mp_env ? std::max(1, std::min(std::atoi(mp_env), static_cast<int>(kMaxPieces)))
+                                       : kMaxPieces;
+    // (measured on config 3 row partitions: 128 blocks split 3 ways 85 -> 71 us,
+    // 256 blocks split 2 ways 100 -> 109 us: only blocks fewer than the SMs split)
+    const uint32_t S = 2 * nb_rows > want ? 1u
+                                          : static_cast<uint32_t>(std::min<uint64_t>(max_pieces, (want + nb_rows - 1) / nb_rows));
+    std::vector<std::array<uint32_t, 4>> bv;
+    std::vector<uint64_t> bcost;
+    std::vector<uint8_t> npieces(std::max<uint64_t>(nb_rows, 1), 0);
+    for (uint64_t i = 0; i < nb_rows; ++i) {
+        const uint32_t s0 = stripe_b[i], s1 = stripe_b[i + 1];
+        const uint32_t P = std::min<uint32_t>(S, s1 - s0);
+        uint64_t total = 0;
+        for (uint32_t s2 = s0; s2 < s1; ++s2) total += B.stages[s2].pad;
+        if (P <= 1) {
+            bv.push_back({s0, s1, static_cast<uint32_t>(i), 0u});
+            bcost.push_back(total);
+            continue;
+        }
+        npieces[i] = static_cast<uint8_t>(P);
+        uint32_t a = s0;
+        uint64_t acc = 0;
+        for (uint32_t q = 0; q < P; ++q) {  // contiguous pieces, cut at cumulative cost q / P
+            uint32_t b = a;
+            uint64_t c = 0;
+            const uint64_t target = total * (q + 1) / P;
+            while (b < s1 && (q + 1 == P || (b == a || acc + c + B.stages[b].pad / 2 <= target)) &&
+                   s1 - b > P - 1 - q) {
+                c += B.stages[b].pad;
+                ++b;
+            }
+            if (q + 1 == P) {
+                while (b < s1) c += B.stages[b++].pad;
+            }
+            bv.push_back({a, b, static_cast<uint32_t>(i), q + 1});
+            bcost.push_back(c);
+            acc += c;
+            a = b;
+        }
+    }
+    std::vector<size_t> bord(bv.size());
+    for (size_t i = 0; i < bord.size(); ++i) bord[i] = i;
+    std::stable_sort(bord.begin(), bord.end(), [&](size_t a2, size_t b2) { return bcost[a2] > bcost[b2]; });
+    std::vector<std::array<uint32_t, 4>> sb;
+    for (size_t i : bord) sb.push_back(bv[i]);
+    h->pieces = S > 1 ? S : 0;
+    if (S > 1) {
+        up(h->npieces, npieces.data(), npieces.size());
+        h->ypart.alloc(static_cast<size_t>(S) * (h->re - h->rb) * h->R * 8);
+    }
     up(h->stripe_a, sa.data(), sa.size() * 16);
     up(h->stripe_b, sb.data(), sb.size() * 16);
     up(h->wcol, wrec.data(), wrec.size());
@@ -2121,7 +2208,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     h->nred = static_cast<uint32_t>(redcols.size());
     stream_sync(s);
     h->nstripe_a = nstripe_a;
-    h->nblocks = static_cast<uint32_t>(nblocks);
+    h->nblocks = static_cast<uint32_t>(sb.size());  // phase-B stripes
     rep.device_arena_bytes = B.arena.size() * 4;
     rep.device_table_bytes = B.stages.size() * (sizeof(Stage) + kCopies * 8) + B.bitems.size() * sizeof(BItem) +
                              B.a_items * sizeof(AItem) +
@@ -2142,6 +2229,7 @@ Params make_params(hcmx_hmat* h, double alpha, double beta, double* y) {
     p.coef = h->coef.as<double>();
     p.wrec = h->wcol.as<uint8_t>();
     p.partial = h->partial.as<double>();
+    p.ypart = h->ypart.as<double>();
     p.x = h->xpad.as<double>();  // padded, 16-byte aligned copy of x (bulk copies)
     p.y = y;
     p.row_begin = static_cast<uint32_t>(h->rb);
@@ -2218,16 +2306,19 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
     const uint32_t ga = std::min<uint32_t>(h->nstripe_a, 2 * nsm), gb = std::min<uint32_t>(h->nblocks, 2 * nsm);
     const uint32_t gr = (h->nred_long + 7) / 8 + (h->nred - h->nred_long + 255) / 256;
     const RedCol* rc = h->redcols.as<RedCol>();
+    const uint32_t gc = static_cast<uint32_t>(std::min<uint64_t>(((h->re - h->rb) * R + 255) / 256, 4 * nsm));
     if (R == 1) {
         if (run_a) launch(k_phase_a<1>, ga, kThreadsA, kSmemBytes, false, p);
         if (h->nred) launch(k_reduce<1>, gr, 256, 0, true, p, rc, h->nred_long, h->nred);
         if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
         if (h->nblocks) launch(k_phase_b<1>, gb, (nwb<1>() + 1) * 32, kSmemBytes, run_a, p);
+        if (h->pieces) launch(k_combine<1>, gc, 256, 0, true, p, h->npieces.as<uint8_t>());
     } else {
         if (run_a) launch(k_phase_a<kMultiR>, ga, kThreadsA, kSmemBytes, false, p);
         if (h->nred) launch(k_reduce<kMultiR>, gr, 256, 0, true, p, rc, h->nred_long, h->nred);
         if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
         if (h->nblocks) launch(k_phase_b<kMultiR>, gb, (nwb<kMultiR>() + 1) * 32, kSmemBytes, run_a, p);
+        if (h->pieces) launch(k_combine<kMultiR>, gc, 256, 0, true, p, h->npieces.as<uint8_t>());
     }
     check_cuda(cudaGetLastError(), "matvec launch");
 #ifdef HCMX_PROF
