@@ -1959,13 +1959,23 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
             pend.clear();
             stripe_bytes = 0;
         };
+        // stripe size: ~kAStripeBytes, smaller when the X factors of this handle
+        // (one rank of a row partition) would give fewer than ~4 stripes per
+        // CTA slot (2 per SM) -- else the slowest stripe sets the phase time
+        uint64_t xbytes_all = 0;
+        for (uint64_t l : leaves)
+            if (d.kind[l] != 0)
+                for (uint32_t i = 0; i < leafa[lr_id[l]].k; ++i)
+                    xbytes_all += B.words_of(xbuf(l, i).first, d.col1[l] - d.col0[l]) * 4;
+        const uint64_t stripe_target =
+            std::max<uint64_t>(2ull * kStageBytes, std::min<uint64_t>(kAStripeBytes, xbytes_all / (4ull * 2 * 148)));
         for (uint64_t l : leaves) {
             if (d.kind[l] == 0) continue;
             const uint32_t id = static_cast<uint32_t>(lr_id[l]);
             pend.push_back(id);
             for (uint32_t i = 0; i < leafa[id].k; ++i)
                 stripe_bytes += B.words_of(xbuf(l, i).first, d.col1[l] - d.col0[l]) * 4;
-            if (stripe_bytes >= kAStripeBytes) flush();
+            if (stripe_bytes >= stripe_target) flush();
         }
         flush();
     }

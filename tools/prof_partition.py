@@ -32,5 +32,11 @@ for N in (1, 2, 4, 8):
         e1.record()
         torch.cuda.synchronize()
         worst = max(worst, e0.elapsed_time(e1) / 30)
+        H.timing(1)
+        for _ in range(30):
+            H.matvec_device(1.0, x, 0.0, y)
+        torch.cuda.synchronize()
+        ma, mb, calls = H.timing(0)
+        print(f"   N={N} rank {r}: phase A {ma / calls:.4f} ms, phase B {mb / calls:.4f} ms (events, no PDL)")
         H.close()
     print(f"N={N}: per-rank product {worst:.4f} ms (max of first/last rank), ideal {0 if N == 1 else 0:.0f}", flush=True)
