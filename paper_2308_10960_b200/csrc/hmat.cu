@@ -43,6 +43,7 @@
 #include <array>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "internal.h"
@@ -2251,16 +2252,32 @@ Params make_params(hcmx_hmat* h, double alpha, double beta, double* y) {
 
 // dx, dy: n-vectors (h->R == 1) or n x R row-major blocks (h->R == kMultiR)
 void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, double* dy, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        const int sm = static_cast<int>(kSmemBytes);
-        check_cuda(cudaFuncSetAttribute(k_phase_a<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-        check_cuda(cudaFuncSetAttribute(k_phase_b<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-        check_cuda(cudaFuncSetAttribute(k_phase_a<kMultiR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
-                   "smem attr");
-        check_cuda(cudaFuncSetAttribute(k_phase_b<kMultiR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
-                   "smem attr");
-        attr_set = true;
+    // per-device setup (kernel attributes are per device; one process may drive several)
+    struct DevInfo {
+        bool ready = false;
+        int nsm = 148;
+    };
+    static std::mutex dev_mu;
+    static DevInfo dev_info[64];
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= 64) throw invalid_argument("matvec: device ordinal out of range");
+    int nsm;
+    {
+        std::lock_guard<std::mutex> g(dev_mu);
+        DevInfo& di = dev_info[dev];
+        if (!di.ready) {
+            const int sm = static_cast<int>(kSmemBytes);
+            check_cuda(cudaFuncSetAttribute(k_phase_a<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+            check_cuda(cudaFuncSetAttribute(k_phase_b<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+            check_cuda(cudaFuncSetAttribute(k_phase_a<kMultiR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+                       "smem attr");
+            check_cuda(cudaFuncSetAttribute(k_phase_b<kMultiR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+                       "smem attr");
+            check_cuda(cudaDeviceGetAttribute(&di.nsm, cudaDevAttrMultiProcessorCount, dev), "SM count");
+            di.ready = true;
+        }
+        nsm = di.nsm;
     }
     const int R = h->R;
     h->last_launches = 0;
@@ -2289,12 +2306,6 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
         rec = {take_event(h), take_event(h), take_event(h)};
         check_cuda(cudaEventRecord(rec.a0, s), "event");
     }
-    static int nsm = [] {
-        int dev = 0, n = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        return n;
-    }();
     // the stripe counters: phase A resets B's and B resets A's for the next
     // product (both start at zero); a product without phase A resets here
     const bool run_a = h->nlr && h->nstripe_a;
