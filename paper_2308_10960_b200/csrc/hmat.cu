@@ -818,18 +818,29 @@ __global__ void k_reduce(Params p, const RedCol* rc, uint32_t nlong, uint32_t n)
         const uint32_t i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31u;
         if (i >= nlong) return;
         const RedCol r = rc[i];
+        double s0[R], s1[R];  // the R right-hand sides of a chunk are adjacent
+#pragma unroll
+        for (int c = 0; c < R; ++c) s0[c] = s1[c] = 0.0;
+        uint32_t ch = lane;
+        for (; ch + 32 < r.nchunks; ch += 64) {
+            const double* a0 = p.partial + static_cast<size_t>(r.p0 + ch * r.stride) * R;
+            const double* a1 = p.partial + static_cast<size_t>(r.p0 + (ch + 32) * r.stride) * R;
+#pragma unroll
+            for (int c = 0; c < R; ++c) {
+                s0[c] += a0[c];
+                s1[c] += a1[c];
+            }
+        }
+        if (ch < r.nchunks) {
+            const double* a0 = p.partial + static_cast<size_t>(r.p0 + ch * r.stride) * R;
+#pragma unroll
+            for (int c = 0; c < R; ++c) s0[c] += a0[c];
+        }
         const double cf = p.alpha * p.coef[r.col];
         double* out = rec_c<R>(p, r.col);
 #pragma unroll
         for (int c = 0; c < R; ++c) {
-            double s0 = 0.0, s1 = 0.0;
-            uint32_t ch = lane;
-            for (; ch + 32 < r.nchunks; ch += 64) {
-                s0 += p.partial[static_cast<size_t>(r.p0 + ch * r.stride) * R + c];
-                s1 += p.partial[static_cast<size_t>(r.p0 + (ch + 32) * r.stride) * R + c];
-            }
-            if (ch < r.nchunks) s0 += p.partial[static_cast<size_t>(r.p0 + ch * r.stride) * R + c];
-            double s = s0 + s1;
+            double s = s0[c] + s1[c];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
             if (lane == 0) out[c] = cf * s;
@@ -839,15 +850,27 @@ __global__ void k_reduce(Params p, const RedCol* rc, uint32_t nlong, uint32_t n)
     const uint32_t i = nlong + (blockIdx.x - long_blocks) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const RedCol r = rc[i];
+    constexpr int NC = R == 1 ? 4 : 1;  // independent chains per right-hand side
+    double s[R][NC];
+#pragma unroll
+    for (int c = 0; c < R; ++c)
+#pragma unroll
+        for (int q = 0; q < NC; ++q) s[c][q] = 0.0;
+#pragma unroll
+    for (uint32_t ch = 0; ch < kRedLong; ++ch) {
+        if (ch < r.nchunks) {
+            const double* a0 = p.partial + static_cast<size_t>(r.p0 + ch * r.stride) * R;
+#pragma unroll
+            for (int c = 0; c < R; ++c) s[c][ch % NC] += a0[c];
+        }
+    }
     const double cf = p.alpha * p.coef[r.col];
     double* out = rec_c<R>(p, r.col);
 #pragma unroll
     for (int c = 0; c < R; ++c) {
-        double s[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains, fixed order
-#pragma unroll
-        for (uint32_t ch = 0; ch < kRedLong; ++ch)
-            if (ch < r.nchunks) s[ch & 3u] += p.partial[static_cast<size_t>(r.p0 + ch * r.stride) * R + c];
-        out[c] = cf * ((s[0] + s[1]) + (s[2] + s[3]));
+        double t = s[c][0];
+        if (NC == 4) t = (s[c][0] + s[c][1 % NC]) + (s[c][2 % NC] + s[c][3 % NC]);
+        out[c] = cf * t;
     }
 }
 
