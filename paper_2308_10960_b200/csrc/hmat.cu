@@ -66,7 +66,6 @@ constexpr int kNWB = HCMX_NWB;            // phase-B consumer warps per CTA
 #define HCMX_STAGE_BYTES 26624
 #endif
 constexpr int kNWA = HCMX_NWA;            // phase-A consumer warps (more registers per thread)
-constexpr int kThreadsB = (kNWB + 1) * 32;  // + one producer warp (bulk copies)
 constexpr int kThreadsA = (kNWA + 1) * 32;
 constexpr int kStageBytes = HCMX_STAGE_BYTES;  // packed data per stage
 constexpr int kMaxItems = 32;             // items per stage (one per producer lane)
@@ -105,7 +104,6 @@ constexpr uint32_t kAGroupMaxMulti = HCMX_AGROUP_MULTI;  // the same for multi-R
 constexpr int kAUnroll = HCMX_AUNROLL;   // row groups per iteration of the phase-A fast body
 constexpr uint64_t kAItemBytes = HCMX_AITEM;  // packed data per phase-A item
 constexpr uint32_t kAItemXBytes = 12288;  // staged x slices per phase-A item
-constexpr int kBDenseGroup = 8;       // max dense columns per B item
 #ifndef HCMX_BGROUP
 #define HCMX_BGROUP 16
 #endif
@@ -405,11 +403,7 @@ __constant__ Pow2Table c_pow2e = make_pow2e();
 // fast-decoder constants from a layout word (w <= 32)
 __device__ __forceinline__ uint32_t fast_mask(unsigned w) { return 0x7fffffffu & ~((0xffffffffu >> (w - 1)) >> 1); }
 
-__device__ __forceinline__ unsigned round16u(unsigned x) { return (x + 15u) & ~15u; }
 
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 
 
 // ------------------------------------------------------- warp pipeline ----
