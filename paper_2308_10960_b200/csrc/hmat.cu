@@ -160,7 +160,10 @@ template <int R>
 __host__ __device__ constexpr int rec_bytes() { return R == 1 ? 32 : (8 * R + 16 + 15) / 16 * 16; }
 constexpr uint32_t kMaxPieces = 4;  // pieces a phase-B row block may be split into
 constexpr int kMultiR = 4;    // right-hand sides per product of a multi-RHS arena
-constexpr int kNWBMulti = 8;  // phase-B consumer warps for R > 1 (R x 4 accumulators per lane)
+#ifndef HCMX_NWB_MULTI
+#define HCMX_NWB_MULTI 8
+#endif
+constexpr int kNWBMulti = HCMX_NWB_MULTI;  // phase-B consumer warps for R > 1 (R x 4 accumulators per lane)
 inline uint32_t rec_bytes_rt(int R) { return R == 1 ? 32u : static_cast<uint32_t>((8 * R + 16 + 15) / 16 * 16); }
 template <int R>
 __host__ __device__ constexpr int nwb() { return R == 1 ? HCMX_NWB : kNWBMulti; }
