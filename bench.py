@@ -282,14 +282,21 @@ def run_ours(args, rank, world, local):
     y = torch.zeros(n, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
     maxlen = max(b - a for a, b in parts)
-    slab = torch.zeros(maxlen, dtype=torch.float64, device="cuda")
     gathered = torch.zeros(maxlen * world, dtype=torch.float64, device="cuda")
 
+    # N > 1: the rank's rows are written straight into its slab of the gather
+    # buffer (the handle writes y[row_begin, row_end) only, so y's base is placed
+    # row_begin rows before the slab) and the all-gather runs in place
+    from paper_2308_10960_b200._lib import check as _check, lib as _lib
+    y_into_slab = gathered.data_ptr() + (rank * maxlen - rr[0]) * 8
+
     def step():
-        H.matvec_device(1.0, x, 0.0, y)
         if world > 1:  # exchange step: every rank needs all of y for the next product
-            slab[: rr[1] - rr[0]].copy_(y[rr[0]: rr[1]])
-            dist.all_gather_into_tensor(gathered, slab)
+            _check(_lib().hcmx_gpu_hmat_matvec_device(H._h, 1.0, x.data_ptr(), 0.0, y_into_slab,
+                                                      stream.cuda_stream), "matvec")
+            dist.all_gather_into_tensor(gathered, gathered.narrow(0, rank * maxlen, maxlen))
+        else:
+            H.matvec_device(1.0, x, 0.0, y)
 
     for _ in range(args.warmup):
         step()

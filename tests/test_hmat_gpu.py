@@ -300,3 +300,33 @@ def test_split_row_blocks(gpu, oracle, monkeypatch, pieces):
     for j, s in enumerate((1.0, -1.0, 2.0)):
         assert rel(Y[:, j], oracle.hmat_matvec(f, 0.5, s * x, -1.25, y0, threads=4)) <= TOL
     H.close()
+
+
+def test_partition_writes_into_gather_slab(gpu, oracle):
+    """the multi-GPU bench step writes a rank's rows straight into its slab of
+    the all-gather buffer (y base pointer placed row_begin rows before it):
+    the slab equals the rank's rows of the full product and nothing else moves"""
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200._lib import check, lib
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    import bench
+    n = 2048
+    f, x = build_small_flat(n=n, eps=1e-6, scheme=0)
+    ref = oracle.hmat_matvec(f, 1.0, x, 0.0, np.zeros(n), threads=4)
+    world = 2
+    parts = bench.partition_rows(f.to_product(), world)
+    maxlen = max(b - a for a, b in parts)
+    gathered = torch.full((maxlen * world,), 7.0, dtype=torch.float64, device="cuda")
+    xd = torch.as_tensor(x).cuda()
+    for rank, rr in enumerate(parts):
+        H = HMatrix(f.to_product(), row_range=rr)
+        base = gathered.data_ptr() + (rank * maxlen - rr[0]) * 8
+        check(lib().hcmx_gpu_hmat_matvec_device(H._h, 1.0, xd.data_ptr(), 0.0, base,
+                                                torch.cuda.current_stream().cuda_stream), "matvec")
+        torch.cuda.synchronize()
+        H.close()
+    g = gathered.cpu().numpy()
+    for rank, (a, b) in enumerate(parts):
+        slab = g[rank * maxlen: rank * maxlen + (b - a)]
+        assert rel(slab, ref[a:b]) <= TOL
+        assert (g[rank * maxlen + (b - a): (rank + 1) * maxlen] == 7.0).all()
