@@ -2634,9 +2634,23 @@ int hcmx_gpu_hmat_matvec(hcmx_hmat* h, double alpha, const double* h_x, double b
             h = h->trans;
         }
         if (!h->xbuf.p) h->xbuf.alloc(h->n_cols * 8);
-        if (!h->ybuf.p) h->ybuf.alloc(h->n_rows * 8);
         const uint64_t nr = h->re - h->rb;
         h2d(h->xbuf.p, h_x, h->n_cols * 8, h->stream);
+        // y in pinned (page-locked, device-mapped) host memory: the kernels write
+        // the rows straight into it over PCIe while phase B runs -- no device
+        // staging and no copy back after the product (x is read many times, so it
+        // is always staged in HBM)
+        static const bool no_mapped = std::getenv("HCMX_NO_MAPPED_Y") != nullptr;  // A/B knob
+        cudaPointerAttributes pa{};
+        const bool mapped = !no_mapped && beta == 0.0 && cudaPointerGetAttributes(&pa, h_y) == cudaSuccess &&
+                            pa.type == cudaMemoryTypeHost && pa.devicePointer != nullptr;
+        cudaGetLastError();  // a pageable pointer may leave an error flag behind
+        if (mapped) {
+            run_matvec(h, alpha, h->xbuf.as<double>(), beta, static_cast<double*>(pa.devicePointer), h->stream);
+            stream_sync(h->stream);
+            return;
+        }
+        if (!h->ybuf.p) h->ybuf.alloc(h->n_rows * 8);
         if (beta != 0.0) h2d(h->ybuf.as<double>() + h->rb, h_y + h->rb, nr * 8, h->stream);
         run_matvec(h, alpha, h->xbuf.as<double>(), beta, h->ybuf.as<double>(), h->stream);
         d2h(h_y + h->rb, h->ybuf.as<double>() + h->rb, nr * 8, h->stream);

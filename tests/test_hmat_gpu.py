@@ -330,3 +330,26 @@ def test_partition_writes_into_gather_slab(gpu, oracle):
         slab = g[rank * maxlen: rank * maxlen + (b - a)]
         assert rel(slab, ref[a:b]) <= TOL
         assert (g[rank * maxlen + (b - a): (rank + 1) * maxlen] == 7.0).all()
+
+
+def test_host_api_pinned_and_pageable_y(gpu, oracle):
+    """hcmx_gpu_hmat_matvec with host pointers: a pinned y is written directly by
+    the kernels (mapped host memory), a pageable y through the staging copy;
+    both equal the oracle, beta != 0 takes the staged path"""
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200._lib import check, lib
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    n = 2048
+    f, x = build_small_flat(n=n, eps=1e-6, scheme=0)
+    H = HMatrix(f.to_product())
+    xh = torch.as_tensor(x).pin_memory()
+    y0 = np.random.default_rng(4).standard_normal(n)
+    for beta in (0.0, 0.5):
+        ref = oracle.hmat_matvec(f, 1.0, x, beta, y0, threads=4)
+        yp = torch.as_tensor(y0.copy()).pin_memory()
+        check(lib().hcmx_gpu_hmat_matvec(H._h, 1.0, xh.data_ptr(), beta, yp.data_ptr(), 0), "matvec")
+        assert rel(yp.numpy(), ref) <= TOL, beta
+        yn = y0.copy()
+        H.matvec(1.0, x, beta, yn)
+        assert rel(yn, ref) <= TOL, beta
+    H.close()
