@@ -416,7 +416,7 @@ def run_ours(args, rank, world, local):
                      "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                      "statistic": "median of K per-call wall times",
                      "mean_value": round(total_bytes * args.steps / e2e_mean_s / 1e9, 2),
-                     "api": "hcmx_gpu_hmat_matvec (host pointers, pinned)"} if e2e_s else None),
+                     "api": "hcmx_gpu_hmat_matvec (host pointers, pinned; y crosses PCIe as the kernels write it into mapped host memory)"} if e2e_s else None),
             "gpu_launches": launches,
             "clocks": clk,
         }
