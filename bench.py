@@ -368,9 +368,15 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         ms4 = e0.elapsed_time(e1) / args.steps
         flops = 4 * 2.0 * rep.uncompressed_equivalent / 8  # 2 flop per stored FP64 entry and RHS
+        fp64_peak = None  # measured DFMA throughput (tools/fp64_peak.cu; MEASURED_PEAKS has no FP64 figure)
+        pk = os.path.join(ROOT, "profiles", "r1_fp64_peak.json")
+        if os.path.exists(pk):
+            fp64_peak = json.load(open(pk)).get("fp64_fma_tflops")
+        tf = flops / (ms4 / 1e3) / 1e12
         rhs4 = {"nrhs": 4, "ms_per_product": round(ms4, 4),
                 "speedup_vs_4_single": round(4 * (ms / args.steps) / ms4, 3),
-                "fp64_tflops": round(flops / (ms4 / 1e3) / 1e12, 3),
+                "fp64_tflops": round(tf, 3), "fp64_peak_tflops": fp64_peak,
+                "fp64_frac": round(tf / fp64_peak, 3) if fp64_peak else None,
                 "note": "matmat4_device: Y = A X for 4 interleaved columns, one decode per field"}
         H4.close()
     line = None
