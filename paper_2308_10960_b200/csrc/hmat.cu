@@ -90,7 +90,10 @@ constexpr int kG = kR / 32;           // row groups (accumulators) per lane
 constexpr int kAChunk = 64;           // rows of a leaf's X columns per phase-A chunk
 constexpr int kARows = 4;             // rows per word-padded group of a phase-A item
 constexpr int kALanes = 32;           // rank columns per phase-A item
-constexpr int kAGroupMax = 8;         // chunks of one rank column summed in-warp
+#ifndef HCMX_AGROUP
+#define HCMX_AGROUP 8
+#endif
+constexpr int kAGroupMax = HCMX_AGROUP;  // chunks of one rank column summed in-warp
 #ifndef HCMX_AGROUP_MULTI
 #define HCMX_AGROUP_MULTI 2
 #endif
