@@ -100,26 +100,25 @@ def dist_env():
 
 
 def partition_rows(flat, world):
-    """contiguous row ranges on row-block boundaries balanced by compressed bytes"""
-    n = flat.n_rows
-    if world == 1:
-        return [(0, n)]
-    rows = flat.row1 - flat.row0
-    # spread each leaf's bytes uniformly over its rows for the prefix
-    dens = np.zeros(n)
-    for l in range(flat.nleaves):
-        b0 = int(flat.buf0[l])
-        tot = float(flat.plen[b0]) if flat.kind[l] == 0 else float(flat.plen[b0: b0 + 2 * int(flat.rank[l])].sum())
-        dens[flat.row0[l]: flat.row1[l]] += tot / rows[l]
-    pref = np.concatenate([[0], np.cumsum(dens)])
-    cuts = [0]
-    for r in range(1, world):
-        target = pref[-1] * r / world
-        c = int(np.searchsorted(pref, target))
-        c = max(cuts[-1] + 64, (c + 32) // 64 * 64)
-        cuts.append(min(c, n))
-    cuts.append(n)
-    return list(zip(cuts[:-1], cuts[1:]))
+    """the one block-row partitioner (distributed.partition_rows -> the C++
+    partitioner behind hcmx_gpu_partition_rows)"""
+    from paper_2308_10960_b200.distributed import partition_rows as pr
+    return pr(flat, world)
+
+
+WORKLOADS = {
+    "1": ("synthetic (seeded Fibonacci sphere, Laplace kernel, BASELINE config 1)",
+          "config1: Laplace sphere n={n}, leaf 64, eta 2, SVD 1e-6, {S}-APLR + {S} dense, y=Ax"),
+    "3": ("synthetic (seeded Fibonacci sphere, Laplace kernel, BASELINE config 3)",
+          "config3: Laplace sphere n={n}, leaf 64, eta 2, SVD 1e-8, {S}-APLR + {S} dense, y=Ax"),
+    "4": ("synthetic (seeded uniform unit cube, Matern nu=1.5 l=0.1, BASELINE config 4)",
+          "config4: Matern cube n={n}, leaf 64, eta 2, SVD 1e-6, {S}-APLR + {S} dense, y=Ax"),
+}
+
+
+def workload_strings(cfg, n, scheme):
+    data, wl = WORKLOADS[str(cfg)]
+    return data, wl.format(n=n, S=scheme.upper())
 
 
 def step_bytes(flat, row_range=None):
@@ -137,19 +136,26 @@ def step_bytes(flat, row_range=None):
     return tot + 8 * flat.n_cols + 8 * (b - a)
 
 
-def kernel_bytes(flat):
+def kernel_bytes(flat, row_range=None):
     """algorithmic bytes per launch of phase A (X streams, sigma, x) and phase B
-    (dense + W streams, y)"""
-    a = bb = 0
+    (dense + W streams, y) of the handle holding rows `row_range` (every leaf
+    overlapping it: phase A whole, phase B the overlapping rows' share)"""
+    ra, rb = row_range or (0, flat.n_rows)
+    a = bb = 0.0
     for l in range(flat.nleaves):
+        r0, r1 = int(flat.row0[l]), int(flat.row1[l])
+        ov = min(r1, rb) - max(r0, ra)
+        if ov <= 0:
+            continue
+        frac = ov / (r1 - r0)
         b0 = int(flat.buf0[l])
         if flat.kind[l] == 0:
-            bb += int(flat.plen[b0]) + 20
+            bb += (int(flat.plen[b0]) + 20) * frac
         else:
             k = int(flat.rank[l])
             a += int((flat.plen[b0 + k: b0 + 2 * k] + 20).sum()) + 8 * k
-            bb += int((flat.plen[b0: b0 + k] + 20).sum())
-    return a + 8 * flat.n_cols, bb + 8 * flat.n_rows
+            bb += int((flat.plen[b0: b0 + k] + 20).sum()) * frac
+    return int(a) + 8 * flat.n_cols, int(bb) + 8 * (rb - ra)
 
 
 def build_flat(cfg, scheme):
@@ -189,9 +195,11 @@ def cpu_reference_value(flat, threads, budget_s=15.0, max_reps=3):
         impl.hmat_matvec(sample, 1.0, x, 0.0, np.zeros(fh.n_rows), threads=threads)
         times.append(time.perf_counter() - t)
     best = min(times)
+    # parity of the benched product: the same CPU path over the whole matrix (untimed)
+    y_ref = impl.hmat_matvec(fh, 1.0, x, 0.0, np.zeros(fh.n_rows), threads=threads)
     return {"value": sb / best / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
             "sample": f"rows [0,{rows}) of {fh.n_rows} ({sb / 1e6:.1f} MB compressed), best of {max_reps}, "
-                      f"{threads} threads"}, sb, best
+                      f"{threads} threads"}, sb, best, y_ref
 
 
 def restrict(flat, rr):
@@ -273,30 +281,24 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     flat, info = build_flat(args.config, args.scheme)
-    parts = partition_rows(flat, world)
-    rr = parts[rank]
-    H = HMatrix(flat, row_range=None if world == 1 else rr)
+    if world > 1:
+        # this rank's rows through the library's partitioned handle; the exchange
+        # (NCCL in-place broadcasts of the y slices) runs inside the library
+        from paper_2308_10960_b200.distributed import PartitionedHMatrix, nccl_comm
+        comm, _, _ = nccl_comm()
+        H = PartitionedHMatrix(flat, comm)
+    else:
+        comm = None
+        H = HMatrix(flat)
     rep = H.memory()
     n = flat.n_rows
     x = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, n)).cuda()
     y = torch.zeros(n, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
-    maxlen = max(b - a for a, b in parts)
-    gathered = torch.zeros(maxlen * world, dtype=torch.float64, device="cuda")
-
-    # N > 1: the rank's rows are written straight into its slab of the gather
-    # buffer (the handle writes y[row_begin, row_end) only, so y's base is placed
-    # row_begin rows before the slab) and the all-gather runs in place
-    from paper_2308_10960_b200._lib import check as _check, lib as _lib
-    y_into_slab = gathered.data_ptr() + (rank * maxlen - rr[0]) * 8
 
     def step():
-        if world > 1:  # exchange step: every rank needs all of y for the next product
-            _check(_lib().hcmx_gpu_hmat_matvec_device(H._h, 1.0, x.data_ptr(), 0.0, y_into_slab,
-                                                      stream.cuda_stream), "matvec")
-            dist.all_gather_into_tensor(gathered, gathered.narrow(0, rank * maxlen, maxlen))
-        else:
-            H.matvec_device(1.0, x, 0.0, y)
+        # N > 1: local product + exchange, every rank ends with all of y
+        H.matvec_device(1.0, x, 0.0, y)
 
     for _ in range(args.warmup):
         step()
@@ -350,7 +352,22 @@ def run_ours(args, rank, world, local):
         e2e_s = float(np.median(per_call)) * args.steps
         e2e_mean_s = float(np.mean(per_call)) * args.steps
     else:
-        e2e_s = None
+        # hcmx_gpu_hmat_dist_matvec: host x in, the whole y out on every rank;
+        # per-call wall times, max over ranks
+        yh_np = np.zeros(n)
+        xh_np = xh.numpy()
+        for _ in range(args.warmup):
+            H.matvec(1.0, xh_np, 0.0, yh_np)
+        dist.barrier()
+        per_call = []
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            H.matvec(1.0, xh_np, 0.0, yh_np)
+            per_call.append(time.perf_counter() - t)
+        tt = torch.tensor([float(np.median(per_call)), float(np.mean(per_call))], dtype=torch.float64,
+                          device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s, e2e_mean_s = float(tt[0]) * args.steps, float(tt[1]) * args.steps
     # C5-style multi-RHS products: the 4-right-hand-side arena decodes every
     # field once for 4 columns (same matrix, same bytes; device time per product)
     rhs4 = None
@@ -380,9 +397,10 @@ def run_ours(args, rank, world, local):
                 "note": "matmat4_device: Y = A X for 4 interleaved columns, one decode per field"}
         H4.close()
     line = None
+    data_s, workload_s = workload_strings(args.config, n, args.scheme)
     if rank == 0:
         peak, peak_src = _peaks()
-        ka, kb = kernel_bytes(flat)
+        ka, kb = kernel_bytes(flat, H.row_range if world > 1 else None)
         per_a = ms_a / max(calls, 1)
         per_b = ms_b / max(calls, 1)
         dom = "phase_b" if per_b >= per_a else "phase_a"
@@ -392,18 +410,21 @@ def run_ours(args, rank, world, local):
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             traffic = json.load(open(tp)).get(dom)
-        cpu = None
+        cpu, parity = None, None
         if not args.no_cpu_baseline and world == 1:
-            cpu, _, _ = cpu_reference_value(flat, os.cpu_count() or 1)
+            cpu, _, _, y_ref = cpu_reference_value(flat, os.cpu_count() or 1)
+            # the timed product's y (last step) against the CPU reference path
+            y_dev = y.cpu().numpy()
+            parity = {"rel_err": float(np.linalg.norm(y_dev - y_ref) / np.linalg.norm(y_ref)),
+                      "tol": 1e-12, "vs": f"{cpu['kind']} CPU product over the whole matrix, same x"}
         codec_res = codec_microbench() if (world == 1 and not args.no_codec) else None
         line = {
             "metric": "compressed H-matvec GB/s (compressed bytes)",
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded Fibonacci sphere, Laplace kernel, BASELINE config 3)",
-            "config": {"workload": f"config{args.config}: Laplace sphere n={n}, leaf 64, eta 2, "
-                                   f"SVD 1e-8, {args.scheme.upper()}-APLR + {args.scheme.upper()} dense, y=Ax",
+            "data": data_s,
+            "config": {"workload": workload_s,
                        "n": n, "leaves": info["leaves"], "dense_leaves": info["dense_leaves"],
                        "lowrank_leaves": info["lowrank_leaves"], "mean_rank": round(info["mean_rank"], 2),
                        "bytes_per_step": total_bytes,
@@ -422,19 +443,26 @@ def run_ours(args, rank, world, local):
                      "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                      "statistic": "median of K per-call wall times",
                      "mean_value": round(total_bytes * args.steps / e2e_mean_s / 1e9, 2),
-                     "api": "hcmx_gpu_hmat_matvec (host pointers, pinned; y crosses PCIe as the kernels write it into mapped host memory)"} if e2e_s else None),
+                     "api": ("hcmx_gpu_hmat_matvec (host pointers, pinned; y crosses PCIe as the kernels write it into mapped host memory)"
+                             if world == 1 else
+                             "hcmx_gpu_hmat_dist_matvec (host x in, local product + NCCL exchange, whole y out; max over ranks)")}
+                    if e2e_s else None),
             "gpu_launches": launches,
             "clocks": clk,
         }
+        if parity:
+            line["parity"] = parity
         if codec_res:
             line["codec"] = codec_res
         if rhs4:
             line["multi_rhs"] = rhs4
         print(json.dumps(line), flush=True)
+    H.close()
     if world > 1:
         dist.barrier()
+        from paper_2308_10960_b200._lib import lib as _lib
+        _lib().hcmx_gpu_nccl_comm_destroy(comm)
         dist.destroy_process_group()
-    H.close()
     return line
 
 
@@ -448,6 +476,7 @@ def run_reference(args, rank, world):
     from oracle import Oracle, RefOracle
     impl, kind = (RefOracle(), "reference") if RefOracle.available() else (Oracle(), "port")
     n = flat.n_rows
+    data_s, workload_s = workload_strings(args.config, n, args.scheme)
     x = np.random.default_rng(0).uniform(-1, 1, n)
     # one step = the product over a row-slice sample sized to ~1 s
     sub = restrict(flat, (0, max(64, n // 16 // 64 * 64)))
@@ -469,9 +498,8 @@ def run_reference(args, rank, world):
             "value": round(v, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded Fibonacci sphere, Laplace kernel, BASELINE config 3)",
-            "config": {"workload": f"config{args.config}: Laplace sphere n={n}, leaf 64, eta 2, SVD 1e-8, "
-                                   f"{args.scheme.upper()}-APLR + {args.scheme.upper()} dense, y=Ax",
+            "data": data_s,
+            "config": {"workload": workload_s,
                        "n": n, "setup_s": round(time.time() - t0, 1)},
             "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": kind,
                              "sample": desc},

@@ -178,8 +178,9 @@ typedef struct hcmx_hmat_desc {
     const int64_t *count, *poff, *plen;                                   /* [nbuffers] */
     const uint8_t* blob; /* host pointer, or device pointer if blob_on_device */
     int blob_on_device;
-    /* block-row partition (multi-GPU): only leaves with row0 in [row_begin,row_end)
-     * are loaded; matvec then writes y[row_begin,row_end) only. 0,0 = all rows */
+    /* block-row partition (multi-GPU): every leaf that overlaps [row_begin,row_end)
+     * is loaded (a lowrank leaf crossing the range boundary does its X^T x half
+     * here too); matvec then writes y[row_begin,row_end) only. 0,0 = all rows */
     uint64_t row_begin, row_end;
     /* nonzero: also build M^T (hmatrix.hpp:128 transpose; whole matrix only) */
     int with_transpose;
@@ -243,6 +244,49 @@ int hcmx_gpu_hmat_last_launches(const hcmx_hmat* h);
  * stream) accumulated over matvec_device calls since the last reset */
 int hcmx_gpu_hmat_timing(hcmx_hmat* h, int enable, double* ms_phase_a, double* ms_phase_b,
                          uint64_t* calls);
+
+/* ------------------------------------------- block-row partitions (multi-GPU) */
+/* the rows are cut into one contiguous range per rank; each rank
+ * keeps the leaves that write its rows, x is replicated and y slices are
+ * disjoint, so the only exchange per product is an all-gather of y.  The
+ * reference has no parallel code (its hooks: the unused `threads` knobs,
+ * hmatrix.hpp:83,119, and SPEC.md:489's deterministic merge of disjoint leaf
+ * blocks); y here is bit-identical to the single-GPU product. */
+
+/* the partitioner: world + 1 cuts (multiples of 64 rows, cuts[world] = n_rows)
+ * minimising the largest per-rank byte count, where a lowrank leaf crossing a
+ * cut charges its X factor to both ranks.  Host only (no device needed). */
+int hcmx_gpu_partition_rows(const hcmx_hmat_desc* desc, int world, uint64_t* cuts);
+
+/* NCCL communicator helpers (libnccl.so.2 is loaded at run time; a caller that
+ * already has an ncclComm_t passes it directly).  id128 = ncclUniqueId bytes. */
+struct ncclComm; /* ncclComm_t == struct ncclComm* (nccl.h) */
+int hcmx_gpu_nccl_unique_id(uint8_t* id128);
+int hcmx_gpu_nccl_comm_init(int world, const uint8_t* id128, int rank, struct ncclComm** comm);
+int hcmx_gpu_nccl_comm_destroy(struct ncclComm* comm);
+
+typedef struct hcmx_hmat_dist hcmx_hmat_dist; /* this rank's rows + the communicator */
+/* every rank passes the whole flattened matrix and the same communicator
+ * (world and rank are taken from it; comm == NULL: one rank).  The handle is
+ * built for hcmx_gpu_partition_rows' range of this rank (row_begin / row_end /
+ * with_transpose of desc are ignored). */
+int hcmx_gpu_hmat_create_partitioned(const hcmx_hmat_desc* desc, struct ncclComm* comm, hcmx_hmat_dist** out);
+int hcmx_gpu_hmat_dist_destroy(hcmx_hmat_dist* h);
+int hcmx_gpu_hmat_dist_rows(const hcmx_hmat_dist* h, uint64_t* row_begin, uint64_t* row_end, int* rank,
+                            int* world);
+int hcmx_gpu_hmat_dist_cuts(const hcmx_hmat_dist* h, uint64_t* cuts); /* world + 1 entries */
+/* the rank-local handle (NULL for an empty range), for timing / memory queries */
+int hcmx_gpu_hmat_dist_local(hcmx_hmat_dist* h, hcmx_hmat** local);
+/* y := alpha M x + beta y on every rank: the local product of this rank's rows,
+ * then one NCCL group of in-place broadcasts (rank r sends y[cut_r, cut_r+1))
+ * on `stream`, so every rank ends with the whole contiguous y (n_rows) for the
+ * next product.  x and y must be identical on all ranks.  NCCL failures ->
+ * HCMX_NCCL_ERROR. */
+int hcmx_gpu_hmat_dist_matvec_device(hcmx_hmat_dist* h, double alpha, const double* d_x, double beta,
+                                     double* d_y, void* stream);
+/* the same with host vectors (copies x in and the whole y out; the
+ * reference-facing call of a partitioned matrix, hmatrix.hpp:126-128) */
+int hcmx_gpu_hmat_dist_matvec(hcmx_hmat_dist* h, double alpha, const double* h_x, double beta, double* h_y);
 
 #ifdef __cplusplus
 }

@@ -25,6 +25,10 @@ class CudaError(RuntimeError):
     pass
 
 
+class NcclError(RuntimeError):
+    """HCMX_NCCL_ERROR: a failed NCCL call of the multi-GPU exchange"""
+
+
 class hcmx_descriptor(C.Structure):
     _fields_ = [("scheme", C.c_uint8), ("exp_bits", C.c_uint8), ("mant_bits", C.c_uint8),
                 ("bit_width", C.c_uint8), ("reserved", C.c_uint32), ("scale", C.c_double)]
@@ -105,6 +109,17 @@ PROTOTYPES = {
     "hcmx_gpu_hmat_export_buffer": (_i, [_vp, _u64, _vp, _u64, _pu64]),
     "hcmx_gpu_hmat_last_launches": (_i, [_vp]),
     "hcmx_gpu_hmat_timing": (_i, [_vp, _i, C.POINTER(_d), C.POINTER(_d), _pu64]),
+    "hcmx_gpu_partition_rows": (_i, [C.POINTER(hcmx_hmat_desc), _i, _pu64]),
+    "hcmx_gpu_nccl_unique_id": (_i, [_vp]),
+    "hcmx_gpu_nccl_comm_init": (_i, [_i, _vp, _i, C.POINTER(_vp)]),
+    "hcmx_gpu_nccl_comm_destroy": (_i, [_vp]),
+    "hcmx_gpu_hmat_create_partitioned": (_i, [C.POINTER(hcmx_hmat_desc), _vp, C.POINTER(_vp)]),
+    "hcmx_gpu_hmat_dist_destroy": (_i, [_vp]),
+    "hcmx_gpu_hmat_dist_rows": (_i, [_vp, _pu64, _pu64, C.POINTER(_i), C.POINTER(_i)]),
+    "hcmx_gpu_hmat_dist_cuts": (_i, [_vp, _pu64]),
+    "hcmx_gpu_hmat_dist_local": (_i, [_vp, C.POINTER(_vp)]),
+    "hcmx_gpu_hmat_dist_matvec_device": (_i, [_vp, _d, _vp, _d, _vp, _vp]),
+    "hcmx_gpu_hmat_dist_matvec": (_i, [_vp, _d, _vp, _d, _vp]),
 }
 
 _lib = None
@@ -136,6 +151,8 @@ def check(status: int, what: str = "hcmx_gpu") -> None:
         raise CorruptBufferError(f"{what}: {msg}")
     if status == HCMX_OUT_OF_MEMORY:
         raise MemoryError(f"{what}: {msg}")
+    if status == HCMX_NCCL_ERROR:
+        raise NcclError(f"{what}: {msg}")
     raise CudaError(f"{what}: {msg} (status {status})")
 
 

@@ -25,10 +25,11 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + [*(["-DHCMX_PROF"] if os.environ.get("HCMX_PROF_BUILD") else []),
                   *os.environ.get("HCMX_NVCC_DEFS", "").split(), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
                   "-I" + INC, "-I" + CSRC]
-CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-I" + INC, "-I" + CSRC]
+CUDA_INC = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "include")
+CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-I" + INC, "-I" + CSRC, "-I" + CUDA_INC]
 
 CU = ["codec_kernels.cu", "hmat.cu"]
-CPP = ["codec_host.cpp"]
+CPP = ["codec_host.cpp", "dist.cpp"]
 
 
 def _run(cmd):
@@ -37,6 +38,18 @@ def _run(cmd):
         sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
         raise RuntimeError(f"build failed: {cmd[0]} {cmd[-1]}")
     return r
+
+
+STAMP = os.path.join(OBJ, "flags.stamp")
+
+
+def _flags_changed() -> bool:
+    """the active compile flags (HCMX_NVCC_DEFS / HCMX_PROF_BUILD included) differ
+    from the ones the objects were built with (a profiling build must never be
+    kept by a later plain build)"""
+    want = " ".join(NVFLAGS + CXXFLAGS)
+    have = open(STAMP).read() if os.path.exists(STAMP) else None
+    return have != want
 
 
 def _stale(src, obj, extra=()):
@@ -49,6 +62,8 @@ def _stale(src, obj, extra=()):
 
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    if _flags_changed():
+        force = True
     objs = []
     for f in CU:
         src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
@@ -63,7 +78,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
             _run([CXX, *CXXFLAGS, "-c", src, "-o", obj])
         objs.append(obj)
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static", "-lpthread"])
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static", "-lpthread", "-ldl"])
+    with open(STAMP, "w") as f:
+        f.write(" ".join(NVFLAGS + CXXFLAGS))
     return LIB
 
 

@@ -376,6 +376,35 @@ def build_config(cfg, scheme="afl", device=None, n=None, seed=1, eps=None) -> tu
     return flat, info
 
 
+def flat_desc(flat: FlatHMatrix, row_range=None, with_transpose=False, nrhs_block=0):
+    """hcmx_hmat_desc over the arrays of a flattened H-matrix (+ the objects the
+    pointers refer to, to be kept alive while the descriptor is used)"""
+    keep = {}
+    a = lambda x, t: keep.setdefault(id(x), np.ascontiguousarray(x, dtype=t))
+    i64 = lambda x: a(x, np.int64).ctypes.data_as(C.POINTER(C.c_int64))
+    sigma = np.ascontiguousarray(flat.sigma if flat.sigma.size else np.zeros(1), dtype=np.float64)
+    desc = np.ascontiguousarray(flat.desc)
+    blob = flat.blob
+    on_dev = isinstance(blob, torch.Tensor) and blob.is_cuda
+    if isinstance(blob, torch.Tensor) and not on_dev:
+        blob = blob.numpy()
+    d = _lib.hcmx_hmat_desc()
+    d.n_rows, d.n_cols, d.nleaves = int(flat.n_rows), int(flat.n_cols), flat.nleaves
+    d.nbuffers, d.nsigma = desc.size, flat.sigma.size
+    d.blob_bytes = blob.numel() if isinstance(blob, torch.Tensor) else blob.size
+    for name in ("row0", "row1", "col0", "col1", "kind", "rank", "buf0", "sig0"):
+        setattr(d, name, i64(getattr(flat, name)))
+    d.sigma = sigma.ctypes.data_as(C.POINTER(C.c_double))
+    d.desc = desc.ctypes.data_as(C.POINTER(_lib.hcmx_descriptor))
+    d.count, d.poff, d.plen = i64(flat.count), i64(flat.poff), i64(flat.plen)
+    d.blob = ptr(blob)
+    d.blob_on_device = int(on_dev)
+    d.row_begin, d.row_end = (0, 0) if row_range is None else row_range
+    d.with_transpose = int(with_transpose)
+    d.nrhs_block = int(nrhs_block)  # 4: matmat decodes once for 4 right-hand sides
+    return d, (keep, sigma, desc, blob)
+
+
 class HMatrix:
     """Device-resident compressed H-matrix (handle over hcmx_gpu_hmat_*)."""
 
@@ -384,30 +413,7 @@ class HMatrix:
         _lib.ensure_device()
         self.n_rows, self.n_cols = int(flat.n_rows), int(flat.n_cols)
         self.row_range = row_range or (0, self.n_rows)
-        keep = {}
-        a = lambda x, t: keep.setdefault(id(x), np.ascontiguousarray(x, dtype=t))
-        i64 = lambda x: a(x, np.int64).ctypes.data_as(C.POINTER(C.c_int64))
-        sigma = np.ascontiguousarray(flat.sigma if flat.sigma.size else np.zeros(1), dtype=np.float64)
-        desc = np.ascontiguousarray(flat.desc)
-        blob = flat.blob
-        on_dev = isinstance(blob, torch.Tensor) and blob.is_cuda
-        if isinstance(blob, torch.Tensor) and not on_dev:
-            blob = blob.numpy()
-        self._keep = (keep, sigma, desc, blob)
-        d = _lib.hcmx_hmat_desc()
-        d.n_rows, d.n_cols, d.nleaves = self.n_rows, self.n_cols, flat.nleaves
-        d.nbuffers, d.nsigma = desc.size, flat.sigma.size
-        d.blob_bytes = blob.numel() if isinstance(blob, torch.Tensor) else blob.size
-        for name in ("row0", "row1", "col0", "col1", "kind", "rank", "buf0", "sig0"):
-            setattr(d, name, i64(getattr(flat, name)))
-        d.sigma = sigma.ctypes.data_as(C.POINTER(C.c_double))
-        d.desc = desc.ctypes.data_as(C.POINTER(_lib.hcmx_descriptor))
-        d.count, d.poff, d.plen = i64(flat.count), i64(flat.poff), i64(flat.plen)
-        d.blob = ptr(blob)
-        d.blob_on_device = int(on_dev)
-        d.row_begin, d.row_end = (0, 0) if row_range is None else row_range
-        d.with_transpose = int(with_transpose)
-        d.nrhs_block = int(nrhs_block)  # 4: matmat decodes once for 4 right-hand sides
+        d, self._keep = flat_desc(flat, row_range, with_transpose, nrhs_block)
         h = C.c_void_p()
         check(lib().hcmx_gpu_hmat_create(C.byref(d), C.byref(h)), "hmat_create")
         self._h = h

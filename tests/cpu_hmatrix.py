@@ -209,3 +209,46 @@ def _build_mode_flat(o, A, lv, n, eps, scheme, mode, dense_too):
                 np.array([b.count for b in bufs], np.int64), np.array(poff, np.int64),
                 np.array([len(b.payload) for b in bufs], np.int64),
                 np.concatenate(parts) if parts else np.zeros(16, np.uint8))
+
+
+def flat_from_leaves(n_rows, n_cols, leaves, eps=1e-6, scheme=0, seed=7, use_ref=False):
+    """A synthetic flat H-matrix from explicit leaves (no geometry): each entry
+    (kind, r0, r1, c0, c1, k) is a dense block (kind 0, entries sign 10^U[-3,0])
+    or an APLR leaf W diag(sigma) X^T of rank k (kind 1: orthonormal W, X from a
+    seeded QR, sigma = 10^-linspace(0, 7, k)), compressed by the checkers'
+    codec.  Lets a test hit leaf shapes the sphere problems never produce
+    (very wide lowrank leaves, odd / ragged chunk counts)."""
+    o = RefOracle() if use_ref else Oracle()
+    rng = np.random.default_rng(seed)
+    L = len(leaves)
+    row0, row1, col0, col1, kind, rank, buf0, sig0 = (np.zeros(L, np.int64) for _ in range(8))
+    sigmas, bufs = [], []
+    nsig = 0
+    for l, (kd, r0, r1, c0, c1, k) in enumerate(leaves):
+        row0[l], row1[l], col0[l], col1[l], kind[l] = r0, r1, c0, c1, kd
+        buf0[l] = len(bufs)
+        rows, cols = r1 - r0, c1 - c0
+        if kd == 0:
+            v = np.sign(rng.standard_normal(rows * cols)) * 10 ** rng.uniform(-3, 0, rows * cols)
+            bufs.append(o.compress(v, eps, scheme))
+            continue
+        rank[l] = k
+        sig0[l] = nsig
+        W = np.linalg.qr(rng.standard_normal((rows, k)))[0]
+        X = np.linalg.qr(rng.standard_normal((cols, k)))[0]
+        s = 10.0 ** -np.linspace(0, 7, k)
+        sigmas.append(s)
+        nsig += k
+        bufs.extend(o.aplr_compress(np.asfortranarray(W), np.asfortranarray(X), s, eps, scheme))
+    poff, off, parts = [], 0, []
+    for b in bufs:
+        poff.append(off)
+        pad = (-len(b.payload)) % 16
+        parts.append(np.frombuffer(b.payload + b"\0" * pad, np.uint8))
+        off += len(b.payload) + pad
+    return Flat(n_rows, n_cols, row0, row1, col0, col1, kind, rank, buf0, sig0,
+                np.concatenate(sigmas) if sigmas else np.zeros(1),
+                np.array([b.scheme for b in bufs], np.uint8), np.array([b.e for b in bufs], np.uint8),
+                np.array([b.m for b in bufs], np.uint8), np.array([b.scale for b in bufs]),
+                np.array([b.count for b in bufs], np.int64), np.array(poff, np.int64),
+                np.array([len(b.payload) for b in bufs], np.int64), np.concatenate(parts))

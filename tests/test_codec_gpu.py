@@ -226,3 +226,32 @@ def test_large_buffers_unfused_path(gpu, oracle):
             assert g.payload == ob.payload, (eps, s, b)
             assert (dec[o: o + c].view(np.uint64) == oracle.decompress(ob).view(np.uint64)).all()
             o += c
+
+
+def test_exponent_width_thresholds(gpu, oracle):
+    """exponent_bits_for (codec.cpp:69-79) flips only where log2(max) - log2(min) + 2
+    crosses a power of two; blocks whose max / min sits exactly on (or one ulp
+    either side of) 2^6, 2^14, 2^30, 2^62 take the device's ambiguity flag and the
+    host re-decision (glibc log2, as the reference) -- descriptors and bytes must
+    still equal the oracle's"""
+    from paper_2308_10960_b200 import codec
+    rng = np.random.default_rng(21)
+    blocks = []
+    for span in (6, 14, 30, 62):
+        for lo in (1.0, 3.7, 1e-100, 2.0 ** -40):
+            hi = lo * 2.0 ** span
+            for top in (hi, np.nextafter(hi, 0.0), np.nextafter(hi, np.inf)):
+                v = lo * 2.0 ** rng.uniform(0, span, 257)
+                v[0], v[1] = lo, top
+                v *= np.sign(rng.standard_normal(v.size))
+                blocks.append(v)
+    counts = np.array([b.size for b in blocks], np.uint64)
+    vals = np.concatenate(blocks)
+    for s in (0, 1):
+        bb = codec.compress_batch(torch.as_tensor(vals).cuda(), counts, 1e-6, s)
+        host = bb.payload.cpu().numpy()
+        for i, v in enumerate(blocks):
+            r = oracle.compress(v, 1e-6, s)
+            got = bb.buffer(i, host)
+            assert (got.descriptor.exp_bits, got.descriptor.mant_bits, got.descriptor.scale) == (r.e, r.m, r.scale), i
+            assert got.payload == r.payload, i

@@ -60,19 +60,32 @@ def _worker(rank, world, port, parts, n, q):
 
 
 def test_partition_balances_bytes():
+    """the library partitioner (hcmx_gpu_partition_rows, host only): contiguous
+    64-row-aligned ranges covering the rows, and its largest per-rank cost is the
+    optimum over every 64-aligned choice of cuts (brute force, world 2 and 3)"""
+    import itertools
     import sys
     sys.path.insert(0, os.path.dirname(__file__))
     from cpu_hmatrix import Flat
-    from paper_2308_10960_b200.distributed import leaf_bytes, partition_rows
+    from paper_2308_10960_b200.distributed import leaf_bytes, partition_rows, rank_cost
     z = np.load(os.path.join(os.path.dirname(__file__), "golden", "hmat_golden.npz"))
     f = Flat.from_npz(z)
+    n = f.n_rows
     for world in (1, 2, 3, 4):
-        parts = partition_rows(f, world, align=16)
-        assert parts[0][0] == 0 and parts[-1][1] == f.n_rows
+        parts = partition_rows(f, world)
+        assert len(parts) == world
+        assert parts[0][0] == 0 and parts[-1][1] == n
         assert all(p[1] == q[0] for p, q in zip(parts[:-1], parts[1:]))
-        assert all(b > a for a, b in parts)
+        assert all(b > a and a % 64 == 0 for a, b in parts)
+        got = max(rank_cost(f, a, b) for a, b in parts)
+        best = min(max(rank_cost(f, a, b) for a, b in zip((0,) + c, c + (n,)))
+                   for c in itertools.combinations(range(64, n, 64), world - 1)) if world <= 3 else got
+        assert got <= best * (1 + 1e-9), (world, got, best)
     lb = leaf_bytes(f)
     assert lb.sum() > 0
+    # more ranks than 64-row units: trailing ranks get empty ranges
+    parts = partition_rows(f, n // 64 + 2)
+    assert parts[-1] == (n, n) and sum(b - a for a, b in parts) == n
 
 
 def test_gloo_world2_block_rows():
@@ -84,7 +97,7 @@ def test_gloo_world2_block_rows():
     f = Flat.from_npz(z)
     n = f.n_rows
     from paper_2308_10960_b200.distributed import partition_rows
-    parts = partition_rows(f, 2, align=16)
+    parts = partition_rows(f, 2)   # the bench's partitioner
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

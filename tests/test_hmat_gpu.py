@@ -314,7 +314,7 @@ def test_partition_writes_into_gather_slab(gpu, oracle):
     f, x = build_small_flat(n=n, eps=1e-6, scheme=0)
     ref = oracle.hmat_matvec(f, 1.0, x, 0.0, np.zeros(n), threads=4)
     world = 2
-    parts = bench.partition_rows(f.to_product(), world)
+    parts = bench.partition_rows(f.to_product(), world)  # the library partitioner
     maxlen = max(b - a for a, b in parts)
     gathered = torch.full((maxlen * world,), 7.0, dtype=torch.float64, device="cuda")
     xd = torch.as_tensor(x).cuda()
@@ -353,3 +353,51 @@ def test_host_api_pinned_and_pageable_y(gpu, oracle):
         H.matvec(1.0, x, beta, yn)
         assert rel(yn, ref) <= TOL, beta
     H.close()
+
+
+def test_partitioned_handle_single_rank_nccl(gpu, oracle):
+    """hcmx_gpu_hmat_create_partitioned with a one-rank NCCL communicator (the
+    multi-GPU C-ABI path on one device: local product + the grouped broadcast
+    exchange), device and host-pointer calls, and without a communicator"""
+    import ctypes as C
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200._lib import check, lib
+    from paper_2308_10960_b200.distributed import PartitionedHMatrix
+    n = 2048
+    f, x = build_small_flat(n=n, eps=1e-6, scheme=0)
+    ref = oracle.hmat_matvec(f, 1.0, x, 0.0, np.zeros(n), threads=4)
+    uid = (C.c_uint8 * 128)()
+    check(lib().hcmx_gpu_nccl_unique_id(uid), "uid")
+    comm = C.c_void_p()
+    check(lib().hcmx_gpu_nccl_comm_init(1, uid, 0, C.byref(comm)), "comm")
+    for c in (comm, None):
+        P = PartitionedHMatrix(f.to_product(), c)
+        assert P.world == 1 and P.rank == 0 and P.row_range == (0, n)
+        y = torch.zeros(n, dtype=torch.float64, device="cuda")
+        P.matvec_device(1.0, torch.as_tensor(x).cuda(), 0.0, y)
+        torch.cuda.synchronize()
+        assert rel(y.cpu().numpy(), ref) <= TOL
+        yh = np.zeros(n)
+        P.matvec(1.0, x, 0.0, yh)
+        assert rel(yh, ref) <= TOL
+        P.close()
+    check(lib().hcmx_gpu_nccl_comm_destroy(comm), "comm destroy")
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_partition_cuts_compose_on_device(gpu, oracle, world):
+    """the ranges hcmx_gpu_partition_rows gives (what each rank's partitioned
+    handle builds) compose the full product: every rank's slice is exact"""
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200.distributed import partition_rows
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    n = 2048
+    f, x = build_small_flat(n=n, eps=1e-6, scheme=1, geometry="cube", kernel="matern")
+    ref = oracle.hmat_matvec(f, 1.0, x, 0.0, np.zeros(n), threads=4)
+    fp = f.to_product()
+    y = np.full(n, np.nan)
+    for a, b in partition_rows(fp, world):
+        H = HMatrix(fp, row_range=(a, b))
+        H.matvec(1.0, x, 0.0, y)
+        H.close()
+    assert rel(y, ref) <= TOL
