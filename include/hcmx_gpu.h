@@ -119,6 +119,28 @@ int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff,
                             uint8_t* d_payload, uint64_t payload_capacity, hcmx_descriptor* h_desc,
                             uint64_t* h_poff, uint64_t* h_total, void* stream);
 
+/* codec.cpp:142-144 compress for a batch with everything on the device and no
+ * host synchronisation (no per-call read-back): counts d_count (each <=
+ * max_count <= 2^17 values), caller-sized payload slots at d_poff (16-byte
+ * aligned; a slot must hold the widest layout the scheme allows, exp_bits 11),
+ * descriptors to d_desc and per-buffer flags to d_flags: bit 0 = the exponent
+ * width was decided next to a 2^k - 2 threshold with the device log2 (the
+ * reference decides it with glibc, codec.cpp:72-73) -- run
+ * hcmx_gpu_codec_compress_fixup before trusting such a buffer; bit 1 =
+ * non-finite input (that buffer is not packed; codec.cpp:119-120). */
+int hcmx_gpu_codec_compress_device(const double* d_values, const uint64_t* d_voff, const uint64_t* d_count,
+                                   uint64_t nbuf, uint64_t max_count, double eps, int scheme,
+                                   const uint64_t* d_poff, uint8_t* d_payload, hcmx_descriptor* d_desc,
+                                   uint32_t* d_flags, void* stream);
+/* completes a compress_device batch bit-exactly: reads the flags (synchronises),
+ * re-decides every flagged exponent width with the reference's host rule and
+ * repacks those buffers; HCMX_INVALID_ARGUMENT if any input was non-finite.
+ * *n_fixed = buffers whose layout changed. */
+int hcmx_gpu_codec_compress_fixup(const double* d_values, const uint64_t* d_voff, const uint64_t* h_count,
+                                  uint64_t nbuf, double eps, int scheme, const uint64_t* h_poff,
+                                  uint8_t* d_payload, hcmx_descriptor* d_desc, const uint32_t* d_flags,
+                                  uint64_t* n_fixed, void* stream);
+
 /* Device time of the batched codec kernels (CUDA events around the fused compress
  * and the unpack launches), accumulated since the last reset.  enable: 1 on, 0 off,
  * < 0 query only (no reset).  Instrumentation for the benchmark, not a reference API. */

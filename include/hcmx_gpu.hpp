@@ -7,8 +7,12 @@
 //     namespace codec = hcmx_gpu::codec;          // instead of hcmx::codec
 //
 // Statuses map back to the reference's exception types: HCMX_INVALID_ARGUMENT
-// -> std::invalid_argument, HCMX_CORRUPT_BUFFER -> corrupt_buffer_error
-// (common.hpp:17-19), anything else -> std::runtime_error.
+// -> std::invalid_argument, HCMX_CORRUPT_BUFFER -> hcmx::corrupt_buffer_error
+// (common.hpp:17-19: the reference's own type when its headers are on the
+// include path, else an identical declaration), anything else ->
+// std::runtime_error.  Where Eigen is available the hmatrix.hpp:126-128
+// signature matvec(double, const M&, const Eigen::VectorXd&, double,
+// Eigen::VectorXd&, bool) is provided too.
 #ifndef HCMX_GPU_HPP
 #define HCMX_GPU_HPP
 
@@ -20,11 +24,27 @@
 
 #include "hcmx_gpu.h"
 
-namespace hcmx_gpu {
-
-struct corrupt_buffer_error : std::runtime_error {
+#if __has_include(<hcmx/common.hpp>)
+#include <hcmx/common.hpp>  // the reference's hcmx::corrupt_buffer_error
+#else
+namespace hcmx {
+// proj/include/hcmx/common.hpp:17-19 (same name, base and constructor)
+class corrupt_buffer_error : public std::runtime_error {
+public:
     using std::runtime_error::runtime_error;
 };
+}  // namespace hcmx
+#endif
+
+#if __has_include(<Eigen/Dense>)
+#include <Eigen/Dense>
+#define HCMX_GPU_HAVE_EIGEN 1
+#endif
+
+namespace hcmx_gpu {
+
+// a reference caller's `catch (const hcmx::corrupt_buffer_error&)` catches it
+using corrupt_buffer_error = hcmx::corrupt_buffer_error;
 
 inline void check(int status, const char* what) {
     if (status == HCMX_OK) return;
@@ -178,18 +198,25 @@ inline CompressedBuffer deserialize(const std::uint8_t* data, std::size_t size, 
 // hcmx_hmat_desc) with the reference's matvec (hmatrix.hpp:126-128).
 class DeviceHMatrix {
 public:
-    explicit DeviceHMatrix(const hcmx_hmat_desc& desc) { check(hcmx_gpu_hmat_create(&desc, &h_), "hmat_create"); }
+    explicit DeviceHMatrix(const hcmx_hmat_desc& desc) : n_rows_(desc.n_rows), n_cols_(desc.n_cols) {
+        check(hcmx_gpu_hmat_create(&desc, &h_), "hmat_create");
+    }
     ~DeviceHMatrix() {
         if (h_) hcmx_gpu_hmat_destroy(h_);
     }
     DeviceHMatrix(const DeviceHMatrix&) = delete;
     DeviceHMatrix& operator=(const DeviceHMatrix&) = delete;
 
-    // y := alpha * M * x + beta * y (host vectors; transpose is not supported yet)
+    // y := alpha * op(M) * x + beta * y (host vectors); transpose needs a matrix
+    // created with desc.with_transpose = 1 (else std::invalid_argument)
     void matvec(double alpha, std::span<const double> x, double beta, std::span<double> y,
-                bool transpose = false) {
+                bool transpose = false) const {
+        if (x.size() != (transpose ? n_rows_ : n_cols_) || y.size() != (transpose ? n_cols_ : n_rows_))
+            throw std::invalid_argument("matvec: dimension mismatch");
         check(hcmx_gpu_hmat_matvec(h_, alpha, x.data(), beta, y.data(), transpose ? 1 : 0), "matvec");
     }
+    std::uint64_t rows() const { return n_rows_; }
+    std::uint64_t cols() const { return n_cols_; }
     hcmx_memory_report memory() const {
         hcmx_memory_report r{};
         check(hcmx_gpu_hmat_memory(h_, &r), "memory");
@@ -199,7 +226,24 @@ public:
 
 private:
     hcmx_hmat* h_ = nullptr;
+    std::uint64_t n_rows_ = 0, n_cols_ = 0;
 };
+
+// hmatrix.hpp:126-128 as a free function (alpha == 0 leaves M untouched, a
+// dimension mismatch throws std::invalid_argument)
+inline void matvec(double alpha, const DeviceHMatrix& M, std::span<const double> x, double beta,
+                   std::span<double> y, bool transpose = false) {
+    M.matvec(alpha, x, beta, y, transpose);
+}
+
+#ifdef HCMX_GPU_HAVE_EIGEN
+// the exact reference signature (hmatrix.hpp:127-128) where Eigen exists
+inline void matvec(double alpha, const DeviceHMatrix& M, const Eigen::VectorXd& x, double beta,
+                   Eigen::VectorXd& y, bool transpose = false) {
+    M.matvec(alpha, std::span<const double>(x.data(), static_cast<std::size_t>(x.size())), beta,
+             std::span<double>(y.data(), static_cast<std::size_t>(y.size())), transpose);
+}
+#endif
 
 }  // namespace hcmx_gpu
 

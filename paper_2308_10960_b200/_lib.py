@@ -90,6 +90,8 @@ PROTOTYPES = {
     "hcmx_gpu_codec_unpack": (_i, [_vp, _vp, _pu64, _vp, _vp, _u64, _vp, _vp]),
     "hcmx_gpu_codec_compress": (_i, [_vp, _vp, _pu64, _u64, _d, _i, _vp, _u64, _vp, _pu64,
                                      _pu64, _vp]),
+    "hcmx_gpu_codec_compress_device": (_i, [_vp, _vp, _vp, _u64, _u64, _d, _i, _vp, _vp, _vp, _vp, _vp]),
+    "hcmx_gpu_codec_compress_fixup": (_i, [_vp, _vp, _pu64, _u64, _d, _i, _pu64, _vp, _vp, _vp, _pu64, _vp]),
     "hcmx_gpu_codec_timing": (_i, [_i, C.POINTER(_d), _pu64, C.POINTER(_d), _pu64]),
     "hcmx_gpu_compress": (_i, [_vp, _u64, _d, _i, _pdesc, _vp, _u64, _pu64]),
     "hcmx_gpu_compress_block": (_i, [_vp, _u64, _pdesc, _vp, _u64, _pu64]),

@@ -4,10 +4,11 @@ runs once before the hot path; torch on the GPU when present).
 Dense (inadmissible) leaves are evaluated entry by entry.  Admissible leaves
 get W, sigma, X with A ~= W diag(sigma) X^T, W and X orthonormal, truncated by
 the reference's rank rule sigma_k > eps * sigma_0 (lowrank.cpp:14-21) -- the
-shape svd_factors produces (lowrank.cpp:76-93).  Blocks up to 256 columns use
-a full SVD; larger blocks a randomized range finder with one power iteration,
-whose sketch is grown until the captured spectrum reaches 1e-3 * eps * sigma_0,
-so the truncation sees the same leading singular values a full SVD would.
+shape svd_factors produces (lowrank.cpp:76-93).  Blocks up to EXACT_SVD_MAX (32)
+columns use a full SVD; larger blocks a randomized range finder whose sketch
+is grown per block until the captured spectrum reaches 1e-3 * eps * sigma_0,
+so the truncation sees the same leading singular values a full SVD would
+(tests/test_assemble.py compares ranks and singular values with a full SVD).
 """
 from __future__ import annotations
 
@@ -22,7 +23,7 @@ import torch
 from .problems import PointKernel
 from .tree import BlockLeaves
 
-EXACT_SVD_MAX = 64
+EXACT_SVD_MAX = 32
 
 
 @dataclass
@@ -52,7 +53,7 @@ def _cpu_svd(M: torch.Tensor):
     """batched SVD of small matrices on the host (LAPACK gesdd per matrix, threads
     over the batch): cuSOLVER runs batched SVDs above 32x32 one matrix at a time"""
     from concurrent.futures import ThreadPoolExecutor
-    a = M.detach().cpu().numpy()
+    a = M.detach().resolve_conj().cpu().numpy()
     B = a.shape[0]
     U = np.empty(a.shape[:-1] + (min(a.shape[-2:]),), a.dtype)
     S = np.empty((B, min(a.shape[-2:])))
@@ -65,30 +66,91 @@ def _cpu_svd(M: torch.Tensor):
         if hi > lo:
             U[lo:hi], S[lo:hi], Vh[lo:hi] = np.linalg.svd(a[lo:hi], full_matrices=False)
 
-    with ThreadPoolExecutor(nt) as ex:
+    # one BLAS thread per worker: numpy's LAPACK would otherwise start a full
+    # OpenBLAS pool inside every worker thread (nt x cores threads thrashing)
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1), ThreadPoolExecutor(nt) as ex:
         list(ex.map(work, range(nt)))
     dev = M.device
     return torch.from_numpy(U).to(dev), torch.from_numpy(S).to(dev), torch.from_numpy(Vh).to(dev)
 
 
-def _svd_batch(A: torch.Tensor, eps: float):
+def _orth(Y: torch.Tensor) -> torch.Tensor:
+    """orthonormal basis of the columns of a batch of tall matrices: classical
+    Gram-Schmidt applied twice per column (batched GEMVs, so it stays fast for
+    many small blocks where the batched Householder QR launches per matrix).
+    Numerically dependent columns become arbitrary orthonormal directions, which
+    a range finder tolerates."""
+    B, m, p = Y.shape
+    Q = torch.empty_like(Y)
+    for j in range(p):
+        v = Y[:, :, j:j + 1]
+        for _ in range(2):
+            if j:
+                Qj = Q[:, :, :j]
+                v = v - Qj @ (Qj.mH @ v)
+        Q[:, :, j:j + 1] = v / torch.clamp(v.norm(dim=1, keepdim=True), min=1e-300)
+    return Q
+
+
+def _core_svd(M: torch.Tensor):
+    """SVD of a batch of small square cores: batched Jacobi on the GPU up to 32 x 32
+    (cuSOLVER's batched gesvdj), host LAPACK beyond"""
+    if M.is_cuda and M.shape[-1] <= 32:
+        U, S, Vh = torch.linalg.svd(M, full_matrices=False)
+        return U, S, Vh
+    return _cpu_svd(M)
+
+
+def _svd_batch(A: torch.Tensor, eps: float, p0: int = 32):
+    """truncation-grade SVD of a batch of blocks: (U, S, Vh) holding at least every
+    singular triple above 1e-3 * eps * sigma_0 (the rank rule then keeps sigma_k >
+    eps * sigma_0, lowrank.cpp:14-21).  Blocks up to EXACT_SVD_MAX columns: full
+    SVD.  Larger: a randomized range finder Q = orth(A Omega) with p columns,
+    then the exact SVD of Q^H A through Z = A^H Q = Q2 R2 (Q^H A = R2^H Q2^H, so
+    R2^H is the p x p core).  p grows per block (32, 64, 128, ...) until the
+    p-th singular value of Q^H A is below 1e-3 * eps * sigma_0, so the sketch
+    spans the whole retained spectrum; blocks that miss are redone with the next
+    p, the others keep their result (zero-padded to the batch's width)."""
     B, m, n = A.shape
     if min(m, n) <= EXACT_SVD_MAX:
-        return _cpu_svd(A)
+        return _core_svd(A) if m == n else _cpu_svd(A)
     g = torch.Generator(device=A.device)
     g.manual_seed(1234 + m)
-    p = min(min(m, n), 64)
+    k = min(m, n)
+    p = min(k, p0)
+    todo = torch.arange(B, device=A.device)
+    U = S = Vh = None
     while True:
-        omega = torch.randn(B, n, p, dtype=A.dtype, device=A.device, generator=g)
-        Q, _ = torch.linalg.qr(A @ omega)
-        Q, _ = torch.linalg.qr(A.mH @ Q)                  # one power iteration
-        Q, _ = torch.linalg.qr(A @ Q)
-        Bt = A.mH @ Q                                     # (Q^H A)^H, n x p
-        Q2, R2 = torch.linalg.qr(Bt)                      # Q^H A = R2^H Q2^H
-        Ur, S, Vrh = _cpu_svd(R2.mH)                      # p x p
-        if p >= min(m, n) or bool((S[:, -1] <= 1e-3 * eps * S[:, 0]).all()):
-            return Q @ Ur, S, (Q2 @ Vrh.mH).mH
-        p = min(min(m, n), 2 * p)
+        Ab = A[todo] if todo.numel() < B else A
+        nb = Ab.shape[0]
+        omega = torch.randn(nb, n, p, dtype=A.dtype, device=A.device, generator=g)
+        Q = _orth(Ab @ omega)                              # range of A, m x p
+        Z = Ab.mH @ Q                                      # (Q^H A)^H, n x p
+        Q2 = _orth(Z)
+        R2 = Q2.mH @ Z                                     # Z = Q2 R2
+        Ur, Sb, Vrh = _core_svd(R2.mH)                     # Q^H A = Ur Sb (Q2 Vrh^H)^H
+        Ub, Vb = Q @ Ur, Vrh @ Q2.mH
+        if U is None:  # width p for now, zero-padded when a later round widens it
+            U = torch.zeros(B, m, p, dtype=A.dtype, device=A.device)
+            S = torch.zeros(B, p, dtype=Sb.dtype, device=A.device)
+            Vh = torch.zeros(B, p, n, dtype=A.dtype, device=A.device)
+        elif U.shape[2] < p:
+            pad = p - U.shape[2]
+            U = torch.nn.functional.pad(U, (0, pad))
+            S = torch.nn.functional.pad(S, (0, pad))
+            Vh = torch.nn.functional.pad(Vh, (0, 0, 0, pad))
+        done = (Sb[:, -1] <= 1e-3 * eps * Sb[:, 0]) | (p >= k)
+        idx = todo[done]
+        U[idx, :, :p] = Ub[done]
+        S[idx, :p] = Sb[done]
+        Vh[idx, :p, :] = Vb[done]
+        todo = todo[~done]
+        if todo.numel() == 0:
+            break
+        p = min(k, 2 * p)
+    w = max(1, int((S > 0).sum(dim=1).max().item())) if B else 1
+    return U[:, :, :w], S[:, :w], Vh[:, :w, :]
 
 
 def assemble(points_internal: np.ndarray, leaves: BlockLeaves, kernel: PointKernel, eps: float,

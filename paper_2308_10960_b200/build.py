@@ -15,8 +15,12 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libhcmx_gpu.so")
+# HCMX_BUILD_TAG (profiling aid): build a variant (e.g. other HCMX_NVCC_DEFS)
+# into variants/libhcmx_gpu_<tag>.so instead of the product library
+_TAG = os.environ.get("HCMX_BUILD_TAG")
+OBJ = os.path.join(HERE, "_build" + (f"_{_TAG}" if _TAG else ""))
+LIB = (os.path.join(ROOT, "variants", f"libhcmx_gpu_{_TAG}.so") if _TAG
+       else os.path.join(HERE, "libhcmx_gpu.so"))
 INC = os.path.join(ROOT, "include")
 
 NVCC = os.environ.get("NVCC", "nvcc")
@@ -62,6 +66,7 @@ def _stale(src, obj, extra=()):
 
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     if _flags_changed():
         force = True
     objs = []

@@ -289,6 +289,60 @@ def compress_batch(values: torch.Tensor, counts, eps: float, scheme, capacity: i
     return bb
 
 
+@dataclass
+class DeviceBatch:
+    """a compress_device batch: every table on the device, nothing read back"""
+    count: np.ndarray         # uint64 [nbuf] (host copy, for the fix-up)
+    poff: np.ndarray          # uint64 [nbuf] slot offsets (host copy)
+    d_count: torch.Tensor
+    d_voff: torch.Tensor
+    d_poff: torch.Tensor
+    d_desc: torch.Tensor      # uint8 [nbuf * 16] (hcmx_descriptor)
+    d_flags: torch.Tensor     # int32 [nbuf]
+    payload: torch.Tensor
+    eps: float
+    scheme: int
+
+
+def device_batch(values: torch.Tensor, counts, eps: float, scheme, voff=None) -> DeviceBatch:
+    """tables for compress_device over `values`: slots sized for the widest layout
+    the scheme allows (exp_bits 11), 16-byte aligned"""
+    counts = np.ascontiguousarray(counts, dtype=np.uint64)
+    nb = counts.size
+    widest = make_descriptor(scheme, eps, 1.0, 11).bit_width()
+    slot = ((counts * np.uint64(widest) + np.uint64(7)) // np.uint64(8) + np.uint64(15)) // np.uint64(16) * np.uint64(16)
+    poff = _offsets(slot)
+    vo = _offsets(counts) if voff is None else np.ascontiguousarray(voff, dtype=np.uint64)
+    tot = int(slot.sum()) + 16
+    dv = lambda a: torch.as_tensor(a.view(np.int64)).cuda()
+    return DeviceBatch(counts, poff, dv(counts), dv(vo), dv(poff),
+                       torch.zeros(16 * max(nb, 1), dtype=torch.uint8, device="cuda"),
+                       torch.zeros(max(nb, 1), dtype=torch.int32, device="cuda"),
+                       torch.empty(tot, dtype=torch.uint8, device="cuda"), float(eps), int(scheme))
+
+
+def compress_device(values: torch.Tensor, db: DeviceBatch) -> DeviceBatch:
+    """hcmx_gpu_codec_compress_device: one asynchronous launch, no read-back"""
+    values = _dev_f64(values)
+    check(lib().hcmx_gpu_codec_compress_device(ptr(values), ptr(db.d_voff), ptr(db.d_count), db.count.size,
+                                               int(db.count.max()) if db.count.size else 0, db.eps, db.scheme,
+                                               ptr(db.d_poff), ptr(db.payload), ptr(db.d_desc), ptr(db.d_flags),
+                                               _stream()), "compress_device")
+    return db
+
+
+def compress_device_finish(values: torch.Tensor, db: DeviceBatch) -> tuple[BatchBuffers, int]:
+    """hcmx_gpu_codec_compress_fixup, then the batch as BatchBuffers (host descriptors)"""
+    values = _dev_f64(values)
+    n = C.c_uint64()
+    check(lib().hcmx_gpu_codec_compress_fixup(ptr(values), ptr(db.d_voff), u64p(db.count), db.count.size, db.eps,
+                                              db.scheme, u64p(db.poff), ptr(db.payload), ptr(db.d_desc),
+                                              ptr(db.d_flags), C.byref(n), _stream()), "compress_fixup")
+    desc = db.d_desc.cpu().numpy()[: 16 * db.count.size].view(DESC_DTYPE).copy()
+    tot = int(db.poff[-1] + (int(db.count[-1]) * int(desc["bit_width"][-1]) + 7) // 8) if db.count.size else 0
+    return BatchBuffers(desc, db.count, db.poff, db.payload, tot), n.value
+
+
 def decompress_batch(bb: BatchBuffers, out: torch.Tensor | None = None, voff=None) -> torch.Tensor:
     """codec::decompress_into for every buffer of a batch (device -> device)"""
     _lib.ensure_device()

@@ -506,7 +506,7 @@ k_compress_cta(const double* __restrict__ values, const uint64_t* __restrict__ v
             st.max_mag = dmax;
             st.all_zero = all_zero ? 1u : 0u;
             st.non_finite = nf;
-            stats[b] = st;
+            if (stats) stats[b] = st;
             flags[b] = ambiguous | (nf ? 2u : 0u);  // bit 1: non-finite input (rejected)
         }
         if (nf) continue;
@@ -989,6 +989,66 @@ int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff, cons
             launch_pack_jobs(d_values, dv1.as<uint64_t>(), dc1.as<uint64_t>(), h_count + b,
                              d1.as<hcmx_descriptor>(), dp1.as<uint64_t>(), 1, d_payload, stream);
         }
+    });
+}
+
+int hcmx_gpu_codec_compress_device(const double* d_values, const uint64_t* d_voff, const uint64_t* d_count,
+                                   uint64_t nbuf, uint64_t max_count, double eps, int scheme, const uint64_t* d_poff,
+                                   uint8_t* d_payload, hcmx_descriptor* d_desc, uint32_t* d_flags, void* stream) {
+    return guarded([&] {
+        require_device();
+        alignment_unit(scheme);
+        const uint8_t m_req = mantissa_bits_for(eps);  // eps validation first (codec.cpp:63-64)
+        if (max_count > kFuseMax) throw invalid_argument("compress_device: buffers above 2^17 values take hcmx_gpu_codec_compress");
+        if (!nbuf) return;
+        cudaStream_t s = (cudaStream_t)stream;
+        const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(nbuf, 148ull * 16));
+        KernelTimer kt(0, s);
+        k_compress_cta<<<grid, kCtaWarps * 32, 0, s>>>(d_values, d_voff, d_count, nbuf, scheme, m_req, d_poff,
+                                                       d_payload, d_desc, nullptr, d_flags);
+        check_cuda(cudaGetLastError(), "compress launch");
+        kt.stop();
+    });
+}
+
+int hcmx_gpu_codec_compress_fixup(const double* d_values, const uint64_t* d_voff, const uint64_t* h_count,
+                                  uint64_t nbuf, double eps, int scheme, const uint64_t* h_poff, uint8_t* d_payload,
+                                  hcmx_descriptor* d_desc, const uint32_t* d_flags, uint64_t* n_fixed, void* stream) {
+    return guarded([&] {
+        require_device();
+        std::vector<uint32_t> fl(nbuf);
+        d2h(fl.data(), d_flags, nbuf * 4, stream);
+        stream_sync(stream);
+        uint64_t fixed = 0;
+        for (uint64_t b = 0; b < nbuf; ++b)
+            if (fl[b] & 2u) throw invalid_argument("compress: values must be finite");
+        for (uint64_t b = 0; b < nbuf; ++b) {
+            if (!(fl[b] & 1u)) continue;
+            // exponent width next to a 2^k - 2 threshold: decide with glibc (codec.cpp:72-73)
+            uint64_t vo = 0;
+            d2h(&vo, d_voff + b, 8, stream);
+            stream_sync(stream);
+            DevBuf dv1 = upload_u64(&vo, 1, stream), dc1 = upload_u64(h_count + b, 1, stream);
+            DevBuf dst(sizeof(hcmx_stats));
+            launch_analyze_jobs(d_values, dv1.as<uint64_t>(), dc1.as<uint64_t>(), h_count + b, 1,
+                                dst.as<hcmx_stats>(), stream);
+            hcmx_stats st{};
+            hcmx_descriptor cur{};
+            d2h(&st, dst.p, sizeof(st), stream);
+            d2h(&cur, d_desc + b, sizeof(cur), stream);
+            stream_sync(stream);
+            const hcmx_descriptor exact = make_descriptor(scheme, eps, st);
+            if (exact.exp_bits == cur.exp_bits) continue;
+            if (payload_bytes(h_count[b], exact.bit_width) > payload_bytes(h_count[b], make_descriptor(scheme, eps, 1.0, 11).bit_width))
+                throw std::logic_error("compress_fixup: slot too small");
+            h2d(d_desc + b, &exact, sizeof(exact), stream);
+            DevBuf dp1 = upload_u64(h_poff + b, 1, stream);
+            launch_pack_jobs(d_values, dv1.as<uint64_t>(), dc1.as<uint64_t>(), h_count + b, d_desc + b,
+                             dp1.as<uint64_t>(), 1, d_payload, stream);
+            ++fixed;
+        }
+        stream_sync(stream);
+        if (n_fixed) *n_fixed = fixed;
     });
 }
 

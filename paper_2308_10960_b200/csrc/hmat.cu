@@ -32,6 +32,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <sys/mman.h>
+
 #include <cstdio>
 #include <cstdlib>
 
@@ -53,11 +55,14 @@ namespace hcmx_gpu {
 namespace {
 
 #ifndef HCMX_NWB
-#define HCMX_NWB 16
+#define HCMX_NWB 8
 #endif
 constexpr int kNWB = HCMX_NWB;            // phase-B consumer warps per CTA
 #ifndef HCMX_NWA
 #define HCMX_NWA 8
+#endif
+#ifndef HCMX_NWB_MULTI
+#define HCMX_NWB_MULTI 8
 #endif
 #ifndef HCMX_NSTAGE
 #define HCMX_NSTAGE 3
@@ -108,17 +113,17 @@ constexpr int kAUnroll = HCMX_AUNROLL;   // row groups per iteration of the phas
 constexpr uint64_t kAItemBytes = HCMX_AITEM;  // packed data per phase-A item
 constexpr uint32_t kAItemXBytes = 12288;  // staged x slices per phase-A item
 #ifndef HCMX_BGROUP
-#define HCMX_BGROUP 16
+#define HCMX_BGROUP 32
 #endif
 #ifndef HCMX_BITEM
-#define HCMX_BITEM 4096
+#define HCMX_BITEM 8192
 #endif
 constexpr int kBLRGroup = HCMX_BGROUP;  // max columns per B item
 constexpr uint64_t kAStripeBytes = 8 * kStageBytes;  // target packed bytes per phase-A CTA
 constexpr uint64_t kItemTarget = 1536;          // packed bytes per item (columns grouped up to this)
 constexpr uint64_t kItemMaxBytes = HCMX_BITEM;  // items merge columns up to this many packed bytes
 constexpr size_t kRingBytes = static_cast<size_t>(kNStage) * kSlotBytes;
-constexpr size_t kRedBytes = (kNWB / 2) * kR * sizeof(double);  // phase-B cross-warp reduction
+constexpr size_t kRedBytes = ((kNWB > HCMX_NWB_MULTI ? kNWB : HCMX_NWB_MULTI) / 2) * kR * sizeof(double);  // phase-B cross-warp reduction
 constexpr size_t kSmemBytes = kRingBytes + kRedBytes + 2 * kNStage * sizeof(uint64_t);  // + full, empty barriers
 constexpr int kCopies = 2 * kMaxItems;  // coefficient copies per stage (two per producer lane)
 // copy entry (u64): [0,32) source element index, [32,48) dst / 16 in the slot,
@@ -163,9 +168,6 @@ template <int R>
 __host__ __device__ constexpr int rec_bytes() { return R == 1 ? 32 : (8 * R + 16 + 15) / 16 * 16; }
 constexpr uint32_t kMaxPieces = 4;  // pieces a phase-B row block may be split into
 constexpr int kMultiR = 4;    // right-hand sides per product of a multi-RHS arena
-#ifndef HCMX_NWB_MULTI
-#define HCMX_NWB_MULTI 8
-#endif
 constexpr int kNWBMulti = HCMX_NWB_MULTI;  // phase-B consumer warps for R > 1 (R x 4 accumulators per lane)
 inline uint32_t rec_bytes_rt(int R) { return R == 1 ? 32u : static_cast<uint32_t>((8 * R + 16 + 15) / 16 * 16); }
 template <int R>
@@ -238,6 +240,9 @@ struct Params {
     double* y;                  // R > 1: n x R, row-major
     uint32_t row_begin, row_end;
     double alpha, beta;
+    uint64_t bias;              // 1023 << 52, the decoders' exponent bias: a runtime value keeps it in
+                                // a register pair (a literal is rematerialised into uniform registers
+                                // inside every decode loop)
     int debug;                  // profiling knob (HCMX_DEBUG): 1 = consumers skip the decode
 };
 
@@ -359,9 +364,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // IMAD with the bias 1023 << 52 rebuilds 1.mant * 2^offset (offset + 1023 <=
 // 2046: no clamp for e <= 10); one DADD takes the 1 off and the sign is xored
 // into the high word.  About 8 instructions per value with the FMA.
-__device__ __forceinline__ double dec_fast(const uint32_t* sp, unsigned s, uint32_t mask, uint32_t mul) {
+__device__ __forceinline__ double dec_fast(const uint32_t* sp, unsigned s, uint32_t mask, uint32_t mul,
+                                          uint64_t bias) {
     const uint32_t t = __funnelshift_l(sp[0], sp[1], s);
-    const uint64_t bits = static_cast<uint64_t>(t & mask) * mul + (1023ull << 52);
+    const uint64_t bits = static_cast<uint64_t>(t & mask) * mul + bias;
     const double v = __longlong_as_double(static_cast<long long>(bits)) - 1.0;
     return __hiloint2double(__double2hiint(v) ^ static_cast<int>(t & 0x80000000u), __double2loint(v));
 }
@@ -686,7 +692,8 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
 // FMA chain per row of the group, R > 1 one chain per right-hand side.
 template <int R>
 __device__ __forceinline__ void a_fast(const uint32_t* data, unsigned P, unsigned w, unsigned e, const double* xs,
-                                       unsigned ngroups, unsigned rowbits, unsigned gwords, double (&res)[R]) {
+                                       unsigned ngroups, unsigned rowbits, unsigned gwords, uint64_t bias,
+                                       double (&res)[R]) {
     const uint32_t mask = fast_mask(w);
     const uint32_t mul = c_pow2e.v[e & 31u];
     const uint32_t* q[kARows];
@@ -712,7 +719,7 @@ __device__ __forceinline__ void a_fast(const uint32_t* data, unsigned P, unsigne
         }
 #pragma unroll
         for (int r = 0; r < kARows; ++r) {
-            const double d = dec_fast(q[r], s[r], mask, mul);
+            const double d = dec_fast(q[r], s[r], mask, mul, bias);
             if (R == 1) {
                 acc[r] = fma(d, xv[r], acc[r]);
             } else {
@@ -775,7 +782,7 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
     const uint32_t* data = recs + ((nl + 3u) & ~3u);
     const double* xs = reinterpret_cast<const double*>(slot) + (rec >> 19);
     double r[R];
-    if (it.body) a_fast<R>(data, P, w, (rec >> 7) & 15u, xs, it.nf / kARows, it.rowbits, it.gwords, r);
+    if (it.body) a_fast<R>(data, P, w, (rec >> 7) & 15u, xs, it.nf / kARows, it.rowbits, it.gwords, p.bias, r);
     else a_generic<R>(data, P, rec, xs, it.nf, it.rowbits, it.gwords, r);
     // the chunks of a slot's rank column (lanes slot, slot + nslot, ...): fixed
     // butterfly (lane `slot` gets the same order on every run); idle lanes add 0
@@ -926,13 +933,14 @@ __device__ __forceinline__ void b_item_generic(const BItem& it, const uint32_t* 
 // each column segment, at the same shift in every group (32 fields = w words)
 template <int GLO, int GHI, int R>
 __device__ __forceinline__ void b_column_full(const uint32_t* seg, unsigned lane, unsigned w, uint32_t mask,
-                                              uint32_t mul, const double (&coef)[R], double (&acc)[kG * R]) {
+                                              uint32_t mul, uint64_t bias, const double (&coef)[R],
+                                              double (&acc)[kG * R]) {
     const unsigned top = (lane + 1) * w;  // one past the sign bit of field `lane`
     const uint32_t* sp = seg + ((top - 1) >> 5) - 1;
     const unsigned s = 0u - top;          // the funnel shift takes it modulo 32
 #pragma unroll
     for (int g = GLO; g < GHI; ++g) {
-        const double d = dec_fast(sp + (g - GLO) * w, s, mask, mul);
+        const double d = dec_fast(sp + (g - GLO) * w, s, mask, mul, bias);
 #pragma unroll
         for (int c = 0; c < R; ++c) acc[g * R + c] = fma(d, coef[c], acc[g * R + c]);
     }
@@ -940,7 +948,7 @@ __device__ __forceinline__ void b_column_full(const uint32_t* seg, unsigned lane
 
 template <int GLO, int GHI, int R>
 __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg, const double* cf, unsigned lane,
-                                            double dmul, double (&acc)[kG * R]) {
+                                            double dmul, uint64_t bias, double (&acc)[kG * R]) {
     const unsigned nseg = it.nseg;
     if (it.kind == 0) {  // dense: one layout for the whole item
         const unsigned w = it.dpacked & 0xffu, e = (it.dpacked >> 16) & 0xffu;
@@ -954,7 +962,7 @@ __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg
 #pragma unroll 2
             for (unsigned c = 0; c < nseg; ++c) {
                 const double xc[R] = {cf[c]};
-                b_column_full<GLO, GHI, R>(seg, lane, w, mask, mul, xc, t);
+                b_column_full<GLO, GHI, R>(seg, lane, w, mask, mul, bias, xc, t);
                 seg += segw;
             }
 #pragma unroll
@@ -964,7 +972,7 @@ __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg
                 double xc[R];
 #pragma unroll
                 for (int q = 0; q < R; ++q) xc[q] = dmul * cf[c * R + q];
-                b_column_full<GLO, GHI, R>(seg, lane, w, mask, mul, xc, acc);
+                b_column_full<GLO, GHI, R>(seg, lane, w, mask, mul, bias, xc, acc);
                 seg += segw;
             }
         }
@@ -991,7 +999,7 @@ __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg
                 mul = pr.y;
                 w = pr.w;
             }
-            b_column_full<GLO, GHI, R>(seg, lane, w, mask, mul, cc, acc);
+            b_column_full<GLO, GHI, R>(seg, lane, w, mask, mul, bias, cc, acc);
             seg += (GHI - GLO) * w;
         }
     }
@@ -1008,9 +1016,9 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
     // which keeps the kernel inside the instruction cache
     static_assert(kG == 4, "fast-path table assumes 128-row blocks");
     switch (it.fcase) {  // the body index, precomputed by bcase_of (a dense jump table)
-        case 1: b_item_full<0, 4, R>(it, seg, cf, lane, dmul, acc); break;
-        case 2: b_item_full<0, 2, R>(it, seg, cf, lane, dmul, acc); break;
-        case 3: b_item_full<2, 4, R>(it, seg, cf, lane, dmul, acc); break;
+        case 1: b_item_full<0, 4, R>(it, seg, cf, lane, dmul, p.bias, acc); break;
+        case 2: b_item_full<0, 2, R>(it, seg, cf, lane, dmul, p.bias, acc); break;
+        case 3: b_item_full<2, 4, R>(it, seg, cf, lane, dmul, p.bias, acc); break;
         default:
             b_item_generic<R>(it, seg, cf, lane, dmul, acc);  // also uncompressed words (modes 3-5)
             break;
@@ -1334,10 +1342,24 @@ std::vector<std::pair<uint32_t, uint32_t>> column_groups(uint32_t n, uint32_t ma
     return g;
 }
 
+// anonymous, lazily backed host mapping (pages cost nothing until written)
+struct HostBlob {
+    uint8_t* p = nullptr;
+    size_t bytes = 0;
+    void map(size_t n) {
+        bytes = std::max<size_t>(n, 1);
+        void* q = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+        if (q == MAP_FAILED) throw oom_error("hmat: host mapping of the blob failed");
+        p = static_cast<uint8_t*>(q);
+    }
+    ~HostBlob() {
+        if (p) munmap(p, bytes);
+    }
+};
+
 struct Builder {
     const hcmx_hmat_desc& d;
     hcmx_hmat* h;
-    std::vector<uint8_t> blob_host;
     const uint8_t* blob = nullptr;
     bool keep_map = false;
 
@@ -1815,13 +1837,6 @@ void validate(const hcmx_hmat_desc& d) {
 void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     validate(d);
     Builder B(d, h);
-    if (d.blob_on_device) {
-        B.blob_host.resize(d.blob_bytes);
-        check_cuda(cudaMemcpy(B.blob_host.data(), d.blob, d.blob_bytes, cudaMemcpyDeviceToHost), "blob d2h");
-        B.blob = B.blob_host.data();
-    } else {
-        B.blob = d.blob;
-    }
     h->n_rows = d.n_rows;
     h->n_cols = d.n_cols;
     h->rb = d.row_begin;
@@ -1835,6 +1850,44 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     std::vector<uint64_t> leaves;
     for (uint64_t l = 0; l < d.nleaves; ++l)
         if ((uint64_t)d.row0[l] < h->re && (uint64_t)d.row1[l] > h->rb) leaves.push_back(l);
+
+    HostBlob hb;
+    if (d.blob_on_device) {
+        // a device-resident blob is read on the host through a lazily backed
+        // mapping: only the byte ranges of this partition's buffers are copied
+        // (and become resident), so one rank of a block-row partition does not
+        // hold the whole matrix in host memory
+        std::vector<std::pair<uint64_t, uint64_t>> rng;  // [begin, end)
+        auto need = [&](int64_t b) {
+            if (d.plen[b] > 0) rng.push_back({static_cast<uint64_t>(d.poff[b]), static_cast<uint64_t>(d.poff[b] + d.plen[b])});
+        };
+        for (uint64_t l : leaves) {
+            const int64_t k = d.rank[l];
+            const int64_t nb = d.kind[l] == 0 ? 1 : d.kind[l] == 1 ? 2 * k : (k > 0 ? 2 : 0);
+            for (int64_t i = 0; i < nb; ++i) need(d.buf0[l] + i);
+        }
+        std::sort(rng.begin(), rng.end());
+        hb.map(d.blob_bytes);
+        uint64_t a = 0, e = 0;
+        bool open = false;
+        auto flush = [&]() {
+            if (open) check_cuda(cudaMemcpy(hb.p + a, d.blob + a, e - a, cudaMemcpyDeviceToHost), "blob d2h");
+        };
+        for (const auto& r : rng) {
+            if (open && r.first <= e + 65536) {
+                e = std::max(e, r.second);
+            } else {
+                flush();
+                a = r.first;
+                e = r.second;
+                open = true;
+            }
+        }
+        flush();
+        B.blob = hb.p;
+    } else {
+        B.blob = d.blob;
+    }
 
     uint64_t total_fields = 0;
     for (uint64_t b = 0; b < d.nbuffers; ++b) total_fields += d.count[b];
@@ -2270,6 +2323,7 @@ Params make_params(hcmx_hmat* h, double alpha, double beta, double* y) {
     p.row_end = static_cast<uint32_t>(h->re);
     p.alpha = alpha;
     p.beta = beta;
+    p.bias = 1023ull << 52;
     return p;
 }
 

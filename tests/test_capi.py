@@ -136,15 +136,23 @@ int main() {
     codec::CompressedBuffer b{d, 0, {}};
     codec::serialize(b, wire);
     std::size_t off = 0;
-    try { codec::deserialize(wire.data(), 10, off); } catch (const hcmx_gpu::corrupt_buffer_error&) { std::printf("corrupt\n"); }
+    // a reference caller catches the reference's own exception type
+    try { codec::deserialize(wire.data(), 10, off); } catch (const hcmx::corrupt_buffer_error&) { std::printf("corrupt\n"); }
+    static_assert(std::is_same_v<hcmx_gpu::corrupt_buffer_error, hcmx::corrupt_buffer_error>);
     return 0;
 }
 ''')
     libdir = os.path.join(root, "paper_2308_10960_b200")
-    exe = tmp_path / "shim"
-    subprocess.run(["g++", "-std=c++20", "-I" + os.path.join(root, "include"), str(src), "-L" + libdir,
-                    "-lhcmx_gpu", "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
-    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
-    m, mant, w, size = out[0].split()
-    assert (m, mant, w, size) == ("19", "26", "32", str(20 + 64 * 4))  # AFLP widens m to a byte multiple
-    assert out[1] == "invalid_argument" and out[2] == "corrupt"
+    # with and (where present) without the reference's headers on the include path:
+    # the shim then throws the reference's hcmx::corrupt_buffer_error (common.hpp:17-19)
+    variants = [[]]
+    if os.path.isfile("/root/reference/proj/include/hcmx/common.hpp"):
+        variants.append(["-I/root/reference/proj/include"])
+    for i, extra in enumerate(variants):
+        exe = tmp_path / f"shim{i}"
+        subprocess.run(["g++", "-std=c++20", "-I" + os.path.join(root, "include"), *extra, str(src), "-L" + libdir,
+                        "-lhcmx_gpu", "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
+        out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+        m, mant, w, size = out[0].split()
+        assert (m, mant, w, size) == ("19", "26", "32", str(20 + 64 * 4))  # AFLP widens m to a byte multiple
+        assert out[1] == "invalid_argument" and out[2] == "corrupt"

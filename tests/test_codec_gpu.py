@@ -255,3 +255,37 @@ def test_exponent_width_thresholds(gpu, oracle):
             got = bb.buffer(i, host)
             assert (got.descriptor.exp_bits, got.descriptor.mant_bits, got.descriptor.scale) == (r.e, r.m, r.scale), i
             assert got.payload == r.payload, i
+
+
+def test_compress_device_api_bit_exact(gpu, oracle):
+    """hcmx_gpu_codec_compress_device (no read-back) + the fix-up: the same bytes
+    and descriptors as the oracle, including blocks on exponent thresholds (which
+    the fix-up re-decides with the host rule) and an all-zero block"""
+    from paper_2308_10960_b200 import codec
+    rng = np.random.default_rng(5)
+    blocks = [np.sign(rng.standard_normal(4096)) * 10 ** rng.uniform(-6, 0, 4096) for _ in range(40)]
+    for span in (6, 14):
+        v = 2.0 ** rng.uniform(0, span, 300)
+        v[0], v[1] = 1.0, 2.0 ** span
+        blocks.append(v)
+    blocks.append(np.zeros(100))
+    counts = np.array([b.size for b in blocks], np.uint64)
+    vals = torch.as_tensor(np.concatenate(blocks)).cuda()
+    for s in (0, 1, 3):
+        db = codec.device_batch(vals, counts, 1e-6, s)
+        codec.compress_device(vals, db)
+        flags = db.d_flags.cpu().numpy()
+        assert (flags[-3:-1] & 1).all() and not (flags[:40] & 1).any()
+        bb, nfix = codec.compress_device_finish(vals, db)
+        host = bb.payload.cpu().numpy()
+        for i, v in enumerate(blocks):
+            r = oracle.compress(v, 1e-6, s)
+            got = bb.buffer(i, host)
+            assert (got.descriptor.exp_bits, got.descriptor.mant_bits, got.descriptor.scale) == (r.e, r.m, r.scale), (s, i)
+            assert got.payload == r.payload, (s, i)
+    bad = vals.clone()
+    bad[5] = float("nan")
+    db = codec.device_batch(bad, counts, 1e-6, 0)
+    codec.compress_device(bad, db)
+    with pytest.raises(ValueError):
+        codec.compress_device_finish(bad, db)

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--cache", default=None)
     ap.add_argument("--rhs4", action="store_true", help="also time the 4-right-hand-side arena")
+    ap.add_argument("--yref", default=None, help="compare y with this saved product (saved if missing)")
     a = ap.parse_args()
     c = problems.config(a.config)
     if a.n:
@@ -76,11 +77,19 @@ def main():
     torch.cuda.synchronize()
     wall = e0.elapsed_time(e1) / a.iters
     r = H.memory()
+    chk = ""
+    if a.yref:
+        yv = y.cpu().numpy()
+        if os.path.exists(a.yref):
+            y0 = np.load(a.yref)
+            chk = f" relerr_vs_ref={np.linalg.norm(yv - y0) / np.linalg.norm(y0):.2e}"
+        else:
+            np.save(a.yref, yv)
     print({k: round(v, 2) for k, v in T.items()})
     print(f"n={n} arena={r.device_arena_bytes/1e6:.1f}MB algo={r.algorithmic_bytes/1e6:.1f}MB "
           f"stagesA={r.stages_a} stagesB={r.stages_b} phaseA={ms_a/calls:.4f}ms phaseB={ms_b/calls:.4f}ms "
           f"total={(ms_a+ms_b)/calls:.4f}ms -> {r.algorithmic_bytes/((ms_a+ms_b)/calls)/1e6:.1f} GB/s "
-          f"wall={wall:.4f}ms -> {r.algorithmic_bytes/wall/1e6:.1f} GB/s")
+          f"wall={wall:.4f}ms -> {r.algorithmic_bytes/wall/1e6:.1f} GB/s" + chk, flush=True)
     if a.rhs4:  # 4 right-hand sides decoded once vs 4 single products
         X4 = torch.as_tensor(np.random.default_rng(1).uniform(-1, 1, (n, 4))).cuda().contiguous()
         Y4 = torch.zeros(n, 4, dtype=torch.float64, device="cuda")
