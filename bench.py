@@ -195,11 +195,53 @@ def cpu_reference_value(flat, threads, budget_s=15.0, max_reps=3):
         impl.hmat_matvec(sample, 1.0, x, 0.0, np.zeros(fh.n_rows), threads=threads)
         times.append(time.perf_counter() - t)
     best = min(times)
+    # one thread on a 1/threads slice of the same sample (T = 1 and T = all)
+    rows1 = max(64, rows // max(1, threads) // 64 * 64)
+    s1 = restrict(fh, (0, rows1))
+    sb1 = step_bytes(fh, (0, rows1))
+    t = time.perf_counter()
+    impl.hmat_matvec(s1, 1.0, x, 0.0, np.zeros(fh.n_rows), threads=1)
+    t1 = time.perf_counter() - t
     # parity of the benched product: the same CPU path over the whole matrix (untimed)
     y_ref = impl.hmat_matvec(fh, 1.0, x, 0.0, np.zeros(fh.n_rows), threads=threads)
     return {"value": sb / best / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
             "sample": f"rows [0,{rows}) of {fh.n_rows} ({sb / 1e6:.1f} MB compressed), best of {max_reps}, "
-                      f"{threads} threads"}, sb, best, y_ref
+                      f"{threads} threads",
+            "one_thread": {"value": round(sb1 / t1 / 1e9, 3), "sample": f"rows [0,{rows1}), 1 thread"}}, sb, best, y_ref
+
+
+def cpu_codec_baseline(threads, nblocks=1024):
+    """the reference codec (oracle/_ref, codec.cpp:142-171) on config-2 blocks on the
+    host: compress and decompress GB/s (same algorithmic bytes as the GPU codec
+    numbers) at 1 thread and at all threads, on a bounded sample of the 4096 blocks"""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle, RefOracle
+    impl, kind = (RefOracle(), "reference") if RefOracle.available() else (Oracle(), "port")
+    rng = np.random.default_rng(2)
+    bs = 4096
+    vals = np.sign(rng.standard_normal(nblocks * bs)) * 10 ** rng.uniform(-6, 0, nblocks * bs)
+    counts = np.full(nblocks, bs, np.int64)
+    res = {"kind": kind, "sample": f"{nblocks} of the 4096 config-2 blocks, eps 1e-6, AFL"}
+    for t in sorted({1, threads}):
+        n = nblocks if t > 1 else max(64, nblocks // 8)
+        v, c = vals[: n * bs], counts[:n]
+        t0 = time.perf_counter()
+        if kind == "reference":
+            e, m, sc, poff, blob, plen = impl.compress_batch(v, c, 1e-6, 0, threads=t)
+        else:
+            e, m, sc, poff, blob = impl.compress_batch(v, c, 1e-6, 0, threads=t)
+            plen = (c * (1 + e + m) + 7) // 8
+        tc = time.perf_counter() - t0
+        algo = 8 * int(c.sum()) + int((plen + 20).sum())
+        t0 = time.perf_counter()
+        if kind == "reference":
+            impl.decompress_batch(blob, poff, plen, c, 0, e, m, sc, threads=t)
+        else:
+            impl.decompress_batch(blob, poff, c, 0, e, m, sc, threads=t)
+        td = time.perf_counter() - t0
+        res[f"threads_{t}"] = {"compress_gbs": round(algo / tc / 1e9, 3), "decompress_gbs": round(algo / td / 1e9, 3)}
+    res["cores"] = threads
+    return res
 
 
 def restrict(flat, rr):
@@ -212,12 +254,16 @@ def restrict(flat, rr):
                    buf0=flat.buf0[sel], sig0=flat.sig0[sel])
 
 
-def codec_microbench(reps=20):
+def codec_microbench(reps=10):
     """BASELINE config 2: 4096 blocks of 64x64, sign * 10^U[-6,0], AFL at 1e-4/1e-6/1e-8.
-    Inputs resident in HBM; `reps` back-to-back batched API calls between CUDA
-    events (compress = the fused kernel + the descriptor read-back the API
-    returns to the host; decompress = the unpack kernel); algorithmic bytes
-    per SURVEY 8(d): 8N + ceil(N w / 8) + 20 per buffer."""
+    Inputs resident in HBM; L2 flushed before every timed call (a 256 MB write
+    outside the events), each call bracketed by CUDA events on the stream.
+      compress_gbs: hcmx_gpu_codec_compress_device (descriptors and flags stay on
+        the device, no read-back), the batched API;
+      compress_host_api_gbs: hcmx_gpu_codec_compress (returns host descriptors:
+        includes the read-back and its synchronisation);
+      decompress_gbs: hcmx_gpu_codec_unpack.
+    Algorithmic bytes per SURVEY 8(d): 8N + ceil(N w / 8) + 20 per buffer."""
     import torch
     from paper_2308_10960_b200 import codec
     nb, bs = 4096, 4096
@@ -226,50 +272,43 @@ def codec_microbench(reps=20):
     d = torch.as_tensor(vals).cuda()
     counts = np.full(nb, bs, np.uint64)
     d_voff = torch.as_tensor((np.arange(nb, dtype=np.int64) * bs)).cuda()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     out = {}
+
+    def timed(fn):
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3)
+        return float(np.median(ts))
+
     for eps in (1e-4, 1e-6, 1e-8):
         bb = codec.compress_batch(d, counts, eps, codec.Scheme.afl, d_voff=d_voff)
         dec = codec.decompress_batch(bb)
+        db = codec.device_batch(d, counts, eps, codec.Scheme.afl)
+        codec.compress_device(d, db)
+        _, nfix = codec.compress_device_finish(d, db)   # bit-exact completion (no threshold cases here)
         torch.cuda.synchronize()
         pay = int(((counts * bb.desc["bit_width"].astype(np.uint64) + 7) // 8).sum()) + 20 * nb
         algo = 8 * nb * bs + pay
-        tc, td = [], []
-        from paper_2308_10960_b200._lib import lib as _L
-        import ctypes as _C
-        for _ in range(3):
-            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            t0.record()
-            for _ in range(reps):
-                codec.compress_batch(d, counts, eps, codec.Scheme.afl, payload=bb.payload, d_voff=d_voff)
-            t1.record()
-            torch.cuda.synchronize()
-            tc.append(t0.elapsed_time(t1) / 1e3 / reps)
-            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            t0.record()
-            for _ in range(reps):
-                codec.decompress_batch(bb, out=dec)
-            t1.record()
-            torch.cuda.synchronize()
-            td.append(t0.elapsed_time(t1) / 1e3 / reps)
-        # kernel-only device time: events around the launches inside the library
-        # (a separate pass, so the per-call events do not perturb the API numbers)
-        _L().hcmx_gpu_codec_timing(1, None, None, None, None)
-        for _ in range(reps):
-            codec.compress_batch(d, counts, eps, codec.Scheme.afl, payload=bb.payload, d_voff=d_voff)
-            codec.decompress_batch(bb, out=dec)
-        torch.cuda.synchronize()
-        mc, md = _C.c_double(), _C.c_double()
-        nc, nd = _C.c_uint64(), _C.c_uint64()
-        _L().hcmx_gpu_codec_timing(0, _C.byref(mc), _C.byref(nc), _C.byref(md), _C.byref(nd))
-        kc = algo / (mc.value / 1e3 / max(nc.value, 1)) / 1e9 if nc.value else None
-        kd = algo / (md.value / 1e3 / max(nd.value, 1)) / 1e9 if nd.value else None
+        tcd = timed(lambda: codec.compress_device(d, db))
+        tch = timed(lambda: codec.compress_batch(d, counts, eps, codec.Scheme.afl, payload=bb.payload,
+                                                 d_voff=d_voff))
+        td = timed(lambda: codec.decompress_batch(bb, out=dec))
+        pk = _peaks()[0]
         out[f"afl_{eps:g}"] = {"w_bits": int(bb.desc["bit_width"][0]),
-                               "compress_kernel_gbs": round(kc, 1) if kc else None,
-                               "decompress_kernel_gbs": round(kd, 1) if kd else None,
-                               "compress_gbs": round(algo / min(tc) / 1e9, 1),
-                               "decompress_gbs": round(algo / min(td) / 1e9, 1),
-                               "compress_frac": round(algo / min(tc) / 1e9 / _peaks()[0], 3),
-                               "decompress_frac": round(algo / min(td) / 1e9 / _peaks()[0], 3)}
+                               "compress_gbs": round(algo / tcd / 1e9, 1),
+                               "compress_host_api_gbs": round(algo / tch / 1e9, 1),
+                               "decompress_gbs": round(algo / td / 1e9, 1),
+                               "compress_frac": round(algo / tcd / 1e9 / pk, 3),
+                               "decompress_frac": round(algo / td / 1e9 / pk, 3),
+                               "fixups": int(nfix)}
+    out["note"] = "L2 flushed before every call; median of per-call CUDA-event times"
     return out
 
 
@@ -418,6 +457,8 @@ def run_ours(args, rank, world, local):
             parity = {"rel_err": float(np.linalg.norm(y_dev - y_ref) / np.linalg.norm(y_ref)),
                       "tol": 1e-12, "vs": f"{cpu['kind']} CPU product over the whole matrix, same x"}
         codec_res = codec_microbench() if (world == 1 and not args.no_codec) else None
+        if codec_res is not None and not args.no_cpu_baseline:
+            codec_res["cpu_baseline"] = cpu_codec_baseline(os.cpu_count() or 1)
         line = {
             "metric": "compressed H-matvec GB/s (compressed bytes)",
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,

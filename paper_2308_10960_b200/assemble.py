@@ -24,6 +24,15 @@ from .problems import PointKernel
 from .tree import BlockLeaves
 
 EXACT_SVD_MAX = 32
+_PROF = {}  # HCMX_VERBOSE: seconds per setup step (synchronised timers)
+
+
+def _tick(name, t0):
+    if os.environ.get("HCMX_VERBOSE"):
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+        _PROF[name] = _PROF.get(name, 0.0) + time.time() - t0
+    return time.time()
 
 
 @dataclass
@@ -122,14 +131,19 @@ def _svd_batch(A: torch.Tensor, eps: float, p0: int = 32):
     todo = torch.arange(B, device=A.device)
     U = S = Vh = None
     while True:
+        t0 = time.time()
         Ab = A[todo] if todo.numel() < B else A
         nb = Ab.shape[0]
         omega = torch.randn(nb, n, p, dtype=A.dtype, device=A.device, generator=g)
-        Q = _orth(Ab @ omega)                              # range of A, m x p
+        Y = Ab @ omega
+        t0 = _tick(f"sketch p{p}", t0)
+        Q = _orth(Y)                                       # range of A, m x p
         Z = Ab.mH @ Q                                      # (Q^H A)^H, n x p
         Q2 = _orth(Z)
         R2 = Q2.mH @ Z                                     # Z = Q2 R2
+        t0 = _tick(f"orth p{p}", t0)
         Ur, Sb, Vrh = _core_svd(R2.mH)                     # Q^H A = Ur Sb (Q2 Vrh^H)^H
+        t0 = _tick(f"core svd p{p}", t0)
         Ub, Vb = Q @ Ur, Vrh @ Q2.mH
         if U is None:  # width p for now, zero-padded when a later round widens it
             U = torch.zeros(B, m, p, dtype=A.dtype, device=A.device)
@@ -146,6 +160,8 @@ def _svd_batch(A: torch.Tensor, eps: float, p0: int = 32):
         S[idx, :p] = Sb[done]
         Vh[idx, :p, :] = Vb[done]
         todo = todo[~done]
+        _PROF[f"blocks p{p}"] = _PROF.get(f"blocks p{p}", 0) + nb
+        t0 = _tick(f"collect p{p}", t0)
         if todo.numel() == 0:
             break
         p = min(k, 2 * p)
@@ -157,7 +173,7 @@ def assemble(points_internal: np.ndarray, leaves: BlockLeaves, kernel: PointKern
              device: str | None = None, batch_bytes: int | None = None) -> Assembled:
     dev = torch.device(device or ("cuda" if torch.cuda.is_available() else "cpu"))
     if batch_bytes is None:
-        batch_bytes = (8 << 30) if dev.type == "cuda" else (1 << 30)
+        batch_bytes = (16 << 30) if dev.type == "cuda" else (1 << 30)
     P = torch.as_tensor(np.ascontiguousarray(points_internal, dtype=np.float64), device=dev)
     L = len(leaves)
     kind = np.where(leaves.admissible, 1, 0).astype(np.int64)
@@ -190,7 +206,9 @@ def assemble(points_internal: np.ndarray, leaves: BlockLeaves, kernel: PointKern
         per = max(1, batch_bytes // (8 * m * n * 3))
         for c0 in range(0, len(ids), per):
             chunk = np.array(ids[c0: c0 + per])
+            t1 = time.time()
             A = _blocks(P, leaves, chunk, kernel)
+            _tick("kernel blocks", t1)
             U, S, Vh = _svd_batch(A, eps)
             ks_t = rank_from_singular_values(S, eps)
             keep = torch.arange(S.shape[1], device=S.device)[None, :] < ks_t[:, None]   # (B, p)
@@ -209,7 +227,9 @@ def assemble(points_internal: np.ndarray, leaves: BlockLeaves, kernel: PointKern
             wo += Wc.numel(); xo += Xc.numel(); so += Sc.size
             del A, U, S, Vh
         if verbose:
-            sys.stderr.write(f"[assemble] {len(ids)} blocks {m}x{n}: {time.time() - t0:.2f}s\n")
+            sys.stderr.write(f"[assemble] {len(ids)} blocks {m}x{n}: {time.time() - t0:.2f}s "
+                             f"{ {k: round(v, 2) for k, v in _PROF.items()} }\n")
+            _PROF.clear()
     W = torch.cat(wl) if wl else torch.zeros(0, dtype=torch.float64, device=dev)
     X = torch.cat(xl) if xl else torch.zeros(0, dtype=torch.float64, device=dev)
     sigma = np.concatenate(sl) if sl else np.zeros(0)
@@ -296,7 +316,9 @@ def assemble_complex(points_internal: np.ndarray, leaves: BlockLeaves, kernel: P
         per = max(1, batch_bytes // (16 * m * n * 3))
         for c0 in range(0, len(ids), per):
             chunk = np.array(ids[c0: c0 + per])
+            t1 = time.time()
             A = _blocks(P, leaves, chunk, kernel)
+            _tick("kernel blocks", t1)
             U, S, Vh = _svd_batch(A, eps)
             ks_t = rank_from_singular_values(S, eps)
             keep = torch.arange(S.shape[1], device=S.device)[None, :] < ks_t[:, None]

@@ -85,7 +85,7 @@ constexpr unsigned kWaitHintNs = HCMX_WAIT_HINT;  // mbarrier try_wait suspend h
 // at the 16-byte aligned end of the stage, so a stage may trade packed data
 // for coefficients (phase A's x slices are ~1/3 of its packed bytes).  The
 // builder bakes slot-relative coefficient offsets into the items.
-constexpr int kStageMax = kMaxItems * kItemBytes + 48 + kStageBytes;
+constexpr int kStageMax = kMaxItems * kItemBytes + 64 + kStageBytes;
 constexpr int kSlotData = kStageMax + kSlack + kCoefBytes;  // stage + coefficients
 constexpr int kOffHdr = kSlotData;    // slot header written by the producer: stripe id, flags,
                                       // item claim counter (phase A), items
@@ -126,6 +126,7 @@ constexpr size_t kRingBytes = static_cast<size_t>(kNStage) * kSlotBytes;
 constexpr size_t kRedBytes = ((kNWB > HCMX_NWB_MULTI ? kNWB : HCMX_NWB_MULTI) / 2) * kR * sizeof(double);  // phase-B cross-warp reduction
 constexpr size_t kSmemBytes = kRingBytes + kRedBytes + 2 * kNStage * sizeof(uint64_t);  // + full, empty barriers
 constexpr int kCopies = 2 * kMaxItems;  // coefficient copies per stage (two per producer lane)
+constexpr int kRangeBytes = 64;         // phase-B stage head: 16 warp item ranges (begin | end << 16)
 // copy entry (u64): [0,32) source element index, [32,48) dst / 16 in the slot,
 // [48,60) bytes / 16, [60,62) source table (0 x, 1 wcol records), bit 63 valid
 static_assert(kOffHdr % 16 == 0 && kSlotBytes % 16 == 0, "slot alignment");
@@ -654,8 +655,9 @@ __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t*
                 i = __shfl_sync(0xffffffffu, nl, 0);
             }
         } else if (!(flags & kHdrEmpty)) {
-            const uint16_t* wb = reinterpret_cast<const uint16_t*>(base + hdr[3] * kItemBytes);
-            for (unsigned i = wb[warp], e = wb[warp + 1]; i < e; ++i) body(base, i);
+            // phase-B stage: [per-warp item ranges, 16 x u32 (begin | end << 16)][items][data]
+            const uint32_t r = reinterpret_cast<const uint32_t*>(base)[warp];
+            for (unsigned i = r & 0xffffu, e = r >> 16; i < e; ++i) body(base, i);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
@@ -1005,9 +1007,81 @@ __device__ __forceinline__ void b_item_full(const BItem& it, const uint32_t* seg
     }
 }
 
+// R = 1 bodies (the single-vector product).  Dense: one layout per item; the
+// column loop keeps two accumulator sets (even / odd columns) so consecutive
+// FMAs on a row do not wait on each other, and one alpha * scale multiply per
+// item.  Lowrank W columns: each column's record {c, mask, mul} + w.
+template <int GLO, int GHI>
+__device__ __forceinline__ void b1_dense(const BItem& it, const uint32_t* seg, const double* xc, unsigned lane,
+                                         double dmul, uint64_t bias, double (&acc)[kG]) {
+    constexpr int NG = GHI - GLO;
+    const unsigned w = it.dpacked & 0xffu, e = (it.dpacked >> 16) & 0xffu;
+    const uint32_t mask = fast_mask(w), mul = c_pow2e.v[e & 31u];
+    const unsigned top = (lane + 1) * w;                 // one past the sign bit of field `lane`
+    const uint32_t* sp = seg + ((top - 1) >> 5) - 1;
+    const unsigned s = 0u - top;
+    const unsigned segw = NG * w;
+    double t0[NG], t1[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) t0[g] = t1[g] = 0.0;
+    const unsigned n = it.nseg;
+    unsigned c = 0;
+    for (; c + 2 <= n; c += 2) {
+        const double x0 = xc[c], x1 = xc[c + 1];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            t0[g] = fma(dec_fast(sp + g * w, s, mask, mul, bias), x0, t0[g]);
+            t1[g] = fma(dec_fast(sp + segw + g * w, s, mask, mul, bias), x1, t1[g]);
+        }
+        sp += 2 * segw;
+    }
+    if (c < n) {
+        const double x0 = xc[c];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) t0[g] = fma(dec_fast(sp + g * w, s, mask, mul, bias), x0, t0[g]);
+    }
+#pragma unroll
+    for (int g = 0; g < NG; ++g) acc[GLO + g] = fma(dmul, t0[g] + t1[g], acc[GLO + g]);
+}
+
+template <int GLO, int GHI>
+__device__ __forceinline__ void b1_lr(const BItem& it, const uint32_t* seg, const uint8_t* rec, unsigned lane,
+                                      uint64_t bias, double (&acc)[kG]) {
+    constexpr int NG = GHI - GLO;
+    const unsigned lp1 = lane + 1;
+    const unsigned n = it.nseg;
+#pragma unroll 2
+    for (unsigned c = 0; c < n; ++c) {
+        const uint4 q0 = reinterpret_cast<const uint4*>(rec)[0];  // {c lo, c hi, mask, mul}
+        const unsigned w = reinterpret_cast<const uint32_t*>(rec)[7];
+        rec += 32;
+        const double cc = __hiloint2double(static_cast<int>(q0.y), static_cast<int>(q0.x));
+        const unsigned top = lp1 * w;
+        const uint32_t* sp = seg + ((top - 1) >> 5) - 1;
+        const unsigned s = 0u - top;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) acc[GLO + g] = fma(dec_fast(sp + g * w, s, q0.z, q0.w, bias), cc, acc[GLO + g]);
+        seg += NG * w;
+    }
+}
+
 template <int R>
 __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const uint8_t* slot, unsigned lane,
                                        double (&acc)[kG * R]) {
+    if constexpr (R == 1) {
+        const double* cf = reinterpret_cast<const double*>(slot + it.coef_off);
+        const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
+        switch (it.fcase | (it.kind << 2)) {  // one jump table: body x leaf kind
+            case 1: b1_dense<0, 4>(it, seg, cf, lane, p.alpha * it.scale, p.bias, acc); return;
+            case 2: b1_dense<0, 2>(it, seg, cf, lane, p.alpha * it.scale, p.bias, acc); return;
+            case 3: b1_dense<2, 4>(it, seg, cf, lane, p.alpha * it.scale, p.bias, acc); return;
+            case 5: b1_lr<0, 4>(it, seg, reinterpret_cast<const uint8_t*>(cf), lane, p.bias, acc); return;
+            case 6: b1_lr<0, 2>(it, seg, reinterpret_cast<const uint8_t*>(cf), lane, p.bias, acc); return;
+            case 7: b1_lr<2, 4>(it, seg, reinterpret_cast<const uint8_t*>(cf), lane, p.bias, acc); return;
+            default: b_item_generic<R>(it, seg, cf, lane, p.alpha * it.scale, acc); return;
+        }
+    }
+    else {
     const double* cf = reinterpret_cast<const double*>(slot + it.coef_off);
     const double dmul = p.alpha * it.scale;  // dense: alpha * buffer scale folded into x
     const uint32_t* seg = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
@@ -1022,6 +1096,7 @@ __device__ __forceinline__ void b_item(const Params& p, const BItem& it, const u
         default:
             b_item_generic<R>(it, seg, cf, lane, dmul, acc);  // also uncompressed words (modes 3-5)
             break;
+    }
     }
 }
 
@@ -1078,7 +1153,7 @@ __global__ void __launch_bounds__((nwb<R>() + 1) * 32, 2) k_phase_b(Params p) {
     consume<NW, false>(
         smem, full, empty, warp, lane, dbg(p),
         [&](const uint8_t* base, unsigned i) {
-            b_item<R>(p, reinterpret_cast<const BItem*>(base)[i], base, lane, acc);
+            b_item<R>(p, reinterpret_cast<const BItem*>(base + kRangeBytes)[i], base, lane, acc);
         },
         [&](uint32_t sid) {  // block done: fixed-order pairwise sum of the warps, then y
             const uint4 sr = p.stripe_b[sid];
@@ -1365,7 +1440,6 @@ struct Builder {
 
     std::vector<uint32_t> arena;  // words
     std::vector<Stage> stages;
-    std::vector<uint16_t> wb;     // phase B: 24 entries per stage (NW + 1 used)
     std::vector<BItem> bitems;
     std::vector<Seg> segs;
     std::vector<uint64_t> copies;  // kCopies per stage
@@ -1498,7 +1572,7 @@ struct Builder {
             }
             slices.swap(merged);
             // the coefficients follow the stage in the slot (slot-relative offsets)
-            size_t data_words = (built.size() * (kItemBytes / 4) + (NW > 0 ? 12 : 0) + 3) & ~size_t(3);
+            size_t data_words = (built.size() * (kItemBytes / 4) + (NW > 0 ? kRangeBytes / 4 : 0) + 3) & ~size_t(3);
             for (const Built& b : built) data_words += b.words;
             data_bytes = static_cast<uint32_t>(((data_words + 3) & ~size_t(3)) * 4);
             coef = data_bytes;
@@ -1527,12 +1601,15 @@ struct Builder {
         if (NW == 0)  // claimed largest first: the last items to finish are the small ones
             std::stable_sort(built.begin(), built.end(),
                              [](const Built& x, const Built& y) { return x.words > y.words; });
-        uint32_t wb_index = 0;
+        static_assert(NW <= kRangeBytes / 4, "phase-B warp ranges");
+        uint32_t ranges[kRangeBytes / 4] = {};
         if (NW > 0) {
-            wb_index = static_cast<uint32_t>(wb.size() / 24);
-            wb.push_back(0);
-            for (uint32_t e : piece_end) wb.push_back(static_cast<uint16_t>(e));
-            while (wb.size() % 24) wb.push_back(static_cast<uint16_t>(built.size()));  // 48 B per stage
+            uint32_t b0 = 0;
+            for (size_t q = 0; q < kRangeBytes / 4; ++q) {
+                const uint32_t e = q < piece_end.size() ? piece_end[q] : static_cast<uint32_t>(built.size());
+                ranges[q] = b0 | (e << 16);
+                b0 = e;
+            }
         }
         const size_t c0 = copies.size();
         copies.resize(c0 + kCopies, 0);
@@ -1543,7 +1620,8 @@ struct Builder {
         Stage st{};
         st.item0 = static_cast<uint32_t>(items.size());
         // [items][warp ranges (B)][data]: item word offsets count from the stage start
-        const size_t meta_words = built.size() * (kItemBytes / 4) + (NW > 0 ? 12 : 0);
+        const size_t head_words = NW > 0 ? kRangeBytes / 4 : 0;  // [warp ranges][items]
+        const size_t meta_words = built.size() * (kItemBytes / 4) + head_words;
         arena.resize(start + ((meta_words + 3) & ~size_t(3)), 0u);
         for (Built& b : built) {
             b.it.word_off = static_cast<uint32_t>(arena.size() - start);
@@ -1554,8 +1632,8 @@ struct Builder {
             items.push_back(b.it);
         }
         for (size_t i = 0; i < built.size(); ++i)
-            std::memcpy(arena.data() + start + i * (kItemBytes / 4), &built[i].it, kItemBytes);
-        if (NW > 0) std::memcpy(arena.data() + start + built.size() * (kItemBytes / 4), &wb[wb_index * 24], 48);
+            std::memcpy(arena.data() + start + head_words + i * (kItemBytes / 4), &built[i].it, kItemBytes);
+        if (NW > 0) std::memcpy(arena.data() + start, ranges, kRangeBytes);
         while (arena.size() % 4) arena.push_back(0u);
         st.byte_off = start * 4;
         st.bytes = static_cast<uint32_t>((arena.size() - start) * 4);
@@ -2199,7 +2277,6 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     };
     up(h->arena, B.arena.data(), B.arena.size() * 4);
     up(h->stages, B.stages.data(), B.stages.size() * sizeof(Stage));
-    B.wb.resize(std::max<size_t>(B.wb.size(), 24));
     up(h->copies, B.copies.data(), B.copies.size() * sizeof(uint64_t));
     h->work.alloc(16);
     check_cuda(cudaMemsetAsync(h->work.p, 0, 16, s), "memset");
