@@ -234,12 +234,17 @@ int hcmx_gpu_hmat_memory(const hcmx_hmat* h, hcmx_memory_report* out);
 int hcmx_gpu_hmat_matvec(hcmx_hmat* h, double alpha, const double* h_x, double beta, double* h_y,
                          int transpose);
 /* several right-hand sides: Y := alpha op(M) X +
- * beta Y for nrhs host columns (column-major, leading dimensions ldx / ldy); one
- * copy of X in and of Y out, one device product per column */
+ * beta Y for nrhs host columns (column-major, leading dimensions ldx / ldy).  A
+ * handle created with nrhs_block = 4 runs blocks of 4 columns through its 4-RHS
+ * arena (every field decoded once per block, a short last block padded with
+ * zero columns); otherwise one device product per column. */
 int hcmx_gpu_hmat_matmat(hcmx_hmat* h, double alpha, const double* h_x, uint64_t ldx, uint64_t nrhs,
                          double beta, double* h_y, uint64_t ldy, int transpose);
 /* device-pointer form on a stream; d_x has n_cols entries, d_y n_rows entries
- * (for a partitioned handle only d_y[row_begin,row_end) is written) */
+ * (for a partitioned handle only d_y[row_begin,row_end) is written).  Products
+ * on one handle share its device scratch: a product issued on another stream
+ * than the handle's previous one waits for that product first (an event), so
+ * one handle may be used from several streams and host threads. */
 int hcmx_gpu_hmat_matvec_device(hcmx_hmat* h, double alpha, const double* d_x, double beta,
                                 double* d_y, void* stream);
 

@@ -115,12 +115,13 @@ def _svd_batch(A: torch.Tensor, eps: float, p0: int = 32):
     """truncation-grade SVD of a batch of blocks: (U, S, Vh) holding at least every
     singular triple above 1e-3 * eps * sigma_0 (the rank rule then keeps sigma_k >
     eps * sigma_0, lowrank.cpp:14-21).  Blocks up to EXACT_SVD_MAX columns: full
-    SVD.  Larger: a randomized range finder Q = orth(A Omega) with p columns,
-    then the exact SVD of Q^H A through Z = A^H Q = Q2 R2 (Q^H A = R2^H Q2^H, so
-    R2^H is the p x p core).  p grows per block (32, 64, 128, ...) until the
-    p-th singular value of Q^H A is below 1e-3 * eps * sigma_0, so the sketch
-    spans the whole retained spectrum; blocks that miss are redone with the next
-    p, the others keep their result (zero-padded to the batch's width)."""
+    SVD.  Larger: a randomized range finder Q = orth(A Omega) with p columns and
+    one power iteration, then the exact SVD of Q^H A through Z = A^H Q = Q2 R2
+    (Q^H A = R2^H Q2^H, so R2^H is the p x p core).  p grows per block (32, 48,
+    64, 128, ...) until the p-th singular value of Q^H A is below
+    0.03 * eps * sigma_0, so the sketch spans the whole retained spectrum;
+    blocks that miss are redone with the next p, the others keep their result
+    (zero-padded to the batch's width)."""
     B, m, n = A.shape
     if min(m, n) <= EXACT_SVD_MAX:
         return _core_svd(A) if m == n else _cpu_svd(A)
@@ -138,6 +139,7 @@ def _svd_batch(A: torch.Tensor, eps: float, p0: int = 32):
         Y = Ab @ omega
         t0 = _tick(f"sketch p{p}", t0)
         Q = _orth(Y)                                       # range of A, m x p
+        Q = _orth(Ab @ _orth(Ab.mH @ Q))                   # one power iteration (A A^H) Q
         Z = Ab.mH @ Q                                      # (Q^H A)^H, n x p
         Q2 = _orth(Z)
         R2 = Q2.mH @ Z                                     # Z = Q2 R2
@@ -154,7 +156,10 @@ def _svd_batch(A: torch.Tensor, eps: float, p0: int = 32):
             U = torch.nn.functional.pad(U, (0, pad))
             S = torch.nn.functional.pad(S, (0, pad))
             Vh = torch.nn.functional.pad(Vh, (0, 0, 0, pad))
-        done = (Sb[:, -1] <= 1e-3 * eps * Sb[:, 0]) | (p >= k)
+        # with one power iteration the error of a captured sigma_i is ~
+        # sigma_{p+1}^4 / sigma_i^3: at sigma_p <= 0.03 eps sigma_0 the values near
+        # the cut eps sigma_0 are exact to ~1e-6 relative, as a full SVD decides them
+        done = (Sb[:, -1] <= 0.03 * eps * Sb[:, 0]) | (p >= k)
         idx = todo[done]
         U[idx, :, :p] = Ub[done]
         S[idx, :p] = Sb[done]
@@ -164,7 +169,7 @@ def _svd_batch(A: torch.Tensor, eps: float, p0: int = 32):
         t0 = _tick(f"collect p{p}", t0)
         if todo.numel() == 0:
             break
-        p = min(k, 2 * p)
+        p = min(k, p + 16 if p < 64 else 2 * p)                # 32, 48, 64, 128, ...
     w = max(1, int((S > 0).sum(dim=1).max().item())) if B else 1
     return U[:, :, :w], S[:, :w], Vh[:, :w, :]
 
@@ -207,7 +212,7 @@ def assemble(points_internal: np.ndarray, leaves: BlockLeaves, kernel: PointKern
         for c0 in range(0, len(ids), per):
             chunk = np.array(ids[c0: c0 + per])
             t1 = time.time()
-            A = _blocks(P, leaves, chunk, kernel)
+            A = _blocks(P, leaves, chunk, kernel, separated=True)  # admissible: separated clusters
             _tick("kernel blocks", t1)
             U, S, Vh = _svd_batch(A, eps)
             ks_t = rank_from_singular_values(S, eps)
@@ -237,14 +242,14 @@ def assemble(points_internal: np.ndarray, leaves: BlockLeaves, kernel: PointKern
                      x_off, sigma, sig_off)
 
 
-def _blocks(P, leaves, ids, kernel):
+def _blocks(P, leaves, ids, kernel, separated=False):
     r0 = torch.as_tensor(leaves.row0[ids], device=P.device)
     c0 = torch.as_tensor(leaves.col0[ids], device=P.device)
     m = int(leaves.row1[ids[0]] - leaves.row0[ids[0]])
     n = int(leaves.col1[ids[0]] - leaves.col0[ids[0]])
     ri = r0[:, None] + torch.arange(m, device=P.device)[None, :]
     ci = c0[:, None] + torch.arange(n, device=P.device)[None, :]
-    return kernel.block(P[ri], P[ci])
+    return kernel.block(P[ri], P[ci], separated)
 
 
 def _fill_blocks(P, leaves, ids, kernel, out, off, batch_bytes):
@@ -317,7 +322,7 @@ def assemble_complex(points_internal: np.ndarray, leaves: BlockLeaves, kernel: P
         for c0 in range(0, len(ids), per):
             chunk = np.array(ids[c0: c0 + per])
             t1 = time.time()
-            A = _blocks(P, leaves, chunk, kernel)
+            A = _blocks(P, leaves, chunk, kernel, separated=True)  # admissible: separated clusters
             _tick("kernel blocks", t1)
             U, S, Vh = _svd_batch(A, eps)
             ks_t = rank_from_singular_values(S, eps)

@@ -46,6 +46,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -1053,7 +1054,7 @@ __device__ __forceinline__ void b1_lr(const BItem& it, const uint32_t* seg, cons
 #pragma unroll 2
     for (unsigned c = 0; c < n; ++c) {
         const uint4 q0 = reinterpret_cast<const uint4*>(rec)[0];  // {c lo, c hi, mask, mul}
-        const unsigned w = reinterpret_cast<const uint32_t*>(rec)[7];
+        const unsigned w = reinterpret_cast<const uint32_t*>(rec)[5];  // WCol::w
         rec += 32;
         const double cc = __hiloint2double(static_cast<int>(q0.y), static_cast<int>(q0.x));
         const unsigned top = lp1 * w;
@@ -1315,6 +1316,12 @@ struct hcmx_hmat {
     uint64_t calls = 0;
     hcmx_hmat* trans = nullptr;  // M^T (hmatrix.hpp:128 transpose), built on request
     hcmx_hmat* multi = nullptr;  // the same matrix laid out for kMultiR right-hand sides (matmat)
+    // products on one handle share its device scratch (stripe counters, x copy,
+    // phase-A results): a product issued on another stream than the previous
+    // one first waits for it (the reference's matvec is re-entrant, const M&)
+    std::mutex mu, io_mu;  // io_mu: the host-pointer calls' staging buffers (xbuf / ybuf)
+    cudaEvent_t last = nullptr;
+    cudaStream_t last_stream = nullptr;
 };
 
 namespace {
@@ -1465,14 +1472,67 @@ struct Builder {
     unsigned width(uint64_t b) const { return d.desc[b].bit_width; }
     uint64_t words_of(uint64_t b, uint64_t nf) const { return (nf * width(b) + 31) / 32; }
 
+    // The layout pass only sizes the arena and records where every field run
+    // goes; the bits are placed afterwards by place_all() on all host cores
+    // (item / segment destinations are disjoint word ranges).
+    struct CopyJob {   // phase B: fields [f0, f0+nf) of buffer buf, word aligned at arena word `at`
+        uint64_t at, buf, f0, nf;
+    };
+    struct LaneJob {   // phase A: one lane of an item (row-interleaved placement)
+        uint64_t data0, buf, f0;
+        uint32_t nf, P, rowbits, gwords;
+    };
+    std::vector<CopyJob> copy_jobs;
+    std::vector<LaneJob> lane_jobs;
+
     // append the words of fields [f0, f0+nf) of buffer b (word aligned)
     void put_fields(const Seg& s) {
         const unsigned w = width(s.buf);
         const uint64_t nw = (s.nf * w + 31) / 32;
         const uint64_t at = arena.size();
         arena.resize(at + nw);
-        copy_bits(blob + d.poff[s.buf], static_cast<uint64_t>(d.plen[s.buf]), s.f0 * w, s.nf * w, arena.data() + at);
+        copy_jobs.push_back({at, s.buf, s.f0, s.nf});
         if (keep_map) h->segs[s.buf].push_back({at, static_cast<uint32_t>(s.f0), static_cast<uint32_t>(s.nf)});
+    }
+
+    void place_all() {
+        unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+        const size_t nc = copy_jobs.size(), nl = lane_jobs.size();
+        auto work = [&](unsigned t) {
+            for (size_t i = t; i < nc; i += nt) {
+                const CopyJob& j = copy_jobs[i];
+                const unsigned w = width(j.buf);
+                copy_bits(blob + d.poff[j.buf], static_cast<uint64_t>(d.plen[j.buf]), j.f0 * w, j.nf * w,
+                          arena.data() + j.at);
+            }
+            // lanes of one item share words: an item's lanes are consecutive in
+            // lane_jobs and go to the same thread (chunks cut at item starts)
+            const size_t per = (nl + nt - 1) / nt;
+            size_t a = std::min(nl, per * t), b = std::min(nl, per * (t + 1));
+            auto item_start = [&](size_t i) {
+                while (i > 0 && i < nl && lane_jobs[i].data0 == lane_jobs[i - 1].data0) ++i;
+                return i;
+            };
+            a = item_start(a);
+            b = item_start(b);
+            for (size_t i = a; i < b; ++i) {
+                const LaneJob& L = lane_jobs[i];
+                const unsigned w = width(L.buf);
+                const uint8_t* src = blob + d.poff[L.buf];
+                const uint64_t len = static_cast<uint64_t>(d.plen[L.buf]);
+                for (uint32_t q = 0; q < L.nf; ++q) {
+                    const uint64_t v = get_bits(src, len, (L.f0 + q) * w, w);
+                    put_bits(arena.data() + L.data0,
+                             static_cast<uint64_t>(q / kARows) * L.gwords * 32 + L.P + (q % kARows) * L.rowbits, v, w);
+                }
+            }
+        };
+        std::vector<std::thread> pool;
+        for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work, t);
+        work(0);
+        for (auto& th : pool) th.join();
+        copy_jobs.clear();
+        lane_jobs.clear();
     }
 
     // One CTA stripe.  Specs are single columns.  Stages take columns in order
@@ -1829,13 +1889,7 @@ struct Builder {
                 if (xo >= 8192u || w > 64) throw std::logic_error("hmat: phase-A lane record");
                 fast = fast && fmt == 0 && w <= 32 && e <= 10 && w == 1 + e + m && xo % 2 == 0;
                 arena[rec0 + q] = w | (e << 7) | ((fmt ? 0u : m) << 11) | ((fmt ? fmt - 2u : 0u) << 17) | (xo << 19);
-                const uint8_t* src = blob + d.poff[L.buf];
-                const uint64_t len = static_cast<uint64_t>(d.plen[L.buf]);
-                for (uint32_t j = 0; j < L.nf; ++j) {
-                    const uint64_t v = get_bits(src, len, (L.f0 + j) * w, w);
-                    put_bits(arena.data() + data0,
-                             static_cast<uint64_t>(j / kARows) * t.gwords * 32 + P + (j % kARows) * t.rowbits, v, w);
-                }
+                lane_jobs.push_back({data0, L.buf, L.f0, L.nf, P, t.rowbits, t.gwords});
                 if (keep_map)
                     h->segs[L.buf].push_back({data0, static_cast<uint32_t>(L.f0), L.nf, P,
                                               static_cast<uint16_t>(t.rowbits), static_cast<uint16_t>(t.gwords)});
@@ -2265,6 +2319,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     }
     B.segs.clear();
     B.segs.shrink_to_fit();
+    B.place_all();
     while (B.arena.size() % 4) B.arena.push_back(0u);
     B.arena.resize(B.arena.size() + 8, 0u);  // tail slack
     if (B.stages.size() >= (1ull << 31)) throw invalid_argument("hmat: too many stages");
@@ -2434,6 +2489,17 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
         nsm = di.nsm;
     }
     const int R = h->R;
+    std::lock_guard<std::mutex> hold(h->mu);
+    if (!h->last) check_cuda(cudaEventCreateWithFlags(&h->last, cudaEventDisableTiming), "event");
+    else if (h->last_stream != s) check_cuda(cudaStreamWaitEvent(s, h->last, 0), "stream wait");
+    struct Mark {  // record the product's end on every exit path
+        hcmx_hmat* h;
+        cudaStream_t s;
+        ~Mark() {
+            cudaEventRecord(h->last, s);
+            h->last_stream = s;
+        }
+    } mark{h, s};
     h->last_launches = 0;
     if (alpha == 0.0) {  // y = beta y without touching M
         const uint64_t n = (h->re - h->rb) * R;
@@ -2640,6 +2706,7 @@ void destroy_handle(hcmx_hmat* h) {
         cudaEventDestroy(r.b1);
     }
     for (auto e : h->ev_pool) cudaEventDestroy(e);
+    if (h->last) cudaEventDestroy(h->last);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }
@@ -2767,6 +2834,7 @@ int hcmx_gpu_hmat_matvec(hcmx_hmat* h, double alpha, const double* h_x, double b
             if (!h->trans) throw invalid_argument("matvec: transpose needs a handle created with with_transpose");
             h = h->trans;
         }
+        std::lock_guard<std::mutex> io(h->io_mu);
         if (!h->xbuf.p) h->xbuf.alloc(h->n_cols * 8);
         const uint64_t nr = h->re - h->rb;
         h2d(h->xbuf.p, h_x, h->n_cols * 8, h->stream);

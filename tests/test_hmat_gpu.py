@@ -401,3 +401,26 @@ def test_partition_cuts_compose_on_device(gpu, oracle, world):
         H.matvec(1.0, x, 0.0, y)
         H.close()
     assert rel(y, ref) <= TOL
+
+
+def test_one_handle_two_streams(gpu, oracle):
+    """products on one handle issued alternately on two streams (shared device
+    scratch): each waits for the previous one, every y is the oracle's"""
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    n = 2048
+    f, x = build_small_flat(n=n, eps=1e-6, scheme=0)
+    H = HMatrix(f.to_product())
+    xs = [torch.as_tensor(x * s).cuda() for s in (1.0, -2.0, 0.5, 3.0)]
+    refs = [oracle.hmat_matvec(f, 1.0, x * s, 0.0, np.zeros(n), threads=4) for s in (1.0, -2.0, 0.5, 3.0)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    ys = [torch.zeros(n, dtype=torch.float64, device="cuda") for _ in xs]
+    torch.cuda.synchronize()
+    for rep in range(5):
+        for i, (xd, yd) in enumerate(zip(xs, ys)):
+            st = streams[i % 2]
+            H.matvec_device(1.0, xd, 0.0, yd, stream=st.cuda_stream)
+    torch.cuda.synchronize()
+    for yd, r in zip(ys, refs):
+        assert rel(yd.cpu().numpy(), r) <= TOL
+    H.close()
