@@ -89,8 +89,10 @@ def _orth(Y: torch.Tensor) -> torch.Tensor:
     Gram-Schmidt applied twice per column (batched GEMVs, so it stays fast for
     many small blocks where the batched Householder QR launches per matrix).
     Numerically dependent columns become arbitrary orthonormal directions, which
-    a range finder tolerates."""
+    a range finder tolerates.  Few large blocks: Householder QR."""
     B, m, p = Y.shape
+    if B <= 64 and m >= 2048:
+        return torch.linalg.qr(Y)[0]
     Q = torch.empty_like(Y)
     for j in range(p):
         v = Y[:, :, j:j + 1]

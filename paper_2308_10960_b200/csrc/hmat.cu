@@ -72,6 +72,13 @@ constexpr int kNWB = HCMX_NWB;            // phase-B consumer warps per CTA
 #define HCMX_STAGE_BYTES 26624
 #endif
 constexpr int kNWA = HCMX_NWA;            // phase-A consumer warps (more registers per thread)
+#ifndef HCMX_AMINB
+#define HCMX_AMINB 2
+#endif
+#ifndef HCMX_BMINB
+#define HCMX_BMINB 2
+#endif
+constexpr int kCtasA = HCMX_AMINB, kCtasB = HCMX_BMINB;  // resident CTAs per SM (persistent grids)
 constexpr int kThreadsA = (kNWA + 1) * 32;
 constexpr int kStageBytes = HCMX_STAGE_BYTES;  // packed data per stage
 constexpr int kMaxItems = 32;             // items per stage (one per producer lane)
@@ -1108,7 +1115,7 @@ __device__ __forceinline__ void consumer_bar() {  // the consumer warps of phase
 
 // Persistent kernels: one CTA per resident slot, stripes claimed dynamically.
 template <int R>
-__global__ void __launch_bounds__(kThreadsA, 2) k_phase_a(Params p) {
+__global__ void __launch_bounds__(kThreadsA, kCtasA) k_phase_a(Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kRedBytes);
     uint64_t* empty = full + kNStage;
@@ -1134,7 +1141,7 @@ __global__ void __launch_bounds__(kThreadsA, 2) k_phase_a(Params p) {
 }
 
 template <int R>
-__global__ void __launch_bounds__((nwb<R>() + 1) * 32, 2) k_phase_b(Params p) {
+__global__ void __launch_bounds__((nwb<R>() + 1) * 32, kCtasB) k_phase_b(Params p) {
     constexpr int NW = nwb<R>();
     extern __shared__ __align__(128) uint8_t smem[];
     double* red = reinterpret_cast<double*>(smem + kRingBytes);
@@ -2177,7 +2184,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                 for (uint32_t i = 0; i < leafa[lr_id[l]].k; ++i)
                     xbytes_all += B.words_of(xbuf(l, i).first, d.col1[l] - d.col0[l]) * 4;
         const uint64_t stripe_target =
-            std::max<uint64_t>(2ull * kStageBytes, std::min<uint64_t>(kAStripeBytes, xbytes_all / (4ull * 2 * 148)));
+            std::max<uint64_t>(2ull * kStageBytes, std::min<uint64_t>(kAStripeBytes, xbytes_all / (4ull * kCtasA * 148)));
         for (uint64_t l : leaves) {
             if (d.kind[l] == 0) continue;
             const uint32_t id = static_cast<uint32_t>(lr_id[l]);
@@ -2360,7 +2367,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     // kMaxPieces stage ranges of similar cost; their partial row sums go to
     // ypart and k_combine adds them (fixed order, beta y once).
     const uint64_t nb_rows = stripe_b.size() - 1;
-    const uint64_t want = 2ull * 148;  // one stripe per CTA slot
+    const uint64_t want = static_cast<uint64_t>(kCtasB) * 148;  // one stripe per CTA slot
     const char* mp_env = std::getenv("HCMX_MAX_PIECES");  // test / profiling knob (1: never split)
     const uint64_t max_pieces = mp_env ? std::max(1, std::min(std::atoi(mp_env), static_cast<int>(kMaxPieces)))
                                        : kMaxPieces;
@@ -2544,7 +2551,7 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
         check_cuda(cudaLaunchKernelEx(&cfg, kernel, args...), "matvec launch");
         h->last_launches++;
     };
-    const uint32_t ga = std::min<uint32_t>(h->nstripe_a, 2 * nsm), gb = std::min<uint32_t>(h->nblocks, 2 * nsm);
+    const uint32_t ga = std::min<uint32_t>(h->nstripe_a, kCtasA * nsm), gb = std::min<uint32_t>(h->nblocks, kCtasB * nsm);
     const uint32_t gr = (h->nred_long + 7) / 8 + (h->nred - h->nred_long + 255) / 256;
     const RedCol* rc = h->redcols.as<RedCol>();
     const uint32_t gc = static_cast<uint32_t>(std::min<uint64_t>(((h->re - h->rb) * R + 255) / 256, 4 * nsm));

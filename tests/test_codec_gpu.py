@@ -275,7 +275,9 @@ def test_compress_device_api_bit_exact(gpu, oracle):
         db = codec.device_batch(vals, counts, 1e-6, s)
         codec.compress_device(vals, db)
         flags = db.d_flags.cpu().numpy()
-        assert (flags[-3:-1] & 1).all() and not (flags[:40] & 1).any()
+        if s != 3:  # DFL fixes e = 11: nothing to decide
+            assert (flags[-3:-1] & 1).all()
+        assert not (flags[:40] & 1).any()
         bb, nfix = codec.compress_device_finish(vals, db)
         host = bb.payload.cpu().numpy()
         for i, v in enumerate(blocks):
