@@ -58,11 +58,39 @@ def rank_from_singular_values(s: torch.Tensor, eps: float) -> torch.Tensor:
     return keep.cumprod(dim=-1).sum(dim=-1)
 
 
+_POOL = None
+
+
+def _svd_chunk(a):
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        return np.linalg.svd(a, full_matrices=False)
+
+
+def _pool():
+    """worker processes for host LAPACK (numpy's batched SVD does not scale over
+    threads: measured 1.4x on 16 threads vs 6.6x on 16 processes); forkserver
+    workers never touch CUDA"""
+    global _POOL
+    if _POOL is None:
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+        _POOL = ProcessPoolExecutor(max(1, min(32, os.cpu_count() or 1)), mp_context=mp.get_context("forkserver"))
+    return _POOL
+
+
 def _cpu_svd(M: torch.Tensor):
-    """batched SVD of small matrices on the host (LAPACK gesdd per matrix, threads
-    over the batch): cuSOLVER runs batched SVDs above 32x32 one matrix at a time"""
+    """batched SVD of small matrices on the host (LAPACK gesdd per matrix):
+    cuSOLVER runs batched SVDs above 32x32 one matrix at a time.  Large batches
+    go to a process pool, small ones run in this process."""
     from concurrent.futures import ThreadPoolExecutor
     a = M.detach().resolve_conj().cpu().numpy()
+    if a.shape[0] >= 2048 and (os.cpu_count() or 1) > 2:
+        parts = np.array_split(a, 4 * (os.cpu_count() or 1))
+        res = list(_pool().map(_svd_chunk, parts))
+        dev = M.device
+        cat = lambda i: torch.from_numpy(np.concatenate([r[i] for r in res])).to(dev)
+        return cat(0), cat(1), cat(2)
     B = a.shape[0]
     U = np.empty(a.shape[:-1] + (min(a.shape[-2:]),), a.dtype)
     S = np.empty((B, min(a.shape[-2:])))

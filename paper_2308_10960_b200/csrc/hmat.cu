@@ -43,6 +43,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -2024,9 +2025,23 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         }
         flush();
         B.blob = hb.p;
+        uint64_t need_bytes = 0;
+        for (const auto& r : rng) need_bytes += r.second - r.first;
+        B.arena.reserve(need_bytes / 4 + need_bytes / 40 + (1u << 20));  // + item / record overhead
     } else {
         B.blob = d.blob;
+        B.arena.reserve(d.blob_bytes / 4 + d.blob_bytes / 40 + (1u << 20));
     }
+    const bool stats = std::getenv("HCMX_BUILD_STATS") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t_build = now();
+    auto lap = [&](const char* what) {
+        if (!stats) return;
+        const auto t = now();
+        std::fprintf(stderr, "[build] %s %.2f s\n", what, std::chrono::duration<double>(t - t_build).count());
+        t_build = t;
+    };
+    lap("blob to host");
 
     uint64_t total_fields = 0;
     for (uint64_t b = 0; b < d.nbuffers; ++b) total_fields += d.count[b];
@@ -2213,6 +2228,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         }
     }
     rep.stages_a = B.stages.size();
+    lap("phase-A layout");
 
     // ---- phase B: one stripe per block of kR rows
     const uint64_t nblocks = (h->re - h->rb + kR - 1) / kR;
@@ -2309,6 +2325,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
         }
     }
     rep.stages_b = B.stages.size() - b_ws0;
+    lap("phase-B layout");
     if (std::getenv("HCMX_BUILD_STATS")) {  // profiling aid: copies / items / bytes per stage
         for (int ph = 0; ph < 2; ++ph) {
             const size_t s0 = ph ? b_ws0 : 0, s1 = ph ? B.stages.size() : b_ws0;
@@ -2327,6 +2344,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     B.segs.clear();
     B.segs.shrink_to_fit();
     B.place_all();
+    lap("bit placement");
     while (B.arena.size() % 4) B.arena.push_back(0u);
     B.arena.resize(B.arena.size() + 8, 0u);  // tail slack
     if (B.stages.size() >= (1ull << 31)) throw invalid_argument("hmat: too many stages");
@@ -2435,6 +2453,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     stream_sync(s);
     h->nstripe_a = nstripe_a;
     h->nblocks = static_cast<uint32_t>(sb.size());  // phase-B stripes
+    lap("upload");
     rep.device_arena_bytes = B.arena.size() * 4;
     rep.device_table_bytes = B.stages.size() * (sizeof(Stage) + kCopies * 8) + B.bitems.size() * sizeof(BItem) +
                              B.a_items * sizeof(AItem) +
