@@ -85,7 +85,13 @@ constexpr int kStageBytes = HCMX_STAGE_BYTES;  // packed data per stage
 constexpr int kMaxItems = 32;             // items per stage (one per producer lane)
 constexpr int kItemBytes = 32;            // descriptor size (A and B)
 constexpr int kCoefBytes = 7936;          // staged coefficients + column params per stage
-constexpr int kNStage = HCMX_NSTAGE;      // ring depth
+constexpr int kNStage = HCMX_NSTAGE;      // ring depth (phase B)
+#ifndef HCMX_NSTAGE_A
+#define HCMX_NSTAGE_A HCMX_NSTAGE
+#endif
+constexpr int kNStageA = HCMX_NSTAGE_A;   // ring depth of phase A (its CTAs need no reduction buffer)
+template <bool PHASE_A>
+__host__ __device__ constexpr int nstage() { return PHASE_A ? kNStageA : kNStage; }
 constexpr int kSlack = 16;                // decode reads up to 2 words past a segment
 constexpr unsigned kWaitHintNs = HCMX_WAIT_HINT;  // mbarrier try_wait suspend hint (ns)
 // A stage is one contiguous arena range, copied by ONE bulk copy into the slot:
@@ -132,8 +138,10 @@ constexpr uint64_t kAStripeBytes = 8 * kStageBytes;  // target packed bytes per 
 constexpr uint64_t kItemTarget = 1536;          // packed bytes per item (columns grouped up to this)
 constexpr uint64_t kItemMaxBytes = HCMX_BITEM;  // items merge columns up to this many packed bytes
 constexpr size_t kRingBytes = static_cast<size_t>(kNStage) * kSlotBytes;
+constexpr size_t kRingBytesA = static_cast<size_t>(kNStageA) * kSlotBytes;
 constexpr size_t kRedBytes = ((kNWB > HCMX_NWB_MULTI ? kNWB : HCMX_NWB_MULTI) / 2) * kR * sizeof(double);  // phase-B cross-warp reduction
 constexpr size_t kSmemBytes = kRingBytes + kRedBytes + 2 * kNStage * sizeof(uint64_t);  // + full, empty barriers
+constexpr size_t kSmemBytesA = kRingBytesA + 2 * kNStageA * sizeof(uint64_t);
 constexpr int kCopies = 2 * kMaxItems;  // coefficient copies per stage (two per producer lane)
 constexpr int kRangeBytes = 64;         // phase-B stage head: 16 warp item ranges (begin | end << 16)
 // copy entry (u64): [0,32) source element index, [32,48) dst / 16 in the slot,
@@ -537,7 +545,8 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
 #endif
     long long t_wait = 0;
     bool waited = false;           // phase B: griddepcontrol.wait done
-    unsigned slot = 0, phase = 0;  // it % kNStage, parity of the slot's previous use
+    constexpr int NS = nstage<PHASE_A>();
+    unsigned slot = 0, phase = 0;  // it % NS, parity of the slot's previous use
     uint32_t it = 0;
     // one stage: issue `cur`, load the metadata of the stage two ahead into
     // `ahead` (three rotating registers sets: no register copy waits on a load)
@@ -545,7 +554,7 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
         seq_next<PHASE_A>(p, q, lane);
         ahead = seq_meta<PHASE_A>(p, q, lane);
         const long long t0 = clk();
-        if (it >= kNStage) mbar_wait(&empty[slot], phase);
+        if (it >= NS) mbar_wait(&empty[slot], phase);
         t_wait += clk() - t0;
         uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
         if (lane == 0) {
@@ -601,9 +610,9 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
             return true;
         }
         ++it;
-        if (++slot == kNStage) {
+        if (++slot == NS) {
             slot = 0;
-            if (it > kNStage) phase ^= 1u;
+            if (it > NS) phase ^= 1u;
         }
         return false;
     };
@@ -632,7 +641,8 @@ template <int NW, bool DYN, class Body, class End>
 __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t* empty, unsigned warp,
                                         unsigned lane, int debug, Body&& body, End&& stripe_end) {
     long long t_wait = 0, t_busy = 0, t_end = 0;
-    unsigned slot = 0, phase = 0;  // ring position of stage it: it % kNStage, (it / kNStage) & 1
+    constexpr int NS = nstage<DYN>();  // DYN consumers are phase A's
+    unsigned slot = 0, phase = 0;  // ring position of stage it: it % NS, (it / NS) & 1
     for (;;) {
         const long long t0 = clk();
         mbar_wait(&full[slot], phase);
@@ -676,17 +686,17 @@ __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t*
             stripe_end(stripe);
             t_end += clk() - t2;
         }
-        if (++slot == kNStage) {
+        if (++slot == NS) {
             slot = 0;
             phase ^= 1u;
         }
     }
 }
 
-template <int NW>
+template <int NW, int NS>
 __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
     if (threadIdx.x == 0) {
-        for (int b = 0; b < kNStage; ++b) {
+        for (int b = 0; b < NS; ++b) {
             mbar_init(&full[b], 1);
             mbar_init(&empty[b], NW);
         }
@@ -1118,8 +1128,8 @@ __device__ __forceinline__ void consumer_bar() {  // the consumer warps of phase
 template <int R>
 __global__ void __launch_bounds__(kThreadsA, kCtasA) k_phase_a(Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kRedBytes);
-    uint64_t* empty = full + kNStage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytesA);
+    uint64_t* empty = full + kNStageA;
     const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     // phase B's stripe counter for this product (A runs first, B claims only
     // after its griddepcontrol.wait, so the store is visible by then)
@@ -1127,7 +1137,7 @@ __global__ void __launch_bounds__(kThreadsA, kCtasA) k_phase_a(Params p) {
         p.work[1] = 0u;
         __threadfence();  // visible before this CTA triggers phase B's launch
     }
-    ring_init<kNWA>(full, empty);
+    ring_init<kNWA, kNStageA>(full, empty);
     pdl_trigger();
     if (warp == kNWA) {
         producer<true, R>(p, smem, full, empty, lane);
@@ -1149,7 +1159,7 @@ __global__ void __launch_bounds__((nwb<R>() + 1) * 32, kCtasB) k_phase_b(Params 
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kRedBytes);
     uint64_t* empty = full + kNStage;
     const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    ring_init<NW>(full, empty);
+    ring_init<NW, kNStage>(full, empty);
     if (warp == NW) {
         producer<false, R>(p, smem, full, empty, lane);
         return;
@@ -2502,10 +2512,10 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
         std::lock_guard<std::mutex> g(dev_mu);
         DevInfo& di = dev_info[dev];
         if (!di.ready) {
-            const int sm = static_cast<int>(kSmemBytes);
-            check_cuda(cudaFuncSetAttribute(k_phase_a<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+            const int sm = static_cast<int>(kSmemBytes), sma = static_cast<int>(kSmemBytesA);
+            check_cuda(cudaFuncSetAttribute(k_phase_a<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sma), "smem attr");
             check_cuda(cudaFuncSetAttribute(k_phase_b<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-            check_cuda(cudaFuncSetAttribute(k_phase_a<kMultiR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+            check_cuda(cudaFuncSetAttribute(k_phase_a<kMultiR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sma),
                        "smem attr");
             check_cuda(cudaFuncSetAttribute(k_phase_b<kMultiR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
                        "smem attr");
@@ -2575,13 +2585,13 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
     const RedCol* rc = h->redcols.as<RedCol>();
     const uint32_t gc = static_cast<uint32_t>(std::min<uint64_t>(((h->re - h->rb) * R + 255) / 256, 4 * nsm));
     if (R == 1) {
-        if (run_a) launch(k_phase_a<1>, ga, kThreadsA, kSmemBytes, false, p);
+        if (run_a) launch(k_phase_a<1>, ga, kThreadsA, kSmemBytesA, false, p);
         if (h->nred) launch(k_reduce<1>, gr, 256, 0, true, p, rc, h->nred_long, h->nred);
         if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
         if (h->nblocks) launch(k_phase_b<1>, gb, (nwb<1>() + 1) * 32, kSmemBytes, run_a, p);
         if (h->pieces) launch(k_combine<1>, gc, 256, 0, true, p, h->npieces.as<uint8_t>());
     } else {
-        if (run_a) launch(k_phase_a<kMultiR>, ga, kThreadsA, kSmemBytes, false, p);
+        if (run_a) launch(k_phase_a<kMultiR>, ga, kThreadsA, kSmemBytesA, false, p);
         if (h->nred) launch(k_reduce<kMultiR>, gr, 256, 0, true, p, rc, h->nred_long, h->nred);
         if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
         if (h->nblocks) launch(k_phase_b<kMultiR>, gb, (nwb<kMultiR>() + 1) * 32, kSmemBytes, run_a, p);

@@ -3,7 +3,7 @@
 # HCMX_BUILD_TAG=<tag> HCMX_NVCC_DEFS=...) on one cached matrix (profiling aid):
 #   tools/ab_variants.sh CONFIG REPS tag1 tag2 ...
 cfg=$1; reps=$2; shift 2
-cache=/tmp/hmat_c${cfg}.pkl
+cache=/dev/shm/hmat_c${cfg}.pkl
 python tools/prof_hmat.py --config $cfg --iters 5 --cache $cache --yref /tmp/yref_c${cfg}.npy 2>&1 | tail -2
 for r in $(seq $reps); do
   for t in base "$@"; do

@@ -52,11 +52,20 @@ def main():
           f"{rep.device_arena_bytes / 1e9:.3f} GB, stages A {rep.stages_a} B {rep.stages_b})", flush=True)
     H.close()
     for N in Ns:
-        times = []
+        times, detail = [], []
         for rr in partition_rows(flat, N):
             Hr = HMatrix(flat, row_range=rr)
             times.append(timed(Hr, x, y))
+            Hr.timing(1)
+            for _ in range(10):
+                Hr.matvec_device(1.0, x, 0.0, y)
+            ma, mb, calls = Hr.timing(0)
+            r = Hr.memory()
+            detail.append(f"[{rr[0]},{rr[1]}) A {ma / calls:.3f} B {mb / calls:.3f} ms, {r.algorithmic_bytes / 1e9:.2f} GB, "
+                          f"stages {r.stages_a}/{r.stages_b}")
             Hr.close()
+        for d in detail:
+            print("     ", d)
         print(f"N={N}: per-rank ms {' '.join(f'{v:.4f}' for v in times)} | max {max(times):.4f}, "
               f"T1/(N*Tmax) = {t1 / (N * max(times)):.3f}", flush=True)
 
