@@ -2,20 +2,27 @@
 """Benchmark of the hot path: compressed H-matrix-vector product on the B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 3] [--scheme afl]
+                    [--config 4] [--scheme afl]
 
 Workload (BASELINE.json metric "compressed H-matvec GB/s (compressed bytes)"):
-config 3 -- Laplace 1/(4 pi r) on n=131072 Fibonacci-sphere points, leaf 64,
-eta 2, SVD truncation 1e-8, AFL-APLR lowrank + AFL dense leaves; a step is one
-FP64 product y = A x over the whole matrix (100 repeated products with fixed x
-in the BASELINE).  Compressed streams (~1 GB) are far larger than L2, so no L2
-flush is needed between products.  Bytes per product follow SURVEY 8(d):
-sum(ceil(N w / 8) + 20) over codec buffers + 8 k per APLR leaf + 8 n (x) + 8 n (y).
+config 4 (default) -- Matern nu=1.5, l=0.1 on n=524288 seeded uniform points in
+the unit cube, leaf 64, eta 2, SVD truncation 1e-6, AFL-APLR lowrank + AFL
+dense leaves (13.9 GB compressed): the largest BASELINE configuration that fits
+one B200 and BASELINE's 1/2/4/8-GPU scaling workload, so the N = 1 line and the
+scaling runs measure the same matrix.  --config 3 (Laplace sphere n=131072,
+1.1 GB) is the single-GPU roofline workload of round 1.  A step is one FP64
+product y = A x over the whole matrix (repeated products with fixed x).
+Compressed streams are far larger than L2, so no L2 flush is needed between
+products.  Bytes per product follow SURVEY 8(d): sum(ceil(N w / 8) + 20) over
+codec buffers + 8 k per APLR leaf + 8 n (x) + 8 n (y).
 
-N > 1 (torchrun): block-row partition, x replicated, NCCL all-gather of the
-y slices after every product (strong scaling: the matrix is fixed).
+N > 1 (torchrun): block-row partition through the library's partitioned
+handle (hcmx_gpu_hmat_create_partitioned), x replicated, the y slices
+exchanged by NCCL in-place broadcasts inside the library after every product
+(strong scaling: the matrix is fixed).
 --impl reference: the reference codec (oracle/_ref, /root/reference
-codec.cpp) + the restated matvec glue on all host cores, rank 0 only.
+codec.cpp) + the restated matvec glue on all host cores, rank 0 only, on a
+bounded row sample (config 4: the first quarter of the rows).
 """
 from __future__ import annotations
 
@@ -446,7 +453,7 @@ def run_ours(args, rank, world, local):
         dom_bytes, dom_ms = (kb, per_b) if dom == "phase_b" else (ka, per_a)
         achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
         traffic = None
-        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        tp = os.path.join(ROOT, "profiles", f"ncu_traffic_c{args.config}.json")
         if os.path.exists(tp):
             traffic = json.load(open(tp)).get(dom)
         cpu, parity = None, None
@@ -511,7 +518,10 @@ def run_reference(args, rank, world):
     if rank != 0:
         return None
     t0 = time.time()
-    flat, info = build_flat_cpu(args.config, args.scheme)
+    # the sample: the whole matrix for configs up to 3, the first quarter of the
+    # rows (leaves inside them) for config 4 -- each step stays ~1 s on the host
+    row_frac = 0.25 if str(args.config) == "4" else 1.0
+    flat, info = build_flat_cpu(args.config, args.scheme, row_frac)
     threads = os.cpu_count() or 1
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import Oracle, RefOracle
@@ -520,11 +530,12 @@ def run_reference(args, rank, world):
     data_s, workload_s = workload_strings(args.config, n, args.scheme)
     x = np.random.default_rng(0).uniform(-1, 1, n)
     # one step = the product over a row-slice sample sized to ~1 s
-    sub = restrict(flat, (0, max(64, n // 16 // 64 * 64)))
+    nr = int(n * row_frac) // 64 * 64
+    sub = restrict(flat, (0, max(64, nr // 16 // 64 * 64)))
     t = time.perf_counter()
     impl.hmat_matvec(sub, 1.0, x, 0.0, np.zeros(n), threads=threads)
     dt = max(time.perf_counter() - t, 1e-6) * 16
-    rows = min(n, max(64, int(n * min(1.0, 1.0 / dt)) // 64 * 64))
+    rows = min(nr, max(64, int(nr * min(1.0, 1.0 / dt)) // 64 * 64))
     sample = restrict(flat, (0, rows))
     sb = step_bytes(flat, (0, rows))
     for _ in range(args.warmup):
@@ -549,9 +560,11 @@ def run_reference(args, rank, world):
     return line
 
 
-def build_flat_cpu(cfg, scheme):
+def build_flat_cpu(cfg, scheme, row_frac=1.0):
     """reference arm setup: FP64 assembly (torch), then the REFERENCE codec on the
-    host (compress for dense leaves, restated APLR glue for lowrank leaves)"""
+    host (compress for dense leaves, restated APLR glue for lowrank leaves).
+    row_frac < 1: only the leaves of rows [0, row_frac n) -- the bounded sample
+    the reference arm times -- are assembled and compressed"""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle import Oracle, RefOracle
@@ -563,6 +576,10 @@ def build_flat_cpu(cfg, scheme):
     pts = problems.make_points(c["geometry"], c["n"], 1)
     ct = tree.build_cluster_tree(pts, c["leaf"])
     lv = tree.build_block_tree(ct, ct, c["eta"])
+    if row_frac < 1.0:
+        from dataclasses import replace as _rep
+        keep = lv.row1 <= int(c["n"] * row_frac) // 64 * 64
+        lv = _rep(lv, **{k: getattr(lv, k)[keep] for k in ("row", "col", "admissible", "row0", "row1", "col0", "col1")})
     A = assemble.assemble(pts[ct.i2e], lv, problems.make_kernel(c["kernel"]), c["eps"])
     dense, W, X = A.dense.cpu().numpy(), A.W.cpu().numpy(), A.X.cpu().numpy()
     rows = (lv.row1 - lv.row0).astype(np.int64)
@@ -614,7 +631,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="3")
+    ap.add_argument("--config", default="4")
     ap.add_argument("--scheme", default="afl", choices=["afl", "aflp", "bfl", "dfl"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-codec", action="store_true")

@@ -2134,6 +2134,16 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     uint32_t nstripe_a = 0;
     std::vector<uint32_t> stripe_a = {0};
     {
+        // stripe size: ~kAStripeBytes, smaller when the X factors of this handle
+        // (one rank of a row partition) would give fewer than ~4 stripes per
+        // CTA slot (2 per SM) -- else the slowest stripe sets the phase time
+        uint64_t xbytes_all = 0;
+        for (uint64_t l : leaves)
+            if (d.kind[l] != 0)
+                for (uint32_t i = 0; i < leafa[lr_id[l]].k; ++i)
+                    xbytes_all += B.words_of(xbuf(l, i).first, d.col1[l] - d.col0[l]) * 4;
+        const uint64_t stripe_target =
+            std::max<uint64_t>(2ull * kStageBytes, std::min<uint64_t>(kAStripeBytes, xbytes_all / (4ull * kCtasA * 148)));
         std::vector<uint32_t> pend;  // lowrank ids of the current stripe
         uint64_t stripe_bytes = 0;
         std::vector<ALane> lanes;
@@ -2194,22 +2204,33 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                 }
             }
             if (npartial >= (1ull << 32) || ncols >= (1u << 31)) throw invalid_argument("hmat: too many rank columns");
-            B.emit_stripe_a(lanes);
-            stripe_a.push_back(static_cast<uint32_t>(B.stages.size()));
-            ++nstripe_a;
+            // one stripe is one CTA's serial work: a leaf whose X factor is larger
+            // than the stripe target (the top-level blocks: 8192 ... 32768
+            // columns) is cut at segment boundaries into several stripes, so its
+            // columns are decoded by several CTAs (segments write separate
+            // partials, k_reduce adds them in fixed order)
+            std::vector<ALane> part;
+            uint64_t pbytes = 0;
+            for (size_t i = 0; i < lanes.size(); ++i) {
+                const ALane& L = lanes[i];
+                if (L.g == 0 && pbytes >= stripe_target && !part.empty()) {
+                    B.emit_stripe_a(part);
+                    stripe_a.push_back(static_cast<uint32_t>(B.stages.size()));
+                    ++nstripe_a;
+                    part.clear();
+                    pbytes = 0;
+                }
+                part.push_back(L);
+                pbytes += (static_cast<uint64_t>(L.nf) * B.width(L.buf) + 7) / 8;
+            }
+            if (!part.empty()) {
+                B.emit_stripe_a(part);
+                stripe_a.push_back(static_cast<uint32_t>(B.stages.size()));
+                ++nstripe_a;
+            }
             pend.clear();
             stripe_bytes = 0;
         };
-        // stripe size: ~kAStripeBytes, smaller when the X factors of this handle
-        // (one rank of a row partition) would give fewer than ~4 stripes per
-        // CTA slot (2 per SM) -- else the slowest stripe sets the phase time
-        uint64_t xbytes_all = 0;
-        for (uint64_t l : leaves)
-            if (d.kind[l] != 0)
-                for (uint32_t i = 0; i < leafa[lr_id[l]].k; ++i)
-                    xbytes_all += B.words_of(xbuf(l, i).first, d.col1[l] - d.col0[l]) * 4;
-        const uint64_t stripe_target =
-            std::max<uint64_t>(2ull * kStageBytes, std::min<uint64_t>(kAStripeBytes, xbytes_all / (4ull * kCtasA * 148)));
         for (uint64_t l : leaves) {
             if (d.kind[l] == 0) continue;
             const uint32_t id = static_cast<uint32_t>(lr_id[l]);
