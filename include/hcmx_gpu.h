@@ -223,6 +223,48 @@ typedef struct hcmx_memory_report {
     uint64_t dense_leaves, lowrank_leaves, stages_a, stages_b;
 } hcmx_memory_report;
 
+/* ------------------------------------------------- compress_in_place ----- */
+/* An assembled, uncompressed H-matrix (the input of compress_in_place,
+ * hmatrix.hpp:115-119): leaf ranges on the host; FP64 payloads on the device.
+ *   kind 0 dense leaf: rows x cols column-major at d_dense + dense_off[l]
+ *   kind 1 lowrank leaf W diag(sigma) X^T (svd_factors' shape, lowrank.cpp:76-93):
+ *          W rows x k column-major at d_W + w_off[l], X cols x k at d_X + x_off[l],
+ *          sigma[sig_off[l] .. + k) on the host */
+typedef struct hcmx_assembled {
+    uint64_t n_rows, n_cols, nleaves;
+    const int64_t *row0, *row1, *col0, *col1, *kind, *rank; /* [nleaves], host */
+    const double* d_dense;
+    const int64_t* dense_off;
+    const double *d_W, *d_X;
+    const int64_t *w_off, *x_off;
+    const double* sigma;
+    const int64_t* sig_off;
+} hcmx_assembled;
+
+/* StorageMode kinds (hmatrix.hpp:32-40) */
+enum hcmx_storage { HCMX_STORE_APLR = 0, HCMX_STORE_CODEC = 1, HCMX_STORE_MP = 2, HCMX_STORE_FP64 = 3 };
+
+typedef struct hcmx_flat hcmx_flat; /* a compressed, flattened H-matrix: host tables + device blob */
+
+/* compress_in_place (hmatrix.hpp:115-119) on the device:
+ *   APLR   dense -> codec::compress iff dense_too (else FP64 words); lowrank ->
+ *          APLR (per-column precision from sigma, mixedprec.cpp:155-187)
+ *   CODEC  dense as above; lowrank U = W diag(sigma), V = X as one codec buffer
+ *          each (CodecLowrank, hmatrix.hpp:46-49)
+ *   MP     dense FP64; lowrank columns in FP64 / FP32 / FP16 groups
+ *          (mp_partition, mixedprec.cpp:66-120)
+ *   FP64   uncompressed (dense FP64, U and V FP64)
+ * Bytes equal the reference codec's (tests).  *report = memory_footprint
+ * (hmatrix.hpp:96-124) of the result. */
+int hcmx_gpu_compress_in_place(const hcmx_assembled* A, double eps, int storage, int scheme, int dense_too,
+                               hcmx_flat** out, hcmx_memory_report* report, void* stream);
+/* the result as an hcmx_hmat_desc (pointers into f, blob_on_device = 1), ready
+ * for hcmx_gpu_hmat_create / _create_partitioned; valid while f lives */
+int hcmx_gpu_flat_desc(const hcmx_flat* f, hcmx_hmat_desc* desc);
+/* copies the device blob (desc.blob_bytes) into caller device memory */
+int hcmx_gpu_flat_copy_blob(const hcmx_flat* f, uint8_t* d_dst, void* stream);
+int hcmx_gpu_flat_destroy(hcmx_flat* f);
+
 int hcmx_gpu_hmat_create(const hcmx_hmat_desc* desc, hcmx_hmat** out);
 int hcmx_gpu_hmat_destroy(hcmx_hmat* h);
 int hcmx_gpu_hmat_memory(const hcmx_hmat* h, hcmx_memory_report* out);

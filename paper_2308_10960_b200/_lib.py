@@ -54,6 +54,14 @@ class hcmx_hmat_desc(C.Structure):
                 ("nrhs_block", C.c_int)]
 
 
+class hcmx_assembled(C.Structure):
+    _fields_ = [("n_rows", C.c_uint64), ("n_cols", C.c_uint64), ("nleaves", C.c_uint64),
+                ("row0", _pi64), ("row1", _pi64), ("col0", _pi64), ("col1", _pi64),
+                ("kind", _pi64), ("rank", _pi64), ("d_dense", C.c_void_p), ("dense_off", _pi64),
+                ("d_W", C.c_void_p), ("d_X", C.c_void_p), ("w_off", _pi64), ("x_off", _pi64),
+                ("sigma", C.POINTER(C.c_double)), ("sig_off", _pi64)]
+
+
 class hcmx_memory_report(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "dense_raw", "dense_compressed", "lowrank_raw", "lowrank_compressed", "overhead",
@@ -111,6 +119,11 @@ PROTOTYPES = {
     "hcmx_gpu_hmat_export_buffer": (_i, [_vp, _u64, _vp, _u64, _pu64]),
     "hcmx_gpu_hmat_last_launches": (_i, [_vp]),
     "hcmx_gpu_hmat_timing": (_i, [_vp, _i, C.POINTER(_d), C.POINTER(_d), _pu64]),
+    "hcmx_gpu_compress_in_place": (_i, [C.POINTER(hcmx_assembled), _d, _i, _i, _i, C.POINTER(_vp),
+                                        C.POINTER(hcmx_memory_report), _vp]),
+    "hcmx_gpu_flat_desc": (_i, [_vp, C.POINTER(hcmx_hmat_desc)]),
+    "hcmx_gpu_flat_destroy": (_i, [_vp]),
+    "hcmx_gpu_flat_copy_blob": (_i, [_vp, _vp, _vp]),
     "hcmx_gpu_partition_rows": (_i, [C.POINTER(hcmx_hmat_desc), _i, _pu64]),
     "hcmx_gpu_nccl_unique_id": (_i, [_vp]),
     "hcmx_gpu_nccl_comm_init": (_i, [_i, _vp, _i, C.POINTER(_vp)]),

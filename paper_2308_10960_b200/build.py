@@ -32,7 +32,7 @@ NVFLAGS = ARCH + [*(["-DHCMX_PROF"] if os.environ.get("HCMX_PROF_BUILD") else []
 CUDA_INC = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "include")
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-I" + INC, "-I" + CSRC, "-I" + CUDA_INC]
 
-CU = ["codec_kernels.cu", "hmat.cu"]
+CU = ["codec_kernels.cu", "hmat.cu", "compress.cu"]
 CPP = ["codec_host.cpp", "dist.cpp"]
 
 

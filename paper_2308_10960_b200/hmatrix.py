@@ -149,28 +149,7 @@ class FlatHMatrix:
 
 
 RAW_F64, RAW_F32, RAW_F16 = 4, 5, 6   # hcmx_scheme raw storage (include/hcmx_gpu.h)
-_RAW_BYTES = {RAW_F64: 8, RAW_F32: 4, RAW_F16: 2}
 MP_ROUNDOFFS = (1.1e-16, 6.0e-8, 4.9e-4)   # mixedprec.hpp:23 (MP-D-S-H)
-
-
-def _raw_desc(n: int, fmt: int) -> np.ndarray:
-    d = np.zeros(n, dtype=DESC_DTYPE)
-    d["scheme"] = fmt
-    d["bit_width"] = 8 * _RAW_BYTES[fmt]
-    d["scale"] = 1.0
-    return d
-
-
-def _pack_raw(v: torch.Tensor, fmt: int) -> torch.Tensor:
-    """PackedSlice::pack (mixedprec.cpp:16-41) on the device: FP64 words as is,
-    FP32 = (float)v, FP16 = float_to_half((float)v) (half.hpp:75: two rounding
-    steps, both round-to-nearest-even; torch's float -> half is the IEEE one)"""
-    v = v.to(torch.float64).contiguous()
-    if fmt == RAW_F64:
-        return v.view(torch.uint8)
-    if fmt == RAW_F32:
-        return v.to(torch.float32).contiguous().view(torch.uint8)
-    return v.to(torch.float32).to(torch.float16).contiguous().view(torch.uint8)
 
 
 def mp_partition(sigma: np.ndarray, delta: float) -> np.ndarray:
@@ -184,176 +163,64 @@ def mp_partition(sigma: np.ndarray, delta: float) -> np.ndarray:
     return g
 
 
+_STORE = {"aplr": 0, "codec": 1, "mp": 2, "fp64": 3}   # enum hcmx_storage (include/hcmx_gpu.h)
+
+
 def compress_in_place(A: Assembled, eps: float, mode: StorageMode | str = "afl-aplr",
                       dense_too: bool = True, threads: int = 1) -> FlatHMatrix:
-    """hmatrix.hpp:115-119 on the device, for every StorageMode kind
-    (hmatrix.hpp:32-40, SPEC.md:449-457):
+    """hmatrix.hpp:115-119 on the device through hcmx_gpu_compress_in_place, for
+    every StorageMode kind (hmatrix.hpp:32-40):
       aplr  dense -> codec::compress (iff dense_too, else FP64); lowrank -> APLR
-            (hcmx_gpu_aplr_compress: per-column precision from sigma)
+            (per-column precision from sigma, mixedprec.cpp:155-187)
       codec dense as above; lowrank U = W diag(sigma), V = X each compressed as
             one buffer (CodecLowrank, hmatrix.hpp:46-49)
       mp    dense FP64 (MP never compresses dense); lowrank W Sigma X^H with the
             columns in FP64 / FP32 / FP16 groups (mp_compress, mixedprec.cpp:94-120)
       fp64  uncompressed: dense FP64, lowrank U, V in FP64 (LowrankBlock)
-    Returns the flattened H-matrix (payload blob resident on the GPU)."""
+    Returns the flattened H-matrix (payload blob resident on the GPU); the
+    MemoryReport of the reference is FlatHMatrix.memory_footprint()."""
     if isinstance(mode, str):
         mode = StorageMode.parse(mode)
     _lib.ensure_device()
-    scheme = int(mode.scheme)
     lv = A.leaves
     L = len(lv)
-    rows = (lv.row1 - lv.row0).astype(np.int64)
-    cols = (lv.col1 - lv.col0).astype(np.int64)
-    didx = np.nonzero(A.kind == 0)[0]
-    lidx = np.nonzero(A.kind == 1)[0]
-    kind = A.kind.astype(np.int64).copy()
-    rank = A.rank.astype(np.int64).copy()
-    sigma = np.ascontiguousarray(A.sigma, np.float64)
-    sig0 = A.sig_off.copy()
-    sig0[sig0 < 0] = 0
-
-    uniform = mode.kind in ("codec", "fp64")  # lowrank leaves as U, V (kind 2)
-    if uniform:
-        kind[lidx] = 2
-    nbuf_leaf = np.where(kind == 0, 1, np.where(kind == 2, np.where(rank > 0, 2, 0), 2 * rank))
-    buf0 = np.concatenate([[0], np.cumsum(nbuf_leaf)[:-1]]).astype(np.int64)
-    nb = int(nbuf_leaf.sum())
-    desc = np.zeros(nb, dtype=DESC_DTYPE)
-    count = np.zeros(nb, np.int64)
-    poff = np.zeros(nb, np.int64)
-    parts, total = [], 0
-
-    def add(payload: torch.Tensor, nbytes: int) -> int:
-        nonlocal total
-        at = total
-        pad = (-nbytes) % 16
-        parts.append(payload[:nbytes])
-        if pad:
-            parts.append(torch.zeros(pad, dtype=torch.uint8, device="cuda"))
-        total += nbytes + pad
-        return at
-
-    # dense leaves
-    dn = rows[didx] * cols[didx]
-    if didx.size:
-        if mode.kind in ("aplr", "codec") and dense_too:
-            bb = compress_batch(A.dense, dn.astype(np.uint64), eps, scheme,
-                                voff=A.dense_off[didx].astype(np.uint64))
-            at = add(bb.payload, bb.total)
-            b = buf0[didx]
-            desc[b] = bb.desc
-            count[b] = dn
-            poff[b] = bb.poff.astype(np.int64) + at
-        else:  # FP64 (StorageMode fp64 / mp, or dense_too = false)
-            dev = A.dense.to("cuda")
-            off = A.dense_off[didx]
-            idx = torch.as_tensor(np.concatenate([np.arange(o, o + c) for o, c in zip(off, dn)])
-                                  if didx.size else np.zeros(0, np.int64)).cuda()
-            raw = _pack_raw(dev.index_select(0, idx), RAW_F64)
-            at = add(raw, raw.numel())
-            b = buf0[didx]
-            desc[b] = _raw_desc(didx.size, RAW_F64)
-            count[b] = dn
-            poff[b] = at + 8 * np.concatenate([[0], np.cumsum(dn)[:-1]])
-
-    kk = rank[lidx]
-    if lidx.size and kk.sum() > 0:
-        W = A.W.to("cuda")
-        X = A.X.to("cuda")
-        if mode.kind == "aplr":
-            lr_boff = np.concatenate([[0], np.cumsum(2 * kk)[:-1]]).astype(np.uint64)
-            nlb = int(2 * kk.sum())
-            cap = int(8 * (A.W.numel() + A.X.numel()) + 16 * nlb + 16)
-            lr_payload = torch.empty(cap, dtype=torch.uint8, device="cuda")
-            lr_desc = np.zeros(nlb, dtype=DESC_DTYPE)
-            lr_poff = np.zeros(nlb, dtype=np.uint64)
-            tot = C.c_uint64()
-            rr = rows[lidx].astype(np.uint64); cc = cols[lidx].astype(np.uint64)
-            wo = A.w_off[lidx].astype(np.uint64); xo = A.x_off[lidx].astype(np.uint64)
-            so = A.sig_off[lidx].astype(np.uint64)
-            check(lib().hcmx_gpu_aplr_compress(lidx.size, u64p(rr), u64p(cc), u64p(kk.astype(np.uint64)),
-                                               ptr(W), u64p(wo), ptr(X), u64p(xo), ptr(sigma), u64p(so),
-                                               u64p(lr_boff), float(eps), scheme, ptr(lr_payload), cap,
-                                               ptr(lr_desc), u64p(lr_poff), C.byref(tot),
-                                               torch.cuda.current_stream().cuda_stream), "aplr_compress")
-            at = add(lr_payload, tot.value)
-            j = 0
-            for l in lidx:
-                k = int(rank[l])
-                sl = slice(int(buf0[l]), int(buf0[l]) + 2 * k)
-                desc[sl] = lr_desc[j: j + 2 * k]
-                count[sl] = [rows[l]] * k + [cols[l]] * k
-                poff[sl] = lr_poff[j: j + 2 * k].astype(np.int64) + at
-                j += 2 * k
-        elif uniform:
-            # U = W diag(sigma) (one FP64 product per element), V = X; one buffer each
-            sig_t = torch.as_tensor(sigma).cuda()
-            us, ucount = [], []
-            for l in lidx:
-                k = int(rank[l])
-                if k == 0:
-                    continue
-                r, c = int(rows[l]), int(cols[l])
-                Wl = W[A.w_off[l]: A.w_off[l] + r * k].view(k, r)
-                s = sig_t[A.sig_off[l]: A.sig_off[l] + k]
-                us.append((Wl * s[:, None]).reshape(-1))
-                us.append(X[A.x_off[l]: A.x_off[l] + c * k])
-                ucount += [r * k, c * k]
-            vals = torch.cat(us) if us else torch.zeros(0, dtype=torch.float64, device="cuda")
-            ucount = np.array(ucount, np.int64)
-            bidx = np.concatenate([[int(buf0[l]), int(buf0[l]) + 1] for l in lidx if rank[l] > 0])
-            if mode.kind == "codec":
-                bb = compress_batch(vals, ucount.astype(np.uint64), eps, scheme)
-                at = add(bb.payload, bb.total)
-                desc[bidx] = bb.desc
-                poff[bidx] = bb.poff.astype(np.int64) + at
-            else:
-                raw = _pack_raw(vals, RAW_F64)
-                at = add(raw, raw.numel())
-                desc[bidx] = _raw_desc(bidx.size, RAW_F64)
-                poff[bidx] = at + 8 * np.concatenate([[0], np.cumsum(ucount)[:-1]])
-            count[bidx] = ucount
-            sigma = np.ones(max(1, sigma.size))  # unused by U V^T leaves
-        else:  # mp: per-column raw formats by the D-S-H partition
-            cols_fmt, ws, xs_, wcnt, xcnt, keep_rank = [], [], [], [], [], rank.copy()
-            for l in lidx:
-                k = int(rank[l])
-                if k == 0:
-                    continue
-                sl = sigma[A.sig_off[l]: A.sig_off[l] + k]
-                g = mp_partition(sl, eps * sl[0])
-                assert (g >= 0).all() and (np.diff(g) >= 0).all(), "sigma must be decreasing above delta"
-                cols_fmt.append(RAW_F64 + g)
-            fmts = np.concatenate(cols_fmt) if cols_fmt else np.zeros(0, np.int64)
-            # buffers in leaf order: W columns then X columns of each leaf
-            wbytes, chunks = [], []
-            j = 0
-            bi, bcount, bfmt = [], [], []
-            for l in lidx:
-                k = int(rank[l])
-                if k == 0:
-                    continue
-                r, c = int(rows[l]), int(cols[l])
-                Wl = W[A.w_off[l]: A.w_off[l] + r * k]
-                Xl = X[A.x_off[l]: A.x_off[l] + c * k]
-                for i in range(k):
-                    f = int(fmts[j + i])
-                    chunks.append((_pack_raw(Wl[i * r:(i + 1) * r], f), r, f, int(buf0[l]) + i))
-                for i in range(k):
-                    f = int(fmts[j + i])
-                    chunks.append((_pack_raw(Xl[i * c:(i + 1) * c], f), c, f, int(buf0[l]) + k + i))
-                j += k
-            for pl, n, f, b in chunks:
-                at = add(pl, pl.numel())
-                desc[b] = _raw_desc(1, f)[0]
-                count[b] = n
-                poff[b] = at
-    blob = torch.cat(parts) if parts else torch.zeros(16, dtype=torch.uint8, device="cuda")
-    plen = (count * desc["bit_width"].astype(np.int64) + 7) // 8
-    return FlatHMatrix(A.n, A.n, lv.row0.astype(np.int64), lv.row1.astype(np.int64),
-                       lv.col0.astype(np.int64), lv.col1.astype(np.int64), kind, rank, buf0, sig0,
-                       np.ascontiguousarray(sigma), desc, count, poff, plen, blob,
-                       meta={"eps": eps, "mode": mode.name(), "dense_too": dense_too})
+    keep = []
+    i64 = lambda x: keep.append(np.ascontiguousarray(x, dtype=np.int64)) or keep[-1].ctypes.data_as(C.POINTER(C.c_int64))
+    dense = A.dense.to("cuda").contiguous()
+    W = A.W.to("cuda").contiguous()
+    X = A.X.to("cuda").contiguous()
+    sigma = np.ascontiguousarray(A.sigma if A.sigma.size else np.zeros(1), np.float64)
+    a = _lib.hcmx_assembled()
+    a.n_rows = a.n_cols = int(A.n)
+    a.nleaves = L
+    a.row0, a.row1, a.col0, a.col1 = i64(lv.row0), i64(lv.row1), i64(lv.col0), i64(lv.col1)
+    a.kind, a.rank = i64(A.kind), i64(A.rank)
+    a.d_dense, a.dense_off = ptr(dense), i64(np.maximum(A.dense_off, 0))
+    a.d_W, a.d_X = ptr(W), ptr(X)
+    a.w_off, a.x_off = i64(np.maximum(A.w_off, 0)), i64(np.maximum(A.x_off, 0))
+    a.sigma = sigma.ctypes.data_as(C.POINTER(C.c_double))
+    a.sig_off = i64(np.maximum(A.sig_off, 0))
+    h = C.c_void_p()
+    rep = _lib.hcmx_memory_report()
+    check(lib().hcmx_gpu_compress_in_place(C.byref(a), float(eps), _STORE[mode.kind], int(mode.scheme),
+                                           int(bool(dense_too)), C.byref(h), C.byref(rep),
+                                           torch.cuda.current_stream().cuda_stream), "compress_in_place")
+    try:
+        d = _lib.hcmx_hmat_desc()
+        check(lib().hcmx_gpu_flat_desc(h, C.byref(d)), "flat_desc")
+        nl, nb, ns = int(d.nleaves), int(d.nbuffers), int(d.nsigma)
+        arr = lambda p_, n: np.ctypeslib.as_array(p_, shape=(n,)).copy() if n else np.zeros(0, np.int64)
+        desc = np.frombuffer(C.string_at(C.cast(d.desc, C.c_void_p), 16 * nb), dtype=DESC_DTYPE).copy()
+        blob = torch.empty(max(int(d.blob_bytes), 16), dtype=torch.uint8, device="cuda")
+        check(lib().hcmx_gpu_flat_copy_blob(h, ptr(blob), torch.cuda.current_stream().cuda_stream), "flat_copy_blob")
+        flat = FlatHMatrix(int(d.n_rows), int(d.n_cols), arr(d.row0, nl), arr(d.row1, nl), arr(d.col0, nl),
+                           arr(d.col1, nl), arr(d.kind, nl), arr(d.rank, nl), arr(d.buf0, nl), arr(d.sig0, nl),
+                           np.ctypeslib.as_array(d.sigma, shape=(ns,)).copy(), desc, arr(d.count, nb),
+                           arr(d.poff, nb), arr(d.plen, nb), blob,
+                           meta={"eps": eps, "mode": mode.name(), "dense_too": dense_too})
+    finally:
+        check(lib().hcmx_gpu_flat_destroy(h), "flat_destroy")
+    return flat
 
 
 def build_config(cfg, scheme="afl", device=None, n=None, seed=1, eps=None) -> tuple[FlatHMatrix, dict]:

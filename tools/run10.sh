@@ -1,0 +1,7 @@
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/tests_r2e.log 2>&1; tail -3 gpurun_out/tests_r2e.log
+timeout 1500 python bench.py > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo bench=$?; cat gpurun_out/bench_c4.json
+timeout 1500 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/ref_c4.json 2> gpurun_out/ref_c4.err; echo ref=$?; cat gpurun_out/ref_c4.json
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name regex:"^k_" -c 4000 --csv --log-file gpurun_out/launches_c4.csv \
+    python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-codec --no-rhs4 > gpurun_out/ncu_launch_c4.log 2>&1; echo launches=$?
+timeout 1200 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none -k regex:"k_phase|k_reduce" -c 3 --csv --log-file gpurun_out/dram_c4.csv \
+    python tools/prof_config.py 4 1 > gpurun_out/ncu_dram_c4.log 2>&1; echo dram=$?
