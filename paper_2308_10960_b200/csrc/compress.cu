@@ -351,12 +351,25 @@ void compress_in_place(const hcmx_assembled& A, double eps, int storage, int sch
         base[q] = total;
         total += pad16(part_bytes[q]);
     }
+    // the parts were sized for the worst case (FP64 words): keep only their used
+    // bytes before the blob is allocated, so the peak stays near the compressed size
+    for (size_t q = 0; q < parts.size(); ++q) {
+        if (parts[q].bytes > pad16(part_bytes[q]) + (64u << 20)) {
+            DevBuf tight(std::max<uint64_t>(16, part_bytes[q]));
+            if (part_bytes[q])
+                check_cuda(cudaMemcpyAsync(tight.p, parts[q].p, part_bytes[q], cudaMemcpyDeviceToDevice, s), "part copy");
+            stream_sync(s);
+            parts[q] = std::move(tight);
+        }
+    }
     f->blob.alloc(std::max<uint64_t>(16, total));
-    for (size_t q = 0; q < parts.size(); ++q)
+    for (size_t q = 0; q < parts.size(); ++q) {
         if (part_bytes[q])
             check_cuda(cudaMemcpyAsync(f->blob.as<uint8_t>() + base[q], parts[q].p, part_bytes[q], cudaMemcpyDeviceToDevice, s),
                        "blob copy");
-    stream_sync(s);
+        stream_sync(s);
+        parts[q].release();
+    }
     f->blob_bytes = total;
     for (uint64_t b = 0; b < nb; ++b) {
         if (part_of[b] < 0) throw std::logic_error("compress_in_place: buffer without payload");

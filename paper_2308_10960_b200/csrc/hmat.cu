@@ -105,6 +105,23 @@ constexpr int kSlotData = kStageMax + kSlack + kCoefBytes;  // stage + coefficie
 constexpr int kOffHdr = kSlotData;    // slot header written by the producer: stripe id, flags,
                                       // item claim counter (phase A), items
 constexpr int kSlotBytes = kOffHdr + 16;
+// phase A may use its own (smaller) stages: HCMX_STAGE_BYTES_A / HCMX_COEF_BYTES_A
+#ifndef HCMX_STAGE_BYTES_A
+#define HCMX_STAGE_BYTES_A HCMX_STAGE_BYTES
+#endif
+#ifndef HCMX_COEF_BYTES_A
+#define HCMX_COEF_BYTES_A 7936
+#endif
+constexpr int kStageBytesA = HCMX_STAGE_BYTES_A;
+constexpr int kStageMaxA = kMaxItems * kItemBytes + 64 + kStageBytesA;
+constexpr int kSlotDataA = kStageMaxA + kSlack + HCMX_COEF_BYTES_A;
+constexpr int kOffHdrA = kSlotDataA;
+constexpr int kSlotBytesA = kOffHdrA + 16;
+static_assert(kOffHdrA % 16 == 0 && kSlotBytesA % 16 == 0, "phase-A slot alignment");
+template <bool PHASE_A>
+__host__ __device__ constexpr int slot_bytes() { return PHASE_A ? kSlotBytesA : kSlotBytes; }
+template <bool PHASE_A>
+__host__ __device__ constexpr int off_hdr() { return PHASE_A ? kOffHdrA : kOffHdr; }
 constexpr int kR = 128;               // rows per phase-B CTA
 constexpr int kG = kR / 32;           // row groups (accumulators) per lane
 constexpr int kAChunk = 64;           // rows of a leaf's X columns per phase-A chunk
@@ -134,11 +151,11 @@ constexpr uint32_t kAItemXBytes = 12288;  // staged x slices per phase-A item
 #define HCMX_BITEM 8192
 #endif
 constexpr int kBLRGroup = HCMX_BGROUP;  // max columns per B item
-constexpr uint64_t kAStripeBytes = 8 * kStageBytes;  // target packed bytes per phase-A CTA
+constexpr uint64_t kAStripeBytes = 8 * 26624;  // target packed bytes per phase-A CTA
 constexpr uint64_t kItemTarget = 1536;          // packed bytes per item (columns grouped up to this)
 constexpr uint64_t kItemMaxBytes = HCMX_BITEM;  // items merge columns up to this many packed bytes
 constexpr size_t kRingBytes = static_cast<size_t>(kNStage) * kSlotBytes;
-constexpr size_t kRingBytesA = static_cast<size_t>(kNStageA) * kSlotBytes;
+constexpr size_t kRingBytesA = static_cast<size_t>(kNStageA) * kSlotBytesA;
 constexpr size_t kRedBytes = ((kNWB > HCMX_NWB_MULTI ? kNWB : HCMX_NWB_MULTI) / 2) * kR * sizeof(double);  // phase-B cross-warp reduction
 constexpr size_t kSmemBytes = kRingBytes + kRedBytes + 2 * kNStage * sizeof(uint64_t);  // + full, empty barriers
 constexpr size_t kSmemBytesA = kRingBytesA + 2 * kNStageA * sizeof(uint64_t);
@@ -556,9 +573,9 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
         const long long t0 = clk();
         if (it >= NS) mbar_wait(&empty[slot], phase);
         t_wait += clk() - t0;
-        uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
+        uint8_t* base = ring + static_cast<size_t>(slot) * slot_bytes<PHASE_A>();
         if (lane == 0) {
-            uint32_t* hdr = reinterpret_cast<uint32_t*>(base + kOffHdr);
+            uint32_t* hdr = reinterpret_cast<uint32_t*>(base + off_hdr<PHASE_A>());
             hdr[0] = cur.stripe;
             hdr[1] = cur.flags;
             hdr[2] = 0u;  // item claim counter
@@ -648,8 +665,8 @@ __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t*
         mbar_wait(&full[slot], phase);
         const long long t1 = clk();
         t_wait += t1 - t0;
-        const uint8_t* base = ring + static_cast<size_t>(slot) * kSlotBytes;
-        uint32_t* hdr = reinterpret_cast<uint32_t*>(ring + static_cast<size_t>(slot) * kSlotBytes + kOffHdr);
+        const uint8_t* base = ring + static_cast<size_t>(slot) * slot_bytes<DYN>();
+        uint32_t* hdr = reinterpret_cast<uint32_t*>(ring + static_cast<size_t>(slot) * slot_bytes<DYN>() + off_hdr<DYN>());
         const uint32_t stripe = hdr[0], flags = hdr[1];
         if (flags & kHdrEnd) {
             if (lane == 0) {
@@ -1795,7 +1812,7 @@ struct Builder {
             size_t end = pos;
             uint64_t bytes = 0;
             while (end < its.size() && end - pos < static_cast<size_t>(kMaxItems) &&
-                   bytes + its[end].bytes + kItemBytes * (end - pos + 1) <= static_cast<uint64_t>(kStageMax))
+                   bytes + its[end].bytes + kItemBytes * (end - pos + 1) <= static_cast<uint64_t>(kStageMaxA))
                 bytes += its[end++].bytes;
             if (end == pos) throw invalid_argument("hmat: phase-A item exceeds a stage");
             while (!try_stage_a(lanes, its, pos, end)) {  // too many x slices: one item fewer
@@ -1850,7 +1867,7 @@ struct Builder {
             copied += r16((x.end - x.start) * 8ull * R);
             coef += r16((x.end - x.start) * 8ull * R) + (x.pad ? 16u : 0u);
         }
-        if (coef > static_cast<uint32_t>(kSlotData) || merged.size() > static_cast<size_t>(kCopies)) return false;
+        if (coef > static_cast<uint32_t>(kSlotDataA) || merged.size() > static_cast<size_t>(kCopies)) return false;
         auto xoff = [&](const ALane& L) -> uint32_t {  // coef-area offset of x[xidx], in doubles
             const uint32_t pad = L.G > 1 ? 1u : 0u;
             for (const Slice& x : merged)
@@ -2143,7 +2160,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                 for (uint32_t i = 0; i < leafa[lr_id[l]].k; ++i)
                     xbytes_all += B.words_of(xbuf(l, i).first, d.col1[l] - d.col0[l]) * 4;
         const uint64_t stripe_target =
-            std::max<uint64_t>(2ull * kStageBytes, std::min<uint64_t>(kAStripeBytes, xbytes_all / (4ull * kCtasA * 148)));
+            std::max<uint64_t>(2ull * kStageBytesA, std::min<uint64_t>(kAStripeBytes, xbytes_all / (4ull * kCtasA * 148)));
         std::vector<uint32_t> pend;  // lowrank ids of the current stripe
         uint64_t stripe_bytes = 0;
         std::vector<ALane> lanes;

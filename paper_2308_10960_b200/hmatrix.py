@@ -202,6 +202,9 @@ def compress_in_place(A: Assembled, eps: float, mode: StorageMode | str = "afl-a
     a.sig_off = i64(np.maximum(A.sig_off, 0))
     h = C.c_void_p()
     rep = _lib.hcmx_memory_report()
+    # the library allocates with cudaMalloc: hand torch's cached (free) blocks back first
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     check(lib().hcmx_gpu_compress_in_place(C.byref(a), float(eps), _STORE[mode.kind], int(mode.scheme),
                                            int(bool(dense_too)), C.byref(h), C.byref(rep),
                                            torch.cuda.current_stream().cuda_stream), "compress_in_place")
@@ -431,3 +434,30 @@ class ComplexHMatrix:
 
     def matvec(self, alpha: complex, x, beta: complex, y):
         return self.matmat(alpha, x, beta, y)
+
+    def matmat_device(self, X: torch.Tensor, Y: torch.Tensor | None = None) -> torch.Tensor:
+        """Y = A X on the device for complex128 cuda X (n x r): blocks of two complex
+        columns go through both real 4-RHS arenas as [Re x1, Im x1, Re x2, Im x2]
+        (every packed field decoded once per block), and the real / imaginary
+        parts are combined on the device: Re y = Ar Re x - Ai Im x,
+        Im y = Ar Im x + Ai Re x.  Needs handles built with nrhs_block = 4."""
+        if X.dtype != torch.complex128 or not X.is_cuda or X.shape[0] != self.n_cols:
+            raise ValueError("matmat_device: complex128 cuda X with n_cols rows required")
+        r = X.shape[1]
+        n = self.n_rows
+        if Y is None:
+            Y = torch.empty(n, r, dtype=torch.complex128, device="cuda")
+        X4 = torch.zeros(self.n_cols, 4, dtype=torch.float64, device="cuda")
+        Pr = torch.empty(n, 4, dtype=torch.float64, device="cuda")
+        Pi = torch.empty_like(Pr)
+        for j in range(0, r, 2):
+            m = min(2, r - j)
+            X4.zero_()
+            X4[:, 0: 2 * m].copy_(torch.view_as_real(X[:, j: j + m]).reshape(self.n_cols, 2 * m))
+            self.re.matmat4_device(1.0, X4, 0.0, Pr)
+            self.im.matmat4_device(1.0, X4, 0.0, Pi)
+            for q in range(m):
+                yr = Pr[:, 2 * q] - Pi[:, 2 * q + 1]
+                yi = Pr[:, 2 * q + 1] + Pi[:, 2 * q]
+                Y[:, j + q] = torch.complex(yr, yi)
+        return Y

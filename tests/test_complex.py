@@ -71,3 +71,26 @@ def test_complex_multi_rhs_vs_oracle(gpu, oracle):
     H.matvec(1.0, X[:, 0], 0.0, y)
     assert np.linalg.norm(y - A @ X[:, 0]) / np.linalg.norm(A @ X[:, 0]) <= 1e-4
     H.close()
+
+
+@pytest.mark.gpu
+def test_complex_matmat_device_16_rhs(gpu, oracle):
+    """config 5's operation at reduced size: 16 complex right-hand sides through the
+    4-RHS arenas with the real / imaginary combination on the device, each column
+    equal to the oracle applied to the same compressed real / imaginary matrices"""
+    from paper_2308_10960_b200.hmatrix import ComplexHMatrix, build_config_complex
+    n = 4096
+    fr, fi, info = build_config_complex("5", n=n)
+    H = ComplexHMatrix(fr, fi)
+    rng = np.random.default_rng(12)
+    X = rng.uniform(-1, 1, (n, 16)) + 1j * rng.uniform(-1, 1, (n, 16))
+    Y = H.matmat_device(torch.as_tensor(X).cuda()).cpu().numpy()
+    frh, fih = fr.host(), fi.host()
+    for j in (0, 7, 15):
+        yr = oracle.hmat_matvec(frh, 1.0, X[:, j].real, 0.0, np.zeros(n), threads=4) - \
+            oracle.hmat_matvec(fih, 1.0, X[:, j].imag, 0.0, np.zeros(n), threads=4)
+        yi = oracle.hmat_matvec(frh, 1.0, X[:, j].imag, 0.0, np.zeros(n), threads=4) + \
+            oracle.hmat_matvec(fih, 1.0, X[:, j].real, 0.0, np.zeros(n), threads=4)
+        ref = yr + 1j * yi
+        assert np.linalg.norm(Y[:, j] - ref) <= TOL * np.linalg.norm(ref), j
+    H.close()

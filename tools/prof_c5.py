@@ -1,0 +1,79 @@
+"""BASELINE config 5 at size (profiling aid): Helmholtz exp(i kappa r)/(4 pi r),
+kappa = 16, n = 262144 sphere points, eps 1e-6, complex FP64, 16 right-hand
+sides through ComplexHMatrix.matmat_device (real / imaginary APLR H-matrices,
+4-RHS arenas, device combine).  Prints setup times, ms per 16-RHS product,
+FP64 TFLOP/s against the measured DFMA peak, and the parity of two columns
+against the CPU oracle (test infrastructure, not timed).
+
+    python tools/prof_c5.py [n]
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+from paper_2308_10960_b200.hmatrix import ComplexHMatrix, build_config_complex  # noqa: E402
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 262144
+    r = 16
+    t = time.time()
+    fr, fi, info = build_config_complex("5", n=n)
+    setup = time.time() - t
+    t = time.time()
+    H = ComplexHMatrix(fr, fi)
+    create = time.time() - t
+    rep_r, rep_i = H.re.memory(), H.im.memory()
+    rng = np.random.default_rng(5)
+    X = rng.uniform(-1, 1, (n, r)) + 1j * rng.uniform(-1, 1, (n, r))
+    Xd = torch.as_tensor(X).cuda()
+    Y = torch.empty(n, r, dtype=torch.complex128, device="cuda")
+    for _ in range(2):
+        H.matmat_device(Xd, Y)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        H.matmat_device(Xd, Y)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    # flops executed: two real H-matrices, each applied to 2r real columns, 2 flop per
+    # stored entry and column (the real arenas store the complex factors' re / im parts)
+    entries = (rep_r.uncompressed_equivalent + rep_i.uncompressed_equivalent) / 8
+    flops = 2.0 * entries * 2 * r
+    tf = flops / (ms / 1e3) / 1e12
+    pk = os.path.join(ROOT, "profiles", "r1_fp64_peak.json")
+    peak = json.load(open(pk)).get("fp64_fma_tflops") if os.path.exists(pk) else None
+    # bytes streamed per 16-RHS product: each real arena's algorithmic bytes per 4-RHS product x r/2 blocks
+    gbytes = (rep_r.algorithmic_bytes + rep_i.algorithmic_bytes) * (r // 2) / 1e9
+    from oracle import Oracle
+    o = Oracle()
+    frh, fih = fr.host(), fi.host()
+    Yh = Y.cpu().numpy()
+    errs = []
+    for j in (0, r - 1):
+        yr = o.hmat_matvec(frh, 1.0, X[:, j].real, 0.0, np.zeros(n), threads=os.cpu_count()) - \
+            o.hmat_matvec(fih, 1.0, X[:, j].imag, 0.0, np.zeros(n), threads=os.cpu_count())
+        yi = o.hmat_matvec(frh, 1.0, X[:, j].imag, 0.0, np.zeros(n), threads=os.cpu_count()) + \
+            o.hmat_matvec(fih, 1.0, X[:, j].real, 0.0, np.zeros(n), threads=os.cpu_count())
+        ref = yr + 1j * yi
+        errs.append(float(np.linalg.norm(Yh[:, j] - ref) / np.linalg.norm(ref)))
+    out = {"config": "5", "n": n, "nrhs": r, "leaves": info["leaves"], "setup_s": round(setup, 1),
+           "create_s": round(create, 1), "compressed_bytes_re_im": int(rep_r.algorithmic_bytes + rep_i.algorithmic_bytes),
+           "ms_per_16rhs_product": round(ms, 3), "fp64_tflops": round(tf, 2), "fp64_peak_tflops": peak,
+           "fp64_frac": round(tf / peak, 3) if peak else None, "streamed_gb_per_product": round(gbytes, 2),
+           "stream_gbs": round(gbytes / (ms / 1e3), 1), "parity_rel_err": errs}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
