@@ -14,6 +14,7 @@
 // rounded operations (__dmul_rn, __dadd_rn: the reference's Release build has no
 // FMA at codec.cpp:124), and 1/scale with IEEE division.  Decoding is
 // exact by construction ((1.mant * 2^off) - 1 is exact, one rounding in * scale).
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -23,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "internal.h"
@@ -116,6 +118,16 @@ namespace {
 constexpr unsigned kGroupsPerJob = 32;  // 1024 values per warp job
 constexpr uint64_t kFuseMax = 1ull << 17;  // fused compress: one warp per buffer up to this size
 constexpr int kWarpsPerBlock = 8;
+// occupancy knobs (resident CTAs per SM asked of ptxas) of the unpack and register-resident compress kernels
+#ifndef HCMX_UNPACK_MINB
+#define HCMX_UNPACK_MINB 1
+#endif
+#ifndef HCMX_COMPRESS_KIND
+#define HCMX_COMPRESS_KIND 0  // buffers <= 4096 values: 0 TMA-staged, 1 register-resident, 2 two-pass CTA
+#endif
+#ifndef HCMX_REG_MINB
+#define HCMX_REG_MINB 1
+#endif
 
 struct Job {
     uint32_t buf;
@@ -391,6 +403,79 @@ k_pack(const double* __restrict__ values, const uint64_t* __restrict__ voff,
     }
 }
 
+// The layout of one buffer from its reduced statistics (codec.cpp:62-101 with
+// the device log2; `ambiguous` flags an exponent width the host must re-decide
+// with glibc, see k_compress_cta), written by thread 0 as descriptor, stats and
+// flags.  Returns w, e, m and the scale through the references.
+__device__ __forceinline__ void cta_layout(uint64_t b, uint64_t mn, uint64_t mx, unsigned nz, unsigned nf, int scheme,
+                                           unsigned m_req, unsigned tid, hcmx_descriptor* __restrict__ desc,
+                                           hcmx_stats* __restrict__ stats, uint32_t* __restrict__ flags,
+                                           unsigned& e_out, unsigned& m_out, unsigned& w_out, double& scale_out) {
+    const bool all_zero = !nz;
+    const double dmin = all_zero ? 0.0 : bitsd(mn), dmax = all_zero ? 0.0 : bitsd(mx);
+    unsigned e = 2, ambiguous = 0;
+    if (scheme == HCMX_BFL) {
+        e = 8;
+    } else if (scheme == HCMX_DFL) {
+        e = 11;
+    } else if (!all_zero) {  // codec.cpp:69-75: e = ceil(log2(log2 max - log2 min + 2)), estimated
+        // log2 of each magnitude = exact binary exponent + MUFU log2 of the
+        // mantissa in [1, 2) (absolute error < 4e-7 each, subnormals through the
+        // libdevice log2); a value of vv within 1e-6 (relative) of a power of two
+        // 2^2..2^10 -- where the estimate could pick the other width -- is flagged
+        // and the host re-decides with glibc log2 exactly like the reference
+        auto lg = [](double x) -> double {
+            const uint32_t hi = static_cast<uint32_t>(__double2hiint(x));
+            const int be = static_cast<int>((hi >> 20) & 0x7ffu);
+            if (be == 0) return log2(x);  // subnormal (rare): the libdevice log2
+            const double mnt = __hiloint2double(static_cast<int>((hi & 0x000fffffu) | 0x3ff00000u), __double2loint(x));
+            return static_cast<double>(be - 1023) + static_cast<double>(__log2f(static_cast<float>(mnt)));
+        };
+        const double vv = (lg(dmax) - lg(dmin) + 1.0) + 1.0;
+        // ceil(log2(vv)) away from powers of two: the exponent of vv, plus 1
+        // unless vv = 2^k exactly.  Ambiguous: vv within 2^-16 (relative) of
+        // 2^2..2^10, read off the top 20 mantissa bits with integer ops (the
+        // estimate's error is < 2e-7 relative)
+        const uint32_t vh = static_cast<uint32_t>(__double2hiint(vv)), fr = vh & 0x000fffffu;
+        const int ve = static_cast<int>((vh >> 20) & 0x7ffu) - 1023;
+        const bool pow2 = fr == 0u && __double2loint(vv) == 0;
+        const int bits = pow2 ? ve : ve + 1;
+        e = static_cast<unsigned>(min(max(bits, 2), 11));
+        ambiguous = ((fr < 16u && ve >= 2 && ve <= 10) || (fr >= 0xffff0u && ve >= 1 && ve <= 9)) ? 1u : 0u;
+    }
+    unsigned m = m_req;
+    const unsigned unit = scheme == HCMX_AFL ? 1u : (scheme == HCMX_DFL ? 16u : 8u);
+    if (scheme != HCMX_AFL) {  // codec.cpp:25-30
+        unsigned w0 = 1 + e + m;
+        w0 += (unit - w0 % unit) % unit;
+        m = min(52u, w0 - 1 - e);
+    }
+    unsigned w = 1 + e + m;
+    w += (unit - w % unit) % unit;
+    const double scale = all_zero ? 1.0 : dmin;
+    if (tid == 0) {
+        hcmx_descriptor d;
+        d.scheme = static_cast<uint8_t>(scheme);
+        d.exp_bits = static_cast<uint8_t>(e);
+        d.mant_bits = static_cast<uint8_t>(m);
+        d.bit_width = static_cast<uint8_t>(w);
+        d.reserved = 0;
+        d.scale = scale;
+        desc[b] = d;
+        hcmx_stats st;
+        st.min_mag = dmin;
+        st.max_mag = dmax;
+        st.all_zero = all_zero ? 1u : 0u;
+        st.non_finite = nf;
+        if (stats) stats[b] = st;
+        flags[b] = ambiguous | (nf ? 2u : 0u);  // bit 1: non-finite input (rejected)
+    }
+    e_out = e;
+    m_out = m;
+    w_out = w;
+    scale_out = scale;
+}
+
 // codec.cpp:142-144 fused per buffer, one CTA of kCtaWarps warps per buffer:
 // pass 1 (min/max, every thread, 8 loads in flight), block reduction, the
 // layout rules, pass 2 packs groups warp-strided (the values come back from
@@ -465,50 +550,9 @@ k_compress_cta(const double* __restrict__ values, const uint64_t* __restrict__ v
         }
         const uint64_t mn = mnm1 + 1;
         __syncthreads();  // s_* reused by the next buffer
-        const bool all_zero = !nz;
-        const double dmin = all_zero ? 0.0 : bitsd(mn), dmax = all_zero ? 0.0 : bitsd(mx);
-        unsigned e = 2, ambiguous = 0;
-        if (scheme == HCMX_BFL) {
-            e = 8;
-        } else if (scheme == HCMX_DFL) {
-            e = 11;
-        } else if (!all_zero) {  // codec.cpp:69-75 with the device log2
-            const double span = log2(dmax) - log2(dmin) + 1.0;
-            const double vv = span + 1.0;
-            const double bits = ceil(log2(vv));
-            e = static_cast<unsigned>(fmin(fmax(bits, 2.0), 11.0));
-            for (int k = 2; k <= 10; ++k) {
-                const double pk = ldexp(1.0, k);
-                if (fabs(vv - pk) <= pk * 1e-9) ambiguous = 1;
-            }
-        }
-        unsigned m = m_req;
-        const unsigned unit = scheme == HCMX_AFL ? 1u : (scheme == HCMX_DFL ? 16u : 8u);
-        if (scheme != HCMX_AFL) {  // codec.cpp:25-30
-            unsigned w0 = 1 + e + m;
-            w0 += (unit - w0 % unit) % unit;
-            m = min(52u, w0 - 1 - e);
-        }
-        unsigned w = 1 + e + m;
-        w += (unit - w % unit) % unit;
-        const double scale = all_zero ? 1.0 : dmin;
-        if (tid == 0) {
-            hcmx_descriptor d;
-            d.scheme = static_cast<uint8_t>(scheme);
-            d.exp_bits = static_cast<uint8_t>(e);
-            d.mant_bits = static_cast<uint8_t>(m);
-            d.bit_width = static_cast<uint8_t>(w);
-            d.reserved = 0;
-            d.scale = scale;
-            desc[b] = d;
-            hcmx_stats st;
-            st.min_mag = dmin;
-            st.max_mag = dmax;
-            st.all_zero = all_zero ? 1u : 0u;
-            st.non_finite = nf;
-            if (stats) stats[b] = st;
-            flags[b] = ambiguous | (nf ? 2u : 0u);  // bit 1: non-finite input (rejected)
-        }
+        unsigned e, m, w;
+        double scale;
+        cta_layout(b, mn, mx, nz, nf, scheme, m_req, tid, desc, stats, flags, e, m, w, scale);
         if (nf) continue;
         if (w <= 32)
             pack_groups32(v, n32, warp, (n32 + 31) / 32, e, m, w, scale,
@@ -516,6 +560,393 @@ k_compress_cta(const double* __restrict__ values, const uint64_t* __restrict__ v
         else
             pack_groups(v, n, warp, static_cast<uint32_t>((n + 31) / 32), e, m, w, scale,
                         reinterpret_cast<uint32_t*>(payload + poff[b]), lane, kCtaWarps);
+    }
+}
+
+// The same for buffers of <= kRegMax values (config 2's 64 x 64 blocks): one
+// CTA of kCtaWarps warps per buffer, every value loaded exactly once into
+// registers (lane l of warp q holds values 32 g + l of groups g = q, q + 4, ...,
+// all loads in flight together), the statistics reduced from the registers,
+// then encoded and packed from the same registers (no second pass over HBM or
+// L2).  Grid: the resident CTAs of the device, buffers strided over them.
+constexpr int kRegJ = 32;                                  // values per thread
+constexpr uint64_t kRegMax = uint64_t(kRegJ) * kCtaWarps * 32;  // 4096
+
+template <bool ZSEL = true>
+__device__ __forceinline__ uint32_t encode32(double x, double inv_scale, uint64_t round_add, bool m_lo, unsigned msh,
+                                             uint32_t mant_mask, uint32_t max_offset, unsigned sgn_sh, unsigned m) {
+    // the field arithmetic of encode_value in 32 bits.  Zeros keep only their
+    // sign: with a finite 1 / scale a zero already encodes to offset 0, mantissa
+    // 0 (vp = 1.0 exactly), so the select is needed (ZSEL) only when 1 / scale
+    // is infinite (a subnormal scale: 0 * inf is NaN)
+    const uint32_t sign = static_cast<uint32_t>(__double2hiint(x)) >> 31;
+    const double vp = __dadd_rn(__dmul_rn(fabs(x), inv_scale), 1.0);  // no FMA (codec.cpp:124)
+    const uint64_t u = dbits(vp) + round_add;
+    const uint32_t uh = static_cast<uint32_t>(u >> 32), ul = static_cast<uint32_t>(u);
+    uint32_t offset = (uh >> 20) - 1023u;
+    uint32_t mant = (m_lo ? uh >> msh : __funnelshift_r(ul, uh, msh)) & mant_mask;
+    const bool sat = offset > max_offset || static_cast<uint32_t>(__double2hiint(vp)) >= 0x7ff00000u;
+    offset = sat ? max_offset : offset;
+    mant = sat ? mant_mask : mant;
+    if (ZSEL) return (sign << sgn_sh) | (x != 0.0 ? (offset << m) | mant : 0u);
+    return (sign << sgn_sh) | (offset << m) | mant;
+}
+
+__global__ void __launch_bounds__(kCtaWarps * 32, HCMX_REG_MINB)
+k_compress_reg(const double* __restrict__ values, const uint64_t* __restrict__ voff,
+               const uint64_t* __restrict__ count, uint64_t nbuf, int scheme, unsigned m_req,
+               const uint64_t* __restrict__ poff, uint8_t* __restrict__ payload,
+               hcmx_descriptor* __restrict__ desc, hcmx_stats* __restrict__ stats,
+               uint32_t* __restrict__ flags) {
+    __shared__ uint64_t s_mn[kCtaWarps], s_mx[kCtaWarps];
+    __shared__ unsigned s_nz[kCtaWarps], s_nf[kCtaWarps];
+    __shared__ uint32_t s_words[kCtaWarps][4][36];
+    const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    uint32_t* sw = &s_words[warp][0][0];
+    for (uint64_t b = blockIdx.x; b < nbuf; b += gridDim.x) {
+        const uint32_t n = static_cast<uint32_t>(count[b]);  // <= kRegMax
+        const double* v = values + voff[b];
+        const uint32_t ngroups = (n + 31) / 32, nfull = n / 32;
+        double xs[kRegJ];
+        if (n == kRegMax) {
+#pragma unroll
+            for (int j = 0; j < kRegJ; ++j) xs[j] = __ldcs(v + (warp + kCtaWarps * j) * 32 + lane);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kRegJ; ++j) {
+                const uint32_t idx = (warp + kCtaWarps * j) * 32 + lane;
+                xs[j] = idx < n ? __ldcs(v + idx) : 0.0;
+            }
+        }
+        uint64_t mnm1 = ~0ull, mx = 0;
+        uint32_t orv = 0;
+#pragma unroll
+        for (int j = 0; j < kRegJ; ++j) {
+            const uint64_t a = dbits(xs[j]) & 0x7fffffffffffffffull;
+            orv |= static_cast<uint32_t>(a >> 32) | static_cast<uint32_t>(a);
+            const uint64_t am1 = a - 1;
+            mnm1 = am1 < mnm1 ? am1 : mnm1;
+            mx = a > mx ? a : mx;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t omn = __shfl_xor_sync(0xffffffffu, mnm1, o);
+            const uint64_t omx = __shfl_xor_sync(0xffffffffu, mx, o);
+            mnm1 = omn < mnm1 ? omn : mnm1;
+            mx = omx > mx ? omx : mx;
+        }
+        unsigned nz = __any_sync(0xffffffffu, orv != 0);
+        unsigned nf = mx >= 0x7FF0000000000000ull ? 1u : 0u;
+        if (lane == 0) {
+            s_mn[warp] = mnm1;
+            s_mx[warp] = mx;
+            s_nz[warp] = nz;
+            s_nf[warp] = nf;
+        }
+        __syncthreads();
+        mnm1 = s_mn[0];
+        mx = s_mx[0];
+        nz = s_nz[0];
+        nf = s_nf[0];
+#pragma unroll
+        for (int q = 1; q < kCtaWarps; ++q) {
+            mnm1 = s_mn[q] < mnm1 ? s_mn[q] : mnm1;
+            mx = s_mx[q] > mx ? s_mx[q] : mx;
+            nz |= s_nz[q];
+            nf |= s_nf[q];
+        }
+        __syncthreads();  // s_* reused by the next buffer
+        unsigned e, m, w;
+        double scale;
+        cta_layout(b, mnm1 + 1, mx, nz, nf, scheme, m_req, tid, desc, stats, flags, e, m, w, scale);
+        if (nf) continue;
+        uint32_t* out = reinterpret_cast<uint32_t*>(payload + poff[b]);
+        if (w > 32) {  // 64-bit fields: the streaming packer (values come back from L2)
+            pack_groups(v, n, warp, ngroups, e, m, w, scale, out, lane, kCtaWarps);
+            continue;
+        }
+        const double inv_scale = 1.0 / scale;  // IEEE division (codec.cpp:107)
+        const uint32_t max_offset = (1u << e) - 1u;
+        const uint64_t round_add = 1ull << (51 - m);
+        const uint32_t mant_mask = (1u << m) - 1u;
+        const bool m_lo = m <= 20;
+        const unsigned msh = m_lo ? 20u - m : 52u - m;
+        const unsigned bit = lane * w, q = bit >> 5, sh = bit & 31u;
+#pragma unroll
+        for (int j4 = 0; j4 < kRegJ; j4 += 4) {
+            const uint32_t gb = warp + kCtaWarps * j4;  // group of round element 0
+            if (gb >= ngroups) break;
+            uint32_t f[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                f[i] = encode32(xs[j4 + i], inv_scale, round_add, m_lo, msh, mant_mask, max_offset, e + m, m);
+                sw[i * 36 + lane] = 0u;
+                if (lane == 0) sw[i * 36 + 32] = 0u;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                // zeros past n encode to 0 (ORing them is harmless)
+                atomicOr(sw + i * 36 + q, f[i] << sh);
+                atomicOr(sw + i * 36 + q + 1, __funnelshift_l(f[i], 0u, sh));
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t g = gb + kCtaWarps * i;
+                if (g < nfull) {
+                    if (lane < w) __stcs(out + g * w + lane, sw[i * 36 + lane]);
+                } else if (g < ngroups) {
+                    const unsigned nwords = ((n - g * 32) * w + 31) / 32;
+                    if (lane < nwords) __stcs(out + g * w + lane, sw[i * 36 + lane]);
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// The same for buffers of <= kRegMax values, with the buffer staged in shared
+// memory by one bulk copy (TMA engine) into a 2-slot ring: the copy of the
+// CTA's next buffer is in flight while the current one is analysed, encoded
+// and packed from shared memory, so the CTA never waits on HBM after its first
+// buffer.  Per buffer: statistics (every warp) | barrier | layout (warp 0:
+// exponent-width estimate, 1 / scale, descriptor) | barrier | encode + pack.
+// Buffers whose values are not 16-byte aligned are copied by the threads
+// instead (same results).  (Measured and rejected: register-resident values,
+// 4 / 16 warps, a 3-slot ring with the layout overlapped by the next buffer's
+// statistics -- 2 CTAs per SM instead of 3 lose more than the overlap gains.)
+#ifndef HCMX_TMA_WARPS
+#define HCMX_TMA_WARPS 8
+#endif
+constexpr int kTmaWarps = HCMX_TMA_WARPS;
+constexpr uint32_t kTmaSlotBytes = static_cast<uint32_t>(kRegMax) * 8;  // 32 KB
+constexpr size_t kTmaSmem = 2 * size_t(kTmaSlotBytes) + 16;               // 2 slots + 2 mbarriers
+
+__device__ __forceinline__ uint32_t cx_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ bool cx_try_wait(uint64_t* bar, unsigned parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(cx_smem(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+// 64-bit unsigned min / max over the warp with the 32-bit REDUX unit: the
+// high words first, then the low words of the lanes holding that high word
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+    const uint32_t hi = static_cast<uint32_t>(v >> 32), lo = static_cast<uint32_t>(v);
+    const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+    const uint32_t ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+    return (static_cast<uint64_t>(mh) << 32) | ml;
+}
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+    const uint32_t hi = static_cast<uint32_t>(v >> 32), lo = static_cast<uint32_t>(v);
+    const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+    const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    return (static_cast<uint64_t>(mh) << 32) | ml;
+}
+
+__global__ void __launch_bounds__(kTmaWarps * 32)
+k_compress_tma(const double* __restrict__ values, const uint64_t* __restrict__ voff,
+               const uint64_t* __restrict__ count, uint64_t nbuf, int scheme, unsigned m_req,
+               const uint64_t* __restrict__ poff, uint8_t* __restrict__ payload,
+               hcmx_descriptor* __restrict__ desc, hcmx_stats* __restrict__ stats,
+               uint32_t* __restrict__ flags) {
+    extern __shared__ __align__(128) uint8_t cx_smem_buf[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(cx_smem_buf + 2 * kTmaSlotBytes);
+    __shared__ uint64_t s_mn[kTmaWarps], s_mx[kTmaWarps];
+    __shared__ unsigned s_nz[kTmaWarps], s_nf[kTmaWarps], s_manual[2];
+    __shared__ struct {
+        unsigned e, m, w, nf;
+        double scale, inv;
+    } s_par;
+    __shared__ __align__(16) uint32_t s_words[kTmaWarps][4 * 32 + 4];
+    const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    constexpr unsigned T = kTmaWarps * 32;
+    uint32_t* sw = &s_words[warp][0];
+    for (unsigned i = lane; i < 4 * 32 + 4; i += 32) sw[i] = 0u;  // kept zero between rounds (read-and-clear)
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cx_smem(bar + i)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // thread 0: start the copy of a buffer of n values at src into slot sl (or
+    // flag it for a thread copy)
+    auto issue = [&](uint64_t n, const double* src, unsigned sl) {
+        const unsigned bytes = static_cast<unsigned>(n * 8);
+        const bool bulk = ((reinterpret_cast<uintptr_t>(src) | bytes) & 15u) == 0 && bytes;
+        s_manual[sl] = bulk ? 0u : 1u;
+        const uint32_t bs = cx_smem(bar + sl);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bs), "r"(bulk ? bytes : 0u)
+                     : "memory");
+        if (bulk)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    cx_smem(cx_smem_buf + sl * kTmaSlotBytes)),
+                "l"(src), "r"(bytes), "r"(bs)
+                : "memory");
+    };
+    uint64_t b = blockIdx.x;
+    if (b < nbuf && tid == 0) issue(count[b], values + voff[b], 0);
+    for (uint32_t it = 0; b < nbuf; ++it, b += gridDim.x) {
+        const unsigned sl = it & 1u, par = (it >> 1) & 1u;
+        // the index loads this iteration needs later, issued before the waits
+        // (no dependent global load on the path after a barrier)
+        const uint32_t n = static_cast<uint32_t>(count[b]);  // <= kRegMax
+        uint32_t* out = reinterpret_cast<uint32_t*>(payload + poff[b]);
+        const bool has_next = b + gridDim.x < nbuf;
+        uint64_t nx_n = 0;
+        const double* nx_src = values;
+        if (tid == 0 && has_next) {
+            nx_n = count[b + gridDim.x];
+            nx_src = values + voff[b + gridDim.x];
+        }
+        while (!cx_try_wait(bar + sl, par)) {
+        }
+        double* xs = reinterpret_cast<double*>(cx_smem_buf + sl * kTmaSlotBytes);
+        if (s_manual[sl]) {  // unaligned source: the threads copy it
+            const double* v = values + voff[b];
+            for (uint32_t i = tid; i < n; i += T) xs[i] = __ldcs(v + i);
+            __syncthreads();
+        }
+        uint64_t mnm1 = ~0ull, mx = 0;
+        uint32_t orv = 0;
+        for (uint32_t i = tid; i < n; i += T) {
+            const uint64_t a = dbits(xs[i]) & 0x7fffffffffffffffull;
+            orv |= static_cast<uint32_t>(a >> 32) | static_cast<uint32_t>(a);
+            const uint64_t am1 = a - 1;
+            mnm1 = am1 < mnm1 ? am1 : mnm1;
+            mx = a > mx ? a : mx;
+        }
+        mnm1 = warp_min_u64(mnm1);
+        mx = warp_max_u64(mx);
+        unsigned nz = __any_sync(0xffffffffu, orv != 0);
+        unsigned nf = mx >= 0x7FF0000000000000ull ? 1u : 0u;
+        if (lane == 0) {
+            s_mn[warp] = mnm1;
+            s_mx[warp] = mx;
+            s_nz[warp] = nz;
+            s_nf[warp] = nf;
+        }
+        __syncthreads();
+        // every thread is past iteration it - 1 (it reached this barrier): slot
+        // sl ^ 1 is free, start the copy of the CTA's next buffer into it
+        if (tid == 0 && has_next) issue(nx_n, nx_src, sl ^ 1u);
+        __syncwarp();  // warp 0 reconverged before its shuffles
+        if (warp == 0) {  // the layout once per buffer (one warp), broadcast through shared memory
+            // the warps' partial statistics: a shuffle tree over lanes 0..kTmaWarps-1
+            const unsigned q = lane < kTmaWarps ? lane : 0u;
+            mnm1 = warp_min_u64(s_mn[q]);
+            mx = warp_max_u64(s_mx[q]);
+            nz = __reduce_or_sync(0xffffffffu, s_nz[q]);
+            nf = __reduce_or_sync(0xffffffffu, s_nf[q]);
+            // 1 / scale first: its Newton chain overlaps the width selection
+            const double inv = 1.0 / (nz ? bitsd(mnm1 + 1) : 1.0);  // IEEE division (codec.cpp:107)
+            unsigned e, m, w;
+            double scale;
+            cta_layout(b, mnm1 + 1, mx, nz, nf, scheme, m_req, tid, desc, stats, flags, e, m, w, scale);
+            if (lane == 0) {
+                s_par.e = e;
+                s_par.m = m;
+                s_par.w = w;
+                s_par.nf = nf;
+                s_par.scale = scale;
+                s_par.inv = inv;
+            }
+        }
+        __syncthreads();
+        const unsigned e = s_par.e, m = s_par.m, w = s_par.w;
+        const double scale = s_par.scale;
+        if (s_par.nf) continue;
+        const uint32_t ngroups = (n + 31) / 32, nfull = n / 32;
+        if (w > 32) {  // 64-bit fields: the streaming packer (values re-read from global memory)
+            pack_groups(values + voff[b], n, warp, ngroups, e, m, w, scale, out, lane, kTmaWarps);
+            continue;
+        }
+        const double inv_scale = s_par.inv;
+        const uint32_t max_offset = (1u << e) - 1u;
+        const uint64_t round_add = 1ull << (51 - m);
+        const uint32_t mant_mask = (1u << m) - 1u;
+        const bool m_lo = m <= 20;
+        const unsigned msh = m_lo ? 20u - m : 52u - m;
+        const unsigned bit = lane * w, q = bit >> 5, sh = bit & 31u;
+        const bool vec_ok = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+        // Z: zeros need the select (1 / scale infinite); HI: m <= 19, the
+        // rounding increment 2^(51 - m) lies in the high word (no carry from the
+        // low word), so the field comes from the high word alone
+        auto pack = [&](auto zsel, auto hisel) {
+            constexpr bool Z = decltype(zsel)::value, HI = decltype(hisel)::value;
+            const uint32_t radd_hi = HI ? (1u << (19 - m)) : 0u;
+            auto enc = [&](double x) -> uint32_t {
+                if (!HI) return encode32<Z>(x, inv_scale, round_add, m_lo, msh, mant_mask, max_offset, e + m, m);
+                const uint32_t sign = static_cast<uint32_t>(__double2hiint(x)) >> 31;
+                const double vp = __dadd_rn(__dmul_rn(fabs(x), inv_scale), 1.0);  // no FMA (codec.cpp:124)
+                const uint32_t uh = static_cast<uint32_t>(__double2hiint(vp)) + radd_hi;
+                uint32_t offset = (uh >> 20) - 1023u;
+                uint32_t mant = (uh >> msh) & mant_mask;
+                const bool sat = offset > max_offset || static_cast<uint32_t>(__double2hiint(vp)) >= 0x7ff00000u;
+                offset = sat ? max_offset : offset;
+                mant = sat ? mant_mask : mant;
+                if (Z) return (sign << (e + m)) | (x != 0.0 ? (offset << m) | mant : 0u);
+                return (sign << (e + m)) | (offset << m) | mant;
+            };
+            // a round: four ADJACENT groups 4j..4j+3 (their 4w packed words are
+            // contiguous in the output, 16-byte aligned), packed into the warp's
+            // word buffer and stored as w 16-byte vectors
+            for (uint32_t g4 = 4 * warp; g4 < ngroups; g4 += 4 * kTmaWarps) {
+                uint32_t f[4];
+                const bool whole = g4 + 3 < nfull;  // four whole groups (warp-uniform)
+                if (whole) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) f[i] = enc(xs[(g4 + i) * 32 + lane]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t idx = (g4 + i) * 32 + lane;
+                        f[i] = enc(idx < n ? xs[idx] : 0.0);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    // words >= 4w only ever receive zero high parts, so the words
+                    // a round reads back are the only ones it must clear
+                    atomicOr(sw + i * w + q, f[i] << sh);
+                    atomicOr(sw + i * w + q + 1, __funnelshift_l(f[i], 0u, sh));
+                }
+                __syncwarp();
+                uint32_t* o = out + g4 * w;
+                if (whole && vec_ok) {
+                    if (lane < w) {
+                        uint4* sv = reinterpret_cast<uint4*>(sw) + lane;
+                        const uint4 v4 = *sv;
+                        *sv = make_uint4(0u, 0u, 0u, 0u);
+                        __stcs(reinterpret_cast<uint4*>(o) + lane, v4);
+                    }
+                } else {
+                    const uint32_t nw = static_cast<uint32_t>(umin64(4ull * w, ((uint64_t)(n - g4 * 32) * w + 31) / 32));
+                    for (uint32_t k = lane; k < 4 * w; k += 32) {
+                        const uint32_t word = sw[k];
+                        sw[k] = 0u;
+                        if (k < nw) __stcs(o + k, word);
+                    }
+                }
+                __syncwarp();
+            }
+        };
+        const bool inf = isinf(inv_scale);
+        if (m <= 19) {
+            if (inf) pack(std::true_type{}, std::true_type{});
+            else pack(std::false_type{}, std::true_type{});
+        } else {
+            if (inf) pack(std::true_type{}, std::false_type{});
+            else pack(std::false_type{}, std::false_type{});
+        }
     }
 }
 
@@ -536,14 +967,16 @@ __device__ __forceinline__ double decode_field(uint64_t field, unsigned e, unsig
 
 // Job-free unpacking: warp chunks of 32 groups (1024 values); chunk c belongs
 // to the buffer found by binary search over coff (cumulative chunks per
-// buffer).  A chunk's packed words are first copied to a per-warp shared
-// buffer with 16-byte loads (all in flight at once: the warp's memory-level
-// parallelism), then every lane decodes its field of each group from shared
-// memory and the doubles are stored coalesced.  w > 32 goes in two halves.
+// buffer).  A piece of a chunk (all of it for w <= 32, half for w > 32) is
+// loaded with 16-byte loads into registers, parked in a per-warp shared
+// buffer, and decoded from there while the loads of the warp's NEXT piece are
+// already in flight (software pipelining: every warp keeps one piece of
+// loads outstanding through its decode and store phase); the doubles are
+// stored coalesced with streaming stores.
 constexpr int kUnpackWarps = 8;
 constexpr unsigned kStageWords = 1024;  // per warp: 16 groups at w <= 64, 32 at w <= 32
 
-// per-chunk metadata, loaded one chunk ahead
+// per-chunk metadata, loaded one chunk ahead of the prefetched piece
 struct ChunkMeta {
     hcmx_descriptor d;
     uint64_t n, poff, voff, c0;
@@ -561,7 +994,32 @@ __device__ __forceinline__ ChunkMeta chunk_meta(uint64_t c, const uint32_t* cbuf
     return m;
 }
 
-__global__ void __launch_bounds__(kUnpackWarps * 32)
+// groups [g0, g1) of the piece of chunk c starting at group g0, and its 16-byte vectors
+struct Piece {
+    uint32_t g0, g1, nvec;
+};
+__device__ __forceinline__ Piece piece_of(const ChunkMeta& m, uint64_t c, uint32_t g0) {
+    const unsigned w = m.d.bit_width;
+    const uint64_t ngroups = (m.n + 31) / 32, nwords_all = (m.n * w + 31) / 32;
+    const uint32_t gc1 = static_cast<uint32_t>(umin64((c - m.c0) * 32 + 32, ngroups));
+    Piece pc;
+    pc.g0 = g0;
+    pc.g1 = min(g0 + (w > 32 ? 16u : 32u), gc1);
+    const uint64_t wb = (uint64_t)g0 * w, we = umin64((uint64_t)pc.g1 * w, nwords_all);
+    pc.nvec = static_cast<unsigned>((we - wb + 3) / 4);  // the slot is 16-byte padded
+    return pc;
+}
+__device__ __forceinline__ void piece_load(const uint8_t* payload, const ChunkMeta& m, const Piece& pc,
+                                           unsigned lane, uint4 (&r)[8]) {
+    const uint4* src = reinterpret_cast<const uint4*>(payload + m.poff) + (uint64_t)pc.g0 * m.d.bit_width / 4;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const unsigned i = lane + 32u * u;
+        if (i < pc.nvec) r[u] = __ldcs(src + i);
+    }
+}
+
+__global__ void __launch_bounds__(kUnpackWarps * 32, HCMX_UNPACK_MINB)
 k_unpack_chunks(const uint8_t* __restrict__ payload, const uint64_t* __restrict__ poff,
                 const uint64_t* __restrict__ count, const hcmx_descriptor* __restrict__ desc,
                 const uint64_t* __restrict__ voff, const uint64_t* __restrict__ coff,
@@ -571,76 +1029,102 @@ k_unpack_chunks(const uint8_t* __restrict__ payload, const uint64_t* __restrict_
     uint32_t* sw = stage[warp];
     const uint64_t gw = blockIdx.x * (uint64_t)kUnpackWarps + warp;
     const uint64_t nw = gridDim.x * (uint64_t)kUnpackWarps;
-    ChunkMeta next{};
-    if (gw < nchunks) next = chunk_meta(gw, cbuf, coff, desc, count, poff, voff);
-    for (uint64_t c = gw; c < nchunks; c += nw) {
-        const ChunkMeta cm = next;
-        if (c + nw < nchunks) next = chunk_meta(c + nw, cbuf, coff, desc, count, poff, voff);
+    if (gw >= nchunks) return;
+    // the prefetched piece (chunk pc_c, meta pm, groups pp) and the meta of the chunk after it
+    uint64_t pc_c = gw;
+    ChunkMeta pm = chunk_meta(gw, cbuf, coff, desc, count, poff, voff), nm{};
+    Piece pp = piece_of(pm, gw, static_cast<uint32_t>((gw - pm.c0) * 32));
+    uint4 r[8];
+    piece_load(payload, pm, pp, lane, r);
+    if (gw + nw < nchunks) nm = chunk_meta(gw + nw, cbuf, coff, desc, count, poff, voff);
+    for (;;) {
+        const ChunkMeta cm = pm;
+        const Piece cp = pp;
+        const uint64_t c = pc_c;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const unsigned i = lane + 32u * u;
+            if (i < cp.nvec) reinterpret_cast<uint4*>(sw)[i] = r[u];
+        }
+        __syncwarp();
+        // issue the next piece's loads before decoding this one
+        bool more = true;
+        const uint32_t gc1 = static_cast<uint32_t>(umin64((c - cm.c0) * 32 + 32, (cm.n + 31) / 32));
+        if (cp.g1 < gc1) {  // second half of a w > 32 chunk
+            pp = piece_of(cm, c, cp.g1);
+            piece_load(payload, pm, pp, lane, r);
+        } else if (c + nw < nchunks) {
+            pc_c = c + nw;
+            pm = nm;
+            pp = piece_of(pm, pc_c, static_cast<uint32_t>((pc_c - pm.c0) * 32));
+            piece_load(payload, pm, pp, lane, r);
+            if (pc_c + nw < nchunks) nm = chunk_meta(pc_c + nw, cbuf, coff, desc, count, poff, voff);
+        } else {
+            more = false;
+        }
         const hcmx_descriptor d = cm.d;
         const unsigned e = d.exp_bits, m = d.mant_bits, w = d.bit_width;
         const uint64_t n = cm.n;
-        const uint32_t* p = reinterpret_cast<const uint32_t*>(payload + cm.poff);
         double* o = out + cm.voff;
-        const uint64_t ngroups = (n + 31) / 32, nwords_all = (n * w + 31) / 32;
-        const uint32_t gc0 = static_cast<uint32_t>((c - cm.c0) * 32);
-        const uint32_t gc1 = static_cast<uint32_t>(umin64(gc0 + 32, ngroups));
-        const uint32_t step = w > 32 ? 16u : 32u;
+        const uint32_t g0 = cp.g0, g1 = cp.g1;
         const unsigned bit = lane * w, q = bit >> 5, sh = bit & 31u;
         const uint64_t wmask = (w == 64) ? ~0ull : ((1ull << w) - 1);
-        for (uint32_t g0 = gc0; g0 < gc1; g0 += step) {
-            const uint32_t g1 = min(g0 + step, gc1);
-            const uint64_t wb = (uint64_t)g0 * w, we = umin64((uint64_t)g1 * w, nwords_all);
-            const unsigned nvec = static_cast<unsigned>((we - wb + 3) / 4);  // the slot is 16-byte padded
-            const uint4* src = reinterpret_cast<const uint4*>(p + wb);
-            uint4 r[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const unsigned i = lane + 32u * u;
-                if (i < nvec) r[u] = __ldcs(src + i);
+        if (w <= 32 && e <= 10 && w == 1 + e + m) {
+            // 32-bit fields, no 2046 clamp: the double is built with integer ops
+            // (exactly the codec's bits - 1.0, one rounding in * scale)
+            const uint32_t mask = 0xffffffffu >> (33u - w);
+            const bool lo_m = m <= 20;
+            const unsigned s1 = lo_m ? 20u - m : m - 20u;
+            const uint32_t nfull = static_cast<uint32_t>(umin64(g1, n / 32));
+            uint32_t g = g0;
+#pragma unroll 4
+            for (; g < nfull; ++g) {
+                const uint32_t* gp = sw + (g - g0) * w + q;
+                const uint32_t t = __funnelshift_r(gp[0], gp[1], sh);
+                const uint32_t pay = t & mask;
+                const uint32_t hi = (lo_m ? pay << s1 : pay >> s1) + (1023u << 20);
+                const uint32_t lo = lo_m ? 0u : pay << (32u - s1);
+                const double v = __dmul_rn(__hiloint2double(hi, lo) - 1.0, d.scale);
+                const double sv = __hiloint2double(__double2hiint(v) ^ ((t << (32u - w)) & 0x80000000u),
+                                                   __double2loint(v));
+                __stcs(o + (uint64_t)g * 32 + lane, sv);
             }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const unsigned i = lane + 32u * u;
-                if (i < nvec) reinterpret_cast<uint4*>(sw)[i] = r[u];
+            for (; g < g1; ++g) {  // ragged last group
+                const uint32_t* gp = sw + (g - g0) * w + q;
+                uint64_t win = ((uint64_t)gp[1] << 32 | gp[0]) >> sh;
+                const uint64_t idx = (uint64_t)g * 32 + lane;
+                if (idx < n) __stcs(o + idx, decode_field(win & wmask, e, m, d.scale));
             }
-            __syncwarp();
-            if (w <= 32 && e <= 10 && w == 1 + e + m) {
-                // 32-bit fields, no 2046 clamp: the double is built with integer ops
-                // (exactly the codec's bits - 1.0, one rounding in * scale)
-                const uint32_t mask = 0xffffffffu >> (33u - w);
-                const bool lo_m = m <= 20;
-                const unsigned s1 = lo_m ? 20u - m : m - 20u;
-                const uint32_t nfull = static_cast<uint32_t>(umin64(g1, n / 32));
-                uint32_t g = g0;
-                for (; g < nfull; ++g) {
-                    const uint32_t* gp = sw + (g - g0) * w + q;
-                    const uint32_t t = __funnelshift_r(gp[0], gp[1], sh);
-                    const uint32_t pay = t & mask;
-                    const uint32_t hi = (lo_m ? pay << s1 : pay >> s1) + (1023u << 20);
-                    const uint32_t lo = lo_m ? 0u : pay << (32u - s1);
-                    const double v = __dmul_rn(__hiloint2double(hi, lo) - 1.0, d.scale);
-                    const double sv = __hiloint2double(__double2hiint(v) ^ ((t << (32u - w)) & 0x80000000u),
-                                                       __double2loint(v));
-                    __stcs(o + (uint64_t)g * 32 + lane, sv);
-                }
-                for (; g < g1; ++g) {  // ragged last group
-                    const uint32_t* gp = sw + (g - g0) * w + q;
-                    uint64_t win = ((uint64_t)gp[1] << 32 | gp[0]) >> sh;
-                    const uint64_t idx = (uint64_t)g * 32 + lane;
-                    if (idx < n) __stcs(o + idx, decode_field(win & wmask, e, m, d.scale));
-                }
-            } else {
-                for (uint32_t g = g0; g < g1; ++g) {
-                    const uint32_t* gp = sw + (g - g0) * w + q;
-                    uint64_t win = ((uint64_t)gp[1] << 32 | gp[0]) >> sh;
-                    if (sh + w > 64) win |= (uint64_t)gp[2] << (64 - sh);
-                    const uint64_t idx = (uint64_t)g * 32 + lane;
-                    if (idx < n) __stcs(o + idx, decode_field(win & wmask, e, m, d.scale));
-                }
+        } else {
+            for (uint32_t g = g0; g < g1; ++g) {
+                const uint32_t* gp = sw + (g - g0) * w + q;
+                uint64_t win = ((uint64_t)gp[1] << 32 | gp[0]) >> sh;
+                if (sh + w > 64) win |= (uint64_t)gp[2] << (64 - sh);
+                const uint64_t idx = (uint64_t)g * 32 + lane;
+                if (idx < n) __stcs(o + idx, decode_field(win & wmask, e, m, d.scale));
             }
-            __syncwarp();
         }
+        __syncwarp();
+        if (!more) break;
     }
+}
+
+// resident blocks of a kernel on the current device (persistent grids: one
+// wave, no tail wave), cached per (kernel slot, device)
+template <class K>
+int resident_grid(int slot, K kernel, int threads, size_t smem) {
+    static std::atomic<int> cache[4][64];
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "device");
+    std::atomic<int>& c = cache[slot & 3][dev & 63];
+    int v = c.load(std::memory_order_relaxed);
+    if (v) return v;
+    int sms = 0, per = 0;
+    check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem), "occupancy");
+    v = std::max(1, sms * std::max(1, per));
+    c.store(v, std::memory_order_relaxed);
+    return v;
 }
 
 int grid_for(uint64_t njobs) {
@@ -819,13 +1303,40 @@ void launch_unpack_jobs(const uint8_t* payload, const uint64_t* poff, const uint
     layout_arrays(h_count, nbuf, stream);
     const uint64_t nch = g_layout.nchunks;
     if (!nch) return;
-    const int grid = (int)std::min<uint64_t>((nch + kUnpackWarps - 1) / kUnpackWarps, 148ull * 8);
+    const int grid = (int)std::min<uint64_t>((nch + kUnpackWarps - 1) / kUnpackWarps,
+                                             resident_grid(0, k_unpack_chunks, kUnpackWarps * 32, 0));
     KernelTimer kt(1, s);
     k_unpack_chunks<<<grid, kUnpackWarps * 32, 0, s>>>(payload, poff, g_layout.count.as<uint64_t>(), desc, voff,
                                                        g_layout.coff.as<uint64_t>(), g_layout.cbuf.as<uint32_t>(),
                                                        nch, out);
     check_cuda(cudaGetLastError(), "unpack launch");
     kt.stop();
+}
+
+// fused compress of buffers of <= kFuseMax values: the register-resident
+// kernel when every buffer fits it, else the two-pass CTA kernel; the grid is
+// the device's resident CTAs (buffers strided over them, no tail wave)
+void launch_compress_fused(const double* values, const uint64_t* voff, const uint64_t* d_count, uint64_t nbuf,
+                           uint64_t max_count, int scheme, unsigned m_req, const uint64_t* poff, uint8_t* payload,
+                           hcmx_descriptor* desc, hcmx_stats* stats, uint32_t* flags, cudaStream_t s) {
+    if (max_count <= kRegMax && HCMX_COMPRESS_KIND == 0) {
+        static std::once_flag attr;
+        std::call_once(attr, [] {
+            check_cuda(cudaFuncSetAttribute(k_compress_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(kTmaSmem)), "attr");
+        });
+        const int grid = (int)std::min<uint64_t>(nbuf, resident_grid(3, k_compress_tma, kTmaWarps * 32, kTmaSmem));
+        k_compress_tma<<<grid, kTmaWarps * 32, kTmaSmem, s>>>(values, voff, d_count, nbuf, scheme, m_req, poff,
+                                                              payload, desc, stats, flags);
+    } else if (max_count <= kRegMax && HCMX_COMPRESS_KIND == 1) {
+        const int grid = (int)std::min<uint64_t>(nbuf, resident_grid(1, k_compress_reg, kCtaWarps * 32, 0));
+        k_compress_reg<<<grid, kCtaWarps * 32, 0, s>>>(values, voff, d_count, nbuf, scheme, m_req, poff, payload,
+                                                       desc, stats, flags);
+    } else {
+        const int grid = (int)std::min<uint64_t>(nbuf, resident_grid(2, k_compress_cta, kCtaWarps * 32, 0));
+        k_compress_cta<<<grid, kCtaWarps * 32, 0, s>>>(values, voff, d_count, nbuf, scheme, m_req, poff, payload,
+                                                       desc, stats, flags);
+    }
 }
 
 }  // namespace hcmx_gpu
@@ -955,12 +1466,10 @@ int hcmx_gpu_codec_compress(const double* d_values, const uint64_t* d_voff, cons
         DevBuf dst(std::max<uint64_t>(24, nbuf * sizeof(hcmx_stats)));
         cudaStream_t s = (cudaStream_t)stream;
         uint8_t* ob = out.as<uint8_t>();
-        const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(nbuf, 148ull * 16));
         KernelTimer kt(0, s);
-        k_compress_cta<<<grid, kCtaWarps * 32, 0, s>>>(d_values, d_voff, g_layout.count.as<uint64_t>(), nbuf,
-                                                       scheme, m_req, dp, d_payload,
-                                                       reinterpret_cast<hcmx_descriptor*>(ob), dst.as<hcmx_stats>(),
-                                                       reinterpret_cast<uint32_t*>(ob + o_fl));
+        launch_compress_fused(d_values, d_voff, g_layout.count.as<uint64_t>(), nbuf, maxc, scheme, m_req, dp,
+                              d_payload, reinterpret_cast<hcmx_descriptor*>(ob), dst.as<hcmx_stats>(),
+                              reinterpret_cast<uint32_t*>(ob + o_fl), s);
         check_cuda(cudaGetLastError(), "compress launch");
         kt.stop();
         std::lock_guard<std::mutex> gp(g_pinned.mu);
@@ -1002,10 +1511,9 @@ int hcmx_gpu_codec_compress_device(const double* d_values, const uint64_t* d_vof
         if (max_count > kFuseMax) throw invalid_argument("compress_device: buffers above 2^17 values take hcmx_gpu_codec_compress");
         if (!nbuf) return;
         cudaStream_t s = (cudaStream_t)stream;
-        const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(nbuf, 148ull * 16));
         KernelTimer kt(0, s);
-        k_compress_cta<<<grid, kCtaWarps * 32, 0, s>>>(d_values, d_voff, d_count, nbuf, scheme, m_req, d_poff,
-                                                       d_payload, d_desc, nullptr, d_flags);
+        launch_compress_fused(d_values, d_voff, d_count, nbuf, max_count, scheme, m_req, d_poff, d_payload, d_desc,
+                              nullptr, d_flags, s);
         check_cuda(cudaGetLastError(), "compress launch");
         kt.stop();
     });
