@@ -399,23 +399,49 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // IMAD with the bias 1023 << 52 rebuilds 1.mant * 2^offset (offset + 1023 <=
 // 2046: no clamp for e <= 10); one DADD takes the 1 off and the sign is xored
 // into the high word.  About 8 instructions per value with the FMA.
-__device__ __forceinline__ double dec_fast(const uint32_t* sp, unsigned s, uint32_t mask, uint32_t mul,
+__device__ __forceinline__ double dec_pair(uint32_t lo, uint32_t hi, unsigned s, uint32_t mask, uint32_t mul,
                                           uint64_t bias) {
-    const uint32_t t = __funnelshift_l(sp[0], sp[1], s);
+    const uint32_t t = __funnelshift_l(lo, hi, s);
     const uint64_t bits = static_cast<uint64_t>(t & mask) * mul + bias;
     const double v = __longlong_as_double(static_cast<long long>(bits)) - 1.0;
     return __hiloint2double(__double2hiint(v) ^ static_cast<int>(t & 0x80000000u), __double2loint(v));
 }
+__device__ __forceinline__ double dec_fast(const uint32_t* sp, unsigned s, uint32_t mask, uint32_t mul,
+                                          uint64_t bias) {
+    return dec_pair(sp[0], sp[1], s, mask, mul, bias);
+}
 
-// Generic decoder: the field at bit sh of sp[0..2] (64-bit window, the
+// Interleaved word streams: NG streams (row groups of a column segment, or the
+// 4 rows of a phase-A group) whose word j sits at NG j + g, so the two words a
+// field needs in every stream come with two NG-word vector loads (LDS.128 for
+// NG = 4, LDS.64 for NG = 2) from one address.  q: the stream words' vector
+// base (16- / 8-byte aligned), o: the word below the fields' sign words (may
+// be -1: the bits it brings are masked off).
+template <int NG>
+__device__ __forceinline__ void il_load(const uint32_t* q, int o, uint32_t (&lo)[NG], uint32_t (&hi)[NG]) {
+    static_assert(NG == 2 || NG == 4, "interleave");
+    if constexpr (NG == 4) {
+        const uint4* v = reinterpret_cast<const uint4*>(q) + o;
+        const uint4 a = v[0], b = v[1];
+        lo[0] = a.x, lo[1] = a.y, lo[2] = a.z, lo[3] = a.w;
+        hi[0] = b.x, hi[1] = b.y, hi[2] = b.z, hi[3] = b.w;
+    } else {
+        const uint2* v = reinterpret_cast<const uint2*>(q) + o;
+        const uint2 a = v[0], b = v[1];
+        lo[0] = a.x, lo[1] = a.y;
+        hi[0] = b.x, hi[1] = b.y;
+    }
+}
+
+// Generic decoder: the field at bit sh of sp[0], sp[st], sp[2 st] (64-bit window, the
 // min(offset + 1023, 2046) clamp), for e = 11, w > 32 and padded layouts;
 // modes 3, 4, 5: uncompressed FP64 / FP32 / FP16 storage (StorageMode fp64 and
 // the MP-D-S-H groups, mixedprec.hpp:20-43), the value itself (scale 1).
-__device__ __forceinline__ double dec_generic(const uint32_t* sp, uint32_t packed, unsigned sh) {
+__device__ __forceinline__ double dec_generic(const uint32_t* sp, uint32_t packed, unsigned sh, unsigned st = 1) {
     const unsigned fmt = packed >> 24;
     const unsigned w = packed & 0xffu, m = (packed >> 8) & 0xffu, e = (packed >> 16) & 0xffu;
-    uint64_t win = ((static_cast<uint64_t>(sp[1]) << 32) | sp[0]) >> sh;
-    if (w > 32 && sh + w > 64) win |= static_cast<uint64_t>(sp[2]) << (64 - sh);
+    uint64_t win = ((static_cast<uint64_t>(sp[st]) << 32) | sp[0]) >> sh;
+    if (w > 32 && sh + w > 64) win |= static_cast<uint64_t>(sp[2 * st]) << (64 - sh);
     if (fmt >= 3) {  // uncompressed words (uniform per item, so the branch is too)
         if (fmt == 3)  // FP64
             return __longlong_as_double(static_cast<long long>(win));
@@ -723,31 +749,32 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
 }
 
 // ------------------------------------------------------------ phase A ----
+// Item data: groups of kARows rows; each row is the lanes' fields back to back
+// (rowbits), padded to whole words, and the kARows rows of a group are
+// word-interleaved (row r's word j at 4 j + r; gwords = 4 * row words), so a
+// lane's field sits at the same (word, shift) in every row: the two words of
+// its four fields in a group come with two LDS.128.
 // Fast body: every lane's field is a codec field with w <= 32 and e <= 10
-// (dec_fast), the item has whole row groups and every lane's x slice is
-// 16-byte aligned.  Lane-constant (word, shift) per row of a group; the group
-// stride is gwords.  xs: this lane's x rows, R values per row.  R = 1 keeps one
+// (dec_pair), the item has whole row groups and every lane's x slice is
+// 16-byte aligned.  xs: this lane's x rows, R values per row.  R = 1 keeps one
 // FMA chain per row of the group, R > 1 one chain per right-hand side.
 template <int R>
 __device__ __forceinline__ void a_fast(const uint32_t* data, unsigned P, unsigned w, unsigned e, const double* xs,
-                                       unsigned ngroups, unsigned rowbits, unsigned gwords, uint64_t bias,
-                                       double (&res)[R]) {
+                                       unsigned ngroups, unsigned gwords, uint64_t bias, double (&res)[R]) {
     const uint32_t mask = fast_mask(w);
     const uint32_t mul = c_pow2e.v[e & 31u];
-    const uint32_t* q[kARows];
-    unsigned s[kARows];
-#pragma unroll
-    for (int r = 0; r < kARows; ++r) {
-        const unsigned top = P + r * rowbits + w;  // one past the field's sign bit
-        q[r] = data + ((top - 1) >> 5) - 1;        // the word below the one holding the sign
-        s[r] = 0u - top;                           // the funnel shift takes it modulo 32
-    }
+    const unsigned top = P + w;                          // one past the field's sign bit (in a row)
+    const int o = static_cast<int>((top - 1) >> 5) - 1;  // the word below the sign word
+    const unsigned s = 0u - top;                         // the funnel shift takes it modulo 32
+    const uint32_t* q = data;
     constexpr int NA = R == 1 ? kARows : R;
     double acc[NA];
 #pragma unroll
     for (int i = 0; i < NA; ++i) acc[i] = 0.0;
 #pragma unroll kAUnroll
     for (unsigned g = 0; g < ngroups; ++g) {
+        uint32_t lo[kARows], hi[kARows];
+        il_load<kARows>(q, o, lo, hi);
         double xv[kARows * R];
 #pragma unroll
         for (int i = 0; i < kARows * R / 2; ++i) {
@@ -757,15 +784,15 @@ __device__ __forceinline__ void a_fast(const uint32_t* data, unsigned P, unsigne
         }
 #pragma unroll
         for (int r = 0; r < kARows; ++r) {
-            const double d = dec_fast(q[r], s[r], mask, mul, bias);
+            const double d = dec_pair(lo[r], hi[r], s, mask, mul, bias);
             if (R == 1) {
                 acc[r] = fma(d, xv[r], acc[r]);
             } else {
 #pragma unroll
                 for (int c = 0; c < R; ++c) acc[c % NA] = fma(d, xv[r * R + c], acc[c % NA]);
             }
-            q[r] += gwords;
         }
+        q += gwords;
     }
     if (R == 1) res[0] = (acc[0] + acc[1]) + (acc[2 % NA] + acc[3 % NA]);
     else {
@@ -775,18 +802,17 @@ __device__ __forceinline__ void a_fast(const uint32_t* data, unsigned P, unsigne
 }
 
 // Generic body: any layout (e = 11, w > 32, uncompressed words), any row count,
-// any x alignment -- the mode-2 decoder per field.
+// any x alignment -- the mode-2 decoder per field (row words 4 apart).
 template <int R>
 __device__ __forceinline__ void a_generic(const uint32_t* data, unsigned P, uint32_t rec, const double* xs,
-                                          unsigned nf, unsigned rowbits, unsigned gwords, double (&res)[R]) {
+                                          unsigned nf, unsigned gwords, double (&res)[R]) {
     const unsigned w = rec & 127u, e = (rec >> 7) & 15u, m = (rec >> 11) & 63u, fmt = (rec >> 17) & 3u;
     const uint32_t packed = w | (m << 8) | (e << 16) | ((fmt ? fmt + 2u : 2u) << 24);  // 1-3: raw f64 / f32 / f16
 #pragma unroll
     for (int c = 0; c < R; ++c) res[c] = 0.0;
+    const uint32_t* row0 = data + 4 * (P >> 5);
     for (unsigned j = 0; j < nf; ++j) {
-        const unsigned bit = P + (j % kARows) * rowbits;
-        const uint32_t* sp = data + (j / kARows) * gwords + (bit >> 5);
-        const double d = dec_generic(sp, packed, bit & 31u);
+        const double d = dec_generic(row0 + (j / kARows) * gwords + (j % kARows), packed, P & 31u, kARows);
 #pragma unroll
         for (int c = 0; c < R; ++c) res[c] = fma(d, xs[j * R + c], res[c]);
     }
@@ -820,8 +846,8 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
     const uint32_t* data = recs + ((nl + 3u) & ~3u);
     const double* xs = reinterpret_cast<const double*>(slot) + (rec >> 19);
     double r[R];
-    if (it.body) a_fast<R>(data, P, w, (rec >> 7) & 15u, xs, it.nf / kARows, it.rowbits, it.gwords, p.bias, r);
-    else a_generic<R>(data, P, rec, xs, it.nf, it.rowbits, it.gwords, r);
+    if (it.body) a_fast<R>(data, P, w, (rec >> 7) & 15u, xs, it.nf / kARows, it.gwords, p.bias, r);
+    else a_generic<R>(data, P, rec, xs, it.nf, it.gwords, r);
     // the chunks of a slot's rank column (lanes slot, slot + nslot, ...): fixed
     // butterfly (lane `slot` gets the same order on every run); idle lanes add 0
 #pragma unroll
@@ -967,18 +993,22 @@ __device__ __forceinline__ void b_item_generic(const BItem& it, const uint32_t* 
 }
 
 // fast path: the item covers row groups [GLO, GHI) of the block completely and
-// every column decodes with dec_fast: lane l takes field l + 32 (g - GLO) of
-// each column segment, at the same shift in every group (32 fields = w words)
+// every column decodes with dec_pair: lane l takes field l + 32 (g - GLO) of
+// each column segment, at the same shift in every group.  A segment's NG =
+// GHI - GLO groups (32 fields = w words each) are word-interleaved (group g's
+// word j at NG j + g): one pair of NG-word vector loads per column.
 template <int GLO, int GHI, int R>
 __device__ __forceinline__ void b_column_full(const uint32_t* seg, unsigned lane, unsigned w, uint32_t mask,
                                               uint32_t mul, uint64_t bias, const double (&coef)[R],
                                               double (&acc)[kG * R]) {
+    constexpr int NG = GHI - GLO;
     const unsigned top = (lane + 1) * w;  // one past the sign bit of field `lane`
-    const uint32_t* sp = seg + ((top - 1) >> 5) - 1;
     const unsigned s = 0u - top;          // the funnel shift takes it modulo 32
+    uint32_t lo[NG], hi[NG];
+    il_load<NG>(seg, static_cast<int>((top - 1) >> 5) - 1, lo, hi);
 #pragma unroll
     for (int g = GLO; g < GHI; ++g) {
-        const double d = dec_fast(sp + (g - GLO) * w, s, mask, mul, bias);
+        const double d = dec_pair(lo[g - GLO], hi[g - GLO], s, mask, mul, bias);
 #pragma unroll
         for (int c = 0; c < R; ++c) acc[g * R + c] = fma(d, coef[c], acc[g * R + c]);
     }
@@ -1054,7 +1084,7 @@ __device__ __forceinline__ void b1_dense(const BItem& it, const uint32_t* seg, c
     const unsigned w = it.dpacked & 0xffu, e = (it.dpacked >> 16) & 0xffu;
     const uint32_t mask = fast_mask(w), mul = c_pow2e.v[e & 31u];
     const unsigned top = (lane + 1) * w;                 // one past the sign bit of field `lane`
-    const uint32_t* sp = seg + ((top - 1) >> 5) - 1;
+    const int o = static_cast<int>((top - 1) >> 5) - 1;  // same word and shift in every column
     const unsigned s = 0u - top;
     const unsigned segw = NG * w;
     double t0[NG], t1[NG];
@@ -1064,17 +1094,22 @@ __device__ __forceinline__ void b1_dense(const BItem& it, const uint32_t* seg, c
     unsigned c = 0;
     for (; c + 2 <= n; c += 2) {
         const double x0 = xc[c], x1 = xc[c + 1];
+        uint32_t l0[NG], h0[NG], l1[NG], h1[NG];
+        il_load<NG>(seg, o, l0, h0);
+        il_load<NG>(seg + segw, o, l1, h1);
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
-            t0[g] = fma(dec_fast(sp + g * w, s, mask, mul, bias), x0, t0[g]);
-            t1[g] = fma(dec_fast(sp + segw + g * w, s, mask, mul, bias), x1, t1[g]);
+            t0[g] = fma(dec_pair(l0[g], h0[g], s, mask, mul, bias), x0, t0[g]);
+            t1[g] = fma(dec_pair(l1[g], h1[g], s, mask, mul, bias), x1, t1[g]);
         }
-        sp += 2 * segw;
+        seg += 2 * segw;
     }
     if (c < n) {
         const double x0 = xc[c];
+        uint32_t l0[NG], h0[NG];
+        il_load<NG>(seg, o, l0, h0);
 #pragma unroll
-        for (int g = 0; g < NG; ++g) t0[g] = fma(dec_fast(sp + g * w, s, mask, mul, bias), x0, t0[g]);
+        for (int g = 0; g < NG; ++g) t0[g] = fma(dec_pair(l0[g], h0[g], s, mask, mul, bias), x0, t0[g]);
     }
 #pragma unroll
     for (int g = 0; g < NG; ++g) acc[GLO + g] = fma(dmul, t0[g] + t1[g], acc[GLO + g]);
@@ -1093,10 +1128,11 @@ __device__ __forceinline__ void b1_lr(const BItem& it, const uint32_t* seg, cons
         rec += 32;
         const double cc = __hiloint2double(static_cast<int>(q0.y), static_cast<int>(q0.x));
         const unsigned top = lp1 * w;
-        const uint32_t* sp = seg + ((top - 1) >> 5) - 1;
+        uint32_t lo[NG], hi[NG];
+        il_load<NG>(seg, static_cast<int>((top - 1) >> 5) - 1, lo, hi);
         const unsigned s = 0u - top;
 #pragma unroll
-        for (int g = 0; g < NG; ++g) acc[GLO + g] = fma(dec_fast(sp + g * w, s, q0.z, q0.w, bias), cc, acc[GLO + g]);
+        for (int g = 0; g < NG; ++g) acc[GLO + g] = fma(dec_pair(lo[g], hi[g], s, q0.z, q0.w, bias), cc, acc[GLO + g]);
         seg += NG * w;
     }
 }
@@ -1282,11 +1318,27 @@ void copy_bits(const uint8_t* src, uint64_t len, uint64_t bit, uint64_t nbits, u
 struct SegRef {  // where a run of a buffer's fields landed in the arena (export)
     uint64_t word;  // arena word index
     uint32_t f0, nf;
-    // phase-A items (gwords > 0): field j at bit (j / kARows) * 32 gwords +
-    // pbit + (j % kARows) * rowbits from `word`; else the fields are contiguous
+    // phase-A items (gwords > 0): field j in row j % kARows of group j / kARows
+    // at bit pbit of the row, the row's words kARows apart from `word` +
+    // (j / kARows) gwords + j % kARows; phase-B segments with il > 1: il
+    // word-interleaved groups of 32 fields (field j at bit (j % 32) w of group
+    // j / 32, whose words are il apart from `word` + j / 32); else contiguous
     uint32_t pbit;
     uint16_t rowbits, gwords;
+    uint8_t il = 0;
 };
+
+// field locator of a SegRef: the word-strided stream (first word, stride) and bit of field j
+struct FieldLoc {
+    uint64_t word;
+    unsigned stride;
+    uint64_t bit;
+};
+inline FieldLoc field_loc(const SegRef& r, uint64_t j, unsigned w) {
+    if (r.gwords) return {(j / kARows) * r.gwords + (j % kARows), static_cast<unsigned>(kARows), r.pbit};
+    if (r.il > 1) return {j / 32, r.il, (j % 32) * w};
+    return {0, 1u, j * w};
+}
 
 // w (<= 64) bits at bit offset `bit` of the LSB-first stream src[0, len)
 // (bytes past len read as 0)
@@ -1301,16 +1353,30 @@ uint64_t get_bits(const uint8_t* src, uint64_t len, uint64_t bit, unsigned w) {
     return w >= 64 ? r : (r & ((1ull << w) - 1));
 }
 
-// OR the low w bits of v into the word stream dst at bit offset `bit`
-void put_bits(uint32_t* dst, uint64_t bit, uint64_t v, unsigned w) {
+// OR the low w bits of v into the word stream dst at bit offset `bit` (the
+// stream's words `stride` apart)
+void put_bits(uint32_t* dst, uint64_t bit, uint64_t v, unsigned w, unsigned stride = 1) {
     while (w) {
         const unsigned sh = static_cast<unsigned>(bit & 31), take = std::min(32u - sh, w);
         const uint64_t part = take == 64 ? v : (v & ((1ull << take) - 1));
-        dst[bit >> 5] |= static_cast<uint32_t>(part << sh);
+        dst[(bit >> 5) * stride] |= static_cast<uint32_t>(part << sh);
         v = take >= 64 ? 0 : v >> take;
         bit += take;
         w -= take;
     }
+}
+
+// w (<= 64) bits at bit offset `bit` of a word stream whose words are `stride`
+// apart (words past nwords read as 0)
+uint64_t get_bits_strided(const uint32_t* src, uint64_t nwords, unsigned stride, uint64_t bit, unsigned w) {
+    unsigned __int128 v = 0;
+    const uint64_t k0 = bit >> 5;
+    for (unsigned t = 0; t < 3; ++t) {
+        const uint64_t idx = (k0 + t) * stride;
+        if (idx < nwords) v |= static_cast<unsigned __int128>(src[idx]) << (32 * t);
+    }
+    const uint64_t r = static_cast<uint64_t>(v >> (bit & 31));
+    return w >= 64 ? r : (r & ((1ull << w) - 1));
 }
 
 // one lane of a phase-A item: fields [f0, f0 + nf) of codec buffer `buf`
@@ -1459,6 +1525,13 @@ std::vector<std::pair<uint32_t, uint32_t>> column_groups(uint32_t n, uint32_t ma
     return g;
 }
 
+// word interleave of a phase-B item's column segments: the fast bodies read
+// NG = 4 (rows [0,128)) or 2 (rows [0,64) / [64,128)) interleaved groups per
+// column; generic items keep each segment's fields contiguous
+inline unsigned il_of(const BItem& it) { return it.fcase == 1 ? 4u : (it.fcase == 2 || it.fcase == 3) ? 2u : 1u; }
+template <class Item>
+inline unsigned il_of(const Item&) { return 1u; }
+
 // anonymous, lazily backed host mapping (pages cost nothing until written)
 struct HostBlob {
     uint8_t* p = nullptr;
@@ -1512,6 +1585,7 @@ struct Builder {
     // (item / segment destinations are disjoint word ranges).
     struct CopyJob {   // phase B: fields [f0, f0+nf) of buffer buf, word aligned at arena word `at`
         uint64_t at, buf, f0, nf;
+        unsigned il;    // > 1: il groups of 32 fields, word-interleaved (fast-body segments)
     };
     struct LaneJob {   // phase A: one lane of an item (row-interleaved placement)
         uint64_t data0, buf, f0;
@@ -1520,25 +1594,41 @@ struct Builder {
     std::vector<CopyJob> copy_jobs;
     std::vector<LaneJob> lane_jobs;
 
-    // append the words of fields [f0, f0+nf) of buffer b (word aligned)
-    void put_fields(const Seg& s) {
+    // append the words of fields [f0, f0+nf) of buffer b (word aligned); il >
+    // 1: nf = 32 il fields as il word-interleaved groups (group g's word j at
+    // il j + g, the layout of the phase-B fast bodies)
+    void put_fields(const Seg& s, unsigned il = 1) {
         const unsigned w = width(s.buf);
         const uint64_t nw = (s.nf * w + 31) / 32;
+        if (il > 1 && s.nf != 32ull * il) throw std::logic_error("hmat: interleaved segment");
         const uint64_t at = arena.size();
         arena.resize(at + nw);
-        copy_jobs.push_back({at, s.buf, s.f0, s.nf});
-        if (keep_map) h->segs[s.buf].push_back({at, static_cast<uint32_t>(s.f0), static_cast<uint32_t>(s.nf)});
+        copy_jobs.push_back({at, s.buf, s.f0, s.nf, il});
+        if (keep_map) {
+            SegRef r{at, static_cast<uint32_t>(s.f0), static_cast<uint32_t>(s.nf), 0, 0, 0};
+            r.il = static_cast<uint8_t>(il);
+            h->segs[s.buf].push_back(r);
+        }
     }
 
     void place_all() {
         unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
         const size_t nc = copy_jobs.size(), nl = lane_jobs.size();
         auto work = [&](unsigned t) {
+            uint32_t tmp[64];
             for (size_t i = t; i < nc; i += nt) {
                 const CopyJob& j = copy_jobs[i];
                 const unsigned w = width(j.buf);
-                copy_bits(blob + d.poff[j.buf], static_cast<uint64_t>(d.plen[j.buf]), j.f0 * w, j.nf * w,
-                          arena.data() + j.at);
+                if (j.il <= 1) {
+                    copy_bits(blob + d.poff[j.buf], static_cast<uint64_t>(d.plen[j.buf]), j.f0 * w, j.nf * w,
+                              arena.data() + j.at);
+                    continue;
+                }
+                for (unsigned g = 0; g < j.il; ++g) {  // group g: w words, scattered il apart
+                    copy_bits(blob + d.poff[j.buf], static_cast<uint64_t>(d.plen[j.buf]), (j.f0 + 32ull * g) * w,
+                              32ull * w, tmp);
+                    for (unsigned q = 0; q < w; ++q) arena[j.at + static_cast<uint64_t>(q) * j.il + g] = tmp[q];
+                }
             }
             // lanes of one item share words: an item's lanes are consecutive in
             // lane_jobs and go to the same thread (chunks cut at item starts)
@@ -1557,8 +1647,9 @@ struct Builder {
                 const uint64_t len = static_cast<uint64_t>(d.plen[L.buf]);
                 for (uint32_t q = 0; q < L.nf; ++q) {
                     const uint64_t v = get_bits(src, len, (L.f0 + q) * w, w);
-                    put_bits(arena.data() + L.data0,
-                             static_cast<uint64_t>(q / kARows) * L.gwords * 32 + L.P + (q % kARows) * L.rowbits, v, w);
+                    // row q % kARows of group q / kARows: its words kARows apart
+                    put_bits(arena.data() + L.data0 + static_cast<uint64_t>(q / kARows) * L.gwords + q % kARows, L.P, v,
+                             w, kARows);
                 }
             }
         };
@@ -1668,7 +1759,7 @@ struct Builder {
             slices.swap(merged);
             // the coefficients follow the stage in the slot (slot-relative offsets)
             size_t data_words = (built.size() * (kItemBytes / 4) + (NW > 0 ? kRangeBytes / 4 : 0) + 3) & ~size_t(3);
-            for (const Built& b : built) data_words += b.words;
+            for (const Built& b : built) data_words = ((data_words + il_of(b.it) - 1) & ~size_t(il_of(b.it) - 1)) + b.words;
             data_bytes = static_cast<uint32_t>(((data_words + 3) & ~size_t(3)) * 4);
             coef = data_bytes;
             for (Slice& s : slices) {
@@ -1719,11 +1810,13 @@ struct Builder {
         const size_t meta_words = built.size() * (kItemBytes / 4) + head_words;
         arena.resize(start + ((meta_words + 3) & ~size_t(3)), 0u);
         for (Built& b : built) {
+            const unsigned il = il_of(b.it);  // interleaved segments: il-word aligned item data
+            while ((arena.size() - start) % il) arena.push_back(0u);
             b.it.word_off = static_cast<uint32_t>(arena.size() - start);
             if (IS_A)  // packed column layouts ahead of the segments
                 for (size_t k = b.first; k < b.first + b.n; ++k) arena.push_back(specs[k].param);
             for (size_t k = b.first; k < b.first + b.n; ++k)
-                for (uint32_t q = 0; q < specs[k].nseg; ++q) put_fields(segs[specs[k].seg0 + q]);
+                for (uint32_t q = 0; q < specs[k].nseg; ++q) put_fields(segs[specs[k].seg0 + q], il);
             items.push_back(b.it);
         }
         for (size_t i = 0; i < built.size(); ++i)
@@ -1800,7 +1893,7 @@ struct Builder {
             t.l0 = i;
             t.nl = j - i;
             t.rowbits = rb;
-            t.gwords = (kARows * rb + 31) / 32;
+            t.gwords = kARows * ((rb + 31) / 32);  // rows padded to words, word-interleaved
             t.ngroups = (lanes[i].nf + kARows - 1) / kARows;
             const size_t nrec = lanes[i].G == 1 ? t.nl : static_cast<size_t>(kALanes);  // lane records
             t.bytes = r16(4 * (((nrec + 3) & ~size_t(3)) + static_cast<uint64_t>(t.ngroups) * t.gwords));
@@ -2950,12 +3043,11 @@ int hcmx_gpu_hmat_export_buffer(const hcmx_hmat* h, uint64_t b, uint8_t* h_paylo
             std::vector<uint32_t> words(nw + 2, 0u);
             check_cuda(cudaMemcpy(words.data(), h->arena.as<uint32_t>() + sref.word, nw * 4, cudaMemcpyDeviceToHost),
                        "export d2h");
-            const uint8_t* wb = reinterpret_cast<const uint8_t*>(words.data());
             for (uint64_t j = 0; j < sref.nf; ++j) {
-                // the field's bit in the arena run, written back at its original offset
-                const uint64_t from = sref.gwords ? (j / kARows) * sref.gwords * 32ull + sref.pbit + (j % kARows) * sref.rowbits
-                                                  : j * w;
-                put_bits(reinterpret_cast<uint32_t*>(bits.data()), (sref.f0 + j) * w, get_bits(wb, words.size() * 4, from, w), w);
+                // the field in the arena run, written back at its original offset
+                const FieldLoc fl = field_loc(sref, j, w);
+                put_bits(reinterpret_cast<uint32_t*>(bits.data()), (sref.f0 + j) * w,
+                         get_bits_strided(words.data() + fl.word, words.size() - fl.word, fl.stride, fl.bit, w), w);
             }
         }
         std::memcpy(h_payload, bits.data(), n);
