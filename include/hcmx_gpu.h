@@ -209,6 +209,17 @@ typedef struct hcmx_hmat_desc {
     /* 4: also lay the matrix out for products with 4 right-hand sides at once
      * (hcmx_gpu_hmat_matmat decodes every field once for 4 columns); 0: off */
     int nrhs_block;
+    /* nonzero: a COMPLEX matrix A = Ar + i Ai stored once with real codec streams
+     * (BASELINE config 5; needs nrhs_block = 4, no transpose).  Lowrank leaves
+     * (kind 1) hold A's truncated SVD U S V^H as W = [Ur Ui], X = [Vr Vi] and
+     * sigma = [S S] (rank 2k: every real / imaginary factor column is its own
+     * APLR stream, decoded once per product); dense leaves are Re A (imag 0) and
+     * Im A (dense_imag[l] = 1, same row / column range).  The 4-RHS products then
+     * take two complex columns interleaved, [Re x1, Im x1, Re x2, Im x2], and
+     * return [Re y1, Im y1, Re y2, Im y2]; the complex combination of the
+     * X^T x halves runs on the device between the phases. */
+    int complex_pairs;
+    const uint8_t* dense_imag; /* [nleaves], or NULL */
 } hcmx_hmat_desc;
 
 typedef struct hcmx_hmat hcmx_hmat; /* opaque, device resident */

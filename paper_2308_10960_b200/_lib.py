@@ -51,7 +51,7 @@ class hcmx_hmat_desc(C.Structure):
                 ("count", _pi64), ("poff", _pi64), ("plen", _pi64),
                 ("blob", C.c_void_p), ("blob_on_device", C.c_int),
                 ("row_begin", C.c_uint64), ("row_end", C.c_uint64), ("with_transpose", C.c_int),
-                ("nrhs_block", C.c_int)]
+                ("nrhs_block", C.c_int), ("complex_pairs", C.c_int), ("dense_imag", C.POINTER(C.c_uint8))]
 
 
 class hcmx_assembled(C.Structure):

@@ -270,6 +270,7 @@ struct Params {
     uint8_t* wrec;              // per rank column: record {c[R], mask, mul, packed, w} (rec_bytes<R>):
                                 // c = alpha * coef * (X^T x) per right-hand side (phase A) + W decoder constants
     double* partial;
+    const double* x2;           // complex arenas: the swapped right-hand sides (-Im x, Re x) per pair
     const double* x;            // R = 1: padded internal copy (16-byte aligned, readable + 16 B);
                                 // R > 1: n x R, row-major (the R right-hand sides interleaved)
     double* y;                  // R > 1: n x R, row-major
@@ -496,6 +497,7 @@ __device__ __forceinline__ void issue_copy(const Params& p, uint64_t c, uint8_t*
     const void* src;
     switch (static_cast<unsigned>((c >> 60) & 3u)) {
         case 0: src = p.x + static_cast<size_t>(idx) * R; break;
+        case 2: src = p.x2 + static_cast<size_t>(idx) * R; break;  // complex: swapped x
         default: src = p.wrec + static_cast<size_t>(idx) * rec_bytes<R>(); break;
     }
     bulk_g2s_plain(cdst + dst, src, bytes, bar);
@@ -1288,6 +1290,43 @@ __global__ void k_combine(Params p, const uint8_t* npieces) {
     }
 }
 
+// ---------------------------------------------------- complex arenas ----
+// A = U S V^H with U = Ur + i Ui, V = Vr + i Vi held as W = [Ur Ui], X = [Vr Vi]
+// (hcmx_hmat_desc::complex_pairs); x and y interleave two complex columns,
+// [Re x1, Im x1, Re x2, Im x2].  V^H x = (Vr^T Re x + Vi^T Im x) + i (Vr^T Im x -
+// Vi^T Re x): phase A leaves a = alpha s_Vr Vr'^T x4 and b = alpha s_Vi Vi'^T x4
+// in the records of the pair's two X columns; k_ccombine forms t = V^H x and
+// writes the W columns' coefficients, Ur_j: s_Ur sigma (t_r, t_i), Ui_j:
+// s_Ui sigma (-t_i, t_r), so phase B's real accumulation gives Re / Im y.  The
+// imaginary dense parts read the swapped x (-Im x, Re x) (copy table 2).
+struct CPair {
+    uint32_t a, b;  // record (rank column) of Ur_j / Vr_j and of Ui_j / Vi_j
+    double sig, sa, sb;
+};
+static_assert(sizeof(CPair) == 32, "CPair layout");
+
+__global__ void k_xswap(const double* __restrict__ x4, double* __restrict__ x2, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (uint64_t)blockDim.x) {
+        const double2 u = reinterpret_cast<const double2*>(x4)[2 * i], v = reinterpret_cast<const double2*>(x4)[2 * i + 1];
+        reinterpret_cast<double2*>(x2)[2 * i] = make_double2(-u.y, u.x);
+        reinterpret_cast<double2*>(x2)[2 * i + 1] = make_double2(-v.y, v.x);
+    }
+}
+
+__global__ void k_ccombine(Params p, const CPair* __restrict__ cp, uint32_t n) {
+    pdl_trigger();
+    pdl_wait();  // phase A (and k_reduce) wrote the X^T x halves
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const CPair q = cp[i];
+        double* ra = rec_c<kMultiR>(p, q.a);
+        double* rb = rec_c<kMultiR>(p, q.b);
+        const double tr1 = q.sig * (ra[0] + rb[1]), ti1 = q.sig * (ra[1] - rb[0]);
+        const double tr2 = q.sig * (ra[2] + rb[3]), ti2 = q.sig * (ra[3] - rb[2]);
+        ra[0] = q.sa * tr1, ra[1] = q.sa * ti1, ra[2] = q.sa * tr2, ra[3] = q.sa * ti2;
+        rb[0] = -q.sb * ti1, rb[1] = q.sb * tr1, rb[2] = -q.sb * ti2, rb[3] = q.sb * tr2;
+    }
+}
+
 __global__ void k_scale(double* y, uint64_t n, double beta) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (uint64_t)blockDim.x)
         y[i] = beta == 0.0 ? 0.0 : beta * y[i];
@@ -1417,6 +1456,9 @@ struct hcmx_hmat {
     uint64_t calls = 0;
     hcmx_hmat* trans = nullptr;  // M^T (hmatrix.hpp:128 transpose), built on request
     hcmx_hmat* multi = nullptr;  // the same matrix laid out for kMultiR right-hand sides (matmat)
+    bool cplx = false;           // complex arena (hcmx_hmat_desc::complex_pairs; R = kMultiR)
+    DevBuf xswap, cpairs;        // complex: swapped x (n x 4), rank-pair table for k_ccombine
+    uint32_t ncpairs = 0;
     // products on one handle share its device scratch (stripe counters, x copy,
     // phase-A results): a product issued on another stream than the previous
     // one first waits for it (the reference's matvec is re-entrant, const M&)
@@ -1707,7 +1749,7 @@ struct Builder {
         };
         std::vector<Slice> slices;
         uint32_t coef = 0, data_bytes = 0;
-        auto esize = [&](uint32_t table) { return table == 0 ? 8u * R : rec_bytes_rt(R); };
+        auto esize = [&](uint32_t table) { return table == 1 ? rec_bytes_rt(R) : 8u * R; };  // 0 x, 2 swapped x: R doubles
         auto slice_bytes = [&](const Slice& s) { return r16((s.end - s.start) * esize(s.table)); };
         std::vector<size_t> cut = {pos, end};
         if (NW > 0) {
@@ -1736,7 +1778,7 @@ struct Builder {
             Item it = specs[i].it;
             it.nseg = static_cast<uint8_t>(j - i);
             const uint32_t t = specs[i].sl_table;
-            slices.push_back({t, t == 0 ? specs[i].sl_start & ~1u : specs[i].sl_start,
+            slices.push_back({t, t != 1 ? specs[i].sl_start & ~1u : specs[i].sl_start,
                               specs[i].sl_start + specs[i].sl_count, 0});
             built.push_back({it, i, j - i, words});
             i = j;
@@ -1749,7 +1791,7 @@ struct Builder {
             });
             std::vector<Slice> merged;
             for (const Slice& s : slices) {
-                const uint32_t gap = s.table == 0 ? 32u : 4u;  // elements (256 B of x, 128 B of records)
+                const uint32_t gap = s.table != 1 ? 32u : 4u;  // elements (256 B of x, 128 B of records)
                 if (!merged.empty() && merged.back().table == s.table && s.start <= merged.back().end + gap) {
                     merged.back().end = std::max(merged.back().end, s.end);
                 } else {
@@ -2365,7 +2407,20 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
             // record {c[R] (phase A writes it), mask, mul, packed, w}
             const uint32_t par[4] = {cp.mask, cp.mul, cp.packed, xw.bit_width};
             std::memcpy(wrec.data() + static_cast<size_t>(leafa[id].colbase + i) * rb + 8 * h->R, par, sizeof(par));
-            coef[leafa[id].colbase + i] = (uniform ? 1.0 : d.sigma[d.sig0[l] + i]) * xx.scale * xw.scale;
+            // complex arenas: phase A leaves alpha scale_X (X^T x); k_ccombine applies
+            // sigma and the W scales while pairing the real / imaginary halves
+            coef[leafa[id].colbase + i] = h->cplx ? xx.scale : (uniform ? 1.0 : d.sigma[d.sig0[l] + i]) * xx.scale * xw.scale;
+        }
+    }
+    std::vector<CPair> pairs;  // complex: rank pairs (Ur_j | Vr_j, Ui_j | Vi_j) of every lowrank leaf
+    if (h->cplx) {
+        for (uint32_t id = 0; id < leafa.size(); ++id) {
+            const uint64_t l = lr_leaf[id];
+            const uint32_t k2 = leafa[id].k, k = k2 / 2;
+            if (k2 % 2) throw invalid_argument("hmat: complex lowrank leaf with odd real rank");
+            for (uint32_t j = 0; j < k; ++j)
+                pairs.push_back({leafa[id].colbase + j, leafa[id].colbase + k + j, d.sigma[d.sig0[l] + j],
+                                 d.desc[wbuf(l, j).first].scale, d.desc[wbuf(l, k + j).first].scale});
         }
     }
     rep.stages_a = B.stages.size();
@@ -2422,7 +2477,9 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                         it.fcase = bcase_of(r0 - b0, nr, it.mode);
                         it.scale = d.desc[b].scale;
                         sp.elem = it.src;
-                        sp.sl_table = 0;  // x slice of the dense leaf's columns
+                        // x slice of the dense leaf's columns; the imaginary part of a
+                        // complex dense block reads the swapped x (-Im x, Re x)
+                        sp.sl_table = (h->cplx && d.dense_imag && d.dense_imag[l]) ? 2 : 0;
                         sp.sl_start = static_cast<uint32_t>(d.col0[l]);
                         sp.sl_count = static_cast<uint32_t>(cols);
                         sp.cost = 3 * nr + 128;  // ~decode instructions (x8) of one column segment
@@ -2582,6 +2639,12 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     up(h->stripe_b, sb.data(), sb.size() * 16);
     up(h->wcol, wrec.data(), wrec.size());
     up(h->coef, coef.data(), coef.size() * 8);
+    if (h->cplx) {
+        h->ncpairs = static_cast<uint32_t>(pairs.size());
+        up(h->cpairs, pairs.data(), pairs.size() * sizeof(CPair));
+        h->xswap.alloc((d.n_cols + 4) * kMultiR * 8);
+        check_cuda(cudaMemsetAsync(h->xswap.p, 0, h->xswap.bytes, s), "memset");
+    }
     h->xpad.alloc((d.n_cols + 4) * 8);
     check_cuda(cudaMemsetAsync(h->xpad.p, 0, h->xpad.bytes, s), "memset");
     h->partial.alloc(std::max<size_t>(16, npartial * 8 * h->R));
@@ -2683,6 +2746,13 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
     if (!direct) check_cuda(cudaMemcpyAsync(h->xpad.p, dx, h->n_cols * 8, cudaMemcpyDeviceToDevice, s), "x copy");
     Params p = make_params(h, alpha, beta, dy);
     if (direct) p.x = dx;
+    if (h->cplx) {  // the swapped right-hand sides of the imaginary dense parts
+        p.x2 = h->xswap.as<double>();
+        k_xswap<<<static_cast<int>(std::min<uint64_t>((h->n_cols + 255) / 256, 4ull * nsm)), 256, 0, s>>>(
+            dx, h->xswap.as<double>(), h->n_cols);
+        check_cuda(cudaGetLastError(), "xswap launch");
+        h->last_launches++;
+    }
     static const int debug_knob = [] {
         const char* e = std::getenv("HCMX_DEBUG");
         return e ? std::atoi(e) : 0;
@@ -2724,6 +2794,9 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
     } else {
         if (run_a) launch(k_phase_a<kMultiR>, ga, kThreadsA, kSmemBytesA, false, p);
         if (h->nred) launch(k_reduce<kMultiR>, gr, 256, 0, true, p, rc, h->nred_long, h->nred);
+        if (h->cplx && h->ncpairs)
+            launch(k_ccombine, std::min<uint32_t>((h->ncpairs + 255) / 256, 8 * nsm), 256, 0, true, p,
+                   h->cpairs.as<CPair>(), h->ncpairs);
         if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
         if (h->nblocks) launch(k_phase_b<kMultiR>, gb, (nwb<kMultiR>() + 1) * 32, kSmemBytes, run_a, p);
         if (h->pieces) launch(k_combine<kMultiR>, gc, 256, 0, true, p, h->npieces.as<uint8_t>());
@@ -2882,6 +2955,27 @@ hcmx_hmat* create_handle(const hcmx_hmat_desc& d) {
     auto* h = new hcmx_hmat();
     try {
         check_cuda(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        if (d.complex_pairs) {
+            // a complex matrix exists only as the 4-RHS arena (two complex columns per
+            // product); the outer handle is a shell that forwards to it
+            if (d.nrhs_block != kMultiR) throw invalid_argument("hmat: a complex matrix needs nrhs_block = 4");
+            if (d.with_transpose || d.row_begin || d.row_end)
+                throw invalid_argument("hmat: complex matrices: no transpose, no row partition");
+            for (uint64_t l = 0; l < d.nleaves; ++l)
+                if (d.kind[l] == 2) throw invalid_argument("hmat: complex matrices take APLR lowrank leaves (kind 1)");
+            h->multi = new hcmx_hmat();
+            h->multi->R = kMultiR;
+            h->multi->cplx = true;
+            check_cuda(cudaStreamCreateWithFlags(&h->multi->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            build(d, h->multi);
+            h->cplx = true;
+            h->n_rows = h->multi->n_rows;
+            h->n_cols = h->multi->n_cols;
+            h->rb = h->multi->rb;
+            h->re = h->multi->re;
+            h->report = h->multi->report;
+            return h;
+        }
         build(d, h);
         if (d.nrhs_block) {
             if (d.nrhs_block != kMultiR) throw invalid_argument("hmat: nrhs_block must be 0 or 4");
@@ -2933,6 +3027,7 @@ int hcmx_gpu_hmat_memory(const hcmx_hmat* h, hcmx_memory_report* out) {
 int hcmx_gpu_hmat_matmat(hcmx_hmat* h, double alpha, const double* h_x, uint64_t ldx, uint64_t nrhs,
                          double beta, double* h_y, uint64_t ldy, int transpose) {
     return guarded([&] {
+        if (h->cplx) throw invalid_argument("hmat: a complex matrix runs through hcmx_gpu_hmat_matmat4_device (two complex columns per product)");
         if (transpose) {
             if (!h->trans) throw invalid_argument("matmat: transpose needs a handle created with with_transpose");
             h = h->trans;
@@ -2982,7 +3077,10 @@ int hcmx_gpu_hmat_matmat(hcmx_hmat* h, double alpha, const double* h_x, uint64_t
 
 int hcmx_gpu_hmat_matvec_device(hcmx_hmat* h, double alpha, const double* d_x, double beta, double* d_y,
                                 void* stream) {
-    return guarded([&] { run_matvec(h, alpha, d_x, beta, d_y, (cudaStream_t)stream); });
+    return guarded([&] {
+        if (h->cplx) throw invalid_argument("hmat: a complex matrix runs through hcmx_gpu_hmat_matmat4_device (two complex columns per product)");
+        run_matvec(h, alpha, d_x, beta, d_y, (cudaStream_t)stream);
+    });
 }
 
 int hcmx_gpu_hmat_matmat4_device(hcmx_hmat* h, double alpha, const double* d_x4, double beta, double* d_y4,
@@ -2997,6 +3095,7 @@ int hcmx_gpu_hmat_matmat4_device(hcmx_hmat* h, double alpha, const double* d_x4,
 int hcmx_gpu_hmat_matvec(hcmx_hmat* h, double alpha, const double* h_x, double beta, double* h_y,
                          int transpose) {
     return guarded([&] {
+        if (h->cplx) throw invalid_argument("hmat: a complex matrix runs through hcmx_gpu_hmat_matmat4_device (two complex columns per product)");
         if (transpose) {  // hmatrix.hpp:128: y (n_cols) := alpha M^T x + beta y
             if (!h->trans) throw invalid_argument("matvec: transpose needs a handle created with with_transpose");
             h = h->trans;

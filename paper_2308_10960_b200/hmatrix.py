@@ -100,6 +100,9 @@ class FlatHMatrix:
     blob: object              # np.uint8 (host) or torch.uint8 (cuda)
     raw: np.ndarray | None = None
     meta: dict = field(default_factory=dict)
+    # complex matrices (config 5, complex_flat): per leaf, 1 for the imaginary part
+    # of a dense block; None for real matrices
+    imag: np.ndarray | None = None
 
     # oracle-facing views
     @property
@@ -272,7 +275,12 @@ def flat_desc(flat: FlatHMatrix, row_range=None, with_transpose=False, nrhs_bloc
     d.row_begin, d.row_end = (0, 0) if row_range is None else row_range
     d.with_transpose = int(with_transpose)
     d.nrhs_block = int(nrhs_block)  # 4: matmat decodes once for 4 right-hand sides
-    return d, (keep, sigma, desc, blob)
+    imag = None
+    if flat.imag is not None:  # a complex matrix: [Ur Ui] / [Vr Vi] lowrank leaves, Re / Im dense leaves
+        imag = np.ascontiguousarray(flat.imag, dtype=np.uint8)
+        d.complex_pairs = 1
+        d.dense_imag = imag.ctypes.data_as(C.POINTER(C.c_uint8))
+    return d, (keep, sigma, desc, blob, imag)
 
 
 class HMatrix:
@@ -397,67 +405,96 @@ def build_config_complex(cfg, scheme="afl", device=None, n=None, seed=1, eps=Non
     return fr, fi, info
 
 
-class ComplexHMatrix:
-    """A = Ar + i Ai (config 5): two device-resident real H-matrices on one tree
-    whose factors hold the real and imaginary parts as separate codec streams.
-    Y = A X for complex X (n x r): [Ar; Ai] applied to [Re X, Im X] (one fused
-    product per real column), combined as Re Y = Ar Re X - Ai Im X,
-    Im Y = Ar Im X + Ai Re X."""
+def complex_flat(fr: FlatHMatrix, fi: FlatHMatrix) -> FlatHMatrix:
+    """One complex H-matrix from the real / imaginary pair of assemble_complex:
+    every lowrank leaf of fr already holds A's truncated SVD as W = [Ur Ui], X =
+    [Vr Vi], sigma = [S S] (fi's lowrank leaves, [Ui -Ur], are the same streams up
+    to signs and are dropped); dense leaves are fr's (Re) plus fi's (Im, flagged
+    in `imag`).  Each real / imaginary stream is stored -- and decoded -- once."""
+    if fr.n_rows != fi.n_rows or fr.nleaves != fi.nleaves or not np.array_equal(fr.kind, fi.kind):
+        raise ValueError("complex_flat: the real and imaginary parts must share one block tree")
+    dl = np.nonzero(fi.kind == 0)[0]
+    fb = fi.buf0[dl]
+    nb = fr.desc.size
+    br, bi = fr.blob, fi.blob
+    if isinstance(br, torch.Tensor) != isinstance(bi, torch.Tensor):
+        raise ValueError("complex_flat: both blobs on the device or both on the host")
+    base = (int(br.numel() if isinstance(br, torch.Tensor) else br.size) + 15) // 16 * 16
+    if isinstance(br, torch.Tensor):
+        pad = torch.zeros(base - br.numel(), dtype=torch.uint8, device=br.device)
+        blob = torch.cat([br, pad, bi])
+    else:
+        blob = np.concatenate([br, np.zeros(base - br.size, np.uint8), bi])
+    cat = lambda a, b: np.concatenate([np.asarray(a), np.asarray(b)])
+    z = np.zeros(dl.size, np.int64)
+    return FlatHMatrix(fr.n_rows, fr.n_cols, cat(fr.row0, fi.row0[dl]), cat(fr.row1, fi.row1[dl]),
+                       cat(fr.col0, fi.col0[dl]), cat(fr.col1, fi.col1[dl]), cat(fr.kind, z), cat(fr.rank, z),
+                       cat(fr.buf0, nb + np.arange(dl.size, dtype=np.int64)), cat(fr.sig0, z), fr.sigma,
+                       np.concatenate([fr.desc, fi.desc[fb]]), cat(fr.count, fi.count[fb]),
+                       cat(fr.poff, fi.poff[fb] + base), cat(fr.plen, fi.plen[fb]), blob,
+                       meta=dict(fr.meta, complex=True),
+                       imag=np.concatenate([np.zeros(fr.nleaves, np.uint8), np.ones(dl.size, np.uint8)]))
 
-    def __init__(self, fr: FlatHMatrix, fi: FlatHMatrix, nrhs_block: int = 4):
-        self.re, self.im = HMatrix(fr, nrhs_block=nrhs_block), HMatrix(fi, nrhs_block=nrhs_block)
-        self.n_rows, self.n_cols = self.re.n_rows, self.re.n_cols
+
+class ComplexHMatrix:
+    """A = Ar + i Ai (config 5) as ONE device-resident complex arena (complex_flat:
+    hcmx_hmat_desc::complex_pairs): each real / imaginary factor or block stream
+    is decoded once per product and feeds the real and the imaginary output.
+    Products take two complex columns at a time through the 4-RHS kernels
+    ([Re x1, Im x1, Re x2, Im x2] in, [Re y1, Im y1, Re y2, Im y2] out); the
+    complex combination of the X^T x halves runs on the device between the
+    phases (k_ccombine), so Y = A X needs no host arithmetic."""
+
+    def __init__(self, fr: FlatHMatrix, fi: FlatHMatrix | None = None):
+        cf = fr if fi is None else complex_flat(fr, fi)
+        if cf.imag is None:
+            raise ValueError("ComplexHMatrix: a complex flat (complex_flat) or the real / imaginary pair")
+        self.h = HMatrix(cf, nrhs_block=4)
+        self.n_rows, self.n_cols = self.h.n_rows, self.h.n_cols
 
     def close(self):
-        self.re.close()
-        self.im.close()
+        self.h.close()
+
+    def memory(self):
+        return self.h.memory()
+
+    def matmat_device(self, X: torch.Tensor, Y: torch.Tensor | None = None, alpha: complex = 1.0,
+                      beta: complex = 0.0) -> torch.Tensor:
+        """Y := alpha A X + beta Y for complex128 cuda X (n x r), two columns per
+        device product"""
+        if X.dtype != torch.complex128 or not X.is_cuda or X.ndim != 2 or X.shape[0] != self.n_cols:
+            raise ValueError("matmat_device: complex128 cuda X (n_cols x r) required")
+        r, n = X.shape[1], self.n_rows
+        if Y is None:
+            Y = torch.zeros(n, r, dtype=torch.complex128, device="cuda")
+        elif Y.dtype != torch.complex128 or Y.shape != (n, r):
+            raise ValueError("matmat_device: Y must be complex128 n_rows x r")
+        X4 = torch.zeros(self.n_cols, 4, dtype=torch.float64, device="cuda")
+        Y4 = torch.empty(n, 4, dtype=torch.float64, device="cuda")
+        for j in range(0, r, 2):
+            m = min(2, r - j)
+            if m < 2:
+                X4.zero_()
+            X4[:, 0: 2 * m].copy_(torch.view_as_real(X[:, j: j + m]).reshape(self.n_cols, 2 * m))
+            self.h.matmat4_device(1.0, X4, 0.0, Y4)
+            AX = torch.view_as_complex(Y4.view(n, 2, 2))[:, :m]
+            if beta == 0:
+                Y[:, j: j + m] = alpha * AX if alpha != 1 else AX
+            else:
+                Y[:, j: j + m] = alpha * AX + beta * Y[:, j: j + m]
+        return Y
 
     def matmat(self, alpha: complex, X, beta: complex, Y):
         """Y := alpha A X + beta Y (host complex128, X: n x r or n)"""
         X = np.asarray(X, dtype=np.complex128)
-        Y = np.asarray(Y)
         vec = X.ndim == 1
         X2 = X[:, None] if vec else X
         if X2.shape[0] != self.n_cols or Y.shape != ((self.n_rows,) if vec else (self.n_rows, X2.shape[1])):
             raise ValueError("matmat: dimension mismatch")
-        r = X2.shape[1]
-        XX = np.asfortranarray(np.concatenate([X2.real, X2.imag], axis=1))   # [Re X, Im X]
-        Pr = np.zeros((self.n_rows, 2 * r), order="F")
-        Pi = np.zeros((self.n_rows, 2 * r), order="F")
-        self.re.matmat(1.0, XX, 0.0, Pr)
-        self.im.matmat(1.0, XX, 0.0, Pi)
-        AX = (Pr[:, :r] - Pi[:, r:]) + 1j * (Pr[:, r:] + Pi[:, :r])
-        out = alpha * AX + (beta * (Y[:, None] if vec else Y) if beta != 0 else 0.0)
-        out = out[:, 0] if vec else out
-        Y[...] = out
+        Yd = torch.as_tensor(np.ascontiguousarray(Y).reshape(self.n_rows, -1)).cuda()
+        out = self.matmat_device(torch.as_tensor(np.ascontiguousarray(X2)).cuda(), Yd, alpha, beta).cpu().numpy()
+        Y[...] = out[:, 0] if vec else out
         return Y
 
     def matvec(self, alpha: complex, x, beta: complex, y):
         return self.matmat(alpha, x, beta, y)
-
-    def matmat_device(self, X: torch.Tensor, Y: torch.Tensor | None = None) -> torch.Tensor:
-        """Y = A X on the device for complex128 cuda X (n x r): blocks of two complex
-        columns go through both real 4-RHS arenas as [Re x1, Im x1, Re x2, Im x2]
-        (every packed field decoded once per block), and the real / imaginary
-        parts are combined on the device: Re y = Ar Re x - Ai Im x,
-        Im y = Ar Im x + Ai Re x.  Needs handles built with nrhs_block = 4."""
-        if X.dtype != torch.complex128 or not X.is_cuda or X.shape[0] != self.n_cols:
-            raise ValueError("matmat_device: complex128 cuda X with n_cols rows required")
-        r = X.shape[1]
-        n = self.n_rows
-        if Y is None:
-            Y = torch.empty(n, r, dtype=torch.complex128, device="cuda")
-        X4 = torch.zeros(self.n_cols, 4, dtype=torch.float64, device="cuda")
-        Pr = torch.empty(n, 4, dtype=torch.float64, device="cuda")
-        Pi = torch.empty_like(Pr)
-        for j in range(0, r, 2):
-            m = min(2, r - j)
-            X4.zero_()
-            X4[:, 0: 2 * m].copy_(torch.view_as_real(X[:, j: j + m]).reshape(self.n_cols, 2 * m))
-            self.re.matmat4_device(1.0, X4, 0.0, Pr)
-            self.im.matmat4_device(1.0, X4, 0.0, Pi)
-            for q in range(m):
-                yr = Pr[:, 2 * q] - Pi[:, 2 * q + 1]
-                yi = Pr[:, 2 * q + 1] + Pi[:, 2 * q]
-                Y[:, j + q] = torch.complex(yr, yi)
-        return Y

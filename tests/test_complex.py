@@ -94,3 +94,36 @@ def test_complex_matmat_device_16_rhs(gpu, oracle):
         ref = yr + 1j * yi
         assert np.linalg.norm(Y[:, j] - ref) <= TOL * np.linalg.norm(ref), j
     H.close()
+
+
+@pytest.mark.gpu
+def test_complex_arena_decodes_each_stream_once(gpu, oracle):
+    """the complex arena holds every real / imaginary stream once (the lowrank
+    bytes of one real H-matrix -- the other's [Ui -Ur] factors are the same
+    streams -- plus both dense parts), odd column counts and beta != 0 work, and
+    the real-vector entry points refuse a complex handle"""
+    from paper_2308_10960_b200.hmatrix import ComplexHMatrix, HMatrix, compress_in_place, complex_flat
+    n, r = 2048, 3
+    P, lv, K, Ar, Ai = _setup(n, "cuda")
+    fr, fi = compress_in_place(Ar, 1e-6, "afl-aplr"), compress_in_place(Ai, 1e-6, "afl-aplr")
+    H = ComplexHMatrix(complex_flat(fr, fi))
+    Hr, Hi = HMatrix(fr), HMatrix(fi)
+    mc, mr, mi = H.memory(), Hr.memory(), Hi.memory()
+    assert mc.lowrank_compressed == mr.lowrank_compressed
+    assert mc.dense_compressed == mr.dense_compressed + mi.dense_compressed
+    Hr.close()
+    Hi.close()
+    rng = np.random.default_rng(3)
+    X = rng.uniform(-1, 1, (n, r)) + 1j * rng.uniform(-1, 1, (n, r))
+    Y0 = rng.standard_normal((n, r)) + 1j * rng.standard_normal((n, r))
+    Yd = H.matmat_device(torch.as_tensor(X).cuda(), torch.as_tensor(Y0).cuda(), alpha=2.0 - 1.0j, beta=0.5j)
+    hr, hi = fr.host(), fi.host()
+    mv = lambda h, v: oracle.hmat_matvec(h, 1.0, v, 0.0, np.zeros(n), threads=4)
+    Y = Yd.cpu().numpy()
+    for j in range(r):
+        xr, xi = X[:, j].real.copy(), X[:, j].imag.copy()
+        ref = (2.0 - 1.0j) * ((mv(hr, xr) - mv(hi, xi)) + 1j * (mv(hr, xi) + mv(hi, xr))) + 0.5j * Y0[:, j]
+        assert np.linalg.norm(Y[:, j] - ref) <= TOL * np.linalg.norm(ref), j
+    with pytest.raises(ValueError):
+        H.h.matvec(1.0, np.zeros(n), 0.0, np.zeros(n))
+    H.close()
