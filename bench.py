@@ -442,6 +442,9 @@ def run_ours(args, rank, world, local):
                 "fp64_frac": round(tf / fp64_peak, 3) if fp64_peak else None,
                 "note": "matmat4_device: Y = A X for 4 interleaved columns, one decode per field"}
         H4.close()
+    cplx = None
+    if world == 1 and not args.no_complex:
+        cplx = complex_bench(args)
     line = None
     data_s, workload_s = workload_strings(args.config, n, args.scheme)
     if rank == 0:
@@ -504,6 +507,8 @@ def run_ours(args, rank, world, local):
             line["codec"] = codec_res
         if rhs4:
             line["multi_rhs"] = rhs4
+        if cplx:
+            line["complex"] = cplx
         print(json.dumps(line), flush=True)
     H.close()
     if world > 1:
@@ -512,6 +517,62 @@ def run_ours(args, rank, world, local):
         _lib().hcmx_gpu_nccl_comm_destroy(comm)
         dist.destroy_process_group()
     return line
+
+
+def complex_bench(args, reps=5):
+    """BASELINE config 5: Helmholtz exp(i kappa r)/(4 pi r), kappa 16, n = 262144
+    sphere points, eps 1e-6, 16 complex right-hand sides U[-1,1] + i U[-1,1],
+    through ONE complex arena (ComplexHMatrix: every real / imaginary stream
+    decoded once per product of two complex columns, complex combination on the
+    device).  FP64-bound: reported as FP64 TFLOP/s executed against
+    the measured DFMA peak; parity of one column against the CPU oracle applied
+    to the same compressed real / imaginary matrices (checker only, untimed)."""
+    import torch
+    from paper_2308_10960_b200.hmatrix import ComplexHMatrix, build_config_complex
+    t0 = time.time()
+    fr, fi, info = build_config_complex("5")
+    H = ComplexHMatrix(fr, fi)
+    setup = time.time() - t0
+    n, r = H.n_rows, 16
+    rng = np.random.default_rng(5)
+    X = rng.uniform(-1, 1, (n, r)) + 1j * rng.uniform(-1, 1, (n, r))
+    Xd = torch.as_tensor(X).cuda()
+    Y = torch.empty(n, r, dtype=torch.complex128, device="cuda")
+    for _ in range(2):
+        H.matmat_device(Xd, Y)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        H.matmat_device(Xd, Y)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    rep = H.memory()
+    # every stored real entry: 2 flops per real right-hand-side slot, 4 slots per
+    # product of two complex columns, r / 2 products
+    flops = 2.0 * (rep.uncompressed_equivalent / 8) * 4 * (r // 2)
+    tf = flops / (ms / 1e3) / 1e12
+    pk = os.path.join(ROOT, "profiles", "r1_fp64_peak.json")
+    peak = json.load(open(pk)).get("fp64_fma_tflops") if os.path.exists(pk) else None
+    out = {"workload": "config5: Helmholtz kappa=16 sphere n=%d, leaf 64, eta 2, eps 1e-6, AFL-APLR, 16 complex RHS" % n,
+           "ms_per_16rhs_product": round(ms, 3), "fp64_tflops": round(tf, 3), "fp64_peak_tflops": peak,
+           "fp64_frac": round(tf / peak, 3) if peak else None,
+           "compressed_bytes": int(rep.algorithmic_bytes), "setup_s": round(setup, 1),
+           "note": "one complex arena; per product of two complex columns every stream is decoded once"}
+    if not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from oracle import Oracle
+        o, th = Oracle(), os.cpu_count() or 1
+        frh, fih = fr.host(), fi.host()
+        j = r - 1
+        mv = lambda h, v: o.hmat_matvec(h, 1.0, np.ascontiguousarray(v), 0.0, np.zeros(n), threads=th)
+        ref = (mv(frh, X[:, j].real) - mv(fih, X[:, j].imag)) + 1j * (mv(frh, X[:, j].imag) + mv(fih, X[:, j].real))
+        yj = Y[:, j].cpu().numpy()
+        out["parity"] = {"rel_err": float(np.linalg.norm(yj - ref) / np.linalg.norm(ref)), "tol": 1e-12,
+                         "vs": "port CPU oracle on the same compressed real / imaginary matrices, column 16"}
+    H.close()
+    return out
 
 
 def run_reference(args, rank, world):
@@ -636,6 +697,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-codec", action="store_true")
     ap.add_argument("--no-rhs4", action="store_true")
+    ap.add_argument("--no-complex", action="store_true", help="skip the config-5 complex multi-RHS measurement")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank, world, local = dist_env()
