@@ -67,6 +67,14 @@ def _svd_chunk(a):
         return np.linalg.svd(a, full_matrices=False)
 
 
+def _host_workers() -> int:
+    """host workers for this process: the cores divided among the GPU ranks of the
+    node (torchrun's LOCAL_WORLD_SIZE), so N ranks setting up at once do not
+    oversubscribe the host"""
+    local = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1") or 1))
+    return max(1, min(32, (os.cpu_count() or 1) // local))
+
+
 def _pool():
     """worker processes for host LAPACK (numpy's batched SVD does not scale over
     threads: measured 1.4x on 16 threads vs 6.6x on 16 processes); forkserver
@@ -75,7 +83,7 @@ def _pool():
     if _POOL is None:
         import multiprocessing as mp
         from concurrent.futures import ProcessPoolExecutor
-        _POOL = ProcessPoolExecutor(max(1, min(32, os.cpu_count() or 1)), mp_context=mp.get_context("forkserver"))
+        _POOL = ProcessPoolExecutor(_host_workers(), mp_context=mp.get_context("forkserver"))
     return _POOL
 
 
@@ -85,8 +93,8 @@ def _cpu_svd(M: torch.Tensor):
     go to a process pool, small ones run in this process."""
     from concurrent.futures import ThreadPoolExecutor
     a = M.detach().resolve_conj().cpu().numpy()
-    if a.shape[0] >= 2048 and (os.cpu_count() or 1) > 2:
-        parts = np.array_split(a, 4 * (os.cpu_count() or 1))
+    if a.shape[0] >= 2048 and _host_workers() > 2:
+        parts = np.array_split(a, 4 * _host_workers())
         res = list(_pool().map(_svd_chunk, parts))
         dev = M.device
         cat = lambda i: torch.from_numpy(np.concatenate([r[i] for r in res])).to(dev)
@@ -95,7 +103,7 @@ def _cpu_svd(M: torch.Tensor):
     U = np.empty(a.shape[:-1] + (min(a.shape[-2:]),), a.dtype)
     S = np.empty((B, min(a.shape[-2:])))
     Vh = np.empty((B, min(a.shape[-2:]), a.shape[-1]), a.dtype)
-    nt = min(32, os.cpu_count() or 1)
+    nt = _host_workers()
     cuts = np.linspace(0, B, nt + 1).astype(int)
 
     def work(i):
