@@ -206,17 +206,18 @@ typedef struct hcmx_hmat_desc {
     uint64_t row_begin, row_end;
     /* nonzero: also build M^T (hmatrix.hpp:128 transpose; whole matrix only) */
     int with_transpose;
-    /* 4: also lay the matrix out for products with 4 right-hand sides at once
-     * (hcmx_gpu_hmat_matmat decodes every field once for 4 columns); 0: off */
+    /* 4 or 8: also lay the matrix out for products with 4 / 8 right-hand sides
+     * at once (hcmx_gpu_hmat_matmat decodes every field once per block of
+     * nrhs_block columns); 0: off */
     int nrhs_block;
     /* nonzero: a COMPLEX matrix A = Ar + i Ai stored once with real codec streams
-     * (BASELINE config 5; needs nrhs_block = 4, no transpose).  Lowrank leaves
+     * (BASELINE config 5; needs nrhs_block = 4 or 8, no transpose).  Lowrank leaves
      * (kind 1) hold A's truncated SVD U S V^H as W = [Ur Ui], X = [Vr Vi] and
      * sigma = [S S] (rank 2k: every real / imaginary factor column is its own
      * APLR stream, decoded once per product); dense leaves are Re A (imag 0) and
-     * Im A (dense_imag[l] = 1, same row / column range).  The 4-RHS products then
-     * take two complex columns interleaved, [Re x1, Im x1, Re x2, Im x2], and
-     * return [Re y1, Im y1, Re y2, Im y2]; the complex combination of the
+     * Im A (dense_imag[l] = 1, same row / column range).  The block products then
+     * take nrhs_block / 2 complex columns interleaved, [Re x1, Im x1, Re x2, ...],
+     * and return [Re y1, Im y1, Re y2, ...]; the complex combination of the
      * X^T x halves runs on the device between the phases. */
     int complex_pairs;
     const uint8_t* dense_imag; /* [nleaves], or NULL */
@@ -308,6 +309,12 @@ int hcmx_gpu_hmat_matvec_device(hcmx_hmat* h, double alpha, const double* d_x, d
  * hcmx_gpu_hmat_matvec_device.  C5's multi-RHS products. */
 int hcmx_gpu_hmat_matmat4_device(hcmx_hmat* h, double alpha, const double* d_x4, double beta, double* d_y4,
                                  void* stream);
+/* the same with the handle's nrhs_block (4 or 8) columns interleaved: x is
+ * n_cols x nrhs_block, y n_rows x nrhs_block, row-major, 16-byte aligned */
+int hcmx_gpu_hmat_matmat_block_device(hcmx_hmat* h, double alpha, const double* d_x, double beta,
+                                      double* d_y, void* stream);
+/* the right-hand sides per product of the handle's multi-RHS arena (0: none) */
+int hcmx_gpu_hmat_nrhs_block(const hcmx_hmat* h);
 
 /* the handle of M^T inside a handle created with with_transpose (owned by h;
  * use it with the _device / _timing calls) */

@@ -115,6 +115,8 @@ PROTOTYPES = {
     "hcmx_gpu_hmat_matmat": (_i, [_vp, _d, _vp, _u64, _u64, _d, _vp, _u64, _i]),
     "hcmx_gpu_hmat_matvec_device": (_i, [_vp, _d, _vp, _d, _vp, _vp]),
     "hcmx_gpu_hmat_matmat4_device": (_i, [_vp, _d, _vp, _d, _vp, _vp]),
+    "hcmx_gpu_hmat_matmat_block_device": (_i, [_vp, _d, _vp, _d, _vp, _vp]),
+    "hcmx_gpu_hmat_nrhs_block": (_i, [_vp]),
     "hcmx_gpu_hmat_transposed": (_i, [_vp, C.POINTER(_vp)]),
     "hcmx_gpu_hmat_export_buffer": (_i, [_vp, _u64, _vp, _u64, _pu64]),
     "hcmx_gpu_hmat_last_launches": (_i, [_vp]),

@@ -203,10 +203,11 @@ template <int R>
 __host__ __device__ constexpr int rec_bytes() { return R == 1 ? 32 : (8 * R + 16 + 15) / 16 * 16; }
 constexpr uint32_t kMaxPieces = 4;  // pieces a phase-B row block may be split into
 constexpr int kMultiR = 4;    // right-hand sides per product of a multi-RHS arena
+constexpr int kMultiR2 = 8;   // ... of the wide multi-RHS arena (nrhs_block = 8)
 constexpr int kNWBMulti = HCMX_NWB_MULTI;  // phase-B consumer warps for R > 1 (R x 4 accumulators per lane)
 inline uint32_t rec_bytes_rt(int R) { return R == 1 ? 32u : static_cast<uint32_t>((8 * R + 16 + 15) / 16 * 16); }
 template <int R>
-__host__ __device__ constexpr int nwb() { return R == 1 ? HCMX_NWB : kNWBMulti; }
+__host__ __device__ constexpr int nwb() { return R == 1 ? HCMX_NWB : (R == 4 ? kNWBMulti : 6); }  // R = 8: 4 R accumulators per lane
 
 struct BItem {
     uint32_t word_off;   // packed data, from the warp-stage start
@@ -777,21 +778,35 @@ __device__ __forceinline__ void a_fast(const uint32_t* data, unsigned P, unsigne
     for (unsigned g = 0; g < ngroups; ++g) {
         uint32_t lo[kARows], hi[kARows];
         il_load<kARows>(q, o, lo, hi);
-        double xv[kARows * R];
+        if constexpr (R >= 8) {  // the x values row by row (R doubles per row)
 #pragma unroll
-        for (int i = 0; i < kARows * R / 2; ++i) {
-            const double2 t = reinterpret_cast<const double2*>(xs)[2 * R * g + i];
-            xv[2 * i] = t.x;
-            xv[2 * i + 1] = t.y;
-        }
+            for (int r = 0; r < kARows; ++r) {
+                const double d = dec_pair(lo[r], hi[r], s, mask, mul, bias);
+                const double2* xr = reinterpret_cast<const double2*>(xs) + (kARows * g + r) * (R / 2);
 #pragma unroll
-        for (int r = 0; r < kARows; ++r) {
-            const double d = dec_pair(lo[r], hi[r], s, mask, mul, bias);
-            if (R == 1) {
-                acc[r] = fma(d, xv[r], acc[r]);
-            } else {
+                for (int i = 0; i < R / 2; ++i) {
+                    const double2 t = xr[i];
+                    acc[2 * i] = fma(d, t.x, acc[2 * i]);
+                    acc[2 * i + 1] = fma(d, t.y, acc[2 * i + 1]);
+                }
+            }
+        } else {
+            double xv[kARows * R];
 #pragma unroll
-                for (int c = 0; c < R; ++c) acc[c % NA] = fma(d, xv[r * R + c], acc[c % NA]);
+            for (int i = 0; i < kARows * R / 2; ++i) {
+                const double2 t = reinterpret_cast<const double2*>(xs)[2 * R * g + i];
+                xv[2 * i] = t.x;
+                xv[2 * i + 1] = t.y;
+            }
+#pragma unroll
+            for (int r = 0; r < kARows; ++r) {
+                const double d = dec_pair(lo[r], hi[r], s, mask, mul, bias);
+                if (R == 1) {
+                    acc[r] = fma(d, xv[r], acc[r]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < R; ++c) acc[c % NA] = fma(d, xv[r * R + c], acc[c % NA]);
+                }
             }
         }
         q += gwords;
@@ -1305,25 +1320,29 @@ struct CPair {
 };
 static_assert(sizeof(CPair) == 32, "CPair layout");
 
-__global__ void k_xswap(const double* __restrict__ x4, double* __restrict__ x2, uint64_t n) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (uint64_t)blockDim.x) {
-        const double2 u = reinterpret_cast<const double2*>(x4)[2 * i], v = reinterpret_cast<const double2*>(x4)[2 * i + 1];
-        reinterpret_cast<double2*>(x2)[2 * i] = make_double2(-u.y, u.x);
-        reinterpret_cast<double2*>(x2)[2 * i + 1] = make_double2(-v.y, v.x);
+// x: n x R row-major, R / 2 complex columns interleaved (Re, Im): each (Re, Im)
+// pair becomes (-Im, Re)
+__global__ void k_xswap(const double* __restrict__ x, double* __restrict__ x2, uint64_t npairs) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * (uint64_t)blockDim.x) {
+        const double2 u = reinterpret_cast<const double2*>(x)[i];
+        reinterpret_cast<double2*>(x2)[i] = make_double2(-u.y, u.x);
     }
 }
 
+template <int R>
 __global__ void k_ccombine(Params p, const CPair* __restrict__ cp, uint32_t n) {
     pdl_trigger();
     pdl_wait();  // phase A (and k_reduce) wrote the X^T x halves
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const CPair q = cp[i];
-        double* ra = rec_c<kMultiR>(p, q.a);
-        double* rb = rec_c<kMultiR>(p, q.b);
-        const double tr1 = q.sig * (ra[0] + rb[1]), ti1 = q.sig * (ra[1] - rb[0]);
-        const double tr2 = q.sig * (ra[2] + rb[3]), ti2 = q.sig * (ra[3] - rb[2]);
-        ra[0] = q.sa * tr1, ra[1] = q.sa * ti1, ra[2] = q.sa * tr2, ra[3] = q.sa * ti2;
-        rb[0] = -q.sb * ti1, rb[1] = q.sb * tr1, rb[2] = -q.sb * ti2, rb[3] = q.sb * tr2;
+        double* ra = rec_c<R>(p, q.a);
+        double* rb = rec_c<R>(p, q.b);
+#pragma unroll
+        for (int c = 0; c < R; c += 2) {  // complex column c / 2
+            const double tr = q.sig * (ra[c] + rb[c + 1]), ti = q.sig * (ra[c + 1] - rb[c]);
+            ra[c] = q.sa * tr, ra[c + 1] = q.sa * ti;
+            rb[c] = -q.sb * ti, rb[c + 1] = q.sb * tr;
+        }
     }
 }
 
@@ -2328,7 +2347,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                 uint32_t G = 1;
                 // R right-hand sides stage R x slices per chunk: smaller segments
                 // keep a segment's x (G chunks x 64 rows x R doubles) a fraction of a slot
-                const uint32_t gmax = h->R == 1 ? static_cast<uint32_t>(kAGroupMax) : kAGroupMaxMulti;
+                const uint32_t gmax = h->R == 1 ? static_cast<uint32_t>(kAGroupMax) : (h->R == kMultiR ? kAGroupMaxMulti : 1u);
                 while (2 * G <= gmax && nfull % (2 * G) == 0) G *= 2;
                 const uint32_t ngrp = nfull / G + (rag ? 1u : 0u);
                 L.colbase = ncols;
@@ -2518,7 +2537,8 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                 }
             }
             if (h->R == 1) B.emit_stripe<BItem, kBLRGroup, kNWB>(specs, B.bitems);
-            else B.emit_stripe<BItem, kBLRGroup, kNWBMulti>(specs, B.bitems);
+            else if (h->R == kMultiR) B.emit_stripe<BItem, kBLRGroup, nwb<kMultiR>()>(specs, B.bitems);
+            else B.emit_stripe<BItem, kBLRGroup, nwb<kMultiR2>()>(specs, B.bitems);
             stripe_b.push_back(static_cast<uint32_t>(B.stages.size()));
         }
     }
@@ -2642,7 +2662,7 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     if (h->cplx) {
         h->ncpairs = static_cast<uint32_t>(pairs.size());
         up(h->cpairs, pairs.data(), pairs.size() * sizeof(CPair));
-        h->xswap.alloc((d.n_cols + 4) * kMultiR * 8);
+        h->xswap.alloc((d.n_cols + 4) * h->R * 8);
         check_cuda(cudaMemsetAsync(h->xswap.p, 0, h->xswap.bytes, s), "memset");
     }
     h->xpad.alloc((d.n_cols + 4) * 8);
@@ -2713,6 +2733,10 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
                        "smem attr");
             check_cuda(cudaFuncSetAttribute(k_phase_b<kMultiR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
                        "smem attr");
+            check_cuda(cudaFuncSetAttribute(k_phase_a<kMultiR2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sma),
+                       "smem attr");
+            check_cuda(cudaFuncSetAttribute(k_phase_b<kMultiR2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+                       "smem attr");
             check_cuda(cudaDeviceGetAttribute(&di.nsm, cudaDevAttrMultiProcessorCount, dev), "SM count");
             di.ready = true;
         }
@@ -2748,8 +2772,9 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
     if (direct) p.x = dx;
     if (h->cplx) {  // the swapped right-hand sides of the imaginary dense parts
         p.x2 = h->xswap.as<double>();
-        k_xswap<<<static_cast<int>(std::min<uint64_t>((h->n_cols + 255) / 256, 4ull * nsm)), 256, 0, s>>>(
-            dx, h->xswap.as<double>(), h->n_cols);
+        const uint64_t npairs = h->n_cols * R / 2;
+        k_xswap<<<static_cast<int>(std::min<uint64_t>((npairs + 255) / 256, 4ull * nsm)), 256, 0, s>>>(
+            dx, h->xswap.as<double>(), npairs);
         check_cuda(cudaGetLastError(), "xswap launch");
         h->last_launches++;
     }
@@ -2785,22 +2810,20 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
     const uint32_t gr = (h->nred_long + 7) / 8 + (h->nred - h->nred_long + 255) / 256;
     const RedCol* rc = h->redcols.as<RedCol>();
     const uint32_t gc = static_cast<uint32_t>(std::min<uint64_t>(((h->re - h->rb) * R + 255) / 256, 4 * nsm));
-    if (R == 1) {
-        if (run_a) launch(k_phase_a<1>, ga, kThreadsA, kSmemBytesA, false, p);
-        if (h->nred) launch(k_reduce<1>, gr, 256, 0, true, p, rc, h->nred_long, h->nred);
-        if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
-        if (h->nblocks) launch(k_phase_b<1>, gb, (nwb<1>() + 1) * 32, kSmemBytes, run_a, p);
-        if (h->pieces) launch(k_combine<1>, gc, 256, 0, true, p, h->npieces.as<uint8_t>());
-    } else {
-        if (run_a) launch(k_phase_a<kMultiR>, ga, kThreadsA, kSmemBytesA, false, p);
-        if (h->nred) launch(k_reduce<kMultiR>, gr, 256, 0, true, p, rc, h->nred_long, h->nred);
-        if (h->cplx && h->ncpairs)
-            launch(k_ccombine, std::min<uint32_t>((h->ncpairs + 255) / 256, 8 * nsm), 256, 0, true, p,
+    auto chain = [&](auto rt) {
+        constexpr int RR = decltype(rt)::value;
+        if (run_a) launch(k_phase_a<RR>, ga, kThreadsA, kSmemBytesA, false, p);
+        if (h->nred) launch(k_reduce<RR>, gr, 256, 0, true, p, rc, h->nred_long, h->nred);
+        if (RR > 1 && h->cplx && h->ncpairs)
+            launch(k_ccombine<RR>, std::min<uint32_t>((h->ncpairs + 255) / 256, 8 * nsm), 256, 0, true, p,
                    h->cpairs.as<CPair>(), h->ncpairs);
         if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
-        if (h->nblocks) launch(k_phase_b<kMultiR>, gb, (nwb<kMultiR>() + 1) * 32, kSmemBytes, run_a, p);
-        if (h->pieces) launch(k_combine<kMultiR>, gc, 256, 0, true, p, h->npieces.as<uint8_t>());
-    }
+        if (h->nblocks) launch(k_phase_b<RR>, gb, (nwb<RR>() + 1) * 32, kSmemBytes, run_a, p);
+        if (h->pieces) launch(k_combine<RR>, gc, 256, 0, true, p, h->npieces.as<uint8_t>());
+    };
+    if (R == 1) chain(std::integral_constant<int, 1>{});
+    else if (R == kMultiR) chain(std::integral_constant<int, kMultiR>{});
+    else chain(std::integral_constant<int, kMultiR2>{});
     check_cuda(cudaGetLastError(), "matvec launch");
 #ifdef HCMX_PROF
     static const bool prof_env = std::getenv("HCMX_PROF") != nullptr;
@@ -2958,13 +2981,14 @@ hcmx_hmat* create_handle(const hcmx_hmat_desc& d) {
         if (d.complex_pairs) {
             // a complex matrix exists only as the 4-RHS arena (two complex columns per
             // product); the outer handle is a shell that forwards to it
-            if (d.nrhs_block != kMultiR) throw invalid_argument("hmat: a complex matrix needs nrhs_block = 4");
+            if (d.nrhs_block != kMultiR && d.nrhs_block != kMultiR2)
+                throw invalid_argument("hmat: a complex matrix needs nrhs_block = 4 or 8");
             if (d.with_transpose || d.row_begin || d.row_end)
                 throw invalid_argument("hmat: complex matrices: no transpose, no row partition");
             for (uint64_t l = 0; l < d.nleaves; ++l)
                 if (d.kind[l] == 2) throw invalid_argument("hmat: complex matrices take APLR lowrank leaves (kind 1)");
             h->multi = new hcmx_hmat();
-            h->multi->R = kMultiR;
+            h->multi->R = d.nrhs_block;
             h->multi->cplx = true;
             check_cuda(cudaStreamCreateWithFlags(&h->multi->stream, cudaStreamNonBlocking), "cudaStreamCreate");
             build(d, h->multi);
@@ -2978,9 +3002,10 @@ hcmx_hmat* create_handle(const hcmx_hmat_desc& d) {
         }
         build(d, h);
         if (d.nrhs_block) {
-            if (d.nrhs_block != kMultiR) throw invalid_argument("hmat: nrhs_block must be 0 or 4");
+            if (d.nrhs_block != kMultiR && d.nrhs_block != kMultiR2)
+                throw invalid_argument("hmat: nrhs_block must be 0, 4 or 8");
             h->multi = new hcmx_hmat();
-            h->multi->R = kMultiR;
+            h->multi->R = d.nrhs_block;
             check_cuda(cudaStreamCreateWithFlags(&h->multi->stream, cudaStreamNonBlocking), "cudaStreamCreate");
             build(d, h->multi);
         }
@@ -3035,11 +3060,11 @@ int hcmx_gpu_hmat_matmat(hcmx_hmat* h, double alpha, const double* h_x, uint64_t
         if (ldx < h->n_cols || ldy < h->n_rows) throw invalid_argument("matmat: leading dimension too small");
         if (!nrhs) return;
         if (h->multi && nrhs >= 2) {
-            // blocks of kMultiR columns through the multi-RHS arena: each field is
-            // decoded once for the block (x and y interleaved n x kMultiR; a short
+            // blocks of nrhs_block columns through the multi-RHS arena: each field is
+            // decoded once for the block (x and y interleaved n x nrhs_block; a short
             // last block is padded with zero columns)
             hcmx_hmat* mh = h->multi;
-            constexpr uint64_t B = kMultiR;
+            const uint64_t B = static_cast<uint64_t>(mh->R);
             const uint64_t n = h->n_cols, nr = h->re - h->rb;
             DevBuf dx(n * B * 8), dy(h->n_rows * B * 8);
             std::vector<double> hx(n * B), hy(nr * B);
@@ -3087,10 +3112,22 @@ int hcmx_gpu_hmat_matmat4_device(hcmx_hmat* h, double alpha, const double* d_x4,
                                  void* stream) {
     return guarded([&] {
         if (!h->multi) throw invalid_argument("matmat4: handle created without nrhs_block = 4");
+        if (h->multi->R != kMultiR) throw invalid_argument("matmat4: handle built with nrhs_block = 8 (use matmat_block_device)");
         if (reinterpret_cast<uintptr_t>(d_x4) % 16) throw invalid_argument("matmat4: x must be 16-byte aligned");
         run_matvec(h->multi, alpha, d_x4, beta, d_y4, (cudaStream_t)stream);
     });
 }
+
+int hcmx_gpu_hmat_matmat_block_device(hcmx_hmat* h, double alpha, const double* d_x, double beta, double* d_y,
+                                      void* stream) {
+    return guarded([&] {
+        if (!h->multi) throw invalid_argument("matmat_block: handle created without nrhs_block");
+        if (reinterpret_cast<uintptr_t>(d_x) % 16) throw invalid_argument("matmat_block: x must be 16-byte aligned");
+        run_matvec(h->multi, alpha, d_x, beta, d_y, (cudaStream_t)stream);
+    });
+}
+
+int hcmx_gpu_hmat_nrhs_block(const hcmx_hmat* h) { return h && h->multi ? h->multi->R : 0; }
 
 int hcmx_gpu_hmat_matvec(hcmx_hmat* h, double alpha, const double* h_x, double beta, double* h_y,
                          int transpose) {

@@ -296,6 +296,7 @@ class HMatrix:
         check(lib().hcmx_gpu_hmat_create(C.byref(d), C.byref(h)), "hmat_create")
         self._h = h
         self._keep = None
+        self.nrhs_block = int(lib().hcmx_gpu_hmat_nrhs_block(h))
 
     def close(self):
         if getattr(self, "_h", None):
@@ -324,6 +325,17 @@ class HMatrix:
         check(lib().hcmx_gpu_hmat_matvec_device(self._h, float(alpha), ptr(x), float(beta), ptr(y), s),
               "matvec")
         return y
+
+    def matmat_block_device(self, alpha: float, X: torch.Tensor, beta: float, Y: torch.Tensor):
+        """Y := alpha M X + beta Y with X (n_cols, B), Y (n_rows, B) row-major cuda
+        float64, B = nrhs_block (4 or 8): every field decoded once for the B columns"""
+        B = self.nrhs_block
+        if not B or X.shape != (self.n_cols, B) or Y.shape != (self.n_rows, B) or not (X.is_contiguous() and
+                                                                                     Y.is_contiguous()):
+            raise ValueError("matmat_block: contiguous (n, nrhs_block) float64 tensors required")
+        check(lib().hcmx_gpu_hmat_matmat_block_device(self._h, float(alpha), ptr(X), float(beta), ptr(Y),
+                                                      torch.cuda.current_stream().cuda_stream), "matmat_block")
+        return Y
 
     def matmat4_device(self, alpha: float, X4: torch.Tensor, beta: float, Y4: torch.Tensor):
         """Y4 := alpha M X4 + beta Y4 with X4 (n_cols, 4), Y4 (n_rows, 4) row-major
@@ -440,16 +452,17 @@ class ComplexHMatrix:
     """A = Ar + i Ai (config 5) as ONE device-resident complex arena (complex_flat:
     hcmx_hmat_desc::complex_pairs): each real / imaginary factor or block stream
     is decoded once per product and feeds the real and the imaginary output.
-    Products take two complex columns at a time through the 4-RHS kernels
-    ([Re x1, Im x1, Re x2, Im x2] in, [Re y1, Im y1, Re y2, Im y2] out); the
+    Products take nrhs_block / 2 complex columns at a time through the block
+    kernels ([Re x1, Im x1, Re x2, ...] in, [Re y1, Im y1, ...] out); the
     complex combination of the X^T x halves runs on the device between the
     phases (k_ccombine), so Y = A X needs no host arithmetic."""
 
-    def __init__(self, fr: FlatHMatrix, fi: FlatHMatrix | None = None):
+    def __init__(self, fr: FlatHMatrix, fi: FlatHMatrix | None = None, nrhs_block: int = 4):
         cf = fr if fi is None else complex_flat(fr, fi)
         if cf.imag is None:
             raise ValueError("ComplexHMatrix: a complex flat (complex_flat) or the real / imaginary pair")
-        self.h = HMatrix(cf, nrhs_block=4)
+        self.h = HMatrix(cf, nrhs_block=nrhs_block)
+        self.pairs = nrhs_block // 2  # complex columns per device product
         self.n_rows, self.n_cols = self.h.n_rows, self.h.n_cols
 
     def close(self):
@@ -460,8 +473,8 @@ class ComplexHMatrix:
 
     def matmat_device(self, X: torch.Tensor, Y: torch.Tensor | None = None, alpha: complex = 1.0,
                       beta: complex = 0.0) -> torch.Tensor:
-        """Y := alpha A X + beta Y for complex128 cuda X (n x r), two columns per
-        device product"""
+        """Y := alpha A X + beta Y for complex128 cuda X (n x r), nrhs_block / 2
+        columns per device product"""
         if X.dtype != torch.complex128 or not X.is_cuda or X.ndim != 2 or X.shape[0] != self.n_cols:
             raise ValueError("matmat_device: complex128 cuda X (n_cols x r) required")
         r, n = X.shape[1], self.n_rows
@@ -469,15 +482,16 @@ class ComplexHMatrix:
             Y = torch.zeros(n, r, dtype=torch.complex128, device="cuda")
         elif Y.dtype != torch.complex128 or Y.shape != (n, r):
             raise ValueError("matmat_device: Y must be complex128 n_rows x r")
-        X4 = torch.zeros(self.n_cols, 4, dtype=torch.float64, device="cuda")
-        Y4 = torch.empty(n, 4, dtype=torch.float64, device="cuda")
-        for j in range(0, r, 2):
-            m = min(2, r - j)
-            if m < 2:
-                X4.zero_()
-            X4[:, 0: 2 * m].copy_(torch.view_as_real(X[:, j: j + m]).reshape(self.n_cols, 2 * m))
-            self.h.matmat4_device(1.0, X4, 0.0, Y4)
-            AX = torch.view_as_complex(Y4.view(n, 2, 2))[:, :m]
+        q, B = self.pairs, 2 * self.pairs
+        XB = torch.zeros(self.n_cols, B, dtype=torch.float64, device="cuda")
+        YB = torch.empty(n, B, dtype=torch.float64, device="cuda")
+        for j in range(0, r, q):
+            m = min(q, r - j)
+            if m < q:
+                XB.zero_()
+            XB[:, 0: 2 * m].copy_(torch.view_as_real(X[:, j: j + m]).reshape(self.n_cols, 2 * m))
+            self.h.matmat_block_device(1.0, XB, 0.0, YB)
+            AX = torch.view_as_complex(YB.view(n, q, 2))[:, :m]
             if beta == 0:
                 Y[:, j: j + m] = alpha * AX if alpha != 1 else AX
             else:

@@ -81,7 +81,7 @@ def test_complex_matmat_device_16_rhs(gpu, oracle):
     from paper_2308_10960_b200.hmatrix import ComplexHMatrix, build_config_complex
     n = 4096
     fr, fi, info = build_config_complex("5", n=n)
-    H = ComplexHMatrix(fr, fi)
+    H = ComplexHMatrix(fr, fi, nrhs_block=8)  # 8 real slots: 4 complex columns per device product
     rng = np.random.default_rng(12)
     X = rng.uniform(-1, 1, (n, 16)) + 1j * rng.uniform(-1, 1, (n, 16))
     Y = H.matmat_device(torch.as_tensor(X).cuda()).cpu().numpy()
@@ -106,7 +106,7 @@ def test_complex_arena_decodes_each_stream_once(gpu, oracle):
     n, r = 2048, 3
     P, lv, K, Ar, Ai = _setup(n, "cuda")
     fr, fi = compress_in_place(Ar, 1e-6, "afl-aplr"), compress_in_place(Ai, 1e-6, "afl-aplr")
-    H = ComplexHMatrix(complex_flat(fr, fi))
+    H = ComplexHMatrix(complex_flat(fr, fi), nrhs_block=4)  # 2 complex columns per product
     Hr, Hi = HMatrix(fr), HMatrix(fi)
     mc, mr, mi = H.memory(), Hr.memory(), Hi.memory()
     assert mc.lowrank_compressed == mr.lowrank_compressed

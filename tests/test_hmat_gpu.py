@@ -256,16 +256,19 @@ def test_matmat_multi_rhs(gpu, oracle):
             assert rel(Y[:, j], ref) <= TOL, (tr, j)
 
 
-@pytest.mark.parametrize("mode,scheme,nrhs", [("aplr", 0, 4), ("aplr", 1, 7), ("codec", 2, 5), ("mp", 0, 2)])
-def test_multi_rhs_decode_once(gpu, oracle, mode, scheme, nrhs):
-    """matmat through the 4-right-hand-side arena (every field decoded once per
-    block of 4 columns; a short last block padded): each column equals the
-    oracle's product (ragged clusters, every leaf kind, alpha / beta)"""
+@pytest.mark.parametrize("mode,scheme,nrhs,block", [("aplr", 0, 4, 4), ("aplr", 1, 7, 4), ("codec", 2, 5, 4),
+                                                   ("mp", 0, 2, 4), ("aplr", 0, 11, 8), ("codec", 3, 8, 8),
+                                                   ("mp", 1, 3, 8)])
+def test_multi_rhs_decode_once(gpu, oracle, mode, scheme, nrhs, block):
+    """matmat through the 4- and 8-right-hand-side arenas (every field decoded
+    once per block of columns; a short last block padded): each column equals
+    the oracle's product (ragged clusters, every leaf kind, alpha / beta)"""
     from cpu_hmatrix import build_small_flat
     from paper_2308_10960_b200.hmatrix import HMatrix
     n = 1100
     f, _ = build_small_flat(n=n, eps=1e-6, scheme=scheme, mode=mode, geometry="sphere")
-    H = HMatrix(f.to_product(), nrhs_block=4)
+    H = HMatrix(f.to_product(), nrhs_block=block)
+    assert H.nrhs_block == block
     rng = np.random.default_rng(11)
     X = np.asfortranarray(rng.uniform(-1, 1, (n, nrhs)))
     Y0 = np.asfortranarray(rng.standard_normal((n, nrhs)))

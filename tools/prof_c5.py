@@ -24,12 +24,13 @@ from paper_2308_10960_b200.hmatrix import ComplexHMatrix, build_config_complex  
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 262144
+    block = int(sys.argv[2]) if len(sys.argv) > 2 else 4  # real slots per device product (4 or 8)
     r = 16
     t = time.time()
     fr, fi, info = build_config_complex("5", n=n)
     setup = time.time() - t
     t = time.time()
-    H = ComplexHMatrix(fr, fi)
+    H = ComplexHMatrix(fr, fi, nrhs_block=block)
     create = time.time() - t
     rep = H.memory()
     rng = np.random.default_rng(5)
@@ -55,8 +56,8 @@ def main():
     tf = flops / (ms / 1e3) / 1e12
     pk = os.path.join(ROOT, "profiles", "r1_fp64_peak.json")
     peak = json.load(open(pk)).get("fp64_fma_tflops") if os.path.exists(pk) else None
-    # bytes streamed per 16-RHS product: the arena's algorithmic bytes per 4-slot product x r / 2
-    gbytes = rep.algorithmic_bytes * (r // 2) / 1e9
+    # bytes streamed per 16-RHS product: the arena's algorithmic bytes per block product x 2 r / block
+    gbytes = rep.algorithmic_bytes * (2 * r // block) / 1e9
     from oracle import Oracle
     o = Oracle()
     frh, fih = fr.host(), fi.host()
@@ -69,7 +70,7 @@ def main():
             o.hmat_matvec(fih, 1.0, X[:, j].real, 0.0, np.zeros(n), threads=os.cpu_count())
         ref = yr + 1j * yi
         errs.append(float(np.linalg.norm(Yh[:, j] - ref) / np.linalg.norm(ref)))
-    out = {"config": "5", "n": n, "nrhs": r, "leaves": info["leaves"], "setup_s": round(setup, 1),
+    out = {"config": "5", "n": n, "nrhs": r, "nrhs_block": block, "leaves": info["leaves"], "setup_s": round(setup, 1),
            "create_s": round(create, 1), "compressed_bytes": int(rep.algorithmic_bytes), "arena_bytes": int(rep.device_arena_bytes),
            "ms_per_16rhs_product": round(ms, 3), "fp64_tflops": round(tf, 2), "fp64_peak_tflops": peak,
            "fp64_frac": round(tf / peak, 3) if peak else None, "streamed_gb_per_product": round(gbytes, 2),
