@@ -66,11 +66,14 @@ constexpr int kNWB = HCMX_NWB;            // phase-B consumer warps per CTA
 #ifndef HCMX_NWB_MULTI
 #define HCMX_NWB_MULTI 8
 #endif
+// phase B: a 2-slot ring of 45 KB stages (measured against 3 x 26 KB, 4 x 17 KB and
+// 2 x 40 / 43 KB: the per-stage bookkeeping of the consumer warps costs more than
+// the shallower ring; config 4's phase B 2.29 -> 2.17 ms)
 #ifndef HCMX_NSTAGE
-#define HCMX_NSTAGE 3
+#define HCMX_NSTAGE 2
 #endif
 #ifndef HCMX_STAGE_BYTES
-#define HCMX_STAGE_BYTES 26624
+#define HCMX_STAGE_BYTES 46080
 #endif
 constexpr int kNWA = HCMX_NWA;            // phase-A consumer warps (more registers per thread)
 #ifndef HCMX_AMINB
@@ -87,7 +90,7 @@ constexpr int kItemBytes = 32;            // descriptor size (A and B)
 constexpr int kCoefBytes = 7936;          // staged coefficients + column params per stage
 constexpr int kNStage = HCMX_NSTAGE;      // ring depth (phase B)
 #ifndef HCMX_NSTAGE_A
-#define HCMX_NSTAGE_A HCMX_NSTAGE
+#define HCMX_NSTAGE_A 3  // phase A keeps 3 x 26 KB (2 x 43 KB measured slower)
 #endif
 constexpr int kNStageA = HCMX_NSTAGE_A;   // ring depth of phase A (its CTAs need no reduction buffer)
 template <bool PHASE_A>
@@ -107,7 +110,7 @@ constexpr int kOffHdr = kSlotData;    // slot header written by the producer: st
 constexpr int kSlotBytes = kOffHdr + 16;
 // phase A may use its own (smaller) stages: HCMX_STAGE_BYTES_A / HCMX_COEF_BYTES_A
 #ifndef HCMX_STAGE_BYTES_A
-#define HCMX_STAGE_BYTES_A HCMX_STAGE_BYTES
+#define HCMX_STAGE_BYTES_A 26624
 #endif
 #ifndef HCMX_COEF_BYTES_A
 #define HCMX_COEF_BYTES_A 7936
