@@ -76,6 +76,9 @@ constexpr int kNWB = HCMX_NWB;            // phase-B consumer warps per CTA
 #define HCMX_STAGE_BYTES 46080
 #endif
 constexpr int kNWA = HCMX_NWA;            // phase-A consumer warps (more registers per thread)
+#ifndef HCMX_COSCHED
+#define HCMX_COSCHED 0
+#endif
 #ifndef HCMX_AMINB
 #define HCMX_AMINB 2
 #endif
@@ -2616,9 +2619,43 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
                                           : static_cast<uint32_t>(std::min<uint64_t>(max_pieces, (want + nb_rows - 1) / nb_rows));
     std::vector<std::array<uint32_t, 4>> bv;
     std::vector<uint64_t> bcost;
+    std::vector<uint8_t> dense_only;  // HCMX_COSCHED: stripes that never wait for phase A
     std::vector<uint8_t> npieces(std::max<uint64_t>(nb_rows, 1), 0);
+    // HCMX_COSCHED (experiment, off): every row block with dense and lowrank
+    // stages is cut into two pieces at its first stage that reads phase-A
+    // results, and the dense pieces are claimed first -- phase B's CTAs work on
+    // them while phase A still runs on the same SMs (phase A at one CTA per SM
+    // leaves room for one of B's).  Measured slower: config 4 4.45 vs 3.89 ms
+    // (phase A at one CTA per SM loses more than the overlap gains), 3.88 ms
+    // with phase A at two CTAs per SM (no co-residence, dense pieces first).
+    auto needs_a = [&](uint32_t st) {
+        for (size_t q = static_cast<size_t>(st) * kCopies; q < static_cast<size_t>(st + 1) * kCopies; ++q)
+            if ((B.copies[q] >> 63) && ((B.copies[q] >> 60) & 3u) == 1u) return true;
+        return false;
+    };
     for (uint64_t i = 0; i < nb_rows; ++i) {
         const uint32_t s0 = stripe_b[i], s1 = stripe_b[i + 1];
+        if (HCMX_COSCHED && S == 1) {
+            uint32_t sx = s0;
+            while (sx < s1 && !needs_a(sx)) ++sx;
+            uint64_t c1 = 0, c2 = 0;
+            for (uint32_t s2 = s0; s2 < sx; ++s2) c1 += B.stages[s2].pad;
+            for (uint32_t s2 = sx; s2 < s1; ++s2) c2 += B.stages[s2].pad;
+            if (sx == s0 || sx == s1) {  // dense only or lowrank only: one piece
+                bv.push_back({s0, s1, static_cast<uint32_t>(i), 0u});
+                bcost.push_back(sx == s1 ? c1 : c2);
+                dense_only.push_back(sx == s1 ? 1u : 0u);
+            } else {
+                npieces[i] = 2;
+                bv.push_back({s0, sx, static_cast<uint32_t>(i), 1u});
+                bcost.push_back(c1);
+                dense_only.push_back(1u);
+                bv.push_back({sx, s1, static_cast<uint32_t>(i), 2u});
+                bcost.push_back(c2);
+                dense_only.push_back(0u);
+            }
+            continue;
+        }
         const uint32_t P = std::min<uint32_t>(S, s1 - s0);
         uint64_t total = 0;
         for (uint32_t s2 = s0; s2 < s1; ++s2) total += B.stages[s2].pad;
@@ -2650,13 +2687,19 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     }
     std::vector<size_t> bord(bv.size());
     for (size_t i = 0; i < bord.size(); ++i) bord[i] = i;
-    std::stable_sort(bord.begin(), bord.end(), [&](size_t a2, size_t b2) { return bcost[a2] > bcost[b2]; });
+    std::stable_sort(bord.begin(), bord.end(), [&](size_t a2, size_t b2) {
+        if (!dense_only.empty() && dense_only[a2] != dense_only[b2]) return dense_only[a2] > dense_only[b2];
+        return bcost[a2] > bcost[b2];
+    });
     std::vector<std::array<uint32_t, 4>> sb;
     for (size_t i : bord) sb.push_back(bv[i]);
-    h->pieces = S > 1 ? S : 0;
-    if (S > 1) {
+    uint32_t SP = S;
+    if (HCMX_COSCHED && S == 1)
+        for (uint8_t q : npieces) SP = std::max<uint32_t>(SP, q);
+    h->pieces = SP > 1 ? SP : 0;
+    if (SP > 1) {
         up(h->npieces, npieces.data(), npieces.size());
-        h->ypart.alloc(static_cast<size_t>(S) * (h->re - h->rb) * h->R * 8);
+        h->ypart.alloc(static_cast<size_t>(SP) * (h->re - h->rb) * h->R * 8);
     }
     up(h->stripe_a, sa.data(), sa.size() * 16);
     up(h->stripe_b, sb.data(), sb.size() * 16);
