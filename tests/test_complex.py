@@ -127,3 +127,26 @@ def test_complex_arena_decodes_each_stream_once(gpu, oracle):
     with pytest.raises(ValueError):
         H.h.matvec(1.0, np.zeros(n), 0.0, np.zeros(n))
     H.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode,block", [("aflp-aplr", 4), ("bfl-aplr", 8), ("dfl-aplr", 4)])
+def test_complex_arena_schemes(gpu, oracle, mode, block):
+    """the complex arena over every codec scheme (BFL / DFL: fixed exponent
+    widths, the generic decoder for e = 11) and both block widths, against the
+    oracle on the same compressed real / imaginary matrices"""
+    from paper_2308_10960_b200.hmatrix import ComplexHMatrix, compress_in_place
+    n, r = 2048, 5
+    P, lv, K, Ar, Ai = _setup(n, "cuda")
+    fr, fi = compress_in_place(Ar, 1e-6, mode), compress_in_place(Ai, 1e-6, mode)
+    H = ComplexHMatrix(fr, fi, nrhs_block=block)
+    rng = np.random.default_rng(9)
+    X = rng.uniform(-1, 1, (n, r)) + 1j * rng.uniform(-1, 1, (n, r))
+    Y = H.matmat_device(torch.as_tensor(X).cuda()).cpu().numpy()
+    hr, hi = fr.host(), fi.host()
+    mv = lambda h, v: oracle.hmat_matvec(h, 1.0, v, 0.0, np.zeros(n), threads=4)
+    for j in range(r):
+        xr, xi = X[:, j].real.copy(), X[:, j].imag.copy()
+        ref = (mv(hr, xr) - mv(hi, xi)) + 1j * (mv(hr, xi) + mv(hi, xr))
+        assert np.linalg.norm(Y[:, j] - ref) <= TOL * np.linalg.norm(ref), j
+    H.close()

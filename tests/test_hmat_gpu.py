@@ -427,3 +427,24 @@ def test_one_handle_two_streams(gpu, oracle):
     for yd, r in zip(ys, refs):
         assert rel(yd.cpu().numpy(), r) <= TOL
     H.close()
+
+
+@pytest.mark.parametrize("block", [4, 8])
+def test_multi_rhs_transposed(gpu, oracle, block):
+    """M^T with several right-hand sides through the transposed handle's block
+    arena (4 or 8 columns decoded once): each column equals the oracle's
+    transposed product"""
+    from cpu_hmatrix import build_small_flat
+    from paper_2308_10960_b200.hmatrix import HMatrix
+    n = 1100
+    f, _ = build_small_flat(n=n, eps=1e-6, scheme=0, mode="aplr", geometry="sphere")
+    H = HMatrix(f.to_product(), with_transpose=True, nrhs_block=block)
+    rng = np.random.default_rng(21)
+    X = np.asfortranarray(rng.uniform(-1, 1, (n, block + 1)))
+    Y0 = np.asfortranarray(rng.standard_normal((n, block + 1)))
+    Y = Y0.copy(order="F")
+    H.matmat(0.75, X, -0.5, Y, transpose=True)
+    for j in range(block + 1):
+        ref = oracle.hmat_matvec(f, 0.75, X[:, j], -0.5, Y0[:, j], threads=4, transpose=True)
+        assert rel(Y[:, j], ref) <= TOL, j
+    H.close()
