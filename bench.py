@@ -310,6 +310,7 @@ def codec_microbench(reps=10):
         pk = _peaks()[0]
         out[f"afl_{eps:g}"] = {"w_bits": int(bb.desc["bit_width"][0]),
                                "compress_gbs": round(algo / tcd / 1e9, 1),
+                               "decompress_fp64_gbs": round(8 * nb * bs / td / 1e9, 1),  # FP64 side
                                "compress_host_api_gbs": round(algo / tch / 1e9, 1),
                                "decompress_gbs": round(algo / td / 1e9, 1),
                                "compress_frac": round(algo / tcd / 1e9 / pk, 3),
@@ -498,6 +499,7 @@ def run_ours(args, rank, world, local):
                        "matvec_frac_of_peak": round(value / world / peak, 4)},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "frac_vs_nominal_8tbs": round(achieved / 8000.0, 4),  # north_star's "~8 TB/s"
                          "traffic": traffic, "algorithmic_bytes_per_launch": dom_bytes,
                          "ms_per_launch": round(dom_ms, 5),
                          "phase_ms": {"phase_a": round(per_a, 5), "phase_b": round(per_b, 5)}},
