@@ -1244,6 +1244,7 @@ __global__ void __launch_bounds__((nwb<R>() + 1) * 32, kCtasB) k_phase_b(Params 
 #pragma unroll
     for (int g = 0; g < kG * R; ++g) acc[g] = 0.0;
     constexpr unsigned H = NW / 2;
+    static_assert(NW % 2 == 0, "phase B's pairwise warp reduction needs an even number of consumer warps");
     static_assert(H * kR * sizeof(double) <= kRedBytes, "phase-B reduction buffer");
     consume<NW, false>(
         smem, full, empty, warp, lane, dbg(p),

@@ -1,0 +1,1 @@
+timeout 1500 tools/ab_variants.sh 3 2 nwb7 nwb11 2>&1 | grep -E "==|GB/s"
