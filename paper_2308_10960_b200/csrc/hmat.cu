@@ -767,9 +767,10 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
 // (dec_pair), the item has whole row groups and every lane's x slice is
 // 16-byte aligned.  xs: this lane's x rows, R values per row.  R = 1 keeps one
 // FMA chain per row of the group, R > 1 one chain per right-hand side.
-template <int R>
+template <int R, int NGC = 0>  // NGC > 0: exactly NGC row groups (fully unrolled, no trip count)
 __device__ __forceinline__ void a_fast(const uint32_t* data, unsigned P, unsigned w, unsigned e, const double* xs,
-                                       unsigned ngroups, unsigned gwords, uint64_t bias, double (&res)[R]) {
+                                       unsigned ngroups_rt, unsigned gwords, uint64_t bias, double (&res)[R]) {
+    const unsigned ngroups = NGC > 0 ? static_cast<unsigned>(NGC) : ngroups_rt;
     const uint32_t mask = fast_mask(w);
     const uint32_t mul = c_pow2e.v[e & 31u];
     const unsigned top = P + w;                          // one past the field's sign bit (in a row)
@@ -780,7 +781,7 @@ __device__ __forceinline__ void a_fast(const uint32_t* data, unsigned P, unsigne
     double acc[NA];
 #pragma unroll
     for (int i = 0; i < NA; ++i) acc[i] = 0.0;
-#pragma unroll kAUnroll
+#pragma unroll (NGC > 0 ? NGC : kAUnroll)
     for (unsigned g = 0; g < ngroups; ++g) {
         uint32_t lo[kARows], hi[kARows];
         il_load<kARows>(q, o, lo, hi);
@@ -869,7 +870,11 @@ __device__ __forceinline__ void a_item(const Params& p, const AItem& it, const u
     const uint32_t* data = recs + ((nl + 3u) & ~3u);
     const double* xs = reinterpret_cast<const double*>(slot) + (rec >> 19);
     double r[R];
-    if (it.body) a_fast<R>(data, P, w, (rec >> 7) & 15u, xs, it.nf / kARows, it.gwords, p.bias, r);
+    if (it.body) {
+        // whole 64-row chunks (most items): the 16 row groups fully unrolled
+        if (R == 1 && it.nf == kAChunk) a_fast<R, kAChunk / kARows>(data, P, w, (rec >> 7) & 15u, xs, 0, it.gwords, p.bias, r);
+        else a_fast<R>(data, P, w, (rec >> 7) & 15u, xs, it.nf / kARows, it.gwords, p.bias, r);
+    }
     else a_generic<R>(data, P, rec, xs, it.nf, it.gwords, r);
     // the chunks of a slot's rank column (lanes slot, slot + nslot, ...): fixed
     // butterfly (lane `slot` gets the same order on every run); idle lanes add 0
