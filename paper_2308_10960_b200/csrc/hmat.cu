@@ -150,6 +150,10 @@ constexpr uint32_t kAGroupMaxMulti = HCMX_AGROUP_MULTI;  // the same for multi-R
 constexpr int kAUnroll = HCMX_AUNROLL;   // row groups per iteration of the phase-A fast body
 constexpr uint64_t kAItemBytes = HCMX_AITEM;  // packed data per phase-A item
 constexpr uint32_t kAItemXBytes = 12288;  // staged x slices per phase-A item
+#ifndef HCMX_BLR_UNROLL
+#define HCMX_BLR_UNROLL 2
+#endif
+constexpr int kBLRUnroll = HCMX_BLR_UNROLL;  // columns per iteration of the phase-B lowrank body (R = 1) on 4 row groups; twice as many on 2
 #ifndef HCMX_BGROUP
 #define HCMX_BGROUP 32
 #endif
@@ -400,23 +404,30 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // decoder returns +-((1.mant * 2^offset) - 1) -- exactly the codec's value /
 // scale (codec.cpp:161-169).
 //
-// Fast decoder (w == 1 + e + m <= 32, e <= 10, codec fields): sp[1] is the
-// word holding the field's sign bit, sp[0] the word below it; the funnel shift
-// by s left-aligns the field (sign in bit 31).  The offset and mantissa bits
+// Fast decoder (w == 1 + e + m <= 32, e <= 10, codec fields): with `top` the
+// stream bit one past the field's sign bit, hi is word top >> 5 and lo the word
+// below it; the right funnel shift by top (mod 32) brings stream bits [top - 32,
+// top) into one register: the field left-aligned, sign in bit 31 (top a
+// multiple of 32: the shift is 0 and lo is the result).  Neither the word index
+// nor the shift needs top - 1 or a negation.  The offset and mantissa bits
 // times 2^(21 + e) land at bits [52 - m, 52 + e) of the double, so one wide
 // IMAD with the bias 1023 << 52 rebuilds 1.mant * 2^offset (offset + 1023 <=
 // 2046: no clamp for e <= 10); one DADD takes the 1 off and the sign is xored
 // into the high word.  About 8 instructions per value with the FMA.
 __device__ __forceinline__ double dec_pair(uint32_t lo, uint32_t hi, unsigned s, uint32_t mask, uint32_t mul,
                                           uint64_t bias) {
-    const uint32_t t = __funnelshift_l(lo, hi, s);
+    const uint32_t t = __funnelshift_r(lo, hi, s);
     const uint64_t bits = static_cast<uint64_t>(t & mask) * mul + bias;
     const double v = __longlong_as_double(static_cast<long long>(bits)) - 1.0;
     return __hiloint2double(__double2hiint(v) ^ static_cast<int>(t & 0x80000000u), __double2loint(v));
 }
-__device__ __forceinline__ double dec_fast(const uint32_t* sp, unsigned s, uint32_t mask, uint32_t mul,
-                                          uint64_t bias) {
-    return dec_pair(sp[0], sp[1], s, mask, mul, bias);
+
+// top >> 5 kept as a shift (an opaque one: the compiler otherwise rewrites the
+// scaled vector index into shift + mask + add, one instruction more per column)
+__device__ __forceinline__ unsigned word_of(unsigned top) {
+    unsigned r;
+    asm("shr.u32 %0, %1, 5;" : "=r"(r) : "r"(top));
+    return r;
 }
 
 // Interleaved word streams: NG streams (row groups of a column segment, or the
@@ -424,7 +435,8 @@ __device__ __forceinline__ double dec_fast(const uint32_t* sp, unsigned s, uint3
 // field needs in every stream come with two NG-word vector loads (LDS.128 for
 // NG = 4, LDS.64 for NG = 2) from one address.  q: the stream words' vector
 // base (16- / 8-byte aligned), o: the word below the fields' sign words (may
-// be -1: the bits it brings are masked off).
+// be -1: the bits it brings are masked off; the word above may lie one vector
+// past the stream, inside the slot: it is shifted out).
 template <int NG>
 __device__ __forceinline__ void il_load(const uint32_t* q, int o, uint32_t (&lo)[NG], uint32_t (&hi)[NG]) {
     static_assert(NG == 2 || NG == 4, "interleave");
@@ -774,8 +786,8 @@ __device__ __forceinline__ void a_fast(const uint32_t* data, unsigned P, unsigne
     const uint32_t mask = fast_mask(w);
     const uint32_t mul = c_pow2e.v[e & 31u];
     const unsigned top = P + w;                          // one past the field's sign bit (in a row)
-    const int o = static_cast<int>((top - 1) >> 5) - 1;  // the word below the sign word
-    const unsigned s = 0u - top;                         // the funnel shift takes it modulo 32
+    const int o = static_cast<int>(top >> 5) - 1;        // the word below the one holding bit `top`
+    const unsigned s = top;                              // the funnel shift takes it modulo 32
     const uint32_t* q = data;
     constexpr int NA = R == 1 ? kARows : R;
     double acc[NA];
@@ -1031,9 +1043,9 @@ __device__ __forceinline__ void b_column_full(const uint32_t* seg, unsigned lane
                                               double (&acc)[kG * R]) {
     constexpr int NG = GHI - GLO;
     const unsigned top = (lane + 1) * w;  // one past the sign bit of field `lane`
-    const unsigned s = 0u - top;          // the funnel shift takes it modulo 32
+    const unsigned s = top;               // the funnel shift takes it modulo 32
     uint32_t lo[NG], hi[NG];
-    il_load<NG>(seg, static_cast<int>((top - 1) >> 5) - 1, lo, hi);
+    il_load<NG>(seg, static_cast<int>(top >> 5) - 1, lo, hi);
 #pragma unroll
     for (int g = GLO; g < GHI; ++g) {
         const double d = dec_pair(lo[g - GLO], hi[g - GLO], s, mask, mul, bias);
@@ -1112,32 +1124,43 @@ __device__ __forceinline__ void b1_dense(const BItem& it, const uint32_t* seg, c
     const unsigned w = it.dpacked & 0xffu, e = (it.dpacked >> 16) & 0xffu;
     const uint32_t mask = fast_mask(w), mul = c_pow2e.v[e & 31u];
     const unsigned top = (lane + 1) * w;                 // one past the sign bit of field `lane`
-    const int o = static_cast<int>((top - 1) >> 5) - 1;  // same word and shift in every column
-    const unsigned s = 0u - top;
+    const int o = static_cast<int>(top >> 5) - 1;  // same word and shift in every column
+    const unsigned s = top;
     const unsigned segw = NG * w;
     double t0[NG], t1[NG];
 #pragma unroll
     for (int g = 0; g < NG; ++g) t0[g] = t1[g] = 0.0;
     const unsigned n = it.nseg;
-    unsigned c = 0;
-    for (; c + 2 <= n; c += 2) {
-        const double x0 = xc[c], x1 = xc[c + 1];
-        uint32_t l0[NG], h0[NG], l1[NG], h1[NG];
-        il_load<NG>(seg, o, l0, h0);
-        il_load<NG>(seg + segw, o, l1, h1);
+    // pointer induction: the vectors of the CP columns of an iteration (8 fields
+    // per lane) sit at fixed offsets from one pointer
+    constexpr unsigned CP = 8 / NG;
+    seg += static_cast<int>(NG) * o;  // vector o of the first column
+    const double* xe = xc + (n & ~(CP - 1u));
+    for (; xc != xe; xc += CP) {
+        double xv[CP];
+        uint32_t l[CP][NG], h[CP][NG];
+#pragma unroll
+        for (unsigned j = 0; j < CP; ++j) {
+            xv[j] = xc[j];
+            il_load<NG>(seg + j * segw, 0, l[j], h[j]);
+        }
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
-            t0[g] = fma(dec_pair(l0[g], h0[g], s, mask, mul, bias), x0, t0[g]);
-            t1[g] = fma(dec_pair(l1[g], h1[g], s, mask, mul, bias), x1, t1[g]);
+#pragma unroll
+            for (unsigned j = 0; j < CP; j += 2) {
+                t0[g] = fma(dec_pair(l[j][g], h[j][g], s, mask, mul, bias), xv[j], t0[g]);
+                t1[g] = fma(dec_pair(l[j + 1][g], h[j + 1][g], s, mask, mul, bias), xv[j + 1], t1[g]);
+            }
         }
-        seg += 2 * segw;
+        seg += CP * segw;
     }
-    if (c < n) {
-        const double x0 = xc[c];
+    for (unsigned r = n & (CP - 1u); r; --r) {
+        const double x0 = *xc++;
         uint32_t l0[NG], h0[NG];
-        il_load<NG>(seg, o, l0, h0);
+        il_load<NG>(seg, 0, l0, h0);
 #pragma unroll
         for (int g = 0; g < NG; ++g) t0[g] = fma(dec_pair(l0[g], h0[g], s, mask, mul, bias), x0, t0[g]);
+        seg += segw;
     }
 #pragma unroll
     for (int g = 0; g < NG; ++g) acc[GLO + g] = fma(dmul, t0[g] + t1[g], acc[GLO + g]);
@@ -1149,7 +1172,7 @@ __device__ __forceinline__ void b1_lr(const BItem& it, const uint32_t* seg, cons
     constexpr int NG = GHI - GLO;
     const unsigned lp1 = lane + 1;
     const unsigned n = it.nseg;
-#pragma unroll 2
+#pragma unroll (kBLRUnroll * 4 / NG)
     for (unsigned c = 0; c < n; ++c) {
         const uint4 q0 = reinterpret_cast<const uint4*>(rec)[0];  // {c lo, c hi, mask, mul}
         const unsigned w = reinterpret_cast<const uint32_t*>(rec)[5];  // WCol::w
@@ -1157,10 +1180,9 @@ __device__ __forceinline__ void b1_lr(const BItem& it, const uint32_t* seg, cons
         const double cc = __hiloint2double(static_cast<int>(q0.y), static_cast<int>(q0.x));
         const unsigned top = lp1 * w;
         uint32_t lo[NG], hi[NG];
-        il_load<NG>(seg, static_cast<int>((top - 1) >> 5) - 1, lo, hi);
-        const unsigned s = 0u - top;
+        il_load<NG>(seg, static_cast<int>(word_of(top)) - 1, lo, hi);
 #pragma unroll
-        for (int g = 0; g < NG; ++g) acc[GLO + g] = fma(dec_pair(lo[g], hi[g], s, q0.z, q0.w, bias), cc, acc[GLO + g]);
+        for (int g = 0; g < NG; ++g) acc[GLO + g] = fma(dec_pair(lo[g], hi[g], top, q0.z, q0.w, bias), cc, acc[GLO + g]);
         seg += NG * w;
     }
 }
