@@ -86,7 +86,16 @@ constexpr int kNWA = HCMX_NWA;            // phase-A consumer warps (more regist
 #define HCMX_BMINB 2
 #endif
 constexpr int kCtasA = HCMX_AMINB, kCtasB = HCMX_BMINB;  // resident CTAs per SM (persistent grids)
-constexpr int kThreadsA = (kNWA + 1) * 32;
+// The coefficient copies of a stage (x slices, phase-A results: ~12 small bulk
+// copies per phase-A stage, each an ELECT / R2UR round trip of ~130 clocks) are
+// issued by a second producer warp; the first one issues the stage's one large
+// copy and runs the stage sequence.  (One producer warp was busy 88 % of phase A
+// and the consumer warps waited for data 23 % of it.)
+#ifndef HCMX_COEF_WARP
+#define HCMX_COEF_WARP 1
+#endif
+constexpr int kNProd = HCMX_COEF_WARP ? 2 : 1;  // producer warps per CTA
+constexpr int kThreadsA = (kNWA + kNProd) * 32;
 constexpr int kStageBytes = HCMX_STAGE_BYTES;  // packed data per stage
 constexpr int kMaxItems = 32;             // items per stage (one per producer lane)
 constexpr int kItemBytes = 32;            // descriptor size (A and B)
@@ -167,8 +176,11 @@ constexpr uint64_t kItemMaxBytes = HCMX_BITEM;  // items merge columns up to thi
 constexpr size_t kRingBytes = static_cast<size_t>(kNStage) * kSlotBytes;
 constexpr size_t kRingBytesA = static_cast<size_t>(kNStageA) * kSlotBytesA;
 constexpr size_t kRedBytes = ((kNWB > HCMX_NWB_MULTI ? kNWB : HCMX_NWB_MULTI) / 2) * kR * sizeof(double);  // phase-B cross-warp reduction
-constexpr size_t kSmemBytes = kRingBytes + kRedBytes + 2 * kNStage * sizeof(uint64_t);  // + full, empty barriers
-constexpr size_t kSmemBytesA = kRingBytesA + 2 * kNStageA * sizeof(uint64_t);
+constexpr int kMailSlots = 8;  // stage indices published by the first producer warp for the second
+constexpr size_t kMailBytes = (kMailSlots + 2) * sizeof(uint32_t) + 8;  // + published / read counters, padding
+constexpr size_t kSmemBytes = kRingBytes + kRedBytes + 2 * kNStage * sizeof(uint64_t) + kMailBytes;  // + full, empty barriers
+constexpr size_t kSmemBytesA = kRingBytesA + 2 * kNStageA * sizeof(uint64_t) + kMailBytes;
+static_assert(kNStage + 2 <= kMailSlots && kNStageA + 2 <= kMailSlots, "mailbox depth");
 constexpr int kCopies = 2 * kMaxItems;  // coefficient copies per stage (two per producer lane)
 constexpr int kRangeBytes = 64;         // phase-B stage head: 16 warp item ranges (begin | end << 16)
 // copy entry (u64): [0,32) source element index, [32,48) dst / 16 in the slot,
@@ -563,25 +575,54 @@ struct StageMeta {  // what the producer needs for one stage, loaded ahead
     uint64_t c0, c1;
     uint32_t stripe;
     uint32_t flags;  // kHdrLast / kHdrEnd
+    uint32_t sidx;   // stage index (kMailEnd / kMailSkip for header-only stages): what the second producer warp is told
     bool empty;      // a row block without stages: header only
 };
+constexpr uint32_t kMailEnd = 0xffffffffu, kMailSkip = 0xfffffffeu;
+
+// mailbox between the two producer warps (shared memory): seq[it % kMailSlots]
+// = stage index of the CTA's it-th stage, pub = stages published, rd = stages read
+struct Mail {
+    uint32_t seq[kMailSlots];
+    uint32_t pub, rd;
+};
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void spin_until_ge(const uint32_t* p, uint32_t v) {
+    uint32_t n = 0;
+    while (static_cast<int32_t>(ld_acquire(p) - v) < 0) {
+        __nanosleep(20);
+        if (++n == (1u << 26)) __trap();
+    }
+}
 
 template <bool PHASE_A>
 __device__ __forceinline__ StageMeta seq_meta(const Params& p, const StageSeq& q, unsigned lane) {
     StageMeta m{};
     if (q.done) {
         m.flags = kHdrEnd;
+        m.sidx = kMailEnd;
         return m;
     }
     m.stripe = q.stripe;
     if (q.s >= q.e) {  // empty phase-B row block
         m.empty = true;
         m.flags = kHdrLast | kHdrEmpty;
+        m.sidx = kMailSkip;
         return m;
     }
     m.st = p.stages[q.s];
-    m.c0 = __ldg(p.copies + static_cast<size_t>(q.s) * kCopies + lane);
-    m.c1 = __ldg(p.copies + static_cast<size_t>(q.s) * kCopies + 32 + lane);
+    m.sidx = q.s;
+    if (kNProd == 1) {
+        m.c0 = __ldg(p.copies + static_cast<size_t>(q.s) * kCopies + lane);
+        m.c1 = __ldg(p.copies + static_cast<size_t>(q.s) * kCopies + 32 + lane);
+    }
     m.flags = q.s + 1 == q.e ? kHdrLast : 0u;
     return m;
 }
@@ -594,14 +635,26 @@ __device__ __forceinline__ StageMeta seq_meta(const Params& p, const StageSeq& q
 // two stages ahead, so no global load sits on the producer's critical path.
 template <bool PHASE_A, int R>
 __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_t* full, uint64_t* empty,
-                                         unsigned lane) {
+                                         Mail* mail, unsigned lane) {
     const uint64_t policy = evict_first_policy();
     StageSeq q;
     q.s = q.e = 0;
+    uint32_t npub = 0;  // stages published to the second producer warp
+    auto publish = [&](const StageMeta& m) {
+        if (kNProd == 1) return;
+        if (lane == 0) {
+            if (npub >= kMailSlots) spin_until_ge(&mail->rd, npub - kMailSlots + 1);  // the entry overwritten was read
+            mail->seq[npub % kMailSlots] = m.sidx;
+            st_release(&mail->pub, npub + 1);
+        }
+        ++npub;
+    };
     seq_next<PHASE_A>(p, q, lane);
     StageMeta mx = seq_meta<PHASE_A>(p, q, lane);
+    publish(mx);
     seq_next<PHASE_A>(p, q, lane);
     StageMeta my = seq_meta<PHASE_A>(p, q, lane);
+    publish(my);
     StageMeta mz;
     const long long t_start = clk();
 #ifdef HCMX_PROF
@@ -617,6 +670,7 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
     auto step = [&](const StageMeta& cur, StageMeta& ahead) -> bool {
         seq_next<PHASE_A>(p, q, lane);
         ahead = seq_meta<PHASE_A>(p, q, lane);
+        publish(ahead);
         const long long t0 = clk();
         if (it >= NS) mbar_wait(&empty[slot], phase);
         t_wait += clk() - t0;
@@ -632,7 +686,7 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
         if (cur.flags & kHdrEnd || cur.empty) {  // header only
             if (lane == 0) mbar_arrive(&full[slot]);
         } else {
-            if (!PHASE_A && !waited) {
+            if (!PHASE_A && !waited && kNProd == 1) {
                 // the first stage that copies phase-A column coefficients (table
                 // 1) waits for phase A and k_reduce to complete; dense stages
                 // before it run while they drain
@@ -649,7 +703,7 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
                 bulk_g2s(base, p.arena + cur.st.byte_off, cur.st.bytes, &full[slot], policy);
             }
             __syncwarp();
-            if (!no_coef) {
+            if (!no_coef && kNProd == 1) {
                 issue_copy<R>(p, cur.c0, base, &full[slot]);
                 issue_copy<R>(p, cur.c1, base, &full[slot]);
             }
@@ -684,6 +738,67 @@ __device__ __forceinline__ void producer(const Params& p, uint8_t* ring, uint64_
         if (step(mx, mz)) return;
         if (step(my, mx)) return;
         if (step(mz, my)) return;
+    }
+}
+
+// The second producer warp: the coefficient copies of every stage, in the
+// stage order the first producer warp publishes (two stages ahead of its own
+// copies, so the copy entries are loaded before the slot is free).  Both warps
+// wait for the slot's empty barrier; the first one posts the expected bytes of
+// all the stage's copies (a copy that lands before that only drives the
+// barrier's transaction count negative until the expect arrives -- the phase
+// cannot complete before the producer's arrival).
+template <bool PHASE_A, int R>
+__device__ __forceinline__ void coef_producer(const Params& p, uint8_t* ring, uint64_t* full, uint64_t* empty,
+                                              Mail* mail, unsigned lane) {
+    constexpr int NS = nstage<PHASE_A>();
+    const bool no_coef = dbg(p) >= 2;
+    unsigned slot = 0, phase = 0;
+    uint32_t it = 0;
+    bool waited = false;  // phase B: griddepcontrol.wait done by this warp
+    auto fetch = [&](uint32_t i, uint32_t& sidx, uint64_t& c0, uint64_t& c1) {
+        spin_until_ge(&mail->pub, i + 1);
+        sidx = mail->seq[i % kMailSlots];
+        __syncwarp();
+        if (lane == 0) st_release(&mail->rd, i + 1);
+        c0 = c1 = 0;
+        if (sidx < kMailSkip) {
+            c0 = __ldg(p.copies + static_cast<size_t>(sidx) * kCopies + lane);
+            c1 = __ldg(p.copies + static_cast<size_t>(sidx) * kCopies + 32 + lane);
+        }
+    };
+    uint32_t sx, sy;
+    uint64_t x0, x1, y0, y1;
+    fetch(0, sx, x0, x1);
+    auto step = [&](uint32_t cur, uint64_t c0, uint64_t c1, uint32_t& nsidx, uint64_t& n0, uint64_t& n1) -> bool {
+        if (cur == kMailEnd) return true;
+        fetch(it + 1, nsidx, n0, n1);  // the next stage's entries are in flight during this one's copies
+        if (cur != kMailSkip && !no_coef) {
+            if (it >= NS) mbar_wait(&empty[slot], phase);
+            if (!PHASE_A && !waited) {
+                // the first stage that copies phase-A column coefficients (table
+                // 1) waits for phase A and k_reduce to complete; dense stages
+                // before it run while they drain
+                const bool needs_a = ((c0 >> 63) && ((c0 >> 60) & 3u) == 1u) || ((c1 >> 63) && ((c1 >> 60) & 3u) == 1u);
+                if (__any_sync(0xffffffffu, needs_a)) {
+                    pdl_wait();
+                    waited = true;
+                }
+            }
+            uint8_t* base = ring + static_cast<size_t>(slot) * slot_bytes<PHASE_A>();
+            issue_copy<R>(p, c0, base, &full[slot]);
+            issue_copy<R>(p, c1, base, &full[slot]);
+        }
+        ++it;
+        if (++slot == NS) {
+            slot = 0;
+            if (it > NS) phase ^= 1u;
+        }
+        return false;
+    };
+    for (;;) {
+        if (step(sx, x0, x1, sy, y0, y1)) return;
+        if (step(sy, y0, y1, sx, x0, x1)) return;
     }
 }
 
@@ -758,8 +873,9 @@ __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t*
 }
 
 template <int NW, int NS>
-__device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
+__device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty, Mail* mail) {
     if (threadIdx.x == 0) {
+        mail->pub = mail->rd = 0u;
         for (int b = 0; b < NS; ++b) {
             mbar_init(&full[b], 1);
             mbar_init(&empty[b], NW);
@@ -1233,6 +1349,7 @@ __global__ void __launch_bounds__(kThreadsA, kCtasA) k_phase_a(Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytesA);
     uint64_t* empty = full + kNStageA;
+    Mail* mail = reinterpret_cast<Mail*>(empty + kNStageA);
     const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     // phase B's stripe counter for this product (A runs first, B claims only
     // after its griddepcontrol.wait, so the store is visible by then)
@@ -1240,10 +1357,14 @@ __global__ void __launch_bounds__(kThreadsA, kCtasA) k_phase_a(Params p) {
         p.work[1] = 0u;
         __threadfence();  // visible before this CTA triggers phase B's launch
     }
-    ring_init<kNWA, kNStageA>(full, empty);
+    ring_init<kNWA, kNStageA>(full, empty, mail);
     pdl_trigger();
     if (warp == kNWA) {
-        producer<true, R>(p, smem, full, empty, lane);
+        producer<true, R>(p, smem, full, empty, mail, lane);
+        return;
+    }
+    if (warp > kNWA) {
+        coef_producer<true, R>(p, smem, full, empty, mail, lane);
         return;
     }
     consume<kNWA, true>(
@@ -1255,16 +1376,21 @@ __global__ void __launch_bounds__(kThreadsA, kCtasA) k_phase_a(Params p) {
 }
 
 template <int R>
-__global__ void __launch_bounds__((nwb<R>() + 1) * 32, kCtasB) k_phase_b(Params p) {
+__global__ void __launch_bounds__((nwb<R>() + kNProd) * 32, kCtasB) k_phase_b(Params p) {
     constexpr int NW = nwb<R>();
     extern __shared__ __align__(128) uint8_t smem[];
     double* red = reinterpret_cast<double*>(smem + kRingBytes);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kRedBytes);
     uint64_t* empty = full + kNStage;
+    Mail* mail = reinterpret_cast<Mail*>(empty + kNStage);
     const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    ring_init<NW, kNStage>(full, empty);
+    ring_init<NW, kNStage>(full, empty, mail);
     if (warp == NW) {
-        producer<false, R>(p, smem, full, empty, lane);
+        producer<false, R>(p, smem, full, empty, mail, lane);
+        return;
+    }
+    if (warp > NW) {
+        coef_producer<false, R>(p, smem, full, empty, mail, lane);
         return;
     }
     double acc[kG * R];
@@ -2892,7 +3018,7 @@ void run_matvec(hcmx_hmat* h, double alpha, const double* dx, double beta, doubl
             launch(k_ccombine<RR>, std::min<uint32_t>((h->ncpairs + 255) / 256, 8 * nsm), 256, 0, true, p,
                    h->cpairs.as<CPair>(), h->ncpairs);
         if (h->timing) check_cuda(cudaEventRecord(rec.a1, s), "event");
-        if (h->nblocks) launch(k_phase_b<RR>, gb, (nwb<RR>() + 1) * 32, kSmemBytes, run_a, p);
+        if (h->nblocks) launch(k_phase_b<RR>, gb, (nwb<RR>() + kNProd) * 32, kSmemBytes, run_a, p);
         if (h->pieces) launch(k_combine<RR>, gc, 256, 0, true, p, h->npieces.as<uint8_t>());
     };
     if (R == 1) chain(std::integral_constant<int, 1>{});
