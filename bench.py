@@ -366,12 +366,15 @@ def run_ours(args, rank, world, local):
     # per-phase kernel times (roofline) from a second pass of the same K steps
     # with events around each phase: events between the kernels replace their
     # programmatic dependent launch, so the headline pass above runs without them
+    # (the board reaches its power cap after ~20 back-to-back config-4 products:
+    # a 1 s pause puts this pass in the same power state as the headline pass)
+    clk = clocks.stop()
+    time.sleep(1.0)
     H.timing(1)
     for _ in range(args.steps):
         step()
     torch.cuda.synchronize()
     ms_a, ms_b, calls = H.timing(0)
-    clk = clocks.stop()
     launches = H.launches() * args.steps
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
