@@ -978,50 +978,78 @@ __device__ __forceinline__ double* rec_c(const Params& p, uint32_t col) {
     return reinterpret_cast<double*>(p.wrec + static_cast<size_t>(col) * rec_bytes<R>());
 }
 
+// the chunks of a slot's rank column (lanes slot, slot + nslot, ...): fixed
+// butterfly (lane `slot` gets the same order on every run); idle lanes add 0;
+// then the slot lanes write c = alpha coef (X^T x) or the partial sum
 template <int R>
-__device__ __forceinline__ void a_item(const Params& p, const AItem& it, const uint8_t* slot, unsigned lane) {
-    const unsigned nl = it.nl;  // lane records
-    const uint32_t* recs = reinterpret_cast<const uint32_t*>(slot) + it.word_off;
-    const uint32_t r0 = recs[lane < nl ? lane : 0u];
-    const bool act = lane < nl && (r0 & 127u) != 0u;
-    const uint32_t rec = act ? r0 : recs[0];  // idle lanes shadow lane 0 (results dropped)
-    const unsigned nslot = 1u << it.cshift;
-    const unsigned dest = it.dest0 + lane;      // written by the slot lanes (g == 0) only
-    double cf = 0.0;
-    if (act && lane < nslot && it.final_) cf = __ldg(p.coef + dest);  // in flight during the decode
-    // this lane's bit offset inside a row: exclusive prefix sum of the widths
-    const unsigned w = rec & 127u;
-    unsigned P = act ? w : 0u;
-#pragma unroll
-    for (unsigned o = 1; o < 32; o <<= 1) {
-        const unsigned v = __shfl_up_sync(0xffffffffu, P, o);
-        if (lane >= o) P += v;
-    }
-    P = act ? P - w : 0u;
-    const uint32_t* data = recs + ((nl + 3u) & ~3u);
-    const double* xs = reinterpret_cast<const double*>(slot) + (rec >> 19);
-    double r[R];
-    if (it.body) {
-        // whole 64-row chunks (most items): the 16 row groups fully unrolled
-        if (R == 1 && it.nf == kAChunk) a_fast<R, kAChunk / kARows>(data, P, w, (rec >> 7) & 15u, xs, 0, it.gwords, p.bias, r);
-        else a_fast<R>(data, P, w, (rec >> 7) & 15u, xs, it.nf / kARows, it.gwords, p.bias, r);
-    }
-    else a_generic<R>(data, P, rec, xs, it.nf, it.gwords, r);
-    // the chunks of a slot's rank column (lanes slot, slot + nslot, ...): fixed
-    // butterfly (lane `slot` gets the same order on every run); idle lanes add 0
+__device__ __forceinline__ void a_finish(const Params& p, double (&r)[R], bool act, unsigned lane, unsigned nslot,
+                                         unsigned dest, unsigned final_, double cf) {
 #pragma unroll
     for (int c = 0; c < R; ++c) {
         if (!act) r[c] = 0.0;
         for (unsigned o = nslot; o < 32u; o <<= 1) r[c] += __shfl_xor_sync(0xffffffffu, r[c], o);
     }
     if (!act || lane >= nslot) return;
-    if (it.final_) {
+    if (final_) {
         double* out = rec_c<R>(p, dest);
 #pragma unroll
         for (int c = 0; c < R; ++c) out[c] = p.alpha * cf * r[c];
     } else {
 #pragma unroll
         for (int c = 0; c < R; ++c) p.partial[static_cast<size_t>(dest) * R + c] = r[c];
+    }
+}
+
+// Lane records.  Fast items (AItem::body = 1: every lane a codec field with
+// w <= 32, e <= 10, an even x offset): [0,5) w - 1, [5,9) e, [9,19) the lane's bit
+// offset inside a row (the exclusive prefix sum of the widths, baked by the
+// builder: no 5-round shuffle scan per item), [19,31) x offset / 2 (doubles in
+// the slot), bit 31 valid.  Generic items: [0,7) w, [7,11) e, [11,17) m,
+// [17,19) format, [19,32) x offset; w = 0 idle.
+constexpr uint32_t kARecValid = 0x80000000u;
+
+template <int R>
+__device__ __forceinline__ void a_item(const Params& p, const AItem* ip, const uint8_t* slot, unsigned lane) {
+    // the descriptor with two loads issued together (word_off | nf, nl, body | dest0 | rowbits, gwords || final_, cshift)
+    const uint4 d0 = *reinterpret_cast<const uint4*>(ip);
+    const uint32_t d1 = reinterpret_cast<const uint32_t*>(ip)[4];
+    const unsigned it_nf = d0.y & 0xffffu, nl = (d0.y >> 16) & 0xffu, it_body = d0.y >> 24;
+    const unsigned it_gwords = d0.w >> 16, it_final = d1 & 0xffu, it_cshift = (d1 >> 8) & 0xffu;
+    const uint32_t* recs = reinterpret_cast<const uint32_t*>(slot) + d0.x;
+    const uint32_t r0 = recs[lane < nl ? lane : 0u];
+    const unsigned nslot = 1u << it_cshift;
+    const unsigned dest = d0.z + lane;      // written by the slot lanes (g == 0) only
+    const uint32_t* data = recs + ((nl + 3u) & ~3u);
+    double r[R];
+    bool act;
+    if (it_body) {
+        act = lane < nl && (r0 & kARecValid) != 0u;
+        double cf = 0.0;
+        if (act && lane < nslot && it_final) cf = __ldg(p.coef + dest);  // in flight during the decode
+        const uint32_t rec = act ? r0 : recs[0];  // idle lanes shadow lane 0 (results dropped)
+        const unsigned w = (rec & 31u) + 1u, e = (rec >> 5) & 15u, P = (rec >> 9) & 1023u;
+        const double* xs = reinterpret_cast<const double*>(slot) + 2u * ((rec >> 19) & 4095u);
+        // whole 64-row chunks (most items): the 16 row groups fully unrolled
+        if (R == 1 && it_nf == kAChunk) a_fast<R, kAChunk / kARows>(data, P, w, e, xs, 0, it_gwords, p.bias, r);
+        else a_fast<R>(data, P, w, e, xs, it_nf / kARows, it_gwords, p.bias, r);
+        a_finish<R>(p, r, act, lane, nslot, dest, it_final, cf);
+    } else {
+        act = lane < nl && (r0 & 127u) != 0u;
+        double cf = 0.0;
+        if (act && lane < nslot && it_final) cf = __ldg(p.coef + dest);
+        const uint32_t rec = act ? r0 : recs[0];
+        // this lane's bit offset inside a row: exclusive prefix sum of the widths
+        const unsigned w = rec & 127u;
+        unsigned P = act ? w : 0u;
+#pragma unroll
+        for (unsigned o = 1; o < 32; o <<= 1) {
+            const unsigned v = __shfl_up_sync(0xffffffffu, P, o);
+            if (lane >= o) P += v;
+        }
+        P = act ? P - w : 0u;
+        const double* xs = reinterpret_cast<const double*>(slot) + (rec >> 19);
+        a_generic<R>(data, P, rec, xs, it_nf, it_gwords, r);
+        a_finish<R>(p, r, act, lane, nslot, dest, it_final, cf);
     }
 }
 
@@ -1373,7 +1401,7 @@ __global__ void __launch_bounds__(kThreadsA, kCtasA) k_phase_a(Params p) {
     consume<kNWA, true>(
         smem, full, empty, warp, lane, dbg(p),
         [&](const uint8_t* base, unsigned i) {
-            a_item<R>(p, reinterpret_cast<const AItem*>(base)[i], base, lane);
+            a_item<R>(p, reinterpret_cast<const AItem*>(base) + i, base, lane);
         },
         [](uint32_t) {});
 }
@@ -2225,6 +2253,7 @@ struct Builder {
                 return sg * G < t.nl ? static_cast<long>(t.l0 + sg * G + g) : -1L;
             };
             bool fast = it.nf % kARows == 0;
+            std::vector<std::pair<uint64_t, uint32_t>> fast_rec;  // the records of a fast item (see a_item)
             const uint64_t rec0 = arena.size();
             arena.resize(rec0 + ((nrec + 3) & ~size_t(3)), 0u);
             const uint64_t data0 = arena.size();
@@ -2241,6 +2270,8 @@ struct Builder {
                 if (xo >= 8192u || w > 64) throw std::logic_error("hmat: phase-A lane record");
                 fast = fast && fmt == 0 && w <= 32 && e <= 10 && w == 1 + e + m && xo % 2 == 0;
                 arena[rec0 + q] = w | (e << 7) | ((fmt ? 0u : m) << 11) | ((fmt ? fmt - 2u : 0u) << 17) | (xo << 19);
+                fast_rec.push_back({rec0 + q, ((w - 1u) & 31u) | (e << 5) | (P << 9) | ((xo / 2u) << 19) | kARecValid});
+                fast = fast && P < 1024u && xo / 2u < 4096u;
                 lane_jobs.push_back({data0, L.buf, L.f0, L.nf, P, t.rowbits, t.gwords});
                 if (keep_map)
                     h->segs[L.buf].push_back({data0, static_cast<uint32_t>(L.f0), L.nf, P,
@@ -2248,6 +2279,8 @@ struct Builder {
                 P += w;
             }
             it.body = fast ? 1 : 0;
+            if (fast)
+                for (const auto& fr : fast_rec) arena[fr.first] = fr.second;
             std::memcpy(arena.data() + start + n * (kItemBytes / 4), &it, kItemBytes);
             while (arena.size() % 4) arena.push_back(0u);
             cost += 60 + 40ull * t.ngroups * (fast ? 1 : 3);  // ~warp instructions
