@@ -139,6 +139,9 @@ template <bool PHASE_A>
 __host__ __device__ constexpr int off_hdr() { return PHASE_A ? kOffHdrA : kOffHdr; }
 constexpr int kR = 128;               // rows per phase-B CTA
 constexpr int kG = kR / 32;           // row groups (accumulators) per lane
+#ifndef HCMX_A_STATIC
+#define HCMX_A_STATIC 1
+#endif
 #ifndef HCMX_ACHUNK
 #define HCMX_ACHUNK 64  // 32 measured: phase A 0.122 -> 0.136 ms (the per-item work doubles)
 #endif
@@ -825,6 +828,7 @@ __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t*
     long long t_wait = 0, t_busy = 0, t_end = 0;
     constexpr int NS = nstage<DYN>();  // DYN consumers are phase A's
     unsigned slot = 0, phase = 0;  // ring position of stage it: it % NS, (it / NS) & 1
+    unsigned rot = 0;              // stage count modulo NW (static item deal)
     for (;;) {
         const long long t0 = clk();
         mbar_wait(&full[slot], phase);
@@ -843,7 +847,18 @@ __device__ __forceinline__ void consume(uint8_t* ring, uint64_t* full, uint64_t*
             return;
         }
         if (debug) {
+#if HCMX_A_STATIC
         } else if (DYN) {
+            // items of a stage dealt round-robin to the warps, the deal rotated by
+            // one warp per stage (items are sorted largest first); every item
+            // writes its own results, so any assignment gives the same bits
+            const unsigned n = hdr[3];
+            for (unsigned i = (warp + NW - rot) % NW; i < n; i += NW) body(base, i);
+            rot = rot + 1 == NW ? 0u : rot + 1;
+        } else if (false) {
+#else
+        } else if (DYN) {
+#endif
             // the next claim is issued before the current item is decoded, so the
             // shared atomic's latency hides behind it
             const unsigned n = hdr[3];
