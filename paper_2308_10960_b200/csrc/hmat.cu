@@ -810,10 +810,14 @@ __device__ __forceinline__ void coef_producer(const Params& p, uint8_t* ring, ui
 
 // consumer warps of a persistent CTA: body(slot_base, first, end) for the
 // warp's items of every stage; at the last stage of a stripe, stripe_end(id)
-// DYN: warps claim a stage's items one at a time (phase A: every item writes
-// its own results, so any assignment gives the same bits).  Otherwise each
-// warp takes its precomputed contiguous range (phase B: a warp's row sums
-// must see the same items in the same order on every run: deterministic y).
+// DYN (phase A: every item writes its own results, so any assignment gives
+// the same bits): the stage's items are dealt round-robin to the warps, the
+// deal rotated by one warp per stage (HCMX_A_STATIC = 1, the default; with 0
+// the warps claim the items one at a time with a shared-memory atomic, which
+// measured 3-5 % slower: a claim and its shuffle per item and per stage visit).
+// Otherwise each warp takes its precomputed contiguous range (phase B: a
+// warp's row sums must see the same items in the same order on every run:
+// deterministic y).
 // one item claim: a plain shared-memory atomic from one lane (atomicAdd from a
 // lane-0 branch compiles to the warp-aggregated sequence, ~12 instructions)
 __device__ __forceinline__ unsigned claim(uint32_t* counter) {
@@ -2234,7 +2238,7 @@ struct Builder {
                 if (x.pad == pad && x.start <= L.xidx && L.xidx + L.nf <= x.end) return x.off / 8 + (L.xidx - x.start) * static_cast<uint32_t>(R);
             throw std::logic_error("hmat: x slice");
         };
-        // descriptors largest first (warps claim a stage's items in order)
+        // descriptors largest first (the rotating deal spreads the large ones over the warps)
         std::vector<size_t> ord;
         for (size_t t = pos; t < end; ++t) ord.push_back(t);
         std::stable_sort(ord.begin(), ord.end(), [&](size_t a2, size_t b2) { return its[a2].bytes > its[b2].bytes; });
