@@ -139,6 +139,9 @@ template <bool PHASE_A>
 __host__ __device__ constexpr int off_hdr() { return PHASE_A ? kOffHdrA : kOffHdr; }
 constexpr int kR = 128;               // rows per phase-B CTA
 constexpr int kG = kR / 32;           // row groups (accumulators) per lane
+#ifndef HCMX_A_SIGMA
+#define HCMX_A_SIGMA 1
+#endif
 #ifndef HCMX_A_STATIC
 #define HCMX_A_STATIC 1
 #endif
@@ -2617,8 +2620,21 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
             pend.clear();
             stripe_bytes = 0;
         };
-        for (uint64_t l : leaves) {
-            if (d.kind[l] == 0) continue;
+        // Leaves in column-cluster order: the admissible blocks of one column
+        // cluster share their x slice, so an item's lanes (rank columns of
+        // consecutive leaves) and a stage's items mostly read ONE staged slice --
+        // fewer coefficient copies per stage and fewer slot bytes spent on x
+        // (in leaf order a third of a stage's packed bytes).
+        std::vector<uint64_t> leaves_a;
+        for (uint64_t l : leaves)
+            if (d.kind[l] != 0) leaves_a.push_back(l);
+#if HCMX_A_SIGMA
+        std::stable_sort(leaves_a.begin(), leaves_a.end(), [&](uint64_t a2, uint64_t b2) {
+            if (d.col0[a2] != d.col0[b2]) return d.col0[a2] < d.col0[b2];
+            return d.col1[a2] < d.col1[b2];
+        });
+#endif
+        for (uint64_t l : leaves_a) {
             const uint32_t id = static_cast<uint32_t>(lr_id[l]);
             pend.push_back(id);
             for (uint32_t i = 0; i < leafa[id].k; ++i)
