@@ -179,7 +179,10 @@ constexpr int kBLRUnroll = HCMX_BLR_UNROLL;  // columns per iteration of the pha
 #define HCMX_BITEM 8192
 #endif
 constexpr int kBLRGroup = HCMX_BGROUP;  // max columns per B item
-constexpr uint64_t kAStripeBytes = 8 * 26624;  // target packed bytes per phase-A CTA
+#ifndef HCMX_ASTRIPE
+#define HCMX_ASTRIPE 32
+#endif
+constexpr uint64_t kAStripeBytes = HCMX_ASTRIPE * 26624ull;  // target packed bytes per phase-A stripe (one CTA's claim)
 constexpr uint64_t kItemTarget = 1536;          // packed bytes per item (columns grouped up to this)
 constexpr uint64_t kItemMaxBytes = HCMX_BITEM;  // items merge columns up to this many packed bytes
 constexpr size_t kRingBytes = static_cast<size_t>(kNStage) * kSlotBytes;
@@ -2523,16 +2526,19 @@ void build(const hcmx_hmat_desc& d, hcmx_hmat* h) {
     uint32_t nstripe_a = 0;
     std::vector<uint32_t> stripe_a = {0};
     {
-        // stripe size: ~kAStripeBytes, smaller when the X factors of this handle
-        // (one rank of a row partition) would give fewer than ~4 stripes per
-        // CTA slot (2 per SM) -- else the slowest stripe sets the phase time
+        // stripe size: up to kAStripeBytes (32 stages: fewer partly filled last
+        // stages and stripe claims; config 4 phase A -3 % against 8 stages),
+        // smaller when the X factors of this handle would give fewer than ~6
+        // stripes per CTA slot (2 per SM) -- else the slowest stripe sets the
+        // phase time (config 3, 1.1 GB: 8 stages per stripe measured best, 12 or
+        // more +3.5 %)
         uint64_t xbytes_all = 0;
         for (uint64_t l : leaves)
             if (d.kind[l] != 0)
                 for (uint32_t i = 0; i < leafa[lr_id[l]].k; ++i)
                     xbytes_all += B.words_of(xbuf(l, i).first, d.col1[l] - d.col0[l]) * 4;
         const uint64_t stripe_target =
-            std::max<uint64_t>(2ull * kStageBytesA, std::min<uint64_t>(kAStripeBytes, xbytes_all / (4ull * kCtasA * 148)));
+            std::max<uint64_t>(2ull * kStageBytesA, std::min<uint64_t>(kAStripeBytes, xbytes_all / (19ull * kCtasA * 148 / 3)));
         std::vector<uint32_t> pend;  // lowrank ids of the current stripe
         uint64_t stripe_bytes = 0;
         std::vector<ALane> lanes;
